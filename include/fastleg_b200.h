@@ -1,0 +1,155 @@
+/*
+ * libfastleg_b200 -- C ABI of the B200-native fast discrete Legendre
+ * transform (DLT/IDLT) hot path.
+ *
+ * This is the drop-in boundary. The reference (`fastleg`, a header-only C++20
+ * library) has no C ABI; every entry point below replaces one function of its
+ * header API (paths relative to /root/reference/proj/include/fastleg/). The
+ * C++ drop-in headers in include/fastleg/*.hpp re-expose these with the
+ * reference's exact signatures and exception types.
+ *
+ * Conventions
+ *  - Plain pointers and sizes only. Every double* may point to HOST memory
+ *    (the drop-in path: the library stages it through device memory) or to
+ *    DEVICE memory (the throughput path: no copies). Pointers of one call
+ *    must be all-host or all-device per argument; the library inspects each.
+ *  - Batched extension (absent in the reference): `batch`
+ *    independent columns, column j at ptr + j*ld (ld >= n). batch = 1,
+ *    ld = n is the reference's single-vector call.
+ *  - `stream` is a cudaStream_t (NULL = legacy default stream). Calls are
+ *    synchronous with respect to the host: they return after the results are
+ *    complete, as the reference's functions do, so validation errors found on
+ *    the device (non-finite input) can be reported as a status.
+ *  - Thread-safe: immutable per-size tables are built once under a lock;
+ *    scratch is stream-ordered per call (transforms.hpp:15-18, trig.hpp:28-30).
+ *  - fp64 throughout. There is no CPU fallback: without a usable CUDA device
+ *    every compute entry point returns FL_CUDA_ERROR.
+ */
+#ifndef FASTLEG_B200_H
+#define FASTLEG_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* Status codes; the drop-in headers rethrow the reference's exception type
+ * (SURVEY.md section 5): */
+typedef enum {
+  FL_OK = 0,
+  FL_INVALID_ARGUMENT = 1, /* std::invalid_argument */
+  FL_DOMAIN_ERROR = 2,     /* std::domain_error */
+  FL_OVERFLOW_ERROR = 3,   /* std::overflow_error */
+  FL_RUNTIME_ERROR = 4,    /* std::runtime_error */
+  FL_CUDA_ERROR = 5        /* std::runtime_error (no reference analogue) */
+} fl_status;
+
+/* types.hpp:14 GridKind */
+typedef enum { FL_CHEB1 = 0, FL_CHEBSTAR = 1 } fl_grid_kind;
+
+/* trig.hpp:55,76,100,118 */
+typedef enum { FL_DCT_III = 0, FL_DST_III = 1, FL_DCT_III_T = 2, FL_DST_III_T = 3 } fl_trig_op;
+
+/* Message of the last failing call on this thread (the reference's what()). */
+const char* fl_last_error(void);
+
+/* 1 when a CUDA device is usable, else 0 (message in fl_last_error). */
+int fl_device_available(void);
+
+/* quadrature.hpp:76-143 legendre_nodes_weights(n): theta ascending in (0,pi),
+ * x = cos(theta) descending, weights 2/(dP_N/dtheta)^2; lower half computed,
+ * upper half by exact reflection, odd-N middle node (pi/2, 0).
+ * n == 0 -> FL_INVALID_ARGUMENT ("legendre_nodes_weights: size must be positive"). */
+fl_status fl_nodes_weights(size_t n, double* theta, double* x, double* weights, void* stream);
+
+/* quadrature.hpp:147-158 reference_grid(grid, kind): theta_star and
+ * delta_theta = theta - theta_star. */
+fl_status fl_reference_grid(size_t n, int kind, const double* theta, double* theta_star,
+                            double* delta_theta, void* stream);
+
+/* conversion.hpp:25-30 LambdaCache(max_index): Lambda(z) = Gamma(z+1/2)/Gamma(z+1)
+ * for z = 0..max_index (max_index + 1 doubles). */
+fl_status fl_lambda_table(size_t max_index, double* table, void* stream);
+
+/* trig.hpp:55-136 dct_iii / dst_iii / dct_iii_transpose / dst_iii_transpose.
+ * n == 0 -> FL_INVALID_ARGUMENT ("<op>: empty input"). */
+fl_status fl_trig(int op, int kind, size_t n, const double* in, double* out, size_t batch,
+                  size_t ld, void* stream);
+
+/* ndct.hpp:98-117 ndct_apply (transpose = 0) and ndct.hpp:121-143
+ * ndct_apply_transpose (transpose = 1) for a TaylorPlan given by its fields
+ * (kind, size n, num_terms, reference.delta_theta). Validation as
+ * ndct.hpp:79-91: non-finite input -> FL_INVALID_ARGUMENT, n^(L-1) overflow
+ * guard -> FL_OVERFLOW_ERROR. */
+fl_status fl_ndct(int transpose, int kind, size_t n, int num_terms, const double* delta_theta,
+                  const double* in, double* out, size_t batch, size_t ld, void* stream);
+
+/* ndct.hpp:147-155 ndct_error_bound(plan, coeffs): min((N max|delta|)^L / L!,
+ * C(L)) * ||c||_1, with the two O(N) reductions done on the device. */
+fl_status fl_ndct_error_bound(size_t n, int kind, int num_terms, const double* delta_theta,
+                              const double* coeffs, double* bound, void* stream);
+
+/* conversion.hpp:100-113 leg2cheb_apply (transpose = 0) and :121-135
+ * leg2cheb_apply_transpose (transpose = 1) with the Lambda table of a
+ * LambdaCache (lambda_len = max_index + 1 entries, host or device).
+ * lambda_len < n -> FL_INVALID_ARGUMENT. */
+fl_status fl_leg2cheb(int transpose, size_t n, const double* lambda_table, size_t lambda_len,
+                      const double* in, double* out, size_t batch, size_t ld, void* stream);
+
+/* transforms.hpp:19-38 TransformConfig(n, tolerance, kind): an immutable
+ * device-resident plan (grid, NDCT plan, Lambda table). Building it is O(N)
+ * on the device. */
+typedef struct fl_plan fl_plan;
+fl_status fl_plan_create(size_t n, double tolerance, int kind, fl_plan** plan);
+/* As fl_plan_create but with a caller-supplied grid (theta, x, weights; host
+ * or device), i.e. plan_ndct(const LegendreGrid&, ...) at ndct.hpp:61. */
+fl_status fl_plan_create_from_grid(size_t n, double tolerance, int kind, const double* theta,
+                                   const double* x, const double* weights, fl_plan** plan);
+fl_status fl_plan_destroy(fl_plan* plan);
+/* Accessors (transforms.hpp:26-31); outputs may be host or device. */
+size_t fl_plan_size(const fl_plan* plan);
+int fl_plan_kind(const fl_plan* plan);
+double fl_plan_tolerance(const fl_plan* plan);
+int fl_plan_num_terms(const fl_plan* plan);
+fl_status fl_plan_grid(const fl_plan* plan, double* theta, double* x, double* weights);
+fl_status fl_plan_reference(const fl_plan* plan, double* theta_star, double* delta_theta);
+fl_status fl_plan_lambda(const fl_plan* plan, double* table /* n entries */);
+
+/* transforms.hpp:42-49 dlt: f = NDCT(M c) at the plan's Legendre nodes. */
+fl_status fl_dlt(const fl_plan* plan, const double* in, double* out, size_t batch, size_t ld,
+                 void* stream);
+/* transforms.hpp:54-64 idlt: c = D_s M^T T^T D_w f. */
+fl_status fl_idlt(const fl_plan* plan, const double* in, double* out, size_t batch, size_t ld,
+                  void* stream);
+
+/* NDCT evaluation mode for plans of kind chebstar (the default grid):
+ *   0 = FL_NDCT_LITERAL : L chebstar terms over length-(2N+1) transforms,
+ *                         exactly the reference's algorithm (ndct.hpp:98-143);
+ *   1 = FL_NDCT_FAST    : same nodes, evaluated internally about the cheb1
+ *                         grid with min_taylor_terms(cheb1, tol) terms over
+ *                         power-of-two real DCTs (SURVEY.md 7 H2 option B).
+ * Both are within the reference's certified bound of each other
+ * (test_ndct.cpp:173-183). Default FL_NDCT_FAST for dlt/idlt of power-of-two
+ * sizes; the free-function fl_ndct always evaluates its plan literally. */
+enum { FL_NDCT_LITERAL = 0, FL_NDCT_FAST = 1 };
+fl_status fl_plan_set_ndct_mode(fl_plan* plan, int mode);
+int fl_plan_ndct_mode(const fl_plan* plan);
+
+/* random.hpp:15-55 input generators (host memory; std::mt19937_64 +
+ * Box-Muller): random_decaying(n, decay, seed), and the uniform [-1,1)
+ * recipe u = 2*((r()>>11)*2^-53) - 1 of SURVEY.md 8d (C4). Batched: column
+ * j uses seed + j. `threads` host threads (0 = hardware concurrency). */
+void fl_random_decaying(size_t n, double decay, uint64_t seed, double* out, size_t batch,
+                        int threads);
+void fl_random_uniform_pm1(size_t n, uint64_t seed, double* out, size_t batch, int threads);
+
+/* Number of kernels this library has launched since load (telemetry for the
+ * bench's gpu_launches field). */
+uint64_t fl_kernel_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FASTLEG_B200_H */

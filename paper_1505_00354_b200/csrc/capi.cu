@@ -1,0 +1,693 @@
+// The C ABI (include/fastleg_b200.h): argument validation in the reference's
+// order with its messages, host/device staging, per-call stream-ordered
+// scratch, and the TransformConfig-equivalent device plan.
+#include <atomic>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <new>
+#include <random>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "common.cuh"
+#include "czt.cuh"
+#include "fast_ndct.cuh"
+#include "launch.cuh"
+#include "leg2cheb.cuh"
+
+namespace flb {
+
+namespace {
+thread_local std::string g_last_error;
+std::atomic<unsigned long long> g_launches{0};
+}  // namespace
+
+void fail(fl_status s, const std::string& msg) { throw Error{s, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    throw Error{FL_CUDA_ERROR, std::string("CUDA error: ") + cudaGetErrorString(e) + " (" + what + ")"};
+  }
+}
+
+void note_launch(const char* name) {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cuda_check(cudaGetLastError(), name);
+}
+
+namespace {
+
+template <class F>
+fl_status guarded(F&& f) {
+  try {
+    f();
+    g_last_error.clear();
+    return FL_OK;
+  } catch (const Error& e) {
+    g_last_error = e.message;
+    return e.status;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "fastleg_b200: host allocation failed";
+    return FL_RUNTIME_ERROR;
+  } catch (...) {
+    g_last_error = "fastleg_b200: unknown error";
+    return FL_RUNTIME_ERROR;
+  }
+}
+
+void require_device() {
+  int count = 0;
+  const cudaError_t e = cudaGetDeviceCount(&count);
+  if (e != cudaSuccess || count == 0) {
+    cudaGetLastError();
+    fail(FL_CUDA_ERROR, std::string("fastleg_b200: no usable CUDA device (") +
+                            (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices") +
+                            "); there is no CPU fallback");
+  }
+}
+
+bool is_device_ptr(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  const cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// A column block (n rows x batch columns, stride ld) as a device pointer.
+struct DevIn {
+  const double* ptr = nullptr;
+  size_t ld = 0;
+  double* owned = nullptr;
+  cudaStream_t s;
+  DevIn(const double* user, size_t n, size_t batch, size_t ld_user, cudaStream_t st) : s(st) {
+    if (is_device_ptr(user)) {
+      ptr = user;
+      ld = ld_user;
+      return;
+    }
+    const size_t bytes = n * batch * sizeof(double);
+    FLB_CUDA(cudaMallocAsync(&owned, bytes ? bytes : 8, s));
+    if (bytes)
+      FLB_CUDA(cudaMemcpy2DAsync(owned, n * sizeof(double), user, ld_user * sizeof(double),
+                                 n * sizeof(double), batch, cudaMemcpyHostToDevice, s));
+    ptr = owned;
+    ld = n;
+  }
+  ~DevIn() {
+    if (owned) cudaFreeAsync(owned, s);
+  }
+};
+
+struct DevOut {
+  double* ptr = nullptr;
+  size_t ld = 0;
+  double* user;
+  size_t n, batch, ld_user;
+  bool host;
+  cudaStream_t s;
+  DevOut(double* u, size_t n_, size_t batch_, size_t ld_u, cudaStream_t st)
+      : user(u), n(n_), batch(batch_), ld_user(ld_u), s(st) {
+    host = !is_device_ptr(u);
+    if (!host) {
+      ptr = u;
+      ld = ld_u;
+      return;
+    }
+    const size_t bytes = n * batch * sizeof(double);
+    FLB_CUDA(cudaMallocAsync(&ptr, bytes ? bytes : 8, s));
+    ld = n;
+  }
+  void finish() {
+    if (host && n * batch)
+      FLB_CUDA(cudaMemcpy2DAsync(user, ld_user * sizeof(double), ptr, n * sizeof(double),
+                                 n * sizeof(double), batch, cudaMemcpyDeviceToHost, s));
+  }
+  ~DevOut() {
+    if (host && ptr) cudaFreeAsync(ptr, s);
+  }
+};
+
+template <class T>
+struct DevScratch {
+  T* p = nullptr;
+  cudaStream_t s;
+  DevScratch(size_t count, cudaStream_t st) : s(st) {
+    FLB_CUDA(cudaMallocAsync(&p, (count ? count : 1) * sizeof(T), s));
+  }
+  ~DevScratch() {
+    if (p) cudaFreeAsync(p, s);
+  }
+};
+
+void sync(cudaStream_t s) { FLB_CUDA(cudaStreamSynchronize(s)); }
+
+const char* trig_name(int op) {
+  switch (op) {
+    case FL_DCT_III: return "dct_iii";
+    case FL_DST_III: return "dst_iii";
+    case FL_DCT_III_T: return "dct_iii_transpose";
+    default: return "dst_iii_transpose";
+  }
+}
+
+void check_kind(int kind) {
+  if (kind != FL_CHEB1 && kind != FL_CHEBSTAR) fail(FL_INVALID_ARGUMENT, "fastleg: unknown grid kind");
+}
+
+void check_ld(size_t n, size_t ld, size_t batch) {
+  if (batch > 1 && ld < n) fail(FL_INVALID_ARGUMENT, "fastleg: column stride smaller than size");
+}
+
+// ndct.hpp:49-59 min_taylor_terms
+int min_taylor_terms(int kind, double tolerance) {
+  if (!(tolerance > 0.0 && tolerance < 1.0))
+    fail(FL_INVALID_ARGUMENT, "min_taylor_terms: tolerance must lie in (0, 1)");
+  const double q = kind == FL_CHEB1 ? 0.83845 : 1.0 / (6.0 * kPi);
+  double bound = 1.0;
+  for (int l = 1; l <= 30; ++l) {
+    bound *= q / static_cast<double>(l);
+    if (bound <= tolerance) return l;
+  }
+  fail(FL_DOMAIN_ERROR, "min_taylor_terms: tolerance unattainable with <= 30 terms");
+}
+
+bool overflow_guard(size_t n, int num_terms) {  // ndct.hpp:87-88
+  return n > 1 && static_cast<double>(num_terms - 1) * std::log10(static_cast<double>(n - 1)) > 300.0;
+}
+
+__global__ void nonfinite_kernel(const double* __restrict__ v, size_t n, size_t batch, size_t ld,
+                                 const double* __restrict__ mult, int* flag) {
+  const size_t total = n * batch;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t col = i / n, row = i % n;
+    double x = v[col * ld + row];
+    if (mult) x *= mult[row];
+    if (!isfinite(x)) atomicOr(flag, 1);
+  }
+}
+
+// one CTA: r[0] = max_k |delta_k|, r[1] = sum_k |c_k| (fixed reduction order)
+__global__ void maxabs_l1_kernel(const double* __restrict__ d, const double* __restrict__ c,
+                                 size_t n, double* r) {
+  __shared__ double sm[2][1024];
+  double m = 0.0, s = 0.0;
+  for (size_t i = threadIdx.x; i < n; i += blockDim.x) {
+    m = fmax(m, fabs(d[i]));
+    s += fabs(c[i]);
+  }
+  sm[0][threadIdx.x] = m;
+  sm[1][threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) {
+      sm[0][threadIdx.x] = fmax(sm[0][threadIdx.x], sm[0][threadIdx.x + w]);
+      sm[1][threadIdx.x] += sm[1][threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    r[0] = sm[0][0];
+    r[1] = sm[1][0];
+  }
+}
+
+void reduce_maxabs_l1(const double* d, const double* c, size_t n, double* r, cudaStream_t s) {
+  maxabs_l1_kernel<<<1, 1024, 0, s>>>(d, c, n, r);
+  note_launch("maxabs_l1_kernel");
+}
+
+bool any_nonfinite(const double* v, size_t n, size_t batch, size_t ld, const double* mult,
+                   cudaStream_t s) {
+  DevScratch<int> flag(1, s);
+  FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+  nonfinite_kernel<<<sm_count() * 4, 256, 0, s>>>(v, n, batch, ld, mult, flag.p);
+  note_launch("nonfinite_kernel");
+  int h = 0;
+  FLB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  sync(s);
+  return h != 0;
+}
+
+// Runs an NDCT (literal kind, or the fast cheb1 path) with the reference's
+// validation order: non-finite (invalid_argument) before overflow.
+void run_ndct(const char* where, int transpose, int kind, size_t n, int num_terms,
+              const double* delta, const double* in, size_t ld_in, double* out, size_t ld_out,
+              size_t batch, const double* in_mult, const FastNdct* fast, cudaStream_t s) {
+  if (overflow_guard(n, num_terms)) {
+    if (any_nonfinite(in, n, batch, ld_in, in_mult, s))
+      fail(FL_INVALID_ARGUMENT, std::string(where) + ": non-finite input");
+    fail(FL_OVERFLOW_ERROR, std::string(where) + ": n^l exceeds double range");
+  }
+  DevScratch<int> flag(1, s);
+  FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+  if (num_terms <= 0) {
+    FLB_CUDA(cudaMemset2DAsync(out, ld_out * sizeof(double), 0, n * sizeof(double), batch, s));
+    nonfinite_kernel<<<sm_count() * 4, 256, 0, s>>>(in, n, batch, ld_in, in_mult, flag.p);
+    note_launch("nonfinite_kernel");
+  } else if (fast) {
+    fast_ndct_run(*fast, transpose, in, ld_in, out, ld_out, batch, in_mult, flag.p, s);
+  } else {
+    if (ld_in != ld_out && batch > 1)
+      fail(FL_RUNTIME_ERROR, "ndct: mismatched strides");  // internal: callers pass equal ld
+    czt_ndct(transpose, kind, n, num_terms, delta, in, out, batch, ld_in, in_mult, flag.p, s);
+  }
+  int h = 0;
+  FLB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+  sync(s);
+  if (h) fail(FL_INVALID_ARGUMENT, std::string(where) + ": non-finite input");
+}
+
+}  // namespace
+}  // namespace flb
+
+using namespace flb;
+
+// ---------------------------------------------------------------------------
+// plan
+// ---------------------------------------------------------------------------
+struct fl_plan {
+  size_t n = 0;
+  double tolerance = 0.0;
+  int kind = FL_CHEBSTAR;
+  int num_terms = 0;
+  int mode = FL_NDCT_FAST;
+  int device = 0;
+  double* theta = nullptr;   // n
+  double* x = nullptr;       // n
+  double* w = nullptr;       // n
+  double* tstar = nullptr;   // n (plan kind)
+  double* delta = nullptr;   // n (plan kind)
+  double* lambda = nullptr;  // n  (LambdaCache(n - 1))
+  double* s = nullptr;       // n  (scaled Lambda)
+  FastNdct* fast = nullptr;  // cheb1-internal NDCT (power-of-two n), or null
+  std::mutex mu;
+};
+
+namespace {
+
+void plan_free(fl_plan* p) {
+  for (double* q : {p->theta, p->x, p->w, p->tstar, p->delta, p->lambda, p->s})
+    if (q) cudaFree(q);
+  if (p->fast) fast_ndct_destroy(p->fast);
+  delete p;
+}
+
+void plan_finish(fl_plan* p) {
+  const size_t n = p->n;
+  FLB_CUDA(cudaMalloc(&p->tstar, n * 8));
+  FLB_CUDA(cudaMalloc(&p->delta, n * 8));
+  FLB_CUDA(cudaMalloc(&p->lambda, n * 8));
+  FLB_CUDA(cudaMalloc(&p->s, n * 8));
+  launch_reference_grid(n, p->kind, p->theta, p->tstar, p->delta, 0);
+  launch_lambda(n - 1, p->lambda, 0);
+  scaled_lambda(p->lambda, p->s, n, 0);
+  p->fast = fast_ndct_create(n, p->tolerance, p->kind, p->theta);
+  FLB_CUDA(cudaDeviceSynchronize());
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* fl_last_error(void) { return g_last_error.c_str(); }
+
+int fl_device_available(void) {
+  return guarded([] { require_device(); }) == FL_OK ? 1 : 0;
+}
+
+uint64_t fl_kernel_launch_count(void) { return g_launches.load(); }
+
+fl_status fl_nodes_weights(size_t n, double* theta, double* x, double* weights, void* stream) {
+  return guarded([&] {
+    if (n == 0) fail(FL_INVALID_ARGUMENT, "legendre_nodes_weights: size must be positive");
+    require_device();
+    cudaStream_t s = as_stream(stream);
+    DevOut t(theta, n, 1, n, s), xo(x, n, 1, n, s), wo(weights, n, 1, n, s);
+    launch_nodes(n, t.ptr, xo.ptr, wo.ptr, s);
+    t.finish();
+    xo.finish();
+    wo.finish();
+    sync(s);
+  });
+}
+
+fl_status fl_reference_grid(size_t n, int kind, const double* theta, double* theta_star,
+                            double* delta_theta, void* stream) {
+  return guarded([&] {
+    check_kind(kind);
+    if (n == 0) return;
+    require_device();
+    cudaStream_t s = as_stream(stream);
+    DevIn th(theta, n, 1, n, s);
+    DevOut ts(theta_star, n, 1, n, s), dl(delta_theta, n, 1, n, s);
+    launch_reference_grid(n, kind, th.ptr, ts.ptr, dl.ptr, s);
+    ts.finish();
+    dl.finish();
+    sync(s);
+  });
+}
+
+fl_status fl_lambda_table(size_t max_index, double* table, void* stream) {
+  return guarded([&] {
+    require_device();
+    cudaStream_t s = as_stream(stream);
+    DevOut t(table, max_index + 1, 1, max_index + 1, s);
+    launch_lambda(max_index, t.ptr, s);
+    t.finish();
+    sync(s);
+  });
+}
+
+fl_status fl_trig(int op, int kind, size_t n, const double* in, double* out, size_t batch,
+                  size_t ld, void* stream) {
+  return guarded([&] {
+    if (op < FL_DCT_III || op > FL_DST_III_T) fail(FL_INVALID_ARGUMENT, "fastleg: unknown trig op");
+    if (n == 0) fail(FL_INVALID_ARGUMENT, std::string(trig_name(op)) + ": empty input");
+    check_kind(kind);
+    if (batch == 0) return;
+    if (batch == 1) ld = n;
+    check_ld(n, ld, batch);
+    require_device();
+    cudaStream_t s = as_stream(stream);
+    DevIn i(in, n, batch, ld, s);
+    DevOut o(out, n, batch, ld, s);
+    if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
+    czt_trig(op, kind, n, i.ptr, o.ptr, batch, o.ld, s);
+    o.finish();
+    sync(s);
+  });
+}
+
+fl_status fl_ndct(int transpose, int kind, size_t n, int num_terms, const double* delta_theta,
+                  const double* in, double* out, size_t batch, size_t ld, void* stream) {
+  return guarded([&] {
+    check_kind(kind);
+    const char* where = transpose ? "ndct_apply_transpose" : "ndct_apply";
+    if (n == 0 || batch == 0) {
+      if (overflow_guard(n, num_terms)) fail(FL_OVERFLOW_ERROR, std::string(where) + ": n^l exceeds double range");
+      return;
+    }
+    if (batch == 1) ld = n;
+    check_ld(n, ld, batch);
+    require_device();
+    cudaStream_t s = as_stream(stream);
+    DevIn d(delta_theta, n, 1, n, s);
+    DevIn i(in, n, batch, ld, s);
+    DevOut o(out, n, batch, ld, s);
+    if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
+    const FastNdct* fast = nullptr;
+    FastNdctHolder holder;
+    if (num_terms > 0 && fast_ndct_literal_ok(n, kind)) {
+      holder.p = fast_ndct_create_literal(n, kind, num_terms, d.ptr, s);
+      fast = holder.p;
+    }
+    run_ndct(where, transpose, kind, n, num_terms, d.ptr, i.ptr, i.ld, o.ptr, o.ld, batch,
+             nullptr, fast, s);
+    o.finish();
+    sync(s);
+  });
+}
+
+fl_status fl_ndct_error_bound(size_t n, int kind, int num_terms, const double* delta_theta,
+                              const double* coeffs, double* bound, void* stream) {
+  return guarded([&] {
+    check_kind(kind);
+    double maxd = 0.0, l1 = 0.0;
+    if (n > 0) {
+      require_device();
+      cudaStream_t s = as_stream(stream);
+      DevIn d(delta_theta, n, 1, n, s);
+      DevIn c(coeffs, n, 1, n, s);
+      DevScratch<double> r(2, s);
+      reduce_maxabs_l1(d.ptr, c.ptr, n, r.p, s);
+      double h[2];
+      FLB_CUDA(cudaMemcpyAsync(h, r.p, sizeof h, cudaMemcpyDeviceToHost, s));
+      sync(s);
+      maxd = h[0];
+      l1 = h[1];
+    }
+    // ndct.hpp:150-154
+    const double q = static_cast<double>(n) * maxd;
+    double node_bound = 1.0;
+    for (int l = 1; l <= num_terms; ++l) node_bound *= q / static_cast<double>(l);
+    const double qq = kind == FL_CHEB1 ? 0.83845 : 1.0 / (6.0 * kPi);
+    double grid_bound = 1.0;
+    for (int l = 1; l <= num_terms; ++l) grid_bound *= qq / static_cast<double>(l);
+    *bound = (grid_bound < node_bound ? grid_bound : node_bound) * l1;
+  });
+}
+
+fl_status fl_leg2cheb(int transpose, size_t n, const double* lambda_table, size_t lambda_len,
+                      const double* in, double* out, size_t batch, size_t ld, void* stream) {
+  return guarded([&] {
+    if (n > 0 && lambda_len < n)  // conversion.hpp:90
+      fail(FL_INVALID_ARGUMENT, "leg2cheb: Lambda cache smaller than the coefficient vector");
+    if (n == 0 || batch == 0) return;
+    if (batch == 1) ld = n;
+    check_ld(n, ld, batch);
+    require_device();
+    cudaStream_t s = as_stream(stream);
+    DevIn t(lambda_table, n, 1, n, s);
+    DevScratch<double> sc(n, s);
+    scaled_lambda(t.ptr, sc.p, n, s);
+    DevIn i(in, n, batch, ld, s);
+    DevOut o(out, n, batch, ld, s);
+    if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
+    if (i.ptr == o.ptr) fail(FL_INVALID_ARGUMENT, "leg2cheb: input and output must not alias");
+    leg2cheb_direct(transpose, n, sc.p, i.ptr, o.ptr, batch, o.ld, 0, s);
+    o.finish();
+    sync(s);
+  });
+}
+
+fl_status fl_plan_create(size_t n, double tolerance, int kind, fl_plan** plan) {
+  return guarded([&] {
+    *plan = nullptr;
+    // transforms.hpp:21-24 member order: grid, then plan, then Lambda cache
+    if (n == 0) fail(FL_INVALID_ARGUMENT, "legendre_nodes_weights: size must be positive");
+    check_kind(kind);
+    require_device();
+    const int L = min_taylor_terms(kind, tolerance);
+    fl_plan* p = new fl_plan;
+    try {
+      p->n = n;
+      p->tolerance = tolerance;
+      p->kind = kind;
+      p->num_terms = L;
+      FLB_CUDA(cudaGetDevice(&p->device));
+      FLB_CUDA(cudaMalloc(&p->theta, n * 8));
+      FLB_CUDA(cudaMalloc(&p->x, n * 8));
+      FLB_CUDA(cudaMalloc(&p->w, n * 8));
+      launch_nodes(n, p->theta, p->x, p->w, 0);
+      plan_finish(p);
+    } catch (...) {
+      plan_free(p);
+      throw;
+    }
+    *plan = p;
+  });
+}
+
+fl_status fl_plan_create_from_grid(size_t n, double tolerance, int kind, const double* theta,
+                                   const double* x, const double* weights, fl_plan** plan) {
+  return guarded([&] {
+    *plan = nullptr;
+    if (n == 0) fail(FL_INVALID_ARGUMENT, "plan: size must be positive");
+    check_kind(kind);
+    require_device();
+    const int L = min_taylor_terms(kind, tolerance);
+    fl_plan* p = new fl_plan;
+    try {
+      p->n = n;
+      p->tolerance = tolerance;
+      p->kind = kind;
+      p->num_terms = L;
+      FLB_CUDA(cudaGetDevice(&p->device));
+      FLB_CUDA(cudaMalloc(&p->theta, n * 8));
+      FLB_CUDA(cudaMalloc(&p->x, n * 8));
+      FLB_CUDA(cudaMalloc(&p->w, n * 8));
+      FLB_CUDA(cudaMemcpy(p->theta, theta, n * 8, cudaMemcpyDefault));
+      FLB_CUDA(cudaMemcpy(p->x, x, n * 8, cudaMemcpyDefault));
+      FLB_CUDA(cudaMemcpy(p->w, weights, n * 8, cudaMemcpyDefault));
+      plan_finish(p);
+    } catch (...) {
+      plan_free(p);
+      throw;
+    }
+    *plan = p;
+  });
+}
+
+fl_status fl_plan_destroy(fl_plan* plan) {
+  return guarded([&] {
+    if (plan) plan_free(plan);
+  });
+}
+
+size_t fl_plan_size(const fl_plan* p) { return p ? p->n : 0; }
+int fl_plan_kind(const fl_plan* p) { return p ? p->kind : -1; }
+double fl_plan_tolerance(const fl_plan* p) { return p ? p->tolerance : 0.0; }
+int fl_plan_num_terms(const fl_plan* p) { return p ? p->num_terms : 0; }
+
+fl_status fl_plan_grid(const fl_plan* p, double* theta, double* x, double* weights) {
+  return guarded([&] {
+    const size_t b = p->n * 8;
+    if (theta) FLB_CUDA(cudaMemcpy(theta, p->theta, b, cudaMemcpyDefault));
+    if (x) FLB_CUDA(cudaMemcpy(x, p->x, b, cudaMemcpyDefault));
+    if (weights) FLB_CUDA(cudaMemcpy(weights, p->w, b, cudaMemcpyDefault));
+  });
+}
+
+fl_status fl_plan_reference(const fl_plan* p, double* theta_star, double* delta_theta) {
+  return guarded([&] {
+    const size_t b = p->n * 8;
+    if (theta_star) FLB_CUDA(cudaMemcpy(theta_star, p->tstar, b, cudaMemcpyDefault));
+    if (delta_theta) FLB_CUDA(cudaMemcpy(delta_theta, p->delta, b, cudaMemcpyDefault));
+  });
+}
+
+fl_status fl_plan_lambda(const fl_plan* p, double* table) {
+  return guarded([&] { FLB_CUDA(cudaMemcpy(table, p->lambda, p->n * 8, cudaMemcpyDefault)); });
+}
+
+fl_status fl_plan_set_ndct_mode(fl_plan* p, int mode) {
+  return guarded([&] {
+    if (mode != FL_NDCT_LITERAL && mode != FL_NDCT_FAST)
+      fail(FL_INVALID_ARGUMENT, "plan: unknown NDCT mode");
+    p->mode = mode;
+  });
+}
+
+int fl_plan_ndct_mode(const fl_plan* p) { return p ? p->mode : -1; }
+
+fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, size_t ld,
+                 void* stream) {
+  return guarded([&] {
+    const size_t n = p->n;
+    if (batch == 0) return;
+    if (batch == 1) ld = n;
+    check_ld(n, ld, batch);
+    FLB_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = as_stream(stream);
+    DevIn i(in, n, batch, ld, s);
+    DevOut o(out, n, batch, ld, s);
+    if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
+    // transforms.hpp:47-48: chat = M c (scratch), f = NDCT(chat)
+    DevScratch<double> chat(n * batch, s);
+    leg2cheb_direct(0, n, p->s, i.ptr, chat.p, batch, n, 0, s);
+    const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
+    if (o.ld != n) {
+      DevScratch<double> f(n * batch, s);
+      run_ndct("ndct_apply", 0, p->kind, n, p->num_terms, p->delta, chat.p, n, f.p, n, batch,
+               nullptr, fast, s);
+      FLB_CUDA(cudaMemcpy2DAsync(o.ptr, o.ld * 8, f.p, n * 8, n * 8, batch,
+                                 cudaMemcpyDeviceToDevice, s));
+    } else {
+      run_ndct("ndct_apply", 0, p->kind, n, p->num_terms, p->delta, chat.p, n, o.ptr, n, batch,
+               nullptr, fast, s);
+    }
+    o.finish();
+    sync(s);
+  });
+}
+
+fl_status fl_idlt(const fl_plan* p, const double* in, double* out, size_t batch, size_t ld,
+                  void* stream) {
+  return guarded([&] {
+    const size_t n = p->n;
+    if (batch == 0) return;
+    if (batch == 1) ld = n;
+    check_ld(n, ld, batch);
+    FLB_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = as_stream(stream);
+    DevIn i(in, n, batch, ld, s);
+    DevOut o(out, n, batch, ld, s);
+    // transforms.hpp:58-62: back = NDCT^T(w . f); c = (m + 1/2) M^T back
+    DevScratch<double> back(n * batch, s);
+    const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
+    if (i.ld != n) {
+      DevScratch<double> f(n * batch, s);
+      FLB_CUDA(cudaMemcpy2DAsync(f.p, n * 8, i.ptr, i.ld * 8, n * 8, batch,
+                                 cudaMemcpyDeviceToDevice, s));
+      run_ndct("ndct_apply_transpose", 1, p->kind, n, p->num_terms, p->delta, f.p, n, back.p, n,
+               batch, p->w, fast, s);
+    } else {
+      run_ndct("ndct_apply_transpose", 1, p->kind, n, p->num_terms, p->delta, i.ptr, n, back.p,
+               n, batch, p->w, fast, s);
+    }
+    leg2cheb_direct(1, n, p->s, back.p, o.ptr, batch, o.ld, 1, s);
+    o.finish();
+    sync(s);
+  });
+}
+
+// random.hpp:15-55 (host input generation; not part of the device path)
+static void gen_columns(size_t n, size_t batch, int threads,
+                        void (*col)(size_t n, uint64_t seed, double* out, double decay),
+                        uint64_t seed, double* out, double decay) {
+  if (threads <= 0) threads = (int)std::thread::hardware_concurrency();
+  if (threads <= 0) threads = 1;
+  std::atomic<size_t> next{0};
+  auto work = [&] {
+    for (;;) {
+      const size_t j = next.fetch_add(1);
+      if (j >= batch) break;
+      col(n, seed + j, out + j * n, decay);
+    }
+  };
+  std::vector<std::thread> pool;
+  for (int t = 1; t < threads && (size_t)t < batch; ++t) pool.emplace_back(work);
+  work();
+  for (auto& t : pool) t.join();
+}
+
+static void decaying_column(size_t n, uint64_t seed, double* out, double decay) {
+  std::mt19937_64 rng(seed);
+  auto u01 = [&] { return static_cast<double>(rng() >> 11) * 0x1.0p-53; };
+  bool have = false;
+  double spare = 0.0;
+  for (size_t i = 0; i < n; ++i) {
+    double g;
+    if (have) {
+      have = false;
+      g = spare;
+    } else {
+      double u1;
+      do {
+        u1 = u01();
+      } while (u1 == 0.0);
+      const double u2 = u01();
+      const double r = std::sqrt(-2.0 * std::log(u1));
+      have = true;
+      spare = r * std::sin(2.0 * kPi * u2);
+      g = r * std::cos(2.0 * kPi * u2);
+    }
+    out[i] = g * std::pow(static_cast<double>(i + 1), -decay);
+  }
+}
+
+static void uniform_column(size_t n, uint64_t seed, double* out, double) {
+  std::mt19937_64 rng(seed);
+  for (size_t i = 0; i < n; ++i) out[i] = 2.0 * (static_cast<double>(rng() >> 11) * 0x1.0p-53) - 1.0;
+}
+
+void fl_random_decaying(size_t n, double decay, uint64_t seed, double* out, size_t batch,
+                        int threads) {
+  gen_columns(n, batch, threads, decaying_column, seed, out, decay);
+}
+
+void fl_random_uniform_pm1(size_t n, uint64_t seed, double* out, size_t batch, int threads) {
+  gen_columns(n, batch, threads, uniform_column, seed, out, 0.0);
+}
+
+}  // extern "C"

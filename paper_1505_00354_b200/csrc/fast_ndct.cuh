@@ -1,0 +1,33 @@
+// Fused Taylor NDCT on the cheb1 grid for power-of-two N (the hot path).
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace flb {
+
+struct FastNdct;
+
+// Plan for the nodes `theta` (device, n entries): Taylor expansion about the
+// cheb1 angles with min_taylor_terms(cheb1, tol) terms. Returns null when n
+// is not a supported power of two.
+FastNdct* fast_ndct_create(size_t n, double tol, int kind, const double* theta);
+// A literal cheb1 plan with caller-owned device delta_theta (fl_ndct).
+bool fast_ndct_literal_ok(size_t n, int kind);
+FastNdct* fast_ndct_create_literal(size_t n, int kind, int num_terms, const double* delta,
+                                   cudaStream_t s);
+void fast_ndct_destroy(FastNdct* p);
+
+struct FastNdctHolder {
+  FastNdct* p = nullptr;
+  ~FastNdctHolder() {
+    if (p) fast_ndct_destroy(p);
+  }
+};
+
+// forward: out = NDCT(in); transpose: out = NDCT^T(in_mult . in).
+// nonfinite: device flag, set when a (weighted) input is not finite.
+void fast_ndct_run(const FastNdct& p, int transpose, const double* in, size_t ld_in, double* out,
+                   size_t ld_out, size_t batch, const double* in_mult, int* nonfinite,
+                   cudaStream_t s);
+
+}  // namespace flb

@@ -1,0 +1,139 @@
+// Batched power-of-two complex fp64 FFT engine (the replacement of FFTW's
+// codelets behind trig.hpp:31-47). Used by the generic chirp-z DCT/DST path
+// (any N, both grid kinds). Forward = e^{-2 pi i jk/P}, inverse = e^{+...},
+// both unnormalised.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace flb {
+
+// Device table e^{-2 pi i m / P}, m < P (cached per device and P).
+const double2* twiddle_table(int log2p);
+
+// In-place batched FFT of `batch` contiguous rows of length 2^log2p.
+// `scratch` must hold batch * 2^log2p elements when log2p > 13 (six-step).
+void fft_pow2(double2* data, double2* scratch, int log2p, size_t batch, bool inverse,
+              cudaStream_t s);
+
+constexpr int kMaxSmemLog2 = 13;  // 8192 points = 128 KiB of double2 per CTA
+constexpr int kMaxLog2 = 26;
+
+// Register-resident small DFTs (natural order in and out).
+template <bool INV>
+__device__ __forceinline__ void dft2(double2& a, double2& b) {
+  const double2 t = a;
+  a = make_double2(t.x + b.x, t.y + b.y);
+  b = make_double2(t.x - b.x, t.y - b.y);
+}
+
+template <bool INV>
+__device__ __forceinline__ double2 rot_mi(double2 v) {  // v * (-i) forward, v * (+i) inverse
+  return INV ? make_double2(-v.y, v.x) : make_double2(v.y, -v.x);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft4(double2& v0, double2& v1, double2& v2, double2& v3) {
+  const double2 t0 = make_double2(v0.x + v2.x, v0.y + v2.y);
+  const double2 t1 = make_double2(v0.x - v2.x, v0.y - v2.y);
+  const double2 t2 = make_double2(v1.x + v3.x, v1.y + v3.y);
+  const double2 t3 = rot_mi<INV>(make_double2(v1.x - v3.x, v1.y - v3.y));
+  v0 = make_double2(t0.x + t2.x, t0.y + t2.y);
+  v2 = make_double2(t0.x - t2.x, t0.y - t2.y);
+  v1 = make_double2(t1.x + t3.x, t1.y + t3.y);
+  v3 = make_double2(t1.x - t3.x, t1.y - t3.y);
+}
+
+template <bool INV>
+__device__ __forceinline__ void dft8(double2* v) {
+  constexpr double h = 0.70710678118654752440084436210484903928;
+  double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6];
+  double2 o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  dft4<INV>(e0, e1, e2, e3);
+  dft4<INV>(o0, o1, o2, o3);
+  // w^k, w = e^{-+ 2 pi i / 8}
+  const double2 w1o = INV ? make_double2(h * (o1.x - o1.y), h * (o1.x + o1.y))
+                          : make_double2(h * (o1.x + o1.y), h * (o1.y - o1.x));
+  const double2 w2o = rot_mi<INV>(o2);
+  const double2 w3o = INV ? make_double2(-h * (o3.x + o3.y), h * (o3.x - o3.y))
+                          : make_double2(h * (o3.y - o3.x), -h * (o3.x + o3.y));
+  v[0] = make_double2(e0.x + o0.x, e0.y + o0.y);
+  v[4] = make_double2(e0.x - o0.x, e0.y - o0.y);
+  v[1] = make_double2(e1.x + w1o.x, e1.y + w1o.y);
+  v[5] = make_double2(e1.x - w1o.x, e1.y - w1o.y);
+  v[2] = make_double2(e2.x + w2o.x, e2.y + w2o.y);
+  v[6] = make_double2(e2.x - w2o.x, e2.y - w2o.y);
+  v[3] = make_double2(e3.x + w3o.x, e3.y + w3o.y);
+  v[7] = make_double2(e3.x - w3o.x, e3.y - w3o.y);
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void dft_r(double2* v) {
+  if constexpr (R == 2) {
+    dft2<INV>(v[0], v[1]);
+  } else if constexpr (R == 4) {
+    dft4<INV>(v[0], v[1], v[2], v[3]);
+  } else {
+    dft8<INV>(v);
+  }
+}
+
+// One Stockham pass over a shared-memory row of P points held by TR threads,
+// each doing E/R radix-R butterflies:
+//   v_r = x[j + r P/R] * w_{Ns R}^{r (j mod Ns)};  DFT_R;
+//   y[(j/Ns) Ns R + (j mod Ns) + r Ns] = V_r.
+template <int P, int E, int R, bool INV>
+__device__ __forceinline__ void stockham_pass(double2* s, int tid, int Ns,
+                                              const double2* __restrict__ tw) {
+  constexpr int TR = P / E;
+  constexpr int NB = E / R;
+  double2 v[E];
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    const int j = tid + q * TR;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[q * R + r] = s[j + r * (P / R)];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < NB; ++q) {
+    const int j = tid + q * TR;
+    const int k = j % Ns;
+    const int step = (P / R) / Ns;  // P / (Ns R)
+#pragma unroll
+    for (int r = 1; r < R; ++r) {
+      double2 w = __ldg(&tw[r * k * step]);
+      if (INV) w.y = -w.y;
+      const double2 a = v[q * R + r];
+      v[q * R + r] = make_double2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
+    }
+    dft_r<R, INV>(&v[q * R]);
+    const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[base + r * Ns] = v[q * R + r];
+  }
+  __syncthreads();
+}
+
+// Full in-smem FFT of one row (P points, TR = P/E threads).
+template <int P, int E, bool INV>
+__device__ __forceinline__ void fft_row_smem(double2* s, int tid, const double2* __restrict__ tw) {
+  int Ns = 1;
+#pragma unroll 1
+  while (Ns < P) {
+    const int rem = P / Ns;
+    if (rem >= 8 && E >= 8) {
+      stockham_pass<P, E, 8, INV>(s, tid, Ns, tw);
+      Ns *= 8;
+    } else if (rem >= 4) {
+      stockham_pass<P, E, 4, INV>(s, tid, Ns, tw);
+      Ns *= 4;
+    } else {
+      stockham_pass<P, E, 2, INV>(s, tid, Ns, tw);
+      Ns *= 2;
+    }
+  }
+}
+
+}  // namespace flb
