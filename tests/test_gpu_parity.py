@@ -92,7 +92,8 @@ def test_nodes_vs_reference_model(n):
     g = fl.legendre_nodes_weights(n)
     s = np.sin(g.theta)
     assert np.all(np.abs(g.theta - th) <= 4 * EPS / s + 2 * EPS)
-    assert np.all(np.abs(g.weights - w) <= (8 / s ** 2 + n / 64 + 16) * EPS * w)
+    # the reference's weights carry ~N/18 eps of recurrence rounding in the interior
+    assert np.all(np.abs(g.weights - w) <= (8 / s ** 2 + n / 16 + 16) * EPS * w)
 
 
 def test_quadrature_exactness():  # acceptance.cpp:127-141, test_quadrature.cpp:130-141
