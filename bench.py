@@ -1,0 +1,324 @@
+"""Benchmark: fp64 DLT coefficients/sec on B200 (BASELINE.json metric), with
+the reference CPU path timed beside it.
+
+Workload (BASELINE.json configs[3], "C4"): batched DLT, N = 4096, 65536
+independent columns (2 GiB fp64 input), coefficients iid U[-1,1) from
+std::mt19937_64(4000 + j), columns sharded evenly over the
+ranks with no collective. One step = one DLT of this rank's shard through
+the C ABI (fl_dlt) on device-resident input. `e2e` is the same call with
+pinned HOST buffers (H2D + D2H inside the timed region).
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                  [--config c4|c1|c3] [--cols C]
+
+Multi-GPU: launched by torchrun, one rank per GPU (NCCL only for the barrier
+and the max-over-ranks timing; the data path has no collective).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
+FP64_PEAK_TFLOPS = 37.0  # tools/fp64_peak.cu on this pool's B200 (profiles/r01_fp64_peak.log): DMMA 37.0, DFMA 33.7
+
+CONFIGS = {
+    # name: (N, total columns, generator, description)
+    "c4": (4096, 65536, "uniform", "C4 batched DLT N=4096 x 65536 cols, U[-1,1)"),
+    "c1": (1024, 1, "decay0.5", "C1 DLT N=1024, c_n = g_n/(n+1)^0.5"),
+    "c3": (1 << 20, 1, "decay1", "C3 DLT N=2^20, c_n = g_n/(n+1)"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--config", choices=sorted(CONFIGS), default="c4")
+    ap.add_argument("--cols", type=int, default=0, help="override total columns")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index, self.rows, self.stop_ev = index, [], threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        while not self.stop_ev.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                     timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([s.strip() for s in out.split(",")])
+            except Exception:
+                pass
+            self.stop_ev.wait(0.2)
+
+    def __enter__(self):
+        self.th.start()
+        return self
+
+    def __exit__(self, *a):
+        self.stop_ev.set()
+        self.th.join(timeout=10)
+
+    def summary(self) -> dict:
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def make_inputs(cfg: str, n: int, col0: int, cols: int) -> np.ndarray:
+    import paper_1505_00354_b200 as fl
+    gen = CONFIGS[cfg][2]
+    if gen == "uniform":
+        return fl.random_uniform_pm1(n, 4000 + col0, batch=cols).reshape(cols, n)
+    decay = 0.5 if gen == "decay0.5" else 1.0
+    seed = 1 if cfg == "c1" else 3
+    return fl.random_decaying(n, decay, seed + col0, batch=cols).reshape(cols, n)
+
+
+def cpu_baseline(cfg: str, n: int, budget_s: float, threads: int) -> dict:
+    """The reference's own CPU path (reference headers compiled in place,
+    oracle/_ref) on a bounded sample of the workload, all host threads."""
+    import ctypes as C
+    from oracle import _ref
+    if _ref is None:
+        return {"value": None, "unit": "coeffs/s", "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref not built"}
+    vp, sz, i, d = C.c_void_p, C.c_size_t, C.c_int, C.c_double
+    _ref.fr_config_create.argtypes = [sz, d, i, C.POINTER(vp)]
+    _ref.fr_config_create.restype = i
+    _ref.fr_batch.argtypes = [vp, i, sz, sz, vp, vp, i]
+    _ref.fr_batch.restype = i
+    _ref.fr_config_destroy.argtypes = [vp]
+    h = vp()
+    t0 = time.perf_counter()
+    assert _ref.fr_config_create(n, 2.0 ** -52, 1, C.byref(h)) == 0
+    t_cfg = time.perf_counter() - t0
+    cols = max(threads, 1) if n <= 8192 else 1
+    x = make_inputs(cfg, n, 0, cols)
+    y = np.empty_like(x)
+    done, elapsed = 0, 0.0
+    while elapsed < budget_s:
+        t0 = time.perf_counter()
+        rc = _ref.fr_batch(h, 0, cols, n, vp(x.ctypes.data), vp(y.ctypes.data), threads)
+        elapsed += time.perf_counter() - t0
+        assert rc == 0
+        done += cols
+        if n > 8192:
+            break
+    _ref.fr_config_destroy(h)
+    return {"value": done * n / elapsed, "unit": "coeffs/s", "cores": threads, "kind": "reference",
+            "sample": f"{done} columns of N={n} ({elapsed:.1f} s, TransformConfig build {t_cfg:.2f} s "
+                      f"excluded); reference headers + FFTW-API shim (FFTW absent)"}
+
+
+def run_reference(args, rank: int, world: int) -> None:
+    if rank != 0:
+        return
+    n, total, _, desc = CONFIGS[args.config]
+    threads = os.cpu_count() or 1
+    vals = []
+    for s in range(args.warmup + args.steps):
+        b = cpu_baseline(args.config, n, max(args.cpu_seconds / max(args.steps, 1), 1.0), threads)
+        if s >= args.warmup:
+            vals.append(b["value"])
+    v = float(np.median(vals))
+    line = {"metric": "fp64 DLT coeffs/sec", "value": v, "unit": "coeffs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": desc, "N": n, "columns": total, "parallelism": f"{threads} host threads"},
+            "cpu_baseline": {**b, "value": v},
+            "e2e": {"value": v, "unit": "coeffs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+def main() -> None:
+    args = parse()
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+
+    import torch
+    import paper_1505_00354_b200 as fl
+    from paper_1505_00354_b200 import _lib
+
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n, total, _, desc = CONFIGS[args.config]
+    if args.cols:
+        total = args.cols
+    per = (total + world - 1) // world
+    col0 = rank * per
+    cols = max(0, min(per, total - col0))
+    stream = torch.cuda.current_stream()
+    sp = ctypes_stream = __import__("ctypes").c_void_p(stream.cuda_stream)
+
+    cfg = fl.TransformConfig(n)  # chebstar, tol 2^-52; plan built once, not timed
+    x_host = make_inputs(args.config, n, col0, cols)
+    x = torch.from_numpy(x_host).to(f"cuda:{local}")
+    y = torch.empty_like(x)
+    vp = __import__("ctypes").c_void_p
+
+    def step():
+        _lib.check(_lib.LIB.fl_dlt(cfg.handle, vp(x.data_ptr()), vp(y.data_ptr()), cols, n, sp))
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    barrier()
+    l0 = fl.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        e0.record(stream)
+        for _ in range(args.steps):
+            step()
+        e1.record(stream)
+        barrier()
+    launches = fl.launch_count() - l0
+    ms = e0.elapsed_time(e1) / args.steps
+    t = torch.tensor([ms], device=f"cuda:{local}")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = n * total / (ms_max / 1e3)
+
+    # ---- per-kernel split (same stream, CUDA events): leg2cheb GEMM vs NDCT
+    th = torch.from_numpy(cfg.grid().theta).to(x.device)
+    d1 = torch.empty_like(th)
+    _lib.check(_lib.LIB.fl_reference_grid(n, fl.GridKind.cheb1, vp(th.data_ptr()), None, vp(d1.data_ptr()), sp))
+    lam = torch.from_numpy(cfg.lambda_().table).to(x.device)
+    L1 = fl.min_taylor_terms(fl.GridKind.cheb1, cfg.tolerance())
+    chat = torch.empty_like(x)
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a.record(stream)
+        for _ in range(reps):
+            fn()
+        b.record(stream)
+        torch.cuda.synchronize()
+        return a.elapsed_time(b) / reps
+
+    ms_l2c = timed(lambda: _lib.check(_lib.LIB.fl_leg2cheb(0, n, vp(lam.data_ptr()), n, vp(x.data_ptr()),
+                                                           vp(chat.data_ptr()), cols, n, sp)))
+    ms_ndct = timed(lambda: _lib.check(_lib.LIB.fl_ndct(0, fl.GridKind.cheb1, n, L1, vp(d1.data_ptr()),
+                                                        vp(chat.data_ptr()), vp(y.data_ptr()), cols, n, sp)))
+    ms_dct = timed(lambda: _lib.check(_lib.LIB.fl_trig(0, fl.GridKind.cheb1, n, vp(x.data_ptr()),
+                                                       vp(y.data_ptr()), cols, n, sp)))
+    coef = n * cols
+    l2c_flops = coef * (n / 2.0)                   # N^2/4 MACs per column = N/2 flop per coefficient
+    ndct_flops = coef * L1 * (2.5 * math.log2(n) + 3)  # L (2.5 log2 N + 3)
+    dom = "leg2cheb_fwd_tiled" if ms_l2c >= ms_ndct else "fast_ndct_fwd_kernel"
+    achieved = (l2c_flops / (ms_l2c / 1e3) if dom == "leg2cheb_fwd_tiled" else ndct_flops / (ms_ndct / 1e3)) / 1e12
+    hbm_peak = json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else 6650.0
+    dct_gbs = 16.0 * coef / (ms_dct / 1e3) / 1e9
+
+    # ---- end to end through the public API with pinned host buffers
+    xh = torch.from_numpy(x_host).pin_memory()
+    yh = torch.empty_like(xh).pin_memory()
+
+    def e2e_step():
+        _lib.check(_lib.LIB.fl_dlt(cfg.handle, vp(xh.data_ptr()), vp(yh.data_ptr()), cols, n, sp))
+
+    e2e_step()
+    barrier()
+    e_steps = max(1, min(args.steps, 5))
+    e0.record(stream)
+    for _ in range(e_steps):
+        e2e_step()
+    e1.record(stream)
+    barrier()
+    e2e_ms = e0.elapsed_time(e1) / e_steps
+    t = torch.tensor([e2e_ms], device=f"cuda:{local}")
+    if dist is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_ms = float(t.item())
+
+    # parity spot check of this run's output against the oracle (not timed)
+    if rank == 0:
+        from oracle import ORACLE
+        g = cfg.grid()
+        j = cols - 1
+        ref = ORACLE.dlt_grid(x_host[j], 1, cfg.tolerance(), g.theta, g.x, g.weights)
+        parity = float(np.max(np.abs(yh[j].numpy() - ref)) / np.abs(x_host[j]).sum())
+    base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base = cpu_baseline(args.config, n, args.cpu_seconds, os.cpu_count() or 1)
+    if rank == 0:
+        line = {
+            "metric": "fp64 DLT coeffs/sec", "value": value, "unit": "coeffs/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms_max,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": desc, "N": n, "columns": total, "columns_per_rank": per,
+                       "grid": "chebstar (default TransformConfig), NDCT evaluated about cheb1 (fast mode)",
+                       "parallelism": f"column shards x{world}, no collective",
+                       "l2": "inputs (2 GiB) larger than L2 (126 MB); no flush"},
+            "roofline": {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                         "peak_source": "measured DMMA/DFMA peak, tools/fp64_peak.cu (profiles/r01_fp64_peak.log)",
+                         "algorithmic": "leg2cheb N/2 flop/coef; NDCT L(2.5 log2N + 3) flop/coef"},
+            "roofline_hbm": {"bound": "hbm", "achieved": 16.0 * value / 1e9, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": 16.0 * value / 1e9 / hbm_peak,
+                             "note": "16 B/coef algorithmic (one fp64 read + one write), whole DLT",
+                             "dct_pass_gbs": dct_gbs, "dct_pass_frac": dct_gbs / hbm_peak},
+            "kernels_ms": {"leg2cheb": ms_l2c, "ndct": ms_ndct, "dct_iii_pass": ms_dct, "dlt_step": ms},
+            "e2e": {"value": n * total / (e2e_ms / 1e3), "unit": "coeffs/s",
+                    "h2d_bytes_per_step": int(8 * n * cols), "d2h_bytes_per_step": int(8 * n * cols)},
+            "gpu_launches": launches,
+            "clocks": clk.summary(),
+            "parity_check": {"column": col0 + cols - 1, "rel_err_vs_oracle": parity,
+                             "tolerance": 1e-13 * math.log2(n)},
+        }
+        if base is not None:
+            line["cpu_baseline"] = base
+        print(json.dumps(line))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

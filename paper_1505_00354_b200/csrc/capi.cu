@@ -116,8 +116,8 @@ struct DevOut {
   cudaStream_t s;
   DevOut(double* u, size_t n_, size_t batch_, size_t ld_u, cudaStream_t st)
       : user(u), n(n_), batch(batch_), ld_user(ld_u), s(st) {
-    host = !is_device_ptr(u);
-    if (!host) {
+    host = u != nullptr && !is_device_ptr(u);
+    if (!host) {  // device pointer, or an output the caller does not want (null)
       ptr = u;
       ld = ld_u;
       return;
@@ -382,7 +382,10 @@ fl_status fl_trig(int op, int kind, size_t n, const double* in, double* out, siz
     DevIn i(in, n, batch, ld, s);
     DevOut o(out, n, batch, ld, s);
     if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
-    czt_trig(op, kind, n, i.ptr, o.ptr, batch, o.ld, s);
+    if (fast_trig_ok(n, kind))
+      fast_trig(op, n, i.ptr, o.ptr, batch, o.ld, s);
+    else
+      czt_trig(op, kind, n, i.ptr, o.ptr, batch, o.ld, s);
     o.finish();
     sync(s);
   });

@@ -1,20 +1,366 @@
+// Fused Taylor NDCT on the cheb1 grid for power-of-two N: one CTA per
+// column, all L terms on chip.
+//
+// Replaces ndct.hpp:98-143 (L separate FFTW calls, each allocating and
+// re-reading the column) on the hot path. Per column the kernel reads c once
+// from HBM, keeps the stage vector (n/N)^l c_n in shared memory, runs the L
+// real DCT-III (l even) / DST-III (l odd) transforms as N/2-point complex
+// FFTs in shared memory (Makhoul's real-DCT packing), multiplies each by its
+// Taylor weight sign_l (N delta_k)^l / l! in registers and writes f once:
+// 16 B of HBM traffic per coefficient instead of the reference's ~48 B x L.
+//
+//   DST-III via DCT-III:  sum_n c_n sin(n t_k) = (-1)^k sum_{m>=1} c_{N-m} cos(m t_k)
+//   DCT-III(a)_k, N even (t_k = (k+1/2) pi / N):
+//     X_0 = a_0, X_j = a_j / 2, X_N = 0;  W_j = e^{i pi j/(2N)} (X_j - i X_{N-j})
+//     Z_m = (W_m + W_{m+N/2}) + i (W_m - W_{m+N/2}) e^{2 pi i m/N},  m < N/2
+//     z = IFFT_{N/2}(Z) (unnormalised);  w_{2m} = Re z_m, w_{2m+1} = Im z_m
+//     y_{2n} = w_n,  y_{2n+1} = w_{N-1-n}
+//   The transpose (ndct.hpp:121-143) is the mirror image: DCT-II through one
+//   forward N/2-point FFT of the packed real sequence.
+//
+// The same kernels with one unscaled term are the power-of-two cheb1
+// dct_iii / dst_iii / *_transpose of trig.hpp (so ndct with zero
+// perturbation stays bit-identical to dct_iii, test_ndct.cpp:112-125).
+#include <map>
+#include <mutex>
+#include <tuple>
+
 #include "common.cuh"
 #include "fast_ndct.cuh"
+#include "fft.cuh"
 #include "launch.cuh"
 
 namespace flb {
 
+constexpr int kFastMinLog2 = 9;   // N = 512 (32 threads per column)
+constexpr int kFastMaxLog2 = 13;  // N = 8192 (128 KiB of shared memory)
+
 struct FastNdct {
-  size_t n;
+  size_t n = 0;
+  int log2n = 0;
+  int num_terms = 0;
+  const double* delta = nullptr;  // cheb1 perturbations (device)
+  double* owned_delta = nullptr;
 };
 
-FastNdct* fast_ndct_create(size_t, double, int, const double*) { return nullptr; }
-bool fast_ndct_literal_ok(size_t, int) { return false; }
-FastNdct* fast_ndct_create_literal(size_t, int, int, const double*, cudaStream_t) { return nullptr; }
-void fast_ndct_destroy(FastNdct* p) { delete p; }
-void fast_ndct_run(const FastNdct&, int, const double*, size_t, double*, size_t, size_t,
-                   const double*, int*, cudaStream_t) {
-  fail(FL_RUNTIME_ERROR, "fast ndct: not available");
+namespace {
+
+__device__ __forceinline__ double taylor_sign_d(int l) { return ((l + 1) / 2) % 2 == 0 ? 1.0 : -1.0; }
+
+template <int LOG2N>
+struct Cfg {
+  static constexpr int N = 1 << LOG2N;
+  static constexpr int P = N / 2;
+  static constexpr int E = 8;
+  static constexpr int T = P / E;       // threads per column
+  static constexpr int OWN = N / T;     // rows owned per thread (= 2E)
+  static constexpr size_t SMEM = N * sizeof(double) + P * sizeof(double2);
+};
+
+// plain_op: -1 = Taylor NDCT with num_terms terms; 0 = one plain DCT-III;
+// 1 = one plain DST-III.
+template <int LOG2N>
+__global__ void __launch_bounds__(Cfg<LOG2N>::T)
+    fast_ndct_fwd_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
+                         size_t ld_out, const double* __restrict__ delta, int num_terms,
+                         int plain_op, const double2* __restrict__ tw4n,
+                         const double2* __restrict__ fftw, int* nonfinite) {
+  using C = Cfg<LOG2N>;
+  constexpr int N = C::N, P = C::P, T = C::T, OWN = C::OWN;
+  extern __shared__ double smem[];
+  double* stage = smem;
+  double2* zb = reinterpret_cast<double2*>(smem + N);
+  const int t = threadIdx.x;
+  const size_t col = blockIdx.x;
+  const double* src = in + col * ld_in;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) {
+    const int n = t + T * i;
+    const double v = src[n];
+    bad |= !isfinite(v);
+    stage[n] = v;
+  }
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
+  double f[OWN], p[OWN], nd[OWN];
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) {
+    f[i] = 0.0;
+    p[i] = 1.0;
+    nd[i] = (plain_op < 0) ? (double)N * delta[t + T * i] : 0.0;
+  }
+  const int terms = plain_op < 0 ? num_terms : 1;
+  for (int l = 0; l < terms; ++l) {
+    const bool odd = plain_op < 0 ? (l & 1) : (plain_op == 1);
+    if (l > 0) {
+#pragma unroll
+      for (int i = 0; i < OWN; ++i) {
+        const int n = t + T * i;
+        stage[n] *= (double)n / (double)N;   // (n/N)^l c_n
+        p[i] *= nd[i] / (double)l;           // (N delta)^l / l!
+      }
+    }
+    __syncthreads();
+    // ---- pack: Z_m for m = t + T i -------------------------------------
+#pragma unroll
+    for (int i = 0; i < C::E; ++i) {
+      const int m = t + T * i;
+      auto X = [&](int j) -> double {  // X_j of the current term, 0 <= j <= N
+        if (j == 0) return odd ? 0.0 : stage[0];
+        if (j >= N) return 0.0;
+        return 0.5 * (odd ? stage[N - j] : stage[j]);
+      };
+      const double2 ta = __ldg(&tw4n[m]);       // e^{i pi m/(2N)}
+      const double2 tb = __ldg(&tw4n[m + P]);   // e^{i pi (m+P)/(2N)}
+      const double2 r4 = __ldg(&tw4n[4 * m]);   // e^{2 pi i m/N}
+      const double xa = X(m), xan = X(N - m), xb = X(m + P), xbn = X(P - m);
+      // W = tw (X_j - i X_{N-j})
+      const double2 Wa = make_double2(ta.x * xa + ta.y * xan, ta.y * xa - ta.x * xan);
+      const double2 Wb = make_double2(tb.x * xb + tb.y * xbn, tb.y * xb - tb.x * xbn);
+      const double2 s = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
+      const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
+      const double2 dr = make_double2(d.x * r4.x - d.y * r4.y, d.x * r4.y + d.y * r4.x);
+      zb[m] = make_double2(s.x - dr.y, s.y + dr.x);  // s + i dr
+    }
+    __syncthreads();
+    fft_row_smem<P, C::E, true>(zb, t, fftw);
+    // ---- unpack + Taylor weight + accumulate ----------------------------
+    const double sign = plain_op < 0 ? taylor_sign_d(l) : 1.0;
+#pragma unroll
+    for (int i = 0; i < OWN; ++i) {
+      const int k = t + T * i;
+      const int q = (k & 1) ? (N - 1 - (k >> 1)) : (k >> 1);
+      const double2 z = zb[q >> 1];
+      double y = (q & 1) ? z.y : z.x;
+      if (odd && (k & 1)) y = -y;
+      f[i] += sign * p[i] * y;
+    }
+    __syncthreads();
+  }
+  double* dst = out + col * ld_out;
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) dst[t + T * i] = f[i];
+}
+
+template <int LOG2N>
+__global__ void __launch_bounds__(Cfg<LOG2N>::T)
+    fast_ndct_tr_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
+                        size_t ld_out, const double* __restrict__ delta, int num_terms,
+                        int plain_op, const double* __restrict__ mult,
+                        const double2* __restrict__ tw4n, const double2* __restrict__ fftw,
+                        int* nonfinite) {
+  using C = Cfg<LOG2N>;
+  constexpr int N = C::N, P = C::P, T = C::T, OWN = C::OWN;
+  extern __shared__ double smem[];
+  double* hs = smem;  // h_k = (N delta_k)^l / l! g_k (times (-1)^k for odd l)
+  double2* zb = reinterpret_cast<double2*>(smem + N);
+  const int t = threadIdx.x;
+  const size_t col = blockIdx.x;
+  const double* src = in + col * ld_in;
+  double g[OWN], p[OWN], nd[OWN], o[OWN], rp[OWN];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) {
+    const int k = t + T * i;
+    double v = src[k];
+    if (mult) v = mult[k] * v;  // transforms.hpp:59 weighted = w_k f_k
+    bad |= !isfinite(v);
+    g[i] = v;
+    p[i] = 1.0;
+    nd[i] = (plain_op < 0) ? (double)N * delta[k] : 0.0;
+    o[i] = 0.0;
+    rp[i] = 1.0;
+  }
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
+  const int terms = plain_op < 0 ? num_terms : 1;
+  for (int l = 0; l < terms; ++l) {
+    const bool odd = plain_op < 0 ? (l & 1) : (plain_op == 1);
+#pragma unroll
+    for (int i = 0; i < OWN; ++i) {
+      const int k = t + T * i;
+      if (l > 0) {
+        p[i] *= nd[i] / (double)l;
+        rp[i] *= (double)k / (double)N;  // (n/N)^l for output row n = k
+      }
+      const double h = p[i] * g[i];
+      hs[k] = (odd && (k & 1)) ? -h : h;
+    }
+    __syncthreads();
+    // ---- pack: v_q = h_{2q} (q < P), v_{N-1-q} = h_{2q+1}; z_m = v_{2m} + i v_{2m+1}
+#pragma unroll
+    for (int i = 0; i < C::E; ++i) {
+      const int m = t + T * i;
+      auto V = [&](int q) -> double { return q < P ? hs[2 * q] : hs[2 * (N - 1 - q) + 1]; };
+      zb[m] = make_double2(V(2 * m), V(2 * m + 1));
+    }
+    __syncthreads();
+    fft_row_smem<P, C::E, false>(zb, t, fftw);
+    const double sign = plain_op < 0 ? taylor_sign_d(l) : 1.0;
+#pragma unroll
+    for (int i = 0; i < OWN; ++i) {
+      const int n = t + T * i;
+      double X = 0.0;
+      const int kk = odd ? (N - n) : n;  // DST^T row n is DCT-II row N - n
+      if (!(odd && n == 0)) {
+        const int a = kk & (P - 1), b = (P - kk) & (P - 1);
+        const double2 za = zb[a], zc = zb[b];
+        // V = (Za + conj Zb)/2 + e^{-2 pi i kk/N} (Za - conj Zb)/(2i)
+        const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
+        const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));  // (Za - conj Zb)/(2i)
+        // e^{-2 pi i kk / N} = conj(tw4n[4 kk]) with 4 kk reduced below 2N
+        const int q4 = 4 * kk;
+        double2 r = q4 < 2 * N ? __ldg(&tw4n[q4]) : __ldg(&tw4n[q4 - 2 * N]);
+        if (q4 >= 2 * N) r = make_double2(-r.x, -r.y);
+        r.y = -r.y;
+        const double2 Vv = make_double2(ev.x + od.x * r.x - od.y * r.y, ev.y + od.x * r.y + od.y * r.x);
+        const double2 h = __ldg(&tw4n[kk]);  // e^{+i pi kk/(2N)}; X = Re(conj(h) V)
+        X = h.x * Vv.x + h.y * Vv.y;
+      }
+      o[i] += sign * rp[i] * X;
+    }
+    __syncthreads();
+  }
+  double* dst = out + col * ld_out;
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) dst[t + T * i] = o[i];
+}
+
+__global__ void tw4n_kernel(double2* tw, unsigned long long n) {
+  const unsigned long long q = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  if (q >= 2 * n) return;
+  double s, c;
+  sincospi((double)q / (double)(2 * n), &s, &c);  // e^{2 pi i q / (4N)}
+  tw[q] = make_double2(c, s);
+}
+
+const double2* tw4n_table(int log2n) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, double2*> tables;
+  int dev = 0;
+  FLB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  double2*& slot = tables[{dev, log2n}];
+  if (!slot) {
+    const unsigned long long n = 1ull << log2n;
+    FLB_CUDA(cudaMalloc(&slot, 2 * n * sizeof(double2)));
+    tw4n_kernel<<<(unsigned)((2 * n + 255) / 256), 256>>>(slot, n);
+    note_launch("tw4n_kernel");
+    FLB_CUDA(cudaDeviceSynchronize());
+  }
+  return slot;
+}
+
+template <int LOG2N>
+void launch_fast(int transpose, const double* in, size_t ld_in, double* out, size_t ld_out,
+                 size_t batch, const double* delta, int num_terms, int plain_op,
+                 const double* mult, int* nonfinite, cudaStream_t s) {
+  using C = Cfg<LOG2N>;
+  const double2* tw = tw4n_table(LOG2N);
+  const double2* fftw = twiddle_table(LOG2N - 1);
+  for (size_t c0 = 0; c0 < batch; c0 += 0x7fffffff) {
+    const size_t nc = batch - c0 < 0x7fffffff ? batch - c0 : 0x7fffffff;
+    if (transpose) {
+      FLB_CUDA(cudaFuncSetAttribute(fast_ndct_tr_kernel<LOG2N>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      fast_ndct_tr_kernel<LOG2N><<<(unsigned)nc, C::T, C::SMEM, s>>>(
+          in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, delta, num_terms, plain_op, mult, tw,
+          fftw, nonfinite);
+      note_launch("fast_ndct_tr_kernel");
+    } else {
+      FLB_CUDA(cudaFuncSetAttribute(fast_ndct_fwd_kernel<LOG2N>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      fast_ndct_fwd_kernel<LOG2N><<<(unsigned)nc, C::T, C::SMEM, s>>>(
+          in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, delta, num_terms, plain_op, tw, fftw,
+          nonfinite);
+      note_launch("fast_ndct_fwd_kernel");
+    }
+  }
+}
+
+void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* out,
+              size_t ld_out, size_t batch, const double* delta, int num_terms, int plain_op,
+              const double* mult, int* nonfinite, cudaStream_t s) {
+  switch (log2n) {
+    case 9: launch_fast<9>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
+    case 10: launch_fast<10>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
+    case 11: launch_fast<11>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
+    case 12: launch_fast<12>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
+    case 13: launch_fast<13>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
+    default: fail(FL_RUNTIME_ERROR, "fast ndct: unsupported size");
+  }
+}
+
+int log2_exact(size_t n) {
+  if (n == 0 || (n & (n - 1))) return -1;
+  int l = 0;
+  while ((size_t(1) << l) < n) ++l;
+  return l;
+}
+
+int cheb1_terms(double tol) {  // ndct.hpp:49-59 for cheb1; -1 if unattainable
+  if (!(tol > 0.0 && tol < 1.0)) return -1;
+  double b = 1.0;
+  for (int l = 1; l <= 30; ++l) {
+    b *= 0.83845 / (double)l;
+    if (b <= tol) return l;
+  }
+  return -1;
+}
+
+}  // namespace
+
+bool fast_trig_ok(size_t n, int kind) {
+  const int lg = log2_exact(n);
+  return kind == FL_CHEB1 && lg >= kFastMinLog2 && lg <= kFastMaxLog2;
+}
+
+void fast_trig(int op, size_t n, const double* in, double* out, size_t batch, size_t ld,
+               cudaStream_t s) {
+  const int transpose = op == FL_DCT_III_T || op == FL_DST_III_T;
+  const int plain = (op == FL_DST_III || op == FL_DST_III_T) ? 1 : 0;
+  dispatch(log2_exact(n), transpose, in, ld, out, ld, batch, nullptr, 1, plain, nullptr, nullptr, s);
+}
+
+bool fast_ndct_literal_ok(size_t n, int kind) { return fast_trig_ok(n, kind); }
+
+FastNdct* fast_ndct_create_literal(size_t n, int kind, int num_terms, const double* delta,
+                                   cudaStream_t) {
+  if (!fast_ndct_literal_ok(n, kind)) return nullptr;
+  FastNdct* p = new FastNdct;
+  p->n = n;
+  p->log2n = log2_exact(n);
+  p->num_terms = num_terms;
+  p->delta = delta;
+  return p;
+}
+
+FastNdct* fast_ndct_create(size_t n, double tol, int kind, const double* theta) {
+  const int lg = log2_exact(n);
+  if (lg < kFastMinLog2 || lg > kFastMaxLog2) return nullptr;
+  const int L = cheb1_terms(tol);
+  if (L < 0) return nullptr;
+  (void)kind;
+  FastNdct* p = new FastNdct;
+  p->n = n;
+  p->log2n = lg;
+  p->num_terms = L;
+  FLB_CUDA(cudaMalloc(&p->owned_delta, n * sizeof(double)));
+  launch_reference_grid(n, FL_CHEB1, theta, nullptr, p->owned_delta, 0);
+  p->delta = p->owned_delta;
+  return p;
+}
+
+void fast_ndct_destroy(FastNdct* p) {
+  if (!p) return;
+  if (p->owned_delta) cudaFree(p->owned_delta);
+  delete p;
+}
+
+void fast_ndct_run(const FastNdct& p, int transpose, const double* in, size_t ld_in, double* out,
+                   size_t ld_out, size_t batch, const double* in_mult, int* nonfinite,
+                   cudaStream_t s) {
+  dispatch(p.log2n, transpose, in, ld_in, out, ld_out, batch, p.delta, p.num_terms, -1, in_mult,
+           nonfinite, s);
 }
 
 }  // namespace flb

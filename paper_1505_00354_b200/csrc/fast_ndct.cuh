@@ -17,6 +17,12 @@ FastNdct* fast_ndct_create_literal(size_t n, int kind, int num_terms, const doub
                                    cudaStream_t s);
 void fast_ndct_destroy(FastNdct* p);
 
+// Power-of-two cheb1 dct_iii / dst_iii / *_transpose (trig.hpp) through the
+// same fused kernels with one unscaled term.
+bool fast_trig_ok(size_t n, int kind);
+void fast_trig(int op, size_t n, const double* in, double* out, size_t batch, size_t ld,
+               cudaStream_t s);
+
 struct FastNdctHolder {
   FastNdct* p = nullptr;
   ~FastNdctHolder() {
