@@ -67,6 +67,20 @@ void require_device() {
                             (e != cudaSuccess ? cudaGetErrorString(e) : "0 devices") +
                             "); there is no CPU fallback");
   }
+  // Keep stream-ordered scratch cached across calls: the default pool would
+  // otherwise unmap it at every synchronize (re-mapping GiBs per call).
+  static std::mutex mu;
+  static bool done[64] = {};
+  int dev = 0;
+  FLB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 64 && !done[dev]) {
+    cudaMemPool_t pool;
+    FLB_CUDA(cudaDeviceGetDefaultMemPool(&pool, dev));
+    uint64_t threshold = UINT64_MAX;
+    FLB_CUDA(cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &threshold));
+    done[dev] = true;
+  }
 }
 
 bool is_device_ptr(const void* p) {

@@ -55,12 +55,14 @@ struct Cfg {
   static constexpr int T = P / E;       // threads per column
   static constexpr int OWN = N / T;     // rows owned per thread (= 2E)
   static constexpr size_t SMEM = N * sizeof(double) + P * sizeof(double2);
+  // resident CTAs per SM the register budget is shaped for
+  static constexpr int MINB = T >= 512 ? 1 : (T >= 256 ? 2 : 4);
 };
 
 // plain_op: -1 = Taylor NDCT with num_terms terms; 0 = one plain DCT-III;
 // 1 = one plain DST-III.
 template <int LOG2N>
-__global__ void __launch_bounds__(Cfg<LOG2N>::T)
+__global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
     fast_ndct_fwd_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                          size_t ld_out, const double* __restrict__ delta, int num_terms,
                          int plain_op, const double2* __restrict__ tw4n,
@@ -82,12 +84,11 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T)
     stage[n] = v;
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
-  double f[OWN], p[OWN], nd[OWN];
+  double f[OWN], p[OWN];
 #pragma unroll
   for (int i = 0; i < OWN; ++i) {
     f[i] = 0.0;
     p[i] = 1.0;
-    nd[i] = (plain_op < 0) ? (double)N * delta[t + T * i] : 0.0;
   }
   const int terms = plain_op < 0 ? num_terms : 1;
   for (int l = 0; l < terms; ++l) {
@@ -96,8 +97,8 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T)
 #pragma unroll
       for (int i = 0; i < OWN; ++i) {
         const int n = t + T * i;
-        stage[n] *= (double)n / (double)N;   // (n/N)^l c_n
-        p[i] *= nd[i] / (double)l;           // (N delta)^l / l!
+        stage[n] *= (double)n / (double)N;               // (n/N)^l c_n
+        p[i] *= (double)N * __ldg(&delta[n]) / (double)l;  // (N delta)^l / l!
       }
     }
     __syncthreads();
@@ -143,7 +144,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T)
 }
 
 template <int LOG2N>
-__global__ void __launch_bounds__(Cfg<LOG2N>::T)
+__global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
     fast_ndct_tr_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                         size_t ld_out, const double* __restrict__ delta, int num_terms,
                         int plain_op, const double* __restrict__ mult,
@@ -152,12 +153,12 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T)
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, OWN = C::OWN;
   extern __shared__ double smem[];
-  double* hs = smem;  // h_k = (N delta_k)^l / l! g_k (times (-1)^k for odd l)
+  double* hs = smem;  // h_k = (N delta_k)^l / l! g_k, updated in place per term
   double2* zb = reinterpret_cast<double2*>(smem + N);
   const int t = threadIdx.x;
   const size_t col = blockIdx.x;
   const double* src = in + col * ld_in;
-  double g[OWN], p[OWN], nd[OWN], o[OWN], rp[OWN];
+  double o[OWN], rp[OWN];
   bool bad = false;
 #pragma unroll
   for (int i = 0; i < OWN; ++i) {
@@ -165,9 +166,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T)
     double v = src[k];
     if (mult) v = mult[k] * v;  // transforms.hpp:59 weighted = w_k f_k
     bad |= !isfinite(v);
-    g[i] = v;
-    p[i] = 1.0;
-    nd[i] = (plain_op < 0) ? (double)N * delta[k] : 0.0;
+    hs[k] = v;
     o[i] = 0.0;
     rp[i] = 1.0;
   }
@@ -175,22 +174,22 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T)
   const int terms = plain_op < 0 ? num_terms : 1;
   for (int l = 0; l < terms; ++l) {
     const bool odd = plain_op < 0 ? (l & 1) : (plain_op == 1);
+    if (l > 0) {
 #pragma unroll
-    for (int i = 0; i < OWN; ++i) {
-      const int k = t + T * i;
-      if (l > 0) {
-        p[i] *= nd[i] / (double)l;
+      for (int i = 0; i < OWN; ++i) {
+        const int k = t + T * i;
+        hs[k] *= (double)N * __ldg(&delta[k]) / (double)l;
         rp[i] *= (double)k / (double)N;  // (n/N)^l for output row n = k
       }
-      const double h = p[i] * g[i];
-      hs[k] = (odd && (k & 1)) ? -h : h;
     }
     __syncthreads();
-    // ---- pack: v_q = h_{2q} (q < P), v_{N-1-q} = h_{2q+1}; z_m = v_{2m} + i v_{2m+1}
+    // ---- pack: v_q = h_{2q} (q < P), v_{N-1-q} = h_{2q+1}; z_m = v_{2m} + i v_{2m+1};
+    // odd terms (DST^T) use (-1)^k h_k, i.e. negate the odd-index entries
+    const double fl = odd ? -1.0 : 1.0;
 #pragma unroll
     for (int i = 0; i < C::E; ++i) {
       const int m = t + T * i;
-      auto V = [&](int q) -> double { return q < P ? hs[2 * q] : hs[2 * (N - 1 - q) + 1]; };
+      auto V = [&](int q) -> double { return q < P ? hs[2 * q] : fl * hs[2 * (N - 1 - q) + 1]; };
       zb[m] = make_double2(V(2 * m), V(2 * m + 1));
     }
     __syncthreads();
