@@ -54,7 +54,7 @@ struct Cfg {
   static constexpr int E = 8;
   static constexpr int T = P / E;       // threads per column
   static constexpr int OWN = N / T;     // rows owned per thread (= 2E)
-  static constexpr size_t SMEM = N * sizeof(double) + P * sizeof(double2);
+  static constexpr size_t SMEM = N * sizeof(double) + smem_row(P) * sizeof(double2);
   // resident CTAs per SM the register budget is shaped for
   static constexpr int MINB = T >= 512 ? 1 : (T >= 256 ? 2 : 4);
 };
@@ -121,7 +121,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
       const double2 s = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
       const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
       const double2 dr = make_double2(d.x * r4.x - d.y * r4.y, d.x * r4.y + d.y * r4.x);
-      zb[m] = make_double2(s.x - dr.y, s.y + dr.x);  // s + i dr
+      zb[smem_pad(m)] = make_double2(s.x - dr.y, s.y + dr.x);  // s + i dr
     }
     __syncthreads();
     fft_row_smem<P, C::E, true>(zb, t, fftw);
@@ -131,7 +131,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
     for (int i = 0; i < OWN; ++i) {
       const int k = t + T * i;
       const int q = (k & 1) ? (N - 1 - (k >> 1)) : (k >> 1);
-      const double2 z = zb[q >> 1];
+      const double2 z = zb[smem_pad(q >> 1)];
       double y = (q & 1) ? z.y : z.x;
       if (odd && (k & 1)) y = -y;
       f[i] += sign * p[i] * y;
@@ -190,7 +190,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
     for (int i = 0; i < C::E; ++i) {
       const int m = t + T * i;
       auto V = [&](int q) -> double { return q < P ? hs[2 * q] : fl * hs[2 * (N - 1 - q) + 1]; };
-      zb[m] = make_double2(V(2 * m), V(2 * m + 1));
+      zb[smem_pad(m)] = make_double2(V(2 * m), V(2 * m + 1));
     }
     __syncthreads();
     fft_row_smem<P, C::E, false>(zb, t, fftw);
@@ -202,7 +202,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
       const int kk = odd ? (N - n) : n;  // DST^T row n is DCT-II row N - n
       if (!(odd && n == 0)) {
         const int a = kk & (P - 1), b = (P - kk) & (P - 1);
-        const double2 za = zb[a], zc = zb[b];
+        const double2 za = zb[smem_pad(a)], zc = zb[smem_pad(b)];
         // V = (Za + conj Zb)/2 + e^{-2 pi i kk/N} (Za - conj Zb)/(2i)
         const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
         const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));  // (Za - conj Zb)/(2i)

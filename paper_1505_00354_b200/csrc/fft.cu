@@ -32,14 +32,14 @@ __global__ void __launch_bounds__(512) fft_smem_kernel(double2* __restrict__ dat
   const size_t row0 = (size_t)blockIdx.x * RPC;
   for (int i = threadIdx.x; i < RPC * P; i += blockDim.x) {
     const size_t r = row0 + i / P;
-    sm[i] = r < rows ? data[r * P + (i % P)] : make_double2(0.0, 0.0);
+    sm[(i / P) * smem_row(P) + smem_pad(i % P)] = r < rows ? data[r * P + (i % P)] : make_double2(0.0, 0.0);
   }
   __syncthreads();
   const int lr = threadIdx.x / TR, tid = threadIdx.x % TR;
-  fft_row_smem<P, E, INV>(sm + lr * P, tid, tw);
+  fft_row_smem<P, E, INV>(sm + lr * smem_row(P), tid, tw);
   for (int i = threadIdx.x; i < RPC * P; i += blockDim.x) {
     const size_t r = row0 + i / P;
-    if (r < rows) data[r * P + (i % P)] = sm[i];
+    if (r < rows) data[r * P + (i % P)] = sm[(i / P) * smem_row(P) + smem_pad(i % P)];
   }
 }
 
@@ -102,13 +102,9 @@ void launch_smem(double2* data, size_t rows, const double2* tw, cudaStream_t s) 
   constexpr int E = P >= 8192 ? 16 : 8;
   constexpr int TR = P / E;
   constexpr int RPC = TR >= 256 ? 1 : 256 / TR;
-  const size_t smem = (size_t)RPC * P * sizeof(double2);
-  static bool configured = false;
-  if (!configured) {
-    FLB_CUDA(cudaFuncSetAttribute(fft_smem_kernel<LOG2P, INV>,
-                                  cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    configured = true;
-  }
+  const size_t smem = (size_t)RPC * smem_row(P) * sizeof(double2);
+  FLB_CUDA(cudaFuncSetAttribute(fft_smem_kernel<LOG2P, INV>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   const size_t grid = (rows + RPC - 1) / RPC;
   fft_smem_kernel<LOG2P, INV><<<(unsigned)grid, TR * RPC, smem, s>>>(data, rows, tw);
   note_launch("fft_smem_kernel");

@@ -79,61 +79,65 @@ __device__ __forceinline__ void dft_r(double2* v) {
   }
 }
 
-// One Stockham pass over a shared-memory row of P points held by TR threads,
-// each doing E/R radix-R butterflies:
+// Shared-memory rows are padded with one element after every 8 so that the
+// stride-8 accesses of the first radix-8 pass are bank-conflict free
+// (8 lanes x 16 B fill one 128 B wavefront).
+__host__ __device__ constexpr int smem_pad(int i) { return i + (i >> 3); }
+__host__ __device__ constexpr int smem_row(int p) { return p + p / 8; }
+
+// One Stockham pass (compile-time Ns and radix R) over a padded
+// shared-memory row of P points held by TR = P/E threads, each doing E/R
+// radix-R butterflies:
 //   v_r = x[j + r P/R] * w_{Ns R}^{r (j mod Ns)};  DFT_R;
 //   y[(j/Ns) Ns R + (j mod Ns) + r Ns] = V_r.
-template <int P, int E, int R, bool INV>
-__device__ __forceinline__ void stockham_pass(double2* s, int tid, int Ns,
-                                              const double2* __restrict__ tw) {
+template <int P, int E, int R, int NS, bool INV>
+__device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2* __restrict__ tw) {
   constexpr int TR = P / E;
   constexpr int NB = E / R;
+  constexpr int STEP = (P / R) / NS;  // twiddle stride in the length-P table
   double2 v[E];
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
     const int j = tid + q * TR;
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[q * R + r] = s[j + r * (P / R)];
+    for (int r = 0; r < R; ++r) v[q * R + r] = s[smem_pad(j + r * (P / R))];
   }
   __syncthreads();
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
     const int j = tid + q * TR;
-    const int k = j % Ns;
-    const int step = (P / R) / Ns;  // P / (Ns R)
+    const int k = j & (NS - 1);
+    if (NS > 1) {
 #pragma unroll
-    for (int r = 1; r < R; ++r) {
-      double2 w = __ldg(&tw[r * k * step]);
-      if (INV) w.y = -w.y;
-      const double2 a = v[q * R + r];
-      v[q * R + r] = make_double2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
+      for (int r = 1; r < R; ++r) {
+        double2 w = __ldg(&tw[r * k * STEP]);
+        if (INV) w.y = -w.y;
+        const double2 a = v[q * R + r];
+        v[q * R + r] = make_double2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
+      }
     }
     dft_r<R, INV>(&v[q * R]);
-    const int base = (j / Ns) * Ns * R + k;
+    const int base = (j - k) * R + k;  // (j/Ns) Ns R + (j mod Ns)
 #pragma unroll
-    for (int r = 0; r < R; ++r) s[base + r * Ns] = v[q * R + r];
+    for (int r = 0; r < R; ++r) s[smem_pad(base + r * NS)] = v[q * R + r];
   }
   __syncthreads();
 }
 
-// Full in-smem FFT of one row (P points, TR = P/E threads).
+template <int P, int E, int NS, bool INV>
+__device__ __forceinline__ void fft_passes(double2* s, int tid, const double2* __restrict__ tw) {
+  if constexpr (NS < P) {
+    constexpr int R = (P / NS >= 8) ? 8 : P / NS;
+    stockham_pass<P, E, R, NS, INV>(s, tid, tw);
+    fft_passes<P, E, NS * R, INV>(s, tid, tw);
+  }
+}
+
+// Full in-smem FFT of one padded row (P points, TR = P/E threads); input and
+// output in natural order at s[smem_pad(i)]. Ends with __syncthreads().
 template <int P, int E, bool INV>
 __device__ __forceinline__ void fft_row_smem(double2* s, int tid, const double2* __restrict__ tw) {
-  int Ns = 1;
-#pragma unroll 1
-  while (Ns < P) {
-    const int rem = P / Ns;
-    if (rem >= 8 && E >= 8) {
-      stockham_pass<P, E, 8, INV>(s, tid, Ns, tw);
-      Ns *= 8;
-    } else if (rem >= 4) {
-      stockham_pass<P, E, 4, INV>(s, tid, Ns, tw);
-      Ns *= 4;
-    } else {
-      stockham_pass<P, E, 2, INV>(s, tid, Ns, tw);
-      Ns *= 2;
-    }
-  }
+  fft_passes<P, E, 1, INV>(s, tid, tw);
 }
 
 }  // namespace flb
