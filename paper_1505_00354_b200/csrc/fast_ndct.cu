@@ -255,7 +255,7 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
                  const double* mult, int* nonfinite, cudaStream_t s) {
   using C = Cfg<LOG2N>;
   const double2* tw = tw4n_table(LOG2N);
-  const double2* fftw = twiddle_table(LOG2N - 1);
+  const double2* fftw = pass_twiddles(LOG2N - 1);
   for (size_t c0 = 0; c0 < batch; c0 += 0x7fffffff) {
     const size_t nc = batch - c0 < 0x7fffffff ? batch - c0 : 0x7fffffff;
     if (transpose) {

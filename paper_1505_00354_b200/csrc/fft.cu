@@ -3,7 +3,9 @@
 // transpose) through HBM above that.
 #include <map>
 #include <mutex>
+#include <cmath>
 #include <utility>
+#include <vector>
 
 #include "common.cuh"
 #include "fft.cuh"
@@ -152,7 +154,7 @@ void fft_rows(double2* data, int log2p, size_t rows, bool inverse, cudaStream_t 
     note_launch("fft_tiny_kernel");
     return;
   }
-  const double2* tw = twiddle_table(log2p);
+  const double2* tw = pass_twiddles(log2p);
   if (inverse)
     launch_smem_dispatch<true>(log2p, data, rows, tw, s);
   else
@@ -174,6 +176,36 @@ const double2* twiddle_table(int log2p) {
     twiddle_kernel<<<(unsigned)((p + 255) / 256), 256>>>(slot, p);
     note_launch("twiddle_kernel");
     FLB_CUDA(cudaDeviceSynchronize());
+  }
+  return slot;
+}
+
+const double2* pass_twiddles(int log2p) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, double2*> tables;
+  int dev = 0;
+  FLB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  double2*& slot = tables[{dev, log2p}];
+  if (!slot) {
+    const int p = 1 << log2p;
+    std::vector<double2> h;
+    h.reserve(twiddle_entries(p) + 1);
+    const long double pi_l = 3.14159265358979323846264338327950288L;
+    for (int ns = 1; ns < p; ns *= pass_radix(p, ns)) {
+      const int r_ = pass_radix(p, ns);
+      if (ns == 1) continue;
+      for (int r = 1; r < r_; ++r)
+        for (int k = 0; k < ns; ++k) {
+          // w_{ns R}^{r k} = e^{-2 pi i r k / (ns R)}, phase reduced exactly
+          const long long m = (long long)r * k % (long long)(ns * r_);
+          const long double a = 2.0L * pi_l * (long double)m / (long double)(ns * r_);
+          h.push_back(make_double2((double)cosl(a), (double)-sinl(a)));
+        }
+    }
+    if (h.empty()) h.push_back(make_double2(1.0, 0.0));
+    FLB_CUDA(cudaMalloc(&slot, h.size() * sizeof(double2)));
+    FLB_CUDA(cudaMemcpy(slot, h.data(), h.size() * sizeof(double2), cudaMemcpyHostToDevice));
   }
   return slot;
 }

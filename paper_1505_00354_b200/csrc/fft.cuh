@@ -90,11 +90,15 @@ __host__ __device__ constexpr int smem_row(int p) { return p + p / 8; }
 // radix-R butterflies:
 //   v_r = x[j + r P/R] * w_{Ns R}^{r (j mod Ns)};  DFT_R;
 //   y[(j/Ns) Ns R + (j mod Ns) + r Ns] = V_r.
+//
+// Twiddles come from a pass-major table (global, L1/L2-resident): for each pass with
+// Ns > 1, entries (r-1) Ns + k hold w_{Ns R}^{r k}, r = 1..R-1, k < Ns, so a
+// warp reads consecutive k (bank-conflict free) and the table is only
+// sum_passes (R-1) Ns ~ P entries.
 template <int P, int E, int R, int NS, bool INV>
 __device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2* __restrict__ tw) {
   constexpr int TR = P / E;
   constexpr int NB = E / R;
-  constexpr int STEP = (P / R) / NS;  // twiddle stride in the length-P table
   double2 v[E];
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
@@ -110,7 +114,7 @@ __device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2
     if (NS > 1) {
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        double2 w = __ldg(&tw[r * k * STEP]);
+        double2 w = __ldg(&tw[(r - 1) * NS + k]);
         if (INV) w.y = -w.y;
         const double2 a = v[q * R + r];
         v[q * R + r] = make_double2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
@@ -124,20 +128,40 @@ __device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2
   __syncthreads();
 }
 
-template <int P, int E, int NS, bool INV>
-__device__ __forceinline__ void fft_passes(double2* s, int tid, const double2* __restrict__ tw) {
+__host__ __device__ constexpr int pass_radix(int p, int ns) { return p / ns >= 8 ? 8 : p / ns; }
+
+// Entries of the pass-major twiddle table for a length-P row.
+__host__ __device__ constexpr int twiddle_entries(int p) {
+  int total = 0;
+  for (int ns = 1; ns < p; ns *= pass_radix(p, ns))
+    if (ns > 1) total += (pass_radix(p, ns) - 1) * ns;
+  return total;
+}
+
+template <int P, int E, int NS, int OFF, bool INV>
+__device__ __forceinline__ void fft_passes(double2* s, int tid, const double2* tw) {
   if constexpr (NS < P) {
-    constexpr int R = (P / NS >= 8) ? 8 : P / NS;
-    stockham_pass<P, E, R, NS, INV>(s, tid, tw);
-    fft_passes<P, E, NS * R, INV>(s, tid, tw);
+    constexpr int R = pass_radix(P, NS);
+    stockham_pass<P, E, R, NS, INV>(s, tid, tw + OFF);
+    fft_passes<P, E, NS * R, OFF + (NS > 1 ? (R - 1) * NS : 0), INV>(s, tid, tw);
   }
 }
 
 // Full in-smem FFT of one padded row (P points, TR = P/E threads); input and
-// output in natural order at s[smem_pad(i)]. Ends with __syncthreads().
+// output in natural order at s[smem_pad(i)]; `tw` = the pass-major table
+// (forward signs; conjugated on the fly for the inverse). Ends with
+// __syncthreads().
 template <int P, int E, bool INV>
-__device__ __forceinline__ void fft_row_smem(double2* s, int tid, const double2* __restrict__ tw) {
-  fft_passes<P, E, 1, INV>(s, tid, tw);
+__device__ __forceinline__ void fft_row_smem(double2* s, int tid, const double2* tw) {
+  fft_passes<P, E, 1, 0, INV>(s, tid, tw);
+}
+
+// Device pass-major twiddle table for length 2^log2p (cached per device).
+const double2* pass_twiddles(int log2p);
+
+// Cooperative copy of a table into shared memory.
+__device__ __forceinline__ void load_table(double2* dst, const double2* __restrict__ src, int count) {
+  for (int i = threadIdx.x; i < count; i += blockDim.x) dst[i] = src[i];
 }
 
 }  // namespace flb
