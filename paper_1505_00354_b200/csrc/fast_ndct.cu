@@ -1,5 +1,5 @@
-// Fused Taylor NDCT on the cheb1 grid for power-of-two N: one CTA per
-// column, all L terms on chip.
+// Fused Taylor NDCT on the cheb1 grid for power-of-two N: all L terms on
+// chip, several columns per CTA.
 //
 // Replaces ndct.hpp:98-143 (L separate FFTW calls, each allocating and
 // re-reading the column) on the hot path. Per column the kernel reads c once
@@ -18,6 +18,11 @@
 //   The transpose (ndct.hpp:121-143) is the mirror image: DCT-II through one
 //   forward N/2-point FFT of the packed real sequence.
 //
+// CTA layout: 512 threads = COLS groups of T = N/16 threads, one column per
+// group, each group synchronising on its own named barrier so the columns of
+// a CTA run out of phase. The column-independent tables -- N delta_k and the
+// pass-major FFT twiddles -- are loaded into shared memory once per CTA.
+//
 // The same kernels with one unscaled term are the power-of-two cheb1
 // dct_iii / dst_iii / *_transpose of trig.hpp (so ndct with zero
 // perturbation stays bit-identical to dct_iii, test_ndct.cpp:112-125).
@@ -32,8 +37,8 @@
 
 namespace flb {
 
-constexpr int kFastMinLog2 = 9;   // N = 512 (32 threads per column)
-constexpr int kFastMaxLog2 = 13;  // N = 8192 (128 KiB of shared memory)
+constexpr int kFastMinLog2 = 9;   // N = 512 (one warp per column)
+constexpr int kFastMaxLog2 = 13;  // N = 8192 (one column per CTA)
 
 struct FastNdct {
   size_t n = 0;
@@ -52,28 +57,50 @@ struct Cfg {
   static constexpr int N = 1 << LOG2N;
   static constexpr int P = N / 2;
   static constexpr int E = 8;
-  static constexpr int T = P / E;       // threads per column
-  static constexpr int OWN = N / T;     // rows owned per thread (= 2E)
-  static constexpr size_t SMEM = N * sizeof(double) + smem_row(P) * sizeof(double2);
-  // resident CTAs per SM the register budget is shaped for
-  static constexpr int MINB = T >= 512 ? 1 : (T >= 256 ? 2 : 4);
+  static constexpr int T = P / E;                 // threads per column
+  static constexpr int OWN = N / T;               // rows owned per thread (= 2E)
+  static constexpr int COLS = T >= 512 ? 1 : 512 / T;
+  static constexpr int THREADS = T * COLS;
+  static constexpr int TW = twiddle_entries(P);   // pass-major FFT twiddles
+  static constexpr size_t COL_BYTES = N * sizeof(double) + smem_row(P) * sizeof(double2);
+  // tables in shared memory when they fit beside the columns
+  static constexpr bool SMEM_TABLES = COLS * COL_BYTES + N * 8 + TW * 16 <= 220 * 1024;
+  static constexpr size_t SMEM = COLS * COL_BYTES + (SMEM_TABLES ? N * 8 + TW * 16 : 0);
+  static constexpr int GT = COLS == 1 ? 0 : T;    // group barrier width (0 = whole CTA)
 };
+
+template <int GT>
+__device__ __forceinline__ void col_sync(int bar) {
+  group_sync<GT>(bar);
+}
 
 // plain_op: -1 = Taylor NDCT with num_terms terms; 0 = one plain DCT-III;
 // 1 = one plain DST-III.
 template <int LOG2N>
-__global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     fast_ndct_fwd_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
-                         size_t ld_out, const double* __restrict__ delta, int num_terms,
-                         int plain_op, const double2* __restrict__ tw4n,
-                         const double2* __restrict__ fftw, int* nonfinite) {
+                         size_t ld_out, size_t batch, const double* __restrict__ delta,
+                         int num_terms, int plain_op, const double2* __restrict__ tw4n,
+                         const double2* __restrict__ fftw_g, int* nonfinite) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, OWN = C::OWN;
   extern __shared__ double smem[];
-  double* stage = smem;
-  double2* zb = reinterpret_cast<double2*>(smem + N);
-  const int t = threadIdx.x;
-  const size_t col = blockIdx.x;
+  // shared tables: nd[N] = N delta_k, then the FFT twiddles
+  double* nd = smem + C::COLS * (C::COL_BYTES / 8);
+  double2* fftw_s = reinterpret_cast<double2*>(nd + N);
+  const double2* fftw = C::SMEM_TABLES ? fftw_s : fftw_g;
+  if (C::SMEM_TABLES) {
+    if (plain_op < 0)
+      for (int i = threadIdx.x; i < N; i += blockDim.x) nd[i] = (double)N * delta[i];
+    load_table(fftw_s, fftw_g, C::TW);
+    __syncthreads();
+  }
+  const int g = threadIdx.x / T, t = threadIdx.x % T;
+  const int bar = 1 + g;
+  const size_t col = (size_t)blockIdx.x * C::COLS + g;
+  if (col >= batch) return;
+  double* stage = smem + g * (C::COL_BYTES / 8);
+  double2* zb = reinterpret_cast<double2*>(stage + N);
   const double* src = in + col * ld_in;
   bool bad = false;
 #pragma unroll
@@ -94,14 +121,16 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
   for (int l = 0; l < terms; ++l) {
     const bool odd = plain_op < 0 ? (l & 1) : (plain_op == 1);
     if (l > 0) {
+      const double inv_l = 1.0 / (double)l;
 #pragma unroll
       for (int i = 0; i < OWN; ++i) {
         const int n = t + T * i;
-        stage[n] *= (double)n / (double)N;               // (n/N)^l c_n
-        p[i] *= (double)N * __ldg(&delta[n]) / (double)l;  // (N delta)^l / l!
+        stage[n] *= (double)n / (double)N;  // (n/N)^l c_n
+        const double q = C::SMEM_TABLES ? nd[n] : (double)N * __ldg(&delta[n]);
+        p[i] *= q * inv_l;                   // (N delta)^l / l!
       }
     }
-    __syncthreads();
+    col_sync<C::GT>(bar);
     // ---- pack: Z_m for m = t + T i -------------------------------------
 #pragma unroll
     for (int i = 0; i < C::E; ++i) {
@@ -123,8 +152,8 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
       const double2 dr = make_double2(d.x * r4.x - d.y * r4.y, d.x * r4.y + d.y * r4.x);
       zb[smem_pad(m)] = make_double2(s.x - dr.y, s.y + dr.x);  // s + i dr
     }
-    __syncthreads();
-    fft_row_smem<P, C::E, true>(zb, t, fftw);
+    col_sync<C::GT>(bar);
+    fft_row_smem<P, C::E, true, C::GT>(zb, t, fftw, bar);
     // ---- unpack + Taylor weight + accumulate ----------------------------
     const double sign = plain_op < 0 ? taylor_sign_d(l) : 1.0;
 #pragma unroll
@@ -136,7 +165,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
       if (odd && (k & 1)) y = -y;
       f[i] += sign * p[i] * y;
     }
-    __syncthreads();
+    col_sync<C::GT>(bar);
   }
   double* dst = out + col * ld_out;
 #pragma unroll
@@ -144,19 +173,30 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
 }
 
 template <int LOG2N>
-__global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     fast_ndct_tr_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
-                        size_t ld_out, const double* __restrict__ delta, int num_terms,
-                        int plain_op, const double* __restrict__ mult,
-                        const double2* __restrict__ tw4n, const double2* __restrict__ fftw,
+                        size_t ld_out, size_t batch, const double* __restrict__ delta,
+                        int num_terms, int plain_op, const double* __restrict__ mult,
+                        const double2* __restrict__ tw4n, const double2* __restrict__ fftw_g,
                         int* nonfinite) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, OWN = C::OWN;
   extern __shared__ double smem[];
-  double* hs = smem;  // h_k = (N delta_k)^l / l! g_k, updated in place per term
-  double2* zb = reinterpret_cast<double2*>(smem + N);
-  const int t = threadIdx.x;
-  const size_t col = blockIdx.x;
+  double* nd = smem + C::COLS * (C::COL_BYTES / 8);
+  double2* fftw_s = reinterpret_cast<double2*>(nd + N);
+  const double2* fftw = C::SMEM_TABLES ? fftw_s : fftw_g;
+  if (C::SMEM_TABLES) {
+    if (plain_op < 0)
+      for (int i = threadIdx.x; i < N; i += blockDim.x) nd[i] = (double)N * delta[i];
+    load_table(fftw_s, fftw_g, C::TW);
+    __syncthreads();
+  }
+  const int g = threadIdx.x / T, t = threadIdx.x % T;
+  const int bar = 1 + g;
+  const size_t col = (size_t)blockIdx.x * C::COLS + g;
+  if (col >= batch) return;
+  double* hs = smem + g * (C::COL_BYTES / 8);  // h_k = (N delta_k)^l / l! g_k, in place
+  double2* zb = reinterpret_cast<double2*>(hs + N);
   const double* src = in + col * ld_in;
   double o[OWN], rp[OWN];
   bool bad = false;
@@ -175,14 +215,16 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
   for (int l = 0; l < terms; ++l) {
     const bool odd = plain_op < 0 ? (l & 1) : (plain_op == 1);
     if (l > 0) {
+      const double inv_l = 1.0 / (double)l;
 #pragma unroll
       for (int i = 0; i < OWN; ++i) {
         const int k = t + T * i;
-        hs[k] *= (double)N * __ldg(&delta[k]) / (double)l;
+        const double q = C::SMEM_TABLES ? nd[k] : (double)N * __ldg(&delta[k]);
+        hs[k] *= q * inv_l;
         rp[i] *= (double)k / (double)N;  // (n/N)^l for output row n = k
       }
     }
-    __syncthreads();
+    col_sync<C::GT>(bar);
     // ---- pack: v_q = h_{2q} (q < P), v_{N-1-q} = h_{2q+1}; z_m = v_{2m} + i v_{2m+1};
     // odd terms (DST^T) use (-1)^k h_k, i.e. negate the odd-index entries
     const double fl = odd ? -1.0 : 1.0;
@@ -192,8 +234,8 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
       auto V = [&](int q) -> double { return q < P ? hs[2 * q] : fl * hs[2 * (N - 1 - q) + 1]; };
       zb[smem_pad(m)] = make_double2(V(2 * m), V(2 * m + 1));
     }
-    __syncthreads();
-    fft_row_smem<P, C::E, false>(zb, t, fftw);
+    col_sync<C::GT>(bar);
+    fft_row_smem<P, C::E, false, C::GT>(zb, t, fftw, bar);
     const double sign = plain_op < 0 ? taylor_sign_d(l) : 1.0;
 #pragma unroll
     for (int i = 0; i < OWN; ++i) {
@@ -205,7 +247,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
         const double2 za = zb[smem_pad(a)], zc = zb[smem_pad(b)];
         // V = (Za + conj Zb)/2 + e^{-2 pi i kk/N} (Za - conj Zb)/(2i)
         const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
-        const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));  // (Za - conj Zb)/(2i)
+        const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));
         // e^{-2 pi i kk / N} = conj(tw4n[4 kk]) with 4 kk reduced below 2N
         const int q4 = 4 * kk;
         double2 r = q4 < 2 * N ? __ldg(&tw4n[q4]) : __ldg(&tw4n[q4 - 2 * N]);
@@ -217,7 +259,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::T, Cfg<LOG2N>::MINB)
       }
       o[i] += sign * rp[i] * X;
     }
-    __syncthreads();
+    col_sync<C::GT>(bar);
   }
   double* dst = out + col * ld_out;
 #pragma unroll
@@ -256,21 +298,23 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
   using C = Cfg<LOG2N>;
   const double2* tw = tw4n_table(LOG2N);
   const double2* fftw = pass_twiddles(LOG2N - 1);
-  for (size_t c0 = 0; c0 < batch; c0 += 0x7fffffff) {
-    const size_t nc = batch - c0 < 0x7fffffff ? batch - c0 : 0x7fffffff;
+  const size_t max_cols = (size_t)0x7fffffff * C::COLS;
+  for (size_t c0 = 0; c0 < batch; c0 += max_cols) {
+    const size_t nc = batch - c0 < max_cols ? batch - c0 : max_cols;
+    const unsigned grid = (unsigned)((nc + C::COLS - 1) / C::COLS);
     if (transpose) {
       FLB_CUDA(cudaFuncSetAttribute(fast_ndct_tr_kernel<LOG2N>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      fast_ndct_tr_kernel<LOG2N><<<(unsigned)nc, C::T, C::SMEM, s>>>(
-          in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, delta, num_terms, plain_op, mult, tw,
-          fftw, nonfinite);
+      fast_ndct_tr_kernel<LOG2N><<<grid, C::THREADS, C::SMEM, s>>>(
+          in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta, num_terms, plain_op, mult,
+          tw, fftw, nonfinite);
       note_launch("fast_ndct_tr_kernel");
     } else {
       FLB_CUDA(cudaFuncSetAttribute(fast_ndct_fwd_kernel<LOG2N>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      fast_ndct_fwd_kernel<LOG2N><<<(unsigned)nc, C::T, C::SMEM, s>>>(
-          in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, delta, num_terms, plain_op, tw, fftw,
-          nonfinite);
+      fast_ndct_fwd_kernel<LOG2N><<<grid, C::THREADS, C::SMEM, s>>>(
+          in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta, num_terms, plain_op, tw,
+          fftw, nonfinite);
       note_launch("fast_ndct_fwd_kernel");
     }
   }

@@ -95,8 +95,22 @@ __host__ __device__ constexpr int smem_row(int p) { return p + p / 8; }
 // Ns > 1, entries (r-1) Ns + k hold w_{Ns R}^{r k}, r = 1..R-1, k < Ns, so a
 // warp reads consecutive k (bank-conflict free) and the table is only
 // sum_passes (R-1) Ns ~ P entries.
-template <int P, int E, int R, int NS, bool INV>
-__device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2* __restrict__ tw) {
+// Barrier over the threads that own one row: the whole CTA (GT = 0), one
+// warp (GT = 32), or a named barrier `bar` of GT threads (several rows per CTA
+// progress independently).
+template <int GT>
+__device__ __forceinline__ void group_sync(int bar) {
+  if constexpr (GT == 0) {
+    __syncthreads();
+  } else if constexpr (GT == 32) {
+    __syncwarp();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(GT) : "memory");
+  }
+}
+
+template <int P, int E, int R, int NS, bool INV, int GT>
+__device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2* tw, int bar) {
   constexpr int TR = P / E;
   constexpr int NB = E / R;
   double2 v[E];
@@ -106,7 +120,7 @@ __device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2
 #pragma unroll
     for (int r = 0; r < R; ++r) v[q * R + r] = s[smem_pad(j + r * (P / R))];
   }
-  __syncthreads();
+  group_sync<GT>(bar);
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
     const int j = tid + q * TR;
@@ -114,7 +128,7 @@ __device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2
     if (NS > 1) {
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        double2 w = __ldg(&tw[(r - 1) * NS + k]);
+        double2 w = tw[(r - 1) * NS + k];
         if (INV) w.y = -w.y;
         const double2 a = v[q * R + r];
         v[q * R + r] = make_double2(a.x * w.x - a.y * w.y, a.x * w.y + a.y * w.x);
@@ -125,7 +139,7 @@ __device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2
 #pragma unroll
     for (int r = 0; r < R; ++r) s[smem_pad(base + r * NS)] = v[q * R + r];
   }
-  __syncthreads();
+  group_sync<GT>(bar);
 }
 
 __host__ __device__ constexpr int pass_radix(int p, int ns) { return p / ns >= 8 ? 8 : p / ns; }
@@ -138,22 +152,22 @@ __host__ __device__ constexpr int twiddle_entries(int p) {
   return total;
 }
 
-template <int P, int E, int NS, int OFF, bool INV>
-__device__ __forceinline__ void fft_passes(double2* s, int tid, const double2* tw) {
+template <int P, int E, int NS, int OFF, bool INV, int GT>
+__device__ __forceinline__ void fft_passes(double2* s, int tid, const double2* tw, int bar) {
   if constexpr (NS < P) {
     constexpr int R = pass_radix(P, NS);
-    stockham_pass<P, E, R, NS, INV>(s, tid, tw + OFF);
-    fft_passes<P, E, NS * R, OFF + (NS > 1 ? (R - 1) * NS : 0), INV>(s, tid, tw);
+    stockham_pass<P, E, R, NS, INV, GT>(s, tid, tw + OFF, bar);
+    fft_passes<P, E, NS * R, OFF + (NS > 1 ? (R - 1) * NS : 0), INV, GT>(s, tid, tw, bar);
   }
 }
 
 // Full in-smem FFT of one padded row (P points, TR = P/E threads); input and
 // output in natural order at s[smem_pad(i)]; `tw` = the pass-major table
-// (forward signs; conjugated on the fly for the inverse). Ends with
-// __syncthreads().
-template <int P, int E, bool INV>
-__device__ __forceinline__ void fft_row_smem(double2* s, int tid, const double2* tw) {
-  fft_passes<P, E, 1, 0, INV>(s, tid, tw);
+// (forward signs; conjugated on the fly for the inverse; global or shared).
+// Ends with a barrier over the row's threads (see group_sync).
+template <int P, int E, bool INV, int GT = 0>
+__device__ __forceinline__ void fft_row_smem(double2* s, int tid, const double2* tw, int bar = 0) {
+  fft_passes<P, E, 1, 0, INV, GT>(s, tid, tw, bar);
 }
 
 // Device pass-major twiddle table for length 2^log2p (cached per device).
