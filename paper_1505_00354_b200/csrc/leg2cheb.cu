@@ -162,6 +162,167 @@ __global__ void __launch_bounds__(THREADS)
   }
 }
 
+// ---------------------------------------------------------------------------
+// fp64 tensor-core version (mma.sync.m8n8k4.f64, DMMA). One CTA owns 32 rows
+// of BOTH parity classes (output rows [2 a0, 2 a0 + 64), contiguous) x 128
+// columns; 8 warps, warp w computes parity w & 1, columns (w >> 1) * 32 + [0, 32)
+// as a 4 x 4 grid of 8 x 8 accumulator tiles. The inner dimension streams in
+// chunks of 16 per parity: the M chunk is generated from the s table into
+// shared memory, the input chunk (rows [2 b0, 2 b0 + 32) of 128 columns, both
+// parities) is prefetched into registers one chunk ahead and split by parity
+// on the way into shared memory. The epilogue stages the 64 x 128 output
+// tile in shared memory and writes whole column segments (coalesced).
+//   forward  : A[a][b] = s_{b-a} s_{a+b+p}           (b >= a),  row scale 1 | 2
+//   transpose: A[b][a] = pref_{2a+p} s_{b-a} s_{a+b+p} (a <= b), row scale (m + 1/2) opt.
+// ---------------------------------------------------------------------------
+namespace mma {
+constexpr int RA = 32;        // rows per parity per CTA
+constexpr int CT = 128;       // columns per CTA
+constexpr int KB = 16;        // inner chunk per parity
+constexpr int LDA = KB + 4;   // 160 B rows: 8 rows x 32 B hit distinct bank groups per phase
+constexpr int LDB = CT + 8;   // 1088 B rows (= 64 mod 128)
+constexpr int THREADS = 256;
+constexpr int SM_A = 2 * RA * LDA;   // doubles
+constexpr int SM_B = 2 * KB * LDB;   // doubles
+constexpr int LDO = 2 * RA + 2;      // epilogue tile: [CT][2 RA] (+2 pad)
+constexpr int SM_O = CT * LDO;
+constexpr int SMEM_DOUBLES = (SM_A + SM_B) > SM_O ? (SM_A + SM_B) : SM_O;
+}  // namespace mma
+
+__device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c[0]), "+d"(c[1])
+               : "d"(a), "d"(b));
+}
+
+template <bool TR>
+__global__ void __launch_bounds__(mma::THREADS)
+    leg2cheb_mma_kernel(const double* __restrict__ s, const double* __restrict__ in,
+                        double* __restrict__ out, size_t n, size_t cols, size_t ld,
+                        int scale_half) {
+  constexpr int RA = mma::RA, CT = mma::CT, KB = mma::KB, LDA = mma::LDA, LDB = mma::LDB;
+  constexpr int THREADS = mma::THREADS, SM_A = mma::SM_A, LDO = mma::LDO;
+  extern __shared__ double sm[];
+  double* As = sm;           // [2][RA][LDA]
+  double* Bs = sm + SM_A;    // [2][KB][LDB]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wp = warp & 1, wc = (warp >> 1) * 32;
+  const size_t a0 = (size_t)blockIdx.x * RA;
+  const size_t c0 = (size_t)blockIdx.y * CT;
+  const size_t nr[2] = {(n + 1) / 2, n / 2};  // rows per parity
+  if (a0 >= nr[0]) return;
+  // inner range (union over both parities), chunk aligned
+  size_t k_begin, k_end;
+  if (!TR) {
+    k_begin = a0 - (a0 % KB);
+    k_end = nr[0];
+  } else {
+    k_begin = 0;
+    k_end = a0 + RA < nr[0] ? a0 + RA : nr[0];
+  }
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+
+  // register prefetch of one input chunk: 8 x double2 (rows 2b0..2b0+31, 128 cols)
+  double2 pre[8];
+  auto load_b = [&](size_t b0) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + THREADS * i;
+      const int col = idx >> 4, pr = idx & 15;
+      const size_t b = b0 + pr, gc = c0 + col;
+      double2 v = make_double2(0.0, 0.0);
+      if (gc < cols) {
+        const double* src = in + gc * ld + 2 * b;
+        if (2 * b + 1 < n)
+          v = __ldg(reinterpret_cast<const double2*>(src));
+        else if (2 * b < n)
+          v.x = __ldg(src);
+      }
+      pre[i] = v;
+    }
+  };
+  auto store_b = [&]() {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int idx = tid + THREADS * i;
+      const int col = idx >> 4, pr = idx & 15;
+      Bs[(0 * KB + pr) * LDB + col] = pre[i].x;
+      Bs[(1 * KB + pr) * LDB + col] = pre[i].y;
+    }
+  };
+  auto gen_a = [&](size_t b0) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + THREADS * i;
+      const int p = idx >> 9, r = (idx >> 4) & 31, kk = idx & 15;
+      const size_t row = a0 + r, inner = b0 + kk;
+      double v = 0.0;
+      if (!TR) {
+        if (inner >= row && inner < nr[p]) v = s[inner - row] * s[row + inner + p];
+      } else {
+        if (inner <= row && row < nr[p]) {
+          const double pref = (2 * inner + p) == 0 ? 1.0 : 2.0;
+          v = pref * (s[row - inner] * s[row + inner + p]);
+        }
+      }
+      As[(p * RA + r) * LDA + kk] = v;
+    }
+  };
+
+  load_b(k_begin);
+  for (size_t b0 = k_begin; b0 < k_end; b0 += KB) {
+    __syncthreads();  // previous chunk's smem reads are done
+    store_b();
+    gen_a(b0);
+    __syncthreads();
+    if (b0 + KB < k_end) load_b(b0 + KB);  // overlaps with the MMAs below
+    const double* Ap = As + wp * RA * LDA;
+    const double* Bp = Bs + wp * KB * LDB;
+#pragma unroll
+    for (int ks = 0; ks < KB; ks += 4) {
+      double af[4], bf[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) af[i] = Ap[(8 * i + (lane >> 2)) * LDA + ks + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) bf[j] = Bp[(ks + (lane & 3)) * LDB + wc + 8 * j + (lane >> 2)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884(acc[i][j], af[i], bf[j]);
+    }
+  }
+  __syncthreads();
+  // epilogue: O[col][k_local], k_local = 2 a + p in [0, 64)
+  double* O = sm;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int r = 8 * i + (lane >> 2);
+      const int cl = wc + 8 * j + 2 * (lane & 3);
+      const int kl = 2 * r + wp;
+      O[cl * LDO + kl] = acc[i][j][0];
+      O[(cl + 1) * LDO + kl] = acc[i][j][1];
+    }
+  __syncthreads();
+  const size_t k0 = 2 * a0;
+  for (int idx = tid; idx < CT * 2 * RA; idx += THREADS) {
+    const int cl = idx >> 6, kl = idx & 63;
+    const size_t gc = c0 + cl, k = k0 + kl;
+    if (gc >= cols || k >= n) continue;
+    double v = O[cl * LDO + kl];
+    if (!TR)
+      v = (k == 0 ? 1.0 : 2.0) * v;
+    else if (scale_half)
+      v = ((double)k + 0.5) * v;
+    out[gc * ld + k] = v;
+  }
+}
+
 }  // namespace
 
 void scaled_lambda(const double* table, double* s, size_t count, cudaStream_t st) {
@@ -174,6 +335,27 @@ void leg2cheb_direct(int transpose, size_t n, const double* s, const double* in,
                      size_t cols, size_t ld, int scale_half, cudaStream_t st) {
   if (n == 0 || cols == 0) return;
   const size_t rows = (n + 1) / 2;
+  const bool aligned = (ld % 2 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
+  if (aligned && n >= 64) {
+    const size_t smem = mma::SMEM_DOUBLES * sizeof(double);
+    for (size_t c0 = 0; c0 < cols; c0 += (size_t)65535 * mma::CT) {
+      const size_t nc = cols - c0 < (size_t)65535 * mma::CT ? cols - c0 : (size_t)65535 * mma::CT;
+      dim3 grid((unsigned)((rows + mma::RA - 1) / mma::RA), (unsigned)((nc + mma::CT - 1) / mma::CT));
+      if (transpose) {
+        FLB_CUDA(cudaFuncSetAttribute(leg2cheb_mma_kernel<true>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        leg2cheb_mma_kernel<true><<<grid, mma::THREADS, smem, st>>>(s, in + c0 * ld, out + c0 * ld,
+                                                                    n, nc, ld, scale_half);
+      } else {
+        FLB_CUDA(cudaFuncSetAttribute(leg2cheb_mma_kernel<false>,
+                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        leg2cheb_mma_kernel<false><<<grid, mma::THREADS, smem, st>>>(s, in + c0 * ld, out + c0 * ld,
+                                                                     n, nc, ld, 0);
+      }
+      note_launch(transpose ? "leg2cheb_mma_kernel<T>" : "leg2cheb_mma_kernel<F>");
+    }
+    return;
+  }
   for (size_t c0 = 0; c0 < cols; c0 += (size_t)65535 * TC) {
     const size_t nc = cols - c0 < (size_t)65535 * TC ? cols - c0 : (size_t)65535 * TC;
     dim3 grid((unsigned)((rows + TA - 1) / TA), (unsigned)((nc + TC - 1) / TC), n > 1 ? 2 : 1);
