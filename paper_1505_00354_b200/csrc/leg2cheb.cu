@@ -180,10 +180,10 @@ constexpr int RA = 32;        // rows per parity per CTA
 constexpr int CT = 128;       // columns per CTA
 constexpr int KB = 16;        // inner chunk per parity
 constexpr int LDA = KB + 4;   // 160 B rows: 8 rows x 32 B hit distinct bank groups per phase
-constexpr int LDB = CT + 8;   // 1088 B rows (= 64 mod 128)
+constexpr int LDB = KB + 4;   // input chunk stored column-major [col][k], same 160 B rows
 constexpr int THREADS = 256;
 constexpr int SM_A = 2 * RA * LDA;   // doubles
-constexpr int SM_B = 2 * KB * LDB;   // doubles
+constexpr int SM_B = 2 * CT * LDB;   // doubles
 constexpr int LDO = 2 * RA + 2;      // epilogue tile: [CT][2 RA] (+2 pad)
 constexpr int SM_O = CT * LDO;
 constexpr int SMEM_DOUBLES = (SM_A + SM_B) > SM_O ? (SM_A + SM_B) : SM_O;
@@ -196,7 +196,7 @@ __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
 }
 
 template <bool TR>
-__global__ void __launch_bounds__(mma::THREADS)
+__global__ void __launch_bounds__(mma::THREADS, 2)
     leg2cheb_mma_kernel(const double* __restrict__ s, const double* __restrict__ in,
                         double* __restrict__ out, size_t n, size_t cols, size_t ld,
                         int scale_half) {
@@ -250,8 +250,8 @@ __global__ void __launch_bounds__(mma::THREADS)
     for (int i = 0; i < 8; ++i) {
       const int idx = tid + THREADS * i;
       const int col = idx >> 4, pr = idx & 15;
-      Bs[(0 * KB + pr) * LDB + col] = pre[i].x;
-      Bs[(1 * KB + pr) * LDB + col] = pre[i].y;
+      Bs[(0 * CT + col) * LDB + pr] = pre[i].x;
+      Bs[(1 * CT + col) * LDB + pr] = pre[i].y;
     }
   };
   auto gen_a = [&](size_t b0) {
@@ -281,14 +281,14 @@ __global__ void __launch_bounds__(mma::THREADS)
     __syncthreads();
     if (b0 + KB < k_end) load_b(b0 + KB);  // overlaps with the MMAs below
     const double* Ap = As + wp * RA * LDA;
-    const double* Bp = Bs + wp * KB * LDB;
+    const double* Bp = Bs + wp * CT * LDB;
 #pragma unroll
     for (int ks = 0; ks < KB; ks += 4) {
       double af[4], bf[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) af[i] = Ap[(8 * i + (lane >> 2)) * LDA + ks + (lane & 3)];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) bf[j] = Bp[(ks + (lane & 3)) * LDB + wc + 8 * j + (lane >> 2)];
+      for (int j = 0; j < 4; ++j) bf[j] = Bp[(wc + 8 * j + (lane >> 2)) * LDB + ks + (lane & 3)];
 #pragma unroll
       for (int i = 0; i < 4; ++i)
 #pragma unroll
