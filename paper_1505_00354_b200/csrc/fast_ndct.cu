@@ -18,6 +18,12 @@
 //   The transpose (ndct.hpp:121-143) is the mirror image: DCT-II through one
 //   forward N/2-point FFT of the packed real sequence.
 //
+// Per term the packing feeds the first radix-8 FFT pass straight from
+// registers, and (forward) the last pass is consumed in registers: each
+// thread owns the 16 outputs its last-pass butterflies produce, so the Taylor
+// weights are applied without another shared-memory round trip. The term
+// parity (DCT/DST) is a template parameter.
+//
 // CTA layout: 512 threads = COLS groups of T = N/16 threads, one column per
 // group, each group synchronising on its own named barrier so the columns of
 // a CTA run out of phase. The column-independent tables -- N delta_k and the
@@ -62,6 +68,8 @@ struct Cfg {
   static constexpr int COLS = T >= 512 ? 1 : 512 / T;
   static constexpr int THREADS = T * COLS;
   static constexpr int TW = twiddle_entries(P);   // pass-major FFT twiddles
+  static constexpr int NSL = last_pass_ns(P);     // last FFT pass
+  static constexpr int RL = P / NSL;
   static constexpr size_t COL_BYTES = N * sizeof(double) + smem_row(P) * sizeof(double2);
   // tables in shared memory when they fit beside the columns
   static constexpr bool SMEM_TABLES = COLS * COL_BYTES + N * 8 + TW * 16 <= 220 * 1024;
@@ -69,9 +77,65 @@ struct Cfg {
   static constexpr int GT = COLS == 1 ? 0 : T;    // group barrier width (0 = whole CTA)
 };
 
-template <int GT>
-__device__ __forceinline__ void col_sync(int bar) {
-  group_sync<GT>(bar);
+// Output row k of w index q (q = 2m or 2m+1 of the inverse FFT output z_m).
+template <int N>
+__device__ __forceinline__ int fwd_row_of(int q) {
+  return q < N / 2 ? 2 * q : 2 * (N - 1 - q) + 1;
+}
+
+// Packed Z_m of the forward transform for term parity ODD.
+template <int N, bool ODD>
+__device__ __forceinline__ double2 fwd_pack(const double* stage, int m,
+                                            const double2* __restrict__ tw4n) {
+  constexpr int P = N / 2;
+  auto X = [&](int j) -> double {  // X_j, 0 <= j <= N
+    if (j == 0) return ODD ? 0.0 : stage[0];
+    if (j >= N) return 0.0;
+    return 0.5 * (ODD ? stage[N - j] : stage[j]);
+  };
+  const double2 ta = __ldg(&tw4n[m]);      // e^{i pi m/(2N)}
+  const double2 tb = __ldg(&tw4n[m + P]);  // e^{i pi (m+P)/(2N)}
+  const double2 r4 = __ldg(&tw4n[4 * m]);  // e^{2 pi i m/N}
+  const double xa = X(m), xan = X(N - m), xb = X(m + P), xbn = X(P - m);
+  const double2 Wa = make_double2(ta.x * xa + ta.y * xan, ta.y * xa - ta.x * xan);
+  const double2 Wb = make_double2(tb.x * xb + tb.y * xbn, tb.y * xb - tb.x * xbn);
+  const double2 s = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
+  const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
+  const double2 dr = make_double2(d.x * r4.x - d.y * r4.y, d.x * r4.y + d.y * r4.x);
+  return make_double2(s.x - dr.y, s.y + dr.x);  // s + i dr
+}
+
+// One forward Taylor term (or one plain transform): f[i] += sign p[i] y_{k_i}.
+template <int LOG2N, bool ODD>
+__device__ __forceinline__ void fwd_term(const double* stage, double2* zb, int t, int bar,
+                                         const double2* __restrict__ tw4n, const double2* fftw,
+                                         const double* p, double* f, double sign) {
+  using C = Cfg<LOG2N>;
+  constexpr int N = C::N, P = C::P, T = C::T, E = C::E, NSL = C::NSL, RL = C::RL;
+  double2 v[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) v[r] = fwd_pack<N, ODD>(stage, t + r * T, tw4n);
+  pass_compute<P, E, 8, 1, true>(v, t, fftw);
+  pass_store<P, E, 8, 1>(v, zb, t);
+  group_sync<C::GT>(bar);
+  mid_passes<P, E, 8, NSL, true, C::GT>(zb, t, fftw, bar);
+  pass_load<P, E, RL>(v, zb, t);
+  pass_compute<P, E, RL, NSL, true>(v, t, fftw + pass_tw_offset(P, NSL));
+#pragma unroll
+  for (int q = 0; q < E / RL; ++q)
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      const int m = t + q * T + r * NSL;
+      const double2 z = v[q * RL + r];
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        const int i = 2 * (q * RL + r) + part;
+        const int k = fwd_row_of<N>(2 * m + part);
+        double y = part ? z.y : z.x;
+        if (ODD && (k & 1)) y = -y;
+        f[i] += sign * p[i] * y;
+      }
+    }
 }
 
 // plain_op: -1 = Taylor NDCT with num_terms terms; 0 = one plain DCT-III;
@@ -83,9 +147,8 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
                          int num_terms, int plain_op, const double2* __restrict__ tw4n,
                          const double2* __restrict__ fftw_g, int* nonfinite) {
   using C = Cfg<LOG2N>;
-  constexpr int N = C::N, P = C::P, T = C::T, OWN = C::OWN;
+  constexpr int N = C::N, T = C::T, OWN = C::OWN, E = C::E, NSL = C::NSL, RL = C::RL;
   extern __shared__ double smem[];
-  // shared tables: nd[N] = N delta_k, then the FFT twiddles
   double* nd = smem + C::COLS * (C::COL_BYTES / 8);
   double2* fftw_s = reinterpret_cast<double2*>(nd + N);
   const double2* fftw = C::SMEM_TABLES ? fftw_s : fftw_g;
@@ -111,65 +174,99 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     stage[n] = v;
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
+  // the rows this thread accumulates: the outputs of its last-pass butterflies
+  int kown[OWN];
+#pragma unroll
+  for (int q = 0; q < E / RL; ++q)
+#pragma unroll
+    for (int r = 0; r < RL; ++r)
+#pragma unroll
+      for (int part = 0; part < 2; ++part)
+        kown[2 * (q * RL + r) + part] = fwd_row_of<N>(2 * (t + q * T + r * NSL) + part);
   double f[OWN], p[OWN];
 #pragma unroll
   for (int i = 0; i < OWN; ++i) {
     f[i] = 0.0;
     p[i] = 1.0;
   }
-  const int terms = plain_op < 0 ? num_terms : 1;
-  for (int l = 0; l < terms; ++l) {
-    const bool odd = plain_op < 0 ? (l & 1) : (plain_op == 1);
-    if (l > 0) {
-      const double inv_l = 1.0 / (double)l;
+  group_sync<C::GT>(bar);
+  if (plain_op >= 0) {
+    if (plain_op == 1)
+      fwd_term<LOG2N, true>(stage, zb, t, bar, tw4n, fftw, p, f, 1.0);
+    else
+      fwd_term<LOG2N, false>(stage, zb, t, bar, tw4n, fftw, p, f, 1.0);
+  } else {
+    for (int l = 0; l < num_terms; ++l) {
+      if (l > 0) {
+        const double inv_l = 1.0 / (double)l;
 #pragma unroll
-      for (int i = 0; i < OWN; ++i) {
-        const int n = t + T * i;
-        stage[n] *= (double)n / (double)N;  // (n/N)^l c_n
-        const double q = C::SMEM_TABLES ? nd[n] : (double)N * __ldg(&delta[n]);
-        p[i] *= q * inv_l;                   // (N delta)^l / l!
+        for (int i = 0; i < OWN; ++i) {
+          const int n = t + T * i;
+          stage[n] *= (double)n / (double)N;  // (n/N)^l c_n
+          const int k = kown[i];
+          const double q = C::SMEM_TABLES ? nd[k] : (double)N * __ldg(&delta[k]);
+          p[i] *= q * inv_l;                   // (N delta_k)^l / l!
+        }
+        group_sync<C::GT>(bar);
       }
+      if (l & 1)
+        fwd_term<LOG2N, true>(stage, zb, t, bar, tw4n, fftw, p, f, taylor_sign_d(l));
+      else
+        fwd_term<LOG2N, false>(stage, zb, t, bar, tw4n, fftw, p, f, taylor_sign_d(l));
     }
-    col_sync<C::GT>(bar);
-    // ---- pack: Z_m for m = t + T i -------------------------------------
-#pragma unroll
-    for (int i = 0; i < C::E; ++i) {
-      const int m = t + T * i;
-      auto X = [&](int j) -> double {  // X_j of the current term, 0 <= j <= N
-        if (j == 0) return odd ? 0.0 : stage[0];
-        if (j >= N) return 0.0;
-        return 0.5 * (odd ? stage[N - j] : stage[j]);
-      };
-      const double2 ta = __ldg(&tw4n[m]);       // e^{i pi m/(2N)}
-      const double2 tb = __ldg(&tw4n[m + P]);   // e^{i pi (m+P)/(2N)}
-      const double2 r4 = __ldg(&tw4n[4 * m]);   // e^{2 pi i m/N}
-      const double xa = X(m), xan = X(N - m), xb = X(m + P), xbn = X(P - m);
-      // W = tw (X_j - i X_{N-j})
-      const double2 Wa = make_double2(ta.x * xa + ta.y * xan, ta.y * xa - ta.x * xan);
-      const double2 Wb = make_double2(tb.x * xb + tb.y * xbn, tb.y * xb - tb.x * xbn);
-      const double2 s = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
-      const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
-      const double2 dr = make_double2(d.x * r4.x - d.y * r4.y, d.x * r4.y + d.y * r4.x);
-      zb[smem_pad(m)] = make_double2(s.x - dr.y, s.y + dr.x);  // s + i dr
-    }
-    col_sync<C::GT>(bar);
-    fft_row_smem<P, C::E, true, C::GT>(zb, t, fftw, bar);
-    // ---- unpack + Taylor weight + accumulate ----------------------------
-    const double sign = plain_op < 0 ? taylor_sign_d(l) : 1.0;
-#pragma unroll
-    for (int i = 0; i < OWN; ++i) {
-      const int k = t + T * i;
-      const int q = (k & 1) ? (N - 1 - (k >> 1)) : (k >> 1);
-      const double2 z = zb[smem_pad(q >> 1)];
-      double y = (q & 1) ? z.y : z.x;
-      if (odd && (k & 1)) y = -y;
-      f[i] += sign * p[i] * y;
-    }
-    col_sync<C::GT>(bar);
   }
+  // scatter the owned rows through shared memory, then one coalesced store
+  group_sync<C::GT>(bar);
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) stage[kown[i]] = f[i];
+  group_sync<C::GT>(bar);
   double* dst = out + col * ld_out;
 #pragma unroll
-  for (int i = 0; i < OWN; ++i) dst[t + T * i] = f[i];
+  for (int i = 0; i < OWN; ++i) dst[t + T * i] = stage[t + T * i];
+}
+
+// One transposed Taylor term: o[i] += sign rp[i] X_{row i}.
+template <int LOG2N, bool ODD>
+__device__ __forceinline__ void tr_term(const double* hs, double2* zb, int t, int bar,
+                                        const double2* __restrict__ tw4n, const double2* fftw,
+                                        const double* rp, double* o, double sign) {
+  using C = Cfg<LOG2N>;
+  constexpr int N = C::N, P = C::P, T = C::T, E = C::E, OWN = C::OWN;
+  // pack v_q = h_{2q} (q < P), v_{N-1-q} = h_{2q+1}; z_m = v_{2m} + i v_{2m+1};
+  // odd terms (DST^T) use (-1)^k h_k, i.e. negate the odd-index entries
+  auto V = [&](int q) -> double { return q < P ? hs[2 * q] : (ODD ? -1.0 : 1.0) * hs[2 * (N - 1 - q) + 1]; };
+  double2 v[E];
+#pragma unroll
+  for (int r = 0; r < E; ++r) {
+    const int m = t + r * T;
+    v[r] = make_double2(V(2 * m), V(2 * m + 1));
+  }
+  pass_compute<P, E, 8, 1, false>(v, t, fftw);
+  pass_store<P, E, 8, 1>(v, zb, t);
+  group_sync<C::GT>(bar);
+  mid_passes<P, E, 8, P, false, C::GT>(zb, t, fftw, bar);
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) {
+    const int n = t + T * i;
+    double X = 0.0;
+    const int kk = ODD ? (N - n) : n;  // DST^T row n is DCT-II row N - n
+    if (!(ODD && n == 0)) {
+      const int a = kk & (P - 1), b = (P - kk) & (P - 1);
+      const double2 za = zb[smem_pad(a)], zc = zb[smem_pad(b)];
+      // V = (Za + conj Zb)/2 + e^{-2 pi i kk/N} (Za - conj Zb)/(2i)
+      const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
+      const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));
+      // e^{-2 pi i kk / N} = conj(tw4n[4 kk]) with 4 kk reduced below 2N
+      const int q4 = 4 * kk;
+      double2 r = q4 < 2 * N ? __ldg(&tw4n[q4]) : __ldg(&tw4n[q4 - 2 * N]);
+      if (q4 >= 2 * N) r = make_double2(-r.x, -r.y);
+      r.y = -r.y;
+      const double2 Vv = make_double2(ev.x + od.x * r.x - od.y * r.y, ev.y + od.x * r.y + od.y * r.x);
+      const double2 h = __ldg(&tw4n[kk]);  // e^{+i pi kk/(2N)}; X = Re(conj(h) V)
+      X = h.x * Vv.x + h.y * Vv.y;
+    }
+    o[i] += sign * rp[i] * X;
+  }
 }
 
 template <int LOG2N>
@@ -180,7 +277,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
                         const double2* __restrict__ tw4n, const double2* __restrict__ fftw_g,
                         int* nonfinite) {
   using C = Cfg<LOG2N>;
-  constexpr int N = C::N, P = C::P, T = C::T, OWN = C::OWN;
+  constexpr int N = C::N, T = C::T, OWN = C::OWN;
   extern __shared__ double smem[];
   double* nd = smem + C::COLS * (C::COL_BYTES / 8);
   double2* fftw_s = reinterpret_cast<double2*>(nd + N);
@@ -211,55 +308,31 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     rp[i] = 1.0;
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
-  const int terms = plain_op < 0 ? num_terms : 1;
-  for (int l = 0; l < terms; ++l) {
-    const bool odd = plain_op < 0 ? (l & 1) : (plain_op == 1);
-    if (l > 0) {
-      const double inv_l = 1.0 / (double)l;
+  group_sync<C::GT>(bar);
+  if (plain_op >= 0) {
+    if (plain_op == 1)
+      tr_term<LOG2N, true>(hs, zb, t, bar, tw4n, fftw, rp, o, 1.0);
+    else
+      tr_term<LOG2N, false>(hs, zb, t, bar, tw4n, fftw, rp, o, 1.0);
+  } else {
+    for (int l = 0; l < num_terms; ++l) {
+      if (l > 0) {
+        const double inv_l = 1.0 / (double)l;
+        group_sync<C::GT>(bar);  // the previous term's reads of zb and hs are done
 #pragma unroll
-      for (int i = 0; i < OWN; ++i) {
-        const int k = t + T * i;
-        const double q = C::SMEM_TABLES ? nd[k] : (double)N * __ldg(&delta[k]);
-        hs[k] *= q * inv_l;
-        rp[i] *= (double)k / (double)N;  // (n/N)^l for output row n = k
+        for (int i = 0; i < OWN; ++i) {
+          const int k = t + T * i;
+          const double q = C::SMEM_TABLES ? nd[k] : (double)N * __ldg(&delta[k]);
+          hs[k] *= q * inv_l;
+          rp[i] *= (double)k / (double)N;  // (n/N)^l for output row n = k
+        }
+        group_sync<C::GT>(bar);
       }
+      if (l & 1)
+        tr_term<LOG2N, true>(hs, zb, t, bar, tw4n, fftw, rp, o, taylor_sign_d(l));
+      else
+        tr_term<LOG2N, false>(hs, zb, t, bar, tw4n, fftw, rp, o, taylor_sign_d(l));
     }
-    col_sync<C::GT>(bar);
-    // ---- pack: v_q = h_{2q} (q < P), v_{N-1-q} = h_{2q+1}; z_m = v_{2m} + i v_{2m+1};
-    // odd terms (DST^T) use (-1)^k h_k, i.e. negate the odd-index entries
-    const double fl = odd ? -1.0 : 1.0;
-#pragma unroll
-    for (int i = 0; i < C::E; ++i) {
-      const int m = t + T * i;
-      auto V = [&](int q) -> double { return q < P ? hs[2 * q] : fl * hs[2 * (N - 1 - q) + 1]; };
-      zb[smem_pad(m)] = make_double2(V(2 * m), V(2 * m + 1));
-    }
-    col_sync<C::GT>(bar);
-    fft_row_smem<P, C::E, false, C::GT>(zb, t, fftw, bar);
-    const double sign = plain_op < 0 ? taylor_sign_d(l) : 1.0;
-#pragma unroll
-    for (int i = 0; i < OWN; ++i) {
-      const int n = t + T * i;
-      double X = 0.0;
-      const int kk = odd ? (N - n) : n;  // DST^T row n is DCT-II row N - n
-      if (!(odd && n == 0)) {
-        const int a = kk & (P - 1), b = (P - kk) & (P - 1);
-        const double2 za = zb[smem_pad(a)], zc = zb[smem_pad(b)];
-        // V = (Za + conj Zb)/2 + e^{-2 pi i kk/N} (Za - conj Zb)/(2i)
-        const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
-        const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));
-        // e^{-2 pi i kk / N} = conj(tw4n[4 kk]) with 4 kk reduced below 2N
-        const int q4 = 4 * kk;
-        double2 r = q4 < 2 * N ? __ldg(&tw4n[q4]) : __ldg(&tw4n[q4 - 2 * N]);
-        if (q4 >= 2 * N) r = make_double2(-r.x, -r.y);
-        r.y = -r.y;
-        const double2 Vv = make_double2(ev.x + od.x * r.x - od.y * r.y, ev.y + od.x * r.y + od.y * r.x);
-        const double2 h = __ldg(&tw4n[kk]);  // e^{+i pi kk/(2N)}; X = Re(conj(h) V)
-        X = h.x * Vv.x + h.y * Vv.y;
-      }
-      o[i] += sign * rp[i] * X;
-    }
-    col_sync<C::GT>(bar);
   }
   double* dst = out + col * ld_out;
 #pragma unroll

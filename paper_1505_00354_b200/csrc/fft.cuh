@@ -109,18 +109,23 @@ __device__ __forceinline__ void group_sync(int bar) {
   }
 }
 
-template <int P, int E, int R, int NS, bool INV, int GT>
-__device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2* tw, int bar) {
-  constexpr int TR = P / E;
-  constexpr int NB = E / R;
-  double2 v[E];
+// The three stages of a pass, usable separately so that a kernel can feed the
+// first pass from registers and consume the last pass in registers.
+// Input of butterfly q of thread tid: v[q R + r] = x[j + r P/R], j = tid + q TR.
+template <int P, int E, int R>
+__device__ __forceinline__ void pass_load(double2* v, const double2* s, int tid) {
+  constexpr int TR = P / E, NB = E / R;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
     const int j = tid + q * TR;
 #pragma unroll
     for (int r = 0; r < R; ++r) v[q * R + r] = s[smem_pad(j + r * (P / R))];
   }
-  group_sync<GT>(bar);
+}
+
+template <int P, int E, int R, int NS, bool INV>
+__device__ __forceinline__ void pass_compute(double2* v, int tid, const double2* tw) {
+  constexpr int TR = P / E, NB = E / R;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
     const int j = tid + q * TR;
@@ -135,12 +140,38 @@ __device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2
       }
     }
     dft_r<R, INV>(&v[q * R]);
-    const int base = (j - k) * R + k;  // (j/Ns) Ns R + (j mod Ns)
-#pragma unroll
-    for (int r = 0; r < R; ++r) s[smem_pad(base + r * NS)] = v[q * R + r];
   }
+}
+
+// Output r of butterfly q goes to index (j - k) R + k + r Ns, k = j mod Ns.
+template <int P, int E, int R, int NS>
+__host__ __device__ constexpr int pass_out_index(int tid, int q, int r) {
+  return ((tid + q * (P / E)) - ((tid + q * (P / E)) & (NS - 1))) * R +
+         ((tid + q * (P / E)) & (NS - 1)) + r * NS;
+}
+
+template <int P, int E, int R, int NS>
+__device__ __forceinline__ void pass_store(const double2* v, double2* s, int tid) {
+  constexpr int NB = E / R;
+#pragma unroll
+  for (int q = 0; q < NB; ++q)
+#pragma unroll
+    for (int r = 0; r < R; ++r) s[smem_pad(pass_out_index<P, E, R, NS>(tid, q, r))] = v[q * R + r];
+}
+
+template <int P, int E, int R, int NS, bool INV, int GT>
+__device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2* tw, int bar) {
+  double2 v[E];
+  pass_load<P, E, R>(v, s, tid);
+  group_sync<GT>(bar);
+  pass_compute<P, E, R, NS, INV>(v, tid, tw);
+  pass_store<P, E, R, NS>(v, s, tid);
   group_sync<GT>(bar);
 }
+
+// Passes NS0 .. P of a row (pass-major twiddle offset OFF of the first one).
+template <int P, int E, int NS, int OFF, bool INV, int GT>
+__device__ __forceinline__ void fft_passes(double2* s, int tid, const double2* tw, int bar);
 
 __host__ __device__ constexpr int pass_radix(int p, int ns) { return p / ns >= 8 ? 8 : p / ns; }
 
@@ -168,6 +199,29 @@ __device__ __forceinline__ void fft_passes(double2* s, int tid, const double2* t
 template <int P, int E, bool INV, int GT = 0>
 __device__ __forceinline__ void fft_row_smem(double2* s, int tid, const double2* tw, int bar = 0) {
   fft_passes<P, E, 1, 0, INV, GT>(s, tid, tw, bar);
+}
+
+// Ns of the last pass, and the pass-major table offset of the pass with Ns.
+__host__ __device__ constexpr int last_pass_ns(int p) {
+  int ns = 1;
+  while (ns * pass_radix(p, ns) < p) ns *= pass_radix(p, ns);
+  return ns;
+}
+__host__ __device__ constexpr int pass_tw_offset(int p, int ns_target) {
+  int off = 0;
+  for (int ns = 1; ns < ns_target; ns *= pass_radix(p, ns))
+    if (ns > 1) off += (pass_radix(p, ns) - 1) * ns;
+  return off;
+}
+
+// The passes with NS <= ns < NS_END (each ending with a row barrier).
+template <int P, int E, int NS, int NS_END, bool INV, int GT>
+__device__ __forceinline__ void mid_passes(double2* s, int tid, const double2* tw, int bar) {
+  if constexpr (NS < NS_END) {
+    constexpr int R = pass_radix(P, NS);
+    stockham_pass<P, E, R, NS, INV, GT>(s, tid, tw + pass_tw_offset(P, NS), bar);
+    mid_passes<P, E, NS * R, NS_END, INV, GT>(s, tid, tw, bar);
+  }
 }
 
 // Device pass-major twiddle table for length 2^log2p (cached per device).
