@@ -83,19 +83,63 @@ __device__ __forceinline__ int fwd_row_of(int q) {
   return q < N / 2 ? 2 * q : 2 * (N - 1 - q) + 1;
 }
 
-// Packed Z_m of the forward transform for term parity ODD.
-template <int N, bool ODD>
-__device__ __forceinline__ double2 fwd_pack(const double* stage, int m,
-                                            const double2* __restrict__ tw4n) {
+// e^{i pi r/32} and e^{i pi r/8}, r < 8: with T = N/16 threads per column the
+// pack twiddles of m = t + r T are per-thread bases times these constants.
+// (16 entries: the transpose's unpack uses rows n = t + i T, i < 16.)
+struct PackConst {
+  static constexpr double c32[16][2] = {
+      {1.0, 0.0}, {0.9951847266721969, 0.0980171403295606}, {0.9807852804032304, 0.19509032201612828},
+      {0.9569403357322088, 0.2902846772544624}, {0.9238795325112867, 0.3826834323650898},
+      {0.881921264348355, 0.47139673682599764}, {0.8314696123025452, 0.5555702330196022},
+      {0.773010453362737, 0.6343932841636455}, {0.7071067811865476, 0.7071067811865476},
+      {0.6343932841636455, 0.773010453362737}, {0.5555702330196022, 0.8314696123025452},
+      {0.47139673682599764, 0.881921264348355}, {0.3826834323650898, 0.9238795325112867},
+      {0.2902846772544624, 0.9569403357322088}, {0.19509032201612828, 0.9807852804032304},
+      {0.0980171403295606, 0.9951847266721969}};
+  static constexpr double c8[16][2] = {
+      {1.0, 0.0}, {0.9238795325112867, 0.3826834323650898}, {0.7071067811865476, 0.7071067811865476},
+      {0.3826834323650898, 0.9238795325112867}, {0.0, 1.0}, {-0.3826834323650898, 0.9238795325112867},
+      {-0.7071067811865476, 0.7071067811865476}, {-0.9238795325112867, 0.3826834323650898},
+      {-1.0, 0.0}, {-0.9238795325112867, -0.3826834323650898}, {-0.7071067811865476, -0.7071067811865476},
+      {-0.3826834323650898, -0.9238795325112867}, {0.0, -1.0}, {0.3826834323650898, -0.9238795325112867},
+      {0.7071067811865476, -0.7071067811865476}, {0.9238795325112867, -0.3826834323650898}};
+};
+
+// The same constants in constant memory, for loop-indexed use.
+__constant__ double kC32[16][2] = {
+    {1.0, 0.0}, {0.9951847266721969, 0.0980171403295606}, {0.9807852804032304, 0.19509032201612828},
+    {0.9569403357322088, 0.2902846772544624}, {0.9238795325112867, 0.3826834323650898},
+    {0.881921264348355, 0.47139673682599764}, {0.8314696123025452, 0.5555702330196022},
+    {0.773010453362737, 0.6343932841636455}, {0.7071067811865476, 0.7071067811865476},
+    {0.6343932841636455, 0.773010453362737}, {0.5555702330196022, 0.8314696123025452},
+    {0.47139673682599764, 0.881921264348355}, {0.3826834323650898, 0.9238795325112867},
+    {0.2902846772544624, 0.9569403357322088}, {0.19509032201612828, 0.9807852804032304},
+    {0.0980171403295606, 0.9951847266721969}};
+__constant__ double kC8[16][2] = {
+    {1.0, 0.0}, {0.9238795325112867, 0.3826834323650898}, {0.7071067811865476, 0.7071067811865476},
+    {0.3826834323650898, 0.9238795325112867}, {0.0, 1.0}, {-0.3826834323650898, 0.9238795325112867},
+    {-0.7071067811865476, 0.7071067811865476}, {-0.9238795325112867, 0.3826834323650898},
+    {-1.0, 0.0}, {-0.9238795325112867, -0.3826834323650898}, {-0.7071067811865476, -0.7071067811865476},
+    {-0.3826834323650898, -0.9238795325112867}, {0.0, -1.0}, {0.3826834323650898, -0.9238795325112867},
+    {0.7071067811865476, -0.7071067811865476}, {0.9238795325112867, -0.3826834323650898}};
+
+// Packed Z_m of the forward transform for term parity ODD, m = t + r T.
+// ta_t = e^{i pi t/(2N)}, r4_t = e^{2 pi i t/N} (per-thread bases).
+template <int N, bool ODD, int R>
+__device__ __forceinline__ double2 fwd_pack(const double* stage, int m, double2 ta_t, double2 r4_t) {
   constexpr int P = N / 2;
+  constexpr double h = 0.70710678118654752440;
   auto X = [&](int j) -> double {  // X_j, 0 <= j <= N
     if (j == 0) return ODD ? 0.0 : stage[0];
     if (j >= N) return 0.0;
     return 0.5 * (ODD ? stage[N - j] : stage[j]);
   };
-  const double2 ta = __ldg(&tw4n[m]);      // e^{i pi m/(2N)}
-  const double2 tb = __ldg(&tw4n[m + P]);  // e^{i pi (m+P)/(2N)}
-  const double2 r4 = __ldg(&tw4n[4 * m]);  // e^{2 pi i m/N}
+  constexpr double a32x = PackConst::c32[R][0], a32y = PackConst::c32[R][1];
+  constexpr double a8x = PackConst::c8[R][0], a8y = PackConst::c8[R][1];
+  // e^{i pi m/(2N)}, e^{i pi (m+P)/(2N)} = e^{i pi/4} e^{i pi m/(2N)}, e^{2 pi i m/N}
+  const double2 ta = make_double2(ta_t.x * a32x - ta_t.y * a32y, ta_t.x * a32y + ta_t.y * a32x);
+  const double2 tb = make_double2(h * (ta.x - ta.y), h * (ta.x + ta.y));
+  const double2 r4 = make_double2(r4_t.x * a8x - r4_t.y * a8y, r4_t.x * a8y + r4_t.y * a8x);
   const double xa = X(m), xan = X(N - m), xb = X(m + P), xbn = X(P - m);
   const double2 Wa = make_double2(ta.x * xa + ta.y * xan, ta.y * xa - ta.x * xan);
   const double2 Wb = make_double2(tb.x * xb + tb.y * xbn, tb.y * xb - tb.x * xbn);
@@ -106,15 +150,24 @@ __device__ __forceinline__ double2 fwd_pack(const double* stage, int m,
 }
 
 // One forward Taylor term (or one plain transform): f[i] += sign p[i] y_{k_i}.
+template <int N, bool ODD, int R>
+__device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, int t, double2 ta_t,
+                                             double2 r4_t) {
+  if constexpr (R < 8) {
+    v[R] = fwd_pack<N, ODD, R>(stage, t + R * (N / 16), ta_t, r4_t);
+    fwd_pack_all<N, ODD, R + 1>(v, stage, t, ta_t, r4_t);
+  }
+}
+
 template <int LOG2N, bool ODD>
 __device__ __forceinline__ void fwd_term(const double* stage, double2* zb, int t, int bar,
-                                         const double2* __restrict__ tw4n, const double2* fftw,
+                                         double2 ta_t, double2 r4_t, const double2* fftw,
                                          const double* p, double* f, double sign) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, NSL = C::NSL, RL = C::RL;
+  static_assert(E == 8 && T == N / 16, "pack twiddle constants assume T = N/16");
   double2 v[E];
-#pragma unroll
-  for (int r = 0; r < E; ++r) v[r] = fwd_pack<N, ODD>(stage, t + r * T, tw4n);
+  fwd_pack_all<N, ODD, 0>(v, stage, t, ta_t, r4_t);
   pass_compute<P, E, 8, 1, true>(v, t, fftw);
   pass_store<P, E, 8, 1>(v, zb, t);
   group_sync<C::GT>(bar);
@@ -189,12 +242,15 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     f[i] = 0.0;
     p[i] = 1.0;
   }
+  // per-thread pack twiddle bases e^{i pi t/(2N)}, e^{2 pi i t/N} (table of 4N-th roots)
+  const double2 ta_t = __ldg(&tw4n[t]);
+  const double2 r4_t = __ldg(&tw4n[4 * t]);
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      fwd_term<LOG2N, true>(stage, zb, t, bar, tw4n, fftw, p, f, 1.0);
+      fwd_term<LOG2N, true>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
     else
-      fwd_term<LOG2N, false>(stage, zb, t, bar, tw4n, fftw, p, f, 1.0);
+      fwd_term<LOG2N, false>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
   } else {
     for (int l = 0; l < num_terms; ++l) {
       if (l > 0) {
@@ -210,9 +266,9 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
         group_sync<C::GT>(bar);
       }
       if (l & 1)
-        fwd_term<LOG2N, true>(stage, zb, t, bar, tw4n, fftw, p, f, taylor_sign_d(l));
+        fwd_term<LOG2N, true>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, taylor_sign_d(l));
       else
-        fwd_term<LOG2N, false>(stage, zb, t, bar, tw4n, fftw, p, f, taylor_sign_d(l));
+        fwd_term<LOG2N, false>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, taylor_sign_d(l));
     }
   }
   // scatter the owned rows through shared memory, then one coalesced store
@@ -228,7 +284,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
 // One transposed Taylor term: o[i] += sign rp[i] X_{row i}.
 template <int LOG2N, bool ODD>
 __device__ __forceinline__ void tr_term(const double* hs, double2* zb, int t, int bar,
-                                        const double2* __restrict__ tw4n, const double2* fftw,
+                                        double2 ta_t, double2 r4_t, const double2* fftw,
                                         const double* rp, double* o, double sign) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, OWN = C::OWN;
@@ -256,14 +312,16 @@ __device__ __forceinline__ void tr_term(const double* hs, double2* zb, int t, in
       // V = (Za + conj Zb)/2 + e^{-2 pi i kk/N} (Za - conj Zb)/(2i)
       const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
       const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));
-      // e^{-2 pi i kk / N} = conj(tw4n[4 kk]) with 4 kk reduced below 2N
-      const int q4 = 4 * kk;
-      double2 r = q4 < 2 * N ? __ldg(&tw4n[q4]) : __ldg(&tw4n[q4 - 2 * N]);
-      if (q4 >= 2 * N) r = make_double2(-r.x, -r.y);
-      r.y = -r.y;
+      // n = t + i T: e^{i pi n/(2N)} = ta_t c32[i], e^{2 pi i n/N} = r4_t c8[i]
+      const double a32x = kC32[i][0], a32y = kC32[i][1];
+      const double a8x = kC8[i][0], a8y = kC8[i][1];
+      const double2 tn = make_double2(ta_t.x * a32x - ta_t.y * a32y, ta_t.x * a32y + ta_t.y * a32x);
+      const double2 rn = make_double2(r4_t.x * a8x - r4_t.y * a8y, r4_t.x * a8y + r4_t.y * a8x);
+      // r = e^{-2 pi i kk/N}, h = e^{i pi kk/(2N)} for kk = n (DCT) or N - n (DST)
+      const double2 r = ODD ? rn : make_double2(rn.x, -rn.y);
+      const double2 h = ODD ? make_double2(tn.y, tn.x) : tn;
       const double2 Vv = make_double2(ev.x + od.x * r.x - od.y * r.y, ev.y + od.x * r.y + od.y * r.x);
-      const double2 h = __ldg(&tw4n[kk]);  // e^{+i pi kk/(2N)}; X = Re(conj(h) V)
-      X = h.x * Vv.x + h.y * Vv.y;
+      X = h.x * Vv.x + h.y * Vv.y;  // Re(conj(h) V)
     }
     o[i] += sign * rp[i] * X;
   }
@@ -308,12 +366,14 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     rp[i] = 1.0;
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
+  const double2 ta_t = __ldg(&tw4n[t]);      // e^{i pi t/(2N)}
+  const double2 r4_t = __ldg(&tw4n[4 * t]);  // e^{2 pi i t/N}
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      tr_term<LOG2N, true>(hs, zb, t, bar, tw4n, fftw, rp, o, 1.0);
+      tr_term<LOG2N, true>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
     else
-      tr_term<LOG2N, false>(hs, zb, t, bar, tw4n, fftw, rp, o, 1.0);
+      tr_term<LOG2N, false>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
   } else {
     for (int l = 0; l < num_terms; ++l) {
       if (l > 0) {
@@ -329,9 +389,9 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
         group_sync<C::GT>(bar);
       }
       if (l & 1)
-        tr_term<LOG2N, true>(hs, zb, t, bar, tw4n, fftw, rp, o, taylor_sign_d(l));
+        tr_term<LOG2N, true>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
       else
-        tr_term<LOG2N, false>(hs, zb, t, bar, tw4n, fftw, rp, o, taylor_sign_d(l));
+        tr_term<LOG2N, false>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
     }
   }
   double* dst = out + col * ld_out;
