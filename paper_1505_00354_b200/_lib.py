@@ -11,7 +11,7 @@ import ctypes as C
 import os
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libfastleg_b200.so")
+LIB_PATH = os.environ.get("FLB_LIB_PATH") or os.path.join(HERE, "libfastleg_b200.so")
 
 FL_OK, FL_INVALID_ARGUMENT, FL_DOMAIN_ERROR, FL_OVERFLOW_ERROR, FL_RUNTIME_ERROR, FL_CUDA_ERROR = range(6)
 CHEB1, CHEBSTAR = 0, 1

@@ -16,7 +16,9 @@ FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",
     "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
     "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include"), "-I" + CSRC,
-]
+] + os.environ.get("FLB_NVCC_EXTRA", "").split()
+if os.environ.get("FLB_LIB_OUT"):  # experiment builds (tools/): alternative library path
+    LIB = os.environ["FLB_LIB_OUT"]
 
 
 def _stale() -> bool:

@@ -65,7 +65,13 @@ struct Cfg {
   static constexpr int E = 8;
   static constexpr int T = P / E;                 // threads per column
   static constexpr int OWN = N / T;               // rows owned per thread (= 2E)
-  static constexpr int COLS = T >= 512 ? 1 : 512 / T;
+// 256 threads per CTA measured faster than 512 at N = 4096 (24.3 vs 27.5 ms for
+// 65536 columns, L = 17): the 255-register budget avoids the spills that the
+// 128-register one forces (tools/bench_kernels.py, profiles/).
+#ifndef FLB_NDCT_CTA_THREADS
+#define FLB_NDCT_CTA_THREADS 256
+#endif
+  static constexpr int COLS = T >= FLB_NDCT_CTA_THREADS ? 1 : FLB_NDCT_CTA_THREADS / T;
   static constexpr int THREADS = T * COLS;
   static constexpr int TW = twiddle_entries(P);   // pass-major FFT twiddles
   static constexpr int NSL = last_pass_ns(P);     // last FFT pass
@@ -228,14 +234,10 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
   // the rows this thread accumulates: the outputs of its last-pass butterflies
-  int kown[OWN];
-#pragma unroll
-  for (int q = 0; q < E / RL; ++q)
-#pragma unroll
-    for (int r = 0; r < RL; ++r)
-#pragma unroll
-      for (int part = 0; part < 2; ++part)
-        kown[2 * (q * RL + r) + part] = fwd_row_of<N>(2 * (t + q * T + r * NSL) + part);
+  auto kown = [&](int i) -> int {
+    const int s = i >> 1, q = s / RL, r = s % RL;
+    return fwd_row_of<N>(2 * (t + q * T + r * NSL) + (i & 1));
+  };
   double f[OWN], p[OWN];
 #pragma unroll
   for (int i = 0; i < OWN; ++i) {
@@ -259,7 +261,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
         for (int i = 0; i < OWN; ++i) {
           const int n = t + T * i;
           stage[n] *= (double)n / (double)N;  // (n/N)^l c_n
-          const int k = kown[i];
+          const int k = kown(i);
           const double q = C::SMEM_TABLES ? nd[k] : (double)N * __ldg(&delta[k]);
           p[i] *= q * inv_l;                   // (N delta_k)^l / l!
         }
@@ -274,7 +276,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   // scatter the owned rows through shared memory, then one coalesced store
   group_sync<C::GT>(bar);
 #pragma unroll
-  for (int i = 0; i < OWN; ++i) stage[kown[i]] = f[i];
+  for (int i = 0; i < OWN; ++i) stage[kown(i)] = f[i];
   group_sync<C::GT>(bar);
   double* dst = out + col * ld_out;
 #pragma unroll
