@@ -250,9 +250,22 @@ def main() -> None:
     coef = n * cols
     l2c_flops = coef * (n / 2.0)                   # N^2/4 MACs per column = N/2 flop per coefficient
     ndct_flops = coef * L1 * (2.5 * math.log2(n) + 3)  # L (2.5 log2 N + 3)
-    dom = "leg2cheb_fwd_tiled" if ms_l2c >= ms_ndct else "fast_ndct_fwd_kernel"
-    achieved = (l2c_flops / (ms_l2c / 1e3) if dom == "leg2cheb_fwd_tiled" else ndct_flops / (ms_ndct / 1e3)) / 1e12
+    dom = "leg2cheb_mma_kernel" if ms_l2c >= ms_ndct else "fast_ndct_fwd_kernel"
+    achieved = (l2c_flops / (ms_l2c / 1e3) if dom == "leg2cheb_mma_kernel" else ndct_flops / (ms_ndct / 1e3)) / 1e12
     hbm_peak = json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else 6650.0
+    # DRAM traffic of the dominant kernel per launch, from the committed ncu
+    # --set full capture (profiles/ncu_traffic.json: bytes per coefficient)
+    traffic = None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tfile):
+        tj = json.load(open(tfile))
+        for name, rec in tj.items():
+            if name.startswith(dom.split("<")[0]) and f"<{int(math.log2(n))}>" in name or (
+                    dom.startswith("leg2cheb") and name.startswith("leg2cheb_mma_kernel<0>")):
+                traffic = {"bytes_per_launch": rec["dram_bytes_per_coef"] * coef,
+                           "bytes_per_coef": rec["dram_bytes_per_coef"],
+                           "algorithmic_bytes_per_coef": 16.0, "source": rec["capture"]}
+                break
     dct_gbs = 16.0 * coef / (ms_dct / 1e3) / 1e9
 
     # ---- end to end through the public API with pinned host buffers
@@ -297,7 +310,7 @@ def main() -> None:
                        "parallelism": f"column shards x{world}, no collective",
                        "l2": "inputs (2 GiB) larger than L2 (126 MB); no flush"},
             "roofline": {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
                          "peak_source": "measured DMMA/DFMA peak, tools/fp64_peak.cu (profiles/r01_fp64_peak.log)",
                          "algorithmic": "leg2cheb N/2 flop/coef; NDCT L(2.5 log2N + 3) flop/coef"},
             "roofline_hbm": {"bound": "hbm", "achieved": 16.0 * value / 1e9, "peak": hbm_peak, "unit": "GB/s",

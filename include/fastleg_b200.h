@@ -137,6 +137,21 @@ enum { FL_NDCT_LITERAL = 0, FL_NDCT_FAST = 1 };
 fl_status fl_plan_set_ndct_mode(fl_plan* plan, int mode);
 int fl_plan_ndct_mode(const fl_plan* plan);
 
+/* oracle.hpp:19-153 direct O(N^2) evaluations, on the device (independent of
+ * the fast path: plain three-term recurrences, no FFTs).
+ *   eval_legendre_direct / eval_chebyshev_direct: out[j] = sum_n c_n P_n(xs[j])
+ *     (resp. T_n); any |xs[j]| > 1 -> FL_DOMAIN_ERROR.
+ *   idlt_direct: c_m = (m + 1/2) sum_k w_k f_k P_m(x_k).
+ *   cheb_coeffs_of_legendre: the n+1 Chebyshev coefficients of P_n from m
+ *     first-kind samples; m <= n -> FL_INVALID_ARGUMENT. */
+fl_status fl_eval_legendre_direct(const double* c, size_t n, const double* xs, size_t m,
+                                  double* out, void* stream);
+fl_status fl_eval_chebyshev_direct(const double* c, size_t n, const double* xs, size_t m,
+                                   double* out, void* stream);
+fl_status fl_idlt_direct(const double* f, size_t n, const double* x, const double* weights,
+                         double* out, void* stream);
+fl_status fl_cheb_coeffs_of_legendre(size_t n, size_t m, double* out, void* stream);
+
 /* random.hpp:15-55 input generators (host memory; std::mt19937_64 +
  * Box-Muller): random_decaying(n, decay, seed), and the uniform [-1,1)
  * recipe u = 2*((r()>>11)*2^-53) - 1 of SURVEY.md 8d (C4). Batched: column

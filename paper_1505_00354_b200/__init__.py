@@ -19,4 +19,5 @@ from .api import (  # noqa: F401
     leg2cheb_entry, legendre_coefficients, legendre_nodes_weights, max_taylor_terms,
     min_taylor_terms, ndct_apply, ndct_apply_transpose, ndct_error_bound, plan_ndct,
     random_decaying, random_uniform_pm1, reference_angle, reference_grid, taylor_term_bound,
+    eval_legendre_direct, eval_chebyshev_direct, idlt_direct, cheb_coeffs_of_legendre,
 )

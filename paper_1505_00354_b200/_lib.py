@@ -59,6 +59,8 @@ EXPORTS = [
     "fl_plan_tolerance", "fl_plan_num_terms", "fl_plan_grid", "fl_plan_reference",
     "fl_plan_lambda", "fl_dlt", "fl_idlt", "fl_plan_set_ndct_mode", "fl_plan_ndct_mode",
     "fl_random_decaying", "fl_random_uniform_pm1", "fl_kernel_launch_count",
+    "fl_eval_legendre_direct", "fl_eval_chebyshev_direct", "fl_idlt_direct",
+    "fl_cheb_coeffs_of_legendre",
 ]
 
 
@@ -96,6 +98,10 @@ def _load() -> C.CDLL:
         "fl_random_decaying": (None, [sz, d, u64, dp, sz, i]),
         "fl_random_uniform_pm1": (None, [sz, u64, dp, sz, i]),
         "fl_kernel_launch_count": (u64, []),
+        "fl_eval_legendre_direct": (i, [dp, sz, dp, sz, dp, vp]),
+        "fl_eval_chebyshev_direct": (i, [dp, sz, dp, sz, dp, vp]),
+        "fl_idlt_direct": (i, [dp, sz, dp, dp, dp, vp]),
+        "fl_cheb_coeffs_of_legendre": (i, [sz, sz, dp, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

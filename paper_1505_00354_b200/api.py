@@ -451,6 +451,47 @@ def idlt(f, config: TransformConfig) -> CoefficientVector:  # transforms.hpp:54-
 
 
 # ---------------------------------------------------------------------------
+# oracle.hpp (direct O(N^2) evaluations, as device kernels)
+# ---------------------------------------------------------------------------
+
+def _direct_eval(c: CoefficientVector, xs, chebyshev: int, where: str):
+    want = Basis.chebyshev if chebyshev else Basis.legendre
+    if c.basis != want:
+        raise _lib.InvalidArgument(f"{where}: expected {want.name.capitalize()} coefficients")
+    cv, x = _Arr(c.values), _Arr(xs)
+    n, m = _ncols_n(cv.obj)[1], _ncols_n(x.obj)[1]
+    out = _Arr(None, out_like=x, shape=(m,))
+    fn = LIB.fl_eval_chebyshev_direct if chebyshev else LIB.fl_eval_legendre_direct
+    check(fn(_vp(cv.ptr), n, _vp(x.ptr), m, _vp(out.ptr), x.stream))
+    return out.obj
+
+
+def eval_legendre_direct(c: CoefficientVector, xs):  # oracle.hpp:19-48
+    return _direct_eval(c, xs, 0, "eval_legendre_direct")
+
+
+def eval_chebyshev_direct(c: CoefficientVector, xs):  # oracle.hpp:52-79
+    return _direct_eval(c, xs, 1, "eval_chebyshev_direct")
+
+
+def idlt_direct(f, grid: LegendreGrid) -> CoefficientVector:  # oracle.hpp:84-116
+    a = _Arr(f)
+    n = _ncols_n(a.obj)[1]
+    if n != grid.size:
+        raise _lib.InvalidArgument("idlt_direct: value/grid size mismatch")
+    x, w = _Arr(grid.x), _Arr(grid.weights)
+    out = _Arr(None, out_like=a, shape=(n,))
+    check(LIB.fl_idlt_direct(_vp(a.ptr), n, _vp(x.ptr), _vp(w.ptr), _vp(out.ptr), a.stream))
+    return legendre_coefficients(out.obj)
+
+
+def cheb_coeffs_of_legendre(n: int, m: int) -> np.ndarray:  # oracle.hpp:122-153
+    out = np.empty(n + 1)
+    check(LIB.fl_cheb_coeffs_of_legendre(n, m, _vp(out.ctypes.data), None))
+    return out
+
+
+# ---------------------------------------------------------------------------
 # random.hpp (host input generators)
 # ---------------------------------------------------------------------------
 

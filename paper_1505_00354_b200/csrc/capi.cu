@@ -13,6 +13,7 @@
 
 #include "common.cuh"
 #include "czt.cuh"
+#include "direct.cuh"
 #include "fast_ndct.cuh"
 #include "launch.cuh"
 #include "leg2cheb.cuh"
@@ -643,6 +644,61 @@ fl_status fl_idlt(const fl_plan* p, const double* in, double* out, size_t batch,
                n, batch, p->w, fast, s);
     }
     leg2cheb_direct(1, n, p->s, back.p, o.ptr, batch, o.ld, 1, s);
+    o.finish();
+    sync(s);
+  });
+}
+
+static fl_status direct_eval_entry(int chebyshev, const double* c, size_t n, const double* xs,
+                                   size_t m, double* out, void* stream) {
+  return guarded([&] {
+    if (m == 0) return;
+    require_device();
+    cudaStream_t s = as_stream(stream);
+    DevIn x(xs, m, 1, m, s);
+    if (!direct_domain_ok(x.ptr, m, s))
+      fail(FL_DOMAIN_ERROR, std::string(chebyshev ? "eval_chebyshev_direct" : "eval_legendre_direct") +
+                                ": abscissa outside [-1, 1]");
+    DevIn cc(c, n, 1, n, s);
+    DevOut o(out, m, 1, m, s);
+    direct_eval(chebyshev, cc.ptr, n, x.ptr, m, o.ptr, s);
+    o.finish();
+    sync(s);
+  });
+}
+
+fl_status fl_eval_legendre_direct(const double* c, size_t n, const double* xs, size_t m,
+                                  double* out, void* stream) {
+  return direct_eval_entry(0, c, n, xs, m, out, stream);
+}
+
+fl_status fl_eval_chebyshev_direct(const double* c, size_t n, const double* xs, size_t m,
+                                   double* out, void* stream) {
+  return direct_eval_entry(1, c, n, xs, m, out, stream);
+}
+
+fl_status fl_idlt_direct(const double* f, size_t n, const double* x, const double* weights,
+                         double* out, void* stream) {
+  return guarded([&] {
+    if (n == 0) return;
+    require_device();
+    cudaStream_t s = as_stream(stream);
+    DevIn ff(f, n, 1, n, s), xx(x, n, 1, n, s), ww(weights, n, 1, n, s);
+    DevOut o(out, n, 1, n, s);
+    direct_idlt(ff.ptr, xx.ptr, ww.ptr, n, o.ptr, s);
+    o.finish();
+    sync(s);
+  });
+}
+
+fl_status fl_cheb_coeffs_of_legendre(size_t n, size_t m, double* out, void* stream) {
+  return guarded([&] {
+    if (m <= n)
+      fail(FL_INVALID_ARGUMENT, "cheb_coeffs_of_legendre: need more sample points than degree");
+    require_device();
+    cudaStream_t s = as_stream(stream);
+    DevOut o(out, n + 1, 1, n + 1, s);
+    direct_cheb_coeffs(n, m, o.ptr, s);
     o.finish();
     sync(s);
   });
