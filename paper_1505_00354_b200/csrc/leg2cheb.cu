@@ -323,6 +323,112 @@ __global__ void __launch_bounds__(mma::THREADS, 2)
   }
 }
 
+// ---------------------------------------------------------------------------
+// Few columns (single vectors up to large N): a tiled matrix-vector product.
+// A CTA owns TK consecutive rows of one parity and one column and streams the
+// inner index in chunks of KC through shared memory: the Toeplitz factor
+// s_{|row - inner|} and the Hankel factor s_{row + inner + p} are staged as
+// two zero-padded windows, the input chunk (pref folded in for M^T) as a
+// third. Each thread owns RB consecutive rows and slides two RB-register
+// windows along the inner index: per inner step 2 new s values + 1 input
+// (3 shared loads, 2 broadcast-free) feed RB multiply-adds.
+// ---------------------------------------------------------------------------
+namespace mv {
+constexpr int RB = 8;                 // rows per thread
+constexpr int THREADS = 128;
+constexpr int TK = RB * THREADS;      // rows per CTA (1024)
+constexpr int KC = 256;               // inner chunk
+}  // namespace mv
+
+template <bool TR>
+__global__ void __launch_bounds__(mv::THREADS)
+    leg2cheb_mv_kernel(const double* __restrict__ s, const double* __restrict__ in,
+                       double* __restrict__ out, size_t n, size_t ld, int scale_half) {
+  constexpr int RB = mv::RB, TK = mv::TK, KC = mv::KC;
+  // tw[i] = s_{d}, d = (TR ? row - inner : inner - row) over the chunk window
+  __shared__ double tw[TK + KC];
+  __shared__ double hw[TK + KC];  // s_{row + inner + p}
+  __shared__ double xv[KC];       // input at inner index (times pref for M^T)
+  const int p = blockIdx.z;
+  const size_t col = blockIdx.y;
+  const size_t nr = (n + 1 - p) / 2;
+  const size_t r0 = (size_t)blockIdx.x * TK;
+  if (r0 >= nr) return;
+  const double* x = in + col * ld;
+  const int t = threadIdx.x;
+  const size_t rt = r0 + (size_t)t * RB;  // this thread's first row
+  double acc[RB];
+#pragma unroll
+  for (int r = 0; r < RB; ++r) acc[r] = 0.0;
+  // inner range: forward b in [r0, nr); transpose a in [0, min(r0 + TK, nr))
+  const size_t i_begin = TR ? 0 : r0;
+  const size_t i_end = TR ? (r0 + TK < nr ? r0 + TK : nr) : nr;
+  for (size_t i0 = i_begin; i0 < i_end; i0 += KC) {
+    __syncthreads();
+    // Toeplitz window: forward d = inner - row in [i0 - r0 - (TK-1), i0 - r0 + KC - 1]
+    //                  transpose d = row - inner in [r0 - i0 - (KC-1), r0 - i0 + TK - 1]
+    for (int q = t; q < TK + KC; q += mv::THREADS) {
+      const long long d = TR ? (long long)r0 - (long long)i0 - (KC - 1) + q
+                             : (long long)i0 - (long long)r0 - (TK - 1) + q;
+      tw[q] = (d >= 0 && d < (long long)n) ? s[d] : 0.0;
+      const size_t h = r0 + i0 + p + q;  // row + inner + p, row - r0 + inner - i0 = q
+      hw[q] = h < n ? s[h] : 0.0;
+    }
+    for (int q = t; q < KC; q += mv::THREADS) {
+      const size_t i = i0 + q;
+      double v = 0.0;
+      if (i < i_end && i < nr) {
+        v = x[2 * i + p];
+        if (TR && (2 * i + p) != 0) v *= 2.0;  // pref of row k = 2a + p of M
+      }
+      xv[q] = v;
+    }
+    __syncthreads();
+    // Row r = rt + rr, inner i = i0 + j:
+    //   forward   Toeplitz index (i - row) + (TK-1) - (i0 - r0) = j - (rt - r0) - rr + TK - 1
+    //   transpose Toeplitz index (row - i) + (KC-1) - (r0 - i0) = (rt - r0) + rr - j + KC - 1
+    //   Hankel index row + i - r0 - i0 = (rt - r0) + rr + j
+    const int lr = (int)(rt - r0);
+    double tv[RB], hv[RB];
+#pragma unroll
+    for (int rr = 0; rr < RB; ++rr) {
+      tv[rr] = TR ? tw[lr + rr + KC - 1] : tw[TK - 1 - lr - rr];
+      hv[rr] = hw[lr + rr];
+    }
+    for (int j = 0; j < KC; j += RB) {
+#pragma unroll
+      for (int u = 0; u < RB; ++u) {
+        const int jj = j + u;  // tv/hv hold the factors of inner index i0 + jj
+        const double xj = xv[jj];
+#pragma unroll
+        for (int rr = 0; rr < RB; ++rr) acc[rr] = fma(tv[rr] * hv[rr], xj, acc[rr]);
+        if (jj + 1 == KC) break;
+        // slide: row rr at jj+1 takes row rr-1's Toeplitz factor at jj (both
+        // directions) and row rr+1's Hankel factor; one new value each
+#pragma unroll
+        for (int rr = RB - 1; rr > 0; --rr) tv[rr] = tv[rr - 1];
+        tv[0] = TR ? tw[lr + KC - 2 - jj] : tw[TK - lr + jj];
+#pragma unroll
+        for (int rr = 0; rr + 1 < RB; ++rr) hv[rr] = hv[rr + 1];
+        hv[RB - 1] = hw[lr + RB + jj];
+      }
+    }
+  }
+  // write: forward pref (k == 0 ? 1 : 2); transpose optional (m + 1/2)
+#pragma unroll
+  for (int rr = 0; rr < RB; ++rr) {
+    const size_t row = rt + rr;
+    if (row >= nr) continue;
+    const size_t k = 2 * row + p;
+    double v = acc[rr];
+    if (!TR)
+      v *= (k == 0 ? 1.0 : 2.0);
+    else if (scale_half)
+      v *= (double)k + 0.5;
+    out[col * ld + k] = v;
+  }
+}
+
 }  // namespace
 
 void scaled_lambda(const double* table, double* s, size_t count, cudaStream_t st) {
@@ -335,6 +441,15 @@ void leg2cheb_direct(int transpose, size_t n, const double* s, const double* in,
                      size_t cols, size_t ld, int scale_half, cudaStream_t st) {
   if (n == 0 || cols == 0) return;
   const size_t rows = (n + 1) / 2;
+  if (cols <= 16 && n >= 2) {  // single vectors / few columns: tiled matrix-vector product
+    dim3 grid((unsigned)((rows + mv::TK - 1) / mv::TK), (unsigned)cols, 2);
+    if (transpose)
+      leg2cheb_mv_kernel<true><<<grid, mv::THREADS, 0, st>>>(s, in, out, n, ld, scale_half);
+    else
+      leg2cheb_mv_kernel<false><<<grid, mv::THREADS, 0, st>>>(s, in, out, n, ld, 0);
+    note_launch(transpose ? "leg2cheb_mv_kernel<T>" : "leg2cheb_mv_kernel<F>");
+    return;
+  }
   const bool aligned = (ld % 2 == 0) && (reinterpret_cast<uintptr_t>(in) % 16 == 0);
   if (aligned && n >= 64) {
     const size_t smem = mma::SMEM_DOUBLES * sizeof(double);

@@ -463,3 +463,46 @@ def test_device_resident_batched_matches_host():
     assert np.array_equal(f_dev.cpu().numpy(), f_host)
     for j in range(b):
         assert np.array_equal(fl.dlt(c[j], cfg), f_host[j])
+
+
+@pytest.mark.parametrize("n", [64, 100, 1024, 4096])
+def test_leg2cheb_tensor_core_path(n):
+    """> 16 columns: the DMMA (fp64 mma.sync) GEMM kernel; odd N / unaligned
+    strides take the FMA-tiled kernel. Both against the oracle."""
+    rng = np.random.default_rng(n)
+    c = rng.uniform(-1, 1, (40, n))
+    f = fl.leg2cheb_apply(fl.legendre_coefficients(c)).values
+    t = fl.leg2cheb_apply_transpose(c)
+    for j in (0, 17, 39):
+        assert rel_err(f[j], O.leg2cheb(c[j]), np.abs(c[j]).sum()) <= tol_n(n)
+        assert rel_err(t[j], O.leg2cheb(c[j], True), np.abs(c[j]).sum()) <= tol_n(n)
+
+
+@pytest.mark.parametrize("n", [1 << 14, 1 << 16])
+def test_leg2cheb_single_vector_large(n):
+    c = fl.random_decaying(n, 1.0, 3)
+    f = fl.leg2cheb_apply(fl.legendre_coefficients(c)).values
+    t = fl.leg2cheb_apply_transpose(c)
+    assert rel_err(f, O.leg2cheb(c), np.abs(c).sum()) <= tol_n(n)
+    assert rel_err(t, O.leg2cheb(c, True), np.abs(c).sum()) <= tol_n(n)
+
+
+def test_leg2cheb_sampled_rows_2_20():
+    """N = 2^20 (C3 size; the O(N^2) CPU loop is minutes): sampled rows of
+    conversion.hpp:106-111 / :126-133 restated in numpy, O(N) each."""
+    n = 1 << 20
+    c = fl.random_decaying(n, 1.0, 3)
+    f = fl.leg2cheb_apply(fl.legendre_coefficients(c)).values
+    t = fl.leg2cheb_apply_transpose(c)
+    lam = O.lambda_table(n - 1)
+    s = lam / lam[0]
+    for k in (0, 1, 2, 777, n // 2, n - 2, n - 1):
+        j = np.arange((n - k + 1) // 2)
+        ref = (1.0 if k == 0 else 2.0) * np.sum(s[j] * s[k + j] * c[k + 2 * j])
+        assert abs(f[k] - ref) <= tol_n(n) * np.abs(c).sum()
+        m = k
+        j = np.arange((m + 1) // 2) if m % 2 else np.arange(m // 2)
+        reft = 2.0 * np.sum(s[j] * s[m - j] * c[m - 2 * j])
+        if m % 2 == 0:
+            reft += s[m // 2] * s[m - m // 2] * c[0]
+        assert abs(t[m] - reft) <= tol_n(n) * np.abs(c).sum()
