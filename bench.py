@@ -97,6 +97,8 @@ class Clocks:
 def make_inputs(cfg: str, n: int, col0: int, cols: int) -> np.ndarray:
     import paper_1505_00354_b200 as fl
     gen = CONFIGS[cfg][2]
+    if cols == 0:
+        return np.empty((0, n))
     if gen == "uniform":
         return fl.random_uniform_pm1(n, 4000 + col0, batch=cols).reshape(cols, n)
     decay = 0.5 if gen == "decay0.5" else 1.0
@@ -182,11 +184,11 @@ def main() -> None:
     n, total, _, desc = CONFIGS[args.config]
     if args.cols:
         total = args.cols
+    from paper_1505_00354_b200.shard import column_shard, max_over_ranks
+    col0, cols = column_shard(total, world, rank)
     per = (total + world - 1) // world
-    col0 = rank * per
-    cols = max(0, min(per, total - col0))
     stream = torch.cuda.current_stream()
-    sp = ctypes_stream = __import__("ctypes").c_void_p(stream.cuda_stream)
+    sp = __import__("ctypes").c_void_p(stream.cuda_stream)
 
     cfg = fl.TransformConfig(n)  # chebstar, tol 2^-52; plan built once, not timed
     x_host = make_inputs(args.config, n, col0, cols)
@@ -216,10 +218,7 @@ def main() -> None:
         barrier()
     launches = fl.launch_count() - l0
     ms = e0.elapsed_time(e1) / args.steps
-    t = torch.tensor([ms], device=f"cuda:{local}")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(ms, dist, f"cuda:{local}")
     value = n * total / (ms_max / 1e3)
 
     # ---- per-kernel split (same stream, CUDA events): leg2cheb GEMM vs NDCT
@@ -283,11 +282,7 @@ def main() -> None:
         e2e_step()
     e1.record(stream)
     barrier()
-    e2e_ms = e0.elapsed_time(e1) / e_steps
-    t = torch.tensor([e2e_ms], device=f"cuda:{local}")
-    if dist is not None:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    e2e_ms = float(t.item())
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1) / e_steps, dist, f"cuda:{local}")
 
     # parity spot check of this run's output against the oracle (not timed)
     if rank == 0:
