@@ -32,6 +32,7 @@
 // The same kernels with one unscaled term are the power-of-two cheb1
 // dct_iii / dst_iii / *_transpose of trig.hpp (so ndct with zero
 // perturbation stays bit-identical to dct_iii, test_ndct.cpp:112-125).
+#include <algorithm>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -44,7 +45,7 @@
 namespace flb {
 
 constexpr int kFastMinLog2 = 9;   // N = 512 (one warp per column)
-constexpr int kFastMaxLog2 = 13;  // N = 8192 (one column per CTA)
+constexpr int kFastMaxLog2 = 27;  // N <= 8192: one column per CTA; above: multi-pass (P <= 2^26)
 
 struct FastNdct {
   size_t n = 0;
@@ -455,9 +456,183 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
   }
 }
 
+// ---------------------------------------------------------------------------
+// N > 8192 (one column no longer fits a CTA): the same real-DCT packing per
+// term, with the N/2-point FFT done by the multi-pass engine (fft_pow2,
+// six-step through HBM / L2). Per term: pack kernel (reads c, applies
+// (n/N)^l by repeated squaring), FFT, unpack kernel (applies
+// sign_l (N delta_k)^l / l! and accumulates into f). Batched over columns.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ double ipow(double r, int l) {
+  double acc = 1.0;
+  while (l) {
+    if (l & 1) acc *= r;
+    r *= r;
+    l >>= 1;
+  }
+  return acc;
+}
+
+// (N delta)^l / l!, the reference's running product order (ndct.hpp:108)
+__device__ __forceinline__ double taylor_weight(double nd, int l) {
+  double p = 1.0;
+  for (int i = 1; i <= l; ++i) p *= nd / (double)i;
+  return p;
+}
+
+__global__ void big_fwd_pack_kernel(const double* __restrict__ in, size_t ld, size_t n, int l,
+                                    int odd, double2* __restrict__ Z, int* nonfinite) {
+  const size_t P = n / 2;
+  const size_t col = blockIdx.y;
+  const double* c = in + col * ld;
+  const double nd = (double)n;
+  for (size_t m = blockIdx.x * (size_t)blockDim.x + threadIdx.x; m < P;
+       m += (size_t)gridDim.x * blockDim.x) {
+    auto st = [&](size_t j) -> double { return c[j] * ipow((double)j / nd, l); };
+    auto X = [&](size_t j) -> double {
+      if (j == 0) return odd ? 0.0 : st(0);
+      if (j >= n) return 0.0;
+      return 0.5 * (odd ? st(n - j) : st(j));
+    };
+    if (nonfinite && l == 0) {
+      if (!isfinite(c[m]) || !isfinite(c[m + P])) atomicOr(nonfinite, 1);
+    }
+    double sa, ca, sb, cb, s4, c4;
+    sincospi((double)m / (2.0 * nd), &sa, &ca);        // e^{i pi m/(2N)}
+    sincospi((double)(m + P) / (2.0 * nd), &sb, &cb);  // e^{i pi (m+P)/(2N)}
+    sincospi(2.0 * (double)m / nd, &s4, &c4);          // e^{2 pi i m/N}
+    const double xa = X(m), xan = X(n - m), xb = X(m + P), xbn = X(P - m);
+    const double2 Wa = make_double2(ca * xa + sa * xan, sa * xa - ca * xan);
+    const double2 Wb = make_double2(cb * xb + sb * xbn, sb * xb - cb * xbn);
+    const double2 sm = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
+    const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
+    const double2 dr = make_double2(d.x * c4 - d.y * s4, d.x * s4 + d.y * c4);
+    Z[col * P + m] = make_double2(sm.x - dr.y, sm.y + dr.x);
+  }
+}
+
+__global__ void big_fwd_unpack_kernel(const double2* __restrict__ Z, size_t n, int l, int odd,
+                                      double sign, const double* __restrict__ delta, int plain,
+                                      double* __restrict__ out, size_t ld) {
+  const size_t P = n / 2;
+  const size_t col = blockIdx.y;
+  for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
+       k += (size_t)gridDim.x * blockDim.x) {
+    const size_t q = (k & 1) ? (n - 1 - (k >> 1)) : (k >> 1);
+    const double2 z = Z[col * P + (q >> 1)];
+    double y = (q & 1) ? z.y : z.x;
+    if (odd && (k & 1)) y = -y;
+    const double p = plain ? 1.0 : taylor_weight((double)n * delta[k], l);
+    double* o = out + col * ld + k;
+    *o = (l == 0 ? 0.0 : *o) + sign * p * y;
+  }
+}
+
+__global__ void big_tr_pack_kernel(const double* __restrict__ in, size_t ld, size_t n, int l,
+                                   int odd, const double* __restrict__ delta, int plain,
+                                   const double* __restrict__ mult, double2* __restrict__ Z,
+                                   int* nonfinite) {
+  const size_t P = n / 2;
+  const size_t col = blockIdx.y;
+  const double* g = in + col * ld;
+  auto h = [&](size_t k) -> double {
+    double v = g[k];
+    if (mult) v = mult[k] * v;
+    const double p = plain ? 1.0 : taylor_weight((double)n * delta[k], l);
+    v = p * v;
+    return (odd && (k & 1)) ? -v : v;
+  };
+  auto V = [&](size_t q) -> double { return q < P ? h(2 * q) : h(2 * (n - 1 - q) + 1); };
+  for (size_t m = blockIdx.x * (size_t)blockDim.x + threadIdx.x; m < P;
+       m += (size_t)gridDim.x * blockDim.x) {
+    if (nonfinite && l == 0) {
+      double a = g[2 * m], b = g[2 * m + 1];
+      if (mult) {
+        a *= mult[2 * m];
+        b *= mult[2 * m + 1];
+      }
+      if (!isfinite(a) || !isfinite(b)) atomicOr(nonfinite, 1);
+    }
+    Z[col * P + m] = make_double2(V(2 * m), V(2 * m + 1));
+  }
+}
+
+__global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, int l, int odd,
+                                     double sign, int plain, double* __restrict__ out, size_t ld) {
+  const size_t P = n / 2;
+  const size_t col = blockIdx.y;
+  const double nd = (double)n;
+  for (size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x; r < n;
+       r += (size_t)gridDim.x * blockDim.x) {
+    double X = 0.0;
+    const size_t kk = odd ? (n - r) : r;
+    if (!(odd && r == 0)) {
+      const size_t a = kk & (P - 1), b = (P - kk) & (P - 1);
+      const double2 za = Z[col * P + a], zc = Z[col * P + b];
+      const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
+      const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));
+      double s2, c2, sh, ch;
+      sincospi(-2.0 * (double)kk / nd, &s2, &c2);  // e^{-2 pi i kk/N}
+      sincospi((double)kk / (2.0 * nd), &sh, &ch);  // e^{i pi kk/(2N)}
+      const double2 Vv = make_double2(ev.x + od.x * c2 - od.y * s2, ev.y + od.x * s2 + od.y * c2);
+      X = ch * Vv.x + sh * Vv.y;
+    }
+    const double rp = plain ? 1.0 : ipow((double)r / nd, l);
+    double* o = out + col * ld + r;
+    *o = (l == 0 ? 0.0 : *o) + sign * rp * X;
+  }
+}
+
+void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double* out,
+                size_t ld_out, size_t batch, const double* delta, int num_terms, int plain_op,
+                const double* mult, int* nonfinite, cudaStream_t s) {
+  const size_t n = size_t(1) << log2n, P = n / 2;
+  if (ld_in != ld_out) fail(FL_RUNTIME_ERROR, "fast ndct: mismatched strides");
+  const size_t chunk_cap = std::max<size_t>(1, (size_t(1) << 30) / (2 * P * sizeof(double2)));
+  const size_t chunk = batch < chunk_cap ? batch : chunk_cap;
+  double2 *Z = nullptr, *S = nullptr;
+  FLB_CUDA(cudaMallocAsync(&Z, chunk * P * sizeof(double2), s));
+  FLB_CUDA(cudaMallocAsync(&S, chunk * P * sizeof(double2), s));
+  const int terms = plain_op < 0 ? num_terms : 1;
+  const int plain = plain_op >= 0;
+  const unsigned gx = (unsigned)std::min<size_t>((P + 255) / 256, 2048);
+  for (size_t c0 = 0; c0 < batch; c0 += chunk) {
+    const size_t nc = batch - c0 < chunk ? batch - c0 : chunk;
+    dim3 grid(gx, (unsigned)nc);
+    for (int l = 0; l < terms; ++l) {
+      const int odd = plain ? plain_op : (l & 1);
+      const double sign = plain ? 1.0 : (((l + 1) / 2) % 2 == 0 ? 1.0 : -1.0);
+      if (!transpose) {
+        big_fwd_pack_kernel<<<grid, 256, 0, s>>>(in + c0 * ld_in, ld_in, n, plain ? 0 : l, odd, Z,
+                                                 nonfinite);
+        note_launch("big_fwd_pack_kernel");
+        fft_pow2(Z, S, log2n - 1, nc, true, s);
+        big_fwd_unpack_kernel<<<grid, 256, 0, s>>>(Z, n, plain ? 0 : l, odd, sign, delta, plain,
+                                                   out + c0 * ld_out, ld_out);
+        note_launch("big_fwd_unpack_kernel");
+      } else {
+        big_tr_pack_kernel<<<grid, 256, 0, s>>>(in + c0 * ld_in, ld_in, n, plain ? 0 : l, odd,
+                                                delta, plain, mult, Z, nonfinite);
+        note_launch("big_tr_pack_kernel");
+        fft_pow2(Z, S, log2n - 1, nc, false, s);
+        big_tr_unpack_kernel<<<grid, 256, 0, s>>>(Z, n, plain ? 0 : l, odd, sign, plain,
+                                                  out + c0 * ld_out, ld_out);
+        note_launch("big_tr_unpack_kernel");
+      }
+    }
+  }
+  cudaFreeAsync(Z, s);
+  cudaFreeAsync(S, s);
+}
+
 void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* out,
               size_t ld_out, size_t batch, const double* delta, int num_terms, int plain_op,
               const double* mult, int* nonfinite, cudaStream_t s) {
+  if (log2n > 13) {
+    launch_big(log2n, transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult,
+               nonfinite, s);
+    return;
+  }
   switch (log2n) {
     case 9: launch_fast<9>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
     case 10: launch_fast<10>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;

@@ -506,3 +506,37 @@ def test_leg2cheb_sampled_rows_2_20():
         if m % 2 == 0:
             reft += s[m // 2] * s[m - m // 2] * c[0]
         assert abs(t[m] - reft) <= tol_n(n) * np.abs(c).sum()
+
+
+@pytest.mark.parametrize("n", [16384, 65536])
+def test_ndct_multipass_power_of_two(n):
+    """N > 8192: the multi-pass fast NDCT (cheb1 packing + six-step FFT)."""
+    grid = fl.legendre_nodes_weights(n)
+    c = np.random.default_rng(n).standard_normal((2, n))
+    for tol in (2.0 ** -23, 2.0 ** -52):
+        plan = fl.plan_ndct(grid, fl.GridKind.cheb1, tol)
+        delta = np.asarray(plan.reference.delta_theta)
+        f = fl.ndct_apply(plan, c)
+        t = fl.ndct_apply_transpose(plan, c)
+        for j in range(2):
+            s = np.abs(c[j]).sum()
+            assert rel_err(f[j], O.ndct(c[j], CHEB1, plan.num_terms, delta), s) <= tol_n(n)
+            assert rel_err(t[j], O.ndct(c[j], CHEB1, plan.num_terms, delta, True), s) <= tol_n(n)
+    for op, fn in enumerate((fl.dct_iii, fl.dst_iii, fl.dct_iii_transpose, fl.dst_iii_transpose)):
+        got = fn(c[0], fl.GridKind.cheb1)
+        assert rel_err(got, O.trig(op, c[0], CHEB1), np.abs(c[0]).sum()) <= tol_n(n)
+
+
+def test_dlt_idlt_2_20_sampled():
+    """C3 size (N = 2^20): fast-mode DLT against the device's direct Legendre
+    evaluation at sampled nodes (incl. both ends), IDLT round trip."""
+    n = 1 << 20
+    cfg = fl.TransformConfig(n)
+    g = cfg.grid()
+    c = fl.random_decaying(n, 1.0, 3)
+    f = fl.dlt(fl.legendre_coefficients(c), cfg)
+    idx = np.array([0, 1, 2, 1000, n // 3, n // 2, n - 2, n - 1])
+    direct = fl.eval_legendre_direct(fl.legendre_coefficients(c), g.x[idx])
+    assert np.max(np.abs(f[idx] - direct)) <= tol_n(n) * np.abs(c).sum()
+    back = fl.idlt(f, cfg).values
+    assert np.max(np.abs(back - c)) <= 1e-9 * np.max(np.abs(c))
