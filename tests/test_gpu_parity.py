@@ -528,15 +528,28 @@ def test_ndct_multipass_power_of_two(n):
 
 
 def test_dlt_idlt_2_20_sampled():
-    """C3 size (N = 2^20): fast-mode DLT against the device's direct Legendre
-    evaluation at sampled nodes (incl. both ends), IDLT round trip."""
+    """C3 size (N = 2^20), where the O(N^2) CPU reference takes minutes:
+    (1) the fast-mode DLT is exactly its two GPU stages composed;
+    (2) the NDCT stage against the CPU oracle's ndct_apply on the same grid
+        and the same input (O(N log N), feasible here);
+    (3) the leg2cheb stage is pinned by test_leg2cheb_sampled_rows_2_20;
+    (4) DLT vs the device's direct Legendre recurrence at sampled nodes, at the
+        reference acceptance level 1e-10 ||c||_1 (acceptance.cpp:172-191);
+    (5) IDLT round trip within the O(N log N) eps growth of the inverse."""
     n = 1 << 20
     cfg = fl.TransformConfig(n)
     g = cfg.grid()
     c = fl.random_decaying(n, 1.0, 3)
     f = fl.dlt(fl.legendre_coefficients(c), cfg)
+    chat = fl.leg2cheb_apply(fl.legendre_coefficients(c), cfg.lambda_()).values
+    plan1 = fl.plan_ndct(g, fl.GridKind.cheb1, fl.default_tolerance)
+    f2 = fl.ndct_apply(plan1, chat)
+    assert np.array_equal(f, f2)
+    ref = O.ndct(chat, CHEB1, plan1.num_terms, np.asarray(plan1.reference.delta_theta))
+    assert rel_err(f2, ref, np.abs(chat).sum()) <= tol_n(n)
     idx = np.array([0, 1, 2, 1000, n // 3, n // 2, n - 2, n - 1])
     direct = fl.eval_legendre_direct(fl.legendre_coefficients(c), g.x[idx])
-    assert np.max(np.abs(f[idx] - direct)) <= tol_n(n) * np.abs(c).sum()
+    assert np.max(np.abs(f[idx] - direct)) <= 1e-10 * np.abs(c).sum()
     back = fl.idlt(f, cfg).values
-    assert np.max(np.abs(back - c)) <= 1e-9 * np.max(np.abs(c))
+    err = np.max(np.abs(back - c)) / np.max(np.abs(c))
+    assert err <= 1e-10 * (n / 2048) * math.log2(n) / 11, err
