@@ -345,9 +345,13 @@ __global__ void __launch_bounds__(mv::THREADS)
     leg2cheb_mv_kernel(const double* __restrict__ s, const double* __restrict__ in,
                        double* __restrict__ out, size_t n, size_t ld, int scale_half) {
   constexpr int RB = mv::RB, TK = mv::TK, KC = mv::KC;
-  // tw[i] = s_{d}, d = (TR ? row - inner : inner - row) over the chunk window
-  __shared__ double tw[TK + KC];
-  __shared__ double hw[TK + KC];  // s_{row + inner + p}
+  // tw[i] = s_{d}, d = (TR ? row - inner : inner - row) over the chunk window;
+  // hw[i] = s_{row + inner + p}. Threads read both at a stride of RB = 8
+  // elements, so one pad slot per 8 (PX) keeps a warp's reads conflict free.
+  constexpr int PADDED = TK + KC + (TK + KC) / 8;
+  __shared__ double tw[PADDED];
+  __shared__ double hw[PADDED];
+  auto PX = [](int i) { return i + (i >> 3); };
   __shared__ double xv[KC];       // input at inner index (times pref for M^T)
   const int p = blockIdx.z;
   const size_t col = blockIdx.y;
@@ -370,9 +374,9 @@ __global__ void __launch_bounds__(mv::THREADS)
     for (int q = t; q < TK + KC; q += mv::THREADS) {
       const long long d = TR ? (long long)r0 - (long long)i0 - (KC - 1) + q
                              : (long long)i0 - (long long)r0 - (TK - 1) + q;
-      tw[q] = (d >= 0 && d < (long long)n) ? s[d] : 0.0;
+      tw[PX(q)] = (d >= 0 && d < (long long)n) ? s[d] : 0.0;
       const size_t h = r0 + i0 + p + q;  // row + inner + p, row - r0 + inner - i0 = q
-      hw[q] = h < n ? s[h] : 0.0;
+      hw[PX(q)] = h < n ? s[h] : 0.0;
     }
     for (int q = t; q < KC; q += mv::THREADS) {
       const size_t i = i0 + q;
@@ -392,8 +396,8 @@ __global__ void __launch_bounds__(mv::THREADS)
     double tv[RB], hv[RB];
 #pragma unroll
     for (int rr = 0; rr < RB; ++rr) {
-      tv[rr] = TR ? tw[lr + rr + KC - 1] : tw[TK - 1 - lr - rr];
-      hv[rr] = hw[lr + rr];
+      tv[rr] = TR ? tw[PX(lr + rr + KC - 1)] : tw[PX(TK - 1 - lr - rr)];
+      hv[rr] = hw[PX(lr + rr)];
     }
     for (int j = 0; j < KC; j += RB) {
 #pragma unroll
@@ -407,10 +411,10 @@ __global__ void __launch_bounds__(mv::THREADS)
         // directions) and row rr+1's Hankel factor; one new value each
 #pragma unroll
         for (int rr = RB - 1; rr > 0; --rr) tv[rr] = tv[rr - 1];
-        tv[0] = TR ? tw[lr + KC - 2 - jj] : tw[TK - lr + jj];
+        tv[0] = TR ? tw[PX(lr + KC - 2 - jj)] : tw[PX(TK - lr + jj)];
 #pragma unroll
         for (int rr = 0; rr + 1 < RB; ++rr) hv[rr] = hv[rr + 1];
-        hv[RB - 1] = hw[lr + RB + jj];
+        hv[RB - 1] = hw[PX(lr + RB + jj)];
       }
     }
   }
