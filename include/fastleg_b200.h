@@ -137,6 +137,18 @@ enum { FL_NDCT_LITERAL = 0, FL_NDCT_FAST = 1 };
 fl_status fl_plan_set_ndct_mode(fl_plan* plan, int mode);
 int fl_plan_ndct_mode(const fl_plan* plan);
 
+/* Legendre -> Chebyshev conversion inside dlt/idlt of plans with n >= 2^15
+ * and at most 16 columns:
+ *   0 = FL_LEG2CHEB_DIRECT : the reference's O(N^2) triangular product;
+ *   1 = FL_LEG2CHEB_FAST   : Toeplitz-Hankel factorisation, per parity
+ *       A = T .* H with H ~ sum_r l_r l_r^T (pivoted Cholesky, residual
+ *       <= 1e-17, so |error| <= 1e-17 ||c||_1), applied as K FFT-based
+ *       Toeplitz products (default).
+ * fl_plan_leg2cheb_rank returns K for a parity (0 when not built). */
+enum { FL_LEG2CHEB_DIRECT = 0, FL_LEG2CHEB_FAST = 1 };
+fl_status fl_plan_set_leg2cheb_mode(fl_plan* plan, int mode);
+int fl_plan_leg2cheb_rank(const fl_plan* plan, int parity);
+
 /* oracle.hpp:19-153 direct O(N^2) evaluations, on the device (independent of
  * the fast path: plain three-term recurrences, no FFTs).
  *   eval_legendre_direct / eval_chebyshev_direct: out[j] = sum_n c_n P_n(xs[j])

@@ -9,7 +9,8 @@ reference's header API; ``include/fastleg/*.hpp`` is the C++ one.
 """
 from ._lib import (  # noqa: F401
     DomainError, FastlegCudaError, FastlegError, InvalidArgument, OverflowErrorFL,
-    RuntimeErrorFL, device_available, launch_count, NDCT_FAST, NDCT_LITERAL,
+    RuntimeErrorFL, device_available, launch_count, NDCT_FAST, NDCT_LITERAL, LEG2CHEB_DIRECT,
+    LEG2CHEB_FAST,
 )
 from .api import *  # noqa: F401,F403
 from .api import (  # noqa: F401

@@ -17,6 +17,7 @@ FL_OK, FL_INVALID_ARGUMENT, FL_DOMAIN_ERROR, FL_OVERFLOW_ERROR, FL_RUNTIME_ERROR
 CHEB1, CHEBSTAR = 0, 1
 DCT_III, DST_III, DCT_III_T, DST_III_T = range(4)
 NDCT_LITERAL, NDCT_FAST = 0, 1
+LEG2CHEB_DIRECT, LEG2CHEB_FAST = 0, 1
 
 
 class FastlegError(Exception):
@@ -60,7 +61,7 @@ EXPORTS = [
     "fl_plan_lambda", "fl_dlt", "fl_idlt", "fl_plan_set_ndct_mode", "fl_plan_ndct_mode",
     "fl_random_decaying", "fl_random_uniform_pm1", "fl_kernel_launch_count",
     "fl_eval_legendre_direct", "fl_eval_chebyshev_direct", "fl_idlt_direct",
-    "fl_cheb_coeffs_of_legendre",
+    "fl_cheb_coeffs_of_legendre", "fl_plan_set_leg2cheb_mode", "fl_plan_leg2cheb_rank",
 ]
 
 
@@ -102,6 +103,8 @@ def _load() -> C.CDLL:
         "fl_eval_chebyshev_direct": (i, [dp, sz, dp, sz, dp, vp]),
         "fl_idlt_direct": (i, [dp, sz, dp, dp, dp, vp]),
         "fl_cheb_coeffs_of_legendre": (i, [sz, sz, dp, vp]),
+        "fl_plan_set_leg2cheb_mode": (i, [vp, i]),
+        "fl_plan_leg2cheb_rank": (i, [vp, i]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

@@ -403,6 +403,14 @@ class TransformConfig:  # transforms.hpp:19-38
     def set_ndct_mode(self, mode: int) -> None:
         check(LIB.fl_plan_set_ndct_mode(self._h, int(mode)))
 
+    def set_leg2cheb_mode(self, mode: int) -> None:
+        """LEG2CHEB_DIRECT (reference O(N^2) product) or LEG2CHEB_FAST
+        (Toeplitz-Hankel, plans with n >= 2^15, <= 16 columns)."""
+        check(LIB.fl_plan_set_leg2cheb_mode(self._h, int(mode)))
+
+    def leg2cheb_rank(self, parity: int = 0) -> int:
+        return int(LIB.fl_plan_leg2cheb_rank(self._h, int(parity)))
+
     def grid(self) -> LegendreGrid:
         if self._grid is None:
             n = self.size()

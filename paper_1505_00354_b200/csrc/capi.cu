@@ -16,6 +16,7 @@
 #include "direct.cuh"
 #include "fast_ndct.cuh"
 #include "launch.cuh"
+#include "l2c_fast.cuh"
 #include "leg2cheb.cuh"
 
 namespace flb {
@@ -305,6 +306,8 @@ struct fl_plan {
   double* lambda = nullptr;  // n  (LambdaCache(n - 1))
   double* s = nullptr;       // n  (scaled Lambda)
   FastNdct* fast = nullptr;  // cheb1-internal NDCT (power-of-two n), or null
+  L2CFast* l2c = nullptr;    // Toeplitz-Hankel leg2cheb (n >= kL2CFastMin), or null
+  int l2c_mode = 1;          // 1: fast conversion for few columns when available; 0: direct
   std::mutex mu;
 };
 
@@ -314,6 +317,7 @@ void plan_free(fl_plan* p) {
   for (double* q : {p->theta, p->x, p->w, p->tstar, p->delta, p->lambda, p->s})
     if (q) cudaFree(q);
   if (p->fast) fast_ndct_destroy(p->fast);
+  if (p->l2c) l2c_fast_destroy(p->l2c);
   delete p;
 }
 
@@ -327,6 +331,7 @@ void plan_finish(fl_plan* p) {
   launch_lambda(n - 1, p->lambda, 0);
   scaled_lambda(p->lambda, p->s, n, 0);
   p->fast = fast_ndct_create(n, p->tolerance, p->kind, p->theta);
+  if (n >= kL2CFastMin) p->l2c = l2c_fast_create(n, p->s, 0);
   FLB_CUDA(cudaDeviceSynchronize());
 }
 
@@ -482,7 +487,20 @@ fl_status fl_leg2cheb(int transpose, size_t n, const double* lambda_table, size_
     DevOut o(out, n, batch, ld, s);
     if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
     if (i.ptr == o.ptr) fail(FL_INVALID_ARGUMENT, "leg2cheb: input and output must not alias");
-    leg2cheb_direct(transpose, n, sc.p, i.ptr, o.ptr, batch, o.ld, 0, s);
+    if (n >= 4 * kL2CFastMin && batch <= kL2CFastMaxCols) {
+      // large single vectors: build the low-rank factors for this table once
+      L2CFast* f = l2c_fast_create(n, sc.p, s);
+      try {
+        l2c_fast_apply(*f, transpose, i.ptr, o.ptr, batch, o.ld, 0, s);
+      } catch (...) {
+        l2c_fast_destroy(f);
+        throw;
+      }
+      FLB_CUDA(cudaStreamSynchronize(s));
+      l2c_fast_destroy(f);
+    } else {
+      leg2cheb_direct(transpose, n, sc.p, i.ptr, o.ptr, batch, o.ld, 0, s);
+    }
     o.finish();
     sync(s);
   });
@@ -588,6 +606,19 @@ fl_status fl_plan_set_ndct_mode(fl_plan* p, int mode) {
 
 int fl_plan_ndct_mode(const fl_plan* p) { return p ? p->mode : -1; }
 
+fl_status fl_plan_set_leg2cheb_mode(fl_plan* p, int mode) {
+  return guarded([&] {
+    if (mode != FL_LEG2CHEB_DIRECT && mode != FL_LEG2CHEB_FAST)
+      fail(FL_INVALID_ARGUMENT, "plan: unknown leg2cheb mode");
+    p->l2c_mode = mode;
+  });
+}
+
+int fl_plan_leg2cheb_rank(const fl_plan* p, int parity) {
+  if (!p || !p->l2c || parity < 0 || parity > 1) return 0;
+  return l2c_fast_rank(*p->l2c, parity);
+}
+
 fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, size_t ld,
                  void* stream) {
   return guarded([&] {
@@ -602,7 +633,10 @@ fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, 
     if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
     // transforms.hpp:47-48: chat = M c (scratch), f = NDCT(chat)
     DevScratch<double> chat(n * batch, s);
-    leg2cheb_direct(0, n, p->s, i.ptr, chat.p, batch, n, 0, s);
+    if (p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)
+      l2c_fast_apply(*p->l2c, 0, i.ptr, chat.p, batch, n, 0, s);
+    else
+      leg2cheb_direct(0, n, p->s, i.ptr, chat.p, batch, n, 0, s);
     const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
     if (o.ld != n) {
       DevScratch<double> f(n * batch, s);
@@ -643,7 +677,10 @@ fl_status fl_idlt(const fl_plan* p, const double* in, double* out, size_t batch,
       run_ndct("ndct_apply_transpose", 1, p->kind, n, p->num_terms, p->delta, i.ptr, n, back.p,
                n, batch, p->w, fast, s);
     }
-    leg2cheb_direct(1, n, p->s, back.p, o.ptr, batch, o.ld, 1, s);
+    if (p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)
+      l2c_fast_apply(*p->l2c, 1, back.p, o.ptr, batch, o.ld, 1, s);
+    else
+      leg2cheb_direct(1, n, p->s, back.p, o.ptr, batch, o.ld, 1, s);
     o.finish();
     sync(s);
   });

@@ -555,3 +555,27 @@ def test_dlt_idlt_2_20_sampled():
     back = fl.idlt(f, cfg).values
     err = np.max(np.abs(back - c)) / np.max(np.abs(c))
     assert err <= 1e-10 * (n / 2048) * math.log2(n) / 11, err
+
+
+@pytest.mark.parametrize("n", [1 << 15, (1 << 16) + 3])
+def test_leg2cheb_fast_toeplitz_hankel_vs_direct(n):
+    """The Toeplitz-Hankel conversion inside dlt/idlt against the direct
+    triangular product (same plan, mode switch) and the CPU oracle."""
+    cfg = fl.TransformConfig(n)
+    k0, k1 = cfg.leg2cheb_rank(0), cfg.leg2cheb_rank(1)
+    assert 10 < k0 < 100 and 10 < k1 < 100, (k0, k1)
+    c = fl.random_decaying(n, 0.5, 11, batch=2)
+    f_fast = fl.dlt(c, cfg)
+    b_fast = fl.idlt(f_fast, cfg).values
+    cfg.set_leg2cheb_mode(fl.LEG2CHEB_DIRECT)
+    f_dir = fl.dlt(c, cfg)
+    b_dir = fl.idlt(f_fast, cfg).values
+    for j in range(2):
+        assert rel_err(f_fast[j], f_dir[j], np.abs(c[j]).sum()) <= tol_n(n)
+        assert rel_err(b_fast[j], b_dir[j], np.abs(f_fast[j]).sum()) <= tol_n(n)
+    v = c[0]
+    g = cfg.grid()
+    ref = O.leg2cheb(v)
+    lam = fl.LambdaCache(n - 1)
+    got = fl.leg2cheb_apply(fl.legendre_coefficients(v), lam).values  # free function (direct < 2^17)
+    assert rel_err(got, ref, np.abs(v).sum()) <= tol_n(n)
