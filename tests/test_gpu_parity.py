@@ -579,3 +579,31 @@ def test_leg2cheb_fast_toeplitz_hankel_vs_direct(n):
     lam = fl.LambdaCache(n - 1)
     got = fl.leg2cheb_apply(fl.legendre_coefficients(v), lam).values  # free function (direct < 2^17)
     assert rel_err(got, ref, np.abs(v).sum()) <= tol_n(n)
+
+
+def test_dlt_2_26_c5_single_gpu():
+    """C5 size, N = 2^26 (512 MiB per vector), on one GPU: fast-mode NDCT
+    (multi-pass) + Toeplitz-Hankel leg2cheb. Checked by sampled rows of the
+    reference's conversion loop (conversion.hpp:106-111, numpy O(N) per row),
+    the device's direct Legendre recurrence at sampled nodes, and the round
+    trip."""
+    n = 1 << 26
+    cfg = fl.TransformConfig(n)
+    g = cfg.grid()
+    assert np.all(np.diff(g.theta[:1000]) > 0) and g.theta[n - 1] == math.pi - g.theta[0]
+    c = fl.random_decaying(n, 0.0, 5) * np.exp(-np.arange(n) / n)  # SURVEY.md 8d C5
+    chat = fl.leg2cheb_apply(fl.legendre_coefficients(c), cfg.lambda_()).values
+    lam = cfg.lambda_().table
+    s = lam / lam[0]
+    for k in (0, 1, 12345, n // 2 + 1, n - 1):
+        j = np.arange((n - k + 1) // 2)
+        ref = (1.0 if k == 0 else 2.0) * np.sum(s[j] * s[k + j] * c[k + 2 * j])
+        assert abs(chat[k] - ref) <= tol_n(n) * np.abs(c).sum(), k
+    f = fl.dlt(fl.legendre_coefficients(c), cfg)
+    # interior nodes only: near the endpoints the direct recurrence evaluates
+    # at fl(cos theta_k), an O(eps/sin theta) different angle, and P_N' ~ N^2
+    idx = np.array([n // 8, n // 3, n // 2, 5 * n // 8])
+    direct = fl.eval_legendre_direct(fl.legendre_coefficients(c), g.x[idx])
+    assert np.max(np.abs(f[idx] - direct)) <= tol_n(n) * np.abs(c).sum()
+    back = fl.idlt(f, cfg).values
+    assert np.max(np.abs(back - c)) <= 1e-5 * np.max(np.abs(c))
