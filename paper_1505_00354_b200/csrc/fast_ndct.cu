@@ -33,9 +33,7 @@
 // dct_iii / dst_iii / *_transpose of trig.hpp (so ndct with zero
 // perturbation stays bit-identical to dct_iii, test_ndct.cpp:112-125).
 #include <algorithm>
-#include <cstdlib>
 #include <map>
-#include <string>
 #include <mutex>
 #include <tuple>
 
@@ -168,9 +166,7 @@ __device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, in
   }
 }
 
-// p[i * PSTRIDE]: the Taylor weight of the thread's i-th owned row (registers
-// when PSTRIDE == 1, the CTA-shared table when PSTRIDE == T).
-template <int LOG2N, bool ODD, int PSTRIDE = 1>
+template <int LOG2N, bool ODD>
 __device__ __forceinline__ void fwd_term(const double* stage, double2* zb, int t, int bar,
                                          double2 ta_t, double2 r4_t, const double2* fftw,
                                          const double* p, double* f, double sign) {
@@ -197,107 +193,9 @@ __device__ __forceinline__ void fwd_term(const double* stage, double2* zb, int t
         const int k = fwd_row_of<N>(2 * m + part);
         double y = part ? z.y : z.x;
         if (ODD && (k & 1)) y = -y;
-        f[i] += sign * p[i * PSTRIDE] * y;
+        f[i] += sign * p[i] * y;
       }
     }
-}
-
-// ---------------------------------------------------------------------------
-// Shared-weight variant: the Taylor weights p_k = (N delta_k)^l / l! and the
-// transpose's (n/N)^l do not depend on the column, so the COLS columns of a
-// CTA advance term by term in lockstep and read ONE weight table in shared
-// memory (stored in each thread's owned-row order, conflict free). Per thread
-// only the accumulators stay in registers (16 instead of 32 doubles), which
-// fits the 128-register budget of 512-thread CTAs without spilling.
-// ---------------------------------------------------------------------------
-template <int LOG2N>
-struct CfgS {
-  using C = Cfg<LOG2N>;
-  static constexpr int COLS = C::T >= 512 ? 1 : 512 / C::T;
-  static constexpr int THREADS = C::T * COLS;
-  static constexpr size_t COL_BYTES = C::COL_BYTES;
-  static constexpr bool SMEM_TW = COLS * COL_BYTES + C::N * 8 + C::TW * 16 <= 220 * 1024;
-  static constexpr size_t SMEM = COLS * COL_BYTES + C::N * 8 + (SMEM_TW ? C::TW * 16 : 0);
-  static constexpr int GT = COLS == 1 ? 0 : C::T;
-};
-
-template <int LOG2N>
-__global__ void __launch_bounds__(CfgS<LOG2N>::THREADS, 1)
-    fast_ndct_fwd_shw_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
-                             size_t ld_out, size_t batch, const double* __restrict__ delta,
-                             int num_terms, int plain_op, const double2* __restrict__ tw4n,
-                             const double2* __restrict__ fftw_g, int* nonfinite) {
-  using C = Cfg<LOG2N>;
-  using S = CfgS<LOG2N>;
-  constexpr int N = C::N, T = C::T, OWN = C::OWN, NSL = C::NSL, RL = C::RL;
-  extern __shared__ double smem[];
-  double* pw = smem + S::COLS * (S::COL_BYTES / 8);  // [OWN][T] weights, owned-row order
-  double2* fftw_s = reinterpret_cast<double2*>(pw + N);
-  const double2* fftw = S::SMEM_TW ? fftw_s : fftw_g;
-  for (int j = threadIdx.x; j < N; j += blockDim.x) pw[j] = 1.0;
-  if (S::SMEM_TW) load_table(fftw_s, fftw_g, C::TW);
-  const int g = threadIdx.x / T, t = threadIdx.x % T;
-  const int bar = 1 + g;
-  const size_t col = (size_t)blockIdx.x * S::COLS + g;
-  const bool active = col < batch;
-  double* stage = smem + g * (S::COL_BYTES / 8);
-  double2* zb = reinterpret_cast<double2*>(stage + N);
-  auto kown = [&](int tt, int i) -> int {
-    const int s = i >> 1, q = s / RL, r = s % RL;
-    return fwd_row_of<N>(2 * (tt + q * T + r * NSL) + (i & 1));
-  };
-  if (active) {
-    const double* src = in + col * ld_in;
-    bool bad = false;
-#pragma unroll
-    for (int i = 0; i < OWN; ++i) {
-      const int n = t + T * i;
-      const double v = src[n];
-      bad |= !isfinite(v);
-      stage[n] = v;
-    }
-    if (bad && nonfinite) atomicOr(nonfinite, 1);
-  }
-  double f[OWN];
-#pragma unroll
-  for (int i = 0; i < OWN; ++i) f[i] = 0.0;
-  const double2 ta_t = __ldg(&tw4n[t]);
-  const double2 r4_t = __ldg(&tw4n[4 * t]);
-  __syncthreads();
-  const int terms = plain_op < 0 ? num_terms : 1;
-  for (int l = 0; l < terms; ++l) {
-    if (l > 0) {
-      const double inv_l = 1.0 / (double)l;
-      if (active) {
-#pragma unroll
-        for (int i = 0; i < OWN; ++i) {
-          const int n = t + T * i;
-          stage[n] *= (double)n / (double)N;  // (n/N)^l c_n
-        }
-      }
-      for (int j = threadIdx.x; j < N; j += blockDim.x) {  // (N delta_k)^l / l!
-        const int k = kown(j % T, j / T);
-        pw[j] *= (double)N * __ldg(&delta[k]) * inv_l;
-      }
-      __syncthreads();
-    }
-    if (active) {
-      const bool odd = plain_op < 0 ? (l & 1) : (plain_op == 1);
-      const double sign = plain_op < 0 ? taylor_sign_d(l) : 1.0;
-      if (odd)
-        fwd_term<LOG2N, true, T>(stage, zb, t, bar, ta_t, r4_t, fftw, pw + t, f, sign);
-      else
-        fwd_term<LOG2N, false, T>(stage, zb, t, bar, ta_t, r4_t, fftw, pw + t, f, sign);
-    }
-    __syncthreads();  // every column is done with this term's weights and stage
-  }
-  if (!active) return;
-#pragma unroll
-  for (int i = 0; i < OWN; ++i) stage[kown(t, i)] = f[i];
-  group_sync<S::GT>(bar);
-  double* dst = out + col * ld_out;
-#pragma unroll
-  for (int i = 0; i < OWN; ++i) dst[t + T * i] = stage[t + T * i];
 }
 
 // plain_op: -1 = Taylor NDCT with num_terms terms; 0 = one plain DCT-III;
@@ -387,7 +285,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
 }
 
 // One transposed Taylor term: o[i] += sign rp[i] X_{row i}.
-template <int LOG2N, bool ODD, int PSTRIDE = 1>
+template <int LOG2N, bool ODD>
 __device__ __forceinline__ void tr_term(const double* hs, double2* zb, int t, int bar,
                                         double2 ta_t, double2 r4_t, const double2* fftw,
                                         const double* rp, double* o, double sign) {
@@ -428,80 +326,8 @@ __device__ __forceinline__ void tr_term(const double* hs, double2* zb, int t, in
       const double2 Vv = make_double2(ev.x + od.x * r.x - od.y * r.y, ev.y + od.x * r.y + od.y * r.x);
       X = h.x * Vv.x + h.y * Vv.y;  // Re(conj(h) V)
     }
-    o[i] += sign * rp[i * PSTRIDE] * X;
+    o[i] += sign * rp[i] * X;
   }
-}
-
-// Shared-weight transpose: (n/N)^l shared by the CTA's columns (lockstep).
-template <int LOG2N>
-__global__ void __launch_bounds__(CfgS<LOG2N>::THREADS, 1)
-    fast_ndct_tr_shw_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
-                            size_t ld_out, size_t batch, const double* __restrict__ delta,
-                            int num_terms, int plain_op, const double* __restrict__ mult,
-                            const double2* __restrict__ tw4n, const double2* __restrict__ fftw_g,
-                            int* nonfinite) {
-  using C = Cfg<LOG2N>;
-  using S = CfgS<LOG2N>;
-  constexpr int N = C::N, T = C::T, OWN = C::OWN;
-  extern __shared__ double smem[];
-  double* rpw = smem + S::COLS * (S::COL_BYTES / 8);  // (n/N)^l, natural order
-  double2* fftw_s = reinterpret_cast<double2*>(rpw + N);
-  const double2* fftw = S::SMEM_TW ? fftw_s : fftw_g;
-  for (int j = threadIdx.x; j < N; j += blockDim.x) rpw[j] = 1.0;
-  if (S::SMEM_TW) load_table(fftw_s, fftw_g, C::TW);
-  const int g = threadIdx.x / T, t = threadIdx.x % T;
-  const int bar = 1 + g;
-  const size_t col = (size_t)blockIdx.x * S::COLS + g;
-  const bool active = col < batch;
-  double* hs = smem + g * (S::COL_BYTES / 8);  // h_k = (N delta_k)^l / l! g_k, in place
-  double2* zb = reinterpret_cast<double2*>(hs + N);
-  if (active) {
-    const double* src = in + col * ld_in;
-    bool bad = false;
-#pragma unroll
-    for (int i = 0; i < OWN; ++i) {
-      const int k = t + T * i;
-      double v = src[k];
-      if (mult) v = mult[k] * v;  // transforms.hpp:59 weighted = w_k f_k
-      bad |= !isfinite(v);
-      hs[k] = v;
-    }
-    if (bad && nonfinite) atomicOr(nonfinite, 1);
-  }
-  double o[OWN];
-#pragma unroll
-  for (int i = 0; i < OWN; ++i) o[i] = 0.0;
-  const double2 ta_t = __ldg(&tw4n[t]);
-  const double2 r4_t = __ldg(&tw4n[4 * t]);
-  __syncthreads();
-  const int terms = plain_op < 0 ? num_terms : 1;
-  for (int l = 0; l < terms; ++l) {
-    if (l > 0) {
-      const double inv_l = 1.0 / (double)l;
-      if (active) {
-#pragma unroll
-        for (int i = 0; i < OWN; ++i) {
-          const int k = t + T * i;
-          hs[k] *= (double)N * __ldg(&delta[k]) * inv_l;
-        }
-      }
-      for (int j = threadIdx.x; j < N; j += blockDim.x) rpw[j] *= (double)j / (double)N;
-      __syncthreads();
-    }
-    if (active) {
-      const bool odd = plain_op < 0 ? (l & 1) : (plain_op == 1);
-      const double sign = plain_op < 0 ? taylor_sign_d(l) : 1.0;
-      if (odd)
-        tr_term<LOG2N, true, T>(hs, zb, t, bar, ta_t, r4_t, fftw, rpw + t, o, sign);
-      else
-        tr_term<LOG2N, false, T>(hs, zb, t, bar, ta_t, r4_t, fftw, rpw + t, o, sign);
-    }
-    __syncthreads();
-  }
-  if (!active) return;
-  double* dst = out + col * ld_out;
-#pragma unroll
-  for (int i = 0; i < OWN; ++i) dst[t + T * i] = o[i];
 }
 
 template <int LOG2N>
@@ -608,34 +434,6 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
   using C = Cfg<LOG2N>;
   const double2* tw = tw4n_table(LOG2N);
   const double2* fftw = pass_twiddles(LOG2N - 1);
-  static const bool shared_weights = [] {
-    const char* v = getenv("FLB_NDCT_VARIANT");
-    return v == nullptr || std::string(v) != "reg";
-  }();
-  if (shared_weights) {
-    using S = CfgS<LOG2N>;
-    const size_t max_c = (size_t)0x7fffffff * S::COLS;
-    for (size_t c0 = 0; c0 < batch; c0 += max_c) {
-      const size_t nc = batch - c0 < max_c ? batch - c0 : max_c;
-      const unsigned grid = (unsigned)((nc + S::COLS - 1) / S::COLS);
-      if (transpose) {
-        FLB_CUDA(cudaFuncSetAttribute(fast_ndct_tr_shw_kernel<LOG2N>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-        fast_ndct_tr_shw_kernel<LOG2N><<<grid, S::THREADS, S::SMEM, s>>>(
-            in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta, num_terms, plain_op,
-            mult, tw, fftw, nonfinite);
-        note_launch("fast_ndct_tr_shw_kernel");
-      } else {
-        FLB_CUDA(cudaFuncSetAttribute(fast_ndct_fwd_shw_kernel<LOG2N>,
-                                      cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::SMEM));
-        fast_ndct_fwd_shw_kernel<LOG2N><<<grid, S::THREADS, S::SMEM, s>>>(
-            in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta, num_terms, plain_op, tw,
-            fftw, nonfinite);
-        note_launch("fast_ndct_fwd_shw_kernel");
-      }
-    }
-    return;
-  }
   const size_t max_cols = (size_t)0x7fffffff * C::COLS;
   for (size_t c0 = 0; c0 < batch; c0 += max_cols) {
     const size_t nc = batch - c0 < max_cols ? batch - c0 : max_cols;
