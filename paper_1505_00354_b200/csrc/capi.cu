@@ -633,43 +633,6 @@ fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, 
     if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
     // transforms.hpp:47-48: chat = M c (scratch), f = NDCT(chat)
     DevScratch<double> chat(n * batch, s);
-    const FastNdct* fastp = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
-    static const bool pipeline = [] {
-      const char* v = getenv("FLB_DLT_PIPELINE");
-      return v == nullptr || v[0] != '0';
-    }();
-    if (pipeline && fastp && batch >= 4096 && o.ld == n && i.ld == n &&
-        !overflow_guard(n, p->num_terms) &&
-        !(p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)) {
-      // Column chunks in a two-stream pipeline: the conversion of chunk c+1
-      // (fp64 tensor-core GEMM) overlaps the NDCT of chunk c (FP64 FMA pipe
-      // and shared memory) instead of the two kernels running back to back.
-      const size_t nchunk = 8, chunk = (batch + nchunk - 1) / nchunk;
-      cudaStream_t s2 = nullptr;
-      FLB_CUDA(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
-      std::vector<cudaEvent_t> ev(nchunk + 1);
-      for (auto& e : ev) FLB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-      DevScratch<int> flag(1, s);
-      FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
-      size_t k = 0;
-      for (size_t c0 = 0; c0 < batch; c0 += chunk, ++k) {
-        const size_t nc = batch - c0 < chunk ? batch - c0 : chunk;
-        leg2cheb_direct(0, n, p->s, i.ptr + c0 * i.ld, chat.p + c0 * n, nc, n, 0, s);
-        FLB_CUDA(cudaEventRecord(ev[k], s));
-        FLB_CUDA(cudaStreamWaitEvent(s2, ev[k], 0));
-        fast_ndct_run(*fastp, 0, chat.p + c0 * n, n, o.ptr + c0 * n, n, nc, nullptr, flag.p, s2);
-      }
-      FLB_CUDA(cudaEventRecord(ev[nchunk], s2));
-      FLB_CUDA(cudaStreamWaitEvent(s, ev[nchunk], 0));
-      int h = 0;
-      FLB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-      o.finish();
-      sync(s);
-      for (auto& e : ev) cudaEventDestroy(e);
-      cudaStreamDestroy(s2);
-      if (h) fail(FL_INVALID_ARGUMENT, "ndct_apply: non-finite input");
-      return;
-    }
     if (p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)
       l2c_fast_apply(*p->l2c, 0, i.ptr, chat.p, batch, n, 0, s);
     else

@@ -69,9 +69,6 @@ struct Cfg {
 // 256 threads per CTA measured faster than 512 at N = 4096 (24.3 vs 27.5 ms for
 // 65536 columns, L = 17): the 255-register budget avoids the spills that the
 // 128-register one forces (tools/bench_kernels.py, profiles/).
-#ifndef FLB_NDCT_MINB  // resident CTAs per SM the register budget targets
-#define FLB_NDCT_MINB 1
-#endif
 #ifndef FLB_NDCT_CTA_THREADS
 #define FLB_NDCT_CTA_THREADS 256
 #endif
@@ -204,7 +201,7 @@ __device__ __forceinline__ void fwd_term(const double* stage, double2* zb, int t
 // plain_op: -1 = Taylor NDCT with num_terms terms; 0 = one plain DCT-III;
 // 1 = one plain DST-III.
 template <int LOG2N>
-__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FLB_NDCT_MINB)
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     fast_ndct_fwd_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                          size_t ld_out, size_t batch, const double* __restrict__ delta,
                          int num_terms, int plain_op, const double2* __restrict__ tw4n,
@@ -334,7 +331,7 @@ __device__ __forceinline__ void tr_term(const double* hs, double2* zb, int t, in
 }
 
 template <int LOG2N>
-__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FLB_NDCT_MINB)
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     fast_ndct_tr_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                         size_t ld_out, size_t batch, const double* __restrict__ delta,
                         int num_terms, int plain_op, const double* __restrict__ mult,
