@@ -186,7 +186,7 @@ constexpr int SM_A = 2 * RA * LDA;   // doubles
 constexpr int SM_B = 2 * CT * LDB;   // doubles
 constexpr int LDO = 2 * RA + 2;      // epilogue tile: [CT][2 RA] (+2 pad)
 constexpr int SM_O = CT * LDO;
-constexpr int SMEM_DOUBLES = (SM_A + SM_B) > SM_O ? (SM_A + SM_B) : SM_O;
+constexpr int SMEM_DOUBLES = 2 * (SM_A + SM_B) > SM_O ? 2 * (SM_A + SM_B) : SM_O;
 }  // namespace mma
 
 __device__ __forceinline__ void dmma884(double (&c)[2], double a, double b) {
@@ -201,10 +201,10 @@ __global__ void __launch_bounds__(mma::THREADS, 2)
                         double* __restrict__ out, size_t n, size_t cols, size_t ld,
                         int scale_half) {
   constexpr int RA = mma::RA, CT = mma::CT, KB = mma::KB, LDA = mma::LDA, LDB = mma::LDB;
-  constexpr int THREADS = mma::THREADS, SM_A = mma::SM_A, LDO = mma::LDO;
+  constexpr int THREADS = mma::THREADS, SM_A = mma::SM_A, SM_B = mma::SM_B, LDO = mma::LDO;
   extern __shared__ double sm[];
-  double* As = sm;           // [2][RA][LDA]
-  double* Bs = sm + SM_A;    // [2][KB][LDB]
+  double* As = sm;               // [stage][parity][RA][LDA]
+  double* Bs = sm + 2 * SM_A;    // [stage][parity][CT][LDB]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wp = warp & 1, wc = (warp >> 1) * 32;
   const size_t a0 = (size_t)blockIdx.x * RA;
@@ -245,16 +245,17 @@ __global__ void __launch_bounds__(mma::THREADS, 2)
       pre[i] = v;
     }
   };
-  auto store_b = [&]() {
+  auto store_b = [&](int stg) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       const int idx = tid + THREADS * i;
       const int col = idx >> 4, pr = idx & 15;
-      Bs[(0 * CT + col) * LDB + pr] = pre[i].x;
-      Bs[(1 * CT + col) * LDB + pr] = pre[i].y;
+      Bs[stg * SM_B + (0 * CT + col) * LDB + pr] = pre[i].x;
+      Bs[stg * SM_B + (1 * CT + col) * LDB + pr] = pre[i].y;
     }
   };
-  auto gen_a = [&](size_t b0) {
+  double preA[4];
+  auto calc_a = [&](size_t b0) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int idx = tid + THREADS * i;
@@ -269,19 +270,35 @@ __global__ void __launch_bounds__(mma::THREADS, 2)
           v = pref * (s[row - inner] * s[row + inner + p]);
         }
       }
-      As[(p * RA + r) * LDA + kk] = v;
+      preA[i] = v;
+    }
+  };
+  auto store_a = [&](int stg) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int idx = tid + THREADS * i;
+      const int p = idx >> 9, r = (idx >> 4) & 31, kk = idx & 15;
+      As[stg * SM_A + (p * RA + r) * LDA + kk] = preA[i];
     }
   };
 
+  // two shared-memory stages: chunk c is multiplied from stage c & 1 while
+  // chunk c+1 (prefetched into registers during the MMAs) fills the other one,
+  // so one barrier per chunk separates them
   load_b(k_begin);
+  calc_a(k_begin);
+  store_b(0);
+  store_a(0);
+  __syncthreads();
+  int stg = 0;
   for (size_t b0 = k_begin; b0 < k_end; b0 += KB) {
-    __syncthreads();  // previous chunk's smem reads are done
-    store_b();
-    gen_a(b0);
-    __syncthreads();
-    if (b0 + KB < k_end) load_b(b0 + KB);  // overlaps with the MMAs below
-    const double* Ap = As + wp * RA * LDA;
-    const double* Bp = Bs + wp * CT * LDB;
+    const bool more = b0 + KB < k_end;
+    if (more) {
+      load_b(b0 + KB);
+      calc_a(b0 + KB);
+    }
+    const double* Ap = As + stg * SM_A + wp * RA * LDA;
+    const double* Bp = Bs + stg * SM_B + wp * CT * LDB;
 #pragma unroll
     for (int ks = 0; ks < KB; ks += 4) {
       double af[4], bf[4];
@@ -294,6 +311,12 @@ __global__ void __launch_bounds__(mma::THREADS, 2)
 #pragma unroll
         for (int j = 0; j < 4; ++j) dmma884(acc[i][j], af[i], bf[j]);
     }
+    if (more) {
+      store_b(stg ^ 1);
+      store_a(stg ^ 1);
+    }
+    __syncthreads();
+    stg ^= 1;
   }
   __syncthreads();
   // epilogue: O[col][k_local], k_local = 2 a + p in [0, 64)
