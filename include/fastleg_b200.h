@@ -149,6 +149,21 @@ enum { FL_LEG2CHEB_DIRECT = 0, FL_LEG2CHEB_FAST = 1 };
 fl_status fl_plan_set_leg2cheb_mode(fl_plan* plan, int mode);
 int fl_plan_leg2cheb_rank(const fl_plan* plan, int parity);
 
+/* Term-parallel pieces of dlt / idlt (multi-GPU extension for one large
+ * vector, C5). Both stages of fl_dlt are sums of independent terms, so P
+ * ranks each take a slice and one collective sums the partials
+ * (paper_1505_00354_b200/distributed.py):
+ *   FL_STAGE_LEG2CHEB : chat = sum_{r in [lo,hi)} D(l_r) T D(l_r) c, the
+ *                       Toeplitz-Hankel rank terms of M (idlt: M^T with (m+1/2));
+ *   FL_STAGE_NDCT     : f = sum_{l in [lo,hi)} Taylor term l of the NDCT
+ *                       (idlt: the transpose, with the quadrature weights).
+ * One column; needs the fast paths (n >= 2^15 and a power of two > 8192).
+ * fl_plan_stage_terms gives the number of terms of a stage. */
+enum { FL_STAGE_LEG2CHEB = 0, FL_STAGE_NDCT = 1 };
+fl_status fl_plan_stage_terms(const fl_plan* plan, int stage, int* count);
+fl_status fl_dlt_stage(const fl_plan* plan, int inverse, int stage, int lo, int hi,
+                       const double* in, double* out, void* stream);
+
 /* oracle.hpp:19-153 direct O(N^2) evaluations, on the device (independent of
  * the fast path: plain three-term recurrences, no FFTs).
  *   eval_legendre_direct / eval_chebyshev_direct: out[j] = sum_n c_n P_n(xs[j])

@@ -62,6 +62,7 @@ EXPORTS = [
     "fl_random_decaying", "fl_random_uniform_pm1", "fl_kernel_launch_count",
     "fl_eval_legendre_direct", "fl_eval_chebyshev_direct", "fl_idlt_direct",
     "fl_cheb_coeffs_of_legendre", "fl_plan_set_leg2cheb_mode", "fl_plan_leg2cheb_rank",
+    "fl_plan_stage_terms", "fl_dlt_stage",
 ]
 
 
@@ -105,6 +106,8 @@ def _load() -> C.CDLL:
         "fl_cheb_coeffs_of_legendre": (i, [sz, sz, dp, vp]),
         "fl_plan_set_leg2cheb_mode": (i, [vp, i]),
         "fl_plan_leg2cheb_rank": (i, [vp, i]),
+        "fl_plan_stage_terms": (i, [vp, i, C.POINTER(i)]),
+        "fl_dlt_stage": (i, [vp, i, i, i, i, dp, dp, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

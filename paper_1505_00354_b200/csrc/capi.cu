@@ -1,6 +1,7 @@
 // The C ABI (include/fastleg_b200.h): argument validation in the reference's
 // order with its messages, host/device staging, per-call stream-ordered
 // scratch, and the TransformConfig-equivalent device plan.
+#include <algorithm>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -605,6 +606,54 @@ fl_status fl_plan_set_ndct_mode(fl_plan* p, int mode) {
 }
 
 int fl_plan_ndct_mode(const fl_plan* p) { return p ? p->mode : -1; }
+
+fl_status fl_plan_stage_terms(const fl_plan* p, int stage, int* count) {
+  return guarded([&] {
+    *count = 0;
+    if (stage == FL_STAGE_LEG2CHEB) {
+      if (!p->l2c) fail(FL_INVALID_ARGUMENT, "dlt_stage: no Toeplitz-Hankel conversion for this size");
+      *count = std::max(l2c_fast_rank(*p->l2c, 0), l2c_fast_rank(*p->l2c, 1));
+    } else if (stage == FL_STAGE_NDCT) {
+      if (!p->fast || p->n <= 8192)
+        fail(FL_INVALID_ARGUMENT, "dlt_stage: term-parallel NDCT needs a power-of-two N > 8192");
+      *count = fast_ndct_terms(*p->fast);
+    } else {
+      fail(FL_INVALID_ARGUMENT, "dlt_stage: unknown stage");
+    }
+  });
+}
+
+fl_status fl_dlt_stage(const fl_plan* p, int inverse, int stage, int lo, int hi, const double* in,
+                       double* out, void* stream) {
+  return guarded([&] {
+    int count = 0;
+    const fl_status st = fl_plan_stage_terms(p, stage, &count);
+    if (st != FL_OK) fail(st, fl_last_error());
+    if (lo < 0 || hi > count || lo > hi) fail(FL_INVALID_ARGUMENT, "dlt_stage: term range out of bounds");
+    const size_t n = p->n;
+    FLB_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = as_stream(stream);
+    DevIn i(in, n, 1, n, s);
+    DevOut o(out, n, 1, n, s);
+    if (lo == hi) {
+      FLB_CUDA(cudaMemsetAsync(o.ptr, 0, n * sizeof(double), s));
+    } else if (stage == FL_STAGE_LEG2CHEB) {
+      l2c_fast_apply(*p->l2c, inverse, i.ptr, o.ptr, 1, n, inverse, s, lo, hi);
+    } else {
+      DevScratch<int> flag(1, s);
+      FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+      fast_ndct_run(*p->fast, inverse, i.ptr, n, o.ptr, n, 1, inverse ? p->w : nullptr, flag.p, s,
+                    lo, hi);
+      int h = 0;
+      FLB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      sync(s);
+      if (h) fail(FL_INVALID_ARGUMENT, inverse ? "ndct_apply_transpose: non-finite input"
+                                               : "ndct_apply: non-finite input");
+    }
+    o.finish();
+    sync(s);
+  });
+}
 
 fl_status fl_plan_set_leg2cheb_mode(fl_plan* p, int mode) {
   return guarded([&] {

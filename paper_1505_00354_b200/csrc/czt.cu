@@ -252,13 +252,14 @@ static double taylor_sign(int l) { return ((l + 1) / 2) % 2 == 0 ? 1.0 : -1.0; }
 
 void czt_ndct(int transpose, int kind, size_t n, int num_terms, const double* delta,
               const double* in, double* out, size_t batch, size_t ld, const double* in_mult,
-              int* nonfinite, cudaStream_t s) {
+              int* nonfinite, cudaStream_t s, int l_lo, int l_hi) {
+  if (l_hi < 0) l_hi = num_terms;
   const CztPlan& p = czt_plan(kind, n);
   const size_t chunk = chunk_cols(p, batch);
   Scratch sc(p, chunk, s);
   for (size_t c0 = 0; c0 < batch; c0 += chunk) {
     const size_t nc = batch - c0 < chunk ? batch - c0 : chunk;
-    for (int l = 0; l < num_terms; ++l) {
+    for (int l = l_lo; l < l_hi; ++l) {
       const int imag = l % 2;
       Scale load, store;
       if (!transpose) {
@@ -270,7 +271,7 @@ void czt_ndct(int transpose, int kind, size_t n, int num_terms, const double* de
         load = Scale{2, l, 1.0, delta, in_mult};
         store = Scale{1, l, taylor_sign(l), nullptr, nullptr};
       }
-      czt_term(p, transpose, imag, in + c0 * ld, ld, out + c0 * ld, ld, nc, load, store, l > 0,
+      czt_term(p, transpose, imag, in + c0 * ld, ld, out + c0 * ld, ld, nc, load, store, l > l_lo,
                l == 0 ? nonfinite : nullptr, sc.A, sc.S, s);
     }
   }

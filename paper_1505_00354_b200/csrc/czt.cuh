@@ -14,6 +14,6 @@ void czt_trig(int op, int kind, size_t n, const double* in, double* out, size_t 
 // nonfinite (nullable): device flag set when a term-0 input is not finite.
 void czt_ndct(int transpose, int kind, size_t n, int num_terms, const double* delta,
               const double* in, double* out, size_t batch, size_t ld, const double* in_mult,
-              int* nonfinite, cudaStream_t s);
+              int* nonfinite, cudaStream_t s, int l_lo = 0, int l_hi = -1);
 
 }  // namespace flb

@@ -513,7 +513,7 @@ __global__ void big_fwd_pack_kernel(const double* __restrict__ in, size_t ld, si
 
 __global__ void big_fwd_unpack_kernel(const double2* __restrict__ Z, size_t n, int l, int odd,
                                       double sign, const double* __restrict__ delta, int plain,
-                                      double* __restrict__ out, size_t ld) {
+                                      double* __restrict__ out, size_t ld, int first) {
   const size_t P = n / 2;
   const size_t col = blockIdx.y;
   for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
@@ -524,7 +524,7 @@ __global__ void big_fwd_unpack_kernel(const double2* __restrict__ Z, size_t n, i
     if (odd && (k & 1)) y = -y;
     const double p = plain ? 1.0 : taylor_weight((double)n * delta[k], l);
     double* o = out + col * ld + k;
-    *o = (l == 0 ? 0.0 : *o) + sign * p * y;
+    *o = (first ? 0.0 : *o) + sign * p * y;
   }
 }
 
@@ -558,7 +558,8 @@ __global__ void big_tr_pack_kernel(const double* __restrict__ in, size_t ld, siz
 }
 
 __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, int l, int odd,
-                                     double sign, int plain, double* __restrict__ out, size_t ld) {
+                                     double sign, int plain, double* __restrict__ out, size_t ld,
+                                     int first) {
   const size_t P = n / 2;
   const size_t col = blockIdx.y;
   const double nd = (double)n;
@@ -579,13 +580,13 @@ __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, in
     }
     const double rp = plain ? 1.0 : ipow((double)r / nd, l);
     double* o = out + col * ld + r;
-    *o = (l == 0 ? 0.0 : *o) + sign * rp * X;
+    *o = (first ? 0.0 : *o) + sign * rp * X;
   }
 }
 
 void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double* out,
-                size_t ld_out, size_t batch, const double* delta, int num_terms, int plain_op,
-                const double* mult, int* nonfinite, cudaStream_t s) {
+                size_t ld_out, size_t batch, const double* delta, int l_lo, int l_hi,
+                int plain_op, const double* mult, int* nonfinite, cudaStream_t s) {
   const size_t n = size_t(1) << log2n, P = n / 2;
   if (ld_in != ld_out) fail(FL_RUNTIME_ERROR, "fast ndct: mismatched strides");
   const size_t chunk_cap = std::max<size_t>(1, (size_t(1) << 30) / (2 * P * sizeof(double2)));
@@ -593,30 +594,34 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
   double2 *Z = nullptr, *S = nullptr;
   FLB_CUDA(cudaMallocAsync(&Z, chunk * P * sizeof(double2), s));
   FLB_CUDA(cudaMallocAsync(&S, chunk * P * sizeof(double2), s));
-  const int terms = plain_op < 0 ? num_terms : 1;
   const int plain = plain_op >= 0;
+  if (plain) {
+    l_lo = 0;
+    l_hi = 1;
+  }
   const unsigned gx = (unsigned)std::min<size_t>((P + 255) / 256, 2048);
   for (size_t c0 = 0; c0 < batch; c0 += chunk) {
     const size_t nc = batch - c0 < chunk ? batch - c0 : chunk;
     dim3 grid(gx, (unsigned)nc);
-    for (int l = 0; l < terms; ++l) {
+    for (int l = l_lo; l < l_hi; ++l) {
+      const int first = l == l_lo;
       const int odd = plain ? plain_op : (l & 1);
       const double sign = plain ? 1.0 : (((l + 1) / 2) % 2 == 0 ? 1.0 : -1.0);
       if (!transpose) {
         big_fwd_pack_kernel<<<grid, 256, 0, s>>>(in + c0 * ld_in, ld_in, n, plain ? 0 : l, odd, Z,
-                                                 nonfinite);
+                                                 l == 0 ? nonfinite : nullptr);
         note_launch("big_fwd_pack_kernel");
         fft_pow2(Z, S, log2n - 1, nc, true, s);
         big_fwd_unpack_kernel<<<grid, 256, 0, s>>>(Z, n, plain ? 0 : l, odd, sign, delta, plain,
-                                                   out + c0 * ld_out, ld_out);
+                                                   out + c0 * ld_out, ld_out, first);
         note_launch("big_fwd_unpack_kernel");
       } else {
         big_tr_pack_kernel<<<grid, 256, 0, s>>>(in + c0 * ld_in, ld_in, n, plain ? 0 : l, odd,
-                                                delta, plain, mult, Z, nonfinite);
+                                                delta, plain, mult, Z, l == 0 ? nonfinite : nullptr);
         note_launch("big_tr_pack_kernel");
         fft_pow2(Z, S, log2n - 1, nc, false, s);
         big_tr_unpack_kernel<<<grid, 256, 0, s>>>(Z, n, plain ? 0 : l, odd, sign, plain,
-                                                  out + c0 * ld_out, ld_out);
+                                                  out + c0 * ld_out, ld_out, first);
         note_launch("big_tr_unpack_kernel");
       }
     }
@@ -627,12 +632,15 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
 
 void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* out,
               size_t ld_out, size_t batch, const double* delta, int num_terms, int plain_op,
-              const double* mult, int* nonfinite, cudaStream_t s) {
+              const double* mult, int* nonfinite, cudaStream_t s, int l_lo = 0, int l_hi = -1) {
+  if (l_hi < 0) l_hi = num_terms;
   if (log2n > 13) {
-    launch_big(log2n, transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult,
+    launch_big(log2n, transpose, in, ld_in, out, ld_out, batch, delta, l_lo, l_hi, plain_op, mult,
                nonfinite, s);
     return;
   }
+  if (plain_op < 0 && (l_lo != 0 || l_hi != num_terms))
+    fail(FL_INVALID_ARGUMENT, "ndct: term subsets need N > 8192 (multi-pass path)");
   switch (log2n) {
     case 9: launch_fast<9>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
     case 10: launch_fast<10>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
@@ -711,9 +719,13 @@ void fast_ndct_destroy(FastNdct* p) {
 
 void fast_ndct_run(const FastNdct& p, int transpose, const double* in, size_t ld_in, double* out,
                    size_t ld_out, size_t batch, const double* in_mult, int* nonfinite,
-                   cudaStream_t s) {
+                   cudaStream_t s, int l_lo, int l_hi) {
   dispatch(p.log2n, transpose, in, ld_in, out, ld_out, batch, p.delta, p.num_terms, -1, in_mult,
-           nonfinite, s);
+           nonfinite, s, l_lo, l_hi);
 }
 
+}  // namespace flb
+
+namespace flb {
+int fast_ndct_terms(const FastNdct& p) { return p.num_terms; }
 }  // namespace flb

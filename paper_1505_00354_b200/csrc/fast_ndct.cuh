@@ -32,8 +32,11 @@ struct FastNdctHolder {
 
 // forward: out = NDCT(in); transpose: out = NDCT^T(in_mult . in).
 // nonfinite: device flag, set when a (weighted) input is not finite.
+// Terms [l_lo, l_hi) only (l_hi < 0: all): a partial Taylor sum, used by the
+// term-parallel multi-GPU DLT (only for N > 8192, the multi-pass path).
 void fast_ndct_run(const FastNdct& p, int transpose, const double* in, size_t ld_in, double* out,
                    size_t ld_out, size_t batch, const double* in_mult, int* nonfinite,
-                   cudaStream_t s);
+                   cudaStream_t s, int l_lo = 0, int l_hi = -1);
+int fast_ndct_terms(const FastNdct& p);
 
 }  // namespace flb

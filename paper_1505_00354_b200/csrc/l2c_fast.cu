@@ -280,18 +280,21 @@ void l2c_fast_destroy(L2CFast* f) {
 int l2c_fast_rank(const L2CFast& f, int parity) { return f.K[parity]; }
 
 void l2c_fast_apply(const L2CFast& f, int transpose, const double* in, double* out, size_t cols,
-                    size_t ld, int scale_half, cudaStream_t st) {
+                    size_t ld, int scale_half, cudaStream_t st, int r_lo, int r_hi) {
   const size_t n = f.n;
   for (int p = 0; p < 2; ++p) {
     const size_t np = f.np[p];
     if (np == 0) continue;
     const int lg = f.log2L[p];
     const size_t L = size_t(1) << lg;
-    const int K = f.K[p];
-    const int pairs_total = (K + 1) / 2;
+    // rank terms [r_lo, r_hi) of this parity (a partial sum for the
+    // rank-parallel multi-GPU path; all of them by default)
+    const int K = r_hi < 0 ? f.K[p] : std::min(r_hi, f.K[p]);
+    const int r_first = std::min(std::max(r_lo, 0), K);
+    const int pairs_total = (K - r_first + 1) / 2;
     // rank pairs per batched FFT, bounded to ~2 GiB of work buffers
     const size_t cap = std::max<size_t>(1, (size_t(1) << 31) / (2 * L * sizeof(double2)));
-    const int chunk = (int)std::min<size_t>(cap, (size_t)pairs_total);
+    const int chunk = (int)std::max<size_t>(1, std::min<size_t>(cap, (size_t)pairs_total));
     double2 *V = nullptr, *S = nullptr;
     double* y = nullptr;
     FLB_CUDA(cudaMallocAsync(&V, (size_t)chunk * L * sizeof(double2), st));
@@ -299,18 +302,20 @@ void l2c_fast_apply(const L2CFast& f, int transpose, const double* in, double* o
     FLB_CUDA(cudaMallocAsync(&y, np * sizeof(double), st));
     for (size_t c = 0; c < cols; ++c) {
       const double* x = in + c * ld;
+      if (pairs_total == 0) FLB_CUDA(cudaMemsetAsync(y, 0, np * sizeof(double), st));
       for (int q0 = 0; q0 < pairs_total; q0 += chunk) {
         const int pq = std::min(chunk, pairs_total - q0);
         dim3 g(grid1(L), (unsigned)pq);
-        th_pack_kernel<<<g, 256, 0, st>>>(x, p, n, np, L, f.ell[p], K, 2 * q0, pq, transpose, V);
+        th_pack_kernel<<<g, 256, 0, st>>>(x, p, n, np, L, f.ell[p], K, r_first + 2 * q0, pq,
+                                           transpose, V);
         note_launch("th_pack_kernel");
         fft_pow2(V, S, lg, pq, false, st);
         th_mul_kernel<<<grid1((size_t)pq * L), 256, 0, st>>>(V, f.shat[p], L, (size_t)pq * L,
                                                               transpose);
         note_launch("th_mul_kernel");
         fft_pow2(V, S, lg, pq, true, st);
-        th_accum_kernel<<<grid1(np), 256, 0, st>>>(V, np, L, f.ell[p], K, 2 * q0, pq, y,
-                                                    q0 == 0);
+        th_accum_kernel<<<grid1(np), 256, 0, st>>>(V, np, L, f.ell[p], K, r_first + 2 * q0, pq,
+                                                    y, q0 == 0);
         note_launch("th_accum_kernel");
       }
       th_store_kernel<<<grid1(np), 256, 0, st>>>(y, p, n, np, transpose, scale_half,

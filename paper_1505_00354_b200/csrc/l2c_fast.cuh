@@ -15,8 +15,10 @@ int l2c_fast_rank(const L2CFast& f, int parity);
 
 // out = M in (transpose 0) or M^T in (1, optional (m + 1/2) scaling); columns
 // of stride ld; in and out must not alias.
+// r_lo/r_hi: only the rank terms [r_lo, r_hi) of each parity (a partial
+// sum; the rank-parallel multi-GPU DLT splits them over ranks).
 void l2c_fast_apply(const L2CFast& f, int transpose, const double* in, double* out, size_t cols,
-                    size_t ld, int scale_half, cudaStream_t st);
+                    size_t ld, int scale_half, cudaStream_t st, int r_lo = 0, int r_hi = -1);
 
 // Size from which the fast conversion replaces the direct one for few columns.
 constexpr size_t kL2CFastMin = size_t(1) << 15;
