@@ -38,7 +38,60 @@ CONFIGS = {
     "c4": (4096, 65536, "uniform", "C4 batched DLT N=4096 x 65536 cols, U[-1,1)"),
     "c1": (1024, 1, "decay0.5", "C1 DLT N=1024, c_n = g_n/(n+1)^0.5"),
     "c3": (1 << 20, 1, "decay1", "C3 DLT N=2^20, c_n = g_n/(n+1)"),
+    "c5": (1 << 26, 1, "c5", "C5 DLT N=2^26 (512 MiB), c_n = g_n e^{-n/N}, term-parallel over ranks"),
 }
+
+
+def run_c5(args, rank: int, world: int, local: int) -> None:
+    """C5: one 2^26 DLT, its Taylor terms and Toeplitz-Hankel rank terms split
+    over the ranks, partial sums combined by NCCL all-reduce / reduce-scatter
+    (paper_1505_00354_b200/distributed.py). Fixed N: strong scaling."""
+    import torch
+    import paper_1505_00354_b200 as fl
+    from paper_1505_00354_b200 import distributed as D
+    from paper_1505_00354_b200.shard import max_over_ranks
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    n = CONFIGS["c5"][0]
+    cfg = fl.TransformConfig(n)
+    c = fl.random_decaying(n, 0.0, 5) * np.exp(-np.arange(n) / n)
+    x = torch.from_numpy(c).cuda()
+
+    def barrier():
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(max(args.warmup, 3)):
+        D.dlt(cfg, x, dist, scatter=True)
+    barrier()
+    l0 = fl.launch_count()
+    s = torch.cuda.current_stream()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        barrier()
+        e0.record(s)
+        for _ in range(args.steps):
+            D.dlt(cfg, x, dist, scatter=True)
+        e1.record(s)
+        barrier()
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, f"cuda:{local}")
+    if rank == 0:
+        print(json.dumps({
+            "metric": "fp64 DLT coeffs/sec", "value": n / (ms / 1e3), "unit": "coeffs/s",
+            "n_gpus": world, "steps": args.steps, "warmup": max(args.warmup, 3), "ms_per_step": ms,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": CONFIGS["c5"][3], "N": n, "parallelism": f"term-parallel x{world}",
+                       "leg2cheb_rank": [cfg.leg2cheb_rank(0), cfg.leg2cheb_rank(1)],
+                       "l2": "512 MiB vectors > L2"},
+            "gpu_launches": fl.launch_count() - l0, "clocks": clk.summary()}))
+    if dist is not None:
+        dist.barrier()
+        dist.destroy_process_group()
 
 
 def parse():
@@ -170,6 +223,9 @@ def main() -> None:
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if args.impl == "reference":
         run_reference(args, rank, world)
+        return
+    if args.config == "c5":
+        run_c5(args, rank, world, local)
         return
 
     import torch
