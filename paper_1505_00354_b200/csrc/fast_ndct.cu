@@ -79,8 +79,20 @@ struct Cfg {
   static constexpr int RL = P / NSL;
   static constexpr size_t COL_BYTES = N * sizeof(double) + smem_row(P) * sizeof(double2);
   // tables in shared memory when they fit beside the columns
-  static constexpr bool SMEM_TABLES = COLS * COL_BYTES + N * 8 + TW * 16 <= 220 * 1024;
-  static constexpr size_t SMEM = COLS * COL_BYTES + (SMEM_TABLES ? N * 8 + TW * 16 : 0);
+#ifndef FLB_NDCT_PSMEM
+#define FLB_NDCT_PSMEM 0
+#endif
+  // PSM: the per-row Taylor weights live in (thread-private) shared memory
+  // instead of registers, so two CTAs fit one SM's register file (128 regs)
+  // and their barrier-separated smem / FP64 phases can overlap. Measured
+  // slower at N = 4096 (25.3 / 33.8 ms vs 24.3 / 26.6 ms fwd / transpose:
+  // the 128-register cap still spills), so it is off by default.
+  static constexpr bool PSM = FLB_NDCT_PSMEM != 0;
+  static constexpr bool SMEM_TABLES =
+      !PSM && COLS * COL_BYTES + N * 8 + TW * 16 <= 220 * 1024;
+  static constexpr size_t SMEM =
+      COLS * COL_BYTES + (PSM ? COLS * N * 8 : 0) + (SMEM_TABLES ? N * 8 + TW * 16 : 0);
+  static constexpr int MINB = PSM ? 2 : 1;
   static constexpr int GT = COLS == 1 ? 0 : T;    // group barrier width (0 = whole CTA)
 };
 
@@ -166,7 +178,9 @@ __device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, in
   }
 }
 
-template <int LOG2N, bool ODD>
+// p[i * PSTRIDE]: the Taylor weight of the thread's i-th owned row (registers
+// when PSTRIDE == 1, shared memory in owned-row order when PSTRIDE == T).
+template <int LOG2N, bool ODD, int PSTRIDE = 1>
 __device__ __forceinline__ void fwd_term(const double* stage, double2* zb, int t, int bar,
                                          double2 ta_t, double2 r4_t, const double2* fftw,
                                          const double* p, double* f, double sign) {
@@ -193,7 +207,7 @@ __device__ __forceinline__ void fwd_term(const double* stage, double2* zb, int t
         const int k = fwd_row_of<N>(2 * m + part);
         double y = part ? z.y : z.x;
         if (ODD && (k & 1)) y = -y;
-        f[i] += sign * p[i] * y;
+        f[i] += sign * p[i * PSTRIDE] * y;
       }
     }
 }
@@ -201,7 +215,7 @@ __device__ __forceinline__ void fwd_term(const double* stage, double2* zb, int t
 // plain_op: -1 = Taylor NDCT with num_terms terms; 0 = one plain DCT-III;
 // 1 = one plain DST-III.
 template <int LOG2N>
-__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, Cfg<LOG2N>::MINB)
     fast_ndct_fwd_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                          size_t ld_out, size_t batch, const double* __restrict__ delta,
                          int num_terms, int plain_op, const double2* __restrict__ tw4n,
@@ -212,9 +226,17 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   double* nd = smem + C::COLS * (C::COL_BYTES / 8);
   double2* fftw_s = reinterpret_cast<double2*>(nd + N);
   const double2* fftw = C::SMEM_TABLES ? fftw_s : fftw_g;
+  // the rows thread t accumulates: the outputs of its last-pass butterflies
+  auto own_row = [](int t, int i) -> int {
+    const int s = i >> 1, q = s / RL, r = s % RL;
+    return fwd_row_of<N>(2 * (t + q * T + r * NSL) + (i & 1));
+  };
   if (C::SMEM_TABLES) {
+    // N delta in owned-row order, nd[i T + t] for row own_row(t, i): the
+    // per-term weight update reads it conflict-free (row order is stride 4)
     if (plain_op < 0)
-      for (int i = threadIdx.x; i < N; i += blockDim.x) nd[i] = (double)N * delta[i];
+      for (int j = threadIdx.x; j < N; j += blockDim.x)
+        nd[j] = (double)N * delta[own_row(j % T, j / T)];
     load_table(fftw_s, fftw_g, C::TW);
     __syncthreads();
   }
@@ -234,16 +256,15 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     stage[n] = v;
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
-  // the rows this thread accumulates: the outputs of its last-pass butterflies
-  auto kown = [&](int i) -> int {
-    const int s = i >> 1, q = s / RL, r = s % RL;
-    return fwd_row_of<N>(2 * (t + q * T + r * NSL) + (i & 1));
-  };
-  double f[OWN], p[OWN];
+  auto kown = [&](int i) -> int { return own_row(t, i); };
+  constexpr int PS = C::PSM ? T : 1;
+  double f[OWN], preg[C::PSM ? 1 : OWN];
+  // PSM: thread-private weights in smem, entry i of thread t at [i T + t]
+  double* p = C::PSM ? smem + C::COLS * (C::COL_BYTES / 8) + g * N + t : preg;
 #pragma unroll
   for (int i = 0; i < OWN; ++i) {
     f[i] = 0.0;
-    p[i] = 1.0;
+    p[i * PS] = 1.0;
   }
   // per-thread pack twiddle bases e^{i pi t/(2N)}, e^{2 pi i t/N} (table of 4N-th roots)
   const double2 ta_t = __ldg(&tw4n[t]);
@@ -251,9 +272,9 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      fwd_term<LOG2N, true>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      fwd_term<LOG2N, true, PS>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
     else
-      fwd_term<LOG2N, false>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      fwd_term<LOG2N, false, PS>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
   } else {
     for (int l = 0; l < num_terms; ++l) {
       if (l > 0) {
@@ -262,16 +283,15 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
         for (int i = 0; i < OWN; ++i) {
           const int n = t + T * i;
           stage[n] *= (double)n / (double)N;  // (n/N)^l c_n
-          const int k = kown(i);
-          const double q = C::SMEM_TABLES ? nd[k] : (double)N * __ldg(&delta[k]);
-          p[i] *= q * inv_l;                   // (N delta_k)^l / l!
+          const double q = C::SMEM_TABLES ? nd[i * T + t] : (double)N * __ldg(&delta[kown(i)]);
+          p[i * PS] *= q * inv_l;              // (N delta_k)^l / l!
         }
         group_sync<C::GT>(bar);
       }
       if (l & 1)
-        fwd_term<LOG2N, true>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, taylor_sign_d(l));
+        fwd_term<LOG2N, true, PS>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, taylor_sign_d(l));
       else
-        fwd_term<LOG2N, false>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, taylor_sign_d(l));
+        fwd_term<LOG2N, false, PS>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, taylor_sign_d(l));
     }
   }
   // scatter the owned rows through shared memory, then one coalesced store
@@ -284,54 +304,103 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   for (int i = 0; i < OWN; ++i) dst[t + T * i] = stage[t + T * i];
 }
 
-// One transposed Taylor term: o[i] += sign rp[i] X_{row i}.
-template <int LOG2N, bool ODD>
+// Layout of the transposed stage h in shared memory: even entries first,
+// hs[q] = h_{2q}, hs[P + q] = h_{2q+1}, so the pack below reads contiguous
+// pairs (row order would be a stride-4, 4-way bank-conflicted read).
+template <int N>
+__device__ __forceinline__ int tr_slot(int k) { return (k & 1) ? N / 2 + (k >> 1) : k >> 1; }
+template <int N>
+__device__ __forceinline__ int tr_entry(int j) { return j < N / 2 ? 2 * j : 2 * (j - N / 2) + 1; }
+
+// Output rows of the transpose owned by thread t: i = 4 g + u, a = t + g T,
+// rows {a, P - a, P + a, N - a} all unpack from the same pair (Z_a, Z_{P-a}),
+// so every Z is read once. a = 0 pairs rows {0, P} (Z_0) with {P/2, 3P/2}
+// (Z_{P/2}), i.e. u = 1, 3 use a1 = P/2.
+template <int N>
+__device__ __forceinline__ int tr_row(int t, int i) {
+  constexpr int P = N / 2, T = N / 16;
+  const int u = i & 3, a = t + (i >> 2) * T, a1 = a ? a : P / 2;
+  return u == 0 ? a : u == 1 ? P - a1 : u == 2 ? P + a : N - a1;
+}
+
+// X_kk of DCT-II row kk from V = (Za + conj Zb)/2 + e^{-2 pi i kk/N} (Za - conj Zb)/(2i),
+// X = Re(conj(h) V), h = e^{i pi kk/(2N)}; tn = e^{i pi n/(2N)}, rn = e^{2 pi i n/N}
+// of the output row n (kk = n, or N - n for the DST^T of odd terms).
+template <bool ODD>
+__device__ __forceinline__ double tr_unpack(double2 za, double2 zc, double2 tn, double2 rn) {
+  const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
+  const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));
+  const double2 r = ODD ? rn : make_double2(rn.x, -rn.y);
+  const double2 h = ODD ? make_double2(tn.y, tn.x) : tn;
+  const double2 Vv = make_double2(ev.x + od.x * r.x - od.y * r.y, ev.y + od.x * r.y + od.y * r.x);
+  return h.x * Vv.x + h.y * Vv.y;
+}
+
+// One transposed Taylor term: o[i] += sign rp[i] X_{tr_row(t, i)}.
+template <int LOG2N, bool ODD, int PSTRIDE = 1>
 __device__ __forceinline__ void tr_term(const double* hs, double2* zb, int t, int bar,
                                         double2 ta_t, double2 r4_t, const double2* fftw,
                                         const double* rp, double* o, double sign) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, OWN = C::OWN;
+  static_assert(E == 8 && T == N / 16, "row grouping assumes T = N/16");
   // pack v_q = h_{2q} (q < P), v_{N-1-q} = h_{2q+1}; z_m = v_{2m} + i v_{2m+1};
-  // odd terms (DST^T) use (-1)^k h_k, i.e. negate the odd-index entries
-  auto V = [&](int q) -> double { return q < P ? hs[2 * q] : (ODD ? -1.0 : 1.0) * hs[2 * (N - 1 - q) + 1]; };
+  // odd terms (DST^T) use (-1)^k h_k, i.e. negate the odd-index entries.
+  // m < N/4: (h_{4m}, h_{4m+2}) = hs[2m .. 2m+1]; else (h_{2(N-1-2m)+1}, h_{2(N-2-2m)+1})
+  // = the swapped pair at hs[P + N - 2 - 2m].
   double2 v[E];
 #pragma unroll
   for (int r = 0; r < E; ++r) {
     const int m = t + r * T;
-    v[r] = make_double2(V(2 * m), V(2 * m + 1));
+    if (r < 4) {
+      v[r] = *reinterpret_cast<const double2*>(hs + 2 * m);
+    } else {
+      const double2 w = *reinterpret_cast<const double2*>(hs + P + N - 2 - 2 * m);
+      v[r] = ODD ? make_double2(-w.y, -w.x) : make_double2(w.y, w.x);
+    }
   }
   pass_compute<P, E, 8, 1, false>(v, t, fftw);
   pass_store<P, E, 8, 1>(v, zb, t);
   group_sync<C::GT>(bar);
   mid_passes<P, E, 8, P, false, C::GT>(zb, t, fftw, bar);
+  constexpr double h = 0.70710678118654752440;
 #pragma unroll
-  for (int i = 0; i < OWN; ++i) {
-    const int n = t + T * i;
-    double X = 0.0;
-    const int kk = ODD ? (N - n) : n;  // DST^T row n is DCT-II row N - n
-    if (!(ODD && n == 0)) {
-      const int a = kk & (P - 1), b = (P - kk) & (P - 1);
-      const double2 za = zb[smem_pad(a)], zc = zb[smem_pad(b)];
-      // V = (Za + conj Zb)/2 + e^{-2 pi i kk/N} (Za - conj Zb)/(2i)
-      const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
-      const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));
-      // n = t + i T: e^{i pi n/(2N)} = ta_t c32[i], e^{2 pi i n/N} = r4_t c8[i]
-      const double a32x = kC32[i][0], a32y = kC32[i][1];
-      const double a8x = kC8[i][0], a8y = kC8[i][1];
-      const double2 tn = make_double2(ta_t.x * a32x - ta_t.y * a32y, ta_t.x * a32y + ta_t.y * a32x);
-      const double2 rn = make_double2(r4_t.x * a8x - r4_t.y * a8y, r4_t.x * a8y + r4_t.y * a8x);
-      // r = e^{-2 pi i kk/N}, h = e^{i pi kk/(2N)} for kk = n (DCT) or N - n (DST)
-      const double2 r = ODD ? rn : make_double2(rn.x, -rn.y);
-      const double2 h = ODD ? make_double2(tn.y, tn.x) : tn;
-      const double2 Vv = make_double2(ev.x + od.x * r.x - od.y * r.y, ev.y + od.x * r.y + od.y * r.x);
-      X = h.x * Vv.x + h.y * Vv.y;  // Re(conj(h) V)
+  for (int g = 0; g < OWN / 4; ++g) {
+    const int a = t + g * T;
+    // A = e^{i pi a/(2N)} = ta_t c32[g], R = e^{2 pi i a/N} = r4_t c8[g]
+    const double2 A = make_double2(ta_t.x * kC32[g][0] - ta_t.y * kC32[g][1],
+                                   ta_t.x * kC32[g][1] + ta_t.y * kC32[g][0]);
+    const double2 R = make_double2(r4_t.x * kC8[g][0] - r4_t.y * kC8[g][1],
+                                   r4_t.x * kC8[g][1] + r4_t.y * kC8[g][0]);
+    const double2 zA = zb[smem_pad(a)], zB = zb[smem_pad((P - a) & (P - 1))];
+    double2 A1 = A, R1 = R, zA1 = zA, zB1 = zB;
+    if (a == 0) {  // rows P/2, 3P/2: a1 = P/2
+      A1 = make_double2(kC32[4][0], kC32[4][1]);  // e^{i pi/8}
+      R1 = make_double2(0.0, 1.0);
+      zA1 = zB1 = zb[smem_pad(P / 2)];
     }
-    o[i] += sign * rp[i] * X;
+    // e^{i pi n/(2N)}, e^{2 pi i n/N} of the four rows, by symmetry from A, R
+    const double2 t0 = A, r0 = R;                                                      // n = a
+    const double2 t1 = make_double2(h * (A1.x + A1.y), h * (A1.x - A1.y));             // P - a1
+    const double2 r1 = make_double2(-R1.x, R1.y);
+    const double2 t2 = make_double2(h * (A.x - A.y), h * (A.x + A.y));                 // P + a
+    const double2 r2 = make_double2(-R.x, -R.y);
+    const double2 t3 = make_double2(A1.y, A1.x);                                       // N - a1
+    const double2 r3 = make_double2(R1.x, -R1.y);
+    // (Z_{kk mod P}, Z_{(P - kk) mod P}) of each row; the DST^T (kk = N - n) swaps them
+    const double x0 = ODD ? (a == 0 ? 0.0 : tr_unpack<true>(zB, zA, t0, r0)) : tr_unpack<false>(zA, zB, t0, r0);
+    const double x1 = ODD ? tr_unpack<true>(zA1, zB1, t1, r1) : tr_unpack<false>(zB1, zA1, t1, r1);
+    const double x2 = ODD ? tr_unpack<true>(zB, zA, t2, r2) : tr_unpack<false>(zA, zB, t2, r2);
+    const double x3 = ODD ? tr_unpack<true>(zA1, zB1, t3, r3) : tr_unpack<false>(zB1, zA1, t3, r3);
+    o[4 * g + 0] += sign * rp[(4 * g + 0) * PSTRIDE] * x0;
+    o[4 * g + 1] += sign * rp[(4 * g + 1) * PSTRIDE] * x1;
+    o[4 * g + 2] += sign * rp[(4 * g + 2) * PSTRIDE] * x2;
+    o[4 * g + 3] += sign * rp[(4 * g + 3) * PSTRIDE] * x3;
   }
 }
 
 template <int LOG2N>
-__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, Cfg<LOG2N>::MINB)
     fast_ndct_tr_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                         size_t ld_out, size_t batch, const double* __restrict__ delta,
                         int num_terms, int plain_op, const double* __restrict__ mult,
@@ -344,8 +413,8 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   double2* fftw_s = reinterpret_cast<double2*>(nd + N);
   const double2* fftw = C::SMEM_TABLES ? fftw_s : fftw_g;
   if (C::SMEM_TABLES) {
-    if (plain_op < 0)
-      for (int i = threadIdx.x; i < N; i += blockDim.x) nd[i] = (double)N * delta[i];
+    if (plain_op < 0)  // in the tr_slot layout of the stage
+      for (int j = threadIdx.x; j < N; j += blockDim.x) nd[j] = (double)N * delta[tr_entry<N>(j)];
     load_table(fftw_s, fftw_g, C::TW);
     __syncthreads();
   }
@@ -353,10 +422,13 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   const int bar = 1 + g;
   const size_t col = (size_t)blockIdx.x * C::COLS + g;
   if (col >= batch) return;
-  double* hs = smem + g * (C::COL_BYTES / 8);  // h_k = (N delta_k)^l / l! g_k, in place
+  // h_k = (N delta_k)^l / l! g_k, in place, at hs[tr_slot(k)]
+  double* hs = smem + g * (C::COL_BYTES / 8);
   double2* zb = reinterpret_cast<double2*>(hs + N);
   const double* src = in + col * ld_in;
-  double o[OWN], rp[OWN];
+  constexpr int PS = C::PSM ? T : 1;
+  double o[OWN], rpreg[C::PSM ? 1 : OWN];
+  double* rp = C::PSM ? smem + C::COLS * (C::COL_BYTES / 8) + g * N + t : rpreg;
   bool bad = false;
 #pragma unroll
   for (int i = 0; i < OWN; ++i) {
@@ -364,9 +436,9 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     double v = src[k];
     if (mult) v = mult[k] * v;  // transforms.hpp:59 weighted = w_k f_k
     bad |= !isfinite(v);
-    hs[k] = v;
+    hs[tr_slot<N>(k)] = v;
     o[i] = 0.0;
-    rp[i] = 1.0;
+    rp[i * PS] = 1.0;
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
   const double2 ta_t = __ldg(&tw4n[t]);      // e^{i pi t/(2N)}
@@ -374,9 +446,9 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      tr_term<LOG2N, true>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
+      tr_term<LOG2N, true, PS>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
     else
-      tr_term<LOG2N, false>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
+      tr_term<LOG2N, false, PS>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
   } else {
     for (int l = 0; l < num_terms; ++l) {
       if (l > 0) {
@@ -384,22 +456,22 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
         group_sync<C::GT>(bar);  // the previous term's reads of zb and hs are done
 #pragma unroll
         for (int i = 0; i < OWN; ++i) {
-          const int k = t + T * i;
-          const double q = C::SMEM_TABLES ? nd[k] : (double)N * __ldg(&delta[k]);
-          hs[k] *= q * inv_l;
-          rp[i] *= (double)k / (double)N;  // (n/N)^l for output row n = k
+          const int j = t + T * i;  // slot j holds h_{tr_entry(j)}
+          const double q = C::SMEM_TABLES ? nd[j] : (double)N * __ldg(&delta[tr_entry<N>(j)]);
+          hs[j] *= q * inv_l;
+          rp[i * PS] *= (double)tr_row<N>(t, i) / (double)N;  // (n/N)^l for output row n
         }
         group_sync<C::GT>(bar);
       }
       if (l & 1)
-        tr_term<LOG2N, true>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
+        tr_term<LOG2N, true, PS>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
       else
-        tr_term<LOG2N, false>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
+        tr_term<LOG2N, false, PS>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
     }
   }
   double* dst = out + col * ld_out;
 #pragma unroll
-  for (int i = 0; i < OWN; ++i) dst[t + T * i] = o[i];
+  for (int i = 0; i < OWN; ++i) dst[tr_row<N>(t, i)] = o[i];
 }
 
 __global__ void tw4n_kernel(double2* tw, unsigned long long n) {
