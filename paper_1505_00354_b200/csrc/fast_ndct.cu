@@ -24,10 +24,13 @@
 // weights are applied without another shared-memory round trip. The term
 // parity (DCT/DST) is a template parameter.
 //
-// CTA layout: 512 threads = COLS groups of T = N/16 threads, one column per
+// CTA layout: 256 threads = COLS groups of T = N/16 threads, one column per
 // group, each group synchronising on its own named barrier so the columns of
-// a CTA run out of phase. The column-independent tables -- N delta_k and the
-// pass-major FFT twiddles -- are loaded into shared memory once per CTA.
+// a CTA run out of phase. The column-independent tables -- N delta_k (in the
+// order the weight updates read it) and the pass-major FFT twiddles -- are
+// loaded into shared memory once per CTA. The stage vector is double-buffered:
+// each term's pack reads its stage and writes the next term's, so the
+// per-term stage update is one store per entry and no extra barrier phase.
 //
 // The same kernels with one unscaled term are the power-of-two cheb1
 // dct_iii / dst_iii / *_transpose of trig.hpp (so ndct with zero
@@ -77,22 +80,12 @@ struct Cfg {
   static constexpr int TW = twiddle_entries(P);   // pass-major FFT twiddles
   static constexpr int NSL = last_pass_ns(P);     // last FFT pass
   static constexpr int RL = P / NSL;
-  static constexpr size_t COL_BYTES = N * sizeof(double) + smem_row(P) * sizeof(double2);
+  // per column: the stage vector double-buffered (term l reads one copy while
+  // its pack writes term l+1's into the other) and the FFT row
+  static constexpr size_t COL_BYTES = 2 * N * sizeof(double) + smem_row(P) * sizeof(double2);
   // tables in shared memory when they fit beside the columns
-#ifndef FLB_NDCT_PSMEM
-#define FLB_NDCT_PSMEM 0
-#endif
-  // PSM: the per-row Taylor weights live in (thread-private) shared memory
-  // instead of registers, so two CTAs fit one SM's register file (128 regs)
-  // and their barrier-separated smem / FP64 phases can overlap. Measured
-  // slower at N = 4096 (25.3 / 33.8 ms vs 24.3 / 26.6 ms fwd / transpose:
-  // the 128-register cap still spills), so it is off by default.
-  static constexpr bool PSM = FLB_NDCT_PSMEM != 0;
-  static constexpr bool SMEM_TABLES =
-      !PSM && COLS * COL_BYTES + N * 8 + TW * 16 <= 220 * 1024;
-  static constexpr size_t SMEM =
-      COLS * COL_BYTES + (PSM ? COLS * N * 8 : 0) + (SMEM_TABLES ? N * 8 + TW * 16 : 0);
-  static constexpr int MINB = PSM ? 2 : 1;
+  static constexpr bool SMEM_TABLES = COLS * COL_BYTES + N * 8 + TW * 16 <= 220 * 1024;
+  static constexpr size_t SMEM = COLS * COL_BYTES + (SMEM_TABLES ? N * 8 + TW * 16 : 0);
   static constexpr int GT = COLS == 1 ? 0 : T;    // group barrier width (0 = whole CTA)
 };
 
@@ -144,22 +137,33 @@ __constant__ double kC8[16][2] = {
 
 // Packed Z_m of the forward transform for term parity ODD, m = t + r T.
 // ta_t = e^{i pi t/(2N)}, r4_t = e^{2 pi i t/N} (per-thread bases).
-template <int N, bool ODD, int R>
-__device__ __forceinline__ double2 fwd_pack(const double* stage, int m, double2 ta_t, double2 r4_t) {
+// The pack of Z_m reads stage entries {m, m + P, N - m, P - m} (both term
+// parities); with NEXT the thread also writes its own two, m and m + P, scaled
+// by n/N into `next` -- the stage of the following term -- so the stage
+// update costs one store per entry and no separate pass.
+template <int N, bool ODD, int R, bool NEXT>
+__device__ __forceinline__ double2 fwd_pack(const double* stage, double* next, int m, double2 ta_t,
+                                            double2 r4_t) {
   constexpr int P = N / 2;
   constexpr double h = 0.70710678118654752440;
-  auto X = [&](int j) -> double {  // X_j, 0 <= j <= N
-    if (j == 0) return ODD ? 0.0 : stage[0];
-    if (j >= N) return 0.0;
-    return 0.5 * (ODD ? stage[N - j] : stage[j]);
-  };
+  const double s_m = stage[m], s_mp = stage[m + P];
+  const double s_nm = stage[(N - m) & (N - 1)], s_pm = stage[P - m];
+  if (NEXT) {
+    next[m] = s_m * ((double)m / (double)N);  // (n/N)^{l+1} c_n
+    next[m + P] = s_mp * ((double)(m + P) / (double)N);
+  }
+  // X_j = a_j / 2 (X_0 = a_0, X_N = 0); a = stage (DCT) or the reversed stage (DST)
+  const bool m0 = m == 0;
+  const double xa = ODD ? (m0 ? 0.0 : 0.5 * s_nm) : (m0 ? s_m : 0.5 * s_m);
+  const double xan = m0 ? 0.0 : 0.5 * (ODD ? s_m : s_nm);
+  const double xb = 0.5 * (ODD ? s_pm : s_mp);
+  const double xbn = 0.5 * (ODD ? s_mp : s_pm);
   constexpr double a32x = PackConst::c32[R][0], a32y = PackConst::c32[R][1];
   constexpr double a8x = PackConst::c8[R][0], a8y = PackConst::c8[R][1];
   // e^{i pi m/(2N)}, e^{i pi (m+P)/(2N)} = e^{i pi/4} e^{i pi m/(2N)}, e^{2 pi i m/N}
   const double2 ta = make_double2(ta_t.x * a32x - ta_t.y * a32y, ta_t.x * a32y + ta_t.y * a32x);
   const double2 tb = make_double2(h * (ta.x - ta.y), h * (ta.x + ta.y));
   const double2 r4 = make_double2(r4_t.x * a8x - r4_t.y * a8y, r4_t.x * a8y + r4_t.y * a8x);
-  const double xa = X(m), xan = X(N - m), xb = X(m + P), xbn = X(P - m);
   const double2 Wa = make_double2(ta.x * xa + ta.y * xan, ta.y * xa - ta.x * xan);
   const double2 Wb = make_double2(tb.x * xb + tb.y * xbn, tb.y * xb - tb.x * xbn);
   const double2 s = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
@@ -169,27 +173,29 @@ __device__ __forceinline__ double2 fwd_pack(const double* stage, int m, double2 
 }
 
 // One forward Taylor term (or one plain transform): f[i] += sign p[i] y_{k_i}.
-template <int N, bool ODD, int R>
-__device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, int t, double2 ta_t,
-                                             double2 r4_t) {
+template <int N, bool ODD, bool NEXT, int R>
+__device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, double* next, int t,
+                                             double2 ta_t, double2 r4_t) {
   if constexpr (R < 8) {
-    v[R] = fwd_pack<N, ODD, R>(stage, t + R * (N / 16), ta_t, r4_t);
-    fwd_pack_all<N, ODD, R + 1>(v, stage, t, ta_t, r4_t);
+    v[R] = fwd_pack<N, ODD, R, NEXT>(stage, next, t + R * (N / 16), ta_t, r4_t);
+    fwd_pack_all<N, ODD, NEXT, R + 1>(v, stage, next, t, ta_t, r4_t);
   }
 }
 
-// p[i * PSTRIDE]: the Taylor weight of the thread's i-th owned row (registers
-// when PSTRIDE == 1, shared memory in owned-row order when PSTRIDE == T).
-template <int LOG2N, bool ODD, int PSTRIDE = 1>
-__device__ __forceinline__ void fwd_term(const double* stage, double2* zb, int t, int bar,
-                                         double2 ta_t, double2 r4_t, const double2* fftw,
+// One forward Taylor term (or one plain transform): f[i] += sign p[i] y_{k_i}.
+// The barrier before the first pass store orders it after the previous
+// term's last-pass reads of zb.
+template <int LOG2N, bool ODD, bool NEXT>
+__device__ __forceinline__ void fwd_term(const double* stage, double* next, double2* zb, int t,
+                                         int bar, double2 ta_t, double2 r4_t, const double2* fftw,
                                          const double* p, double* f, double sign) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, NSL = C::NSL, RL = C::RL;
   static_assert(E == 8 && T == N / 16, "pack twiddle constants assume T = N/16");
   double2 v[E];
-  fwd_pack_all<N, ODD, 0>(v, stage, t, ta_t, r4_t);
+  fwd_pack_all<N, ODD, NEXT, 0>(v, stage, next, t, ta_t, r4_t);
   pass_compute<P, E, 8, 1, true>(v, t, fftw);
+  group_sync<C::GT>(bar);
   pass_store<P, E, 8, 1>(v, zb, t);
   group_sync<C::GT>(bar);
   mid_passes<P, E, 8, NSL, true, C::GT>(zb, t, fftw, bar);
@@ -207,7 +213,7 @@ __device__ __forceinline__ void fwd_term(const double* stage, double2* zb, int t
         const int k = fwd_row_of<N>(2 * m + part);
         double y = part ? z.y : z.x;
         if (ODD && (k & 1)) y = -y;
-        f[i] += sign * p[i * PSTRIDE] * y;
+        f[i] += sign * p[i] * y;
       }
     }
 }
@@ -215,7 +221,7 @@ __device__ __forceinline__ void fwd_term(const double* stage, double2* zb, int t
 // plain_op: -1 = Taylor NDCT with num_terms terms; 0 = one plain DCT-III;
 // 1 = one plain DST-III.
 template <int LOG2N>
-__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, Cfg<LOG2N>::MINB)
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     fast_ndct_fwd_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                          size_t ld_out, size_t batch, const double* __restrict__ delta,
                          int num_terms, int plain_op, const double2* __restrict__ tw4n,
@@ -244,8 +250,9 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, Cfg<LOG2N>::MINB)
   const int bar = 1 + g;
   const size_t col = (size_t)blockIdx.x * C::COLS + g;
   if (col >= batch) return;
-  double* stage = smem + g * (C::COL_BYTES / 8);
-  double2* zb = reinterpret_cast<double2*>(stage + N);
+  double* stage = smem + g * (C::COL_BYTES / 8);  // (n/N)^l c_n, terms l even
+  double* stage_odd = stage + N;                  // terms l odd
+  double2* zb = reinterpret_cast<double2*>(stage + 2 * N);
   const double* src = in + col * ld_in;
   bool bad = false;
 #pragma unroll
@@ -257,14 +264,11 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, Cfg<LOG2N>::MINB)
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
   auto kown = [&](int i) -> int { return own_row(t, i); };
-  constexpr int PS = C::PSM ? T : 1;
-  double f[OWN], preg[C::PSM ? 1 : OWN];
-  // PSM: thread-private weights in smem, entry i of thread t at [i T + t]
-  double* p = C::PSM ? smem + C::COLS * (C::COL_BYTES / 8) + g * N + t : preg;
+  double f[OWN], p[OWN];
 #pragma unroll
   for (int i = 0; i < OWN; ++i) {
     f[i] = 0.0;
-    p[i * PS] = 1.0;
+    p[i] = 1.0;
   }
   // per-thread pack twiddle bases e^{i pi t/(2N)}, e^{2 pi i t/N} (table of 4N-th roots)
   const double2 ta_t = __ldg(&tw4n[t]);
@@ -272,26 +276,25 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, Cfg<LOG2N>::MINB)
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      fwd_term<LOG2N, true, PS>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      fwd_term<LOG2N, true, false>(stage, nullptr, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
     else
-      fwd_term<LOG2N, false, PS>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      fwd_term<LOG2N, false, false>(stage, nullptr, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
   } else {
     for (int l = 0; l < num_terms; ++l) {
       if (l > 0) {
         const double inv_l = 1.0 / (double)l;
 #pragma unroll
         for (int i = 0; i < OWN; ++i) {
-          const int n = t + T * i;
-          stage[n] *= (double)n / (double)N;  // (n/N)^l c_n
           const double q = C::SMEM_TABLES ? nd[i * T + t] : (double)N * __ldg(&delta[kown(i)]);
-          p[i * PS] *= q * inv_l;              // (N delta_k)^l / l!
+          p[i] *= q * inv_l;  // (N delta_k)^l / l!
         }
-        group_sync<C::GT>(bar);
       }
       if (l & 1)
-        fwd_term<LOG2N, true, PS>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, taylor_sign_d(l));
+        fwd_term<LOG2N, true, true>(stage_odd, stage, zb, t, bar, ta_t, r4_t, fftw, p, f,
+                                    taylor_sign_d(l));
       else
-        fwd_term<LOG2N, false, PS>(stage, zb, t, bar, ta_t, r4_t, fftw, p, f, taylor_sign_d(l));
+        fwd_term<LOG2N, false, true>(stage, stage_odd, zb, t, bar, ta_t, r4_t, fftw, p, f,
+                                     taylor_sign_d(l));
     }
   }
   // scatter the owned rows through shared memory, then one coalesced store
@@ -336,11 +339,17 @@ __device__ __forceinline__ double tr_unpack(double2 za, double2 zc, double2 tn, 
   return h.x * Vv.x + h.y * Vv.y;
 }
 
-// One transposed Taylor term: o[i] += sign rp[i] X_{tr_row(t, i)}.
-template <int LOG2N, bool ODD, int PSTRIDE = 1>
-__device__ __forceinline__ void tr_term(const double* hs, double2* zb, int t, int bar,
-                                        double2 ta_t, double2 r4_t, const double2* fftw,
-                                        const double* rp, double* o, double sign) {
+// One transposed Taylor term: o[i] += sign rp[i] X_{tr_row(t, i)}. The pack
+// reads every stage entry exactly once; with NEXT it also writes the next
+// term's stage, h (N delta)/(l+1) = h * nd * inv_next (nd in the tr_slot
+// order), into `next`. The barrier before the first pass store orders it after
+// the previous term's unpack reads of zb.
+template <int LOG2N, bool ODD, bool NEXT>
+__device__ __forceinline__ void tr_term(const double* hs, double* next, const double* nd,
+                                        const double* __restrict__ delta, double inv_next,
+                                        double2* zb, int t, int bar, double2 ta_t, double2 r4_t,
+                                        const double2* fftw, const double* rp, double* o,
+                                        double sign) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, OWN = C::OWN;
   static_assert(E == 8 && T == N / 16, "row grouping assumes T = N/16");
@@ -352,14 +361,22 @@ __device__ __forceinline__ void tr_term(const double* hs, double2* zb, int t, in
 #pragma unroll
   for (int r = 0; r < E; ++r) {
     const int m = t + r * T;
-    if (r < 4) {
-      v[r] = *reinterpret_cast<const double2*>(hs + 2 * m);
-    } else {
-      const double2 w = *reinterpret_cast<const double2*>(hs + P + N - 2 - 2 * m);
-      v[r] = ODD ? make_double2(-w.y, -w.x) : make_double2(w.y, w.x);
+    const int slot = r < 4 ? 2 * m : P + N - 2 - 2 * m;
+    const double2 w = *reinterpret_cast<const double2*>(hs + slot);
+    if (NEXT) {
+      const double2 q = C::SMEM_TABLES
+                            ? *reinterpret_cast<const double2*>(nd + slot)
+                            : make_double2((double)N * __ldg(&delta[tr_entry<N>(slot)]),
+                                           (double)N * __ldg(&delta[tr_entry<N>(slot + 1)]));
+      *reinterpret_cast<double2*>(next + slot) = make_double2(w.x * (q.x * inv_next), w.y * (q.y * inv_next));
     }
+    if (r < 4)
+      v[r] = w;
+    else
+      v[r] = ODD ? make_double2(-w.y, -w.x) : make_double2(w.y, w.x);
   }
   pass_compute<P, E, 8, 1, false>(v, t, fftw);
+  group_sync<C::GT>(bar);
   pass_store<P, E, 8, 1>(v, zb, t);
   group_sync<C::GT>(bar);
   mid_passes<P, E, 8, P, false, C::GT>(zb, t, fftw, bar);
@@ -392,15 +409,15 @@ __device__ __forceinline__ void tr_term(const double* hs, double2* zb, int t, in
     const double x1 = ODD ? tr_unpack<true>(zA1, zB1, t1, r1) : tr_unpack<false>(zB1, zA1, t1, r1);
     const double x2 = ODD ? tr_unpack<true>(zB, zA, t2, r2) : tr_unpack<false>(zA, zB, t2, r2);
     const double x3 = ODD ? tr_unpack<true>(zA1, zB1, t3, r3) : tr_unpack<false>(zB1, zA1, t3, r3);
-    o[4 * g + 0] += sign * rp[(4 * g + 0) * PSTRIDE] * x0;
-    o[4 * g + 1] += sign * rp[(4 * g + 1) * PSTRIDE] * x1;
-    o[4 * g + 2] += sign * rp[(4 * g + 2) * PSTRIDE] * x2;
-    o[4 * g + 3] += sign * rp[(4 * g + 3) * PSTRIDE] * x3;
+    o[4 * g + 0] += sign * rp[4 * g + 0] * x0;
+    o[4 * g + 1] += sign * rp[4 * g + 1] * x1;
+    o[4 * g + 2] += sign * rp[4 * g + 2] * x2;
+    o[4 * g + 3] += sign * rp[4 * g + 3] * x3;
   }
 }
 
 template <int LOG2N>
-__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, Cfg<LOG2N>::MINB)
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     fast_ndct_tr_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                         size_t ld_out, size_t batch, const double* __restrict__ delta,
                         int num_terms, int plain_op, const double* __restrict__ mult,
@@ -422,13 +439,12 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, Cfg<LOG2N>::MINB)
   const int bar = 1 + g;
   const size_t col = (size_t)blockIdx.x * C::COLS + g;
   if (col >= batch) return;
-  // h_k = (N delta_k)^l / l! g_k, in place, at hs[tr_slot(k)]
+  // h_k = (N delta_k)^l / l! g_k at hs[tr_slot(k)], double-buffered by term parity
   double* hs = smem + g * (C::COL_BYTES / 8);
-  double2* zb = reinterpret_cast<double2*>(hs + N);
+  double* hs_odd = hs + N;
+  double2* zb = reinterpret_cast<double2*>(hs + 2 * N);
   const double* src = in + col * ld_in;
-  constexpr int PS = C::PSM ? T : 1;
-  double o[OWN], rpreg[C::PSM ? 1 : OWN];
-  double* rp = C::PSM ? smem + C::COLS * (C::COL_BYTES / 8) + g * N + t : rpreg;
+  double o[OWN], rp[OWN];
   bool bad = false;
 #pragma unroll
   for (int i = 0; i < OWN; ++i) {
@@ -438,7 +454,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, Cfg<LOG2N>::MINB)
     bad |= !isfinite(v);
     hs[tr_slot<N>(k)] = v;
     o[i] = 0.0;
-    rp[i * PS] = 1.0;
+    rp[i] = 1.0;
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
   const double2 ta_t = __ldg(&tw4n[t]);      // e^{i pi t/(2N)}
@@ -446,27 +462,23 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, Cfg<LOG2N>::MINB)
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      tr_term<LOG2N, true, PS>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
+      tr_term<LOG2N, true, false>(hs, nullptr, nd, delta, 0.0, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
     else
-      tr_term<LOG2N, false, PS>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
+      tr_term<LOG2N, false, false>(hs, nullptr, nd, delta, 0.0, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
   } else {
     for (int l = 0; l < num_terms; ++l) {
       if (l > 0) {
-        const double inv_l = 1.0 / (double)l;
-        group_sync<C::GT>(bar);  // the previous term's reads of zb and hs are done
 #pragma unroll
-        for (int i = 0; i < OWN; ++i) {
-          const int j = t + T * i;  // slot j holds h_{tr_entry(j)}
-          const double q = C::SMEM_TABLES ? nd[j] : (double)N * __ldg(&delta[tr_entry<N>(j)]);
-          hs[j] *= q * inv_l;
-          rp[i * PS] *= (double)tr_row<N>(t, i) / (double)N;  // (n/N)^l for output row n
-        }
-        group_sync<C::GT>(bar);
+        for (int i = 0; i < OWN; ++i)
+          rp[i] *= (double)tr_row<N>(t, i) / (double)N;  // (n/N)^l for output row n
       }
+      const double inv_next = 1.0 / (double)(l + 1);
       if (l & 1)
-        tr_term<LOG2N, true, PS>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
+        tr_term<LOG2N, true, true>(hs_odd, hs, nd, delta, inv_next, zb, t, bar, ta_t, r4_t, fftw,
+                                   rp, o, taylor_sign_d(l));
       else
-        tr_term<LOG2N, false, PS>(hs, zb, t, bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
+        tr_term<LOG2N, false, true>(hs, hs_odd, nd, delta, inv_next, zb, t, bar, ta_t, r4_t, fftw,
+                                    rp, o, taylor_sign_d(l));
     }
   }
   double* dst = out + col * ld_out;
