@@ -198,9 +198,9 @@ __device__ __forceinline__ void fwd_term(const double* stage, double* next, doub
   group_sync<C::GT>(bar);
   pass_store<P, E, 8, 1>(v, zb, t);
   group_sync<C::GT>(bar);
-  mid_passes<P, E, 8, NSL, true, C::GT>(zb, t, fftw, bar);
+  mid_passes<P, E, 8, NSL, true, C::GT, true>(zb, t, fftw, bar);
   pass_load<P, E, RL>(v, zb, t);
-  pass_compute<P, E, RL, NSL, true>(v, t, fftw + pass_tw_offset(P, NSL));
+  pass_compute<P, E, RL, NSL, true, true>(v, t, fftw + pass_tw_offset(P, NSL));
 #pragma unroll
   for (int q = 0; q < E / RL; ++q)
 #pragma unroll
@@ -379,7 +379,7 @@ __device__ __forceinline__ void tr_term(const double* hs, double* next, const do
   group_sync<C::GT>(bar);
   pass_store<P, E, 8, 1>(v, zb, t);
   group_sync<C::GT>(bar);
-  mid_passes<P, E, 8, P, false, C::GT>(zb, t, fftw, bar);
+  mid_passes<P, E, 8, P, false, C::GT>(zb, t, fftw, bar);  // TWP measured slower here
   constexpr double h = 0.70710678118654752440;
 #pragma unroll
   for (int g = 0; g < OWN / 4; ++g) {

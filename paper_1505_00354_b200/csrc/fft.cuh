@@ -7,6 +7,8 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include "common.cuh"
+
 namespace flb {
 
 // Device table e^{-2 pi i m / P}, m < P (cached per device and P).
@@ -123,14 +125,35 @@ __device__ __forceinline__ void pass_load(double2* v, const double2* s, int tid)
   }
 }
 
-template <int P, int E, int R, int NS, bool INV>
+// TWP (twiddle powers): instead of loading all R-1 twiddles w^{r k} of a
+// butterfly, load w^k (and w^{4k} for R = 8) and form the rest by complex
+// products (at most three roundings deep): 2 loads instead of 7 for radix 8,
+// 1 instead of 3 for radix 4 -- shared-memory wavefronts traded for FP64 work.
+// Only for NS >= 64: below that a warp's twiddle loads hit few distinct
+// entries (broadcast, ~1 wavefront) and the products cost more than they save.
+template <int P, int E, int R, int NS, bool INV, bool TWP = false>
 __device__ __forceinline__ void pass_compute(double2* v, int tid, const double2* tw) {
   constexpr int TR = P / E, NB = E / R;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
     const int j = tid + q * TR;
     const int k = j & (NS - 1);
-    if (NS > 1) {
+    if constexpr (NS > 1 && TWP && NS >= 64 && (R == 8 || R == 4)) {
+      double2 w[R];
+      w[1] = tw[k];
+      if (INV) w[1].y = -w[1].y;
+      w[2] = cmul(w[1], w[1]);
+      w[3] = cmul(w[2], w[1]);
+      if constexpr (R == 8) {
+        w[4] = tw[3 * NS + k];
+        if (INV) w[4].y = -w[4].y;
+        w[5] = cmul(w[4], w[1]);
+        w[6] = cmul(w[4], w[2]);
+        w[7] = cmul(w[4], w[3]);
+      }
+#pragma unroll
+      for (int r = 1; r < R; ++r) v[q * R + r] = cmul(v[q * R + r], w[r]);
+    } else if (NS > 1) {
 #pragma unroll
       for (int r = 1; r < R; ++r) {
         double2 w = tw[(r - 1) * NS + k];
@@ -159,12 +182,12 @@ __device__ __forceinline__ void pass_store(const double2* v, double2* s, int tid
     for (int r = 0; r < R; ++r) s[smem_pad(pass_out_index<P, E, R, NS>(tid, q, r))] = v[q * R + r];
 }
 
-template <int P, int E, int R, int NS, bool INV, int GT>
+template <int P, int E, int R, int NS, bool INV, int GT, bool TWP = false>
 __device__ __forceinline__ void stockham_pass(double2* s, int tid, const double2* tw, int bar) {
   double2 v[E];
   pass_load<P, E, R>(v, s, tid);
   group_sync<GT>(bar);
-  pass_compute<P, E, R, NS, INV>(v, tid, tw);
+  pass_compute<P, E, R, NS, INV, TWP>(v, tid, tw);
   pass_store<P, E, R, NS>(v, s, tid);
   group_sync<GT>(bar);
 }
@@ -215,12 +238,12 @@ __host__ __device__ constexpr int pass_tw_offset(int p, int ns_target) {
 }
 
 // The passes with NS <= ns < NS_END (each ending with a row barrier).
-template <int P, int E, int NS, int NS_END, bool INV, int GT>
+template <int P, int E, int NS, int NS_END, bool INV, int GT, bool TWP = false>
 __device__ __forceinline__ void mid_passes(double2* s, int tid, const double2* tw, int bar) {
   if constexpr (NS < NS_END) {
     constexpr int R = pass_radix(P, NS);
-    stockham_pass<P, E, R, NS, INV, GT>(s, tid, tw + pass_tw_offset(P, NS), bar);
-    mid_passes<P, E, NS * R, NS_END, INV, GT>(s, tid, tw, bar);
+    stockham_pass<P, E, R, NS, INV, GT, TWP>(s, tid, tw + pass_tw_offset(P, NS), bar);
+    mid_passes<P, E, NS * R, NS_END, INV, GT, TWP>(s, tid, tw, bar);
   }
 }
 
