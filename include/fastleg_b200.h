@@ -149,6 +149,21 @@ enum { FL_LEG2CHEB_DIRECT = 0, FL_LEG2CHEB_FAST = 1 };
 fl_status fl_plan_set_leg2cheb_mode(fl_plan* plan, int mode);
 int fl_plan_leg2cheb_rank(const fl_plan* plan, int parity);
 
+/* Arithmetic of the direct (dense, triangular) conversion product inside
+ * dlt/idlt of plans with more than 16 columns:
+ *   0 = FL_GEMM_FP64       : fp64 tensor cores (mma.sync f64, DMMA);
+ *   1 = FL_GEMM_INT8_SPLIT : exact split-integer product on the tcgen05 int8
+ *       tensor cores: each operand row/column scaled by a power of two and
+ *       split into 8 signed 7-bit digits, the 36 digit products with
+ *       i + j < 8 accumulated exactly in int32 TMEM accumulators and summed
+ *       in fp64 (error <= ~2^-55 max|M row| max|c column| per term, the
+ *       order of fp64 rounding). For n a multiple of 256 in [512, 16384];
+ *       other sizes use FL_GEMM_FP64.
+ * Default FL_GEMM_INT8_SPLIT. fl_plan_gemm_mode returns the current mode. */
+enum { FL_GEMM_FP64 = 0, FL_GEMM_INT8_SPLIT = 1 };
+fl_status fl_plan_set_gemm_mode(fl_plan* plan, int mode);
+int fl_plan_gemm_mode(const fl_plan* plan);
+
 /* Term-parallel pieces of dlt / idlt (multi-GPU extension for one large
  * vector, C5). Both stages of fl_dlt are sums of independent terms, so P
  * ranks each take a slice and one collective sums the partials

@@ -18,6 +18,7 @@ CHEB1, CHEBSTAR = 0, 1
 DCT_III, DST_III, DCT_III_T, DST_III_T = range(4)
 NDCT_LITERAL, NDCT_FAST = 0, 1
 LEG2CHEB_DIRECT, LEG2CHEB_FAST = 0, 1
+GEMM_FP64, GEMM_INT8_SPLIT = 0, 1
 
 
 class FastlegError(Exception):
@@ -62,7 +63,7 @@ EXPORTS = [
     "fl_random_decaying", "fl_random_uniform_pm1", "fl_kernel_launch_count",
     "fl_eval_legendre_direct", "fl_eval_chebyshev_direct", "fl_idlt_direct",
     "fl_cheb_coeffs_of_legendre", "fl_plan_set_leg2cheb_mode", "fl_plan_leg2cheb_rank",
-    "fl_plan_stage_terms", "fl_dlt_stage",
+    "fl_plan_stage_terms", "fl_dlt_stage", "fl_plan_set_gemm_mode", "fl_plan_gemm_mode",
 ]
 
 
@@ -108,6 +109,8 @@ def _load() -> C.CDLL:
         "fl_plan_leg2cheb_rank": (i, [vp, i]),
         "fl_plan_stage_terms": (i, [vp, i, C.POINTER(i)]),
         "fl_dlt_stage": (i, [vp, i, i, i, i, dp, dp, vp]),
+        "fl_plan_set_gemm_mode": (i, [vp, i]),
+        "fl_plan_gemm_mode": (i, [vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

@@ -411,6 +411,15 @@ class TransformConfig:  # transforms.hpp:19-38
     def leg2cheb_rank(self, parity: int = 0) -> int:
         return int(LIB.fl_plan_leg2cheb_rank(self._h, int(parity)))
 
+    def set_gemm_mode(self, mode: int) -> None:
+        """GEMM_INT8_SPLIT (default: exact split-integer conversion product on
+        the int8 tensor cores, n % 256 == 0, 512 <= n <= 16384, > 16 columns)
+        or GEMM_FP64 (fp64 tensor cores)."""
+        check(LIB.fl_plan_set_gemm_mode(self._h, int(mode)))
+
+    def gemm_mode(self) -> int:
+        return int(LIB.fl_plan_gemm_mode(self._h))
+
     def grid(self) -> LegendreGrid:
         if self._grid is None:
             n = self.size()

@@ -18,6 +18,7 @@
 #include "fast_ndct.cuh"
 #include "launch.cuh"
 #include "l2c_fast.cuh"
+#include "l2c_ozaki.cuh"
 #include "leg2cheb.cuh"
 
 namespace flb {
@@ -309,6 +310,8 @@ struct fl_plan {
   FastNdct* fast = nullptr;  // cheb1-internal NDCT (power-of-two n), or null
   L2CFast* l2c = nullptr;    // Toeplitz-Hankel leg2cheb (n >= kL2CFastMin), or null
   int l2c_mode = 1;          // 1: fast conversion for few columns when available; 0: direct
+  int gemm_mode = FL_GEMM_INT8_SPLIT;  // arithmetic of the direct conversion product
+  L2COzaki* oz[2] = {nullptr, nullptr};  // split-int8 slices of M, (m + 1/2) M^T (lazy)
   std::mutex mu;
 };
 
@@ -319,6 +322,7 @@ void plan_free(fl_plan* p) {
     if (q) cudaFree(q);
   if (p->fast) fast_ndct_destroy(p->fast);
   if (p->l2c) l2c_fast_destroy(p->l2c);
+  for (L2COzaki* o : p->oz) l2c_ozaki_destroy(o);
   delete p;
 }
 
@@ -334,6 +338,16 @@ void plan_finish(fl_plan* p) {
   p->fast = fast_ndct_create(n, p->tolerance, p->kind, p->theta);
   if (n >= kL2CFastMin) p->l2c = l2c_fast_create(n, p->s, 0);
   FLB_CUDA(cudaDeviceSynchronize());
+}
+
+// The split-int8 conversion product for this call, or null (fp64 path).
+const L2COzaki* plan_ozaki(fl_plan* p, int transpose, size_t batch, cudaStream_t s) {
+  if (p->gemm_mode != FL_GEMM_INT8_SPLIT || batch <= 16 || !l2c_ozaki_supported(p->n) ||
+      p->n > 16384)
+    return nullptr;
+  std::lock_guard<std::mutex> lock(p->mu);
+  if (!p->oz[transpose]) p->oz[transpose] = l2c_ozaki_create(p->n, p->s, transpose, transpose, s);
+  return p->oz[transpose];
 }
 
 }  // namespace
@@ -663,6 +677,17 @@ fl_status fl_plan_set_leg2cheb_mode(fl_plan* p, int mode) {
   });
 }
 
+fl_status fl_plan_set_gemm_mode(fl_plan* p, int mode) {
+  return guarded([&] {
+    if (!p) fail(FL_INVALID_ARGUMENT, "plan: null");
+    if (mode != FL_GEMM_FP64 && mode != FL_GEMM_INT8_SPLIT)
+      fail(FL_INVALID_ARGUMENT, "plan: unknown gemm mode");
+    p->gemm_mode = mode;
+  });
+}
+
+int fl_plan_gemm_mode(const fl_plan* p) { return p ? p->gemm_mode : -1; }
+
 int fl_plan_leg2cheb_rank(const fl_plan* p, int parity) {
   if (!p || !p->l2c || parity < 0 || parity > 1) return 0;
   return l2c_fast_rank(*p->l2c, parity);
@@ -682,10 +707,20 @@ fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, 
     if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
     // transforms.hpp:47-48: chat = M c (scratch), f = NDCT(chat)
     DevScratch<double> chat(n * batch, s);
+    const double* cin = i.ptr;
+    DevScratch<double> packed(i.ld != n ? n * batch : 0, s);
+    if (i.ld != n) {  // the conversion kernels read columns of stride n
+      FLB_CUDA(cudaMemcpy2DAsync(packed.p, n * 8, i.ptr, i.ld * 8, n * 8, batch,
+                                 cudaMemcpyDeviceToDevice, s));
+      cin = packed.p;
+    }
+    fl_plan* mp = const_cast<fl_plan*>(p);
     if (p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)
-      l2c_fast_apply(*p->l2c, 0, i.ptr, chat.p, batch, n, 0, s);
+      l2c_fast_apply(*p->l2c, 0, cin, chat.p, batch, n, 0, s);
+    else if (const L2COzaki* oz = plan_ozaki(mp, 0, batch, s))
+      l2c_ozaki_apply(*oz, cin, chat.p, batch, n, s);
     else
-      leg2cheb_direct(0, n, p->s, i.ptr, chat.p, batch, n, 0, s);
+      leg2cheb_direct(0, n, p->s, cin, chat.p, batch, n, 0, s);
     const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
     if (o.ld != n) {
       DevScratch<double> f(n * batch, s);
@@ -726,8 +761,11 @@ fl_status fl_idlt(const fl_plan* p, const double* in, double* out, size_t batch,
       run_ndct("ndct_apply_transpose", 1, p->kind, n, p->num_terms, p->delta, i.ptr, n, back.p,
                n, batch, p->w, fast, s);
     }
+    fl_plan* mp = const_cast<fl_plan*>(p);
     if (p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)
       l2c_fast_apply(*p->l2c, 1, back.p, o.ptr, batch, o.ld, 1, s);
+    else if (const L2COzaki* oz = plan_ozaki(mp, 1, batch, s))
+      l2c_ozaki_apply(*oz, back.p, o.ptr, batch, o.ld, s);
     else
       leg2cheb_direct(1, n, p->s, back.p, o.ptr, batch, o.ld, 1, s);
     o.finish();

@@ -1,0 +1,486 @@
+// Legendre <-> Chebyshev conversion (conversion.hpp:100-140) as an exact
+// integer split GEMM on the tcgen05 tensor cores.
+//
+// Per parity class p the conversion is a triangular GEMM  C = A B  with
+// A = the (N/2 x N/2) parity block of M (or of (m + 1/2) M^T for the IDLT)
+// and B = the parity-p entries of the input columns. B200's fp64 tensor
+// path (DMMA, leg2cheb.cu) peaks at ~37 TFLOP/s; its int8 tensor cores at
+// ~4.5 POP/s. The split ("Ozaki") scheme runs the fp64 product on the int8
+// units exactly:
+//
+//   row / column scaling:  A_ab = 2^{ea_a} sum_{i<S} a^(i)_ab 2^{-7(i+1)},
+//                          B_bc = 2^{eb_c} sum_{j<S} b^(j)_bc 2^{-7(j+1)},
+//   digits a^(i), b^(j) in [-64, 64] (round-to-nearest splitting of the
+//   scaled value, exact in fp64), so every digit product is exact and a
+//   K-sum of them fits int32 (|sum| <= 8 * 64^2 * N/2 < 2^31 for N <= 2^16):
+//
+//   C_ac = 2^{ea_a + eb_c} sum_{d < S} 2^{-7(d+2)} sum_{i+j=d} (a^(i) b^(j))_ac
+//
+// Pairs with i + j >= S are dropped (below 2^{-7(S+1)} of the row/column
+// scales; S = 8 keeps the result at fp64 level: ~2^-55 of max|A_a.| max|B_.c|
+// per term, the same order as an fp64 dot product's rounding).
+//
+// Kernel (one CTA per 128 x 64 output tile of one parity):
+//   warp 0     TMA producer: per 64-wide K block, the 8 slices of the A tile
+//              (128 rows x 64 B) and of the B tile (64 columns x 64 B),
+//              SWIZZLE_64B, into a 2-stage ring (96 KB per stage)
+//   warp 1     TMEM allocator and MMA issuer: 36 slice pairs x 2 K-steps of
+//              tcgen05.mma.cta_group::1.kind::i8 (M = 128, N = 64, K = 32)
+//              per stage, pair (i, j) accumulating into TMEM accumulator
+//              d = i + j (8 x 64 int32 columns = all 512 TMEM columns)
+//   warps 2-5  epilogue: tcgen05.ld of the 8 accumulators, exact int32 ->
+//              fp64, scaled sum, row/column scales, store (k = 2a + p)
+// Only the K blocks on or above (forward) / below (transpose) the diagonal
+// block are visited: the triangle costs half the square.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cmath>
+
+#include "common.cuh"
+#include "l2c_ozaki.cuh"
+#include "launch.cuh"
+
+namespace flb {
+
+namespace oz {
+constexpr int S = 8;            // digits per operand
+constexpr int BM = 128;         // output rows per tile (TMEM lanes)
+constexpr int BN = 64;          // output columns per tile
+constexpr int BK = 64;          // K bytes per stage (= SWIZZLE_64B row)
+constexpr int STAGES = 2;
+constexpr int A_TILE = BM * BK;               // 8 KB
+constexpr int B_TILE = BN * BK;               // 4 KB
+constexpr int STAGE_BYTES = S * (A_TILE + B_TILE);  // 96 KB
+constexpr int THREADS = 192;                  // 6 warps
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int PAIRS = S * (S + 1) / 2;        // i + j < S
+// kind::i8 instruction descriptor: D s32, A/B signed, K-major, N = 64, M = 128
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >> 3) << 17) |
+                           ((uint32_t)(BM >> 4) << 24);
+}  // namespace oz
+
+struct L2COzaki {
+  size_t n = 0, r = 0;       // r = n / 2 rows (and K) per parity
+  int transpose = 0;
+  int8_t* a = nullptr;       // [S][2][r][r] digits, K-major rows
+  double* arow = nullptr;    // [2][r] row scales 2^ea
+  CUtensorMap tmap_a;
+};
+
+namespace {
+
+// ---- PTX helpers -------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint32_t bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(bar), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra DONE_%=;\n\t"
+      "bra WAIT_%=;\n"
+      "DONE_%=:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, uint32_t bar,
+                                            int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                   bar)
+               : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// K-major, SWIZZLE_64B canonical layout: 64 B rows, 8-row groups 512 B apart.
+__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) /*LBO (unused)*/ |
+         (32ull << 32) /*SBO = 512 B*/ | (1ull << 46) /*sm100 version*/ |
+         (4ull << 61) /*SWIZZLE_64B*/;
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// ---- digit splitting ---------------------------------------------------
+// Scale exponent e with max * 2^-e < 1/2 (0 for max = 0).
+__device__ __forceinline__ int split_exp(double mx) {
+  if (!(mx > 0.0)) return 0;
+  int e;
+  frexp(mx, &e);  // mx = m 2^e, m in [0.5, 1)
+  return e + 1;
+}
+// Digits of r = x 2^-e (|r| < 1/2): r = sum_j d_j 2^{-7(j+1)} + O(2^{-7S-1}).
+__device__ __forceinline__ void split_digits(double x, int e, int8_t (&d)[oz::S]) {
+  double r = ldexp(x, -e);
+#pragma unroll
+  for (int j = 0; j < oz::S; ++j) {
+    const double t = r * 128.0;
+    const double q = rint(t);
+    d[j] = (int8_t)(int)q;
+    r = t - q;
+  }
+}
+
+// Entry of the parity-p block: forward A[a][b] = pref_{2a+p} s_{b-a} s_{a+b+p}
+// (b >= a); transpose A[b][a'] = sc_{2b+p} pref_{2a'+p} s_{b-a'} s_{a'+b+p} (a' <= b).
+__device__ __forceinline__ double block_entry(const double* __restrict__ s, int transpose,
+                                              int scale_half, int p, size_t row, size_t col) {
+  size_t a, b;
+  if (!transpose) {
+    a = row, b = col;
+  } else {
+    a = col, b = row;
+  }
+  if (b < a) return 0.0;
+  const double pref = (2 * a + p) == 0 ? 1.0 : 2.0;
+  double v = pref * (s[b - a] * s[a + b + p]);
+  if (transpose && scale_half) v *= (double)(2 * b + p) + 0.5;
+  return v;
+}
+
+// One CTA per (parity, row): row scale and the S digit rows of A.
+__global__ void __launch_bounds__(256) oz_split_a_kernel(const double* __restrict__ s, size_t r,
+                                                         int transpose, int scale_half,
+                                                         int8_t* __restrict__ a,
+                                                         double* __restrict__ arow) {
+  const int p = blockIdx.y;
+  const size_t row = blockIdx.x;
+  __shared__ double red[8];
+  __shared__ int e_sh;
+  double mx = 0.0;
+  for (size_t c = threadIdx.x; c < r; c += blockDim.x)
+    mx = fmax(mx, fabs(block_entry(s, transpose, scale_half, p, row, c)));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    e_sh = split_exp(m);
+    arow[p * r + row] = ldexp(1.0, e_sh);
+  }
+  __syncthreads();
+  const int e = e_sh;
+  for (size_t c = threadIdx.x; c < r; c += blockDim.x) {
+    int8_t d[oz::S];
+    split_digits(block_entry(s, transpose, scale_half, p, row, c), e, d);
+#pragma unroll
+    for (int j = 0; j < oz::S; ++j) a[((size_t)(j * 2 + p) * r + row) * r + c] = d[j];
+  }
+}
+
+// One CTA per input column: per-parity scales and the S digit slices,
+// de-interleaved by parity ([S][2][cols][r]). A non-finite column gets a NaN
+// scale so the product column comes out NaN (the NDCT input check reports it).
+__global__ void __launch_bounds__(256) oz_split_b_kernel(const double* __restrict__ in, size_t n,
+                                                         size_t ld, size_t cols,
+                                                         int8_t* __restrict__ b,
+                                                         double* __restrict__ bcol) {
+  const size_t col = blockIdx.x;
+  const size_t r = n / 2;
+  const double* x = in + col * ld;
+  __shared__ double red[2][8];
+  __shared__ int e_sh[2];
+  __shared__ int bad_sh;
+  if (threadIdx.x == 0) bad_sh = 0;
+  double mx0 = 0.0, mx1 = 0.0;
+  bool bad = false;
+  for (size_t c = threadIdx.x; c < n / 16; c += blockDim.x) {
+    const double2* q = reinterpret_cast<const double2*>(x + 16 * c);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double2 v = q[i];
+      bad |= !isfinite(v.x) || !isfinite(v.y);
+      mx0 = fmax(mx0, fabs(v.x));
+      mx1 = fmax(mx1, fabs(v.y));
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx0 = fmax(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+    mx1 = fmax(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+  }
+  __syncthreads();
+  if (bad) atomicOr(&bad_sh, 1);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = mx0;
+    red[1][threadIdx.x >> 5] = mx1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[threadIdx.x][w]);
+    e_sh[threadIdx.x] = split_exp(m);
+    bcol[threadIdx.x * cols + col] = bad_sh ? __longlong_as_double(0x7ff8000000000000ll)
+                                            : ldexp(1.0, e_sh[threadIdx.x]);
+  }
+  __syncthreads();
+  const int e0 = e_sh[0], e1 = e_sh[1];
+  for (size_t c = threadIdx.x; c < n / 16; c += blockDim.x) {
+    const double2* q = reinterpret_cast<const double2*>(x + 16 * c);
+    uint64_t w0[oz::S], w1[oz::S];
+#pragma unroll
+    for (int j = 0; j < oz::S; ++j) w0[j] = w1[j] = 0;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const double2 v = q[i];
+      int8_t d0[oz::S], d1[oz::S];
+      split_digits(isfinite(v.x) ? v.x : 0.0, e0, d0);
+      split_digits(isfinite(v.y) ? v.y : 0.0, e1, d1);
+#pragma unroll
+      for (int j = 0; j < oz::S; ++j) {
+        w0[j] |= (uint64_t)(uint8_t)d0[j] << (8 * i);
+        w1[j] |= (uint64_t)(uint8_t)d1[j] << (8 * i);
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < oz::S; ++j) {
+      *reinterpret_cast<uint64_t*>(b + ((size_t)(j * 2 + 0) * cols + col) * r + 8 * c) = w0[j];
+      *reinterpret_cast<uint64_t*>(b + ((size_t)(j * 2 + 1) * cols + col) * r + 8 * c) = w1[j];
+    }
+  }
+}
+
+// ---- the split GEMM ------------------------------------------------------
+__global__ void __launch_bounds__(oz::THREADS, 1)
+    oz_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                   const __grid_constant__ CUtensorMap tmap_b, const double* __restrict__ arow,
+                   const double* __restrict__ bcol, double* __restrict__ out, size_t r,
+                   size_t cols, size_t ld, int transpose) {
+  using namespace oz;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  // bars[0..1] full, [2..3] empty, [4] accumulators ready
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t rb_count = r / BM;
+  const size_t tile = blockIdx.x;
+  const size_t cb = tile / (2 * rb_count);
+  const int p = (int)(tile % 2);
+  const size_t rb = (tile / 2) % rb_count;
+  // K blocks (of BK) with nonzero entries
+  const int kb_lo = transpose ? 0 : (int)(rb * (BM / BK));
+  const int kb_hi = transpose ? (int)((rb + 1) * (BM / BK)) : (int)(r / BK);
+  const int nk = kb_hi - kb_lo;
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < 2 * STAGES + 1; ++i) mbar_init(smem_u32(&bars[i]), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      // TMA producer
+      for (int it = 0; it < nk; ++it) {
+        const int st = it % STAGES;
+        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+        mbar_wait(smem_u32(&bars[2 + st]), ph ^ 1u);
+        const uint32_t full = smem_u32(&bars[st]);
+        mbar_expect_tx(full, STAGE_BYTES);
+        uint8_t* sa = smem + st * STAGE_BYTES;
+        uint8_t* sb = sa + S * A_TILE;
+        const int k0 = (kb_lo + it) * BK;
+        for (int i = 0; i < S; ++i) {
+          tma_load_3d(smem_u32(sa + i * A_TILE), &tmap_a, full, k0, (int)(rb * BM), i * 2 + p);
+          tma_load_3d(smem_u32(sb + i * B_TILE), &tmap_b, full, k0, (int)(cb * BN), i * 2 + p);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // MMA issuer (one lane)
+    if (lane == 0) {
+      for (int it = 0; it < nk; ++it) {
+        const int st = it % STAGES;
+        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
+        mbar_wait(smem_u32(&bars[st]), ph);
+        tc_fence_after();
+        const uint32_t sa = smem_u32(smem + st * STAGE_BYTES);
+        const uint32_t sb = sa + S * A_TILE;
+#pragma unroll 1
+        for (int i = 0; i < S; ++i) {
+#pragma unroll 1
+          for (int j = 0; i + j < S; ++j) {
+            const uint32_t d_tmem = tmem + (uint32_t)((i + j) * BN);
+#pragma unroll
+            for (int ks = 0; ks < BK / 32; ++ks) {
+              const uint64_t ad = sw64_desc(sa + i * A_TILE + ks * 32);
+              const uint64_t bd = sw64_desc(sb + j * B_TILE + ks * 32);
+              const uint32_t acc = (it > 0 || ks > 0 || i > 0) ? 1u : 0u;
+              tc_mma_i8(d_tmem, ad, bd, IDESC, acc);
+            }
+          }
+        }
+        tc_commit(smem_u32(&bars[2 + st]));  // frees the stage when these MMAs retire
+      }
+      tc_commit(smem_u32(&bars[4]));  // accumulators complete
+    }
+  } else {
+    // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +32 (one output row per thread)
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const size_t arow_idx = (size_t)p * r + rb * BM + row;
+    const size_t k = 2 * (rb * BM + row) + p;  // output row (interleaved parities)
+    mbar_wait(smem_u32(&bars[4]), 0);
+    tc_fence_after();
+    const double ascale = arow[arow_idx];
+#pragma unroll 1
+    for (int h = 0; h < BN / 32; ++h) {
+      double acc[32];
+#pragma unroll
+      for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+      // least significant accumulator first
+#pragma unroll 1
+      for (int d = S - 1; d >= 0; --d) {
+        uint32_t v[32];
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * BN + h * 32), v);
+        const double w = ldexp(1.0, -7 * (d + 2));
+#pragma unroll
+        for (int c = 0; c < 32; ++c) acc[c] = fma((double)(int)v[c], w, acc[c]);
+      }
+#pragma unroll
+      for (int c = 0; c < 32; ++c) {
+        const size_t col = cb * BN + h * 32 + c;
+        if (col < cols) out[col * ld + k] = (acc[c] * ascale) * bcol[(size_t)p * cols + col];
+      }
+    }
+    tc_fence_before();
+  }
+  __syncthreads();
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    FLB_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q));
+    if (q != cudaDriverEntryPointSuccess || !f)
+      fail(FL_CUDA_ERROR, "l2c_ozaki: cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+  }();
+  return fn;
+}
+
+// 3-D int8 map [z][rows][k] with a (BK x box_rows x 1) SWIZZLE_64B box.
+CUtensorMap make_map(const int8_t* base, size_t k, size_t rows, size_t z, int box_rows) {
+  CUtensorMap m;
+  cuuint64_t dims[3] = {(cuuint64_t)k, (cuuint64_t)rows, (cuuint64_t)z};
+  cuuint64_t strides[2] = {(cuuint64_t)k, (cuuint64_t)(k * rows)};
+  cuuint32_t box[3] = {(cuuint32_t)oz::BK, (cuuint32_t)box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult res = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims,
+                                   strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (res != CUDA_SUCCESS) fail(FL_CUDA_ERROR, "l2c_ozaki: tensor map encode failed");
+  return m;
+}
+
+}  // namespace
+
+bool l2c_ozaki_supported(size_t n) { return n % 256 == 0 && n >= 512 && n <= (1u << 16); }
+
+L2COzaki* l2c_ozaki_create(size_t n, const double* s, int transpose, int scale_half,
+                           cudaStream_t st) {
+  if (!l2c_ozaki_supported(n)) fail(FL_INVALID_ARGUMENT, "l2c_ozaki: unsupported size");
+  auto* p = new L2COzaki;
+  p->n = n;
+  p->r = n / 2;
+  p->transpose = transpose;
+  const size_t r = p->r;
+  FLB_CUDA(cudaMalloc(&p->a, (size_t)oz::S * 2 * r * r));
+  FLB_CUDA(cudaMalloc(&p->arow, 2 * r * sizeof(double)));
+  oz_split_a_kernel<<<dim3((unsigned)r, 2), 256, 0, st>>>(s, r, transpose, scale_half, p->a,
+                                                          p->arow);
+  note_launch("oz_split_a_kernel");
+  p->tmap_a = make_map(p->a, r, r, 2 * oz::S, oz::BM);
+  return p;
+}
+
+void l2c_ozaki_destroy(L2COzaki* p) {
+  if (!p) return;
+  cudaFree(p->a);
+  cudaFree(p->arow);
+  delete p;
+}
+
+void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t cols, size_t ld,
+                     cudaStream_t st) {
+  if (cols == 0) return;
+  const size_t n = p.n, r = p.r;
+  int8_t* b = nullptr;
+  double* bcol = nullptr;
+  FLB_CUDA(cudaMallocAsync(&b, (size_t)oz::S * 2 * cols * r, st));
+  FLB_CUDA(cudaMallocAsync(&bcol, 2 * cols * sizeof(double), st));
+  oz_split_b_kernel<<<(unsigned)cols, 256, 0, st>>>(in, n, ld, cols, b, bcol);
+  note_launch("oz_split_b_kernel");
+  const CUtensorMap tmap_b = make_map(b, r, cols, 2 * oz::S, oz::BN);
+  static bool attr = [] {
+    FLB_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  oz::SMEM));
+    return true;
+  }();
+  (void)attr;
+  const size_t tiles = 2 * (r / oz::BM) * ((cols + oz::BN - 1) / oz::BN);
+  oz_gemm_kernel<<<(unsigned)tiles, oz::THREADS, oz::SMEM, st>>>(p.tmap_a, tmap_b, p.arow, bcol,
+                                                                  out, r, cols, ld, p.transpose);
+  note_launch("oz_gemm_kernel");
+  cudaFreeAsync(b, st);
+  cudaFreeAsync(bcol, st);
+}
+
+}  // namespace flb
