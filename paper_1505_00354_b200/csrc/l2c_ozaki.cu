@@ -20,21 +20,26 @@
 // scales; S = 8 keeps the result at fp64 level: ~2^-55 of max|A_a.| max|B_.c|
 // per term, the same order as an fp64 dot product's rounding).
 //
-// Kernel (one CTA per 128 x 64 output tile of one parity):
+// Kernel (persistent, one CTA per SM; output tiles of 128 rows x 64 columns
+// of one parity):
 //   warp 0     TMA producer: per 64-wide K block, the 8 slices of the A tile
 //              (128 rows x 64 B) and of the B tile (64 columns x 64 B),
-//              SWIZZLE_64B, into a 2-stage ring (96 KB per stage)
+//              SWIZZLE_64B, into a 2-stage ring (96 KB per stage; BK = 32 /
+//              SWIZZLE_32B / 4 stages measured 1% slower)
 //   warp 1     TMEM allocator and MMA issuer: 36 slice pairs x 2 K-steps of
 //              tcgen05.mma.cta_group::1.kind::i8 (M = 128, N = 64, K = 32)
-//              per stage, pair (i, j) accumulating into TMEM accumulator
+//              per stage, fully unrolled, issued by one elected lane of the
+//              whole warp (uniform operands); pair (i, j) accumulating into TMEM accumulator
 //              d = i + j (8 x 64 int32 columns = all 512 TMEM columns)
 //   warps 2-5  epilogue: tcgen05.ld of the 8 accumulators, exact int32 ->
-//              fp64, scaled sum, row/column scales, store (k = 2a + p)
+//              fp64 scaled sum in registers, TMEM released to the next tile,
+//              then row/column scales and the store (k = 2a + p)
 // Only the K blocks on or above (forward) / below (transpose) the diagonal
 // block are visited: the triangle costs half the square.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cmath>
 
 #include "common.cuh"
@@ -47,12 +52,19 @@ namespace oz {
 constexpr int S = 8;            // digits per operand
 constexpr int BM = 128;         // output rows per tile (TMEM lanes)
 constexpr int BN = 64;          // output columns per tile
-constexpr int BK = 64;          // K bytes per stage (= SWIZZLE_64B row)
-constexpr int STAGES = 2;
-constexpr int A_TILE = BM * BK;               // 8 KB
-constexpr int B_TILE = BN * BK;               // 4 KB
-constexpr int STAGE_BYTES = S * (A_TILE + B_TILE);  // 96 KB
+#ifndef FLB_OZ_BK
+#define FLB_OZ_BK 64
+#endif
+#ifndef FLB_OZ_STAGES
+#define FLB_OZ_STAGES 2
+#endif
+constexpr int BK = FLB_OZ_BK;   // K bytes per stage (32: SWIZZLE_32B rows, 64: SWIZZLE_64B)
+constexpr int STAGES = FLB_OZ_STAGES;
+constexpr int A_TILE = BM * BK;
+constexpr int B_TILE = BN * BK;
+constexpr int STAGE_BYTES = S * (A_TILE + B_TILE);
 constexpr int THREADS = 192;                  // 6 warps
+constexpr int EPI_THREADS = 128;              // warps 2-5
 constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr int PAIRS = S * (S + 1) / 2;        // i + j < S
 // kind::i8 instruction descriptor: D s32, A/B signed, K-major, N = 64, M = 128
@@ -111,20 +123,37 @@ __device__ __forceinline__ void tc_commit(uint32_t bar) {
                    bar)
                : "memory");
 }
+// Issued by a whole warp with warp-uniform operands (kept in uniform
+// registers); one elected lane executes the MMA / commit. The same lane (the
+// lowest active one) issues both, as tcgen05.commit tracks the issuing
+// thread's MMAs.
 __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
                                           uint32_t idesc, uint32_t accumulate) {
   asm volatile(
-      "{\n\t.reg .pred p;\n\t"
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
       : "memory");
 }
-// K-major, SWIZZLE_64B canonical layout: 64 B rows, 8-row groups 512 B apart.
-__device__ __forceinline__ uint64_t sw64_desc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) /*LBO (unused)*/ |
-         (32ull << 32) /*SBO = 512 B*/ | (1ull << 46) /*sm100 version*/ |
-         (4ull << 61) /*SWIZZLE_64B*/;
+__device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+          bar)
+      : "memory");
+}
+// K-major canonical layout of BK-byte rows swizzled over BK bytes (SWIZZLE_32B
+// or _64B): 8-row groups 8 BK bytes apart (SBO), LBO unused.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
+  constexpr uint64_t layout = oz::BK == 64 ? 4 : 6;  // SWIZZLE_64B : SWIZZLE_32B
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) |
+         ((uint64_t)(8 * oz::BK / 16) << 32) | (1ull << 46) /*sm100 version*/ | (layout << 61);
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
@@ -280,32 +309,44 @@ __global__ void __launch_bounds__(256) oz_split_b_kernel(const double* __restric
 }
 
 // ---- the split GEMM ------------------------------------------------------
+// Persistent: CTA b takes tiles b, b + grid, ... (consecutive CTAs share a
+// column block, so the B digits are reused from L2). The smem ring and its
+// phases run continuously across tiles; the epilogue drains the 8 TMEM
+// accumulators into fp64 registers, releases TMEM (tmem_empty) so the next
+// tile's MMAs start, then scales and stores.
 __global__ void __launch_bounds__(oz::THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const double* __restrict__ arow,
                    const double* __restrict__ bcol, double* __restrict__ out, size_t r,
-                   size_t cols, size_t ld, int transpose) {
+                   size_t cols, size_t ld, int transpose, size_t ntiles) {
   using namespace oz;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                              ~uintptr_t(1023));
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
-  // bars[0..1] full, [2..3] empty, [4] accumulators ready
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 8);
+  // bars[0, STAGES) full, [STAGES, 2 STAGES) empty, [2 STAGES] tmem_full, [2 STAGES + 1] tmem_empty
+  uint64_t* full_b = bars;
+  uint64_t* empty_b = bars + STAGES;
+  uint64_t* tfull_b = bars + 2 * STAGES;
+  uint64_t* tempty_b = bars + 2 * STAGES + 1;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t rb_count = r / BM;
-  const size_t tile = blockIdx.x;
-  const size_t cb = tile / (2 * rb_count);
-  const int p = (int)(tile % 2);
-  const size_t rb = (tile / 2) % rb_count;
-  // K blocks (of BK) with nonzero entries
-  const int kb_lo = transpose ? 0 : (int)(rb * (BM / BK));
-  const int kb_hi = transpose ? (int)((rb + 1) * (BM / BK)) : (int)(r / BK);
-  const int nk = kb_hi - kb_lo;
+  auto tile_coords = [&](size_t tile, size_t& cb, int& p, size_t& rb, int& kb_lo, int& nk) {
+    cb = tile / (2 * rb_count);
+    p = (int)(tile % 2);
+    rb = (tile / 2) % rb_count;
+    // K blocks (of BK) with nonzero entries: on/above (forward) or on/below
+    // (transpose) the diagonal block
+    kb_lo = transpose ? 0 : (int)(rb * (BM / BK));
+    const int kb_hi = transpose ? (int)((rb + 1) * (BM / BK)) : (int)(r / BK);
+    nk = kb_hi - kb_lo;
+  };
 
   if (threadIdx.x == 0) {
     for (int i = 0; i < 2 * STAGES + 1; ++i) mbar_init(smem_u32(&bars[i]), 1);
+    mbar_init(smem_u32(tempty_b), EPI_THREADS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -320,81 +361,98 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   const uint32_t tmem = *tmem_holder;
 
   if (warp == 0) {
-    if (lane == 0) {
-      // TMA producer
-      for (int it = 0; it < nk; ++it) {
-        const int st = it % STAGES;
-        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
-        mbar_wait(smem_u32(&bars[2 + st]), ph ^ 1u);
-        const uint32_t full = smem_u32(&bars[st]);
-        mbar_expect_tx(full, STAGE_BYTES);
-        uint8_t* sa = smem + st * STAGE_BYTES;
-        uint8_t* sb = sa + S * A_TILE;
-        const int k0 = (kb_lo + it) * BK;
-        for (int i = 0; i < S; ++i) {
-          tma_load_3d(smem_u32(sa + i * A_TILE), &tmap_a, full, k0, (int)(rb * BM), i * 2 + p);
-          tma_load_3d(smem_u32(sb + i * B_TILE), &tmap_b, full, k0, (int)(cb * BN), i * 2 + p);
+    if (lane == 0) {  // TMA producer
+      uint32_t it = 0;
+      for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        size_t cb, rb;
+        int p, kb_lo, nk;
+        tile_coords(tile, cb, p, rb, kb_lo, nk);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const uint32_t st = it % STAGES, ph = (it / STAGES) & 1u;
+          mbar_wait(smem_u32(&empty_b[st]), ph ^ 1u);
+          const uint32_t full = smem_u32(&full_b[st]);
+          mbar_expect_tx(full, STAGE_BYTES);
+          uint8_t* sa = smem + st * STAGE_BYTES;
+          uint8_t* sb = sa + S * A_TILE;
+          const int k0 = (kb_lo + kb) * BK;
+          for (int i = 0; i < S; ++i) {
+            tma_load_3d(smem_u32(sa + i * A_TILE), &tmap_a, full, k0, (int)(rb * BM), i * 2 + p);
+            tma_load_3d(smem_u32(sb + i * B_TILE), &tmap_b, full, k0, (int)(cb * BN), i * 2 + p);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    // MMA issuer (one lane)
-    if (lane == 0) {
-      for (int it = 0; it < nk; ++it) {
-        const int st = it % STAGES;
-        const uint32_t ph = (uint32_t)(it / STAGES) & 1u;
-        mbar_wait(smem_u32(&bars[st]), ph);
+    {  // MMA issuer: the whole warp, one elected lane issues
+      uint32_t it = 0, t = 0;
+      for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+        size_t cb, rb;
+        int p, kb_lo, nk;
+        tile_coords(tile, cb, p, rb, kb_lo, nk);
+        mbar_wait(smem_u32(tempty_b), (t & 1u) ^ 1u);  // epilogue drained the accumulators
         tc_fence_after();
-        const uint32_t sa = smem_u32(smem + st * STAGE_BYTES);
-        const uint32_t sb = sa + S * A_TILE;
-#pragma unroll 1
-        for (int i = 0; i < S; ++i) {
-#pragma unroll 1
-          for (int j = 0; i + j < S; ++j) {
-            const uint32_t d_tmem = tmem + (uint32_t)((i + j) * BN);
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const uint32_t st = it % STAGES, ph = (it / STAGES) & 1u;
+          mbar_wait(smem_u32(&full_b[st]), ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + st * STAGE_BYTES);
+          const uint64_t ad0 = smem_desc(sa), bd0 = smem_desc(sa + S * A_TILE);
+          const uint32_t first = kb == 0 ? 0u : 1u;
+          // fully unrolled: each MMA is a descriptor add and the UTCIMMA
 #pragma unroll
-            for (int ks = 0; ks < BK / 32; ++ks) {
-              const uint64_t ad = sw64_desc(sa + i * A_TILE + ks * 32);
-              const uint64_t bd = sw64_desc(sb + j * B_TILE + ks * 32);
-              const uint32_t acc = (it > 0 || ks > 0 || i > 0) ? 1u : 0u;
-              tc_mma_i8(d_tmem, ad, bd, IDESC, acc);
+          for (int i = 0; i < S; ++i) {
+#pragma unroll
+            for (int j = 0; i + j < S; ++j) {
+#pragma unroll
+              for (int ks = 0; ks < BK / 32; ++ks) {
+                const uint64_t ad = ad0 + (uint64_t)((i * A_TILE + ks * 32) >> 4);
+                const uint64_t bd = bd0 + (uint64_t)((j * B_TILE + ks * 32) >> 4);
+                tc_mma_i8(tmem + (uint32_t)((i + j) * BN), ad, bd, IDESC,
+                          (ks > 0 || i > 0) ? 1u : first);
+              }
             }
           }
+          tc_commit_elect(smem_u32(&empty_b[st]));  // frees the stage when these MMAs retire
         }
-        tc_commit(smem_u32(&bars[2 + st]));  // frees the stage when these MMAs retire
+        tc_commit_elect(smem_u32(tfull_b));  // accumulators complete
       }
-      tc_commit(smem_u32(&bars[4]));  // accumulators complete
     }
   } else {
     // epilogue: warp w reads TMEM lanes 32 (w % 4) .. +32 (one output row per thread)
     const int q = warp & 3;
     const int row = q * 32 + lane;
-    const size_t arow_idx = (size_t)p * r + rb * BM + row;
-    const size_t k = 2 * (rb * BM + row) + p;  // output row (interleaved parities)
-    mbar_wait(smem_u32(&bars[4]), 0);
-    tc_fence_after();
-    const double ascale = arow[arow_idx];
-#pragma unroll 1
-    for (int h = 0; h < BN / 32; ++h) {
-      double acc[32];
+    uint32_t t = 0;
+    for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+      size_t cb, rb;
+      int p, kb_lo, nk;
+      tile_coords(tile, cb, p, rb, kb_lo, nk);
+      mbar_wait(smem_u32(tfull_b), t & 1u);
+      tc_fence_after();
+      double acc[BN];
 #pragma unroll
-      for (int c = 0; c < 32; ++c) acc[c] = 0.0;
+      for (int c = 0; c < BN; ++c) acc[c] = 0.0;
       // least significant accumulator first
 #pragma unroll 1
       for (int d = S - 1; d >= 0; --d) {
-        uint32_t v[32];
-        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * BN + h * 32), v);
         const double w = ldexp(1.0, -7 * (d + 2));
 #pragma unroll
-        for (int c = 0; c < 32; ++c) acc[c] = fma((double)(int)v[c], w, acc[c]);
-      }
+        for (int h = 0; h < BN / 32; ++h) {
+          uint32_t v[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * BN + h * 32), v);
 #pragma unroll
-      for (int c = 0; c < 32; ++c) {
-        const size_t col = cb * BN + h * 32 + c;
+          for (int c = 0; c < 32; ++c) acc[h * 32 + c] = fma((double)(int)v[c], w, acc[h * 32 + c]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive(smem_u32(tempty_b));  // TMEM free for the next tile
+      const double ascale = arow[(size_t)p * r + rb * BM + row];
+      const size_t k = 2 * (rb * BM + row) + p;  // output row (interleaved parities)
+#pragma unroll
+      for (int c = 0; c < BN; ++c) {
+        const size_t col = cb * BN + c;
         if (col < cols) out[col * ld + k] = (acc[c] * ascale) * bcol[(size_t)p * cols + col];
       }
     }
-    tc_fence_before();
   }
   __syncthreads();
   if (warp == 1) {
@@ -424,7 +482,8 @@ CUtensorMap make_map(const int8_t* base, size_t k, size_t rows, size_t z, int bo
   cuuint32_t estr[3] = {1, 1, 1};
   const CUresult res = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)base, dims,
                                    strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                                   CU_TENSOR_MAP_SWIZZLE_64B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                   oz::BK == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B,
+                                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (res != CUDA_SUCCESS) fail(FL_CUDA_ERROR, "l2c_ozaki: tensor map encode failed");
   return m;
@@ -476,8 +535,9 @@ void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t co
   }();
   (void)attr;
   const size_t tiles = 2 * (r / oz::BM) * ((cols + oz::BN - 1) / oz::BN);
-  oz_gemm_kernel<<<(unsigned)tiles, oz::THREADS, oz::SMEM, st>>>(p.tmap_a, tmap_b, p.arow, bcol,
-                                                                  out, r, cols, ld, p.transpose);
+  const unsigned grid = (unsigned)std::min<size_t>(tiles, (size_t)sm_count());
+  oz_gemm_kernel<<<grid, oz::THREADS, oz::SMEM, st>>>(p.tmap_a, tmap_b, p.arow, bcol, out, r,
+                                                       cols, ld, p.transpose, tiles);
   note_launch("oz_gemm_kernel");
   cudaFreeAsync(b, st);
   cudaFreeAsync(bcol, st);
