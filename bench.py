@@ -32,6 +32,9 @@ sys.path.insert(0, ROOT)
 
 MEASURED = os.path.join(ROOT, "MEASURED_PEAKS.json")
 FP64_PEAK_TFLOPS = 37.0  # tools/fp64_peak.cu on this pool's B200 (profiles/r01_fp64_peak.log): DMMA 37.0, DFMA 33.7
+DFMA_PEAK_TFLOPS = 33.7  # fp64 CUDA-core FMA peak (same log): the NDCT's FFT arithmetic runs there
+INT8_PEAK_TOPS = 4450.0  # tools/tc_i8_peak.cu: tcgen05 kind::i8 M=128 N=256, dense (profiles/r01_tc_i8_peak.log)
+INT8_N64_CAP_TOPS = 2849.0  # same, N=64 tiles (the split GEMM's shape): shared-memory operand bound
 
 CONFIGS = {
     # name: (N, total columns, generator, description)
@@ -296,8 +299,9 @@ def main() -> None:
         torch.cuda.synchronize()
         return a.elapsed_time(b) / reps
 
-    ms_l2c = timed(lambda: _lib.check(_lib.LIB.fl_leg2cheb(0, n, vp(lam.data_ptr()), n, vp(x.data_ptr()),
-                                                           vp(chat.data_ptr()), cols, n, sp)))
+    # the plan's conversion step exactly as fl_dlt runs it (split-int8 tcgen05 GEMM)
+    ms_l2c = timed(lambda: _lib.check(_lib.LIB.fl_plan_leg2cheb(cfg.handle, 0, vp(x.data_ptr()),
+                                                                vp(chat.data_ptr()), cols, n, sp)))
     ms_ndct = timed(lambda: _lib.check(_lib.LIB.fl_ndct(0, fl.GridKind.cheb1, n, L1, vp(d1.data_ptr()),
                                                         vp(chat.data_ptr()), vp(y.data_ptr()), cols, n, sp)))
     ms_dct = timed(lambda: _lib.check(_lib.LIB.fl_trig(0, fl.GridKind.cheb1, n, vp(x.data_ptr()),
@@ -305,18 +309,24 @@ def main() -> None:
     coef = n * cols
     l2c_flops = coef * (n / 2.0)                   # N^2/4 MACs per column = N/2 flop per coefficient
     ndct_flops = coef * L1 * (2.5 * math.log2(n) + 3)  # L (2.5 log2 N + 3)
-    dom = "leg2cheb_mma_kernel" if ms_l2c >= ms_ndct else "fast_ndct_fwd_kernel"
-    achieved = (l2c_flops / (ms_l2c / 1e3) if dom == "leg2cheb_mma_kernel" else ndct_flops / (ms_ndct / 1e3)) / 1e12
+    # int8 tensor work of the split product: 36 digit pairs x the 128-row-blocked
+    # triangle (K from the diagonal block), 2 ops per MAC, both parities
+    r_rows = n // 2
+    rbs = r_rows // 128
+    tri_macs = sum((r_rows - 128 * rb) * 128 for rb in range(rbs)) * 2 * cols
+    i8_ops = 36 * 2 * tri_macs
+    gemm_mode = cfg.gemm_mode()
+    dom = "fast_ndct_fwd_kernel" if ms_ndct >= ms_l2c else "oz_gemm_kernel"
+    achieved = ndct_flops / (ms_ndct / 1e3) / 1e12
     hbm_peak = json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else 6650.0
-    # DRAM traffic of the dominant kernel per launch, from the committed ncu
+    # DRAM traffic of the NDCT kernel per launch, from the committed ncu
     # --set full capture (profiles/ncu_traffic.json: bytes per coefficient)
     traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         tj = json.load(open(tfile))
         for name, rec in tj.items():
-            if name.startswith(dom.split("<")[0]) and f"<{int(math.log2(n))}>" in name or (
-                    dom.startswith("leg2cheb") and name.startswith("leg2cheb_mma_kernel<0>")):
+            if name.startswith("fast_ndct_fwd_kernel") and f"<{int(math.log2(n))}>" in name:
                 traffic = {"bytes_per_launch": rec["dram_bytes_per_coef"] * coef,
                            "bytes_per_coef": rec["dram_bytes_per_coef"],
                            "algorithmic_bytes_per_coef": 16.0, "source": rec["capture"]}
@@ -360,15 +370,25 @@ def main() -> None:
                        "grid": "chebstar (default TransformConfig), NDCT evaluated about cheb1 (fast mode)",
                        "parallelism": f"column shards x{world}, no collective",
                        "l2": "inputs (2 GiB) larger than L2 (126 MB); no flush"},
-            "roofline": {"bound": "fp64", "kernel": dom, "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-                         "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": traffic,
-                         "peak_source": "measured DMMA/DFMA peak, tools/fp64_peak.cu (profiles/r01_fp64_peak.log)",
-                         "algorithmic": "leg2cheb N/2 flop/coef; NDCT L(2.5 log2N + 3) flop/coef"},
+            "roofline": {"bound": "fp64", "kernel": "fast_ndct_fwd_kernel", "dominant": dom,
+                         "achieved": achieved, "peak": DFMA_PEAK_TFLOPS,
+                         "unit": "TFLOP/s", "frac": achieved / DFMA_PEAK_TFLOPS, "traffic": traffic,
+                         "peak_source": "measured DFMA (fp64 CUDA-core) peak, tools/fp64_peak.cu (profiles/r01_fp64_peak.log)",
+                         "algorithmic": "NDCT L(2.5 log2N + 3) flop/coef, L = 17 (cheb1, 2^-52)"},
+            "roofline_tensor": {"bound": "tensor", "kernel": "oz_split_b_kernel + oz_gemm_kernel",
+                                "gemm_mode": "int8_split" if gemm_mode == fl.GEMM_INT8_SPLIT else "fp64",
+                                "achieved": i8_ops / (ms_l2c / 1e3) / 1e12, "peak": INT8_PEAK_TOPS,
+                                "unit": "TOP/s int8", "frac": i8_ops / (ms_l2c / 1e3) / 1e12 / INT8_PEAK_TOPS,
+                                "tile_cap": INT8_N64_CAP_TOPS,
+                                "fp64_equivalent_tflops": l2c_flops / (ms_l2c / 1e3) / 1e12,
+                                "peak_source": "tools/tc_i8_peak.cu (profiles/r01_tc_i8_peak.log)",
+                                "algorithmic": "36 digit pairs x blocked triangle, 2 ops/MAC; fp64-equivalent N/2 flop/coef"},
             "roofline_hbm": {"bound": "hbm", "achieved": 16.0 * value / 1e9, "peak": hbm_peak, "unit": "GB/s",
                              "frac": 16.0 * value / 1e9 / hbm_peak,
                              "note": "16 B/coef algorithmic (one fp64 read + one write), whole DLT",
                              "dct_pass_gbs": dct_gbs, "dct_pass_frac": dct_gbs / hbm_peak},
-            "kernels_ms": {"leg2cheb": ms_l2c, "ndct": ms_ndct, "dct_iii_pass": ms_dct, "dlt_step": ms},
+            "kernels_ms": {"leg2cheb_split_int8": ms_l2c, "ndct": ms_ndct, "dct_iii_pass": ms_dct,
+                           "dlt_step": ms},
             "e2e": {"value": n * total / (e2e_ms / 1e3), "unit": "coeffs/s",
                     "h2d_bytes_per_step": int(8 * n * cols), "d2h_bytes_per_step": int(8 * n * cols)},
             "gpu_launches": launches,

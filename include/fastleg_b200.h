@@ -164,6 +164,13 @@ enum { FL_GEMM_FP64 = 0, FL_GEMM_INT8_SPLIT = 1 };
 fl_status fl_plan_set_gemm_mode(fl_plan* plan, int mode);
 int fl_plan_gemm_mode(const fl_plan* plan);
 
+/* The plan's conversion step alone, exactly as dlt/idlt run it (same
+ * leg2cheb / gemm mode selection): out = M in (transpose = 0, the first step
+ * of transforms.hpp:47) or (m + 1/2) M^T in (transpose = 1, the last step of
+ * transforms.hpp:62). Host or device pointers, columns of stride ld. */
+fl_status fl_plan_leg2cheb(const fl_plan* plan, int transpose, const double* in, double* out,
+                           size_t batch, size_t ld, void* stream);
+
 /* Term-parallel pieces of dlt / idlt (multi-GPU extension for one large
  * vector, C5). Both stages of fl_dlt are sums of independent terms, so P
  * ranks each take a slice and one collective sums the partials

@@ -350,6 +350,25 @@ const L2COzaki* plan_ozaki(fl_plan* p, int transpose, size_t batch, cudaStream_t
   return p->oz[transpose];
 }
 
+// The plan's conversion product (transforms.hpp:47 / :62): chat = M in, or
+// (m + 1/2) M^T in for the inverse; device columns of stride n.
+void plan_convert(fl_plan* p, int transpose, const double* in, double* out, size_t batch,
+                  size_t ld_out, cudaStream_t s) {
+  const size_t n = p->n;
+  if (p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)
+    l2c_fast_apply(*p->l2c, transpose, in, out, batch, ld_out, transpose, s);
+  else if (const L2COzaki* oz = plan_ozaki(p, transpose, batch, s))
+    l2c_ozaki_apply(*oz, in, out, batch, ld_out, s);
+  else if (ld_out == n)
+    leg2cheb_direct(transpose, n, p->s, in, out, batch, n, transpose, s);
+  else {
+    DevScratch<double> t(n * batch, s);
+    leg2cheb_direct(transpose, n, p->s, in, t.p, batch, n, transpose, s);
+    FLB_CUDA(cudaMemcpy2DAsync(out, ld_out * 8, t.p, n * 8, n * 8, batch,
+                               cudaMemcpyDeviceToDevice, s));
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -677,6 +696,31 @@ fl_status fl_plan_set_leg2cheb_mode(fl_plan* p, int mode) {
   });
 }
 
+fl_status fl_plan_leg2cheb(const fl_plan* p, int transpose, const double* in, double* out,
+                           size_t batch, size_t ld, void* stream) {
+  return guarded([&] {
+    if (!p) fail(FL_INVALID_ARGUMENT, "plan: null");
+    const size_t n = p->n;
+    if (batch == 0) return;
+    if (batch == 1) ld = n;
+    check_ld(n, ld, batch);
+    FLB_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = as_stream(stream);
+    DevIn i(in, n, batch, ld, s);
+    DevOut o(out, n, batch, ld, s);
+    const double* cin = i.ptr;
+    DevScratch<double> packed(i.ld != n ? n * batch : 0, s);
+    if (i.ld != n) {
+      FLB_CUDA(cudaMemcpy2DAsync(packed.p, n * 8, i.ptr, i.ld * 8, n * 8, batch,
+                                 cudaMemcpyDeviceToDevice, s));
+      cin = packed.p;
+    }
+    plan_convert(const_cast<fl_plan*>(p), transpose ? 1 : 0, cin, o.ptr, batch, o.ld, s);
+    o.finish();
+    sync(s);
+  });
+}
+
 fl_status fl_plan_set_gemm_mode(fl_plan* p, int mode) {
   return guarded([&] {
     if (!p) fail(FL_INVALID_ARGUMENT, "plan: null");
@@ -714,13 +758,7 @@ fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, 
                                  cudaMemcpyDeviceToDevice, s));
       cin = packed.p;
     }
-    fl_plan* mp = const_cast<fl_plan*>(p);
-    if (p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)
-      l2c_fast_apply(*p->l2c, 0, cin, chat.p, batch, n, 0, s);
-    else if (const L2COzaki* oz = plan_ozaki(mp, 0, batch, s))
-      l2c_ozaki_apply(*oz, cin, chat.p, batch, n, s);
-    else
-      leg2cheb_direct(0, n, p->s, cin, chat.p, batch, n, 0, s);
+    plan_convert(const_cast<fl_plan*>(p), 0, cin, chat.p, batch, n, s);
     const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
     if (o.ld != n) {
       DevScratch<double> f(n * batch, s);
@@ -761,13 +799,7 @@ fl_status fl_idlt(const fl_plan* p, const double* in, double* out, size_t batch,
       run_ndct("ndct_apply_transpose", 1, p->kind, n, p->num_terms, p->delta, i.ptr, n, back.p,
                n, batch, p->w, fast, s);
     }
-    fl_plan* mp = const_cast<fl_plan*>(p);
-    if (p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)
-      l2c_fast_apply(*p->l2c, 1, back.p, o.ptr, batch, o.ld, 1, s);
-    else if (const L2COzaki* oz = plan_ozaki(mp, 1, batch, s))
-      l2c_ozaki_apply(*oz, back.p, o.ptr, batch, o.ld, s);
-    else
-      leg2cheb_direct(1, n, p->s, back.p, o.ptr, batch, o.ld, 1, s);
+    plan_convert(const_cast<fl_plan*>(p), 1, back.p, o.ptr, batch, o.ld, s);
     o.finish();
     sync(s);
   });

@@ -2,8 +2,9 @@
 # Round evidence on one B200 (run under gpurun from the repo root):
 #   1. the bench line (plain run, no profiler)             -> gpurun_out/bench.json
 #   2. the launch list of the same command (cold, serial)  -> gpurun_out/launches.csv
-#   3. ncu --set full of the two hot kernels at a reduced column count
-#      (same kernels, same N; replay cost bounded)         -> gpurun_out/{ndct,l2c}_full.ncu-rep
+#   3. ncu --set full of the hot kernels of one DLT (split_b, split-int8 GEMM,
+#      NDCT) at a reduced column count (same kernels, same N; replay cost
+#      bounded)                                           -> gpurun_out/hot_full.ncu-rep
 set -u
 mkdir -p gpurun_out
 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
@@ -13,8 +14,7 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline \
     > gpurun_out/ncu_launches.log 2>&1
 echo "launch list rc=$?"
-python tools/bench_kernels.py --cols 8192 --reps 1 --only ndct,l2c > gpurun_out/kern_small.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:"fast_ndct_fwd|leg2cheb_mma" -s 1 -c 3 \
-    -o gpurun_out/hot_full python tools/bench_kernels.py --cols 8192 --reps 1 --only ndct,l2c \
-    > gpurun_out/ncu_full.log 2>&1
+python tools/dbg_oz2.py 4096 8192 > gpurun_out/kern_small.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:"fast_ndct_fwd|oz_gemm|oz_split_b" -s 3 -c 3 \
+    -o gpurun_out/hot_full python tools/dbg_oz2.py 4096 8192 > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"

@@ -1,0 +1,110 @@
+// int8 tcgen05 MMA throughput microbenchmark (development tool): one CTA per
+// SM issues back-to-back tcgen05.mma.cta_group::1.kind::i8 (M = 128, K = 32,
+// N = 64 / 128 / 256) from resident SWIZZLE_64B smem tiles into TMEM, no
+// loads, no epilogue. Reports dense int8 TOP/s, i.e. the tensor roofline of
+// the split conversion product (l2c_ozaki.cu) for each tile width.
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/tc_i8_peak tools/tc_i8_peak.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ uint64_t desc64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | (1ull << 16) | (32ull << 32) | (1ull << 46) |
+         (4ull << 61);
+}
+
+template <int N>
+__global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long long* cycles) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t holder;
+  // A: 8 tiles of 128 x 64 B, B: 8 tiles of N x 64 B (zeros)
+  const int bytes = 8 * (128 * 64) + 8 * (N * 64);
+  for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&holder)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = holder;
+  constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+  constexpr int NACC = 512 / N;  // accumulators that fit
+  unsigned long long t0 = clock64();
+  if (warp == 0) {
+    const uint64_t ad0 = desc64(smem_u32(smem)), bd0 = desc64(smem_u32(smem + 8 * 128 * 64));
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int m = 0; m < 72; ++m) {
+        const int i = m % 8, j = (m / 8) % 8, ks = m & 1;
+        const uint64_t ad = ad0 + (uint64_t)((i * 128 * 64 + ks * 32) >> 4);
+        const uint64_t bd = bd0 + (uint64_t)((j * N * 64 + ks * 32) >> 4);
+        const uint32_t d = tmem + (uint32_t)((m % NACC) * N);
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d),
+            "l"(ad), "l"(bd), "r"(idesc), "r"(1u));
+      }
+      asm volatile(
+          "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+              smem_u32(&bar)));
+      // wait for this batch (keeps <= 72 MMAs in flight, like one pipeline stage)
+      asm volatile(
+          "{\n\t.reg .pred P1;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@P1 bra D_%=;\n\tbra W_%=;\nD_%=:\n\t}" ::"r"(
+              smem_u32(&bar)), "r"((uint32_t)(it & 1)));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = clock64() - t0;
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <int N>
+void run(int sms) {
+  const int smem = 8 * 128 * 64 + 8 * N * 64 + 1024;
+  cudaFuncSetAttribute(peak_kernel<N>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  unsigned long long* cyc;
+  cudaMalloc(&cyc, sms * 8);
+  const int iters = 2000;
+  peak_kernel<N><<<sms, 128, smem>>>(10, cyc);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  peak_kernel<N><<<sms, 128, smem>>>(iters, cyc);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  const cudaError_t e = cudaGetLastError();
+  const double macs = (double)sms * iters * 72 * 128.0 * N * 32.0;
+  std::printf("N=%3d: %s  %.3f ms  %.1f TOP/s int8 dense (%.0f MAC/clk/SM at 1.92 GHz)\n", N,
+              cudaGetErrorString(e), ms, 2 * macs / (ms * 1e-3) / 1e12,
+              macs / sms / (ms * 1e-3) / 1.92e9);
+  cudaFree(cyc);
+}
+
+int main() {
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  run<64>(sms);
+  run<128>(sms);
+  run<256>(sms);
+  return 0;
+}
