@@ -5,6 +5,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <new>
 #include <random>
@@ -256,8 +257,27 @@ bool any_nonfinite(const double* v, size_t n, size_t batch, size_t ld, const dou
   return h != 0;
 }
 
-// Runs an NDCT (literal kind, or the fast cheb1 path) with the reference's
-// validation order: non-finite (invalid_argument) before overflow.
+// Enqueues an NDCT (literal kind, or the fast cheb1 path); non-finite inputs
+// raise *flag (device int, zeroed by the caller). Callers check
+// overflow_guard first.
+void enqueue_ndct(int transpose, int kind, size_t n, int num_terms, const double* delta,
+                  const double* in, size_t ld_in, double* out, size_t ld_out, size_t batch,
+                  const double* in_mult, const FastNdct* fast, int* flag, cudaStream_t s) {
+  if (num_terms <= 0) {
+    FLB_CUDA(cudaMemset2DAsync(out, ld_out * sizeof(double), 0, n * sizeof(double), batch, s));
+    nonfinite_kernel<<<sm_count() * 4, 256, 0, s>>>(in, n, batch, ld_in, in_mult, flag);
+    note_launch("nonfinite_kernel");
+  } else if (fast) {
+    fast_ndct_run(*fast, transpose, in, ld_in, out, ld_out, batch, in_mult, flag, s);
+  } else {
+    if (ld_in != ld_out && batch > 1)
+      fail(FL_RUNTIME_ERROR, "ndct: mismatched strides");  // internal: callers pass equal ld
+    czt_ndct(transpose, kind, n, num_terms, delta, in, out, batch, ld_in, in_mult, flag, s);
+  }
+}
+
+// Runs an NDCT with the reference's validation order: non-finite
+// (invalid_argument) before overflow.
 void run_ndct(const char* where, int transpose, int kind, size_t n, int num_terms,
               const double* delta, const double* in, size_t ld_in, double* out, size_t ld_out,
               size_t batch, const double* in_mult, const FastNdct* fast, cudaStream_t s) {
@@ -268,21 +288,97 @@ void run_ndct(const char* where, int transpose, int kind, size_t n, int num_term
   }
   DevScratch<int> flag(1, s);
   FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
-  if (num_terms <= 0) {
-    FLB_CUDA(cudaMemset2DAsync(out, ld_out * sizeof(double), 0, n * sizeof(double), batch, s));
-    nonfinite_kernel<<<sm_count() * 4, 256, 0, s>>>(in, n, batch, ld_in, in_mult, flag.p);
-    note_launch("nonfinite_kernel");
-  } else if (fast) {
-    fast_ndct_run(*fast, transpose, in, ld_in, out, ld_out, batch, in_mult, flag.p, s);
-  } else {
-    if (ld_in != ld_out && batch > 1)
-      fail(FL_RUNTIME_ERROR, "ndct: mismatched strides");  // internal: callers pass equal ld
-    czt_ndct(transpose, kind, n, num_terms, delta, in, out, batch, ld_in, in_mult, flag.p, s);
-  }
+  enqueue_ndct(transpose, kind, n, num_terms, delta, in, ld_in, out, ld_out, batch, in_mult, fast,
+               flag.p, s);
   int h = 0;
   FLB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
   sync(s);
   if (h) fail(FL_INVALID_ARGUMENT, std::string(where) + ": non-finite input");
+}
+
+// ---- host-buffer pipeline ------------------------------------------------
+// A transform of host columns (host in, host out) is cut into column chunks
+// that flow through three streams -- H2D copy | compute | D2H copy -- with three
+// device buffer sets, so both PCIe directions and the kernels overlap. The
+// non-finite flags of all chunks are checked once at the end.
+struct PipeStreams {
+  cudaStream_t h2d, comp, d2h;
+};
+
+const PipeStreams& pipe_streams(int dev) {
+  static std::mutex mu;
+  static std::map<int, PipeStreams> per_dev;
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = per_dev.find(dev);
+  if (it == per_dev.end()) {
+    PipeStreams ps;
+    FLB_CUDA(cudaStreamCreateWithFlags(&ps.h2d, cudaStreamNonBlocking));
+    FLB_CUDA(cudaStreamCreateWithFlags(&ps.comp, cudaStreamNonBlocking));
+    FLB_CUDA(cudaStreamCreateWithFlags(&ps.d2h, cudaStreamNonBlocking));
+    it = per_dev.emplace(dev, ps).first;
+  }
+  return it->second;
+}
+
+#ifndef FLB_PIPE_CHUNKS
+#define FLB_PIPE_CHUNKS 32
+#endif
+constexpr size_t kPipeMinBytes = size_t(64) << 20;  // below this one copy each way is as fast
+
+bool pipeline_ok(const double* in, const double* out, size_t n, size_t batch) {
+  return out != nullptr && !is_device_ptr(in) && !is_device_ptr(out) && batch >= 8 &&
+         n * batch * sizeof(double) >= kPipeMinBytes;
+}
+
+// compute(din, dout, cols, flag, stream): device columns of stride n.
+template <class F>
+void run_pipelined(int dev, size_t n, const double* in, double* out, size_t batch, size_t ld,
+                   cudaStream_t user, const char* where, F&& compute) {
+  constexpr int NB = 3;  // buffer sets: H2D of chunk i + 3 waits for the D2H of chunk i
+  const PipeStreams& ps = pipe_streams(dev);
+  const size_t chunks = std::max<size_t>(1, std::min<size_t>(FLB_PIPE_CHUNKS, batch / 256));
+  const size_t per = (batch + chunks - 1) / chunks;
+  DevScratch<double> din(NB * per * n, user), dout(NB * per * n, user);
+  DevScratch<int> flags(chunks, user);
+  FLB_CUDA(cudaMemsetAsync(flags.p, 0, chunks * sizeof(int), user));
+  cudaEvent_t start, h2d[NB], comp[NB], d2h[NB];
+  FLB_CUDA(cudaEventCreateWithFlags(&start, cudaEventDisableTiming));
+  for (int b = 0; b < NB; ++b)
+    for (cudaEvent_t* e : {&h2d[b], &comp[b], &d2h[b]})
+      FLB_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+  FLB_CUDA(cudaEventRecord(start, user));  // buffers allocated / flags zeroed on `user`
+  for (cudaStream_t st : {ps.h2d, ps.comp, ps.d2h}) FLB_CUDA(cudaStreamWaitEvent(st, start, 0));
+  for (size_t i = 0; i < chunks; ++i) {
+    const size_t c0 = i * per;
+    if (c0 >= batch) break;
+    const size_t cols = std::min(per, batch - c0);
+    const int b = (int)(i % NB);
+    double* di = din.p + b * per * n;
+    double* dq = dout.p + b * per * n;
+    if (i >= (size_t)NB) FLB_CUDA(cudaStreamWaitEvent(ps.h2d, d2h[b], 0));
+    FLB_CUDA(cudaMemcpy2DAsync(di, n * 8, in + c0 * ld, ld * 8, n * 8, cols,
+                               cudaMemcpyHostToDevice, ps.h2d));
+    FLB_CUDA(cudaEventRecord(h2d[b], ps.h2d));
+    FLB_CUDA(cudaStreamWaitEvent(ps.comp, h2d[b], 0));
+    compute(di, dq, cols, flags.p + i, ps.comp);
+    FLB_CUDA(cudaEventRecord(comp[b], ps.comp));
+    FLB_CUDA(cudaStreamWaitEvent(ps.d2h, comp[b], 0));
+    FLB_CUDA(cudaMemcpy2DAsync(out + c0 * ld, ld * 8, dq, n * 8, n * 8, cols,
+                               cudaMemcpyDeviceToHost, ps.d2h));
+    FLB_CUDA(cudaEventRecord(d2h[b], ps.d2h));
+  }
+  std::vector<int> h(chunks, 0);
+  FLB_CUDA(cudaStreamSynchronize(ps.comp));
+  FLB_CUDA(cudaStreamSynchronize(ps.d2h));
+  FLB_CUDA(cudaStreamSynchronize(ps.h2d));
+  // the scratch frees below are ordered on `user`: make it follow the pipeline
+  FLB_CUDA(cudaMemcpyAsync(h.data(), flags.p, chunks * sizeof(int), cudaMemcpyDeviceToHost, user));
+  sync(user);
+  cudaEventDestroy(start);
+  for (int b = 0; b < NB; ++b)
+    for (cudaEvent_t e : {h2d[b], comp[b], d2h[b]}) cudaEventDestroy(e);
+  for (int v : h)
+    if (v) fail(FL_INVALID_ARGUMENT, std::string(where) + ": non-finite input");
 }
 
 }  // namespace
@@ -746,6 +842,18 @@ fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, 
     check_ld(n, ld, batch);
     FLB_CUDA(cudaSetDevice(p->device));
     cudaStream_t s = as_stream(stream);
+    const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
+    fl_plan* mp = const_cast<fl_plan*>(p);
+    if (pipeline_ok(in, out, n, batch) && !overflow_guard(n, p->num_terms)) {
+      run_pipelined(p->device, n, in, out, batch, ld, s, "ndct_apply",
+                    [&](const double* di, double* dq, size_t cols, int* flag, cudaStream_t cs) {
+                      DevScratch<double> chat(n * cols, cs);
+                      plan_convert(mp, 0, di, chat.p, cols, n, cs);
+                      enqueue_ndct(0, p->kind, n, p->num_terms, p->delta, chat.p, n, dq, n, cols,
+                                   nullptr, fast, flag, cs);
+                    });
+      return;
+    }
     DevIn i(in, n, batch, ld, s);
     DevOut o(out, n, batch, ld, s);
     if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
@@ -758,8 +866,7 @@ fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, 
                                  cudaMemcpyDeviceToDevice, s));
       cin = packed.p;
     }
-    plan_convert(const_cast<fl_plan*>(p), 0, cin, chat.p, batch, n, s);
-    const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
+    plan_convert(mp, 0, cin, chat.p, batch, n, s);
     if (o.ld != n) {
       DevScratch<double> f(n * batch, s);
       run_ndct("ndct_apply", 0, p->kind, n, p->num_terms, p->delta, chat.p, n, f.p, n, batch,
@@ -784,11 +891,22 @@ fl_status fl_idlt(const fl_plan* p, const double* in, double* out, size_t batch,
     check_ld(n, ld, batch);
     FLB_CUDA(cudaSetDevice(p->device));
     cudaStream_t s = as_stream(stream);
+    const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
+    fl_plan* mp = const_cast<fl_plan*>(p);
+    if (pipeline_ok(in, out, n, batch) && !overflow_guard(n, p->num_terms)) {
+      run_pipelined(p->device, n, in, out, batch, ld, s, "ndct_apply_transpose",
+                    [&](const double* di, double* dq, size_t cols, int* flag, cudaStream_t cs) {
+                      DevScratch<double> back(n * cols, cs);
+                      enqueue_ndct(1, p->kind, n, p->num_terms, p->delta, di, n, back.p, n, cols,
+                                   p->w, fast, flag, cs);
+                      plan_convert(mp, 1, back.p, dq, cols, n, cs);
+                    });
+      return;
+    }
     DevIn i(in, n, batch, ld, s);
     DevOut o(out, n, batch, ld, s);
     // transforms.hpp:58-62: back = NDCT^T(w . f); c = (m + 1/2) M^T back
     DevScratch<double> back(n * batch, s);
-    const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
     if (i.ld != n) {
       DevScratch<double> f(n * batch, s);
       FLB_CUDA(cudaMemcpy2DAsync(f.p, n * 8, i.ptr, i.ld * 8, n * 8, batch,
@@ -799,7 +917,7 @@ fl_status fl_idlt(const fl_plan* p, const double* in, double* out, size_t batch,
       run_ndct("ndct_apply_transpose", 1, p->kind, n, p->num_terms, p->delta, i.ptr, n, back.p,
                n, batch, p->w, fast, s);
     }
-    plan_convert(const_cast<fl_plan*>(p), 1, back.p, o.ptr, batch, o.ld, s);
+    plan_convert(mp, 1, back.p, o.ptr, batch, o.ld, s);
     o.finish();
     sync(s);
   });
