@@ -178,14 +178,17 @@ __device__ __forceinline__ int split_exp(double mx) {
   return e + 1;
 }
 // Digits of r = x 2^-e (|r| < 1/2): r = sum_j d_j 2^{-7(j+1)} + O(2^{-7S-1}).
+// rint(t) by the 1.5 * 2^52 shifter: t + M rounds to nearest even in the
+// FP64 adder and the integer sits in the low mantissa bits (no F2I).
 __device__ __forceinline__ void split_digits(double x, int e, int8_t (&d)[oz::S]) {
+  constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
   double r = ldexp(x, -e);
 #pragma unroll
   for (int j = 0; j < oz::S; ++j) {
     const double t = r * 128.0;
-    const double q = rint(t);
-    d[j] = (int8_t)(int)q;
-    r = t - q;
+    const double y = t + kShift;
+    d[j] = (int8_t)__double2loint(y);
+    r = t - (y - kShift);
   }
 }
 
@@ -237,31 +240,33 @@ __global__ void __launch_bounds__(256) oz_split_a_kernel(const double* __restric
   }
 }
 
-// One CTA per input column: per-parity scales and the S digit slices,
-// de-interleaved by parity ([S][2][cols][r]). A non-finite column gets a NaN
-// scale so the product column comes out NaN (the NDCT input check reports it).
-__global__ void __launch_bounds__(256) oz_split_b_kernel(const double* __restrict__ in, size_t n,
-                                                         size_t ld, size_t cols,
-                                                         int8_t* __restrict__ b,
-                                                         double* __restrict__ bcol) {
+// One CTA of n/16 threads per input column (each thread one 16-entry chunk,
+// held in registers between the max reduction and the split): per-parity
+// scales and the S digit slices, de-interleaved by parity ([S][2][cols][r]).
+// A non-finite column gets a NaN scale so the product column comes out NaN
+// (the NDCT input check reports it).
+__global__ void __launch_bounds__(1024) oz_split_b_kernel(const double* __restrict__ in, size_t n,
+                                                          size_t ld, size_t cols,
+                                                          int8_t* __restrict__ b,
+                                                          double* __restrict__ bcol) {
   const size_t col = blockIdx.x;
   const size_t r = n / 2;
-  const double* x = in + col * ld;
-  __shared__ double red[2][8];
+  const size_t c = threadIdx.x;  // chunk: entries 16c .. 16c + 15
+  __shared__ double red[2][32];
   __shared__ int e_sh[2];
   __shared__ int bad_sh;
   if (threadIdx.x == 0) bad_sh = 0;
+  const double2* q = reinterpret_cast<const double2*>(in + col * ld + 16 * c);
+  double2 v[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) v[i] = __ldcs(q + i);  // streamed: read once
   double mx0 = 0.0, mx1 = 0.0;
   bool bad = false;
-  for (size_t c = threadIdx.x; c < n / 16; c += blockDim.x) {
-    const double2* q = reinterpret_cast<const double2*>(x + 16 * c);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const double2 v = q[i];
-      bad |= !isfinite(v.x) || !isfinite(v.y);
-      mx0 = fmax(mx0, fabs(v.x));
-      mx1 = fmax(mx1, fabs(v.y));
-    }
+  for (int i = 0; i < 8; ++i) {
+    bad |= !isfinite(v[i].x) || !isfinite(v[i].y);
+    mx0 = fmax(mx0, fabs(v[i].x));
+    mx1 = fmax(mx1, fabs(v[i].y));
   }
   for (int o = 16; o > 0; o >>= 1) {
     mx0 = fmax(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
@@ -283,28 +288,24 @@ __global__ void __launch_bounds__(256) oz_split_b_kernel(const double* __restric
   }
   __syncthreads();
   const int e0 = e_sh[0], e1 = e_sh[1];
-  for (size_t c = threadIdx.x; c < n / 16; c += blockDim.x) {
-    const double2* q = reinterpret_cast<const double2*>(x + 16 * c);
-    uint64_t w0[oz::S], w1[oz::S];
+  uint64_t w0[oz::S], w1[oz::S];
 #pragma unroll
-    for (int j = 0; j < oz::S; ++j) w0[j] = w1[j] = 0;
+  for (int j = 0; j < oz::S; ++j) w0[j] = w1[j] = 0;
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const double2 v = q[i];
-      int8_t d0[oz::S], d1[oz::S];
-      split_digits(isfinite(v.x) ? v.x : 0.0, e0, d0);
-      split_digits(isfinite(v.y) ? v.y : 0.0, e1, d1);
-#pragma unroll
-      for (int j = 0; j < oz::S; ++j) {
-        w0[j] |= (uint64_t)(uint8_t)d0[j] << (8 * i);
-        w1[j] |= (uint64_t)(uint8_t)d1[j] << (8 * i);
-      }
-    }
+  for (int i = 0; i < 8; ++i) {
+    int8_t d0[oz::S], d1[oz::S];
+    split_digits(isfinite(v[i].x) ? v[i].x : 0.0, e0, d0);
+    split_digits(isfinite(v[i].y) ? v[i].y : 0.0, e1, d1);
 #pragma unroll
     for (int j = 0; j < oz::S; ++j) {
-      *reinterpret_cast<uint64_t*>(b + ((size_t)(j * 2 + 0) * cols + col) * r + 8 * c) = w0[j];
-      *reinterpret_cast<uint64_t*>(b + ((size_t)(j * 2 + 1) * cols + col) * r + 8 * c) = w1[j];
+      w0[j] |= (uint64_t)(uint8_t)d0[j] << (8 * i);
+      w1[j] |= (uint64_t)(uint8_t)d1[j] << (8 * i);
     }
+  }
+#pragma unroll
+  for (int j = 0; j < oz::S; ++j) {
+    *reinterpret_cast<uint64_t*>(b + ((size_t)(j * 2 + 0) * cols + col) * r + 8 * c) = w0[j];
+    *reinterpret_cast<uint64_t*>(b + ((size_t)(j * 2 + 1) * cols + col) * r + 8 * c) = w1[j];
   }
 }
 
@@ -491,7 +492,7 @@ CUtensorMap make_map(const int8_t* base, size_t k, size_t rows, size_t z, int bo
 
 }  // namespace
 
-bool l2c_ozaki_supported(size_t n) { return n % 256 == 0 && n >= 512 && n <= (1u << 16); }
+bool l2c_ozaki_supported(size_t n) { return n % 256 == 0 && n >= 512 && n <= 16384; }
 
 L2COzaki* l2c_ozaki_create(size_t n, const double* s, int transpose, int scale_half,
                            cudaStream_t st) {
@@ -525,7 +526,7 @@ void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t co
   double* bcol = nullptr;
   FLB_CUDA(cudaMallocAsync(&b, (size_t)oz::S * 2 * cols * r, st));
   FLB_CUDA(cudaMallocAsync(&bcol, 2 * cols * sizeof(double), st));
-  oz_split_b_kernel<<<(unsigned)cols, 256, 0, st>>>(in, n, ld, cols, b, bcol);
+  oz_split_b_kernel<<<(unsigned)cols, (unsigned)(n / 16), 0, st>>>(in, n, ld, cols, b, bcol);
   note_launch("oz_split_b_kernel");
   const CUtensorMap tmap_b = make_map(b, r, cols, 2 * oz::S, oz::BN);
   static bool attr = [] {
