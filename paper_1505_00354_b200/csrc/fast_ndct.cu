@@ -56,6 +56,12 @@ struct FastNdct {
   int num_terms = 0;
   const double* delta = nullptr;  // cheb1 perturbations (device)
   double* owned_delta = nullptr;
+  // Chebyshev (Jacobi-Anger) expansion of the same NDCT for the fused kernels
+  // (N <= 8192): bes_terms < num_terms terms, weight / row tables [m][N]
+  int bes_terms = 0;
+  double* bes_wf = nullptr;  // forward weights, owned-row order
+  double* bes_wt = nullptr;  // transpose weights, tr_slot order
+  double* bes_tt = nullptr;  // transpose row factors T_m(n/N), tr_row order
 };
 
 namespace {
@@ -141,16 +147,22 @@ __constant__ double kC8[16][2] = {
 // parities); with NEXT the thread also writes its own two, m and m + P, scaled
 // by n/N into `next` -- the stage of the following term -- so the stage
 // update costs one store per entry and no separate pass.
-template <int N, bool ODD, int R, bool NEXT>
+// NM: 0 = no next stage; 1 = next = x c (Taylor (n/N)^{l+1} c_n, and the
+// Chebyshev T_1); 2 = next = 2 x cur - next (Chebyshev T_{m+1}(x) c_n, the
+// buffer `next` holding T_{m-1}(x) c_n), x = n/N.
+template <int N, bool ODD, int R, int NM>
 __device__ __forceinline__ double2 fwd_pack(const double* stage, double* next, int m, double2 ta_t,
                                             double2 r4_t) {
   constexpr int P = N / 2;
   constexpr double h = 0.70710678118654752440;
   const double s_m = stage[m], s_mp = stage[m + P];
   const double s_nm = stage[(N - m) & (N - 1)], s_pm = stage[P - m];
-  if (NEXT) {
+  if (NM == 1) {
     next[m] = s_m * ((double)m / (double)N);  // (n/N)^{l+1} c_n
     next[m + P] = s_mp * ((double)(m + P) / (double)N);
+  } else if (NM == 2) {
+    next[m] = fma(2.0 * ((double)m / (double)N), s_m, -next[m]);
+    next[m + P] = fma(2.0 * ((double)(m + P) / (double)N), s_mp, -next[m + P]);
   }
   // X_j = a_j / 2 (X_0 = a_0, X_N = 0); a = stage (DCT) or the reversed stage (DST)
   const bool m0 = m == 0;
@@ -172,20 +184,29 @@ __device__ __forceinline__ double2 fwd_pack(const double* stage, double* next, i
   return make_double2(s.x - dr.y, s.y + dr.x);  // s + i dr
 }
 
+// The rows thread t of the forward kernel accumulates: the outputs of its
+// last-pass butterflies (i < OWN).
+template <int LOG2N>
+__device__ __forceinline__ int fwd_own_row(int t, int i) {
+  using C = Cfg<LOG2N>;
+  const int s = i >> 1, q = s / C::RL, r = s % C::RL;
+  return fwd_row_of<C::N>(2 * (t + q * C::T + r * C::NSL) + (i & 1));
+}
+
 // One forward Taylor term (or one plain transform): f[i] += sign p[i] y_{k_i}.
-template <int N, bool ODD, bool NEXT, int R>
+template <int N, bool ODD, int NM, int R>
 __device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, double* next, int t,
                                              double2 ta_t, double2 r4_t) {
   if constexpr (R < 8) {
-    v[R] = fwd_pack<N, ODD, R, NEXT>(stage, next, t + R * (N / 16), ta_t, r4_t);
-    fwd_pack_all<N, ODD, NEXT, R + 1>(v, stage, next, t, ta_t, r4_t);
+    v[R] = fwd_pack<N, ODD, R, NM>(stage, next, t + R * (N / 16), ta_t, r4_t);
+    fwd_pack_all<N, ODD, NM, R + 1>(v, stage, next, t, ta_t, r4_t);
   }
 }
 
 // One forward Taylor term (or one plain transform): f[i] += sign p[i] y_{k_i}.
 // The barrier before the first pass store orders it after the previous
 // term's last-pass reads of zb.
-template <int LOG2N, bool ODD, bool NEXT>
+template <int LOG2N, bool ODD, int NM>
 __device__ __forceinline__ void fwd_term(const double* stage, double* next, double2* zb, int t,
                                          int bar, double2 ta_t, double2 r4_t, const double2* fftw,
                                          const double* p, double* f, double sign) {
@@ -193,7 +214,7 @@ __device__ __forceinline__ void fwd_term(const double* stage, double* next, doub
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, NSL = C::NSL, RL = C::RL;
   static_assert(E == 8 && T == N / 16, "pack twiddle constants assume T = N/16");
   double2 v[E];
-  fwd_pack_all<N, ODD, NEXT, 0>(v, stage, next, t, ta_t, r4_t);
+  fwd_pack_all<N, ODD, NM, 0>(v, stage, next, t, ta_t, r4_t);
   pass_compute<P, E, 8, 1, true>(v, t, fftw);
   group_sync<C::GT>(bar);
   pass_store<P, E, 8, 1>(v, zb, t);
@@ -218,29 +239,28 @@ __device__ __forceinline__ void fwd_term(const double* stage, double* next, doub
     }
 }
 
-// plain_op: -1 = Taylor NDCT with num_terms terms; 0 = one plain DCT-III;
-// 1 = one plain DST-III.
-template <int LOG2N>
+// plain_op: -1 = NDCT with num_terms terms; 0 = one plain DCT-III;
+// 1 = one plain DST-III. BES: Chebyshev (Jacobi-Anger) expansion instead of
+// Taylor -- stage T_m(n/N) c_n by the three-term recurrence, weights
+// wtab[m][i T + t] (sign included) of the thread's owned rows from a table.
+template <int LOG2N, bool BES>
 __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     fast_ndct_fwd_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                          size_t ld_out, size_t batch, const double* __restrict__ delta,
                          int num_terms, int plain_op, const double2* __restrict__ tw4n,
-                         const double2* __restrict__ fftw_g, int* nonfinite) {
+                         const double2* __restrict__ fftw_g, const double* __restrict__ wtab,
+                         int* nonfinite) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, T = C::T, OWN = C::OWN, E = C::E, NSL = C::NSL, RL = C::RL;
   extern __shared__ double smem[];
   double* nd = smem + C::COLS * (C::COL_BYTES / 8);
   double2* fftw_s = reinterpret_cast<double2*>(nd + N);
   const double2* fftw = C::SMEM_TABLES ? fftw_s : fftw_g;
-  // the rows thread t accumulates: the outputs of its last-pass butterflies
-  auto own_row = [](int t, int i) -> int {
-    const int s = i >> 1, q = s / RL, r = s % RL;
-    return fwd_row_of<N>(2 * (t + q * T + r * NSL) + (i & 1));
-  };
+  auto own_row = [](int t, int i) -> int { return fwd_own_row<LOG2N>(t, i); };
   if (C::SMEM_TABLES) {
     // N delta in owned-row order, nd[i T + t] for row own_row(t, i): the
     // per-term weight update reads it conflict-free (row order is stride 4)
-    if (plain_op < 0)
+    if (plain_op < 0 && !BES)
       for (int j = threadIdx.x; j < N; j += blockDim.x)
         nd[j] = (double)N * delta[own_row(j % T, j / T)];
     load_table(fftw_s, fftw_g, C::TW);
@@ -276,9 +296,20 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      fwd_term<LOG2N, true, false>(stage, nullptr, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      fwd_term<LOG2N, true, 0>(stage, nullptr, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
     else
-      fwd_term<LOG2N, false, false>(stage, nullptr, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      fwd_term<LOG2N, false, 0>(stage, nullptr, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+  } else if (BES) {
+    for (int m = 0; m < num_terms; ++m) {
+#pragma unroll
+      for (int i = 0; i < OWN; ++i) p[i] = __ldg(wtab + (size_t)m * N + i * T + t);
+      if (m == 0)
+        fwd_term<LOG2N, false, 1>(stage, stage_odd, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      else if (m & 1)
+        fwd_term<LOG2N, true, 2>(stage_odd, stage, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      else
+        fwd_term<LOG2N, false, 2>(stage, stage_odd, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+    }
   } else {
     for (int l = 0; l < num_terms; ++l) {
       if (l > 0) {
@@ -290,11 +321,11 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
         }
       }
       if (l & 1)
-        fwd_term<LOG2N, true, true>(stage_odd, stage, zb, t, bar, ta_t, r4_t, fftw, p, f,
-                                    taylor_sign_d(l));
+        fwd_term<LOG2N, true, 1>(stage_odd, stage, zb, t, bar, ta_t, r4_t, fftw, p, f,
+                                 taylor_sign_d(l));
       else
-        fwd_term<LOG2N, false, true>(stage, stage_odd, zb, t, bar, ta_t, r4_t, fftw, p, f,
-                                     taylor_sign_d(l));
+        fwd_term<LOG2N, false, 1>(stage, stage_odd, zb, t, bar, ta_t, r4_t, fftw, p, f,
+                                  taylor_sign_d(l));
     }
   }
   // scatter the owned rows through shared memory, then one coalesced store
@@ -339,17 +370,19 @@ __device__ __forceinline__ double tr_unpack(double2 za, double2 zc, double2 tn, 
   return h.x * Vv.x + h.y * Vv.y;
 }
 
-// One transposed Taylor term: o[i] += sign rp[i] X_{tr_row(t, i)}. The pack
-// reads every stage entry exactly once; with NEXT it also writes the next
-// term's stage, h (N delta)/(l+1) = h * nd * inv_next (nd in the tr_slot
-// order), into `next`. The barrier before the first pass store orders it after
-// the previous term's unpack reads of zb.
-template <int LOG2N, bool ODD, bool NEXT>
+// One transposed term: o[i] += sign rp[i] X_{tr_row(t, i)}. The pack reads
+// every stage entry exactly once. PM = 0: the stage as is; PM = 1 (Taylor):
+// it also writes the next term's stage, h (N delta)/(l+1) = h * nd * inv_next
+// (nd in the tr_slot order), into `next`; PM = 2 (Chebyshev): the stage is
+// the input g and each entry is weighted on the fly by wrow[slot] (the
+// term's weights in the tr_slot order). The barrier before the first pass
+// store orders it after the previous term's unpack reads of zb.
+template <int LOG2N, bool ODD, int PM>
 __device__ __forceinline__ void tr_term(const double* hs, double* next, const double* nd,
                                         const double* __restrict__ delta, double inv_next,
-                                        double2* zb, int t, int bar, double2 ta_t, double2 r4_t,
-                                        const double2* fftw, const double* rp, double* o,
-                                        double sign) {
+                                        const double* __restrict__ wrow, double2* zb, int t,
+                                        int bar, double2 ta_t, double2 r4_t, const double2* fftw,
+                                        const double* rp, double* o, double sign) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, OWN = C::OWN;
   static_assert(E == 8 && T == N / 16, "row grouping assumes T = N/16");
@@ -362,8 +395,12 @@ __device__ __forceinline__ void tr_term(const double* hs, double* next, const do
   for (int r = 0; r < E; ++r) {
     const int m = t + r * T;
     const int slot = r < 4 ? 2 * m : P + N - 2 - 2 * m;
-    const double2 w = *reinterpret_cast<const double2*>(hs + slot);
-    if (NEXT) {
+    double2 w = *reinterpret_cast<const double2*>(hs + slot);
+    if (PM == 2) {
+      const double2 q = __ldg(reinterpret_cast<const double2*>(wrow + slot));
+      w = make_double2(w.x * q.x, w.y * q.y);
+    }
+    if (PM == 1) {
       const double2 q = C::SMEM_TABLES
                             ? *reinterpret_cast<const double2*>(nd + slot)
                             : make_double2((double)N * __ldg(&delta[tr_entry<N>(slot)]),
@@ -416,12 +453,16 @@ __device__ __forceinline__ void tr_term(const double* hs, double* next, const do
   }
 }
 
-template <int LOG2N>
+// BES: Chebyshev (Jacobi-Anger) expansion: the stage is the (weighted) input
+// itself, each term weights it on the fly from wtab[m][slot] (tr_slot order)
+// and scales the output rows by ttab[m][i T + t] = T_m(n/N) (tr_row order).
+template <int LOG2N, bool BES>
 __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
     fast_ndct_tr_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                         size_t ld_out, size_t batch, const double* __restrict__ delta,
                         int num_terms, int plain_op, const double* __restrict__ mult,
                         const double2* __restrict__ tw4n, const double2* __restrict__ fftw_g,
+                        const double* __restrict__ wtab, const double* __restrict__ ttab,
                         int* nonfinite) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, T = C::T, OWN = C::OWN;
@@ -430,7 +471,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   double2* fftw_s = reinterpret_cast<double2*>(nd + N);
   const double2* fftw = C::SMEM_TABLES ? fftw_s : fftw_g;
   if (C::SMEM_TABLES) {
-    if (plain_op < 0)  // in the tr_slot layout of the stage
+    if (plain_op < 0 && !BES)  // in the tr_slot layout of the stage
       for (int j = threadIdx.x; j < N; j += blockDim.x) nd[j] = (double)N * delta[tr_entry<N>(j)];
     load_table(fftw_s, fftw_g, C::TW);
     __syncthreads();
@@ -462,9 +503,23 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      tr_term<LOG2N, true, false>(hs, nullptr, nd, delta, 0.0, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
+      tr_term<LOG2N, true, 0>(hs, nullptr, nd, delta, 0.0, nullptr, zb, t, bar, ta_t, r4_t, fftw,
+                              rp, o, 1.0);
     else
-      tr_term<LOG2N, false, false>(hs, nullptr, nd, delta, 0.0, zb, t, bar, ta_t, r4_t, fftw, rp, o, 1.0);
+      tr_term<LOG2N, false, 0>(hs, nullptr, nd, delta, 0.0, nullptr, zb, t, bar, ta_t, r4_t, fftw,
+                               rp, o, 1.0);
+  } else if (BES) {
+    for (int m = 0; m < num_terms; ++m) {
+#pragma unroll
+      for (int i = 0; i < OWN; ++i) rp[i] = __ldg(ttab + (size_t)m * N + i * T + t);
+      const double* wrow = wtab + (size_t)m * N;
+      if (m & 1)
+        tr_term<LOG2N, true, 2>(hs, nullptr, nd, delta, 0.0, wrow, zb, t, bar, ta_t, r4_t, fftw,
+                                rp, o, 1.0);
+      else
+        tr_term<LOG2N, false, 2>(hs, nullptr, nd, delta, 0.0, wrow, zb, t, bar, ta_t, r4_t, fftw,
+                                 rp, o, 1.0);
+    }
   } else {
     for (int l = 0; l < num_terms; ++l) {
       if (l > 0) {
@@ -474,11 +529,11 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
       }
       const double inv_next = 1.0 / (double)(l + 1);
       if (l & 1)
-        tr_term<LOG2N, true, true>(hs_odd, hs, nd, delta, inv_next, zb, t, bar, ta_t, r4_t, fftw,
-                                   rp, o, taylor_sign_d(l));
+        tr_term<LOG2N, true, 1>(hs_odd, hs, nd, delta, inv_next, nullptr, zb, t, bar, ta_t, r4_t,
+                                fftw, rp, o, taylor_sign_d(l));
       else
-        tr_term<LOG2N, false, true>(hs, hs_odd, nd, delta, inv_next, zb, t, bar, ta_t, r4_t, fftw,
-                                    rp, o, taylor_sign_d(l));
+        tr_term<LOG2N, false, 1>(hs, hs_odd, nd, delta, inv_next, nullptr, zb, t, bar, ta_t, r4_t,
+                                 fftw, rp, o, taylor_sign_d(l));
     }
   }
   double* dst = out + col * ld_out;
@@ -514,28 +569,79 @@ const double2* tw4n_table(int log2n) {
 template <int LOG2N>
 void launch_fast(int transpose, const double* in, size_t ld_in, double* out, size_t ld_out,
                  size_t batch, const double* delta, int num_terms, int plain_op,
-                 const double* mult, int* nonfinite, cudaStream_t s) {
+                 const double* mult, int* nonfinite, cudaStream_t s, const FastNdct* bes) {
   using C = Cfg<LOG2N>;
   const double2* tw = tw4n_table(LOG2N);
   const double2* fftw = pass_twiddles(LOG2N - 1);
+  const bool use_bes = bes && bes->bes_terms > 0 && plain_op < 0;
   const size_t max_cols = (size_t)0x7fffffff * C::COLS;
   for (size_t c0 = 0; c0 < batch; c0 += max_cols) {
     const size_t nc = batch - c0 < max_cols ? batch - c0 : max_cols;
     const unsigned grid = (unsigned)((nc + C::COLS - 1) / C::COLS);
     if (transpose) {
-      FLB_CUDA(cudaFuncSetAttribute(fast_ndct_tr_kernel<LOG2N>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      fast_ndct_tr_kernel<LOG2N><<<grid, C::THREADS, C::SMEM, s>>>(
-          in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta, num_terms, plain_op, mult,
-          tw, fftw, nonfinite);
-      note_launch("fast_ndct_tr_kernel");
+      auto kern = use_bes ? fast_ndct_tr_kernel<LOG2N, true> : fast_ndct_tr_kernel<LOG2N, false>;
+      FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      kern<<<grid, C::THREADS, C::SMEM, s>>>(
+          in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta,
+          use_bes ? bes->bes_terms : num_terms, plain_op, mult, tw, fftw,
+          use_bes ? bes->bes_wt : nullptr, use_bes ? bes->bes_tt : nullptr, nonfinite);
+      note_launch(use_bes ? "fast_ndct_tr_kernel<bessel>" : "fast_ndct_tr_kernel");
     } else {
-      FLB_CUDA(cudaFuncSetAttribute(fast_ndct_fwd_kernel<LOG2N>,
-                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      fast_ndct_fwd_kernel<LOG2N><<<grid, C::THREADS, C::SMEM, s>>>(
-          in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta, num_terms, plain_op, tw,
-          fftw, nonfinite);
-      note_launch("fast_ndct_fwd_kernel");
+      auto kern = use_bes ? fast_ndct_fwd_kernel<LOG2N, true> : fast_ndct_fwd_kernel<LOG2N, false>;
+      FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+      kern<<<grid, C::THREADS, C::SMEM, s>>>(
+          in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta,
+          use_bes ? bes->bes_terms : num_terms, plain_op, tw, fftw,
+          use_bes ? bes->bes_wf : nullptr, nonfinite);
+      note_launch(use_bes ? "fast_ndct_fwd_kernel<bessel>" : "fast_ndct_fwd_kernel");
+    }
+  }
+}
+
+// J_m(y), |y| <~ 1, by its power series (alternating, decreasing terms).
+__host__ __device__ inline double bessel_j(int m, double y) {
+  const double h = 0.5 * y;
+  double t = 1.0;
+  for (int i = 1; i <= m; ++i) t *= h / (double)i;
+  double sum = t;
+  for (int k = 1; k < 40; ++k) {
+    t *= -(h * h) / ((double)k * (double)(m + k));
+    sum += t;
+    if (fabs(t) <= 1e-18 * fabs(sum)) break;
+  }
+  return sum;
+}
+
+// Weight of term m (sign and Jacobi-Anger factor included):
+//   cos(x y) = J_0 + 2 sum_k (-1)^k J_2k(y) T_2k(x),  sin(x y) = 2 sum_k (-1)^k J_2k+1(y) T_2k+1(x),
+//   cos(n theta_k) = cos(n theta0_k) cos(x y) - sin(n theta0_k) sin(x y), x = n/N, y = N delta_k.
+__host__ __device__ inline double bessel_weight(int m, double y) {
+  const double j = bessel_j(m, y);
+  if ((m & 1) == 0) return (m == 0 ? 1.0 : 2.0) * (((m >> 1) & 1) ? -j : j);
+  return -2.0 * ((((m - 1) >> 1) & 1) ? -j : j);
+}
+
+template <int LOG2N>
+__global__ void bessel_tables_kernel(const double* __restrict__ delta, int terms,
+                                     double* __restrict__ wf, double* __restrict__ wt,
+                                     double* __restrict__ tt) {
+  using C = Cfg<LOG2N>;
+  constexpr int N = C::N, T = C::T;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const double yf = (double)N * delta[fwd_own_row<LOG2N>(j % T, j / T)];
+  const double yt = (double)N * delta[tr_entry<N>(j)];
+  const double x = (double)tr_row<N>(j % T, j / T) / (double)N;
+  double tm1 = 1.0, tm = x;  // T_{m-1}, T_m
+  for (int m = 0; m < terms; ++m) {
+    wf[(size_t)m * N + j] = bessel_weight(m, yf);
+    wt[(size_t)m * N + j] = bessel_weight(m, yt);
+    const double tv = m == 0 ? 1.0 : m == 1 ? x : tm;
+    tt[(size_t)m * N + j] = tv;
+    if (m >= 1) {  // advance to T_{m+1}
+      const double nx = 2.0 * x * tm - tm1;
+      tm1 = tm;
+      tm = nx;
     }
   }
 }
@@ -716,7 +822,8 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
 
 void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* out,
               size_t ld_out, size_t batch, const double* delta, int num_terms, int plain_op,
-              const double* mult, int* nonfinite, cudaStream_t s, int l_lo = 0, int l_hi = -1) {
+              const double* mult, int* nonfinite, cudaStream_t s, int l_lo = 0, int l_hi = -1,
+              const FastNdct* bes = nullptr) {
   if (l_hi < 0) l_hi = num_terms;
   if (log2n > 13) {
     launch_big(log2n, transpose, in, ld_in, out, ld_out, batch, delta, l_lo, l_hi, plain_op, mult,
@@ -726,11 +833,11 @@ void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* 
   if (plain_op < 0 && (l_lo != 0 || l_hi != num_terms))
     fail(FL_INVALID_ARGUMENT, "ndct: term subsets need N > 8192 (multi-pass path)");
   switch (log2n) {
-    case 9: launch_fast<9>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
-    case 10: launch_fast<10>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
-    case 11: launch_fast<11>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
-    case 12: launch_fast<12>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
-    case 13: launch_fast<13>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s); break;
+    case 9: launch_fast<9>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s, bes); break;
+    case 10: launch_fast<10>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s, bes); break;
+    case 11: launch_fast<11>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s, bes); break;
+    case 12: launch_fast<12>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s, bes); break;
+    case 13: launch_fast<13>(transpose, in, ld_in, out, ld_out, batch, delta, num_terms, plain_op, mult, nonfinite, s, bes); break;
     default: fail(FL_RUNTIME_ERROR, "fast ndct: unsupported size");
   }
 }
@@ -740,6 +847,20 @@ int log2_exact(size_t n) {
   int l = 0;
   while ((size_t(1) << l) < n) ++l;
   return l;
+}
+
+// Terms of the Chebyshev (Jacobi-Anger) expansion with the same perturbation
+// bound as cheb1_terms (|N delta| <= 0.83845): smallest M with
+// 2 sum_{m >= M} |J_m(0.83845)| <= tol (|T_m| <= 1 on [0, 1]); 14 at 2^-52
+// against Taylor's 17.
+int bessel_terms(double tol) {
+  if (!(tol > 0.0 && tol < 1.0)) return -1;
+  for (int M = 1; M <= 30; ++M) {
+    double tail = 0.0;
+    for (int m = M; m < M + 12; ++m) tail += 2.0 * fabs(bessel_j(m, 0.83845));
+    if (tail <= tol) return M;
+  }
+  return -1;
 }
 
 int cheb1_terms(double tol) {  // ndct.hpp:49-59 for cheb1; -1 if unattainable
@@ -792,12 +913,31 @@ FastNdct* fast_ndct_create(size_t n, double tol, int kind, const double* theta) 
   FLB_CUDA(cudaMalloc(&p->owned_delta, n * sizeof(double)));
   launch_reference_grid(n, FL_CHEB1, theta, nullptr, p->owned_delta, 0);
   p->delta = p->owned_delta;
+#ifndef FLB_NDCT_BESSEL
+#define FLB_NDCT_BESSEL 1
+#endif
+  const int M = bessel_terms(tol);
+  if (FLB_NDCT_BESSEL && lg <= 13 && M > 0 && M < L) {
+    p->bes_terms = M;
+    for (double** t : {&p->bes_wf, &p->bes_wt, &p->bes_tt})
+      FLB_CUDA(cudaMalloc(t, (size_t)M * n * sizeof(double)));
+    const unsigned grid = (unsigned)((n + 255) / 256);
+    switch (lg) {
+#define FLB_BES(LG) \
+  case LG: bessel_tables_kernel<LG><<<grid, 256>>>(p->delta, M, p->bes_wf, p->bes_wt, p->bes_tt); break;
+      FLB_BES(9) FLB_BES(10) FLB_BES(11) FLB_BES(12) FLB_BES(13)
+#undef FLB_BES
+    }
+    note_launch("bessel_tables_kernel");
+  }
   return p;
 }
 
 void fast_ndct_destroy(FastNdct* p) {
   if (!p) return;
   if (p->owned_delta) cudaFree(p->owned_delta);
+  for (double* t : {p->bes_wf, p->bes_wt, p->bes_tt})
+    if (t) cudaFree(t);
   delete p;
 }
 
@@ -805,7 +945,7 @@ void fast_ndct_run(const FastNdct& p, int transpose, const double* in, size_t ld
                    size_t ld_out, size_t batch, const double* in_mult, int* nonfinite,
                    cudaStream_t s, int l_lo, int l_hi) {
   dispatch(p.log2n, transpose, in, ld_in, out, ld_out, batch, p.delta, p.num_terms, -1, in_mult,
-           nonfinite, s, l_lo, l_hi);
+           nonfinite, s, l_lo, l_hi, &p);
 }
 
 }  // namespace flb
