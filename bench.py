@@ -280,12 +280,7 @@ def main() -> None:
     ms_max = max_over_ranks(ms, dist, f"cuda:{local}")
     value = n * total / (ms_max / 1e3)
 
-    # ---- per-kernel split (same stream, CUDA events): leg2cheb GEMM vs NDCT
-    th = torch.from_numpy(cfg.grid().theta).to(x.device)
-    d1 = torch.empty_like(th)
-    _lib.check(_lib.LIB.fl_reference_grid(n, fl.GridKind.cheb1, vp(th.data_ptr()), None, vp(d1.data_ptr()), sp))
-    lam = torch.from_numpy(cfg.lambda_().table).to(x.device)
-    L1 = fl.min_taylor_terms(fl.GridKind.cheb1, cfg.tolerance())
+    # ---- per-kernel split (same stream, CUDA events): the plan's two steps
     chat = torch.empty_like(x)
 
     def timed(fn, reps=3):
@@ -302,8 +297,10 @@ def main() -> None:
     # the plan's conversion step exactly as fl_dlt runs it (split-int8 tcgen05 GEMM)
     ms_l2c = timed(lambda: _lib.check(_lib.LIB.fl_plan_leg2cheb(cfg.handle, 0, vp(x.data_ptr()),
                                                                 vp(chat.data_ptr()), cols, n, sp)))
-    ms_ndct = timed(lambda: _lib.check(_lib.LIB.fl_ndct(0, fl.GridKind.cheb1, n, L1, vp(d1.data_ptr()),
-                                                        vp(chat.data_ptr()), vp(y.data_ptr()), cols, n, sp)))
+    # the plan's NDCT step exactly as fl_dlt runs it (fast mode: Chebyshev expansion)
+    L1 = _lib.LIB.fl_plan_ndct_terms(cfg.handle)
+    ms_ndct = timed(lambda: _lib.check(_lib.LIB.fl_plan_ndct(cfg.handle, 0, vp(chat.data_ptr()),
+                                                             vp(y.data_ptr()), cols, n, sp)))
     ms_dct = timed(lambda: _lib.check(_lib.LIB.fl_trig(0, fl.GridKind.cheb1, n, vp(x.data_ptr()),
                                                        vp(y.data_ptr()), cols, n, sp)))
     coef = n * cols
@@ -374,7 +371,8 @@ def main() -> None:
                          "achieved": achieved, "peak": DFMA_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / DFMA_PEAK_TFLOPS, "traffic": traffic,
                          "peak_source": "measured DFMA (fp64 CUDA-core) peak, tools/fp64_peak.cu (profiles/r01_fp64_peak.log)",
-                         "algorithmic": "NDCT L(2.5 log2N + 3) flop/coef, L = 17 (cheb1, 2^-52)"},
+                         "algorithmic": f"NDCT L(2.5 log2N + 3) flop/coef, L = {L1} transforms "
+                                        "(Chebyshev expansion about cheb1, 2^-52)"},
             "roofline_tensor": {"bound": "tensor", "kernel": "oz_split_b_kernel + oz_gemm_kernel",
                                 "gemm_mode": "int8_split" if gemm_mode == fl.GEMM_INT8_SPLIT else "fp64",
                                 "achieved": i8_ops / (ms_l2c / 1e3) / 1e12, "peak": INT8_PEAK_TOPS,

@@ -128,8 +128,12 @@ fl_status fl_idlt(const fl_plan* plan, const double* in, double* out, size_t bat
  *   0 = FL_NDCT_LITERAL : L chebstar terms over length-(2N+1) transforms,
  *                         exactly the reference's algorithm (ndct.hpp:98-143);
  *   1 = FL_NDCT_FAST    : same nodes, evaluated internally about the cheb1
- *                         grid with min_taylor_terms(cheb1, tol) terms over
- *                         power-of-two real DCTs (SURVEY.md 7 H2 option B).
+ *                         grid over power-of-two real DCTs (SURVEY.md 7 H2
+ *                         option B): for N <= 8192 by the Chebyshev
+ *                         (Jacobi-Anger) expansion of cos(n delta), sin(n delta)
+ *                         in n/N -- 14 transforms at 2^-52, tail
+ *                         2 sum_{m>=M} |J_m(0.83845)| <= tol -- above 8192 by
+ *                         min_taylor_terms(cheb1, tol) Taylor terms.
  * Both are within the reference's certified bound of each other
  * (test_ndct.cpp:173-183). Default FL_NDCT_FAST for dlt/idlt of power-of-two
  * sizes; the free-function fl_ndct always evaluates its plan literally. */
@@ -170,6 +174,16 @@ int fl_plan_gemm_mode(const fl_plan* plan);
  * transforms.hpp:62). Host or device pointers, columns of stride ld. */
 fl_status fl_plan_leg2cheb(const fl_plan* plan, int transpose, const double* in, double* out,
                            size_t batch, size_t ld, void* stream);
+
+/* The plan's NDCT step alone, as dlt/idlt run it (same FL_NDCT_* mode):
+ * out = NDCT(in) (transpose = 0, transforms.hpp:48) or NDCT^T(in) (1, the
+ * unweighted ndct_apply_transpose of transforms.hpp:60).
+ * fl_plan_ndct_terms: transforms per column it evaluates (fast mode, N <=
+ * 8192: the Chebyshev / Jacobi-Anger expansion about cheb1, 14 terms at
+ * 2^-52; Taylor about cheb1 above 8192; the plan's own L when literal). */
+fl_status fl_plan_ndct(const fl_plan* plan, int transpose, const double* in, double* out,
+                       size_t batch, size_t ld, void* stream);
+int fl_plan_ndct_terms(const fl_plan* plan);
 
 /* Term-parallel pieces of dlt / idlt (multi-GPU extension for one large
  * vector, C5). Both stages of fl_dlt are sums of independent terms, so P

@@ -64,7 +64,7 @@ EXPORTS = [
     "fl_eval_legendre_direct", "fl_eval_chebyshev_direct", "fl_idlt_direct",
     "fl_cheb_coeffs_of_legendre", "fl_plan_set_leg2cheb_mode", "fl_plan_leg2cheb_rank",
     "fl_plan_stage_terms", "fl_dlt_stage", "fl_plan_set_gemm_mode", "fl_plan_gemm_mode",
-    "fl_plan_leg2cheb",
+    "fl_plan_leg2cheb", "fl_plan_ndct", "fl_plan_ndct_terms",
 ]
 
 
@@ -113,6 +113,8 @@ def _load() -> C.CDLL:
         "fl_plan_set_gemm_mode": (i, [vp, i]),
         "fl_plan_gemm_mode": (i, [vp]),
         "fl_plan_leg2cheb": (i, [vp, i, dp, dp, sz, sz, vp]),
+        "fl_plan_ndct": (i, [vp, i, dp, dp, sz, sz, vp]),
+        "fl_plan_ndct_terms": (i, [vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

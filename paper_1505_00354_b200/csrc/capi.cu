@@ -736,6 +736,33 @@ fl_status fl_plan_set_ndct_mode(fl_plan* p, int mode) {
 
 int fl_plan_ndct_mode(const fl_plan* p) { return p ? p->mode : -1; }
 
+fl_status fl_plan_ndct(const fl_plan* p, int transpose, const double* in, double* out,
+                       size_t batch, size_t ld, void* stream) {
+  return guarded([&] {
+    if (!p) fail(FL_INVALID_ARGUMENT, "plan: null");
+    const size_t n = p->n;
+    if (batch == 0) return;
+    if (batch == 1) ld = n;
+    check_ld(n, ld, batch);
+    FLB_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = as_stream(stream);
+    DevIn i(in, n, batch, ld, s);
+    DevOut o(out, n, batch, ld, s);
+    if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
+    const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
+    run_ndct(transpose ? "ndct_apply_transpose" : "ndct_apply", transpose ? 1 : 0, p->kind, n,
+             p->num_terms, p->delta, i.ptr, i.ld, o.ptr, o.ld, batch, nullptr, fast, s);
+    o.finish();
+    sync(s);
+  });
+}
+
+int fl_plan_ndct_terms(const fl_plan* p) {
+  if (!p) return -1;
+  if (p->mode == FL_NDCT_FAST && p->fast) return fast_ndct_dlt_terms(*p->fast);
+  return p->num_terms;
+}
+
 fl_status fl_plan_stage_terms(const fl_plan* p, int stage, int* count) {
   return guarded([&] {
     *count = 0;

@@ -952,4 +952,5 @@ void fast_ndct_run(const FastNdct& p, int transpose, const double* in, size_t ld
 
 namespace flb {
 int fast_ndct_terms(const FastNdct& p) { return p.num_terms; }
+int fast_ndct_dlt_terms(const FastNdct& p) { return p.bes_terms > 0 ? p.bes_terms : p.num_terms; }
 }  // namespace flb

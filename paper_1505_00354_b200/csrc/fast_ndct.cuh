@@ -38,5 +38,8 @@ void fast_ndct_run(const FastNdct& p, int transpose, const double* in, size_t ld
                    size_t ld_out, size_t batch, const double* in_mult, int* nonfinite,
                    cudaStream_t s, int l_lo = 0, int l_hi = -1);
 int fast_ndct_terms(const FastNdct& p);
+// Transforms per column of fast_ndct_run for N <= 8192 (the Chebyshev
+// expansion's term count when it is in use, else the Taylor count).
+int fast_ndct_dlt_terms(const FastNdct& p);
 
 }  // namespace flb
