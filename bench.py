@@ -303,6 +303,9 @@ def main() -> None:
                                                              vp(y.data_ptr()), cols, n, sp)))
     ms_dct = timed(lambda: _lib.check(_lib.LIB.fl_trig(0, fl.GridKind.cheb1, n, vp(x.data_ptr()),
                                                        vp(y.data_ptr()), cols, n, sp)))
+    # the inverse on the same shard (DLT, IDLT and NDCT reported separately)
+    ms_idlt = timed(lambda: _lib.check(_lib.LIB.fl_idlt(cfg.handle, vp(x.data_ptr()), vp(y.data_ptr()),
+                                                        cols, n, sp)))
     coef = n * cols
     l2c_flops = coef * (n / 2.0)                   # N^2/4 MACs per column = N/2 flop per coefficient
     ndct_flops = coef * L1 * (2.5 * math.log2(n) + 3)  # L (2.5 log2 N + 3)
@@ -386,7 +389,7 @@ def main() -> None:
                              "note": "16 B/coef algorithmic (one fp64 read + one write), whole DLT",
                              "dct_pass_gbs": dct_gbs, "dct_pass_frac": dct_gbs / hbm_peak},
             "kernels_ms": {"leg2cheb_split_int8": ms_l2c, "ndct": ms_ndct, "dct_iii_pass": ms_dct,
-                           "dlt_step": ms},
+                           "dlt_step": ms, "idlt_step": ms_idlt},
             "e2e": {"value": n * total / (e2e_ms / 1e3), "unit": "coeffs/s",
                     "h2d_bytes_per_step": int(8 * n * cols), "d2h_bytes_per_step": int(8 * n * cols)},
             "gpu_launches": launches,
