@@ -87,8 +87,12 @@ struct Cfg {
   static constexpr int NSL = last_pass_ns(P);     // last FFT pass
   static constexpr int RL = P / NSL;
   // per column: the stage vector double-buffered (term l reads one copy while
-  // its pack writes term l+1's into the other) and the FFT row
-  static constexpr size_t COL_BYTES = 2 * N * sizeof(double) + smem_row(P) * sizeof(double2);
+  // its pack writes term l+1's into the other) and the FFT row -- two of
+  // them (ping-pong passes, one barrier per pass) when they fit beside the
+  // tables (not at N = 8192)
+  static constexpr size_t ZB = smem_row(P) * sizeof(double2);
+  static constexpr bool PP = COLS * (2 * N * sizeof(double) + 2 * ZB) + N * 8 + TW * 16 <= 220 * 1024;
+  static constexpr size_t COL_BYTES = 2 * N * sizeof(double) + (PP ? 2 : 1) * ZB;
   // tables in shared memory when they fit beside the columns
   static constexpr bool SMEM_TABLES = COLS * COL_BYTES + N * 8 + TW * 16 <= 220 * 1024;
   static constexpr size_t SMEM = COLS * COL_BYTES + (SMEM_TABLES ? N * 8 + TW * 16 : 0);
@@ -204,23 +208,34 @@ __device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, do
 }
 
 // One forward Taylor term (or one plain transform): f[i] += sign p[i] y_{k_i}.
-// The barrier before the first pass store orders it after the previous
-// term's last-pass reads of zb.
+// The first pass stores into zx. Ping-pong (C::PP): the passes alternate
+// between zx and zy; the caller passes, as the next term's zx, the buffer the
+// last pass did NOT read (returned: the one it read), so no barrier is needed
+// before the first store. In place: a barrier orders the first store after
+// the previous term's last-pass reads.
 template <int LOG2N, bool ODD, int NM>
-__device__ __forceinline__ void fwd_term(const double* stage, double* next, double2* zb, int t,
-                                         int bar, double2 ta_t, double2 r4_t, const double2* fftw,
-                                         const double* p, double* f, double sign) {
+__device__ __forceinline__ double2* fwd_term(const double* stage, double* next, double2* zx,
+                                             double2* zy, int t, int bar, double2 ta_t,
+                                             double2 r4_t, const double2* fftw, const double* p,
+                                             double* f, double sign) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, NSL = C::NSL, RL = C::RL;
   static_assert(E == 8 && T == N / 16, "pack twiddle constants assume T = N/16");
   double2 v[E];
   fwd_pack_all<N, ODD, NM, 0>(v, stage, next, t, ta_t, r4_t);
   pass_compute<P, E, 8, 1, true>(v, t, fftw);
-  group_sync<C::GT>(bar);
-  pass_store<P, E, 8, 1>(v, zb, t);
-  group_sync<C::GT>(bar);
-  mid_passes<P, E, 8, NSL, true, C::GT, true>(zb, t, fftw, bar);
-  pass_load<P, E, RL>(v, zb, t);
+  double2* fin = zx;
+  if constexpr (C::PP) {
+    pass_store<P, E, 8, 1>(v, zx, t);
+    group_sync<C::GT>(bar);
+    fin = mid_passes_pp<P, E, 8, NSL, true, C::GT, true>(zx, zy, t, fftw, bar);
+  } else {
+    group_sync<C::GT>(bar);
+    pass_store<P, E, 8, 1>(v, zx, t);
+    group_sync<C::GT>(bar);
+    mid_passes<P, E, 8, NSL, true, C::GT, true>(zx, t, fftw, bar);
+  }
+  pass_load<P, E, RL>(v, fin, t);
   pass_compute<P, E, RL, NSL, true, true>(v, t, fftw + pass_tw_offset(P, NSL));
 #pragma unroll
   for (int q = 0; q < E / RL; ++q)
@@ -237,6 +252,7 @@ __device__ __forceinline__ void fwd_term(const double* stage, double* next, doub
         f[i] += sign * p[i] * y;
       }
     }
+  return fin;
 }
 
 // plain_op: -1 = NDCT with num_terms terms; 0 = one plain DCT-III;
@@ -272,7 +288,10 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   if (col >= batch) return;
   double* stage = smem + g * (C::COL_BYTES / 8);  // (n/N)^l c_n, terms l even
   double* stage_odd = stage + N;                  // terms l odd
-  double2* zb = reinterpret_cast<double2*>(stage + 2 * N);
+  double2* zbA = reinterpret_cast<double2*>(stage + 2 * N);
+  double2* zbB = C::PP ? zbA + C::ZB / sizeof(double2) : zbA;
+  double2* zx = zbA;  // the first pass's target this term
+  auto other = [&](double2* b) { return b == zbA ? zbB : zbA; };
   const double* src = in + col * ld_in;
   bool bad = false;
 #pragma unroll
@@ -296,19 +315,24 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      fwd_term<LOG2N, true, 0>(stage, nullptr, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      fwd_term<LOG2N, true, 0>(stage, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw, p, f, 1.0);
     else
-      fwd_term<LOG2N, false, 0>(stage, nullptr, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      fwd_term<LOG2N, false, 0>(stage, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw, p, f, 1.0);
   } else if (BES) {
     for (int m = 0; m < num_terms; ++m) {
 #pragma unroll
       for (int i = 0; i < OWN; ++i) p[i] = __ldg(wtab + (size_t)m * N + i * T + t);
+      double2* fin;
       if (m == 0)
-        fwd_term<LOG2N, false, 1>(stage, stage_odd, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+        fin = fwd_term<LOG2N, false, 1>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+                                        p, f, 1.0);
       else if (m & 1)
-        fwd_term<LOG2N, true, 2>(stage_odd, stage, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+        fin = fwd_term<LOG2N, true, 2>(stage_odd, stage, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+                                       p, f, 1.0);
       else
-        fwd_term<LOG2N, false, 2>(stage, stage_odd, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+        fin = fwd_term<LOG2N, false, 2>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+                                        p, f, 1.0);
+      zx = other(fin);
     }
   } else {
     for (int l = 0; l < num_terms; ++l) {
@@ -320,12 +344,14 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
           p[i] *= q * inv_l;  // (N delta_k)^l / l!
         }
       }
+      double2* fin;
       if (l & 1)
-        fwd_term<LOG2N, true, 1>(stage_odd, stage, zb, t, bar, ta_t, r4_t, fftw, p, f,
-                                 taylor_sign_d(l));
+        fin = fwd_term<LOG2N, true, 1>(stage_odd, stage, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+                                       p, f, taylor_sign_d(l));
       else
-        fwd_term<LOG2N, false, 1>(stage, stage_odd, zb, t, bar, ta_t, r4_t, fftw, p, f,
-                                  taylor_sign_d(l));
+        fin = fwd_term<LOG2N, false, 1>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+                                        p, f, taylor_sign_d(l));
+      zx = other(fin);
     }
   }
   // scatter the owned rows through shared memory, then one coalesced store
@@ -375,14 +401,17 @@ __device__ __forceinline__ double tr_unpack(double2 za, double2 zc, double2 tn, 
 // it also writes the next term's stage, h (N delta)/(l+1) = h * nd * inv_next
 // (nd in the tr_slot order), into `next`; PM = 2 (Chebyshev): the stage is
 // the input g and each entry is weighted on the fly by wrow[slot] (the
-// term's weights in the tr_slot order). The barrier before the first pass
-// store orders it after the previous term's unpack reads of zb.
+// term's weights in the tr_slot order). The first pass stores into zx;
+// ping-pong (C::PP) as in fwd_term (returns the buffer the unpack read; the
+// caller passes the other one as the next zx), else in place with a barrier
+// ordering the first store after the previous term's unpack reads.
 template <int LOG2N, bool ODD, int PM>
-__device__ __forceinline__ void tr_term(const double* hs, double* next, const double* nd,
-                                        const double* __restrict__ delta, double inv_next,
-                                        const double* __restrict__ wrow, double2* zb, int t,
-                                        int bar, double2 ta_t, double2 r4_t, const double2* fftw,
-                                        const double* rp, double* o, double sign) {
+__device__ __forceinline__ double2* tr_term(const double* hs, double* next, const double* nd,
+                                            const double* __restrict__ delta, double inv_next,
+                                            const double* __restrict__ wrow, double2* zx,
+                                            double2* zy, int t, int bar, double2 ta_t,
+                                            double2 r4_t, const double2* fftw, const double* rp,
+                                            double* o, double sign) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, OWN = C::OWN;
   static_assert(E == 8 && T == N / 16, "row grouping assumes T = N/16");
@@ -413,10 +442,17 @@ __device__ __forceinline__ void tr_term(const double* hs, double* next, const do
       v[r] = ODD ? make_double2(-w.y, -w.x) : make_double2(w.y, w.x);
   }
   pass_compute<P, E, 8, 1, false>(v, t, fftw);
-  group_sync<C::GT>(bar);
-  pass_store<P, E, 8, 1>(v, zb, t);
-  group_sync<C::GT>(bar);
-  mid_passes<P, E, 8, P, false, C::GT>(zb, t, fftw, bar);  // TWP measured slower here
+  double2* zb = zx;
+  if constexpr (C::PP) {
+    pass_store<P, E, 8, 1>(v, zx, t);
+    group_sync<C::GT>(bar);
+    zb = mid_passes_pp<P, E, 8, P, false, C::GT>(zx, zy, t, fftw, bar);
+  } else {
+    group_sync<C::GT>(bar);
+    pass_store<P, E, 8, 1>(v, zx, t);
+    group_sync<C::GT>(bar);
+    mid_passes<P, E, 8, P, false, C::GT>(zx, t, fftw, bar);  // TWP measured slower here
+  }
   constexpr double h = 0.70710678118654752440;
 #pragma unroll
   for (int g = 0; g < OWN / 4; ++g) {
@@ -451,6 +487,7 @@ __device__ __forceinline__ void tr_term(const double* hs, double* next, const do
     o[4 * g + 2] += sign * rp[4 * g + 2] * x2;
     o[4 * g + 3] += sign * rp[4 * g + 3] * x3;
   }
+  return zb;
 }
 
 // BES: Chebyshev (Jacobi-Anger) expansion: the stage is the (weighted) input
@@ -483,7 +520,10 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   // h_k = (N delta_k)^l / l! g_k at hs[tr_slot(k)], double-buffered by term parity
   double* hs = smem + g * (C::COL_BYTES / 8);
   double* hs_odd = hs + N;
-  double2* zb = reinterpret_cast<double2*>(hs + 2 * N);
+  double2* zbA = reinterpret_cast<double2*>(hs + 2 * N);
+  double2* zbB = C::PP ? zbA + C::ZB / sizeof(double2) : zbA;
+  double2* zx = zbA;  // the first pass's target this term
+  auto other = [&](double2* b) { return b == zbA ? zbB : zbA; };
   const double* src = in + col * ld_in;
   double o[OWN], rp[OWN];
   bool bad = false;
@@ -503,22 +543,24 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      tr_term<LOG2N, true, 0>(hs, nullptr, nd, delta, 0.0, nullptr, zb, t, bar, ta_t, r4_t, fftw,
+      tr_term<LOG2N, true, 0>(hs, nullptr, nd, delta, 0.0, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                               rp, o, 1.0);
     else
-      tr_term<LOG2N, false, 0>(hs, nullptr, nd, delta, 0.0, nullptr, zb, t, bar, ta_t, r4_t, fftw,
+      tr_term<LOG2N, false, 0>(hs, nullptr, nd, delta, 0.0, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                                rp, o, 1.0);
   } else if (BES) {
     for (int m = 0; m < num_terms; ++m) {
 #pragma unroll
       for (int i = 0; i < OWN; ++i) rp[i] = __ldg(ttab + (size_t)m * N + i * T + t);
       const double* wrow = wtab + (size_t)m * N;
+      double2* fin;
       if (m & 1)
-        tr_term<LOG2N, true, 2>(hs, nullptr, nd, delta, 0.0, wrow, zb, t, bar, ta_t, r4_t, fftw,
-                                rp, o, 1.0);
+        fin = tr_term<LOG2N, true, 2>(hs, nullptr, nd, delta, 0.0, wrow, zx, other(zx), t, bar,
+                                      ta_t, r4_t, fftw, rp, o, 1.0);
       else
-        tr_term<LOG2N, false, 2>(hs, nullptr, nd, delta, 0.0, wrow, zb, t, bar, ta_t, r4_t, fftw,
-                                 rp, o, 1.0);
+        fin = tr_term<LOG2N, false, 2>(hs, nullptr, nd, delta, 0.0, wrow, zx, other(zx), t, bar,
+                                       ta_t, r4_t, fftw, rp, o, 1.0);
+      zx = other(fin);
     }
   } else {
     for (int l = 0; l < num_terms; ++l) {
@@ -528,12 +570,14 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
           rp[i] *= (double)tr_row<N>(t, i) / (double)N;  // (n/N)^l for output row n
       }
       const double inv_next = 1.0 / (double)(l + 1);
+      double2* fin;
       if (l & 1)
-        tr_term<LOG2N, true, 1>(hs_odd, hs, nd, delta, inv_next, nullptr, zb, t, bar, ta_t, r4_t,
-                                fftw, rp, o, taylor_sign_d(l));
+        fin = tr_term<LOG2N, true, 1>(hs_odd, hs, nd, delta, inv_next, nullptr, zx, other(zx), t,
+                                      bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
       else
-        tr_term<LOG2N, false, 1>(hs, hs_odd, nd, delta, inv_next, nullptr, zb, t, bar, ta_t, r4_t,
-                                 fftw, rp, o, taylor_sign_d(l));
+        fin = tr_term<LOG2N, false, 1>(hs, hs_odd, nd, delta, inv_next, nullptr, zx, other(zx), t,
+                                       bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
+      zx = other(fin);
     }
   }
   double* dst = out + col * ld_out;

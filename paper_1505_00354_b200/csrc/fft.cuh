@@ -247,6 +247,32 @@ __device__ __forceinline__ void mid_passes(double2* s, int tid, const double2* t
   }
 }
 
+// Ping-pong variant: each pass reads `src` and writes the other buffer, so the
+// only barrier is the one after the store (the in-place pass needs a second
+// one between its loads and its stores). Returns the buffer holding the
+// result of the last pass run (a when NS == NS_END).
+template <int P, int E, int R, int NS, bool INV, int GT, bool TWP = false>
+__device__ __forceinline__ void stockham_pass_pp(const double2* src, double2* dst, int tid,
+                                                 const double2* tw, int bar) {
+  double2 v[E];
+  pass_load<P, E, R>(v, src, tid);
+  pass_compute<P, E, R, NS, INV, TWP>(v, tid, tw);
+  pass_store<P, E, R, NS>(v, dst, tid);
+  group_sync<GT>(bar);
+}
+
+template <int P, int E, int NS, int NS_END, bool INV, int GT, bool TWP = false>
+__device__ __forceinline__ double2* mid_passes_pp(double2* a, double2* b, int tid,
+                                                  const double2* tw, int bar) {
+  if constexpr (NS < NS_END) {
+    constexpr int R = pass_radix(P, NS);
+    stockham_pass_pp<P, E, R, NS, INV, GT, TWP>(a, b, tid, tw + pass_tw_offset(P, NS), bar);
+    return mid_passes_pp<P, E, NS * R, NS_END, INV, GT, TWP>(b, a, tid, tw, bar);
+  } else {
+    return a;
+  }
+}
+
 // Device pass-major twiddle table for length 2^log2p (cached per device).
 const double2* pass_twiddles(int log2p);
 
