@@ -462,6 +462,240 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   }
 }
 
+// ---- the split GEMM on SM pairs (cta_group::2) -----------------------------
+// A cluster of two CTAs on one TPC computes a 256 x 64 output tile (two
+// adjacent 128-row blocks of one parity): each CTA stages its own 128 A rows
+// and HALF of the B tile (32 columns) per K block, the leader issues
+// tcgen05.mma.cta_group::2 (M = 256, N = 64) which reads both CTAs' shared
+// memory, and each CTA's TMEM receives its 128 rows of the 8 accumulators.
+// Per SM the tensor core then reads 4 KiB of A + 1 KiB of B per 32-clock MMA
+// instead of 4 + 2 KiB: the shared-memory operand bound of the 1-SM kernel
+// (64 % of the int8 peak at N = 64) rises to ~80 %.
+namespace oz2 {
+constexpr int A_TILE = oz::BM * oz::BK;            // 128 rows
+constexpr int B_TILE = (oz::BN / 2) * oz::BK;      // 32 columns: this CTA's half
+constexpr int STAGE_BYTES = oz::S * (A_TILE + B_TILE);
+#ifndef FLB_OZ2_STAGES
+#define FLB_OZ2_STAGES 2
+#endif
+constexpr int STAGES = FLB_OZ2_STAGES;
+constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
+constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(oz::BN >> 3) << 17) |
+                           ((uint32_t)(256 >> 4) << 24);
+}  // namespace oz2
+
+__device__ __forceinline__ uint32_t cluster_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t map_to_rank(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+  asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr)
+               : "memory");
+}
+// TMA into this CTA's smem, completion counted on an mbarrier of the pair
+// (the leader's).
+__device__ __forceinline__ void tma_load_3d_pair(uint32_t dst, const CUtensorMap* map,
+                                                 uint32_t cluster_bar, int c0, int c1, int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(cluster_bar), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+__device__ __forceinline__ void tc2_mma_i8(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                           uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// Arrive on the barrier at this offset in BOTH CTAs of the pair once the
+// issuing thread's MMAs retire.
+__device__ __forceinline__ void tc2_commit_both(uint32_t bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;\n\t}" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
+    oz_gemm2_kernel(const __grid_constant__ CUtensorMap tmap_a,
+                    const __grid_constant__ CUtensorMap tmap_b, const double* __restrict__ arow,
+                    const double* __restrict__ bcol, double* __restrict__ out, size_t r,
+                    size_t cols, size_t ld, int transpose, size_t ntiles) {
+  using namespace oz;
+  using oz2::A_TILE;
+  using oz2::B_TILE;
+  using oz2::STAGE_BYTES;
+  using oz2::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* full_b = bars;                 // leader's are used (count 2: both producers)
+  uint64_t* empty_b = bars + STAGES;       // each CTA's own (multicast commit)
+  uint64_t* tfull_b = bars + 2 * STAGES;   // each CTA's own (multicast commit)
+  uint64_t* tempty_b = bars + 2 * STAGES + 1;  // leader's (both epilogues arrive)
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = cluster_rank();
+  const bool leader = rank == 0;
+  const size_t pairs = (r / BM) / 2;  // 256-row blocks
+  const size_t cluster_id = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  auto tile_coords = [&](size_t tile, size_t& cb, int& p, size_t& rp, int& kb_lo, int& nk) {
+    cb = tile / (2 * pairs);
+    p = (int)(tile % 2);
+    rp = (tile / 2) % pairs;
+    // K blocks with nonzero entries for either 128-row block of the pair
+    kb_lo = transpose ? 0 : (int)(rp * 2 * (BM / BK));
+    const int kb_hi = transpose ? (int)((rp + 1) * 2 * (BM / BK)) : (int)(r / BK);
+    nk = kb_hi - kb_lo;
+  };
+
+  if (threadIdx.x == 0) {
+    for (int i = 0; i < STAGES; ++i) {
+      mbar_init(smem_u32(&full_b[i]), 2);
+      mbar_init(smem_u32(&empty_b[i]), 1);
+    }
+    mbar_init(smem_u32(tfull_b), 1);
+    mbar_init(smem_u32(tempty_b), 2 * EPI_THREADS);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                     smem_u32(tmem_holder))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+  }
+  tc_fence_before();
+  cluster_sync_all();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer (both CTAs)
+      uint32_t it = 0;
+      for (size_t tile = cluster_id; tile < ntiles; tile += nclusters) {
+        size_t cb, rp;
+        int p, kb_lo, nk;
+        tile_coords(tile, cb, p, rp, kb_lo, nk);
+        const int row0 = (int)((2 * rp + rank) * BM);
+        const int col0 = (int)(cb * BN + rank * (BN / 2));
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const uint32_t st = it % STAGES, ph = (it / STAGES) & 1u;
+          mbar_wait(smem_u32(&empty_b[st]), ph ^ 1u);
+          const uint32_t full_leader = map_to_rank(smem_u32(&full_b[st]), 0);
+          if (leader)
+            mbar_expect_tx(smem_u32(&full_b[st]), 2 * STAGE_BYTES);
+          else
+            mbar_arrive_remote(full_leader);
+          uint8_t* sa = smem + st * STAGE_BYTES;
+          uint8_t* sb = sa + S * A_TILE;
+          const int k0 = (kb_lo + kb) * BK;
+          for (int i = 0; i < S; ++i) {
+            tma_load_3d_pair(smem_u32(sa + i * A_TILE), &tmap_a, full_leader, k0, row0, i * 2 + p);
+            tma_load_3d_pair(smem_u32(sb + i * B_TILE), &tmap_b, full_leader, k0, col0, i * 2 + p);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (leader) {  // MMA issuer: the leader's whole warp, one elected lane issues
+      uint32_t it = 0, t = 0;
+      for (size_t tile = cluster_id; tile < ntiles; tile += nclusters, ++t) {
+        size_t cb, rp;
+        int p, kb_lo, nk;
+        tile_coords(tile, cb, p, rp, kb_lo, nk);
+        mbar_wait(smem_u32(tempty_b), (t & 1u) ^ 1u);  // both epilogues drained TMEM
+        tc_fence_after();
+        for (int kb = 0; kb < nk; ++kb, ++it) {
+          const uint32_t st = it % STAGES, ph = (it / STAGES) & 1u;
+          mbar_wait(smem_u32(&full_b[st]), ph);
+          tc_fence_after();
+          const uint32_t sa = smem_u32(smem + st * STAGE_BYTES);
+          const uint64_t ad0 = smem_desc(sa), bd0 = smem_desc(sa + S * A_TILE);
+          const uint32_t first = kb == 0 ? 0u : 1u;
+#pragma unroll
+          for (int i = 0; i < S; ++i) {
+#pragma unroll
+            for (int j = 0; i + j < S; ++j) {
+#pragma unroll
+              for (int ks = 0; ks < BK / 32; ++ks) {
+                const uint64_t ad = ad0 + (uint64_t)((i * A_TILE + ks * 32) >> 4);
+                const uint64_t bd = bd0 + (uint64_t)((j * B_TILE + ks * 32) >> 4);
+                tc2_mma_i8(tmem + (uint32_t)((i + j) * BN), ad, bd, oz2::IDESC,
+                           (ks > 0 || i > 0) ? 1u : first);
+              }
+            }
+          }
+          tc2_commit_both(smem_u32(&empty_b[st]));  // frees the stage in both CTAs
+        }
+        tc2_commit_both(smem_u32(tfull_b));  // accumulators complete in both CTAs
+      }
+    }
+  } else {
+    // epilogue (both CTAs): TMEM lanes = this CTA's 128 rows of the 256-row tile
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t tempty_leader = map_to_rank(smem_u32(tempty_b), 0);
+    uint32_t t = 0;
+    for (size_t tile = cluster_id; tile < ntiles; tile += nclusters, ++t) {
+      size_t cb, rp;
+      int p, kb_lo, nk;
+      tile_coords(tile, cb, p, rp, kb_lo, nk);
+      const size_t rb = 2 * rp + rank;
+      mbar_wait(smem_u32(tfull_b), t & 1u);
+      tc_fence_after();
+      double acc[BN];
+#pragma unroll
+      for (int c = 0; c < BN; ++c) acc[c] = 0.0;
+#pragma unroll 1
+      for (int d = S - 1; d >= 0; --d) {
+        const double w = ldexp(1.0, -7 * (d + 2));
+#pragma unroll
+        for (int h = 0; h < BN / 32; ++h) {
+          uint32_t v[32];
+          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * BN + h * 32), v);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) acc[h * 32 + c] = fma((double)(int)v[c], w, acc[h * 32 + c]);
+        }
+      }
+      tc_fence_before();
+      mbar_arrive_remote(tempty_leader);  // TMEM free for the pair's next tile
+      const double ascale = arow[(size_t)p * r + rb * BM + row];
+      const size_t k = 2 * (rb * BM + row) + p;
+#pragma unroll
+      for (int c = 0; c < BN; ++c) {
+        const size_t col = cb * BN + c;
+        if (col < cols) out[col * ld + k] = (acc[c] * ascale) * bcol[(size_t)p * cols + col];
+      }
+    }
+  }
+  tc_fence_before();
+  cluster_sync_all();  // the peer's smem / TMEM stay live until the leader is done
+  if (warp == 1) {
+    tc_fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, 512;" ::"r"(tmem) : "memory");
+  }
+}
+
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
     void* f = nullptr;
@@ -535,11 +769,30 @@ void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t co
     return true;
   }();
   (void)attr;
-  const size_t tiles = 2 * (r / oz::BM) * ((cols + oz::BN - 1) / oz::BN);
-  const unsigned grid = (unsigned)std::min<size_t>(tiles, (size_t)sm_count());
-  oz_gemm_kernel<<<grid, oz::THREADS, oz::SMEM, st>>>(p.tmap_a, tmap_b, p.arow, bcol, out, r,
-                                                       cols, ld, p.transpose, tiles);
-  note_launch("oz_gemm_kernel");
+#ifndef FLB_OZ_PAIR
+#define FLB_OZ_PAIR 1
+#endif
+  if (FLB_OZ_PAIR && (r / oz::BM) % 2 == 0) {
+    // SM pairs: tiles of 256 rows x 64 columns, B staged as two 32-column halves
+    const CUtensorMap tmap_b2 = make_map(b, r, cols, 2 * oz::S, oz::BN / 2);
+    static bool attr2 = [] {
+      FLB_CUDA(cudaFuncSetAttribute(oz_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                    oz2::SMEM));
+      return true;
+    }();
+    (void)attr2;
+    const size_t tiles = 2 * (r / oz::BM / 2) * ((cols + oz::BN - 1) / oz::BN);
+    const unsigned clusters = (unsigned)std::min<size_t>(tiles, (size_t)sm_count() / 2);
+    oz_gemm2_kernel<<<2 * clusters, oz::THREADS, oz2::SMEM, st>>>(
+        p.tmap_a, tmap_b2, p.arow, bcol, out, r, cols, ld, p.transpose, tiles);
+    note_launch("oz_gemm2_kernel");
+  } else {
+    const size_t tiles = 2 * (r / oz::BM) * ((cols + oz::BN - 1) / oz::BN);
+    const unsigned grid = (unsigned)std::min<size_t>(tiles, (size_t)sm_count());
+    oz_gemm_kernel<<<grid, oz::THREADS, oz::SMEM, st>>>(p.tmap_a, tmap_b, p.arow, bcol, out, r,
+                                                         cols, ld, p.transpose, tiles);
+    note_launch("oz_gemm_kernel");
+  }
   cudaFreeAsync(b, st);
   cudaFreeAsync(bcol, st);
 }
