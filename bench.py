@@ -326,7 +326,8 @@ def main() -> None:
     if os.path.exists(tfile):
         tj = json.load(open(tfile))
         for name, rec in tj.items():
-            if name.startswith("fast_ndct_fwd_kernel") and f"<{int(math.log2(n))}>" in name:
+            lg = int(math.log2(n))
+            if name.startswith("fast_ndct_fwd_kernel") and (f"<{lg}>" in name or f"<{lg}, 1>" in name):
                 traffic = {"bytes_per_launch": rec["dram_bytes_per_coef"] * coef,
                            "bytes_per_coef": rec["dram_bytes_per_coef"],
                            "algorithmic_bytes_per_coef": 16.0, "source": rec["capture"]}
@@ -376,7 +377,7 @@ def main() -> None:
                          "peak_source": "measured DFMA (fp64 CUDA-core) peak, tools/fp64_peak.cu (profiles/r01_fp64_peak.log)",
                          "algorithmic": f"NDCT L(2.5 log2N + 3) flop/coef, L = {L1} transforms "
                                         "(Chebyshev expansion about cheb1, 2^-52)"},
-            "roofline_tensor": {"bound": "tensor", "kernel": "oz_split_b_kernel + oz_gemm_kernel",
+            "roofline_tensor": {"bound": "tensor", "kernel": "oz_split_b_kernel + oz_gemm2_kernel",
                                 "gemm_mode": "int8_split" if gemm_mode == fl.GEMM_INT8_SPLIT else "fp64",
                                 "achieved": i8_ops / (ms_l2c / 1e3) / 1e12, "peak": INT8_PEAK_TOPS,
                                 "unit": "TOP/s int8", "frac": i8_ops / (ms_l2c / 1e3) / 1e12 / INT8_PEAK_TOPS,

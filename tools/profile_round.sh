@@ -15,6 +15,6 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     > gpurun_out/ncu_launches.log 2>&1
 echo "launch list rc=$?"
 python tools/dbg_oz2.py 4096 8192 > gpurun_out/kern_small.log 2>&1 &&
-ncu --set full --clock-control none --import-source on -k regex:"fast_ndct_fwd|oz_gemm|oz_split_b" -s 3 -c 3 \
+ncu --set full --clock-control none --import-source on -k regex:"fast_ndct_fwd|oz_gemm2|oz_split_b" -s 3 -c 3 \
     -o gpurun_out/hot_full python tools/dbg_oz2.py 4096 8192 > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"
