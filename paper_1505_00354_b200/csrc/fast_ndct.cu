@@ -213,7 +213,7 @@ __device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, do
 // last pass did NOT read (returned: the one it read), so no barrier is needed
 // before the first store. In place: a barrier orders the first store after
 // the previous term's last-pass reads.
-template <int LOG2N, bool ODD, int NM>
+template <int LOG2N, bool ODD, int NM, bool PPX = Cfg<LOG2N>::PP>
 __device__ __forceinline__ double2* fwd_term(const double* stage, double* next, double2* zx,
                                              double2* zy, int t, int bar, double2 ta_t,
                                              double2 r4_t, const double2* fftw, const double* p,
@@ -225,7 +225,7 @@ __device__ __forceinline__ double2* fwd_term(const double* stage, double* next, 
   fwd_pack_all<N, ODD, NM, 0>(v, stage, next, t, ta_t, r4_t);
   pass_compute<P, E, 8, 1, true>(v, t, fftw);
   double2* fin = zx;
-  if constexpr (C::PP) {
+  if constexpr (PPX) {
     pass_store<P, E, 8, 1>(v, zx, t);
     group_sync<C::GT>(bar);
     fin = mid_passes_pp<P, E, 8, NSL, true, C::GT, true>(zx, zy, t, fftw, bar);
@@ -405,7 +405,7 @@ __device__ __forceinline__ double tr_unpack(double2 za, double2 zc, double2 tn, 
 // ping-pong (C::PP) as in fwd_term (returns the buffer the unpack read; the
 // caller passes the other one as the next zx), else in place with a barrier
 // ordering the first store after the previous term's unpack reads.
-template <int LOG2N, bool ODD, int PM>
+template <int LOG2N, bool ODD, int PM, bool PPX = Cfg<LOG2N>::PP>
 __device__ __forceinline__ double2* tr_term(const double* hs, double* next, const double* nd,
                                             const double* __restrict__ delta, double inv_next,
                                             const double* __restrict__ wrow, double2* zx,
@@ -443,7 +443,7 @@ __device__ __forceinline__ double2* tr_term(const double* hs, double* next, cons
   }
   pass_compute<P, E, 8, 1, false>(v, t, fftw);
   double2* zb = zx;
-  if constexpr (C::PP) {
+  if constexpr (PPX) {
     pass_store<P, E, 8, 1>(v, zx, t);
     group_sync<C::GT>(bar);
     zb = mid_passes_pp<P, E, 8, P, false, C::GT>(zx, zy, t, fftw, bar);
@@ -585,6 +585,102 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   for (int i = 0; i < OWN; ++i) dst[tr_row<N>(t, i)] = o[i];
 }
 
+// One plain DCT-III / DST-III (odd = 1) or transpose per column: the
+// trig.hpp passes on the cheb1 grid. A single term needs neither the stage
+// double buffer nor ping-pong FFT rows nor shared tables, so a CTA takes
+// N*8 + one FFT row of shared memory and <= 128 registers: two or three CTAs
+// per SM overlap one column's loads with another's FFT (the pass is HBM-bound,
+// the many-term kernels above are not).
+template <int LOG2N>
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 2)
+    fast_dct_plain_fwd_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
+                              size_t ld_out, size_t batch, int odd,
+                              const double2* __restrict__ tw4n, const double2* __restrict__ fftw,
+                              int* nonfinite) {
+  using C = Cfg<LOG2N>;
+  constexpr int N = C::N, T = C::T, OWN = C::OWN;
+  constexpr size_t COLW = N + C::ZB / sizeof(double);
+  extern __shared__ double smem[];
+  const int g = threadIdx.x / T, t = threadIdx.x % T;
+  const int bar = 1 + g;
+  const size_t col = (size_t)blockIdx.x * C::COLS + g;
+  if (col >= batch) return;
+  double* stage = smem + g * COLW;
+  double2* zb = reinterpret_cast<double2*>(stage + N);
+  const double* src = in + col * ld_in;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) {
+    const double v = __ldcs(src + t + T * i);
+    bad |= !isfinite(v);
+    stage[t + T * i] = v;
+  }
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
+  double f[OWN], p[OWN];
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) {
+    f[i] = 0.0;
+    p[i] = 1.0;
+  }
+  const double2 ta_t = __ldg(&tw4n[t]);
+  const double2 r4_t = __ldg(&tw4n[4 * t]);
+  group_sync<C::GT>(bar);
+  if (odd)
+    fwd_term<LOG2N, true, 0, false>(stage, nullptr, zb, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+  else
+    fwd_term<LOG2N, false, 0, false>(stage, nullptr, zb, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+  group_sync<C::GT>(bar);
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) stage[fwd_own_row<LOG2N>(t, i)] = f[i];
+  group_sync<C::GT>(bar);
+  double* dst = out + col * ld_out;
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) __stcs(dst + t + T * i, stage[t + T * i]);
+}
+
+template <int LOG2N>
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 2)
+    fast_dct_plain_tr_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
+                             size_t ld_out, size_t batch, int odd,
+                             const double2* __restrict__ tw4n, const double2* __restrict__ fftw,
+                             int* nonfinite) {
+  using C = Cfg<LOG2N>;
+  constexpr int N = C::N, T = C::T, OWN = C::OWN;
+  constexpr size_t COLW = N + C::ZB / sizeof(double);
+  extern __shared__ double smem[];
+  const int g = threadIdx.x / T, t = threadIdx.x % T;
+  const int bar = 1 + g;
+  const size_t col = (size_t)blockIdx.x * C::COLS + g;
+  if (col >= batch) return;
+  double* hs = smem + g * COLW;
+  double2* zb = reinterpret_cast<double2*>(hs + N);
+  const double* src = in + col * ld_in;
+  double o[OWN], rp[OWN];
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) {
+    const int k = t + T * i;
+    const double v = __ldcs(src + k);
+    bad |= !isfinite(v);
+    hs[tr_slot<N>(k)] = v;
+    o[i] = 0.0;
+    rp[i] = 1.0;
+  }
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
+  const double2 ta_t = __ldg(&tw4n[t]);
+  const double2 r4_t = __ldg(&tw4n[4 * t]);
+  group_sync<C::GT>(bar);
+  if (odd)
+    tr_term<LOG2N, true, 0, false>(hs, nullptr, nullptr, nullptr, 0.0, nullptr, zb, zb, t, bar,
+                                   ta_t, r4_t, fftw, rp, o, 1.0);
+  else
+    tr_term<LOG2N, false, 0, false>(hs, nullptr, nullptr, nullptr, 0.0, nullptr, zb, zb, t, bar,
+                                    ta_t, r4_t, fftw, rp, o, 1.0);
+  double* dst = out + col * ld_out;
+#pragma unroll
+  for (int i = 0; i < OWN; ++i) __stcs(dst + tr_row<N>(t, i), o[i]);
+}
+
 __global__ void tw4n_kernel(double2* tw, unsigned long long n) {
   const unsigned long long q = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
   if (q >= 2 * n) return;
@@ -619,6 +715,19 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
   const double2* fftw = pass_twiddles(LOG2N - 1);
   const bool use_bes = bes && bes->bes_terms > 0 && plain_op < 0;
   const size_t max_cols = (size_t)0x7fffffff * C::COLS;
+  if (plain_op >= 0 && !mult) {
+    const size_t smem = C::COLS * (C::N * sizeof(double) + C::ZB);
+    for (size_t c0 = 0; c0 < batch; c0 += max_cols) {
+      const size_t nc = batch - c0 < max_cols ? batch - c0 : max_cols;
+      const unsigned grid = (unsigned)((nc + C::COLS - 1) / C::COLS);
+      auto kern = transpose ? fast_dct_plain_tr_kernel<LOG2N> : fast_dct_plain_fwd_kernel<LOG2N>;
+      FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      kern<<<grid, C::THREADS, smem, s>>>(in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc,
+                                          plain_op, tw, fftw, nonfinite);
+      note_launch(transpose ? "fast_dct_plain_tr_kernel" : "fast_dct_plain_fwd_kernel");
+    }
+    return;
+  }
   for (size_t c0 = 0; c0 < batch; c0 += max_cols) {
     const size_t nc = batch - c0 < max_cols ? batch - c0 : max_cols;
     const unsigned grid = (unsigned)((nc + C::COLS - 1) / C::COLS);
