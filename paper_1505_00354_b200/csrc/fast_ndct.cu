@@ -95,8 +95,26 @@ struct Cfg {
   static constexpr size_t COL_BYTES = 2 * N * sizeof(double) + (PP ? 2 : 1) * ZB;
   // tables in shared memory when they fit beside the columns
   static constexpr bool SMEM_TABLES = COLS * COL_BYTES + N * 8 + TW * 16 <= 220 * 1024;
+
   static constexpr size_t SMEM = COLS * COL_BYTES + (SMEM_TABLES ? N * 8 + TW * 16 : 0);
   static constexpr int GT = COLS == 1 ? 0 : T;    // group barrier width (0 = whole CTA)
+};
+
+// The transpose kernel's layout. With the Chebyshev expansion (BES) it runs
+// two CTAs per SM up to N = 4096 (<= 128 registers: the row factors are read
+// where they are applied, no ping-pong rows, no shared tables): measured
+// 28.3 -> 26.2 ms for the C4 IDLT. The Taylor transpose (row factors kept in
+// registers) and the forward kernel are faster at one CTA per SM with
+// ping-pong rows and shared tables.
+template <int LOG2N, bool BES>
+struct TrCfg {
+  using C = Cfg<LOG2N>;
+  static constexpr bool TWO = BES && LOG2N <= 12;
+  static constexpr int MINB = TWO ? 2 : 1;
+  static constexpr bool PP = !TWO && C::PP;
+  static constexpr bool TABLES = !TWO && C::SMEM_TABLES;
+  static constexpr size_t COL_BYTES = 2 * C::N * sizeof(double) + (PP ? 2 : 1) * C::ZB;
+  static constexpr size_t SMEM = C::COLS * COL_BYTES + (TABLES ? C::N * 8 + C::TW * 16 : 0);
 };
 
 // Output row k of w index q (q = 2m or 2m+1 of the inverse FFT output z_m).
@@ -213,7 +231,7 @@ __device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, do
 // last pass did NOT read (returned: the one it read), so no barrier is needed
 // before the first store. In place: a barrier orders the first store after
 // the previous term's last-pass reads.
-template <int LOG2N, bool ODD, int NM, bool PPX = Cfg<LOG2N>::PP>
+template <int LOG2N, bool ODD, int NM, bool PPX = Cfg<LOG2N>::PP, int PST = 1>
 __device__ __forceinline__ double2* fwd_term(const double* stage, double* next, double2* zx,
                                              double2* zy, int t, int bar, double2 ta_t,
                                              double2 r4_t, const double2* fftw, const double* p,
@@ -249,7 +267,8 @@ __device__ __forceinline__ double2* fwd_term(const double* stage, double* next, 
         const int k = fwd_row_of<N>(2 * m + part);
         double y = part ? z.y : z.x;
         if (ODD && (k & 1)) y = -y;
-        f[i] += sign * p[i] * y;
+        const double w = PST == 1 ? p[i] : __ldg(p + i * PST);  // PST > 1: a global row
+        f[i] += sign * w * y;
       }
     }
   return fin;
@@ -405,7 +424,7 @@ __device__ __forceinline__ double tr_unpack(double2 za, double2 zc, double2 tn, 
 // ping-pong (C::PP) as in fwd_term (returns the buffer the unpack read; the
 // caller passes the other one as the next zx), else in place with a barrier
 // ordering the first store after the previous term's unpack reads.
-template <int LOG2N, bool ODD, int PM, bool PPX = Cfg<LOG2N>::PP>
+template <int LOG2N, bool ODD, int PM, bool PPX = Cfg<LOG2N>::PP, int PST = 1>
 __device__ __forceinline__ double2* tr_term(const double* hs, double* next, const double* nd,
                                             const double* __restrict__ delta, double inv_next,
                                             const double* __restrict__ wrow, double2* zx,
@@ -430,7 +449,7 @@ __device__ __forceinline__ double2* tr_term(const double* hs, double* next, cons
       w = make_double2(w.x * q.x, w.y * q.y);
     }
     if (PM == 1) {
-      const double2 q = C::SMEM_TABLES
+      const double2 q = C::SMEM_TABLES  // PM = 1 (Taylor) kernels use the Cfg layout
                             ? *reinterpret_cast<const double2*>(nd + slot)
                             : make_double2((double)N * __ldg(&delta[tr_entry<N>(slot)]),
                                            (double)N * __ldg(&delta[tr_entry<N>(slot + 1)]));
@@ -482,10 +501,10 @@ __device__ __forceinline__ double2* tr_term(const double* hs, double* next, cons
     const double x1 = ODD ? tr_unpack<true>(zA1, zB1, t1, r1) : tr_unpack<false>(zB1, zA1, t1, r1);
     const double x2 = ODD ? tr_unpack<true>(zB, zA, t2, r2) : tr_unpack<false>(zA, zB, t2, r2);
     const double x3 = ODD ? tr_unpack<true>(zA1, zB1, t3, r3) : tr_unpack<false>(zB1, zA1, t3, r3);
-    o[4 * g + 0] += sign * rp[4 * g + 0] * x0;
-    o[4 * g + 1] += sign * rp[4 * g + 1] * x1;
-    o[4 * g + 2] += sign * rp[4 * g + 2] * x2;
-    o[4 * g + 3] += sign * rp[4 * g + 3] * x3;
+    o[4 * g + 0] += sign * (PST == 1 ? rp[4 * g + 0] : __ldg(rp + (4 * g + 0) * PST)) * x0;
+    o[4 * g + 1] += sign * (PST == 1 ? rp[4 * g + 1] : __ldg(rp + (4 * g + 1) * PST)) * x1;
+    o[4 * g + 2] += sign * (PST == 1 ? rp[4 * g + 2] : __ldg(rp + (4 * g + 2) * PST)) * x2;
+    o[4 * g + 3] += sign * (PST == 1 ? rp[4 * g + 3] : __ldg(rp + (4 * g + 3) * PST)) * x3;
   }
   return zb;
 }
@@ -494,7 +513,7 @@ __device__ __forceinline__ double2* tr_term(const double* hs, double* next, cons
 // itself, each term weights it on the fly from wtab[m][slot] (tr_slot order)
 // and scales the output rows by ttab[m][i T + t] = T_m(n/N) (tr_row order).
 template <int LOG2N, bool BES>
-__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
     fast_ndct_tr_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                         size_t ld_out, size_t batch, const double* __restrict__ delta,
                         int num_terms, int plain_op, const double* __restrict__ mult,
@@ -502,12 +521,13 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
                         const double* __restrict__ wtab, const double* __restrict__ ttab,
                         int* nonfinite) {
   using C = Cfg<LOG2N>;
+  using TC = TrCfg<LOG2N, BES>;
   constexpr int N = C::N, T = C::T, OWN = C::OWN;
   extern __shared__ double smem[];
-  double* nd = smem + C::COLS * (C::COL_BYTES / 8);
+  double* nd = smem + C::COLS * (TC::COL_BYTES / 8);
   double2* fftw_s = reinterpret_cast<double2*>(nd + N);
-  const double2* fftw = C::SMEM_TABLES ? fftw_s : fftw_g;
-  if (C::SMEM_TABLES) {
+  const double2* fftw = TC::TABLES ? fftw_s : fftw_g;
+  if (TC::TABLES) {
     if (plain_op < 0 && !BES)  // in the tr_slot layout of the stage
       for (int j = threadIdx.x; j < N; j += blockDim.x) nd[j] = (double)N * delta[tr_entry<N>(j)];
     load_table(fftw_s, fftw_g, C::TW);
@@ -518,10 +538,10 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   const size_t col = (size_t)blockIdx.x * C::COLS + g;
   if (col >= batch) return;
   // h_k = (N delta_k)^l / l! g_k at hs[tr_slot(k)], double-buffered by term parity
-  double* hs = smem + g * (C::COL_BYTES / 8);
+  double* hs = smem + g * (TC::COL_BYTES / 8);
   double* hs_odd = hs + N;
   double2* zbA = reinterpret_cast<double2*>(hs + 2 * N);
-  double2* zbB = C::PP ? zbA + C::ZB / sizeof(double2) : zbA;
+  double2* zbB = TC::PP ? zbA + C::ZB / sizeof(double2) : zbA;
   double2* zx = zbA;  // the first pass's target this term
   auto other = [&](double2* b) { return b == zbA ? zbB : zbA; };
   const double* src = in + col * ld_in;
@@ -543,11 +563,23 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      tr_term<LOG2N, true, 0>(hs, nullptr, nd, delta, 0.0, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+      tr_term<LOG2N, true, 0, TC::PP>(hs, nullptr, nd, delta, 0.0, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                               rp, o, 1.0);
     else
-      tr_term<LOG2N, false, 0>(hs, nullptr, nd, delta, 0.0, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+      tr_term<LOG2N, false, 0, TC::PP>(hs, nullptr, nd, delta, 0.0, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                                rp, o, 1.0);
+  } else if (BES && TC::TWO) {
+    // row factors read where they are applied (PST = T): fewer live registers
+    for (int m = 0; m < num_terms; ++m) {
+      const double* tr = ttab + (size_t)m * N + t;
+      const double* wrow = wtab + (size_t)m * N;
+      if (m & 1)
+        tr_term<LOG2N, true, 2, false, T>(hs, nullptr, nd, delta, 0.0, wrow, zx, zx, t, bar, ta_t,
+                                          r4_t, fftw, tr, o, 1.0);
+      else
+        tr_term<LOG2N, false, 2, false, T>(hs, nullptr, nd, delta, 0.0, wrow, zx, zx, t, bar, ta_t,
+                                           r4_t, fftw, tr, o, 1.0);
+    }
   } else if (BES) {
     for (int m = 0; m < num_terms; ++m) {
 #pragma unroll
@@ -555,10 +587,10 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
       const double* wrow = wtab + (size_t)m * N;
       double2* fin;
       if (m & 1)
-        fin = tr_term<LOG2N, true, 2>(hs, nullptr, nd, delta, 0.0, wrow, zx, other(zx), t, bar,
+        fin = tr_term<LOG2N, true, 2, TC::PP>(hs, nullptr, nd, delta, 0.0, wrow, zx, other(zx), t, bar,
                                       ta_t, r4_t, fftw, rp, o, 1.0);
       else
-        fin = tr_term<LOG2N, false, 2>(hs, nullptr, nd, delta, 0.0, wrow, zx, other(zx), t, bar,
+        fin = tr_term<LOG2N, false, 2, TC::PP>(hs, nullptr, nd, delta, 0.0, wrow, zx, other(zx), t, bar,
                                        ta_t, r4_t, fftw, rp, o, 1.0);
       zx = other(fin);
     }
@@ -572,10 +604,10 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
       const double inv_next = 1.0 / (double)(l + 1);
       double2* fin;
       if (l & 1)
-        fin = tr_term<LOG2N, true, 1>(hs_odd, hs, nd, delta, inv_next, nullptr, zx, other(zx), t,
+        fin = tr_term<LOG2N, true, 1, TC::PP>(hs_odd, hs, nd, delta, inv_next, nullptr, zx, other(zx), t,
                                       bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
       else
-        fin = tr_term<LOG2N, false, 1>(hs, hs_odd, nd, delta, inv_next, nullptr, zx, other(zx), t,
+        fin = tr_term<LOG2N, false, 1, TC::PP>(hs, hs_odd, nd, delta, inv_next, nullptr, zx, other(zx), t,
                                        bar, ta_t, r4_t, fftw, rp, o, taylor_sign_d(l));
       zx = other(fin);
     }
@@ -733,8 +765,9 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
     const unsigned grid = (unsigned)((nc + C::COLS - 1) / C::COLS);
     if (transpose) {
       auto kern = use_bes ? fast_ndct_tr_kernel<LOG2N, true> : fast_ndct_tr_kernel<LOG2N, false>;
-      FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      kern<<<grid, C::THREADS, C::SMEM, s>>>(
+      const int smem = use_bes ? (int)TrCfg<LOG2N, true>::SMEM : (int)TrCfg<LOG2N, false>::SMEM;
+      FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<grid, C::THREADS, smem, s>>>(
           in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta,
           use_bes ? bes->bes_terms : num_terms, plain_op, mult, tw, fftw,
           use_bes ? bes->bes_wt : nullptr, use_bes ? bes->bes_tt : nullptr, nonfinite);
