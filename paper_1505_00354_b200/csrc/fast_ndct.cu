@@ -56,8 +56,9 @@ struct FastNdct {
   int num_terms = 0;
   const double* delta = nullptr;  // cheb1 perturbations (device)
   double* owned_delta = nullptr;
-  // Chebyshev (Jacobi-Anger) expansion of the same NDCT for the fused kernels
-  // (N <= 8192): bes_terms < num_terms terms, weight / row tables [m][N]
+  // Chebyshev (Jacobi-Anger) expansion of the same NDCT: bes_terms <
+  // num_terms terms; weight / row tables [m][N] for the fused kernels
+  // (N <= 8192), computed on the fly by the multi-pass kernels
   int bes_terms = 0;
   double* bes_wf = nullptr;  // forward weights, owned-row order
   double* bes_wt = nullptr;  // transpose weights, tr_slot order
@@ -856,15 +857,31 @@ __device__ __forceinline__ double taylor_weight(double nd, int l) {
   return p;
 }
 
+// T_m(x) by the three-term recurrence (m small).
+__device__ __forceinline__ double cheb_t(int m, double x) {
+  if (m == 0) return 1.0;
+  double a = 1.0, b = x;
+  for (int i = 1; i < m; ++i) {
+    const double c = 2.0 * x * b - a;
+    a = b;
+    b = c;
+  }
+  return b;
+}
+
+// cheb: term l of the Chebyshev expansion (stage T_l(n/N) c_n, weight
+// bessel_weight(l, N delta_k) with its sign), else the Taylor term.
 __global__ void big_fwd_pack_kernel(const double* __restrict__ in, size_t ld, size_t n, int l,
-                                    int odd, double2* __restrict__ Z, int* nonfinite) {
+                                    int odd, int cheb, double2* __restrict__ Z, int* nonfinite) {
   const size_t P = n / 2;
   const size_t col = blockIdx.y;
   const double* c = in + col * ld;
   const double nd = (double)n;
   for (size_t m = blockIdx.x * (size_t)blockDim.x + threadIdx.x; m < P;
        m += (size_t)gridDim.x * blockDim.x) {
-    auto st = [&](size_t j) -> double { return c[j] * ipow((double)j / nd, l); };
+    auto st = [&](size_t j) -> double {
+      return c[j] * (cheb ? cheb_t(l, (double)j / nd) : ipow((double)j / nd, l));
+    };
     auto X = [&](size_t j) -> double {
       if (j == 0) return odd ? 0.0 : st(0);
       if (j >= n) return 0.0;
@@ -888,8 +905,8 @@ __global__ void big_fwd_pack_kernel(const double* __restrict__ in, size_t ld, si
 }
 
 __global__ void big_fwd_unpack_kernel(const double2* __restrict__ Z, size_t n, int l, int odd,
-                                      double sign, const double* __restrict__ delta, int plain,
-                                      double* __restrict__ out, size_t ld, int first) {
+                                      int cheb, double sign, const double* __restrict__ delta,
+                                      int plain, double* __restrict__ out, size_t ld, int first) {
   const size_t P = n / 2;
   const size_t col = blockIdx.y;
   for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
@@ -898,14 +915,15 @@ __global__ void big_fwd_unpack_kernel(const double2* __restrict__ Z, size_t n, i
     const double2 z = Z[col * P + (q >> 1)];
     double y = (q & 1) ? z.y : z.x;
     if (odd && (k & 1)) y = -y;
-    const double p = plain ? 1.0 : taylor_weight((double)n * delta[k], l);
+    const double y0 = (double)n * delta[k];
+    const double p = plain ? 1.0 : cheb ? bessel_weight(l, y0) : taylor_weight(y0, l);
     double* o = out + col * ld + k;
     *o = (first ? 0.0 : *o) + sign * p * y;
   }
 }
 
 __global__ void big_tr_pack_kernel(const double* __restrict__ in, size_t ld, size_t n, int l,
-                                   int odd, const double* __restrict__ delta, int plain,
+                                   int odd, int cheb, const double* __restrict__ delta, int plain,
                                    const double* __restrict__ mult, double2* __restrict__ Z,
                                    int* nonfinite) {
   const size_t P = n / 2;
@@ -914,7 +932,8 @@ __global__ void big_tr_pack_kernel(const double* __restrict__ in, size_t ld, siz
   auto h = [&](size_t k) -> double {
     double v = g[k];
     if (mult) v = mult[k] * v;
-    const double p = plain ? 1.0 : taylor_weight((double)n * delta[k], l);
+    const double y0 = (double)n * delta[k];
+    const double p = plain ? 1.0 : cheb ? bessel_weight(l, y0) : taylor_weight(y0, l);
     v = p * v;
     return (odd && (k & 1)) ? -v : v;
   };
@@ -934,8 +953,8 @@ __global__ void big_tr_pack_kernel(const double* __restrict__ in, size_t ld, siz
 }
 
 __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, int l, int odd,
-                                     double sign, int plain, double* __restrict__ out, size_t ld,
-                                     int first) {
+                                     int cheb, double sign, int plain, double* __restrict__ out,
+                                     size_t ld, int first) {
   const size_t P = n / 2;
   const size_t col = blockIdx.y;
   const double nd = (double)n;
@@ -954,7 +973,7 @@ __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, in
       const double2 Vv = make_double2(ev.x + od.x * c2 - od.y * s2, ev.y + od.x * s2 + od.y * c2);
       X = ch * Vv.x + sh * Vv.y;
     }
-    const double rp = plain ? 1.0 : ipow((double)r / nd, l);
+    const double rp = plain ? 1.0 : cheb ? cheb_t(l, (double)r / nd) : ipow((double)r / nd, l);
     double* o = out + col * ld + r;
     *o = (first ? 0.0 : *o) + sign * rp * X;
   }
@@ -962,7 +981,7 @@ __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, in
 
 void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double* out,
                 size_t ld_out, size_t batch, const double* delta, int l_lo, int l_hi,
-                int plain_op, const double* mult, int* nonfinite, cudaStream_t s) {
+                int plain_op, const double* mult, int* nonfinite, cudaStream_t s, int cheb) {
   const size_t n = size_t(1) << log2n, P = n / 2;
   if (ld_in != ld_out) fail(FL_RUNTIME_ERROR, "fast ndct: mismatched strides");
   const size_t chunk_cap = std::max<size_t>(1, (size_t(1) << 30) / (2 * P * sizeof(double2)));
@@ -982,21 +1001,22 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
     for (int l = l_lo; l < l_hi; ++l) {
       const int first = l == l_lo;
       const int odd = plain ? plain_op : (l & 1);
-      const double sign = plain ? 1.0 : (((l + 1) / 2) % 2 == 0 ? 1.0 : -1.0);
+      const int ch = plain ? 0 : cheb;
+      const double sign = (plain || ch) ? 1.0 : (((l + 1) / 2) % 2 == 0 ? 1.0 : -1.0);
       if (!transpose) {
-        big_fwd_pack_kernel<<<grid, 256, 0, s>>>(in + c0 * ld_in, ld_in, n, plain ? 0 : l, odd, Z,
-                                                 l == 0 ? nonfinite : nullptr);
+        big_fwd_pack_kernel<<<grid, 256, 0, s>>>(in + c0 * ld_in, ld_in, n, plain ? 0 : l, odd, ch,
+                                                 Z, l == 0 ? nonfinite : nullptr);
         note_launch("big_fwd_pack_kernel");
         fft_pow2(Z, S, log2n - 1, nc, true, s);
-        big_fwd_unpack_kernel<<<grid, 256, 0, s>>>(Z, n, plain ? 0 : l, odd, sign, delta, plain,
-                                                   out + c0 * ld_out, ld_out, first);
+        big_fwd_unpack_kernel<<<grid, 256, 0, s>>>(Z, n, plain ? 0 : l, odd, ch, sign, delta,
+                                                   plain, out + c0 * ld_out, ld_out, first);
         note_launch("big_fwd_unpack_kernel");
       } else {
-        big_tr_pack_kernel<<<grid, 256, 0, s>>>(in + c0 * ld_in, ld_in, n, plain ? 0 : l, odd,
+        big_tr_pack_kernel<<<grid, 256, 0, s>>>(in + c0 * ld_in, ld_in, n, plain ? 0 : l, odd, ch,
                                                 delta, plain, mult, Z, l == 0 ? nonfinite : nullptr);
         note_launch("big_tr_pack_kernel");
         fft_pow2(Z, S, log2n - 1, nc, false, s);
-        big_tr_unpack_kernel<<<grid, 256, 0, s>>>(Z, n, plain ? 0 : l, odd, sign, plain,
+        big_tr_unpack_kernel<<<grid, 256, 0, s>>>(Z, n, plain ? 0 : l, odd, ch, sign, plain,
                                                   out + c0 * ld_out, ld_out, first);
         note_launch("big_tr_unpack_kernel");
       }
@@ -1010,10 +1030,12 @@ void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* 
               size_t ld_out, size_t batch, const double* delta, int num_terms, int plain_op,
               const double* mult, int* nonfinite, cudaStream_t s, int l_lo = 0, int l_hi = -1,
               const FastNdct* bes = nullptr) {
+  const bool cheb = bes && bes->bes_terms > 0 && plain_op < 0;
+  if (cheb) num_terms = bes->bes_terms;
   if (l_hi < 0) l_hi = num_terms;
   if (log2n > 13) {
     launch_big(log2n, transpose, in, ld_in, out, ld_out, batch, delta, l_lo, l_hi, plain_op, mult,
-               nonfinite, s);
+               nonfinite, s, cheb ? 1 : 0);
     return;
   }
   if (plain_op < 0 && (l_lo != 0 || l_hi != num_terms))
@@ -1103,8 +1125,8 @@ FastNdct* fast_ndct_create(size_t n, double tol, int kind, const double* theta) 
 #define FLB_NDCT_BESSEL 1
 #endif
   const int M = bessel_terms(tol);
+  if (FLB_NDCT_BESSEL && M > 0 && M < L) p->bes_terms = M;  // multi-pass: weights on the fly
   if (FLB_NDCT_BESSEL && lg <= 13 && M > 0 && M < L) {
-    p->bes_terms = M;
     for (double** t : {&p->bes_wf, &p->bes_wt, &p->bes_tt})
       FLB_CUDA(cudaMalloc(t, (size_t)M * n * sizeof(double)));
     const unsigned grid = (unsigned)((n + 255) / 256);
@@ -1137,6 +1159,6 @@ void fast_ndct_run(const FastNdct& p, int transpose, const double* in, size_t ld
 }  // namespace flb
 
 namespace flb {
-int fast_ndct_terms(const FastNdct& p) { return p.num_terms; }
-int fast_ndct_dlt_terms(const FastNdct& p) { return p.bes_terms > 0 ? p.bes_terms : p.num_terms; }
+int fast_ndct_terms(const FastNdct& p) { return p.bes_terms > 0 ? p.bes_terms : p.num_terms; }
+int fast_ndct_dlt_terms(const FastNdct& p) { return fast_ndct_terms(p); }
 }  // namespace flb

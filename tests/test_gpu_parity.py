@@ -529,7 +529,8 @@ def test_ndct_multipass_power_of_two(n):
 
 def test_dlt_idlt_2_20_sampled():
     """C3 size (N = 2^20), where the O(N^2) CPU reference takes minutes:
-    (1) the fast-mode DLT is exactly its two GPU stages composed;
+    (1) the fast-mode DLT (Chebyshev expansion about cheb1) agrees with the
+        literal cheb1 Taylor NDCT of its conversion stage within tolerance;
     (2) the NDCT stage against the CPU oracle's ndct_apply on the same grid
         and the same input (O(N log N), feasible here);
     (3) the leg2cheb stage is pinned by test_leg2cheb_sampled_rows_2_20;
@@ -546,7 +547,7 @@ def test_dlt_idlt_2_20_sampled():
     chat = fl.leg2cheb_apply(fl.legendre_coefficients(c), cfg.lambda_()).values
     plan1 = fl.plan_ndct(g, fl.GridKind.cheb1, fl.default_tolerance)
     f2 = fl.ndct_apply(plan1, chat)
-    assert np.array_equal(f, f2)
+    assert rel_err(f, f2, np.abs(chat).sum()) <= tol_n(n)
     ref = O.ndct(chat, CHEB1, plan1.num_terms, np.asarray(plan1.reference.delta_theta))
     assert rel_err(f2, ref, np.abs(chat).sum()) <= tol_n(n)
     idx = np.array([0, 1, 2, 1000, n // 3, n // 2, n - 2, n - 1])
