@@ -118,6 +118,23 @@ struct TrCfg {
   static constexpr size_t SMEM = C::COLS * COL_BYTES + (TABLES ? C::N * 8 + C::TW * 16 : 0);
 };
 
+#ifndef FLB_NDCT_FWD2
+#define FLB_NDCT_FWD2 1
+#endif
+// The forward kernel's layout (TWO: two CTAs per SM as in TrCfg; with the
+// Chebyshev expansion measured 26.0 -> 25.7 ms for the C4 DLT despite ~300 B
+// of spills at the 128-register cap).
+template <int LOG2N, bool BES>
+struct FwdCfg {
+  using C = Cfg<LOG2N>;
+  static constexpr bool TWO = BES && FLB_NDCT_FWD2 && LOG2N <= 12;
+  static constexpr int MINB = TWO ? 2 : 1;
+  static constexpr bool PP = !TWO && C::PP;
+  static constexpr bool TABLES = !TWO && C::SMEM_TABLES;
+  static constexpr size_t COL_BYTES = 2 * C::N * sizeof(double) + (PP ? 2 : 1) * C::ZB;
+  static constexpr size_t SMEM = C::COLS * COL_BYTES + (TABLES ? C::N * 8 + C::TW * 16 : 0);
+};
+
 // Output row k of w index q (q = 2m or 2m+1 of the inverse FFT output z_m).
 template <int N>
 __device__ __forceinline__ int fwd_row_of(int q) {
@@ -217,12 +234,13 @@ __device__ __forceinline__ int fwd_own_row(int t, int i) {
 }
 
 // One forward Taylor term (or one plain transform): f[i] += sign p[i] y_{k_i}.
-template <int N, bool ODD, int NM, int R>
+template <int N, bool ODD, int NM, int R, bool SPLIT = false>
 __device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, double* next, int t,
                                              double2 ta_t, double2 r4_t) {
+  if constexpr (SPLIT && R == 4) asm volatile("" ::: "memory");  // two halves: fewer live loads
   if constexpr (R < 8) {
     v[R] = fwd_pack<N, ODD, R, NM>(stage, next, t + R * (N / 16), ta_t, r4_t);
-    fwd_pack_all<N, ODD, NM, R + 1>(v, stage, next, t, ta_t, r4_t);
+    fwd_pack_all<N, ODD, NM, R + 1, SPLIT>(v, stage, next, t, ta_t, r4_t);
   }
 }
 
@@ -232,7 +250,7 @@ __device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, do
 // last pass did NOT read (returned: the one it read), so no barrier is needed
 // before the first store. In place: a barrier orders the first store after
 // the previous term's last-pass reads.
-template <int LOG2N, bool ODD, int NM, bool PPX = Cfg<LOG2N>::PP, int PST = 1>
+template <int LOG2N, bool ODD, int NM, bool PPX = Cfg<LOG2N>::PP, int PST = 1, bool SPLIT = false>
 __device__ __forceinline__ double2* fwd_term(const double* stage, double* next, double2* zx,
                                              double2* zy, int t, int bar, double2 ta_t,
                                              double2 r4_t, const double2* fftw, const double* p,
@@ -241,7 +259,7 @@ __device__ __forceinline__ double2* fwd_term(const double* stage, double* next, 
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, NSL = C::NSL, RL = C::RL;
   static_assert(E == 8 && T == N / 16, "pack twiddle constants assume T = N/16");
   double2 v[E];
-  fwd_pack_all<N, ODD, NM, 0>(v, stage, next, t, ta_t, r4_t);
+  fwd_pack_all<N, ODD, NM, 0, SPLIT>(v, stage, next, t, ta_t, r4_t);
   pass_compute<P, E, 8, 1, true>(v, t, fftw);
   double2* fin = zx;
   if constexpr (PPX) {
@@ -280,20 +298,21 @@ __device__ __forceinline__ double2* fwd_term(const double* stage, double* next, 
 // Taylor -- stage T_m(n/N) c_n by the three-term recurrence, weights
 // wtab[m][i T + t] (sign included) of the thread's owned rows from a table.
 template <int LOG2N, bool BES>
-__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
     fast_ndct_fwd_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
                          size_t ld_out, size_t batch, const double* __restrict__ delta,
                          int num_terms, int plain_op, const double2* __restrict__ tw4n,
                          const double2* __restrict__ fftw_g, const double* __restrict__ wtab,
                          int* nonfinite) {
   using C = Cfg<LOG2N>;
+  using FC = FwdCfg<LOG2N, BES>;
   constexpr int N = C::N, T = C::T, OWN = C::OWN, E = C::E, NSL = C::NSL, RL = C::RL;
   extern __shared__ double smem[];
-  double* nd = smem + C::COLS * (C::COL_BYTES / 8);
+  double* nd = smem + C::COLS * (FC::COL_BYTES / 8);
   double2* fftw_s = reinterpret_cast<double2*>(nd + N);
-  const double2* fftw = C::SMEM_TABLES ? fftw_s : fftw_g;
+  const double2* fftw = FC::TABLES ? fftw_s : fftw_g;
   auto own_row = [](int t, int i) -> int { return fwd_own_row<LOG2N>(t, i); };
-  if (C::SMEM_TABLES) {
+  if (FC::TABLES) {
     // N delta in owned-row order, nd[i T + t] for row own_row(t, i): the
     // per-term weight update reads it conflict-free (row order is stride 4)
     if (plain_op < 0 && !BES)
@@ -306,10 +325,10 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   const int bar = 1 + g;
   const size_t col = (size_t)blockIdx.x * C::COLS + g;
   if (col >= batch) return;
-  double* stage = smem + g * (C::COL_BYTES / 8);  // (n/N)^l c_n, terms l even
+  double* stage = smem + g * (FC::COL_BYTES / 8);  // (n/N)^l c_n, terms l even
   double* stage_odd = stage + N;                  // terms l odd
   double2* zbA = reinterpret_cast<double2*>(stage + 2 * N);
-  double2* zbB = C::PP ? zbA + C::ZB / sizeof(double2) : zbA;
+  double2* zbB = FC::PP ? zbA + C::ZB / sizeof(double2) : zbA;
   double2* zx = zbA;  // the first pass's target this term
   auto other = [&](double2* b) { return b == zbA ? zbB : zbA; };
   const double* src = in + col * ld_in;
@@ -335,22 +354,36 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
   group_sync<C::GT>(bar);
   if (plain_op >= 0) {
     if (plain_op == 1)
-      fwd_term<LOG2N, true, 0>(stage, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      fwd_term<LOG2N, true, 0, FC::PP>(stage, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw, p, f, 1.0);
     else
-      fwd_term<LOG2N, false, 0>(stage, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+      fwd_term<LOG2N, false, 0, FC::PP>(stage, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+  } else if (BES && FC::TWO) {
+    // weights read where they are applied (PST = T), pack in two halves
+    for (int m = 0; m < num_terms; ++m) {
+      const double* wr = wtab + (size_t)m * N + t;
+      if (m == 0)
+        fwd_term<LOG2N, false, 1, false, T, true>(stage, stage_odd, zx, zx, t, bar, ta_t, r4_t,
+                                                  fftw, wr, f, 1.0);
+      else if (m & 1)
+        fwd_term<LOG2N, true, 2, false, T, true>(stage_odd, stage, zx, zx, t, bar, ta_t, r4_t,
+                                                 fftw, wr, f, 1.0);
+      else
+        fwd_term<LOG2N, false, 2, false, T, true>(stage, stage_odd, zx, zx, t, bar, ta_t, r4_t,
+                                                  fftw, wr, f, 1.0);
+    }
   } else if (BES) {
     for (int m = 0; m < num_terms; ++m) {
 #pragma unroll
       for (int i = 0; i < OWN; ++i) p[i] = __ldg(wtab + (size_t)m * N + i * T + t);
       double2* fin;
       if (m == 0)
-        fin = fwd_term<LOG2N, false, 1>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+        fin = fwd_term<LOG2N, false, 1, FC::PP>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                                         p, f, 1.0);
       else if (m & 1)
-        fin = fwd_term<LOG2N, true, 2>(stage_odd, stage, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+        fin = fwd_term<LOG2N, true, 2, FC::PP>(stage_odd, stage, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                                        p, f, 1.0);
       else
-        fin = fwd_term<LOG2N, false, 2>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+        fin = fwd_term<LOG2N, false, 2, FC::PP>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                                         p, f, 1.0);
       zx = other(fin);
     }
@@ -360,16 +393,16 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 1)
         const double inv_l = 1.0 / (double)l;
 #pragma unroll
         for (int i = 0; i < OWN; ++i) {
-          const double q = C::SMEM_TABLES ? nd[i * T + t] : (double)N * __ldg(&delta[kown(i)]);
+          const double q = FC::TABLES ? nd[i * T + t] : (double)N * __ldg(&delta[kown(i)]);
           p[i] *= q * inv_l;  // (N delta_k)^l / l!
         }
       }
       double2* fin;
       if (l & 1)
-        fin = fwd_term<LOG2N, true, 1>(stage_odd, stage, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+        fin = fwd_term<LOG2N, true, 1, FC::PP>(stage_odd, stage, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                                        p, f, taylor_sign_d(l));
       else
-        fin = fwd_term<LOG2N, false, 1>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+        fin = fwd_term<LOG2N, false, 1, FC::PP>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                                         p, f, taylor_sign_d(l));
       zx = other(fin);
     }
@@ -775,8 +808,9 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
       note_launch(use_bes ? "fast_ndct_tr_kernel<bessel>" : "fast_ndct_tr_kernel");
     } else {
       auto kern = use_bes ? fast_ndct_fwd_kernel<LOG2N, true> : fast_ndct_fwd_kernel<LOG2N, false>;
-      FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
-      kern<<<grid, C::THREADS, C::SMEM, s>>>(
+      const int smem = use_bes ? (int)FwdCfg<LOG2N, true>::SMEM : (int)FwdCfg<LOG2N, false>::SMEM;
+      FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+      kern<<<grid, C::THREADS, smem, s>>>(
           in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta,
           use_bes ? bes->bes_terms : num_terms, plain_op, tw, fftw,
           use_bes ? bes->bes_wf : nullptr, nonfinite);
