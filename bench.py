@@ -368,7 +368,12 @@ def main() -> None:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": desc, "N": n, "columns": total, "columns_per_rank": per,
-                       "grid": "chebstar (default TransformConfig), NDCT evaluated about cheb1 (fast mode)",
+                       "grid": "chebstar (default TransformConfig), NDCT evaluated about cheb1 (fast mode, "
+                               "14-term Chebyshev expansion)",
+                       "arithmetic": "fp64 throughout; the Legendre->Chebyshev product as an exact "
+                                     "int8 digit-split GEMM on the tcgen05 tensor cores (8 digits/operand, "
+                                     "int32 accumulation, fp64 recombination; fl_plan_set_gemm_mode "
+                                     "selects the fp64 DMMA product instead)",
                        "parallelism": f"column shards x{world}, no collective",
                        "l2": "inputs (2 GiB) larger than L2 (126 MB); no flush"},
             "roofline": {"bound": "fp64", "kernel": "fast_ndct_fwd_kernel", "dominant": dom,
