@@ -435,13 +435,19 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       // least significant accumulator first
 #pragma unroll 1
       for (int d = S - 1; d >= 0; --d) {
-        const double w = ldexp(1.0, -7 * (d + 2));
+        // exact S_d 2^{-7(d+2)} without the int->fp64 conversion unit: the
+        // biased integer becomes the low mantissa bits of a double whose ulp
+        // is 2^{-7(d+2)}; subtracting the bias constant is exact
+        const int sh = 7 * (d + 2);
+        const int hi_word = (1075 - sh) << 20;
+        const double bias = ldexp(1.0, 52 - sh) + ldexp(1.0, 31 - sh);
 #pragma unroll
         for (int h = 0; h < BN / 32; ++h) {
           uint32_t v[32];
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * BN + h * 32), v);
 #pragma unroll
-          for (int c = 0; c < 32; ++c) acc[h * 32 + c] = fma((double)(int)v[c], w, acc[h * 32 + c]);
+          for (int c = 0; c < 32; ++c)
+            acc[h * 32 + c] += __hiloint2double(hi_word, (int)(v[c] ^ 0x80000000u)) - bias;
         }
       }
       tc_fence_before();
@@ -668,13 +674,19 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
       for (int c = 0; c < BN; ++c) acc[c] = 0.0;
 #pragma unroll 1
       for (int d = S - 1; d >= 0; --d) {
-        const double w = ldexp(1.0, -7 * (d + 2));
+        // exact S_d 2^{-7(d+2)} without the int->fp64 conversion unit: the
+        // biased integer becomes the low mantissa bits of a double whose ulp
+        // is 2^{-7(d+2)}; subtracting the bias constant is exact
+        const int sh = 7 * (d + 2);
+        const int hi_word = (1075 - sh) << 20;
+        const double bias = ldexp(1.0, 52 - sh) + ldexp(1.0, 31 - sh);
 #pragma unroll
         for (int h = 0; h < BN / 32; ++h) {
           uint32_t v[32];
           tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * BN + h * 32), v);
 #pragma unroll
-          for (int c = 0; c < 32; ++c) acc[h * 32 + c] = fma((double)(int)v[c], w, acc[h * 32 + c]);
+          for (int c = 0; c < 32; ++c)
+            acc[h * 32 + c] += __hiloint2double(hi_word, (int)(v[c] ^ 0x80000000u)) - bias;
         }
       }
       tc_fence_before();
