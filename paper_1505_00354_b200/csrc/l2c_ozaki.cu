@@ -155,6 +155,19 @@ __device__ __forceinline__ uint64_t smem_desc(uint32_t saddr) {
 __device__ __forceinline__ void mbar_arrive(uint32_t bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
 }
+__device__ __forceinline__ void tmem_ld32_nowait(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, "
+      "%28, %29, %30, %31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+        "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+        "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tmem_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
@@ -441,14 +454,16 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
         const int sh = 7 * (d + 2);
         const int hi_word = (1075 - sh) << 20;
         const double bias = ldexp(1.0, 52 - sh) + ldexp(1.0, 31 - sh);
+        uint32_t v[BN / 32][32];  // both halves in flight before one wait
 #pragma unroll
-        for (int h = 0; h < BN / 32; ++h) {
-          uint32_t v[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * BN + h * 32), v);
+        for (int h = 0; h < BN / 32; ++h)
+          tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * BN + h * 32), v[h]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int h = 0; h < BN / 32; ++h)
 #pragma unroll
           for (int c = 0; c < 32; ++c)
-            acc[h * 32 + c] += __hiloint2double(hi_word, (int)(v[c] ^ 0x80000000u)) - bias;
-        }
+            acc[h * 32 + c] += __hiloint2double(hi_word, (int)(v[h][c] ^ 0x80000000u)) - bias;
       }
       tc_fence_before();
       mbar_arrive(smem_u32(tempty_b));  // TMEM free for the next tile
@@ -680,14 +695,16 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
         const int sh = 7 * (d + 2);
         const int hi_word = (1075 - sh) << 20;
         const double bias = ldexp(1.0, 52 - sh) + ldexp(1.0, 31 - sh);
+        uint32_t v[BN / 32][32];  // both halves in flight before one wait
 #pragma unroll
-        for (int h = 0; h < BN / 32; ++h) {
-          uint32_t v[32];
-          tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * BN + h * 32), v);
+        for (int h = 0; h < BN / 32; ++h)
+          tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * BN + h * 32), v[h]);
+        tmem_wait_ld();
+#pragma unroll
+        for (int h = 0; h < BN / 32; ++h)
 #pragma unroll
           for (int c = 0; c < 32; ++c)
-            acc[h * 32 + c] += __hiloint2double(hi_word, (int)(v[c] ^ 0x80000000u)) - bias;
-        }
+            acc[h * 32 + c] += __hiloint2double(hi_word, (int)(v[h][c] ^ 0x80000000u)) - bias;
       }
       tc_fence_before();
       mbar_arrive_remote(tempty_leader);  // TMEM free for the pair's next tile
