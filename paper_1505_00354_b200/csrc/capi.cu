@@ -296,6 +296,35 @@ void run_ndct(const char* where, int transpose, int kind, size_t n, int num_term
   if (h) fail(FL_INVALID_ARGUMENT, std::string(where) + ": non-finite input");
 }
 
+// The NDCT inside dlt/idlt without a host round trip of its own: the
+// non-finite flag is read once, after everything else, by finish_ndct (whose
+// device-to-pageable copy is the call's synchronisation point).
+struct DeferredNdct {
+  DevScratch<int> flag;
+  explicit DeferredNdct(cudaStream_t s) : flag(1, s) {
+    FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+  }
+  void run(const char* where, int transpose, int kind, size_t n, int num_terms,
+           const double* delta, const double* in, size_t ld_in, double* out, size_t ld_out,
+           size_t batch, const double* in_mult, const FastNdct* fast, cudaStream_t s) {
+    if (overflow_guard(n, num_terms)) {  // the reference's order: non-finite, then overflow
+      run_ndct(where, transpose, kind, n, num_terms, delta, in, ld_in, out, ld_out, batch,
+               in_mult, fast, s);
+      return;
+    }
+    enqueue_ndct(transpose, kind, n, num_terms, delta, in, ld_in, out, ld_out, batch, in_mult,
+                 fast, flag.p, s);
+    where_ = where;
+  }
+  void finish(cudaStream_t s) {
+    int h = 0;
+    FLB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    sync(s);
+    if (h) fail(FL_INVALID_ARGUMENT, std::string(where_) + ": non-finite input");
+  }
+  const char* where_ = "ndct_apply";
+};
+
 // ---- host-buffer pipeline ------------------------------------------------
 // A transform of host columns (host in, host out) is cut into column chunks
 // that flow through three streams -- H2D copy | compute | D2H copy -- with three
@@ -894,18 +923,19 @@ fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, 
       cin = packed.p;
     }
     plan_convert(mp, 0, cin, chat.p, batch, n, s);
+    DeferredNdct nd(s);
     if (o.ld != n) {
       DevScratch<double> f(n * batch, s);
-      run_ndct("ndct_apply", 0, p->kind, n, p->num_terms, p->delta, chat.p, n, f.p, n, batch,
-               nullptr, fast, s);
+      nd.run("ndct_apply", 0, p->kind, n, p->num_terms, p->delta, chat.p, n, f.p, n, batch,
+             nullptr, fast, s);
       FLB_CUDA(cudaMemcpy2DAsync(o.ptr, o.ld * 8, f.p, n * 8, n * 8, batch,
                                  cudaMemcpyDeviceToDevice, s));
     } else {
-      run_ndct("ndct_apply", 0, p->kind, n, p->num_terms, p->delta, chat.p, n, o.ptr, n, batch,
-               nullptr, fast, s);
+      nd.run("ndct_apply", 0, p->kind, n, p->num_terms, p->delta, chat.p, n, o.ptr, n, batch,
+             nullptr, fast, s);
     }
     o.finish();
-    sync(s);
+    nd.finish(s);
   });
 }
 
@@ -934,19 +964,20 @@ fl_status fl_idlt(const fl_plan* p, const double* in, double* out, size_t batch,
     DevOut o(out, n, batch, ld, s);
     // transforms.hpp:58-62: back = NDCT^T(w . f); c = (m + 1/2) M^T back
     DevScratch<double> back(n * batch, s);
+    DeferredNdct nd(s);
     if (i.ld != n) {
       DevScratch<double> f(n * batch, s);
       FLB_CUDA(cudaMemcpy2DAsync(f.p, n * 8, i.ptr, i.ld * 8, n * 8, batch,
                                  cudaMemcpyDeviceToDevice, s));
-      run_ndct("ndct_apply_transpose", 1, p->kind, n, p->num_terms, p->delta, f.p, n, back.p, n,
-               batch, p->w, fast, s);
+      nd.run("ndct_apply_transpose", 1, p->kind, n, p->num_terms, p->delta, f.p, n, back.p, n,
+             batch, p->w, fast, s);
     } else {
-      run_ndct("ndct_apply_transpose", 1, p->kind, n, p->num_terms, p->delta, i.ptr, n, back.p,
-               n, batch, p->w, fast, s);
+      nd.run("ndct_apply_transpose", 1, p->kind, n, p->num_terms, p->delta, i.ptr, n, back.p, n,
+             batch, p->w, fast, s);
     }
     plan_convert(mp, 1, back.p, o.ptr, batch, o.ld, s);
     o.finish();
-    sync(s);
+    nd.finish(s);
   });
 }
 
