@@ -704,6 +704,128 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 2)
   for (int i = 0; i < OWN; ++i) __stcs(dst + t + T * i, stage[t + T * i]);
 }
 
+// Persistent, prefetching variant of the plain forward pass for one column
+// per CTA (N >= 4096): while a CTA transforms column i, a bulk copy
+// (cp.async.bulk, mbarrier completion) brings column i + grid into the other
+// stage buffer, so the column load no longer stalls the FFT.
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes,
+                                          uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          dst),
+      "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_init1(uint32_t bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar));
+}
+__device__ __forceinline__ void mbar_expect(uint32_t bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "W_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@P1 bra D_%=;\n\t"
+      "bra W_%=;\n"
+      "D_%=:\n\t}" ::"r"(bar),
+      "r"(parity)
+      : "memory");
+}
+
+// Shared memory: one stage buffer, one FFT row, the pass twiddles. The next
+// column's bulk copy into the stage buffer is issued as soon as every thread
+// has packed the current one (after the first pass's barrier), so it overlaps
+// the remaining passes; the output is staged through the FFT row.
+// Twiddles in shared memory at two CTAs per SM (1.30 ms for 65536 columns of
+// 4096) beat global twiddles at three CTAs and 80 registers (1.43 ms, spills).
+#ifndef FLB_STREAM_TW_SMEM
+#define FLB_STREAM_TW_SMEM 1
+#endif
+template <int LOG2N>
+struct StreamCfg {
+  using C = Cfg<LOG2N>;
+  static constexpr bool TW_SMEM = FLB_STREAM_TW_SMEM != 0;
+  static constexpr size_t SMEM =
+      C::N * sizeof(double) + C::ZB + (TW_SMEM ? C::TW * sizeof(double2) : 0);
+  static constexpr int MINB = LOG2N <= 12 ? (TW_SMEM ? 2 : 3) : 1;
+};
+
+template <int LOG2N>
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, StreamCfg<LOG2N>::MINB)
+    fast_dct_stream_fwd_kernel(const double* __restrict__ in, size_t ld_in,
+                               double* __restrict__ out, size_t ld_out, size_t batch, int odd,
+                               const double2* __restrict__ tw4n, const double2* __restrict__ fftw_g,
+                               int* nonfinite) {
+  using C = Cfg<LOG2N>;
+  static_assert(C::COLS == 1, "one column per CTA");
+  constexpr int N = C::N, P = C::P, T = C::T, E = C::E, OWN = C::OWN, NSL = C::NSL, RL = C::RL;
+  extern __shared__ double smem[];
+  __shared__ uint64_t mbar;
+  double* stage = smem;
+  double2* zb = reinterpret_cast<double2*>(smem + N);
+  double* zo = smem + N;  // output staging (the FFT row, after the last pass)
+  double2* fftw_s = reinterpret_cast<double2*>(smem + N + C::ZB / sizeof(double));
+  const double2* fftw = StreamCfg<LOG2N>::TW_SMEM ? fftw_s : fftw_g;
+  const int t = threadIdx.x;
+  const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar));
+  const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
+  if (t == 0) {
+    mbar_init1(bar);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (StreamCfg<LOG2N>::TW_SMEM) load_table(fftw_s, fftw_g, C::TW);
+  __syncthreads();
+  size_t col = blockIdx.x;
+  if (t == 0 && col < batch) {
+    mbar_expect(bar, N * 8);
+    bulk_load(stage_s, in + col * ld_in, N * 8, bar);
+  }
+  const double2 ta_t = __ldg(&tw4n[t]);
+  const double2 r4_t = __ldg(&tw4n[4 * t]);
+  bool bad = false;
+  for (uint32_t it = 0; col < batch; col += gridDim.x, ++it) {
+    __syncthreads();  // the previous column's output has left the FFT row
+    mbar_wait_parity(bar, it & 1u);
+#pragma unroll
+    for (int i = 0; i < OWN; ++i) bad |= !isfinite(stage[t + T * i]);
+    double2 v[E];
+    if (odd)
+      fwd_pack_all<N, true, 0, 0>(v, stage, nullptr, t, ta_t, r4_t);
+    else
+      fwd_pack_all<N, false, 0, 0>(v, stage, nullptr, t, ta_t, r4_t);
+    pass_compute<P, E, 8, 1, true>(v, t, fftw);
+    pass_store<P, E, 8, 1>(v, zb, t);
+    __syncthreads();  // every thread has packed: the stage buffer takes the next column
+    const size_t nxt = col + gridDim.x;
+    if (t == 0 && nxt < batch) {
+      mbar_expect(bar, N * 8);
+      bulk_load(stage_s, in + nxt * ld_in, N * 8, bar);
+    }
+    mid_passes<P, E, 8, NSL, true, 0, true>(zb, t, fftw, 0);
+    pass_load<P, E, RL>(v, zb, t);
+    pass_compute<P, E, RL, NSL, true, true>(v, t, fftw + pass_tw_offset(P, NSL));
+    __syncthreads();  // all last-pass loads done: the FFT row stages the output
+#pragma unroll
+    for (int q = 0; q < E / RL; ++q)
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        const int m = t + q * T + r * NSL;
+        const double2 z = v[q * RL + r];
+        const int k0 = fwd_row_of<N>(2 * m), k1 = fwd_row_of<N>(2 * m + 1);
+        zo[k0] = (odd && (k0 & 1)) ? -z.x : z.x;
+        zo[k1] = (odd && (k1 & 1)) ? -z.y : z.y;
+      }
+    __syncthreads();
+    double* dst = out + col * ld_out;
+#pragma unroll
+    for (int i = 0; i < OWN; ++i) __stcs(dst + t + T * i, zo[t + T * i]);
+  }
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
+}
+
 template <int LOG2N>
 __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 2)
     fast_dct_plain_tr_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
@@ -781,6 +903,20 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
   const double2* fftw = pass_twiddles(LOG2N - 1);
   const bool use_bes = bes && bes->bes_terms > 0 && plain_op < 0;
   const size_t max_cols = (size_t)0x7fffffff * C::COLS;
+  if constexpr (C::COLS == 1) {
+    if (plain_op >= 0 && !mult && !transpose && ld_in == ld_out && (ld_in % 2) == 0 &&
+        (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+      const size_t smem = StreamCfg<LOG2N>::SMEM;
+      FLB_CUDA(cudaFuncSetAttribute(fast_dct_stream_fwd_kernel<LOG2N>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const unsigned grid =
+          (unsigned)std::min<size_t>(batch, (size_t)sm_count() * StreamCfg<LOG2N>::MINB);
+      fast_dct_stream_fwd_kernel<LOG2N><<<grid, C::THREADS, smem, s>>>(
+          in, ld_in, out, ld_out, batch, plain_op, tw, fftw, nonfinite);
+      note_launch("fast_dct_stream_fwd_kernel");
+      return;
+    }
+  }
   if (plain_op >= 0 && !mult) {
     const size_t smem = C::COLS * (C::N * sizeof(double) + C::ZB);
     for (size_t c0 = 0; c0 < batch; c0 += max_cols) {
