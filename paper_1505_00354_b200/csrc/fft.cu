@@ -98,6 +98,129 @@ __global__ void transpose_kernel(const double2* __restrict__ in, double2* __rest
   }
 }
 
+// ---- multi-pass FFT for P > 8192 ---------------------------------------------
+// P = R C: x[a1 + R a2] -> X[b2 + C b1]. The length-C transform over a2 (per
+// a1) is one line pass (C <= 4096) or two (C = C1 C2, a2 = c1 + C1 c2); the
+// twiddle w_P^{a1 b2} is applied on its way out, and a last pass transforms
+// the contiguous rows over a1 and writes X transposed. Every pass is a "line"
+// FFT in shared memory over lines of length L <= 4096: line l (lo = l mod M,
+// hi = l / M) reads src[lo + hi Hin + e Sin] and writes
+// dst[lo + hi Hout + k Sout] * w_Q^{lo (hi u + k v) + hi k z}. CTAs take
+// adjacent lines (adjacent lo), so every global access is a run of
+// LINES * 16 B. Six-step needed six read+write passes; this needs two (P <=
+// 2^23) or three.
+struct LineMap {
+  unsigned long long M, Hin, Sin, Hout, Sout;   // addressing (M a power of two)
+  unsigned long long Q, u, v, z;                // twiddle exponent (Q = 0: none; a power of two)
+};
+
+template <int LOG2L>
+struct LinePass {
+  static constexpr int L = 1 << LOG2L;
+  static constexpr int E = 8;
+  static constexpr int TL = L / E;                                   // threads per line
+  static constexpr int LINES = L >= 4096 ? 2 : L >= 1024 ? 4 : 8;    // lines per CTA
+  static constexpr int THREADS = TL * LINES;
+  // per-line named barriers need whole warps; short lines sync CTA-wide
+  static constexpr int GT = TL % 32 != 0 ? 0 : TL;
+  // line stride in smem: one extra element so the LINES lines that a warp's
+  // global-order loads / stores touch fall in different banks
+  static constexpr int LS = smem_row(L) + 1;
+  static constexpr size_t SMEM = (size_t)LINES * LS * sizeof(double2);
+};
+
+template <int LOG2L, bool INV>
+__global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
+    fft_line_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
+                    unsigned long long P, LineMap mp, const double2* __restrict__ tw) {
+  using Q = LinePass<LOG2L>;
+  constexpr int L = Q::L, LINES = Q::LINES;
+  extern __shared__ double2 sm[];
+  const size_t item = blockIdx.y;
+  const double2* x = src + item * P;
+  double2* y = dst + item * P;
+  const unsigned long long l0 = (unsigned long long)blockIdx.x * LINES;
+  const unsigned long long mmask = mp.M - 1, qmask = mp.Q - 1;
+  const int mshift = __ffsll((long long)mp.M) - 1;
+  const bool rows_in = mp.Sin == 1;  // contiguous lines: element index fastest
+  for (int i = threadIdx.x; i < LINES * L; i += blockDim.x) {
+    const int j = rows_in ? i / L : i % LINES, e = rows_in ? i % L : i / LINES;
+    const unsigned long long l = l0 + j, lo = l & mmask, hi = l >> mshift;
+    sm[j * Q::LS + smem_pad(e)] = x[lo + hi * mp.Hin + (unsigned long long)e * mp.Sin];
+  }
+  __syncthreads();
+  const int line = threadIdx.x / Q::TL, tid = threadIdx.x % Q::TL;
+  fft_row_smem<L, Q::E, INV, Q::GT>(sm + line * Q::LS, tid, tw, 1 + line);
+  __syncthreads();
+  for (int i = threadIdx.x; i < LINES * L; i += blockDim.x) {
+    const int j = i % LINES, k = i / LINES;
+    const unsigned long long l = l0 + j, lo = l & mmask, hi = l >> mshift;
+    double2 v = sm[j * Q::LS + smem_pad(k)];
+    if (mp.Q) {
+      const unsigned long long kk = (unsigned long long)k;
+      // exponent mod Q by masks (wrap-around of the 64-bit products is harmless mod 2^k)
+      const unsigned long long m = (lo * (hi * mp.u + kk * mp.v) + hi * kk * mp.z) & qmask;
+      double sn, cs;
+      sincospi(2.0 * (double)m / (double)mp.Q, &sn, &cs);
+      if (!INV) sn = -sn;
+      v = make_double2(v.x * cs - v.y * sn, v.x * sn + v.y * cs);
+    }
+    y[lo + hi * mp.Hout + (unsigned long long)k * mp.Sout] = v;
+  }
+}
+
+template <int LOG2L, bool INV>
+void launch_line(const double2* src, double2* dst, unsigned long long P, size_t items,
+                 const LineMap& mp, cudaStream_t s) {
+  using Q = LinePass<LOG2L>;
+  const double2* tw = pass_twiddles(LOG2L);
+  const unsigned long long lines = P >> LOG2L;
+  FLB_CUDA(cudaFuncSetAttribute(fft_line_kernel<LOG2L, INV>,
+                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM));
+  dim3 grid((unsigned)(lines / Q::LINES), (unsigned)items);
+  fft_line_kernel<LOG2L, INV><<<grid, Q::THREADS, Q::SMEM, s>>>(src, dst, P, mp, tw);
+  note_launch("fft_line_kernel");
+}
+
+template <bool INV>
+void line_pass(int log2l, const double2* src, double2* dst, unsigned long long P, size_t items,
+               const LineMap& mp, cudaStream_t s) {
+  switch (log2l) {
+    case 5: launch_line<5, INV>(src, dst, P, items, mp, s); break;
+    case 6: launch_line<6, INV>(src, dst, P, items, mp, s); break;
+    case 7: launch_line<7, INV>(src, dst, P, items, mp, s); break;
+    case 8: launch_line<8, INV>(src, dst, P, items, mp, s); break;
+    case 9: launch_line<9, INV>(src, dst, P, items, mp, s); break;
+    case 10: launch_line<10, INV>(src, dst, P, items, mp, s); break;
+    case 11: launch_line<11, INV>(src, dst, P, items, mp, s); break;
+    case 12: launch_line<12, INV>(src, dst, P, items, mp, s); break;
+    default: fail(FL_RUNTIME_ERROR, "fft: unsupported line length");
+  }
+}
+
+template <bool INV>
+void fft_multipass(double2* d, double2* t, int log2p, size_t items, cudaStream_t s) {
+  const unsigned long long P = 1ull << log2p;
+  const int passes = log2p <= 24 ? 2 : 3;
+  const int lr = passes == 2 ? log2p / 2 : log2p / 3;  // rows (last pass)
+  const int lc = log2p - lr;
+  const unsigned long long R = 1ull << lr, C = 1ull << lc;
+  if (passes == 2) {
+    // columns over a2 (stride R), twiddle w_P^{a1 b2}: d -> t at a1 + R b2
+    line_pass<INV>(lc, d, t, P, items, LineMap{R, 0, R, 0, R, P, 0, 1, 0}, s);
+  } else {
+    const int l1 = lc / 2, l2 = lc - l1;  // a2 = c1 + C1 c2
+    const unsigned long long C1 = 1ull << l1, C2 = 1ull << l2;
+    // over c2 (stride R C1), in place, twiddle w_C^{c1 d2}: lines l = a1 + R c1
+    line_pass<INV>(l2, d, d, P, items, LineMap{R, R, R * C1, R, R * C1, C, 0, 0, 1}, s);
+    // over c1 (stride R) -> t at a1 + R (d2 + C2 d1), twiddle w_P^{a1 (d2 + C2 d1)};
+    // lines l = a1 + R d2: lo = a1, hi = d2
+    line_pass<INV>(l1, d, t, P, items, LineMap{R, R * C1, R, R, R * C2, P, 1, C2, 0}, s);
+  }
+  // rows over a1 (contiguous), written transposed to X[b2 + C b1]: lines l = b2
+  line_pass<INV>(lr, t, d, P, items, LineMap{1, R, 1, 1, C, 0, 0, 0, 0}, s);
+}
+
 template <int LOG2P, bool INV>
 void launch_smem(double2* data, size_t rows, const double2* tw, cudaStream_t s) {
   constexpr int P = 1 << LOG2P;
@@ -218,20 +341,13 @@ void fft_pow2(double2* data, double2* scratch, int log2p, size_t batch, bool inv
     fft_rows(data, log2p, batch, inverse, s);
     return;
   }
-  const int lr = log2p / 2, lc = log2p - lr;
-  const int R = 1 << lr, C = 1 << lc;
   const unsigned long long P = 1ull << log2p;
-  // x[a1 + R a2] viewed as A[a2][a1] (C x R)
   for (size_t b0 = 0; b0 < batch; b0 += 65535) {
     const size_t nb = batch - b0 < 65535 ? batch - b0 : 65535;
-    double2* d = data + b0 * P;
-    double2* t = scratch + b0 * P;
-    transpose(d, t, C, R, nb, 0, inverse, s);           // T1[a1][a2]
-    fft_rows(t, lc, nb * R, inverse, s);                // Y[a1][b2]
-    transpose(t, d, R, C, nb, P, inverse, s);           // T2[b2][a1] * w^{a1 b2}
-    fft_rows(d, lr, nb * C, inverse, s);                // T2[b2][b1] = X[b2 + C b1]
-    transpose(d, t, C, R, nb, 0, inverse, s);           // X[b1][b2]
-    FLB_CUDA(cudaMemcpyAsync(d, t, nb * P * sizeof(double2), cudaMemcpyDeviceToDevice, s));
+    if (inverse)
+      fft_multipass<true>(data + b0 * P, scratch + b0 * P, log2p, nb, s);
+    else
+      fft_multipass<false>(data + b0 * P, scratch + b0 * P, log2p, nb, s);
   }
 }
 
