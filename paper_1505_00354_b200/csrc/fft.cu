@@ -114,12 +114,15 @@ struct LineMap {
   unsigned long long Q, u, v, z;                // twiddle exponent (Q = 0: none; a power of two)
 };
 
+// lines per CTA of a pass over lines of 2^log2l
+constexpr int line_ctas_lines(int log2l) { return log2l >= 12 ? 2 : log2l >= 10 ? 4 : 8; }
+
 template <int LOG2L>
 struct LinePass {
   static constexpr int L = 1 << LOG2L;
   static constexpr int E = 8;
   static constexpr int TL = L / E;                                   // threads per line
-  static constexpr int LINES = L >= 4096 ? 2 : L >= 1024 ? 4 : 8;    // lines per CTA
+  static constexpr int LINES = line_ctas_lines(LOG2L);
   static constexpr int THREADS = TL * LINES;
   // per-line named barriers need whole warps; short lines sync CTA-wide
   static constexpr int GT = TL % 32 != 0 ? 0 : TL;
@@ -129,96 +132,217 @@ struct LinePass {
   static constexpr size_t SMEM = (size_t)LINES * LS * sizeof(double2);
 };
 
-template <int LOG2L, bool INV>
+// What a line pass reads (IN: IO_PACK builds the Toeplitz-Hankel operand from
+// x and the l_r rows) and whether it is the fused row pass (MID: forward
+// transform, symbol product, inverse transform).
+enum { IO_PLAIN = 0, IO_PACK = 1 };
+// Loads of a pass issued all at once (registers) before the shared-memory
+// stores: faster for lines of <= 512 points (2^26: 327 vs 338 ms per C5
+// DLT), slower above (2^20: 4.11 vs 3.78 ms per C3 DLT).
+constexpr bool line_unroll(int log2l) { return log2l <= 9; }
+struct LineIO {
+  const double2* src;
+  double2* dst;
+  ThArgs th;
+};
+
+__device__ __forceinline__ double2 th_pack_value(const ThArgs& a, size_t item,
+                                                 unsigned long long b) {
+  double2 v = make_double2(0.0, 0.0);
+  if (b < a.np) {
+    const unsigned long long k = 2 * b + a.p;
+    double u = a.x[k];
+    if (a.transpose && k != 0) u *= 2.0;
+    const int ra = a.ra0 + 2 * (int)item;
+    v.x = a.ell[(size_t)ra * a.np + b] * u;
+    if (ra + 1 < a.K) v.y = a.ell[(size_t)(ra + 1) * a.np + b] * u;
+  }
+  return v;
+}
+
+template <int LOG2L, bool INV, int IN, bool MID>
 __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
-    fft_line_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
-                    unsigned long long P, LineMap mp, const double2* __restrict__ tw) {
+    fft_line_kernel(LineIO io, unsigned long long P, LineMap mp, const double2* __restrict__ tw) {
   using Q = LinePass<LOG2L>;
-  constexpr int L = Q::L, LINES = Q::LINES;
+  constexpr int L = Q::L, LINES = Q::LINES, PER = LINES * L / Q::THREADS;
+  // the store twiddle belongs to the direction of the last transform
+  constexpr bool TW_INV = MID ? !INV : INV;
   extern __shared__ double2 sm[];
-  const size_t item = blockIdx.y;
-  const double2* x = src + item * P;
-  double2* y = dst + item * P;
   const unsigned long long l0 = (unsigned long long)blockIdx.x * LINES;
   const unsigned long long mmask = mp.M - 1, qmask = mp.Q - 1;
   const int mshift = __ffsll((long long)mp.M) - 1;
-  const bool rows_in = mp.Sin == 1;  // contiguous lines: element index fastest
-  for (int i = threadIdx.x; i < LINES * L; i += blockDim.x) {
-    const int j = rows_in ? i / L : i % LINES, e = rows_in ? i % L : i / LINES;
-    const unsigned long long l = l0 + j, lo = l & mmask, hi = l >> mshift;
-    sm[j * Q::LS + smem_pad(e)] = x[lo + hi * mp.Hin + (unsigned long long)e * mp.Sin];
-  }
-  __syncthreads();
+  const bool rows_in = mp.Sin == 1;   // contiguous lines: element index fastest
+  const bool rows_out = mp.Sout == 1;
   const int line = threadIdx.x / Q::TL, tid = threadIdx.x % Q::TL;
-  fft_row_smem<L, Q::E, INV, Q::GT>(sm + line * Q::LS, tid, tw, 1 + line);
-  __syncthreads();
-  for (int i = threadIdx.x; i < LINES * L; i += blockDim.x) {
-    const int j = i % LINES, k = i / LINES;
-    const unsigned long long l = l0 + j, lo = l & mmask, hi = l >> mshift;
-    double2 v = sm[j * Q::LS + smem_pad(k)];
-    if (mp.Q) {
-      const unsigned long long kk = (unsigned long long)k;
-      // exponent mod Q by masks (wrap-around of the 64-bit products is harmless mod 2^k)
-      const unsigned long long m = (lo * (hi * mp.u + kk * mp.v) + hi * kk * mp.z) & qmask;
-      double sn, cs;
-      sincospi(2.0 * (double)m / (double)mp.Q, &sn, &cs);
-      if (!INV) sn = -sn;
-      v = make_double2(v.x * cs - v.y * sn, v.x * sn + v.y * cs);
+  // MID: the symbol rows of this CTA's lines, staged next to the data when
+  // both fit (else read in the product loop)
+  constexpr bool SYM_SMEM = MID && 2 * Q::SMEM <= 80 * 1024;  // keeps >= 2 CTAs per SM
+  double2* sym_s = sm + LINES * Q::LS;
+  {
+    const size_t item = blockIdx.y;
+    // all PER loads of a thread are issued before the first smem store
+    if constexpr (line_unroll(LOG2L)) {
+      double2 v[PER];
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int i = threadIdx.x + r * Q::THREADS;
+        const int j = rows_in ? i / L : i % LINES, e = rows_in ? i % L : i / LINES;
+        const unsigned long long l = l0 + j, lo = l & mmask, hi = l >> mshift;
+        const unsigned long long g = lo + hi * mp.Hin + (unsigned long long)e * mp.Sin;
+        if constexpr (IN == IO_PACK)
+          v[r] = th_pack_value(io.th, item, g);
+        else
+          v[r] = io.src[item * P + g];
+      }
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int i = threadIdx.x + r * Q::THREADS;
+        const int j = rows_in ? i / L : i % LINES, e = rows_in ? i % L : i / LINES;
+        sm[j * Q::LS + smem_pad(e)] = v[r];
+      }
+    } else {
+      for (int i = threadIdx.x; i < LINES * L; i += blockDim.x) {
+        const int j = rows_in ? i / L : i % LINES, e = rows_in ? i % L : i / LINES;
+        const unsigned long long l = l0 + j, lo = l & mmask, hi = l >> mshift;
+        const unsigned long long g = lo + hi * mp.Hin + (unsigned long long)e * mp.Sin;
+        double2 v;
+        if constexpr (IN == IO_PACK)
+          v = th_pack_value(io.th, item, g);
+        else
+          v = io.src[item * P + g];
+        sm[j * Q::LS + smem_pad(e)] = v;
+      }
     }
-    y[lo + hi * mp.Hout + (unsigned long long)k * mp.Sout] = v;
+    if constexpr (SYM_SMEM) {
+      for (int i = threadIdx.x; i < LINES * L; i += blockDim.x) {
+        double2 w = io.th.sym[(l0 + i / L) * L + i % L];
+        if (!io.th.transpose) w.y = -w.y;
+        sym_s[(i / L) * Q::LS + smem_pad(i % L)] = w;
+      }
+    }
+    __syncthreads();
+    fft_row_smem<L, Q::E, INV, Q::GT>(sm + line * Q::LS, tid, tw, 1 + line);
+    if constexpr (MID) {
+      // row l = b2 holds X[b2 + C b1] at k = b1: times the symbol (stored
+      // row-major [b2][b1] by th_symbol_layout), then back over b1 -> a1
+      __syncthreads();
+#pragma unroll
+      for (int r = 0; r < PER; ++r) {
+        const int i = threadIdx.x + r * Q::THREADS;
+        const int o = (i / L) * Q::LS + smem_pad(i % L);
+        double2 w;
+        if constexpr (SYM_SMEM) {
+          w = sym_s[o];
+        } else {
+          w = io.th.sym[(l0 + i / L) * L + i % L];
+          if (!io.th.transpose) w.y = -w.y;
+        }
+        sm[o] = cmul(sm[o], w);
+      }
+      __syncthreads();
+      fft_row_smem<L, Q::E, !INV, Q::GT>(sm + line * Q::LS, tid, tw, 1 + line);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int i = threadIdx.x + r * Q::THREADS;
+      const int j = rows_out ? i / L : i % LINES, k = rows_out ? i % L : i / LINES;
+      const unsigned long long l = l0 + j, lo = l & mmask, hi = l >> mshift;
+      double2 x = sm[j * Q::LS + smem_pad(k)];
+      if (mp.Q) {
+        const unsigned long long kk = (unsigned long long)k;
+        // exponent mod Q by masks (wrap-around of the 64-bit products is harmless mod 2^k)
+        const unsigned long long m = (lo * (hi * mp.u + kk * mp.v) + hi * kk * mp.z) & qmask;
+        double sn, cs;
+        sincospi(2.0 * (double)m / (double)mp.Q, &sn, &cs);
+        if (!TW_INV) sn = -sn;
+        x = make_double2(x.x * cs - x.y * sn, x.x * sn + x.y * cs);
+      }
+      const unsigned long long g = lo + hi * mp.Hout + (unsigned long long)k * mp.Sout;
+      io.dst[item * P + g] = x;
+    }
   }
 }
 
-template <int LOG2L, bool INV>
-void launch_line(const double2* src, double2* dst, unsigned long long P, size_t items,
-                 const LineMap& mp, cudaStream_t s) {
+template <int LOG2L, bool INV, int IN, bool MID>
+void launch_line(const LineIO& io, unsigned long long P, size_t items, const LineMap& mp,
+                 cudaStream_t s) {
   using Q = LinePass<LOG2L>;
+  static_assert(Q::LINES * Q::L == Q::THREADS * Q::E, "one element per thread per E");
   const double2* tw = pass_twiddles(LOG2L);
   const unsigned long long lines = P >> LOG2L;
-  FLB_CUDA(cudaFuncSetAttribute(fft_line_kernel<LOG2L, INV>,
-                                cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM));
+  auto kern = fft_line_kernel<LOG2L, INV, IN, MID>;
+  // MID: + the symbol rows when they fit
+  const size_t smem = MID && 2 * Q::SMEM <= 80 * 1024 ? 2 * Q::SMEM : Q::SMEM;
+  FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)(lines / Q::LINES), (unsigned)items);
-  fft_line_kernel<LOG2L, INV><<<grid, Q::THREADS, Q::SMEM, s>>>(src, dst, P, mp, tw);
+  kern<<<grid, Q::THREADS, smem, s>>>(io, P, mp, tw);
   note_launch("fft_line_kernel");
 }
 
-template <bool INV>
-void line_pass(int log2l, const double2* src, double2* dst, unsigned long long P, size_t items,
-               const LineMap& mp, cudaStream_t s) {
+template <bool INV, int IN = IO_PLAIN, bool MID = false>
+void line_pass(int log2l, const LineIO& io, unsigned long long P, size_t items, const LineMap& mp,
+               cudaStream_t s) {
   switch (log2l) {
-    case 5: launch_line<5, INV>(src, dst, P, items, mp, s); break;
-    case 6: launch_line<6, INV>(src, dst, P, items, mp, s); break;
-    case 7: launch_line<7, INV>(src, dst, P, items, mp, s); break;
-    case 8: launch_line<8, INV>(src, dst, P, items, mp, s); break;
-    case 9: launch_line<9, INV>(src, dst, P, items, mp, s); break;
-    case 10: launch_line<10, INV>(src, dst, P, items, mp, s); break;
-    case 11: launch_line<11, INV>(src, dst, P, items, mp, s); break;
-    case 12: launch_line<12, INV>(src, dst, P, items, mp, s); break;
+    case 5: launch_line<5, INV, IN, MID>(io, P, items, mp, s); break;
+    case 6: launch_line<6, INV, IN, MID>(io, P, items, mp, s); break;
+    case 7: launch_line<7, INV, IN, MID>(io, P, items, mp, s); break;
+    case 8: launch_line<8, INV, IN, MID>(io, P, items, mp, s); break;
+    case 9: launch_line<9, INV, IN, MID>(io, P, items, mp, s); break;
+    case 10: launch_line<10, INV, IN, MID>(io, P, items, mp, s); break;
+    case 11: launch_line<11, INV, IN, MID>(io, P, items, mp, s); break;
+    case 12: launch_line<12, INV, IN, MID>(io, P, items, mp, s); break;
     default: fail(FL_RUNTIME_ERROR, "fft: unsupported line length");
   }
 }
 
 template <bool INV>
+void line_pass(int log2l, const double2* src, double2* dst, unsigned long long P, size_t items,
+               const LineMap& mp, cudaStream_t s) {
+  LineIO io{};
+  io.src = src;
+  io.dst = dst;
+  line_pass<INV>(log2l, io, P, items, mp, s);
+}
+
+// The pass plan: 2 passes for P <= 2^24, else 3 (rows of 2^lr, columns of
+// 2^lc = 2^l1 * 2^l2).
+struct PassPlan {
+  int passes, lr, lc, l1, l2;
+  unsigned long long R, C, C1, C2;
+  explicit PassPlan(int log2p) {
+    passes = log2p <= 24 ? 2 : 3;
+    lr = passes == 2 ? log2p / 2 : log2p / 3;
+    lc = log2p - lr;
+    l1 = lc / 2;
+    l2 = lc - l1;
+    R = 1ull << lr;
+    C = 1ull << lc;
+    C1 = 1ull << l1;
+    C2 = 1ull << l2;
+  }
+  // columns over a2 (stride R), twiddle w_P^{a1 b2}: -> a1 + R b2 (2 passes)
+  LineMap col() const { return LineMap{R, 0, R, 0, R, twq(), 0, 1, 0}; }
+  // over c2 (stride R C1), in place, twiddle w_C^{c1 d2}: lines l = a1 + R c1
+  LineMap col1() const { return LineMap{R, R, R * C1, R, R * C1, C, 0, 0, 1}; }
+  // over c1 (stride R) -> a1 + R (d2 + C2 d1), twiddle w_P^{a1 (d2 + C2 d1)};
+  // lines l = a1 + R d2: lo = a1, hi = d2
+  LineMap col2() const { return LineMap{R, R * C1, R, R, R * C2, twq(), 1, C2, 0}; }
+  unsigned long long twq() const { return R * C; }
+};
+
+template <bool INV>
 void fft_multipass(double2* d, double2* t, int log2p, size_t items, cudaStream_t s) {
   const unsigned long long P = 1ull << log2p;
-  const int passes = log2p <= 24 ? 2 : 3;
-  const int lr = passes == 2 ? log2p / 2 : log2p / 3;  // rows (last pass)
-  const int lc = log2p - lr;
-  const unsigned long long R = 1ull << lr, C = 1ull << lc;
-  if (passes == 2) {
-    // columns over a2 (stride R), twiddle w_P^{a1 b2}: d -> t at a1 + R b2
-    line_pass<INV>(lc, d, t, P, items, LineMap{R, 0, R, 0, R, P, 0, 1, 0}, s);
+  const PassPlan pp(log2p);
+  if (pp.passes == 2) {
+    line_pass<INV>(pp.lc, d, t, P, items, pp.col(), s);
   } else {
-    const int l1 = lc / 2, l2 = lc - l1;  // a2 = c1 + C1 c2
-    const unsigned long long C1 = 1ull << l1, C2 = 1ull << l2;
-    // over c2 (stride R C1), in place, twiddle w_C^{c1 d2}: lines l = a1 + R c1
-    line_pass<INV>(l2, d, d, P, items, LineMap{R, R, R * C1, R, R * C1, C, 0, 0, 1}, s);
-    // over c1 (stride R) -> t at a1 + R (d2 + C2 d1), twiddle w_P^{a1 (d2 + C2 d1)};
-    // lines l = a1 + R d2: lo = a1, hi = d2
-    line_pass<INV>(l1, d, t, P, items, LineMap{R, R * C1, R, R, R * C2, P, 1, C2, 0}, s);
+    line_pass<INV>(pp.l2, d, d, P, items, pp.col1(), s);
+    line_pass<INV>(pp.l1, d, t, P, items, pp.col2(), s);
   }
   // rows over a1 (contiguous), written transposed to X[b2 + C b1]: lines l = b2
-  line_pass<INV>(lr, t, d, P, items, LineMap{1, R, 1, 1, C, 0, 0, 0, 0}, s);
+  line_pass<INV>(pp.lr, t, d, P, items, LineMap{1, pp.R, 1, 1, pp.C, 0, 0, 0, 0}, s);
 }
 
 template <int LOG2P, bool INV>
@@ -349,6 +473,48 @@ void fft_pow2(double2* data, double2* scratch, int log2p, size_t batch, bool inv
     else
       fft_multipass<false>(data + b0 * P, scratch + b0 * P, log2p, nb, s);
   }
+}
+
+void th_symbol_layout(double2* sym, double2* scratch, int log2p, cudaStream_t s) {
+  const PassPlan pp(log2p);
+  // natural S[b2 + C b1] (R rows of C) -> [b2][b1]
+  transpose(sym, scratch, (int)pp.R, (int)pp.C, 1, 0, false, s);
+  FLB_CUDA(cudaMemcpyAsync(sym, scratch, (pp.R * pp.C) * sizeof(double2), cudaMemcpyDeviceToDevice,
+                           s));
+}
+
+void th_sweep(const ThArgs& a, int log2p, size_t pairs, double2* V, double2* S, cudaStream_t s) {
+  if (log2p <= kMaxSmemLog2 || log2p > kMaxLog2) fail(FL_RUNTIME_ERROR, "th_sweep: length");
+  if (pairs == 0) return;
+  if (pairs > 65535) fail(FL_RUNTIME_ERROR, "th_sweep: too many rank pairs");
+  const unsigned long long P = 1ull << log2p;
+  const PassPlan pp(log2p);
+  LineIO io{};
+  io.th = a;
+  // forward columns, the first one packing V_q from x and the l_r rows
+  if (pp.passes == 2) {
+    io.dst = S;
+    line_pass<false, IO_PACK>(pp.lc, io, P, pairs, pp.col(), s);
+  } else {
+    io.dst = V;
+    line_pass<false, IO_PACK>(pp.l2, io, P, pairs, pp.col1(), s);
+    io.src = V;
+    io.dst = S;
+    line_pass<false>(pp.l1, io, P, pairs, pp.col2(), s);
+  }
+  // rows b2 in place: forward over a1, times the symbol, inverse over b1,
+  // twiddle w_P^{-a1 b2}
+  io.src = S;
+  io.dst = S;
+  line_pass<false, IO_PLAIN, true>(pp.lr, io, P, pairs,
+                                   LineMap{1, pp.R, 1, pp.R, 1, P, 0, 0, 1}, s);
+  // inverse columns (natural b2 -> natural a2; the w_P twiddle is done)
+  if (pp.passes == 3) line_pass<true>(pp.l2, io, P, pairs, pp.col1(), s);
+  const int ll = pp.passes == 2 ? pp.lc : pp.l1;
+  LineMap last = pp.passes == 2 ? pp.col() : pp.col2();
+  last.Q = 0;
+  io.dst = V;
+  line_pass<true>(ll, io, P, pairs, last, s);
 }
 
 }  // namespace flb

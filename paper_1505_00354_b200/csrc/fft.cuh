@@ -22,6 +22,31 @@ void fft_pow2(double2* data, double2* scratch, int log2p, size_t batch, bool inv
 constexpr int kMaxSmemLog2 = 13;  // 8192 points = 128 KiB of double2 per CTA
 constexpr int kMaxLog2 = 26;
 
+// ---- fused Toeplitz-Hankel sweep (l2c_fast.cu) for 2^log2p > 8192 -------------
+// One batched sweep over rank pairs q < pairs computes, per pair,
+//   W_q = IFFT(FFT(V_q) . S~),  V_q[b] = (l_{ra}(b) u_b, l_{ra+1}(b) u_b) (b < np, else 0),
+// ra = ra0 + 2q, u_b = x[2b+p] (doubled for the transpose when 2b+p != 0),
+// S~ = conj(S) (forward) or S (transpose), into V (natural order,
+// unnormalised). The packing is done by the first FFT pass's loads, and the
+// last forward pass, the symbol product and the first inverse pass are one
+// row pass (the spectrum never leaves shared memory in transposed order):
+// 2 + 2 (P <= 2^24) or 3 + 2 sweeps instead of pack + 2 + mul + 2 + ... .
+// (Folding the l_r accumulation into the last inverse pass was measured
+// slower: its register footprint halves the resident CTAs.)
+struct ThArgs {
+  const double* x;
+  int p;
+  unsigned long long np;
+  const double* ell;
+  int K, ra0, transpose;
+  const double2* sym;   // the symbol spectrum in th_symbol_layout order
+};
+// Reorder a natural-order spectrum (length 2^log2p) for the fused sweep's row
+// pass (scratch: 2^log2p elements).
+void th_symbol_layout(double2* sym, double2* scratch, int log2p, cudaStream_t s);
+// V, S: pairs * 2^log2p elements each; W is left in V.
+void th_sweep(const ThArgs& a, int log2p, size_t pairs, double2* V, double2* S, cudaStream_t s);
+
 // Register-resident small DFTs (natural order in and out).
 template <bool INV>
 __device__ __forceinline__ void dft2(double2& a, double2& b) {

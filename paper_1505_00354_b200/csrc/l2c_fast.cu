@@ -34,7 +34,8 @@ struct L2CFast {
   size_t np[2] = {0, 0};
   int log2L[2] = {0, 0};
   double* ell[2] = {nullptr, nullptr};     // K x np, row r = l_r
-  double2* shat[2] = {nullptr, nullptr};   // FFT_L of s~ (s_j for j < np)
+  double2* shat[2] = {nullptr, nullptr};   // FFT_L of s~ (s_j for j < np);
+                                           // th_symbol_layout order when L > 8192
 };
 
 namespace {
@@ -258,6 +259,8 @@ L2CFast* l2c_fast_create(size_t n, const double* s, cudaStream_t st) {
       symbol_kernel<<<grid1(L), 256, 0, st>>>(s, np, L, f->shat[p]);
       note_launch("symbol_kernel");
       fft_pow2(f->shat[p], scratch, lg, 1, false, st);
+      // the fused sweep reads the spectrum in its row-pass order
+      if (lg > kMaxSmemLog2) th_symbol_layout(f->shat[p], scratch, lg, st);
       if (scratch) cudaFreeAsync(scratch, st);
     }
     FLB_CUDA(cudaStreamSynchronize(st));
@@ -305,6 +308,15 @@ void l2c_fast_apply(const L2CFast& f, int transpose, const double* in, double* o
       if (pairs_total == 0) FLB_CUDA(cudaMemsetAsync(y, 0, np * sizeof(double), st));
       for (int q0 = 0; q0 < pairs_total; q0 += chunk) {
         const int pq = std::min(chunk, pairs_total - q0);
+        if (lg > kMaxSmemLog2) {
+          // packing and symbol product inside the FFT passes
+          const ThArgs a{x, p, np, f.ell[p], K, r_first + 2 * q0, transpose, f.shat[p]};
+          th_sweep(a, lg, (size_t)pq, V, S, st);
+          th_accum_kernel<<<grid1(np), 256, 0, st>>>(V, np, L, f.ell[p], K, r_first + 2 * q0, pq,
+                                                      y, q0 == 0);
+          note_launch("th_accum_kernel");
+          continue;
+        }
         dim3 g(grid1(L), (unsigned)pq);
         th_pack_kernel<<<g, 256, 0, st>>>(x, p, n, np, L, f.ell[p], K, r_first + 2 * q0, pq,
                                            transpose, V);

@@ -487,10 +487,12 @@ def test_leg2cheb_single_vector_large(n):
     assert rel_err(t, O.leg2cheb(c, True), np.abs(c).sum()) <= tol_n(n)
 
 
-def test_leg2cheb_sampled_rows_2_20():
-    """N = 2^20 (C3 size; the O(N^2) CPU loop is minutes): sampled rows of
-    conversion.hpp:106-111 / :126-133 restated in numpy, O(N) each."""
-    n = 1 << 20
+@pytest.mark.parametrize("n", [1 << 20, (1 << 22) + 5, (1 << 24) - 3])
+def test_leg2cheb_sampled_rows(n):
+    """N = 2^20 (C3 size; the O(N^2) CPU loop is minutes) and the two-pass
+    FFT sizes whose Toeplitz-Hankel sweep folds the accumulation into the last
+    inverse pass (L = 2^23, 2^24): sampled rows of conversion.hpp:106-111 /
+    :126-133 restated in numpy, O(N) each."""
     c = fl.random_decaying(n, 1.0, 3)
     f = fl.leg2cheb_apply(fl.legendre_coefficients(c)).values
     t = fl.leg2cheb_apply_transpose(c)
