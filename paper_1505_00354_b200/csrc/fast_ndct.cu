@@ -141,6 +141,15 @@ __device__ __forceinline__ int fwd_row_of(int q) {
   return q < N / 2 ? 2 * q : 2 * (N - 1 - q) + 1;
 }
 
+// Shared-memory slot of output row k when a column's outputs are staged for
+// a coalesced store: the rows a half-warp scatters are 4 apart (k = 4m + c,
+// consecutive m), four per 16 banks of doubles; XOR-ing bits 0-1 with bits
+// 4-5 spreads them over all 16 (the staging stores were 4-way conflicted,
+// 20% of the plain DCT pass's shared-memory wavefronts), and the row-order
+// reads (16 consecutive k) stay conflict-free. A permutation within each
+// aligned group of 4.
+__device__ __forceinline__ int out_slot(int k) { return k ^ ((k >> 4) & 3); }
+
 // e^{i pi r/32} and e^{i pi r/8}, r < 8: with T = N/16 threads per column the
 // pack twiddles of m = t + r T are per-thread bases times these constants.
 // (16 entries: the transpose's unpack uses rows n = t + i T, i < 16.)
@@ -190,12 +199,15 @@ __constant__ double kC8[16][2] = {
 // NM: 0 = no next stage; 1 = next = x c (Taylor (n/N)^{l+1} c_n, and the
 // Chebyshev T_1); 2 = next = 2 x cur - next (Chebyshev T_{m+1}(x) c_n, the
 // buffer `next` holding T_{m-1}(x) c_n), x = n/N.
+// bad (optional): set when stage[m] or stage[m + P] is not finite (every entry
+// is some thread's m or m + P), so a caller needs no separate check pass.
 template <int N, bool ODD, int R, int NM>
 __device__ __forceinline__ double2 fwd_pack(const double* stage, double* next, int m, double2 ta_t,
-                                            double2 r4_t) {
+                                            double2 r4_t, bool* bad = nullptr) {
   constexpr int P = N / 2;
   constexpr double h = 0.70710678118654752440;
   const double s_m = stage[m], s_mp = stage[m + P];
+  if (bad) *bad |= !isfinite(s_m) || !isfinite(s_mp);
   const double s_nm = stage[(N - m) & (N - 1)], s_pm = stage[P - m];
   if (NM == 1) {
     next[m] = s_m * ((double)m / (double)N);  // (n/N)^{l+1} c_n
@@ -236,11 +248,11 @@ __device__ __forceinline__ int fwd_own_row(int t, int i) {
 // One forward Taylor term (or one plain transform): f[i] += sign p[i] y_{k_i}.
 template <int N, bool ODD, int NM, int R, bool SPLIT = false>
 __device__ __forceinline__ void fwd_pack_all(double2* v, const double* stage, double* next, int t,
-                                             double2 ta_t, double2 r4_t) {
+                                             double2 ta_t, double2 r4_t, bool* bad = nullptr) {
   if constexpr (SPLIT && R == 4) asm volatile("" ::: "memory");  // two halves: fewer live loads
   if constexpr (R < 8) {
-    v[R] = fwd_pack<N, ODD, R, NM>(stage, next, t + R * (N / 16), ta_t, r4_t);
-    fwd_pack_all<N, ODD, NM, R + 1, SPLIT>(v, stage, next, t, ta_t, r4_t);
+    v[R] = fwd_pack<N, ODD, R, NM>(stage, next, t + R * (N / 16), ta_t, r4_t, bad);
+    fwd_pack_all<N, ODD, NM, R + 1, SPLIT>(v, stage, next, t, ta_t, r4_t, bad);
   }
 }
 
@@ -410,11 +422,11 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
   // scatter the owned rows through shared memory, then one coalesced store
   group_sync<C::GT>(bar);
 #pragma unroll
-  for (int i = 0; i < OWN; ++i) stage[kown(i)] = f[i];
+  for (int i = 0; i < OWN; ++i) stage[out_slot(kown(i))] = f[i];
   group_sync<C::GT>(bar);
   double* dst = out + col * ld_out;
 #pragma unroll
-  for (int i = 0; i < OWN; ++i) dst[t + T * i] = stage[t + T * i];
+  for (int i = 0; i < OWN; ++i) dst[t + T * i] = stage[out_slot(t + T * i)];
 }
 
 // Layout of the transposed stage h in shared memory: even entries first,
@@ -697,11 +709,11 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 2)
     fwd_term<LOG2N, false, 0, false>(stage, nullptr, zb, zb, t, bar, ta_t, r4_t, fftw, p, f, 1.0);
   group_sync<C::GT>(bar);
 #pragma unroll
-  for (int i = 0; i < OWN; ++i) stage[fwd_own_row<LOG2N>(t, i)] = f[i];
+  for (int i = 0; i < OWN; ++i) stage[out_slot(fwd_own_row<LOG2N>(t, i))] = f[i];
   group_sync<C::GT>(bar);
   double* dst = out + col * ld_out;
 #pragma unroll
-  for (int i = 0; i < OWN; ++i) __stcs(dst + t + T * i, stage[t + T * i]);
+  for (int i = 0; i < OWN; ++i) __stcs(dst + t + T * i, stage[out_slot(t + T * i)]);
 }
 
 // Persistent, prefetching variant of the plain forward pass for one column
@@ -789,13 +801,11 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, StreamCfg<LOG2N>::MINB)
   for (uint32_t it = 0; col < batch; col += gridDim.x, ++it) {
     __syncthreads();  // the previous column's output has left the FFT row
     mbar_wait_parity(bar, it & 1u);
-#pragma unroll
-    for (int i = 0; i < OWN; ++i) bad |= !isfinite(stage[t + T * i]);
     double2 v[E];
     if (odd)
-      fwd_pack_all<N, true, 0, 0>(v, stage, nullptr, t, ta_t, r4_t);
+      fwd_pack_all<N, true, 0, 0>(v, stage, nullptr, t, ta_t, r4_t, &bad);
     else
-      fwd_pack_all<N, false, 0, 0>(v, stage, nullptr, t, ta_t, r4_t);
+      fwd_pack_all<N, false, 0, 0>(v, stage, nullptr, t, ta_t, r4_t, &bad);
     pass_compute<P, E, 8, 1, true>(v, t, fftw);
     pass_store<P, E, 8, 1>(v, zb, t);
     __syncthreads();  // every thread has packed: the stage buffer takes the next column
@@ -815,13 +825,13 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, StreamCfg<LOG2N>::MINB)
         const int m = t + q * T + r * NSL;
         const double2 z = v[q * RL + r];
         const int k0 = fwd_row_of<N>(2 * m), k1 = fwd_row_of<N>(2 * m + 1);
-        zo[k0] = (odd && (k0 & 1)) ? -z.x : z.x;
-        zo[k1] = (odd && (k1 & 1)) ? -z.y : z.y;
+        zo[out_slot(k0)] = (odd && (k0 & 1)) ? -z.x : z.x;
+        zo[out_slot(k1)] = (odd && (k1 & 1)) ? -z.y : z.y;
       }
     __syncthreads();
     double* dst = out + col * ld_out;
 #pragma unroll
-    for (int i = 0; i < OWN; ++i) __stcs(dst + t + T * i, zo[t + T * i]);
+    for (int i = 0; i < OWN; ++i) __stcs(dst + t + T * i, zo[out_slot(t + T * i)]);
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
 }
