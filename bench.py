@@ -321,7 +321,7 @@ def main() -> None:
     hbm_peak = json.load(open(MEASURED))["hbm_gbs"] if os.path.exists(MEASURED) else 6650.0
     # DRAM traffic of the NDCT kernel per launch, from the committed ncu
     # --set full capture (profiles/ncu_traffic.json: bytes per coefficient)
-    traffic = None
+    traffic = dct_traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         tj = json.load(open(tfile))
@@ -332,6 +332,10 @@ def main() -> None:
                            "bytes_per_coef": rec["dram_bytes_per_coef"],
                            "algorithmic_bytes_per_coef": 16.0, "source": rec["capture"]}
                 break
+        rec = tj.get(f"fast_dct_stream_fwd_kernel<{int(math.log2(n))}>")
+        if rec:
+            dct_traffic = {"bytes_per_coef": rec["dram_bytes_per_coef"], "algorithmic_bytes_per_coef": 16.0,
+                           "source": rec["capture"]}
     dct_gbs = 16.0 * coef / (ms_dct / 1e3) / 1e9
 
     # ---- end to end through the public API with pinned host buffers
@@ -393,7 +397,9 @@ def main() -> None:
             "roofline_hbm": {"bound": "hbm", "achieved": 16.0 * value / 1e9, "peak": hbm_peak, "unit": "GB/s",
                              "frac": 16.0 * value / 1e9 / hbm_peak,
                              "note": "16 B/coef algorithmic (one fp64 read + one write), whole DLT",
-                             "dct_pass_gbs": dct_gbs, "dct_pass_frac": dct_gbs / hbm_peak},
+                             "dct_pass_gbs": dct_gbs, "dct_pass_frac": dct_gbs / hbm_peak,
+                             "dct_pass_kernel": "fast_dct_stream_fwd_kernel (fl_trig DCT-III, same shard)",
+                             "dct_pass_traffic": dct_traffic},
             "kernels_ms": {"leg2cheb_split_int8": ms_l2c, "ndct": ms_ndct, "dct_iii_pass": ms_dct,
                            "dlt_step": ms, "idlt_step": ms_idlt},
             "e2e": {"value": n * total / (e2e_ms / 1e3), "unit": "coeffs/s",

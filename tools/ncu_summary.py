@@ -78,12 +78,14 @@ def traffic_json(path: str, coefs: int, out: str) -> None:
     import json
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
-    h = rows[0]
+    h, units = rows[0], rows[1]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     res = {}
     for r in rows[2:]:
         d = dict(zip(h, r))
         name = d.get("Kernel Name", "?").split("(")[0].replace("void ", "").replace("unnamed>::", "")
-        b = float(d["dram__bytes_read.sum"].replace(",", "")) * 1e6 + float(d["dram__bytes_write.sum"].replace(",", "")) * 1e6
+        b = sum(float(d[k].replace(",", "")) * scale[units[h.index(k)]]
+                for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
         res[name] = {"dram_bytes_per_coef": b / coefs, "capture": path, "coefs_per_launch": coefs}
     json.dump(res, open(out, "w"), indent=1)
     print(json.dumps(res, indent=1))

@@ -5,6 +5,8 @@
 #   3. ncu --set full of the hot kernels of one DLT (split_b, split-int8 GEMM,
 #      NDCT) at a reduced column count (same kernels, same N; replay cost
 #      bounded)                                           -> gpurun_out/hot_full.ncu-rep
+#   4. ncu --set full of the plain DCT-III pass (streaming kernel, 4096 x 65536,
+#      the HBM-bound pass of north_star's 60% target)      -> gpurun_out/dct_full.ncu-rep
 set -u
 mkdir -p gpurun_out
 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
@@ -18,3 +20,7 @@ python tools/dbg_oz2.py 4096 8192 > gpurun_out/kern_small.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:"fast_ndct_fwd|oz_gemm2|oz_split_b" -s 3 -c 3 \
     -o gpurun_out/hot_full python tools/dbg_oz2.py 4096 8192 > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"
+python tools/dct_probe.py > gpurun_out/dct_probe.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:fast_dct_stream -s 2 -c 1 \
+    -o gpurun_out/dct_full python tools/dct_probe.py > gpurun_out/dct_ncu.log 2>&1
+echo "ncu dct rc=$?"
