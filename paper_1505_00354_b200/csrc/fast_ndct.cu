@@ -781,6 +781,8 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, StreamCfg<LOG2N>::MINB)
   double* zo = smem + N;  // output staging (the FFT row, after the last pass)
   double2* fftw_s = reinterpret_cast<double2*>(smem + N + C::ZB / sizeof(double));
   const double2* fftw = StreamCfg<LOG2N>::TW_SMEM ? fftw_s : fftw_g;
+  // radix-4 last pass, two butterflies per thread: outputs go straight out
+  constexpr bool DIRECT_OUT = RL == 4 && E / RL == 2;
   const int t = threadIdx.x;
   const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar));
   const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
@@ -815,23 +817,59 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, StreamCfg<LOG2N>::MINB)
       bulk_load(stage_s, in + nxt * ld_in, N * 8, bar);
     }
     mid_passes<P, E, 8, NSL, true, 0, true>(zb, t, fftw, 0);
-    pass_load<P, E, RL>(v, zb, t);
-    pass_compute<P, E, RL, NSL, true, true>(v, t, fftw + pass_tw_offset(P, NSL));
-    __syncthreads();  // all last-pass loads done: the FFT row stages the output
-#pragma unroll
-    for (int q = 0; q < E / RL; ++q)
+    double* dst = out + col * ld_out;
+    if constexpr (DIRECT_OUT) {
+      // mirrored last-pass butterflies: z_m (rows 4m, 4m + 2) and z_{P-1-m}
+      // (rows 4m + 3, 4m + 1) in one thread = four contiguous output rows,
+      // stored straight from registers (no staging, two barriers fewer)
+      pass_load<P, E, RL, true>(v, zb, t);
+      pass_compute<P, E, RL, NSL, true, true, true>(v, t, fftw + pass_tw_offset(P, NSL));
+      // A warp's 32 blocks of one r are 1 KB contiguous (ascending in the
+      // lane for m < P/2, descending above); two lane shuffles per half let
+      // each 16-byte store instruction cover 512 contiguous bytes.
+      const double sg = odd ? -1.0 : 1.0;  // DST: odd rows negated
+      const int lane = t & 31, wbase = t - lane;
 #pragma unroll
       for (int r = 0; r < RL; ++r) {
-        const int m = t + q * T + r * NSL;
-        const double2 z = v[q * RL + r];
-        const int k0 = fwd_row_of<N>(2 * m), k1 = fwd_row_of<N>(2 * m + 1);
-        zo[out_slot(k0)] = (odd && (k0 & 1)) ? -z.x : z.x;
-        zo[out_slot(k1)] = (odd && (k1 & 1)) ? -z.y : z.y;
-      }
-    __syncthreads();
-    double* dst = out + col * ld_out;
+        const int m = t + r * NSL;
+        const double2 a = v[r], b = v[RL + RL - 1 - r];  // z_m, z_{P-1-m}
+        const bool lo = r * NSL < P / 2;                  // (warp-uniform)
+        const double2 z = lo ? a : b, w = lo ? b : a;     // z: rows 4m', 4m' + 2
+        const double2 h0 = make_double2(z.x, sg * w.y), h1 = make_double2(z.y, sg * w.x);
+        // the warp's lowest block: lane 0 (ascending) or lane 31 (descending)
+        const int blk0 = lo ? wbase + r * NSL : P - 1 - (wbase + 31 + r * NSL);
+        (void)m;
 #pragma unroll
-    for (int i = 0; i < OWN; ++i) __stcs(dst + t + T * i, zo[out_slot(t + T * i)]);
+        for (int hh = 0; hh < 2; ++hh) {
+          const int bi = 16 * hh + (lane >> 1);  // block in address order
+          const int src = lo ? bi : 31 - bi;
+          double2 g0, g1;
+          g0.x = __shfl_sync(0xffffffffu, h0.x, src);
+          g0.y = __shfl_sync(0xffffffffu, h0.y, src);
+          g1.x = __shfl_sync(0xffffffffu, h1.x, src);
+          g1.y = __shfl_sync(0xffffffffu, h1.y, src);
+          __stcs(reinterpret_cast<double2*>(dst + 4 * blk0 + 64 * hh + 2 * lane),
+                 (lane & 1) ? g1 : g0);
+        }
+      }
+    } else {
+      pass_load<P, E, RL>(v, zb, t);
+      pass_compute<P, E, RL, NSL, true, true>(v, t, fftw + pass_tw_offset(P, NSL));
+      __syncthreads();  // all last-pass loads done: the FFT row stages the output
+#pragma unroll
+      for (int q = 0; q < E / RL; ++q)
+#pragma unroll
+        for (int r = 0; r < RL; ++r) {
+          const int m = t + q * T + r * NSL;
+          const double2 z = v[q * RL + r];
+          const int k0 = fwd_row_of<N>(2 * m), k1 = fwd_row_of<N>(2 * m + 1);
+          zo[out_slot(k0)] = (odd && (k0 & 1)) ? -z.x : z.x;
+          zo[out_slot(k1)] = (odd && (k1 & 1)) ? -z.y : z.y;
+        }
+      __syncthreads();
+#pragma unroll
+      for (int i = 0; i < OWN; ++i) __stcs(dst + t + T * i, zo[out_slot(t + T * i)]);
+    }
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
 }
@@ -915,7 +953,7 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
   const size_t max_cols = (size_t)0x7fffffff * C::COLS;
   if constexpr (C::COLS == 1) {
     if (plain_op >= 0 && !mult && !transpose && ld_in == ld_out && (ld_in % 2) == 0 &&
-        (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+        (reinterpret_cast<uintptr_t>(in) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
       const size_t smem = StreamCfg<LOG2N>::SMEM;
       FLB_CUDA(cudaFuncSetAttribute(fast_dct_stream_fwd_kernel<LOG2N>,
                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

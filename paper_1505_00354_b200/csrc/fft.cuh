@@ -139,12 +139,21 @@ __device__ __forceinline__ void group_sync(int bar) {
 // The three stages of a pass, usable separately so that a kernel can feed the
 // first pass from registers and consume the last pass in registers.
 // Input of butterfly q of thread tid: v[q R + r] = x[j + r P/R], j = tid + q TR.
-template <int P, int E, int R>
+// MIR (two butterflies per thread): j = tid and P/R - 1 - tid instead, so
+// that in the last pass (NS = P/R, outputs j + r NS) a thread holds outputs
+// m and P - 1 - m together.
+template <int P, int E, int R, bool MIR = false>
+__device__ __forceinline__ int butterfly_j(int tid, int q) {
+  static_assert(!MIR || E / R == 2, "mirrored butterflies: two per thread");
+  return MIR ? (q == 0 ? tid : P / R - 1 - tid) : tid + q * (P / E);
+}
+
+template <int P, int E, int R, bool MIR = false>
 __device__ __forceinline__ void pass_load(double2* v, const double2* s, int tid) {
-  constexpr int TR = P / E, NB = E / R;
+  constexpr int NB = E / R;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
-    const int j = tid + q * TR;
+    const int j = butterfly_j<P, E, R, MIR>(tid, q);
 #pragma unroll
     for (int r = 0; r < R; ++r) v[q * R + r] = s[smem_pad(j + r * (P / R))];
   }
@@ -156,12 +165,12 @@ __device__ __forceinline__ void pass_load(double2* v, const double2* s, int tid)
 // 1 instead of 3 for radix 4 -- shared-memory wavefronts traded for FP64 work.
 // Only for NS >= 64: below that a warp's twiddle loads hit few distinct
 // entries (broadcast, ~1 wavefront) and the products cost more than they save.
-template <int P, int E, int R, int NS, bool INV, bool TWP = false>
+template <int P, int E, int R, int NS, bool INV, bool TWP = false, bool MIR = false>
 __device__ __forceinline__ void pass_compute(double2* v, int tid, const double2* tw) {
-  constexpr int TR = P / E, NB = E / R;
+  constexpr int NB = E / R;
 #pragma unroll
   for (int q = 0; q < NB; ++q) {
-    const int j = tid + q * TR;
+    const int j = butterfly_j<P, E, R, MIR>(tid, q);
     const int k = j & (NS - 1);
     if constexpr (NS > 1 && TWP && NS >= 64 && (R == 8 || R == 4)) {
       double2 w[R];

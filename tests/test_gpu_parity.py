@@ -197,6 +197,31 @@ def test_trig_batched_large(n):
                 assert rel_err(got[j], ref, np.abs(c[j]).sum()) <= tol_n(n), (kind, op, j)
 
 
+@pytest.mark.parametrize("op", [0, 1])
+def test_trig_streaming_pass_device(op):
+    """The persistent streaming DCT-III / DST-III pass (device columns, even
+    stride, 16-byte aligned; N = 4096: outputs stored straight from the
+    mirrored last-pass butterflies) against the oracle on sampled columns and
+    against the per-column kernel (odd stride) on all of them."""
+    import ctypes as C
+    import torch
+    from paper_1505_00354_b200 import _lib
+    n, batch = 4096, 1000
+    x = torch.randn(batch, n, dtype=torch.float64, device="cuda")
+    y = torch.full_like(x, 3.0)
+    _lib.check(_lib.LIB.fl_trig(op, 0, n, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), batch, n, None))
+    xs = torch.zeros(batch, n + 1, dtype=torch.float64, device="cuda")
+    xs[:, :n] = x
+    ys = torch.zeros_like(xs)
+    _lib.check(_lib.LIB.fl_trig(op, 0, n, C.c_void_p(xs.data_ptr()), C.c_void_p(ys.data_ptr()), batch, n + 1,
+                                None))
+    yh, xh, ysh = y.cpu().numpy(), x.cpu().numpy(), ys[:, :n].cpu().numpy()
+    scale = np.abs(xh).sum(axis=1)
+    assert np.max(np.abs(yh - ysh).max(axis=1) / scale) <= 1e-15
+    for j in (0, 1, 517, batch - 1):
+        assert rel_err(yh[j], O.trig(op, xh[j], CHEB1), scale[j]) <= tol_n(n), j
+
+
 def test_trig_golden(ref_vectors):
     """Reference outputs (compiled reference headers) on its own inputs."""
     for t in ref_vectors["trig"]:
