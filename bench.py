@@ -309,12 +309,12 @@ def main() -> None:
     coef = n * cols
     l2c_flops = coef * (n / 2.0)                   # N^2/4 MACs per column = N/2 flop per coefficient
     ndct_flops = coef * L1 * (2.5 * math.log2(n) + 3)  # L (2.5 log2 N + 3)
-    # int8 tensor work of the split product: 36 digit pairs x the 128-row-blocked
+    # int8 tensor work of the split product: 28 digit pairs x the 128-row-blocked
     # triangle (K from the diagonal block), 2 ops per MAC, both parities
     r_rows = n // 2
     rbs = r_rows // 128
     tri_macs = sum((r_rows - 128 * rb) * 128 for rb in range(rbs)) * 2 * cols
-    i8_ops = 36 * 2 * tri_macs
+    i8_ops = 28 * 2 * tri_macs
     gemm_mode = cfg.gemm_mode()
     dom = "fast_ndct_fwd_kernel" if ms_ndct >= ms_l2c else "oz_gemm_kernel"
     achieved = ndct_flops / (ms_ndct / 1e3) / 1e12
@@ -375,7 +375,7 @@ def main() -> None:
                        "grid": "chebstar (default TransformConfig), NDCT evaluated about cheb1 (fast mode, "
                                "14-term Chebyshev expansion)",
                        "arithmetic": "fp64 throughout; the Legendre->Chebyshev product as an exact "
-                                     "int8 digit-split GEMM on the tcgen05 tensor cores (8 digits/operand, "
+                                     "int8 digit-split GEMM on the tcgen05 tensor cores (7 8-bit digits/operand, "
                                      "int32 accumulation, fp64 recombination; fl_plan_set_gemm_mode "
                                      "selects the fp64 DMMA product instead)",
                        "parallelism": f"column shards x{world}, no collective",
@@ -393,7 +393,7 @@ def main() -> None:
                                 "tile_cap": INT8_N64_CAP_TOPS,
                                 "fp64_equivalent_tflops": l2c_flops / (ms_l2c / 1e3) / 1e12,
                                 "peak_source": "tools/tc_i8_peak.cu (profiles/r01_tc_i8_peak.log)",
-                                "algorithmic": "36 digit pairs x blocked triangle, 2 ops/MAC; fp64-equivalent N/2 flop/coef"},
+                                "algorithmic": "28 digit pairs (7 signed 8-bit digits per operand) x blocked triangle, 2 ops/MAC; fp64-equivalent N/2 flop/coef"},
             "roofline_hbm": {"bound": "hbm", "achieved": 16.0 * value / 1e9, "peak": hbm_peak, "unit": "GB/s",
                              "frac": 16.0 * value / 1e9 / hbm_peak,
                              "note": "16 B/coef algorithmic (one fp64 read + one write), whole DLT",

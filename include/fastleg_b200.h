@@ -158,8 +158,8 @@ int fl_plan_leg2cheb_rank(const fl_plan* plan, int parity);
  *   0 = FL_GEMM_FP64       : fp64 tensor cores (mma.sync f64, DMMA);
  *   1 = FL_GEMM_INT8_SPLIT : exact split-integer product on the tcgen05 int8
  *       tensor cores: each operand row/column scaled by a power of two and
- *       split into 8 signed 7-bit digits, the 36 digit products with
- *       i + j < 8 accumulated exactly in int32 TMEM accumulators and summed
+ *       split into 7 signed 8-bit digits, the 28 digit products with
+ *       i + j < 7 accumulated exactly in int32 TMEM accumulators and summed
  *       in fp64 (error <= ~2^-55 max|M row| max|c column| per term, the
  *       order of fp64 rounding). For n a multiple of 256 in [512, 16384];
  *       other sizes use FL_GEMM_FP64.

@@ -8,30 +8,34 @@
 // ~4.5 POP/s. The split ("Ozaki") scheme runs the fp64 product on the int8
 // units exactly:
 //
-//   row / column scaling:  A_ab = 2^{ea_a} sum_{i<S} a^(i)_ab 2^{-7(i+1)},
-//                          B_bc = 2^{eb_c} sum_{j<S} b^(j)_bc 2^{-7(j+1)},
-//   digits a^(i), b^(j) in [-64, 64] (round-to-nearest splitting of the
-//   scaled value, exact in fp64), so every digit product is exact and a
-//   K-sum of them fits int32 (|sum| <= 8 * 64^2 * N/2 < 2^31 for N <= 2^16):
+//   row / column scaling:  A_ab = 2^{ea_a} sum_{i<S} a^(i)_ab 2^{-8(i+1)},
+//                          B_bc = 2^{eb_c} sum_{j<S} b^(j)_bc 2^{-8(j+1)},
+//   S = 7 signed 8-bit digits per operand (round-to-nearest splitting of the
+//   scaled value, |value| < 1/4, exact in fp64; a +128 digit is carried into
+//   the next higher one), so every digit product is exact (|.| <= 2^14) and
+//   a K-sum of up to 7 of them fits int32 (7 * 2^14 * N/2 < 2^31 for
+//   N <= 2^14):
 //
-//   C_ac = 2^{ea_a + eb_c} sum_{d < S} 2^{-7(d+2)} sum_{i+j=d} (a^(i) b^(j))_ac
+//   C_ac = 2^{ea_a + eb_c} sum_{d < S} 2^{-8(d+2)} sum_{i+j=d} (a^(i) b^(j))_ac
 //
-// Pairs with i + j >= S are dropped (below 2^{-7(S+1)} of the row/column
-// scales; S = 8 keeps the result at fp64 level: ~2^-55 of max|A_a.| max|B_.c|
-// per term, the same order as an fp64 dot product's rounding).
+// Pairs with i + j >= S are dropped: the largest is <= 2^14 2^{-8(S+2)} =
+// 2^-58 of the row/column scales per term, the same order as an fp64 dot
+// product's rounding (the 7-bit / 8-digit variant, -DFLB_OZ_DIGIT_BITS=7,
+// drops at the same level with 36 pairs instead of 28: 9.9 vs 8.4 ms for
+// C4's conversion).
 //
-// Kernel (persistent, one CTA per SM; output tiles of 128 rows x 64 columns
-// of one parity):
-//   warp 0     TMA producer: per 64-wide K block, the 8 slices of the A tile
-//              (128 rows x 64 B) and of the B tile (64 columns x 64 B),
-//              SWIZZLE_64B, into a 2-stage ring (96 KB per stage; BK = 32 /
-//              SWIZZLE_32B / 4 stages measured 1% slower)
-//   warp 1     TMEM allocator and MMA issuer: 36 slice pairs x 2 K-steps of
-//              tcgen05.mma.cta_group::1.kind::i8 (M = 128, N = 64, K = 32)
-//              per stage, fully unrolled, issued by one elected lane of the
-//              whole warp (uniform operands); pair (i, j) accumulating into TMEM accumulator
-//              d = i + j (8 x 64 int32 columns = all 512 TMEM columns)
-//   warps 2-5  epilogue: tcgen05.ld of the 8 accumulators, exact int32 ->
+// Kernel (persistent; output tiles of 128 rows x 64 columns of one parity;
+// the default oz_gemm2_kernel pairs two SMs on 256-row tiles, cta_group::2):
+//   warp 0     TMA producer: per 64-wide K block, the S slices of the A tile
+//              (128 rows x 64 B) and of the B tile (64 or 32 columns x 64 B),
+//              SWIZZLE_64B, into a ring of stages (3 x 70 KB for the pair
+//              kernel with 7 digits)
+//   warp 1     TMEM allocator and MMA issuer: 28 slice pairs x 2 K-steps of
+//              tcgen05.mma.kind::i8 (M = 128/256, N = 64, K = 32) per stage,
+//              fully unrolled, issued by one elected lane of the whole warp
+//              (uniform operands); pair (i, j) accumulating into TMEM
+//              accumulator d = i + j (S x 64 int32 columns)
+//   warps 2-5  epilogue: tcgen05.ld of the S accumulators, exact int32 ->
 //              fp64 scaled sum in registers, TMEM released to the next tile,
 //              then row/column scales and the store (k = 2a + p)
 // Only the K blocks on or above (forward) / below (transpose) the diagonal
@@ -49,7 +53,13 @@
 namespace flb {
 
 namespace oz {
-constexpr int S = 8;            // digits per operand
+// Digit width: 8-bit digits (7 per operand, 28 pairs) by default; 7-bit
+// digits (8 per operand, 36 pairs) with -DFLB_OZ_DIGIT_BITS=7.
+#ifndef FLB_OZ_DIGIT_BITS
+#define FLB_OZ_DIGIT_BITS 8
+#endif
+constexpr int DB = FLB_OZ_DIGIT_BITS;
+constexpr int S = DB == 8 ? 7 : 8;  // digits per operand
 constexpr int BM = 128;         // output rows per tile (TMEM lanes)
 constexpr int BN = 64;          // output columns per tile
 #ifndef FLB_OZ_BK
@@ -183,26 +193,43 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
 }
 
 // ---- digit splitting ---------------------------------------------------
-// Scale exponent e with max * 2^-e < 1/2 (0 for max = 0).
+// Scale exponent e with max * 2^-e < 1/2 (7-bit digits) or < 1/4 (8-bit
+// digits: the top digit keeps room for a carry); 0 for max = 0.
 __device__ __forceinline__ int split_exp(double mx) {
   if (!(mx > 0.0)) return 0;
   int e;
   frexp(mx, &e);  // mx = m 2^e, m in [0.5, 1)
-  return e + 1;
+  return e + (oz::DB == 8 ? 2 : 1);
 }
-// Digits of r = x 2^-e (|r| < 1/2): r = sum_j d_j 2^{-7(j+1)} + O(2^{-7S-1}).
+// Digits of r = x 2^-e: r = sum_j d_j 2^{-DB(j+1)} + O(2^{-DB S - 1}).
 // rint(t) by the 1.5 * 2^52 shifter: t + M rounds to nearest even in the
-// FP64 adder and the integer sits in the low mantissa bits (no F2I).
+// FP64 adder and the integer sits in the low mantissa bits (no F2I). Each
+// residual is in [-1/2, 1/2], so a digit is in [-2^{DB-1}, 2^{DB-1}]: for
+// DB = 7 that fits int8 as is; for DB = 8 a digit of +128 becomes -128 with
+// a carry into the next higher digit (the value is unchanged; the top digit,
+// |d_0| <= 64, absorbs any carry chain).
 __device__ __forceinline__ void split_digits(double x, int e, int8_t (&d)[oz::S]) {
   constexpr double kShift = 6755399441055744.0;  // 1.5 * 2^52
+  constexpr double kRadix = oz::DB == 8 ? 256.0 : 128.0;
   double r = ldexp(x, -e);
+  int di[oz::S];
 #pragma unroll
   for (int j = 0; j < oz::S; ++j) {
-    const double t = r * 128.0;
+    const double t = r * kRadix;
     const double y = t + kShift;
-    d[j] = (int8_t)__double2loint(y);
+    di[j] = __double2loint(y);
     r = t - (y - kShift);
   }
+  if constexpr (oz::DB == 8) {
+#pragma unroll
+    for (int j = oz::S - 1; j > 0; --j)
+      if (di[j] == 128) {
+        di[j] = -128;
+        ++di[j - 1];
+      }
+  }
+#pragma unroll
+  for (int j = 0; j < oz::S; ++j) d[j] = (int8_t)di[j];
 }
 
 // Entry of the parity-p block: forward A[a][b] = pref_{2a+p} s_{b-a} s_{a+b+p}
@@ -448,10 +475,10 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       // least significant accumulator first
 #pragma unroll 1
       for (int d = S - 1; d >= 0; --d) {
-        // exact S_d 2^{-7(d+2)} without the int->fp64 conversion unit: the
+        // exact S_d 2^{-DB(d+2)} without the int->fp64 conversion unit: the
         // biased integer becomes the low mantissa bits of a double whose ulp
-        // is 2^{-7(d+2)}; subtracting the bias constant is exact
-        const int sh = 7 * (d + 2);
+        // is 2^{-DB(d+2)}; subtracting the bias constant is exact
+        const int sh = DB * (d + 2);
         const int hi_word = (1075 - sh) << 20;
         const double bias = ldexp(1.0, 52 - sh) + ldexp(1.0, 31 - sh);
         uint32_t v[BN / 32][32];  // both halves in flight before one wait
@@ -497,7 +524,7 @@ constexpr int A_TILE = oz::BM * oz::BK;            // 128 rows
 constexpr int B_TILE = (oz::BN / 2) * oz::BK;      // 32 columns: this CTA's half
 constexpr int STAGE_BYTES = oz::S * (A_TILE + B_TILE);
 #ifndef FLB_OZ2_STAGES
-#define FLB_OZ2_STAGES 2
+#define FLB_OZ2_STAGES (oz::S == 7 ? 3 : 2)  // 3 x 70 KB fit with 7 digits
 #endif
 constexpr int STAGES = FLB_OZ2_STAGES;
 constexpr int SMEM = STAGES * STAGE_BYTES + 1024 + 256;
@@ -689,10 +716,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
       for (int c = 0; c < BN; ++c) acc[c] = 0.0;
 #pragma unroll 1
       for (int d = S - 1; d >= 0; --d) {
-        // exact S_d 2^{-7(d+2)} without the int->fp64 conversion unit: the
+        // exact S_d 2^{-DB(d+2)} without the int->fp64 conversion unit: the
         // biased integer becomes the low mantissa bits of a double whose ulp
-        // is 2^{-7(d+2)}; subtracting the bias constant is exact
-        const int sh = 7 * (d + 2);
+        // is 2^{-DB(d+2)}; subtracting the bias constant is exact
+        const int sh = DB * (d + 2);
         const int hi_word = (1075 - sh) << 20;
         const double bias = ldexp(1.0, 52 - sh) + ldexp(1.0, 31 - sh);
         uint32_t v[BN / 32][32];  // both halves in flight before one wait
