@@ -45,6 +45,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <type_traits>
 
 #include "common.cuh"
 #include "l2c_ozaki.cuh"
@@ -280,30 +281,35 @@ __global__ void __launch_bounds__(256) oz_split_a_kernel(const double* __restric
   }
 }
 
-// One CTA of n/16 threads per input column (each thread one 16-entry chunk,
+// One CTA of n/EPT threads per input column (each thread one EPT-entry chunk,
 // held in registers between the max reduction and the split): per-parity
 // scales and the S digit slices, de-interleaved by parity ([S][2][cols][r]).
+// EPT = 8 (n <= 8192: twice the resident warps of EPT = 16, so one CTA's
+// reduction overlaps another's loads) or 16.
 // A non-finite column gets a NaN scale so the product column comes out NaN
 // (the NDCT input check reports it).
+template <int EPT>
 __global__ void __launch_bounds__(1024) oz_split_b_kernel(const double* __restrict__ in, size_t n,
                                                           size_t ld, size_t cols,
                                                           int8_t* __restrict__ b,
                                                           double* __restrict__ bcol) {
+  using W = typename std::conditional<EPT == 16, uint64_t, uint32_t>::type;  // EPT/2 digits
+  constexpr int H = EPT / 2;
   const size_t col = blockIdx.x;
   const size_t r = n / 2;
-  const size_t c = threadIdx.x;  // chunk: entries 16c .. 16c + 15
+  const size_t c = threadIdx.x;  // chunk: entries EPT c .. EPT c + EPT - 1
   __shared__ double red[2][32];
   __shared__ int e_sh[2];
   __shared__ int bad_sh;
   if (threadIdx.x == 0) bad_sh = 0;
-  const double2* q = reinterpret_cast<const double2*>(in + col * ld + 16 * c);
-  double2 v[8];
+  const double2* q = reinterpret_cast<const double2*>(in + col * ld + EPT * c);
+  double2 v[H];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) v[i] = __ldcs(q + i);  // streamed: read once
+  for (int i = 0; i < H; ++i) v[i] = __ldcs(q + i);  // streamed: read once
   double mx0 = 0.0, mx1 = 0.0;
   bool bad = false;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < H; ++i) {
     bad |= !isfinite(v[i].x) || !isfinite(v[i].y);
     mx0 = fmax(mx0, fabs(v[i].x));
     mx1 = fmax(mx1, fabs(v[i].y));
@@ -328,24 +334,24 @@ __global__ void __launch_bounds__(1024) oz_split_b_kernel(const double* __restri
   }
   __syncthreads();
   const int e0 = e_sh[0], e1 = e_sh[1];
-  uint64_t w0[oz::S], w1[oz::S];
+  W w0[oz::S], w1[oz::S];
 #pragma unroll
   for (int j = 0; j < oz::S; ++j) w0[j] = w1[j] = 0;
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+  for (int i = 0; i < H; ++i) {
     int8_t d0[oz::S], d1[oz::S];
     split_digits(isfinite(v[i].x) ? v[i].x : 0.0, e0, d0);
     split_digits(isfinite(v[i].y) ? v[i].y : 0.0, e1, d1);
 #pragma unroll
     for (int j = 0; j < oz::S; ++j) {
-      w0[j] |= (uint64_t)(uint8_t)d0[j] << (8 * i);
-      w1[j] |= (uint64_t)(uint8_t)d1[j] << (8 * i);
+      w0[j] |= (W)(uint8_t)d0[j] << (8 * i);
+      w1[j] |= (W)(uint8_t)d1[j] << (8 * i);
     }
   }
 #pragma unroll
   for (int j = 0; j < oz::S; ++j) {
-    *reinterpret_cast<uint64_t*>(b + ((size_t)(j * 2 + 0) * cols + col) * r + 8 * c) = w0[j];
-    *reinterpret_cast<uint64_t*>(b + ((size_t)(j * 2 + 1) * cols + col) * r + 8 * c) = w1[j];
+    *reinterpret_cast<W*>(b + ((size_t)(j * 2 + 0) * cols + col) * r + H * c) = w0[j];
+    *reinterpret_cast<W*>(b + ((size_t)(j * 2 + 1) * cols + col) * r + H * c) = w1[j];
   }
 }
 
@@ -816,7 +822,10 @@ void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t co
   double* bcol = nullptr;
   FLB_CUDA(cudaMallocAsync(&b, (size_t)oz::S * 2 * cols * r, st));
   FLB_CUDA(cudaMallocAsync(&bcol, 2 * cols * sizeof(double), st));
-  oz_split_b_kernel<<<(unsigned)cols, (unsigned)(n / 16), 0, st>>>(in, n, ld, cols, b, bcol);
+  if (n <= 8192)
+    oz_split_b_kernel<8><<<(unsigned)cols, (unsigned)(n / 8), 0, st>>>(in, n, ld, cols, b, bcol);
+  else
+    oz_split_b_kernel<16><<<(unsigned)cols, (unsigned)(n / 16), 0, st>>>(in, n, ld, cols, b, bcol);
   note_launch("oz_split_b_kernel");
   const CUtensorMap tmap_b = make_map(b, r, cols, 2 * oz::S, oz::BN);
   static bool attr = [] {

@@ -76,6 +76,32 @@ def test_split_matches_fp64_product(n, batch):
             assert rel(a[j], b[j], np.abs(c[j]).sum()) <= 1e-15, (k, j)
 
 
+def test_split_digit_carries():
+    """8-bit digits: a residual in [127.5, 128] / 256 rounds to a digit of
+    +128, which is stored as -128 with a carry into the next higher digit
+    (l2c_ozaki.cu split_digits). Columns built so that (nearly) every entry
+    carries, some in chains (consecutive 0.999.../256 residuals), must still
+    match the fp64 product."""
+    n, batch = 1024, 24
+    cfg = fl.TransformConfig(n)
+    rng = np.random.default_rng(5)
+    c = np.empty((batch, n))
+    for j in range(batch):
+        # per-parity max in [1, 2): scale 2^3, r = x / 8 = (d0 + tail) / 256.
+        # tail 0.499: digit 1 rounds 127.74 -> 128 (one carry); tail
+        # (127 + 0.499) / 256: digit 1 = 127, digit 2 = 128 -> a carry chain
+        # 2 -> 1 -> 0 in the odd columns
+        d0 = rng.integers(-60, 60, n).astype(float)
+        tail = (127.0 + 0.499) / 256.0 if j % 2 else 0.499
+        c[j] = 8.0 * (d0 + np.sign(d0 + 0.5) * tail) / 256.0
+        c[j, 0] = c[j, 1] = 1.0
+    r = both(cfg, c)
+    for k in (0, 1):
+        a, b = r[fl.GEMM_INT8_SPLIT][k], r[fl.GEMM_FP64][k]
+        for j in range(batch):
+            assert rel(a[j], b[j], np.abs(c[j]).sum()) <= 1e-15, (k, j)
+
+
 def test_split_decaying_and_zero_columns():
     """Large per-column dynamic range (decaying coefficients, scales 1e-200 ..
     1e200) and all-zero columns: the power-of-two scaling keeps every column
