@@ -525,7 +525,11 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
 // Per SM the tensor core then reads 4 KiB of A + 1 KiB of B per 32-clock MMA
 // instead of 4 + 2 KiB: the shared-memory operand bound of the 1-SM kernel
 // (64 % of the int8 peak at N = 64) rises to ~80 %.
+#ifndef FLB_OZ_TS
+#define FLB_OZ_TS 1  // A operand from TMEM in the pair kernel (needs S * 64 + 64 <= 512 columns)
+#endif
 namespace oz2 {
+constexpr bool TS = FLB_OZ_TS && oz::S * oz::BN + 64 <= 512;
 constexpr int A_TILE = oz::BM * oz::BK;            // 128 rows
 constexpr int B_TILE = (oz::BN / 2) * oz::BK;      // 32 columns: this CTA's half
 constexpr int STAGE_BYTES = oz::S * (A_TILE + B_TILE);
@@ -574,6 +578,27 @@ __device__ __forceinline__ void tc2_mma_i8(uint32_t d_tmem, uint64_t adesc, uint
       "setp.ne.b32 p, %4, 0;\n\t"
       "@e tcgen05.mma.cta_group::2.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// TS form: A (this CTA's 128 rows) from TMEM, B from shared memory.
+__device__ __forceinline__ void tc2_mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                              uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::2.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+// smem (128 rows x 32 bytes, the operand descriptor's layout) -> TMEM
+// (128 lanes x 8 columns) in both CTAs of the pair; ordered with the MMAs.
+__device__ __forceinline__ void tc2_cp_128x256(uint32_t taddr, uint64_t sdesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.cp.cta_group::2.128x256b [%0], %1;\n\t}" ::"r"(taddr),
+      "l"(sdesc)
       : "memory");
 }
 // Arrive on the barrier at this offset in BOTH CTAs of the pair once the
@@ -672,7 +697,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
     }
   } else if (warp == 1) {
     if (leader) {  // MMA issuer: the leader's whole warp, one elected lane issues
-      uint32_t it = 0, t = 0;
+      uint32_t it = 0, t = 0, aslot = 0;
+      (void)aslot;
       for (size_t tile = cluster_id; tile < ntiles; tile += nclusters, ++t) {
         size_t cb, rp;
         int p, kb_lo, nk;
@@ -686,6 +712,28 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
           const uint32_t sa = smem_u32(smem + st * STAGE_BYTES);
           const uint64_t ad0 = smem_desc(sa), bd0 = smem_desc(sa + S * A_TILE);
           const uint32_t first = kb == 0 ? 0u : 1u;
+          if constexpr (oz2::TS) {
+          // A digit tiles through TMEM: each (K-step, digit) tile is copied
+          // once into one of 8 rotating 8-column slots after the S x 64
+          // accumulator columns and read there by its S - i MMAs (the copy
+          // and the MMAs run in issue order, so a slot is rewritten only
+          // after the MMAs issued before the copy have read it). Shared
+          // memory then serves A once per tile instead of once per MMA.
+#pragma unroll
+          for (int ks = 0; ks < BK / 32; ++ks) {
+#pragma unroll
+            for (int i = 0; i < S; ++i, ++aslot) {
+              const uint32_t ta = tmem + (uint32_t)(S * BN + (aslot & 7u) * 8u);
+              tc2_cp_128x256(ta, ad0 + (uint64_t)((i * A_TILE + ks * 32) >> 4));
+#pragma unroll
+              for (int j = 0; i + j < S; ++j) {
+                const uint64_t bd = bd0 + (uint64_t)((j * B_TILE + ks * 32) >> 4);
+                tc2_mma_i8_ts(tmem + (uint32_t)((i + j) * BN), ta, bd, oz2::IDESC,
+                              (ks > 0 || i > 0) ? 1u : first);
+              }
+            }
+          }
+          } else {
 #pragma unroll
           for (int i = 0; i < S; ++i) {
 #pragma unroll
@@ -698,6 +746,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
                            (ks > 0 || i > 0) ? 1u : first);
               }
             }
+          }
           }
           tc2_commit_both(smem_u32(&empty_b[st]));  // frees the stage in both CTAs
         }
