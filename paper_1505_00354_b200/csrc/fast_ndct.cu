@@ -756,13 +756,22 @@ __device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t parity) 
 #ifndef FLB_STREAM_TW_SMEM
 #define FLB_STREAM_TW_SMEM 1
 #endif
+#ifndef FLB_STREAM_PP
+#define FLB_STREAM_PP 1
+#endif
 template <int LOG2N>
 struct StreamCfg {
   using C = Cfg<LOG2N>;
-  static constexpr bool TW_SMEM = FLB_STREAM_TW_SMEM != 0;
-  static constexpr size_t SMEM =
-      C::N * sizeof(double) + C::ZB + (TW_SMEM ? C::TW * sizeof(double2) : 0);
-  static constexpr int MINB = LOG2N <= 12 ? (TW_SMEM ? 2 : 3) : 1;
+  // outputs straight from the mirrored radix-4 last pass (no staging)
+  static constexpr bool DIRECT_OUT = C::RL == 4 && C::E / C::RL == 2;
+  // PP: two FFT rows used alternately per column and per pass (ping-pong):
+  // one barrier per pass and none between columns; the twiddles then stay
+  // in global memory (L1) so that two CTAs still fit per SM
+  static constexpr bool PP = FLB_STREAM_PP && DIRECT_OUT && LOG2N <= 12;
+  static constexpr bool TW_SMEM = FLB_STREAM_TW_SMEM != 0 && !PP;
+  static constexpr size_t SMEM = C::N * sizeof(double) + (PP ? 2 : 1) * C::ZB +
+                                 (TW_SMEM ? C::TW * sizeof(double2) : 0);
+  static constexpr int MINB = LOG2N <= 12 ? (TW_SMEM || PP ? 2 : 3) : 1;
 };
 
 template <int LOG2N>
@@ -782,7 +791,9 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, StreamCfg<LOG2N>::MINB)
   double2* fftw_s = reinterpret_cast<double2*>(smem + N + C::ZB / sizeof(double));
   const double2* fftw = StreamCfg<LOG2N>::TW_SMEM ? fftw_s : fftw_g;
   // radix-4 last pass, two butterflies per thread: outputs go straight out
-  constexpr bool DIRECT_OUT = RL == 4 && E / RL == 2;
+  constexpr bool DIRECT_OUT = StreamCfg<LOG2N>::DIRECT_OUT;
+  constexpr bool PP = StreamCfg<LOG2N>::PP;
+  double2* zb2 = zb + C::ZB / sizeof(double2);  // PP: the second FFT row
   const int t = threadIdx.x;
   const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar));
   const uint32_t stage_s = static_cast<uint32_t>(__cvta_generic_to_shared(stage));
@@ -801,7 +812,12 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, StreamCfg<LOG2N>::MINB)
   const double2 r4_t = __ldg(&tw4n[4 * t]);
   bool bad = false;
   for (uint32_t it = 0; col < batch; col += gridDim.x, ++it) {
-    __syncthreads();  // the previous column's output has left the FFT row
+    // PP: this column's first pass writes the row the previous column's last
+    // pass did not read, and every later pass sits behind a CTA barrier that
+    // all of the previous column's reads precede
+    double2* za = PP && (it & 1u) ? zb2 : zb;
+    double2* zo2 = PP && (it & 1u) ? zb : zb2;
+    if constexpr (!PP) __syncthreads();  // the previous column's output has left the FFT row
     mbar_wait_parity(bar, it & 1u);
     double2 v[E];
     if (odd)
@@ -809,20 +825,24 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, StreamCfg<LOG2N>::MINB)
     else
       fwd_pack_all<N, false, 0, 0>(v, stage, nullptr, t, ta_t, r4_t, &bad);
     pass_compute<P, E, 8, 1, true>(v, t, fftw);
-    pass_store<P, E, 8, 1>(v, zb, t);
+    pass_store<P, E, 8, 1>(v, za, t);
     __syncthreads();  // every thread has packed: the stage buffer takes the next column
     const size_t nxt = col + gridDim.x;
     if (t == 0 && nxt < batch) {
       mbar_expect(bar, N * 8);
       bulk_load(stage_s, in + nxt * ld_in, N * 8, bar);
     }
-    mid_passes<P, E, 8, NSL, true, 0, true>(zb, t, fftw, 0);
+    double2* fin = za;
+    if constexpr (PP)
+      fin = mid_passes_pp<P, E, 8, NSL, true, 0, true>(za, zo2, t, fftw, 0);
+    else
+      mid_passes<P, E, 8, NSL, true, 0, true>(zb, t, fftw, 0);
     double* dst = out + col * ld_out;
     if constexpr (DIRECT_OUT) {
       // mirrored last-pass butterflies: z_m (rows 4m, 4m + 2) and z_{P-1-m}
       // (rows 4m + 3, 4m + 1) in one thread = four contiguous output rows,
       // stored straight from registers (no staging, two barriers fewer)
-      pass_load<P, E, RL, true>(v, zb, t);
+      pass_load<P, E, RL, true>(v, fin, t);
       pass_compute<P, E, RL, NSL, true, true, true>(v, t, fftw + pass_tw_offset(P, NSL));
       // A warp's 32 blocks of one r are 1 KB contiguous (ascending in the
       // lane for m < P/2, descending above); two lane shuffles per half let
