@@ -118,6 +118,9 @@ struct TrCfg {
   static constexpr size_t SMEM = C::COLS * COL_BYTES + (TABLES ? C::N * 8 + C::TW * 16 : 0);
 };
 
+#ifndef FLB_NDCT_TMEM
+#define FLB_NDCT_TMEM 1
+#endif
 #ifndef FLB_NDCT_FWD2
 #define FLB_NDCT_FWD2 1
 #endif
@@ -128,10 +131,14 @@ template <int LOG2N, bool BES>
 struct FwdCfg {
   using C = Cfg<LOG2N>;
   static constexpr bool TWO = BES && FLB_NDCT_FWD2 && LOG2N <= 12;
+  // TM (two CTAs per SM): the previous Chebyshev stage T_{m-1}(x) c -- read
+  // only at a thread's own entries -- lives in tensor memory, which frees
+  // the second shared stage buffer for a second FFT row (ping-pong passes)
+  static constexpr bool TM = TWO && FLB_NDCT_TMEM && C::COLS == 1;
   static constexpr int MINB = TWO ? 2 : 1;
-  static constexpr bool PP = !TWO && C::PP;
+  static constexpr bool PP = TM || (!TWO && C::PP);
   static constexpr bool TABLES = !TWO && C::SMEM_TABLES;
-  static constexpr size_t COL_BYTES = 2 * C::N * sizeof(double) + (PP ? 2 : 1) * C::ZB;
+  static constexpr size_t COL_BYTES = (TM ? 1 : 2) * C::N * sizeof(double) + (PP ? 2 : 1) * C::ZB;
   static constexpr size_t SMEM = C::COLS * COL_BYTES + (TABLES ? C::N * 8 + C::TW * 16 : 0);
 };
 
@@ -203,10 +210,12 @@ __constant__ double kC8[16][2] = {
 // is some thread's m or m + P), so a caller needs no separate check pass.
 template <int N, bool ODD, int R, int NM>
 __device__ __forceinline__ double2 fwd_pack(const double* stage, double* next, int m, double2 ta_t,
-                                            double2 r4_t, bool* bad = nullptr) {
+                                            double2 r4_t, bool* bad = nullptr,
+                                            double2* own = nullptr) {
   constexpr int P = N / 2;
   constexpr double h = 0.70710678118654752440;
   const double s_m = stage[m], s_mp = stage[m + P];
+  if (own) *own = make_double2(s_m, s_mp);
   if (bad) *bad |= !isfinite(s_m) || !isfinite(s_mp);
   const double s_nm = stage[(N - m) & (N - 1)], s_pm = stage[P - m];
   if (NM == 1) {
@@ -305,6 +314,143 @@ __device__ __forceinline__ double2* fwd_term(const double* stage, double* next, 
   return fin;
 }
 
+// ---- tensor-memory stage (FwdCfg::TM) --------------------------------------
+// Each thread keeps 16 doubles of its own stage entries (m, m + P for its 8
+// m) per slot in its TMEM lane: slot A = T_{m-1}(x) c, slot B = the next
+// stage T_{m+1}(x) c until it is written back to shared memory.
+__device__ __forceinline__ void tm_st16(uint32_t taddr, const uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
+      : "memory");
+}
+__device__ __forceinline__ void tm_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
+      "%11, %12, %13, %14, %15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+        "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_st8(uint32_t taddr, const uint32_t* v) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+      : "memory");
+}
+__device__ __forceinline__ void tm_ld8(uint32_t taddr, uint32_t* v) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+__device__ __forceinline__ void split2(double d, uint32_t* w) {
+  w[0] = (uint32_t)__double2loint(d);
+  w[1] = (uint32_t)__double2hiint(d);
+}
+__device__ __forceinline__ double join2(const uint32_t* w) {
+  return __hiloint2double((int)w[1], (int)w[0]);
+}
+
+// Half h (entries r = 4h .. 4h + 3) of the TM pack: Z_m for m = t + r T from
+// the shared stage T_l c (own and mirrored entries), and at the own entries
+// next = x c (FIRST) or 2 x T_l c - T_{l-1} c; T_l c -> slot A, next -> B.
+template <int N, bool ODD, bool FIRST, int R, int RE>
+__device__ __forceinline__ void tm_pack_rec(double2* v, const double* stage, int t, double2 ta_t,
+                                            double2 r4_t, const uint32_t (&prev)[8],
+                                            uint32_t (&cw)[8], uint32_t (&nw)[8]) {
+  if constexpr (R < RE) {
+    constexpr int P = N / 2, rr = R % 2;
+    const int m = t + R * (N / 16);
+    double2 own;
+    v[R] = fwd_pack<N, ODD, R, 0>(stage, nullptr, m, ta_t, r4_t, nullptr, &own);
+    const double x0 = (double)m / (double)N, x1 = (double)(m + P) / (double)N;
+    double n0, n1;
+    if constexpr (FIRST) {
+      n0 = own.x * x0;
+      n1 = own.y * x1;
+    } else {
+      n0 = fma(2.0 * x0, own.x, -join2(&prev[4 * rr]));
+      n1 = fma(2.0 * x1, own.y, -join2(&prev[4 * rr + 2]));
+    }
+    split2(own.x, &cw[4 * rr]);
+    split2(own.y, &cw[4 * rr + 2]);
+    split2(n0, &nw[4 * rr]);
+    split2(n1, &nw[4 * rr + 2]);
+    tm_pack_rec<N, ODD, FIRST, R + 1, RE>(v, stage, t, ta_t, r4_t, prev, cw, nw);
+  }
+}
+
+// One Chebyshev term of the TM forward kernel (PST = T weights, ping-pong
+// FFT rows zx / zy): returns the row the last pass read.
+template <int LOG2N, bool ODD, bool FIRST>
+__device__ __forceinline__ double2* tm_fwd_term(double* stage, double2* zx, double2* zy, int t,
+                                                double2 ta_t, double2 r4_t, const double2* fftw,
+                                                const double* p, double* f, uint32_t tA,
+                                                uint32_t tB) {
+  using C = Cfg<LOG2N>;
+  constexpr int N = C::N, P = C::P, T = C::T, E = C::E, NSL = C::NSL, RL = C::RL;
+  static_assert(E == 8 && T == N / 16, "pack twiddle constants assume T = N/16");
+  constexpr int PST = T;
+  double2 v[E];
+  // quarters (two entries r each): few live registers around the pack
+#define FLB_TM_QUARTER(Q)                                                                   \
+  {                                                                                         \
+    uint32_t prev[8], cw[8], nw[8];                                                         \
+    if constexpr (!FIRST) tm_ld8(tA + 8 * (Q), prev);                                       \
+    tm_pack_rec<N, ODD, FIRST, 2 * (Q), 2 * (Q) + 2>(v, stage, t, ta_t, r4_t, prev, cw, nw); \
+    tm_st8(tA + 8 * (Q), cw);                                                               \
+    tm_st8(tB + 8 * (Q), nw);                                                               \
+  }
+  FLB_TM_QUARTER(0)
+  FLB_TM_QUARTER(1)
+  FLB_TM_QUARTER(2)
+  FLB_TM_QUARTER(3)
+#undef FLB_TM_QUARTER
+  pass_compute<P, E, 8, 1, true>(v, t, fftw);
+  pass_store<P, E, 8, 1>(v, zx, t);
+  tm_wait_st();
+  __syncthreads();  // pass-1 rows complete; every pack has read the stage
+  // write the next stage back over this one (own entries)
+#pragma unroll
+  for (int h = 0; h < 4; ++h) {
+    uint32_t nw[8];
+    tm_ld8(tB + 8 * h, nw);
+#pragma unroll
+    for (int rr = 0; rr < 2; ++rr) {
+      const int m = t + (2 * h + rr) * T;
+      stage[m] = join2(&nw[4 * rr]);
+      stage[m + P] = join2(&nw[4 * rr + 2]);
+    }
+  }
+  double2* fin = mid_passes_pp<P, E, 8, NSL, true, 0, true>(zx, zy, t, fftw, 0);
+  pass_load<P, E, RL>(v, fin, t);
+  pass_compute<P, E, RL, NSL, true, true>(v, t, fftw + pass_tw_offset(P, NSL));
+#pragma unroll
+  for (int q = 0; q < E / RL; ++q)
+#pragma unroll
+    for (int r = 0; r < RL; ++r) {
+      const int m = t + q * T + r * NSL;
+      const double2 z = v[q * RL + r];
+#pragma unroll
+      for (int part = 0; part < 2; ++part) {
+        const int i = 2 * (q * RL + r) + part;
+        const int k = fwd_row_of<N>(2 * m + part);
+        double y = part ? z.y : z.x;
+        if (ODD && (k & 1)) y = -y;
+        f[i] += __ldg(p + i * PST) * y;
+      }
+    }
+  return fin;
+}
+
 // plain_op: -1 = NDCT with num_terms terms; 0 = one plain DCT-III;
 // 1 = one plain DST-III. BES: Chebyshev (Jacobi-Anger) expansion instead of
 // Taylor -- stage T_m(n/N) c_n by the three-term recurrence, weights
@@ -338,8 +484,8 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
   const size_t col = (size_t)blockIdx.x * C::COLS + g;
   if (col >= batch) return;
   double* stage = smem + g * (FC::COL_BYTES / 8);  // (n/N)^l c_n, terms l even
-  double* stage_odd = stage + N;                  // terms l odd
-  double2* zbA = reinterpret_cast<double2*>(stage + 2 * N);
+  double* stage_odd = stage + N;                  // terms l odd (not with TM)
+  double2* zbA = reinterpret_cast<double2*>(stage + (FC::TM ? 1 : 2) * N);
   double2* zbB = FC::PP ? zbA + C::ZB / sizeof(double2) : zbA;
   double2* zx = zbA;  // the first pass's target this term
   auto other = [&](double2* b) { return b == zbA ? zbB : zbA; };
@@ -369,6 +515,40 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
       fwd_term<LOG2N, true, 0, FC::PP>(stage, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw, p, f, 1.0);
     else
       fwd_term<LOG2N, false, 0, FC::PP>(stage, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw, p, f, 1.0);
+  } else if (BES && FC::TM) {
+    // previous stage in TMEM, ping-pong FFT rows (FwdCfg::TM)
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base)))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // this warp's lane quarter, 64 columns per warp pair
+    const uint32_t tA = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 64u * (uint32_t)(warp >> 2);
+    const uint32_t tB = tA + 32;
+    double2* zy = zbB;
+    for (int m = 0; m < num_terms; ++m) {
+      const double* wr = wtab + (size_t)m * N + t;
+      double2* fin;
+      if (m == 0)
+        fin = tm_fwd_term<LOG2N, false, true>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB);
+      else if (m & 1)
+        fin = tm_fwd_term<LOG2N, true, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB);
+      else
+        fin = tm_fwd_term<LOG2N, false, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB);
+      zy = fin;  // the next term's first pass writes the row the last pass did not read
+      zx = other(fin);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem_base)
+                   : "memory");
   } else if (BES && FC::TWO) {
     // weights read where they are applied (PST = T), pack in two halves
     for (int m = 0; m < num_terms; ++m) {
