@@ -107,20 +107,26 @@ struct Cfg {
 // 28.3 -> 26.2 ms for the C4 IDLT. The Taylor transpose (row factors kept in
 // registers) and the forward kernel are faster at one CTA per SM with
 // ping-pong rows and shared tables.
+#ifndef FLB_NDCT_TMEM
+#define FLB_NDCT_TMEM 1
+#endif
+#ifndef FLB_NDCT_TR_PP
+#define FLB_NDCT_TR_PP 1
+#endif
 template <int LOG2N, bool BES>
 struct TrCfg {
   using C = Cfg<LOG2N>;
   static constexpr bool TWO = BES && LOG2N <= 12;
   static constexpr int MINB = TWO ? 2 : 1;
-  static constexpr bool PP = !TWO && C::PP;
+  // BES: the stage is the (weighted-on-the-fly) input itself, one buffer;
+  // the Taylor stage's second buffer becomes a second FFT row (ping-pong)
+  static constexpr bool ONE_STAGE = BES && TWO && FLB_NDCT_TR_PP && C::COLS == 1;
+  static constexpr bool PP = ONE_STAGE || (!TWO && C::PP);
   static constexpr bool TABLES = !TWO && C::SMEM_TABLES;
-  static constexpr size_t COL_BYTES = 2 * C::N * sizeof(double) + (PP ? 2 : 1) * C::ZB;
+  static constexpr size_t COL_BYTES = (ONE_STAGE ? 1 : 2) * C::N * sizeof(double) + (PP ? 2 : 1) * C::ZB;
   static constexpr size_t SMEM = C::COLS * COL_BYTES + (TABLES ? C::N * 8 + C::TW * 16 : 0);
 };
 
-#ifndef FLB_NDCT_TMEM
-#define FLB_NDCT_TMEM 1
-#endif
 #ifndef FLB_NDCT_FWD2
 #define FLB_NDCT_FWD2 1
 #endif
@@ -765,8 +771,8 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
   if (col >= batch) return;
   // h_k = (N delta_k)^l / l! g_k at hs[tr_slot(k)], double-buffered by term parity
   double* hs = smem + g * (TC::COL_BYTES / 8);
-  double* hs_odd = hs + N;
-  double2* zbA = reinterpret_cast<double2*>(hs + 2 * N);
+  double* hs_odd = hs + N;  // (Taylor only)
+  double2* zbA = reinterpret_cast<double2*>(hs + (TC::ONE_STAGE ? 1 : 2) * N);
   double2* zbB = TC::PP ? zbA + C::ZB / sizeof(double2) : zbA;
   double2* zx = zbA;  // the first pass's target this term
   auto other = [&](double2* b) { return b == zbA ? zbB : zbA; };
@@ -795,16 +801,19 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
       tr_term<LOG2N, false, 0, TC::PP>(hs, nullptr, nd, delta, 0.0, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                                rp, o, 1.0);
   } else if (BES && TC::TWO) {
-    // row factors read where they are applied (PST = T): fewer live registers
+    // row factors read where they are applied (PST = T): fewer live registers;
+    // ping-pong rows when the second stage buffer is free (ONE_STAGE)
     for (int m = 0; m < num_terms; ++m) {
       const double* tr = ttab + (size_t)m * N + t;
       const double* wrow = wtab + (size_t)m * N;
+      double2* fin;
       if (m & 1)
-        tr_term<LOG2N, true, 2, false, T>(hs, nullptr, nd, delta, 0.0, wrow, zx, zx, t, bar, ta_t,
-                                          r4_t, fftw, tr, o, 1.0);
+        fin = tr_term<LOG2N, true, 2, TC::ONE_STAGE, T>(hs, nullptr, nd, delta, 0.0, wrow, zx,
+                                                       other(zx), t, bar, ta_t, r4_t, fftw, tr, o, 1.0);
       else
-        tr_term<LOG2N, false, 2, false, T>(hs, nullptr, nd, delta, 0.0, wrow, zx, zx, t, bar, ta_t,
-                                           r4_t, fftw, tr, o, 1.0);
+        fin = tr_term<LOG2N, false, 2, TC::ONE_STAGE, T>(hs, nullptr, nd, delta, 0.0, wrow, zx,
+                                                        other(zx), t, bar, ta_t, r4_t, fftw, tr, o, 1.0);
+      if (TC::ONE_STAGE) zx = other(fin);
     }
   } else if (BES) {
     for (int m = 0; m < num_terms; ++m) {
