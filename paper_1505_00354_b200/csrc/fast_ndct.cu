@@ -96,8 +96,6 @@ struct Cfg {
   static constexpr size_t COL_BYTES = 2 * N * sizeof(double) + (PP ? 2 : 1) * ZB;
   // tables in shared memory when they fit beside the columns
   static constexpr bool SMEM_TABLES = COLS * COL_BYTES + N * 8 + TW * 16 <= 220 * 1024;
-
-  static constexpr size_t SMEM = COLS * COL_BYTES + (SMEM_TABLES ? N * 8 + TW * 16 : 0);
   static constexpr int GT = COLS == 1 ? 0 : T;    // group barrier width (0 = whole CTA)
 };
 
@@ -324,24 +322,6 @@ __device__ __forceinline__ double2* fwd_term(const double* stage, double* next, 
 // Each thread keeps 16 doubles of its own stage entries (m, m + P for its 8
 // m) per slot in its TMEM lane: slot A = T_{m-1}(x) c, slot B = the next
 // stage T_{m+1}(x) c until it is written back to shared memory.
-__device__ __forceinline__ void tm_st16(uint32_t taddr, const uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-      "%11, %12, %13, %14, %15, %16};" ::"r"(taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
-      "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-      : "memory");
-}
-__device__ __forceinline__ void tm_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, "
-      "%11, %12, %13, %14, %15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-        "=r"(v[14]), "=r"(v[15])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 __device__ __forceinline__ void tm_st8(uint32_t taddr, const uint32_t* v) {
   asm volatile(
       "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"r"(taddr),
@@ -470,7 +450,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
                          int* nonfinite) {
   using C = Cfg<LOG2N>;
   using FC = FwdCfg<LOG2N, BES>;
-  constexpr int N = C::N, T = C::T, OWN = C::OWN, E = C::E, NSL = C::NSL, RL = C::RL;
+  constexpr int N = C::N, T = C::T, OWN = C::OWN;
   extern __shared__ double smem[];
   double* nd = smem + C::COLS * (FC::COL_BYTES / 8);
   double2* fftw_s = reinterpret_cast<double2*>(nd + N);
