@@ -212,7 +212,9 @@ __constant__ double kC8[16][2] = {
 // buffer `next` holding T_{m-1}(x) c_n), x = n/N.
 // bad (optional): set when stage[m] or stage[m + P] is not finite (every entry
 // is some thread's m or m + P), so a caller needs no separate check pass.
-template <int N, bool ODD, int R, int NM>
+// HALF: the stage holds a/2 (the 1/2 of X_j = a_j/2 pre-applied), saving
+// four multiplies per Z.
+template <int N, bool ODD, int R, int NM, bool HALF = false>
 __device__ __forceinline__ double2 fwd_pack(const double* stage, double* next, int m, double2 ta_t,
                                             double2 r4_t, bool* bad = nullptr,
                                             double2* own = nullptr) {
@@ -231,10 +233,11 @@ __device__ __forceinline__ double2 fwd_pack(const double* stage, double* next, i
   }
   // X_j = a_j / 2 (X_0 = a_0, X_N = 0); a = stage (DCT) or the reversed stage (DST)
   const bool m0 = m == 0;
-  const double xa = ODD ? (m0 ? 0.0 : 0.5 * s_nm) : (m0 ? s_m : 0.5 * s_m);
-  const double xan = m0 ? 0.0 : 0.5 * (ODD ? s_m : s_nm);
-  const double xb = 0.5 * (ODD ? s_pm : s_mp);
-  const double xbn = 0.5 * (ODD ? s_mp : s_pm);
+  constexpr double hf = HALF ? 1.0 : 0.5;  // (multiplications by 1.0 fold away)
+  const double xa = ODD ? (m0 ? 0.0 : hf * s_nm) : (m0 ? (HALF ? 2.0 * s_m : s_m) : hf * s_m);
+  const double xan = m0 ? 0.0 : hf * (ODD ? s_m : s_nm);
+  const double xb = hf * (ODD ? s_pm : s_mp);
+  const double xbn = hf * (ODD ? s_mp : s_pm);
   constexpr double a32x = PackConst::c32[R][0], a32y = PackConst::c32[R][1];
   constexpr double a8x = PackConst::c8[R][0], a8y = PackConst::c8[R][1];
   // e^{i pi m/(2N)}, e^{i pi (m+P)/(2N)} = e^{i pi/4} e^{i pi m/(2N)}, e^{2 pi i m/N}
@@ -348,29 +351,32 @@ __device__ __forceinline__ double join2(const uint32_t* w) {
 // Half h (entries r = 4h .. 4h + 3) of the TM pack: Z_m for m = t + r T from
 // the shared stage T_l c (own and mirrored entries), and at the own entries
 // next = x c (FIRST) or 2 x T_l c - T_{l-1} c; T_l c -> slot A, next -> B.
+// The stage holds T_l(x) c / 2 (fwd_pack HALF; the recurrence is linear).
+// xt2 = 2 t / N: 2 x_m = xt2 + R/8 and 2 x_{m+P} = 2 x_m + 1 (m = t + R N/16).
 template <int N, bool ODD, bool FIRST, int R, int RE>
-__device__ __forceinline__ void tm_pack_rec(double2* v, const double* stage, int t, double2 ta_t,
-                                            double2 r4_t, const uint32_t (&prev)[8],
-                                            uint32_t (&cw)[8], uint32_t (&nw)[8]) {
+__device__ __forceinline__ void tm_pack_rec(double2* v, const double* stage, int t, double xt2,
+                                            double2 ta_t, double2 r4_t,
+                                            const uint32_t (&prev)[8], uint32_t (&cw)[8],
+                                            uint32_t (&nw)[8]) {
   if constexpr (R < RE) {
-    constexpr int P = N / 2, rr = R % 2;
+    constexpr int rr = R % 2;
     const int m = t + R * (N / 16);
     double2 own;
-    v[R] = fwd_pack<N, ODD, R, 0>(stage, nullptr, m, ta_t, r4_t, nullptr, &own);
-    const double x0 = (double)m / (double)N, x1 = (double)(m + P) / (double)N;
+    v[R] = fwd_pack<N, ODD, R, 0, true>(stage, nullptr, m, ta_t, r4_t, nullptr, &own);
+    const double tx0 = xt2 + (double)R / 8.0, tx1 = tx0 + 1.0;  // 2 x (exact)
     double n0, n1;
     if constexpr (FIRST) {
-      n0 = own.x * x0;
-      n1 = own.y * x1;
+      n0 = own.x * (0.5 * tx0);
+      n1 = own.y * (0.5 * tx1);
     } else {
-      n0 = fma(2.0 * x0, own.x, -join2(&prev[4 * rr]));
-      n1 = fma(2.0 * x1, own.y, -join2(&prev[4 * rr + 2]));
+      n0 = fma(tx0, own.x, -join2(&prev[4 * rr]));
+      n1 = fma(tx1, own.y, -join2(&prev[4 * rr + 2]));
     }
     split2(own.x, &cw[4 * rr]);
     split2(own.y, &cw[4 * rr + 2]);
     split2(n0, &nw[4 * rr]);
     split2(n1, &nw[4 * rr + 2]);
-    tm_pack_rec<N, ODD, FIRST, R + 1, RE>(v, stage, t, ta_t, r4_t, prev, cw, nw);
+    tm_pack_rec<N, ODD, FIRST, R + 1, RE>(v, stage, t, xt2, ta_t, r4_t, prev, cw, nw);
   }
 }
 
@@ -385,13 +391,14 @@ __device__ __forceinline__ double2* tm_fwd_term(double* stage, double2* zx, doub
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, NSL = C::NSL, RL = C::RL;
   static_assert(E == 8 && T == N / 16, "pack twiddle constants assume T = N/16");
   constexpr int PST = T;
+  const double xt2 = (double)(2 * t) / (double)N;
   double2 v[E];
   // quarters (two entries r each): few live registers around the pack
 #define FLB_TM_QUARTER(Q)                                                                   \
   {                                                                                         \
     uint32_t prev[8], cw[8], nw[8];                                                         \
     if constexpr (!FIRST) tm_ld8(tA + 8 * (Q), prev);                                       \
-    tm_pack_rec<N, ODD, FIRST, 2 * (Q), 2 * (Q) + 2>(v, stage, t, ta_t, r4_t, prev, cw, nw); \
+    tm_pack_rec<N, ODD, FIRST, 2 * (Q), 2 * (Q) + 2>(v, stage, t, xt2, ta_t, r4_t, prev, cw, nw); \
     tm_st8(tA + 8 * (Q), cw);                                                               \
     tm_st8(tB + 8 * (Q), nw);                                                               \
   }
@@ -482,7 +489,8 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
     const int n = t + T * i;
     const double v = src[n];
     bad |= !isfinite(v);
-    stage[n] = v;
+    // the TM Chebyshev path keeps the stage halved (fwd_pack HALF)
+    stage[n] = (BES && FC::TM && plain_op < 0) ? 0.5 * v : v;
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
   auto kown = [&](int i) -> int { return own_row(t, i); };
