@@ -626,9 +626,10 @@ __device__ __forceinline__ int tr_row(int t, int i) {
 // X = Re(conj(h) V), h = e^{i pi kk/(2N)}; tn = e^{i pi n/(2N)}, rn = e^{2 pi i n/N}
 // of the output row n (kk = n, or N - n for the DST^T of odd terms).
 template <bool ODD>
+// (Returns 2 X: the 1/2 of V is applied by the caller, with the term's sign.)
 __device__ __forceinline__ double tr_unpack(double2 za, double2 zc, double2 tn, double2 rn) {
-  const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
-  const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));
+  const double2 ev = make_double2(za.x + zc.x, za.y - zc.y);
+  const double2 od = make_double2(za.y + zc.y, zc.x - za.x);
   const double2 r = ODD ? rn : make_double2(rn.x, -rn.y);
   const double2 h = ODD ? make_double2(tn.y, tn.x) : tn;
   const double2 Vv = make_double2(ev.x + od.x * r.x - od.y * r.y, ev.y + od.x * r.y + od.y * r.x);
@@ -721,10 +722,12 @@ __device__ __forceinline__ double2* tr_term(const double* hs, double* next, cons
     const double x1 = ODD ? tr_unpack<true>(zA1, zB1, t1, r1) : tr_unpack<false>(zB1, zA1, t1, r1);
     const double x2 = ODD ? tr_unpack<true>(zB, zA, t2, r2) : tr_unpack<false>(zA, zB, t2, r2);
     const double x3 = ODD ? tr_unpack<true>(zA1, zB1, t3, r3) : tr_unpack<false>(zB1, zA1, t3, r3);
-    o[4 * g + 0] += sign * (PST == 1 ? rp[4 * g + 0] : __ldg(rp + (4 * g + 0) * PST)) * x0;
-    o[4 * g + 1] += sign * (PST == 1 ? rp[4 * g + 1] : __ldg(rp + (4 * g + 1) * PST)) * x1;
-    o[4 * g + 2] += sign * (PST == 1 ? rp[4 * g + 2] : __ldg(rp + (4 * g + 2) * PST)) * x2;
-    o[4 * g + 3] += sign * (PST == 1 ? rp[4 * g + 3] : __ldg(rp + (4 * g + 3) * PST)) * x3;
+    // x_j = 2 X (tr_unpack): the 1/2 rides on the sign (exact)
+    const double hs2 = 0.5 * sign;
+    o[4 * g + 0] += hs2 * (PST == 1 ? rp[4 * g + 0] : __ldg(rp + (4 * g + 0) * PST)) * x0;
+    o[4 * g + 1] += hs2 * (PST == 1 ? rp[4 * g + 1] : __ldg(rp + (4 * g + 1) * PST)) * x1;
+    o[4 * g + 2] += hs2 * (PST == 1 ? rp[4 * g + 2] : __ldg(rp + (4 * g + 2) * PST)) * x2;
+    o[4 * g + 3] += hs2 * (PST == 1 ? rp[4 * g + 3] : __ldg(rp + (4 * g + 3) * PST)) * x3;
   }
   return zb;
 }
