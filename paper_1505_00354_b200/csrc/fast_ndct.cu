@@ -111,6 +111,10 @@ struct Cfg {
 #ifndef FLB_NDCT_TR_PP
 #define FLB_NDCT_TR_PP 1
 #endif
+#ifndef FLB_TM_FACC
+#define FLB_TM_FACC 1  // TM forward kernel: the 16 accumulators per thread in TMEM too
+#endif
+constexpr int kTmCols = FLB_TM_FACC ? 256 : 128;  // TMEM columns per CTA
 template <int LOG2N, bool BES>
 struct TrCfg {
   using C = Cfg<LOG2N>;
@@ -386,7 +390,7 @@ template <int LOG2N, bool ODD, bool FIRST>
 __device__ __forceinline__ double2* tm_fwd_term(double* stage, double2* zx, double2* zy, int t,
                                                 double2 ta_t, double2 r4_t, const double2* fftw,
                                                 const double* p, double* f, uint32_t tA,
-                                                uint32_t tB) {
+                                                uint32_t tB, uint32_t tF) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, NSL = C::NSL, RL = C::RL;
   static_assert(E == 8 && T == N / 16, "pack twiddle constants assume T = N/16");
@@ -426,21 +430,43 @@ __device__ __forceinline__ double2* tm_fwd_term(double* stage, double2* zx, doub
   double2* fin = mid_passes_pp<P, E, 8, NSL, true, 0, true>(zx, zy, t, fftw, 0);
   pass_load<P, E, RL>(v, fin, t);
   pass_compute<P, E, RL, NSL, true, true>(v, t, fftw + pass_tw_offset(P, NSL));
+  if constexpr (FLB_TM_FACC) {
+    // the accumulators live in TMEM (slot F): load, update, store back
 #pragma unroll
-  for (int q = 0; q < E / RL; ++q)
+    for (int h = 0; h < 2; ++h) {
+      uint32_t fw[16];
+      tm_ld8(tF + 16 * h, fw);
+      tm_ld8(tF + 16 * h + 8, fw + 8);
 #pragma unroll
-    for (int r = 0; r < RL; ++r) {
-      const int m = t + q * T + r * NSL;
-      const double2 z = v[q * RL + r];
-#pragma unroll
-      for (int part = 0; part < 2; ++part) {
-        const int i = 2 * (q * RL + r) + part;
+      for (int i8 = 0; i8 < 8; ++i8) {
+        const int i = 8 * h + i8, s = i >> 1, q = s / RL, r = s % RL, part = i & 1;
+        const int m = t + q * T + r * NSL;
+        const double2 z = v[q * RL + r];
         const int k = fwd_row_of<N>(2 * m + part);
         double y = part ? z.y : z.x;
         if (ODD && (k & 1)) y = -y;
-        f[i] += __ldg(p + i * PST) * y;
+        split2(join2(&fw[2 * i8]) + __ldg(p + i * PST) * y, &fw[2 * i8]);
       }
+      tm_st8(tF + 16 * h, fw);
+      tm_st8(tF + 16 * h + 8, fw + 8);
     }
+  } else {
+#pragma unroll
+    for (int q = 0; q < E / RL; ++q)
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        const int m = t + q * T + r * NSL;
+        const double2 z = v[q * RL + r];
+#pragma unroll
+        for (int part = 0; part < 2; ++part) {
+          const int i = 2 * (q * RL + r) + part;
+          const int k = fwd_row_of<N>(2 * m + part);
+          double y = part ? z.y : z.x;
+          if (ODD && (k & 1)) y = -y;
+          f[i] += __ldg(p + i * PST) * y;
+        }
+      }
+  }
   return fin;
 }
 
@@ -514,34 +540,54 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5;
     if (warp == 0) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
-                       static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base)))
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base))),
+                   "n"(kTmCols)
                    : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // this warp's lane quarter, 64 columns per warp pair
-    const uint32_t tA = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 64u * (uint32_t)(warp >> 2);
+    // this warp's lane quarter; per warp 64 (+ 32 with FLB_TM_FACC) columns
+    constexpr uint32_t kWarpCols = FLB_TM_FACC ? 128u : 64u;
+    const uint32_t tA = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + kWarpCols * (uint32_t)(warp >> 2);
     const uint32_t tB = tA + 32;
+    const uint32_t tF = tA + 64;
+    if constexpr (FLB_TM_FACC) {
+      uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tm_st8(tF + 8 * q, z);
+      tm_wait_st();
+    }
     double2* zy = zbB;
     for (int m = 0; m < num_terms; ++m) {
       const double* wr = wtab + (size_t)m * N + t;
       double2* fin;
       if (m == 0)
-        fin = tm_fwd_term<LOG2N, false, true>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB);
+        fin = tm_fwd_term<LOG2N, false, true>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF);
       else if (m & 1)
-        fin = tm_fwd_term<LOG2N, true, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB);
+        fin = tm_fwd_term<LOG2N, true, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF);
       else
-        fin = tm_fwd_term<LOG2N, false, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB);
+        fin = tm_fwd_term<LOG2N, false, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF);
       zy = fin;  // the next term's first pass writes the row the last pass did not read
       zx = other(fin);
+    }
+    if constexpr (FLB_TM_FACC) {
+      tm_wait_st();
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        uint32_t fw[8];
+        tm_ld8(tF + 8 * q, fw);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) f[4 * q + j] = join2(&fw[2 * j]);
+      }
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem_base)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(kTmCols)
                    : "memory");
   } else if (BES && FC::TWO) {
     // weights read where they are applied (PST = T), pack in two halves
