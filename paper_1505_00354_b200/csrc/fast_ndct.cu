@@ -111,6 +111,9 @@ struct Cfg {
 #ifndef FLB_NDCT_TR_PP
 #define FLB_NDCT_TR_PP 1
 #endif
+#ifndef FLB_NDCT_TR_TMO
+#define FLB_NDCT_TR_TMO 1
+#endif
 #ifndef FLB_TM_FACC
 #define FLB_TM_FACC 1  // TM forward kernel: the 16 accumulators per thread in TMEM too
 #endif
@@ -124,6 +127,8 @@ struct TrCfg {
   // the Taylor stage's second buffer becomes a second FFT row (ping-pong)
   static constexpr bool ONE_STAGE = BES && TWO && FLB_NDCT_TR_PP && C::COLS == 1;
   static constexpr bool PP = ONE_STAGE || (!TWO && C::PP);
+  // TMO: the output accumulators in TMEM (with ONE_STAGE)
+  static constexpr bool TMO = ONE_STAGE && FLB_NDCT_TR_TMO;
   static constexpr bool TABLES = !TWO && C::SMEM_TABLES;
   static constexpr size_t COL_BYTES = (ONE_STAGE ? 1 : 2) * C::N * sizeof(double) + (PP ? 2 : 1) * C::ZB;
   static constexpr size_t SMEM = C::COLS * COL_BYTES + (TABLES ? C::N * 8 + C::TW * 16 : 0);
@@ -691,13 +696,15 @@ __device__ __forceinline__ double tr_unpack(double2 za, double2 zc, double2 tn, 
 // ping-pong (C::PP) as in fwd_term (returns the buffer the unpack read; the
 // caller passes the other one as the next zx), else in place with a barrier
 // ordering the first store after the previous term's unpack reads.
-template <int LOG2N, bool ODD, int PM, bool PPX = Cfg<LOG2N>::PP, int PST = 1>
+// TMO: the 16 output accumulators live in the thread's TMEM lane at tO
+// (loaded, updated and stored back per row group) instead of o[].
+template <int LOG2N, bool ODD, int PM, bool PPX = Cfg<LOG2N>::PP, int PST = 1, bool TMO = false>
 __device__ __forceinline__ double2* tr_term(const double* hs, double* next, const double* nd,
                                             const double* __restrict__ delta, double inv_next,
                                             const double* __restrict__ wrow, double2* zx,
                                             double2* zy, int t, int bar, double2 ta_t,
                                             double2 r4_t, const double2* fftw, const double* rp,
-                                            double* o, double sign) {
+                                            double* o, double sign, uint32_t tO = 0) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, OWN = C::OWN;
   static_assert(E == 8 && T == N / 16, "row grouping assumes T = N/16");
@@ -770,11 +777,22 @@ __device__ __forceinline__ double2* tr_term(const double* hs, double* next, cons
     const double x3 = ODD ? tr_unpack<true>(zA1, zB1, t3, r3) : tr_unpack<false>(zB1, zA1, t3, r3);
     // x_j = 2 X (tr_unpack): the 1/2 rides on the sign (exact)
     const double hs2 = 0.5 * sign;
-    o[4 * g + 0] += hs2 * (PST == 1 ? rp[4 * g + 0] : __ldg(rp + (4 * g + 0) * PST)) * x0;
-    o[4 * g + 1] += hs2 * (PST == 1 ? rp[4 * g + 1] : __ldg(rp + (4 * g + 1) * PST)) * x1;
-    o[4 * g + 2] += hs2 * (PST == 1 ? rp[4 * g + 2] : __ldg(rp + (4 * g + 2) * PST)) * x2;
-    o[4 * g + 3] += hs2 * (PST == 1 ? rp[4 * g + 3] : __ldg(rp + (4 * g + 3) * PST)) * x3;
+    if constexpr (TMO) {
+      uint32_t ow[8];
+      tm_ld8(tO + 8 * g, ow);
+      split2(join2(&ow[0]) + hs2 * (PST == 1 ? rp[4 * g + 0] : __ldg(rp + (4 * g + 0) * PST)) * x0, &ow[0]);
+      split2(join2(&ow[2]) + hs2 * (PST == 1 ? rp[4 * g + 1] : __ldg(rp + (4 * g + 1) * PST)) * x1, &ow[2]);
+      split2(join2(&ow[4]) + hs2 * (PST == 1 ? rp[4 * g + 2] : __ldg(rp + (4 * g + 2) * PST)) * x2, &ow[4]);
+      split2(join2(&ow[6]) + hs2 * (PST == 1 ? rp[4 * g + 3] : __ldg(rp + (4 * g + 3) * PST)) * x3, &ow[6]);
+      tm_st8(tO + 8 * g, ow);
+    } else {
+      o[4 * g + 0] += hs2 * (PST == 1 ? rp[4 * g + 0] : __ldg(rp + (4 * g + 0) * PST)) * x0;
+      o[4 * g + 1] += hs2 * (PST == 1 ? rp[4 * g + 1] : __ldg(rp + (4 * g + 1) * PST)) * x1;
+      o[4 * g + 2] += hs2 * (PST == 1 ? rp[4 * g + 2] : __ldg(rp + (4 * g + 2) * PST)) * x2;
+      o[4 * g + 3] += hs2 * (PST == 1 ? rp[4 * g + 3] : __ldg(rp + (4 * g + 3) * PST)) * x3;
+    }
   }
+  if constexpr (TMO) tm_wait_st();
   return zb;
 }
 
@@ -837,6 +855,50 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
     else
       tr_term<LOG2N, false, 0, TC::PP>(hs, nullptr, nd, delta, 0.0, nullptr, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                                rp, o, 1.0);
+  } else if (BES && TC::TMO) {
+    // as below, with the output accumulators in TMEM (TrCfg::TMO)
+    __shared__ uint32_t tmem_base;
+    const int warp = threadIdx.x >> 5;
+    if (warp == 0) {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base)))
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    const uint32_t tO = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 32u * (uint32_t)(warp >> 2);
+    {
+      uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) tm_st8(tO + 8 * q, z);
+      tm_wait_st();
+    }
+    for (int m = 0; m < num_terms; ++m) {
+      const double* tr = ttab + (size_t)m * N + t;
+      const double* wrow = wtab + (size_t)m * N;
+      double2* fin;
+      if (m & 1)
+        fin = tr_term<LOG2N, true, 2, true, T, true>(hs, nullptr, nd, delta, 0.0, wrow, zx, other(zx),
+                                                     t, bar, ta_t, r4_t, fftw, tr, o, 1.0, tO);
+      else
+        fin = tr_term<LOG2N, false, 2, true, T, true>(hs, nullptr, nd, delta, 0.0, wrow, zx, other(zx),
+                                                      t, bar, ta_t, r4_t, fftw, tr, o, 1.0, tO);
+      zx = other(fin);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t ow[8];
+      tm_ld8(tO + 8 * q, ow);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) o[4 * q + j] = join2(&ow[2 * j]);
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    __syncthreads();
+    if (warp == 0)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem_base)
+                   : "memory");
   } else if (BES && TC::TWO) {
     // row factors read where they are applied (PST = T): fewer live registers;
     // ping-pong rows when the second stage buffer is free (ONE_STAGE)
