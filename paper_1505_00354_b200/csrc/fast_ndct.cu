@@ -117,7 +117,10 @@ struct Cfg {
 #ifndef FLB_TM_FACC
 #define FLB_TM_FACC 1  // TM forward kernel: the 16 accumulators per thread in TMEM too
 #endif
-constexpr int kTmCols = FLB_TM_FACC ? 256 : 128;  // TMEM columns per CTA
+#ifndef FLB_TM_WPF
+#define FLB_TM_WPF 1  // TM forward kernel: the term's weights parked in TMEM (needs FACC's 256 columns)
+#endif
+constexpr int kTmCols = FLB_TM_FACC || FLB_TM_WPF ? 256 : 128;  // TMEM columns per CTA
 template <int LOG2N, bool BES>
 struct TrCfg {
   using C = Cfg<LOG2N>;
@@ -395,7 +398,7 @@ template <int LOG2N, bool ODD, bool FIRST>
 __device__ __forceinline__ double2* tm_fwd_term(double* stage, double2* zx, double2* zy, int t,
                                                 double2 ta_t, double2 r4_t, const double2* fftw,
                                                 const double* p, double* f, uint32_t tA,
-                                                uint32_t tB, uint32_t tF) {
+                                                uint32_t tB, uint32_t tF, uint32_t tW) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, NSL = C::NSL, RL = C::RL;
   static_assert(E == 8 && T == N / 16, "pack twiddle constants assume T = N/16");
@@ -411,11 +414,27 @@ __device__ __forceinline__ double2* tm_fwd_term(double* stage, double2* zx, doub
     tm_st8(tA + 8 * (Q), cw);                                                               \
     tm_st8(tB + 8 * (Q), nw);                                                               \
   }
+  // FLB_TM_WPF: the term's 16 weights are loaded now (L2) and parked in TMEM
+  // slot W after the pack, so the unpack reads them without a global round trip
+  double wq[FLB_TM_WPF ? 16 : 1];
+  if constexpr (FLB_TM_WPF) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) wq[i] = __ldg(p + i * PST);
+  }
   FLB_TM_QUARTER(0)
   FLB_TM_QUARTER(1)
   FLB_TM_QUARTER(2)
   FLB_TM_QUARTER(3)
 #undef FLB_TM_QUARTER
+  if constexpr (FLB_TM_WPF) {
+#pragma unroll
+    for (int h = 0; h < 4; ++h) {
+      uint32_t ww[8];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) split2(wq[4 * h + j], &ww[2 * j]);
+      tm_st8(tW + 8 * h, ww);
+    }
+  }
   pass_compute<P, E, 8, 1, true>(v, t, fftw);
   pass_store<P, E, 8, 1>(v, zx, t);
   tm_wait_st();
@@ -439,9 +458,13 @@ __device__ __forceinline__ double2* tm_fwd_term(double* stage, double2* zx, doub
     // the accumulators live in TMEM (slot F): load, update, store back
 #pragma unroll
     for (int h = 0; h < 2; ++h) {
-      uint32_t fw[16];
+      uint32_t fw[16], wv[16];
       tm_ld8(tF + 16 * h, fw);
       tm_ld8(tF + 16 * h + 8, fw + 8);
+      if constexpr (FLB_TM_WPF) {
+        tm_ld8(tW + 16 * h, wv);
+        tm_ld8(tW + 16 * h + 8, wv + 8);
+      }
 #pragma unroll
       for (int i8 = 0; i8 < 8; ++i8) {
         const int i = 8 * h + i8, s = i >> 1, q = s / RL, r = s % RL, part = i & 1;
@@ -450,7 +473,8 @@ __device__ __forceinline__ double2* tm_fwd_term(double* stage, double2* zx, doub
         const int k = fwd_row_of<N>(2 * m + part);
         double y = part ? z.y : z.x;
         if (ODD && (k & 1)) y = -y;
-        split2(join2(&fw[2 * i8]) + __ldg(p + i * PST) * y, &fw[2 * i8]);
+        const double w = FLB_TM_WPF ? join2(&wv[2 * i8]) : __ldg(p + i * PST);
+        split2(join2(&fw[2 * i8]) + w * y, &fw[2 * i8]);
       }
       tm_st8(tF + 16 * h, fw);
       tm_st8(tF + 16 * h + 8, fw + 8);
@@ -555,10 +579,11 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     // this warp's lane quarter; per warp 64 (+ 32 with FLB_TM_FACC) columns
-    constexpr uint32_t kWarpCols = FLB_TM_FACC ? 128u : 64u;
+    constexpr uint32_t kWarpCols = FLB_TM_FACC || FLB_TM_WPF ? 128u : 64u;
     const uint32_t tA = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + kWarpCols * (uint32_t)(warp >> 2);
     const uint32_t tB = tA + 32;
     const uint32_t tF = tA + 64;
+    const uint32_t tW = tA + 96;  // (FLB_TM_WPF)
     if constexpr (FLB_TM_FACC) {
       uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
@@ -570,11 +595,11 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
       const double* wr = wtab + (size_t)m * N + t;
       double2* fin;
       if (m == 0)
-        fin = tm_fwd_term<LOG2N, false, true>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF);
+        fin = tm_fwd_term<LOG2N, false, true>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF, tW);
       else if (m & 1)
-        fin = tm_fwd_term<LOG2N, true, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF);
+        fin = tm_fwd_term<LOG2N, true, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF, tW);
       else
-        fin = tm_fwd_term<LOG2N, false, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF);
+        fin = tm_fwd_term<LOG2N, false, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF, tW);
       zy = fin;  // the next term's first pass writes the row the last pass did not read
       zx = other(fin);
     }
