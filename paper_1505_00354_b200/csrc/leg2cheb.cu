@@ -363,11 +363,14 @@ constexpr int TK = RB * THREADS;      // rows per CTA (1024)
 constexpr int KC = 256;               // inner chunk
 }  // namespace mv
 
-template <bool TR>
-__global__ void __launch_bounds__(mv::THREADS)
+// RB rows per thread x NT threads per CTA (TK = RB NT rows per CTA): the
+// default 8 x 128, and 2 x 32 for short vectors (N <= 8192), where the
+// default gives one CTA per parity and a 27 us latency at N = 1024.
+template <bool TR, int RB = mv::RB, int NT = mv::THREADS>
+__global__ void __launch_bounds__(NT)
     leg2cheb_mv_kernel(const double* __restrict__ s, const double* __restrict__ in,
                        double* __restrict__ out, size_t n, size_t ld, int scale_half) {
-  constexpr int RB = mv::RB, TK = mv::TK, KC = mv::KC;
+  constexpr int TK = RB * NT, KC = mv::KC;
   // tw[i] = s_{d}, d = (TR ? row - inner : inner - row) over the chunk window;
   // hw[i] = s_{row + inner + p}. Threads read both at a stride of RB = 8
   // elements, so one pad slot per 8 (PX) keeps a warp's reads conflict free.
@@ -394,14 +397,14 @@ __global__ void __launch_bounds__(mv::THREADS)
     __syncthreads();
     // Toeplitz window: forward d = inner - row in [i0 - r0 - (TK-1), i0 - r0 + KC - 1]
     //                  transpose d = row - inner in [r0 - i0 - (KC-1), r0 - i0 + TK - 1]
-    for (int q = t; q < TK + KC; q += mv::THREADS) {
+    for (int q = t; q < TK + KC; q += NT) {
       const long long d = TR ? (long long)r0 - (long long)i0 - (KC - 1) + q
                              : (long long)i0 - (long long)r0 - (TK - 1) + q;
       tw[PX(q)] = (d >= 0 && d < (long long)n) ? s[d] : 0.0;
       const size_t h = r0 + i0 + p + q;  // row + inner + p, row - r0 + inner - i0 = q
       hw[PX(q)] = h < n ? s[h] : 0.0;
     }
-    for (int q = t; q < KC; q += mv::THREADS) {
+    for (int q = t; q < KC; q += NT) {
       const size_t i = i0 + q;
       double v = 0.0;
       if (i < i_end && i < nr) {
@@ -469,11 +472,20 @@ void leg2cheb_direct(int transpose, size_t n, const double* s, const double* in,
   if (n == 0 || cols == 0) return;
   const size_t rows = (n + 1) / 2;
   if (cols <= 16 && n >= 2) {  // single vectors / few columns: tiled matrix-vector product
-    dim3 grid((unsigned)((rows + mv::TK - 1) / mv::TK), (unsigned)cols, 2);
-    if (transpose)
-      leg2cheb_mv_kernel<true><<<grid, mv::THREADS, 0, st>>>(s, in, out, n, ld, scale_half);
-    else
-      leg2cheb_mv_kernel<false><<<grid, mv::THREADS, 0, st>>>(s, in, out, n, ld, 0);
+    if (n <= 8192) {
+      constexpr int RB = 2, NT = 32;
+      dim3 grid((unsigned)((rows + RB * NT - 1) / (RB * NT)), (unsigned)cols, 2);
+      if (transpose)
+        leg2cheb_mv_kernel<true, RB, NT><<<grid, NT, 0, st>>>(s, in, out, n, ld, scale_half);
+      else
+        leg2cheb_mv_kernel<false, RB, NT><<<grid, NT, 0, st>>>(s, in, out, n, ld, 0);
+    } else {
+      dim3 grid((unsigned)((rows + mv::TK - 1) / mv::TK), (unsigned)cols, 2);
+      if (transpose)
+        leg2cheb_mv_kernel<true><<<grid, mv::THREADS, 0, st>>>(s, in, out, n, ld, scale_half);
+      else
+        leg2cheb_mv_kernel<false><<<grid, mv::THREADS, 0, st>>>(s, in, out, n, ld, 0);
+    }
     note_launch(transpose ? "leg2cheb_mv_kernel<T>" : "leg2cheb_mv_kernel<F>");
     return;
   }
