@@ -490,6 +490,28 @@ def test_device_resident_batched_matches_host():
         assert np.array_equal(fl.dlt(c[j], cfg), f_host[j])
 
 
+def test_dlt_idlt_4096_batch_invariance():
+    """N = 4096 (the TMEM-resident Chebyshev NDCT kernels, split GEMM): a
+    column's DLT / IDLT does not depend on the batch it is computed in
+    (17 vs 300 columns, bit-identical) and matches the oracle."""
+    import torch
+    n = 4096
+    cfg = fl.TransformConfig(n)
+    c = fl.random_uniform_pm1(n, 4100, batch=300)
+    dev = torch.from_numpy(c).cuda()
+    f_all = fl.dlt(dev, cfg).cpu().numpy()
+    f_17 = fl.dlt(dev[:17].contiguous(), cfg).cpu().numpy()
+    assert np.array_equal(f_17, f_all[:17])
+    b_all = fl.idlt(torch.from_numpy(f_all).cuda(), cfg).values.cpu().numpy()
+    b_17 = fl.idlt(torch.from_numpy(f_all[:17]).cuda(), cfg).values.cpu().numpy()
+    assert np.array_equal(b_17, b_all[:17])
+    g = cfg.grid()
+    for j in (0, 16, 299):
+        ref = O.dlt_grid(c[j], CHEBSTAR, fl.default_tolerance, g.theta, g.x, g.weights)
+        assert rel_err(f_all[j], ref, np.abs(c[j]).sum()) <= tol_n(n), j
+        assert np.max(np.abs(b_all[j] - c[j])) <= 1e-10 * np.max(np.abs(c[j])), j
+
+
 @pytest.mark.parametrize("n", [64, 100, 1024, 4096])
 def test_leg2cheb_tensor_core_path(n):
     """> 16 columns: the DMMA (fp64 mma.sync) GEMM kernel; odd N / unaligned
