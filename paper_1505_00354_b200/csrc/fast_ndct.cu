@@ -114,6 +114,10 @@ struct Cfg {
 #ifndef FLB_NDCT_TR_TMO
 #define FLB_NDCT_TR_TMO 1
 #endif
+#ifndef FLB_NDCT_TR_T3
+#define FLB_NDCT_TR_T3 1
+#endif
+constexpr int kTrCols = FLB_NDCT_TR_T3 ? 128 : 64;  // TMEM columns per CTA (NDCT^T, TMO)
 #ifndef FLB_TM_FACC
 #define FLB_TM_FACC 1  // TM forward kernel: the 16 accumulators per thread in TMEM too
 #endif
@@ -125,15 +129,19 @@ template <int LOG2N, bool BES>
 struct TrCfg {
   using C = Cfg<LOG2N>;
   static constexpr bool TWO = BES && LOG2N <= 12;
-  static constexpr int MINB = TWO ? 2 : 1;
   // BES: the stage is the (weighted-on-the-fly) input itself, one buffer;
   // the Taylor stage's second buffer becomes a second FFT row (ping-pong)
   static constexpr bool ONE_STAGE = BES && TWO && FLB_NDCT_TR_PP && C::COLS == 1;
   static constexpr bool PP = ONE_STAGE || (!TWO && C::PP);
   // TMO: the output accumulators in TMEM (with ONE_STAGE)
   static constexpr bool TMO = ONE_STAGE && FLB_NDCT_TR_TMO;
+  // T3: the input stage (read only by the pack) in TMEM too: shared memory
+  // holds just the two FFT rows, three CTAs per SM
+  static constexpr bool T3 = TMO && FLB_NDCT_TR_T3;
   static constexpr bool TABLES = !TWO && C::SMEM_TABLES;
-  static constexpr size_t COL_BYTES = (ONE_STAGE ? 1 : 2) * C::N * sizeof(double) + (PP ? 2 : 1) * C::ZB;
+  static constexpr int MINB = T3 ? 3 : TWO ? 2 : 1;
+  static constexpr size_t COL_BYTES =
+      (T3 ? 0 : ONE_STAGE ? 1 : 2) * C::N * sizeof(double) + (PP ? 2 : 1) * C::ZB;
   static constexpr size_t SMEM = C::COLS * COL_BYTES + (TABLES ? C::N * 8 + C::TW * 16 : 0);
 };
 
@@ -351,6 +359,14 @@ __device__ __forceinline__ void tm_ld8(uint32_t taddr, uint32_t* v) {
       : "r"(taddr));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+__device__ __forceinline__ void tm_ld8_nw(uint32_t taddr, uint32_t* v) {  // caller waits
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7])
+      : "r"(taddr));
+}
+__device__ __forceinline__ void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void split2(double d, uint32_t* w) {
   w[0] = (uint32_t)__double2loint(d);
@@ -723,13 +739,17 @@ __device__ __forceinline__ double tr_unpack(double2 za, double2 zc, double2 tn, 
 // ordering the first store after the previous term's unpack reads.
 // TMO: the 16 output accumulators live in the thread's TMEM lane at tO
 // (loaded, updated and stored back per row group) instead of o[].
-template <int LOG2N, bool ODD, int PM, bool PPX = Cfg<LOG2N>::PP, int PST = 1, bool TMO = false>
+// HST: the stage is the thread's own 16 pack entries in its TMEM lane at tH
+// (r-major pairs), not hs.
+template <int LOG2N, bool ODD, int PM, bool PPX = Cfg<LOG2N>::PP, int PST = 1, bool TMO = false,
+          bool HST = false>
 __device__ __forceinline__ double2* tr_term(const double* hs, double* next, const double* nd,
                                             const double* __restrict__ delta, double inv_next,
                                             const double* __restrict__ wrow, double2* zx,
                                             double2* zy, int t, int bar, double2 ta_t,
                                             double2 r4_t, const double2* fftw, const double* rp,
-                                            double* o, double sign, uint32_t tO = 0) {
+                                            double* o, double sign, uint32_t tO = 0,
+                                            uint32_t tH = 0) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, P = C::P, T = C::T, E = C::E, OWN = C::OWN;
   static_assert(E == 8 && T == N / 16, "row grouping assumes T = N/16");
@@ -738,11 +758,22 @@ __device__ __forceinline__ double2* tr_term(const double* hs, double* next, cons
   // m < N/4: (h_{4m}, h_{4m+2}) = hs[2m .. 2m+1]; else (h_{2(N-1-2m)+1}, h_{2(N-2-2m)+1})
   // = the swapped pair at hs[P + N - 2 - 2m].
   double2 v[E];
+  uint32_t hw[HST ? 16 : 1];
 #pragma unroll
   for (int r = 0; r < E; ++r) {
     const int m = t + r * T;
     const int slot = r < 4 ? 2 * m : P + N - 2 - 2 * m;
-    double2 w = *reinterpret_cast<const double2*>(hs + slot);
+    double2 w;
+    if constexpr (HST) {
+      if (r == 0 || r == 4) {
+        tm_ld8_nw(tH + 4 * r, hw);
+        tm_ld8_nw(tH + 4 * r + 8, hw + 8);
+        tm_wait_ld();
+      }
+      w = make_double2(join2(&hw[4 * (r & 3)]), join2(&hw[4 * (r & 3) + 2]));
+    } else {
+      w = *reinterpret_cast<const double2*>(hs + slot);
+    }
     if (PM == 2) {
       const double2 q = __ldg(reinterpret_cast<const double2*>(wrow + slot));
       w = make_double2(w.x * q.x, w.y * q.y);
@@ -850,9 +881,9 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
   const size_t col = (size_t)blockIdx.x * C::COLS + g;
   if (col >= batch) return;
   // h_k = (N delta_k)^l / l! g_k at hs[tr_slot(k)], double-buffered by term parity
-  double* hs = smem + g * (TC::COL_BYTES / 8);
+  double* hs = smem + g * (TC::COL_BYTES / 8);  // (not used with T3)
   double* hs_odd = hs + N;  // (Taylor only)
-  double2* zbA = reinterpret_cast<double2*>(hs + (TC::ONE_STAGE ? 1 : 2) * N);
+  double2* zbA = reinterpret_cast<double2*>(hs + (TC::T3 ? 0 : TC::ONE_STAGE ? 1 : 2) * N);
   double2* zbB = TC::PP ? zbA + C::ZB / sizeof(double2) : zbA;
   double2* zx = zbA;  // the first pass's target this term
   auto other = [&](double2* b) { return b == zbA ? zbB : zbA; };
@@ -861,15 +892,20 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
   bool bad = false;
 #pragma unroll
   for (int i = 0; i < OWN; ++i) {
-    const int k = t + T * i;
-    double v = src[k];
-    if (mult) v = mult[k] * v;  // transforms.hpp:59 weighted = w_k f_k
-    bad |= !isfinite(v);
-    hs[tr_slot<N>(k)] = v;
     o[i] = 0.0;
     rp[i] = 1.0;
   }
-  if (bad && nonfinite) atomicOr(nonfinite, 1);
+  if constexpr (!TC::T3) {
+#pragma unroll
+    for (int i = 0; i < OWN; ++i) {
+      const int k = t + T * i;
+      double v = src[k];
+      if (mult) v = mult[k] * v;  // transforms.hpp:59 weighted = w_k f_k
+      bad |= !isfinite(v);
+      hs[tr_slot<N>(k)] = v;
+    }
+    if (bad && nonfinite) atomicOr(nonfinite, 1);
+  }
   const double2 ta_t = __ldg(&tw4n[t]);      // e^{i pi t/(2N)}
   const double2 r4_t = __ldg(&tw4n[4 * t]);  // e^{2 pi i t/N}
   group_sync<C::GT>(bar);
@@ -885,19 +921,45 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
     __shared__ uint32_t tmem_base;
     const int warp = threadIdx.x >> 5;
     if (warp == 0) {
-      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 64;" ::"r"(
-                       static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base)))
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                       static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base))),
+                   "n"(kTrCols)
                    : "memory");
       asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
     }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    const uint32_t tO = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 32u * (uint32_t)(warp >> 2);
+    const uint32_t tO = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) +
+                        (uint32_t)(kTrCols / 2) * (uint32_t)(warp >> 2);
+    const uint32_t tH = tO + 32;  // (T3) the thread's 16 pack entries
     {
       uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
 #pragma unroll
       for (int q = 0; q < 4; ++q) tm_st8(tO + 8 * q, z);
+      if constexpr (TC::T3) {
+        // the entries (k0, k1) of pack slot pair r: (4m, 4m + 2) for r < 4, the
+        // odd pair (2N - 3 - 4m, 2N - 1 - 4m) for r >= 4 (m = t + r T)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          uint32_t hw8[8];
+#pragma unroll
+          for (int rr = 0; rr < 2; ++rr) {
+            const int r = 2 * q + rr, m = t + r * T;
+            const int k0 = r < 4 ? 4 * m : 2 * N - 3 - 4 * m, k1 = k0 + 2;
+            double v0 = src[k0], v1 = src[k1];
+            if (mult) {
+              v0 *= mult[k0];
+              v1 *= mult[k1];
+            }
+            bad |= !isfinite(v0) || !isfinite(v1);
+            split2(v0, &hw8[4 * rr]);
+            split2(v1, &hw8[4 * rr + 2]);
+          }
+          tm_st8(tH + 8 * q, hw8);
+        }
+        if (bad && nonfinite) atomicOr(nonfinite, 1);
+      }
       tm_wait_st();
     }
     for (int m = 0; m < num_terms; ++m) {
@@ -905,11 +967,13 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
       const double* wrow = wtab + (size_t)m * N;
       double2* fin;
       if (m & 1)
-        fin = tr_term<LOG2N, true, 2, true, T, true>(hs, nullptr, nd, delta, 0.0, wrow, zx, other(zx),
-                                                     t, bar, ta_t, r4_t, fftw, tr, o, 1.0, tO);
+        fin = tr_term<LOG2N, true, 2, true, T, true, TC::T3>(hs, nullptr, nd, delta, 0.0, wrow, zx,
+                                                             other(zx), t, bar, ta_t, r4_t, fftw, tr,
+                                                             o, 1.0, tO, tH);
       else
-        fin = tr_term<LOG2N, false, 2, true, T, true>(hs, nullptr, nd, delta, 0.0, wrow, zx, other(zx),
-                                                      t, bar, ta_t, r4_t, fftw, tr, o, 1.0, tO);
+        fin = tr_term<LOG2N, false, 2, true, T, true, TC::T3>(hs, nullptr, nd, delta, 0.0, wrow, zx,
+                                                              other(zx), t, bar, ta_t, r4_t, fftw, tr,
+                                                              o, 1.0, tO, tH);
       zx = other(fin);
     }
 #pragma unroll
@@ -922,7 +986,8 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     __syncthreads();
     if (warp == 0)
-      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 64;" ::"r"(tmem_base)
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                   "n"(kTrCols)
                    : "memory");
   } else if (BES && TC::TWO) {
     // row factors read where they are applied (PST = T): fewer live registers;
