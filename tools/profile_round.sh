@@ -7,6 +7,8 @@
 #      bounded)                                           -> gpurun_out/hot_full.ncu-rep
 #   4. ncu --set full of the plain DCT-III pass (streaming kernel, 4096 x 65536,
 #      the HBM-bound pass of north_star's 60% target)      -> gpurun_out/dct_full.ncu-rep
+#   5. ncu --set full of the IDLT's NDCT^T kernel (16384 columns)
+#                                                          -> gpurun_out/tr_full.ncu-rep
 set -u
 mkdir -p gpurun_out
 python bench.py --steps 10 --warmup 3 > gpurun_out/bench.json 2> gpurun_out/bench.err
@@ -24,3 +26,7 @@ python tools/dct_probe.py > gpurun_out/dct_probe.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:fast_dct_stream -s 2 -c 1 \
     -o gpurun_out/dct_full python tools/dct_probe.py > gpurun_out/dct_ncu.log 2>&1
 echo "ncu dct rc=$?"
+python tools/idlt_probe.py 16384 > gpurun_out/idlt_probe.log 2>&1 &&
+ncu --set full --clock-control none --import-source on -k regex:fast_ndct_tr -s 1 -c 1 \
+    -o gpurun_out/tr_full python tools/idlt_probe.py 16384 > gpurun_out/tr_ncu.log 2>&1
+echo "ncu tr rc=$?"
