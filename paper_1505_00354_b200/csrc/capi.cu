@@ -477,21 +477,25 @@ const L2COzaki* plan_ozaki(fl_plan* p, int transpose, size_t batch, cudaStream_t
 
 // The plan's conversion product (transforms.hpp:47 / :62): chat = M in, or
 // (m + 1/2) M^T in for the inverse; device columns of stride n.
+// in: columns of stride n; out: stride ld_out. The conversion kernels take a
+// single column stride for both, so a strided output goes through a
+// stride-n scratch.
 void plan_convert(fl_plan* p, int transpose, const double* in, double* out, size_t batch,
                   size_t ld_out, cudaStream_t s) {
   const size_t n = p->n;
-  if (p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)
-    l2c_fast_apply(*p->l2c, transpose, in, out, batch, ld_out, transpose, s);
-  else if (const L2COzaki* oz = plan_ozaki(p, transpose, batch, s))
-    l2c_ozaki_apply(*oz, in, out, batch, ld_out, s);
-  else if (ld_out == n)
-    leg2cheb_direct(transpose, n, p->s, in, out, batch, n, transpose, s);
-  else {
+  if (ld_out != n) {
     DevScratch<double> t(n * batch, s);
-    leg2cheb_direct(transpose, n, p->s, in, t.p, batch, n, transpose, s);
+    plan_convert(p, transpose, in, t.p, batch, n, s);
     FLB_CUDA(cudaMemcpy2DAsync(out, ld_out * 8, t.p, n * 8, n * 8, batch,
                                cudaMemcpyDeviceToDevice, s));
+    return;
   }
+  if (p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)
+    l2c_fast_apply(*p->l2c, transpose, in, out, batch, n, transpose, s);
+  else if (const L2COzaki* oz = plan_ozaki(p, transpose, batch, s))
+    l2c_ozaki_apply(*oz, in, out, batch, n, s);
+  else
+    leg2cheb_direct(transpose, n, p->s, in, out, batch, n, transpose, s);
 }
 
 }  // namespace
