@@ -75,6 +75,101 @@ __global__ void __launch_bounds__(128, 1) peak_kernel(int iters, unsigned long l
   }
 }
 
+// TS form (A from TMEM, as oz_gemm2_kernel): A tiles copied once into 8
+// 8-column slots after 7 x N accumulator columns, then back-to-back MMAs.
+template <int N, bool CP>
+__global__ void __launch_bounds__(128, 1) peak_ts_kernel(int iters, unsigned long long* cycles) {
+  extern __shared__ uint8_t raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar;
+  __shared__ uint32_t holder;
+  const int bytes = 8 * (128 * 64) + 8 * (N * 64);
+  for (int i = threadIdx.x; i < bytes / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(smem)[i] = make_uint4(0, 0, 0, 0);
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  const int warp = threadIdx.x >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(smem_u32(&holder)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = holder;
+  constexpr uint32_t idesc = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (8u << 24);
+  constexpr int NACC = 7;
+  unsigned long long t0 = clock64();
+  if (warp == 0) {
+    const uint64_t ad0 = desc64(smem_u32(smem)), bd0 = desc64(smem_u32(smem + 8 * 128 * 64));
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+      asm volatile(
+          "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(tmem + (uint32_t)(NACC * N + 8 * i)),
+          "l"(ad0 + (uint64_t)((i * 128 * 64) >> 4)));
+    for (int it = 0; it < iters; ++it) {
+#pragma unroll
+      for (int m = 0; m < 72; ++m) {
+        const int i = m % 8, j = (m / 8) % 8, ks = m & 1;
+        const uint64_t bd = bd0 + (uint64_t)((j * N * 64 + ks * 32) >> 4);
+        const uint32_t d = tmem + (uint32_t)((m % NACC) * N);
+        const uint32_t a = tmem + (uint32_t)(NACC * N + 8 * i);
+        if (CP && (m & 3) == 0)  // one A-tile copy per 4 MMAs (oz_gemm2: 7 per 28)
+          asm volatile(
+              "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+              "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(tmem + (uint32_t)(NACC * N + 8 * ((i + 4) & 7))),
+              "l"(ad0 + (uint64_t)((((i + 4) & 7) * 128 * 64) >> 4)));
+        asm volatile(
+            "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+            "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d),
+            "r"(a), "l"(bd), "r"(idesc), "r"(1u));
+      }
+      asm volatile(
+          "{\n\t.reg .pred e;\n\telect.sync _|e, 0xffffffff;\n\t"
+          "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(
+              smem_u32(&bar)));
+      asm volatile(
+          "{\n\t.reg .pred P1;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t@P1 bra D_%=;\n\tbra W_%=;\nD_%=:\n\t}" ::"r"(
+              smem_u32(&bar)), "r"((uint32_t)(it & 1)));
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) cycles[blockIdx.x] = clock64() - t0;
+  if (warp == 0) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+template <int N, bool CP>
+void run_ts(int sms) {
+  const int smem = 8 * 128 * 64 + 8 * N * 64 + 1024;
+  cudaFuncSetAttribute(peak_ts_kernel<N, CP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  unsigned long long* cyc;
+  cudaMalloc(&cyc, sms * 8);
+  const int iters = 2000;
+  peak_ts_kernel<N, CP><<<sms, 128, smem>>>(10, cyc);
+  cudaEvent_t a, b;
+  cudaEventCreate(&a);
+  cudaEventCreate(&b);
+  cudaEventRecord(a);
+  peak_ts_kernel<N, CP><<<sms, 128, smem>>>(iters, cyc);
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms = 0;
+  cudaEventElapsedTime(&ms, a, b);
+  const cudaError_t e = cudaGetLastError();
+  const double macs = (double)sms * iters * 72 * 128.0 * N * 32.0;
+  std::printf("%s N=%3d: %s  %.3f ms  %.1f TOP/s int8 dense (%.0f MAC/clk/SM at 1.92 GHz)\n", CP ? "TS+cp" : "TS", N,
+              cudaGetErrorString(e), ms, 2 * macs / (ms * 1e-3) / 1e12,
+              macs / sms / (ms * 1e-3) / 1.92e9);
+  cudaFree(cyc);
+}
+
 template <int N>
 void run(int sms) {
   const int smem = 8 * 128 * 64 + 8 * N * 64 + 1024;
@@ -104,6 +199,8 @@ int main() {
   int sms = 0;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   run<64>(sms);
+  run_ts<64, false>(sms);
+  run_ts<64, true>(sms);
   run<128>(sms);
   run<256>(sms);
   return 0;
