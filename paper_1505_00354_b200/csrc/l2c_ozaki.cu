@@ -59,6 +59,9 @@ namespace oz {
 #ifndef FLB_OZ_DIGIT_BITS
 #define FLB_OZ_DIGIT_BITS 8
 #endif
+#ifndef FLB_OZ_TS1
+#define FLB_OZ_TS1 1  // A operand from TMEM in the 1-SM kernel too
+#endif
 constexpr int DB = FLB_OZ_DIGIT_BITS;
 constexpr int S = DB == 8 ? 7 : 8;  // digits per operand
 constexpr int BM = 128;         // output rows per tile (TMEM lanes)
@@ -140,6 +143,24 @@ __device__ __forceinline__ void tc_mma_i8(uint32_t d_tmem, uint64_t adesc, uint6
       "setp.ne.b32 p, %4, 0;\n\t"
       "@e tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_mma_i8_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                             uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::i8 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void tc_cp_128x256(uint32_t taddr, uint64_t sdesc) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(taddr),
+      "l"(sdesc)
       : "memory");
 }
 __device__ __forceinline__ void tc_commit_elect(uint32_t bar) {
@@ -412,7 +433,8 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
     }
   } else if (warp == 1) {
     {  // MMA issuer: the whole warp, one elected lane issues
-      uint32_t it = 0, t = 0;
+      uint32_t it = 0, t = 0, aslot = 0;
+      (void)aslot;
       for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
         size_t cb, rb;
         int p, kb_lo, nk;
@@ -426,6 +448,23 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
           const uint32_t sa = smem_u32(smem + st * STAGE_BYTES);
           const uint64_t ad0 = smem_desc(sa), bd0 = smem_desc(sa + S * A_TILE);
           const uint32_t first = kb == 0 ? 0u : 1u;
+          if constexpr (FLB_OZ_TS1 && S * BN + 64 <= 512) {
+            // A digit tiles through TMEM (TS form), as in oz_gemm2_kernel
+#pragma unroll
+            for (int ks = 0; ks < BK / 32; ++ks) {
+#pragma unroll
+              for (int i = 0; i < S; ++i, ++aslot) {
+                const uint32_t ta = tmem + (uint32_t)(S * BN + (aslot & 7u) * 8u);
+                tc_cp_128x256(ta, ad0 + (uint64_t)((i * A_TILE + ks * 32) >> 4));
+#pragma unroll
+                for (int j = 0; i + j < S; ++j) {
+                  const uint64_t bd = bd0 + (uint64_t)((j * B_TILE + ks * 32) >> 4);
+                  tc_mma_i8_ts(tmem + (uint32_t)((i + j) * BN), ta, bd, IDESC,
+                               (ks > 0 || i > 0) ? 1u : first);
+                }
+              }
+            }
+          } else {
           // fully unrolled: each MMA is a descriptor add and the UTCIMMA
 #pragma unroll
           for (int i = 0; i < S; ++i) {
@@ -439,6 +478,7 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
                           (ks > 0 || i > 0) ? 1u : first);
               }
             }
+          }
           }
           tc_commit_elect(smem_u32(&empty_b[st]));  // frees the stage when these MMAs retire
         }
