@@ -239,7 +239,7 @@ __global__ void __launch_bounds__(128, 1) order_kernel(int iters, unsigned long 
     const uint64_t ad0 = desc64(smem_u32(smem)), bd0 = desc64(smem_u32(smem + 8 * 128 * 64));
     uint32_t aslot = 0;
     for (int it = 0; it < iters; ++it) {
-      if constexpr (MODE == 2) {
+      if constexpr (MODE >= 2) {
         // A digit copies one digit ahead of their MMAs: (ks, i) -> slot aslot
         auto cp = [&](int ks, int i, uint32_t slot) {
           asm volatile(
@@ -247,16 +247,19 @@ __global__ void __launch_bounds__(128, 1) order_kernel(int iters, unsigned long 
               "@e tcgen05.cp.cta_group::1.128x256b [%0], %1;\n\t}" ::"r"(tmem + (uint32_t)(7 * N + (slot & 7u) * 8u)),
               "l"(ad0 + (uint64_t)((i * 128 * 64 + ks * 32) >> 4)));
         };
-        if (it == 0) cp(0, 0, aslot);
+        constexpr int AH = MODE == 3 ? 2 : 1;  // copy distance in digits (MODE 4: 1)
+        if (it == 0)
+          for (int a = 0; a < AH; ++a) cp(0, a, aslot + a);
 #pragma unroll
         for (int ks = 0; ks < 2; ++ks) {
 #pragma unroll
           for (int i = 0; i < 7; ++i, ++aslot) {
-            if (i < 6) cp(ks, i + 1, aslot + 1);
-            else cp(ks ^ 1, 0, aslot + 1);
+            const int q = ks * 7 + i + AH;  // digit index AH ahead, wrapping to the next batch
+            cp((q / 7) & 1, q % 7, aslot + AH);
             const uint32_t ta = tmem + (uint32_t)(7 * N + (aslot & 7u) * 8u);
 #pragma unroll
-            for (int j = 0; i + j < 7; ++j) {
+            for (int jj = 0; i + jj < 7; ++jj) {
+              const int j = MODE == 4 ? 6 - i - jj : jj;  // MODE 4: accumulators high to low
               const uint64_t bd = bd0 + (uint64_t)((j * N * 64 + ks * 32) >> 4);
               asm volatile(
                   "{\n\t.reg .pred p, e;\n\telect.sync _|e, 0xffffffff;\n\tsetp.ne.b32 p, %4, 0;\n\t"
@@ -345,7 +348,7 @@ void run_order(int sms) {
   const cudaError_t e = cudaGetLastError();
   const double macs = (double)sms * iters * 56 * 128.0 * N * 32.0;
   std::printf("%s N= 64: %s  %.3f ms  %.1f TOP/s int8 dense (%.0f MAC/clk/SM at 1.92 GHz)\n",
-              MODE == 2 ? "split order, copy ahead" : MODE == 1 ? "split order, spread" : "split order",
+              MODE == 4 ? "split order, copy ahead, d high->low" : MODE == 3 ? "split order, copy 2 ahead" : MODE == 2 ? "split order, copy ahead" : MODE == 1 ? "split order, spread" : "split order",
               cudaGetErrorString(e), ms,
               2 * macs / (ms * 1e-3) / 1e12, macs / sms / (ms * 1e-3) / 1.92e9);
   cudaFree(cyc);
@@ -385,6 +388,8 @@ int main() {
   run_order<0>(sms);
   run_order<1>(sms);
   run_order<2>(sms);
+  run_order<3>(sms);
+  run_order<4>(sms);
   run<128>(sms);
   run<256>(sms);
   return 0;
