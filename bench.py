@@ -111,27 +111,56 @@ def parse():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock / throttle-reason sampling during the timed region (B200_PROFILING.md
+    clocks line). NVML queries take microseconds, so the whole timed region is sampled
+    every 5 ms; nvidia-smi (~100 ms per query) is the fallback when NVML is absent."""
 
     Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
          "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
          "clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
     def __init__(self, index: int):
         self.index, self.rows, self.stop_ev = index, [], threading.Event()
+        self.source, self.nvml = "nvidia-smi", None
+        try:
+            import pynvml
+            import torch
+            pynvml.nvmlInit()
+            p = torch.cuda.get_device_properties(index)
+            bus = f"{p.pci_domain_id:08x}:{p.pci_bus_id:02x}:{p.pci_device_id:02x}.0"
+            try:
+                h = pynvml.nvmlDeviceGetHandleByPciBusId(bus.encode())
+            except Exception:
+                h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.masks = [pynvml.nvmlClocksEventReasonHwSlowdown, pynvml.nvmlClocksEventReasonHwThermalSlowdown,
+                          pynvml.nvmlClocksEventReasonSwThermalSlowdown, pynvml.nvmlClocksEventReasonSwPowerCap]
+            self.max_mhz = float(pynvml.nvmlDeviceGetMaxClockInfo(h, pynvml.NVML_CLOCK_SM))
+            self.nvml, self.h, self.source = pynvml, h, "nvml"
+        except Exception:
+            self.nvml = None
         self.th = threading.Thread(target=self._run, daemon=True)
+
+    def _sample(self):
+        if self.nvml is not None:
+            p = self.nvml
+            sm = float(p.nvmlDeviceGetClockInfo(self.h, p.NVML_CLOCK_SM))
+            r = p.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+            return [str(sm), str(self.max_mhz), ""] + ["Active" if r & m else "Not Active" for m in self.masks]
+        out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                              "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                             timeout=5).stdout.strip()
+        return [s.strip() for s in out.split(",")] if out else None
 
     def _run(self):
         while not self.stop_ev.is_set():
             try:
-                out = subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
-                                      "--format=csv,noheader,nounits"], capture_output=True, text=True,
-                                     timeout=5).stdout.strip()
-                if out:
-                    self.rows.append([s.strip() for s in out.split(",")])
+                row = self._sample()
+                if row:
+                    self.rows.append(row)
             except Exception:
                 pass
-            self.stop_ev.wait(0.2)
+            self.stop_ev.wait(0.005 if self.nvml is not None else 0.2)
 
     def __enter__(self):
         self.th.start()
@@ -144,10 +173,11 @@ class Clocks:
     def summary(self) -> dict:
         sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
         mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in self.rows for i in range(4) if len(r) > 3 + i and r[3 + i] == "Active"})
+        reasons = sorted({self.NAMES[i] for r in self.rows for i in range(4)
+                          if len(r) > 3 + i and r[3 + i] == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(self.rows)}
+                "sm_min_mhz": min(sm) if sm else None, "reasons": reasons, "samples": len(self.rows),
+                "source": self.source}
 
 
 def make_inputs(cfg: str, n: int, col0: int, cols: int) -> np.ndarray:
@@ -209,8 +239,12 @@ def run_reference(args, rank: int, world: int) -> None:
         if s >= args.warmup:
             vals.append(b["value"])
     v = float(np.median(vals))
+    # a step of the full workload (all columns), at the sampled rate; each timed step
+    # itself is a bounded sample (cpu_baseline.sample says how many columns)
+    ms = n * total / v * 1e3
     line = {"metric": "fp64 DLT coeffs/sec", "value": v, "unit": "coeffs/s", "n_gpus": world,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": None, "higher_is_better": True,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "ms_per_step_basis": "full workload at the sampled rate", "higher_is_better": True,
             "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": desc, "N": n, "columns": total, "parallelism": f"{threads} host threads"},
