@@ -34,7 +34,8 @@ def _stale() -> bool:
 def build(force: bool = False, verbose: bool = False) -> str:
     if not force and not _stale():
         return LIB
-    objdir = os.path.join(HERE, "build")
+    # experiment builds keep their objects beside their library
+    objdir = LIB + ".objs" if os.environ.get("FLB_LIB_OUT") else os.path.join(HERE, "build")
     os.makedirs(objdir, exist_ok=True)
     objs = []
     procs = []

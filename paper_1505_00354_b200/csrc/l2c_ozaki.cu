@@ -905,7 +905,10 @@ void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t co
   double* bcol = nullptr;
   FLB_CUDA(cudaMallocAsync(&b, (size_t)oz::S * 2 * cols * r, st));
   FLB_CUDA(cudaMallocAsync(&bcol, 2 * cols * sizeof(double), st));
-  if (n <= 8192)
+#ifndef FLB_OZ_SPLIT8_MAX
+#define FLB_OZ_SPLIT8_MAX 8192  // largest N split with 8 entries per thread
+#endif
+  if (n <= FLB_OZ_SPLIT8_MAX)
     oz_split_b_kernel<8><<<(unsigned)cols, (unsigned)(n / 8), 0, st>>>(in, n, ld, cols, b, bcol);
   else
     oz_split_b_kernel<16><<<(unsigned)cols, (unsigned)(n / 16), 0, st>>>(in, n, ld, cols, b, bcol);
