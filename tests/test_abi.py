@@ -78,3 +78,17 @@ def test_host_generators_match_random_hpp():
         assert np.array_equal(b[j], uniform_pm1(64, 4000 + j))
     b = fl.random_decaying(33, 0.0, 1000, batch=4, threads=2)
     assert np.array_equal(b[2], ORACLE.random_decaying(33, 0.0, 1002))
+
+
+def test_entry_imports_without_library():
+    """A fresh checkout has no library yet: __graft_entry__ (whose build() makes
+    it) must import, while the package itself must refuse loudly."""
+    import subprocess
+    import sys
+    env = dict(os.environ, FLB_LIB_PATH=os.path.join(ROOT, "no_such_lib.so"))
+    ok = subprocess.run([sys.executable, "-c", "import __graft_entry__ as g; assert callable(g.build)"],
+                        cwd=ROOT, env=env, capture_output=True, text=True)
+    assert ok.returncode == 0, ok.stderr
+    bad = subprocess.run([sys.executable, "-c", "import paper_1505_00354_b200"],
+                         cwd=ROOT, env=env, capture_output=True, text=True)
+    assert bad.returncode != 0 and "no CPU fallback" in bad.stderr
