@@ -338,6 +338,11 @@ def main() -> None:
     ms_dct = timed(lambda: _lib.check(_lib.LIB.fl_trig(0, fl.GridKind.cheb1, n, vp(x.data_ptr()),
                                                        vp(y.data_ptr()), cols, n, sp)))
     # the inverse on the same shard (DLT, IDLT and NDCT reported separately)
+    # the IDLT's two steps (transpose = 1): NDCT^T, then the transposed conversion
+    ms_ndct_t = timed(lambda: _lib.check(_lib.LIB.fl_plan_ndct(cfg.handle, 1, vp(x.data_ptr()),
+                                                               vp(chat.data_ptr()), cols, n, sp)))
+    ms_l2c_t = timed(lambda: _lib.check(_lib.LIB.fl_plan_leg2cheb(cfg.handle, 1, vp(chat.data_ptr()),
+                                                                  vp(y.data_ptr()), cols, n, sp)))
     ms_idlt = timed(lambda: _lib.check(_lib.LIB.fl_idlt(cfg.handle, vp(x.data_ptr()), vp(y.data_ptr()),
                                                         cols, n, sp)))
     coef = n * cols
@@ -435,7 +440,8 @@ def main() -> None:
                              "dct_pass_kernel": "fast_dct_stream_fwd_kernel (fl_trig DCT-III, same shard)",
                              "dct_pass_traffic": dct_traffic},
             "kernels_ms": {"leg2cheb_split_int8": ms_l2c, "ndct": ms_ndct, "dct_iii_pass": ms_dct,
-                           "dlt_step": ms, "idlt_step": ms_idlt},
+                           "dlt_step": ms, "idlt_step": ms_idlt,
+                           "ndct_transpose": ms_ndct_t, "leg2cheb_transpose_split_int8": ms_l2c_t},
             "e2e": {"value": n * total / (e2e_ms / 1e3), "unit": "coeffs/s",
                     "h2d_bytes_per_step": int(8 * n * cols), "d2h_bytes_per_step": int(8 * n * cols)},
             "gpu_launches": launches,
