@@ -90,8 +90,9 @@ inline std::vector<double> ndct_apply_transpose(const TaylorPlan& plan,
 inline double ndct_error_bound(const TaylorPlan& plan, const std::vector<double>& coeffs) {
   double bound = 0.0;
   b200::check(fl_ndct_error_bound(plan.size, static_cast<int>(plan.kind), plan.num_terms,
-                                  plan.reference.delta_theta.data(), coeffs.data(), &bound,
-                                  nullptr));
+                                  plan.reference.delta_theta.data(),
+                                  plan.reference.delta_theta.size(), coeffs.data(),
+                                  coeffs.size(), &bound, nullptr));
   return bound;
 }
 

@@ -87,9 +87,12 @@ fl_status fl_ndct(int transpose, int kind, size_t n, int num_terms, const double
                   const double* in, double* out, size_t batch, size_t ld, void* stream);
 
 /* ndct.hpp:147-155 ndct_error_bound(plan, coeffs): min((N max|delta|)^L / L!,
- * C(L)) * ||c||_1, with the two O(N) reductions done on the device. */
+ * C(L)) * ||c||_1, with the two O(N) reductions done on the device, each over
+ * its own vector (delta_len = plan.reference.delta_theta.size(), coeffs_len =
+ * coeffs.size(); N = n = plan.size). */
 fl_status fl_ndct_error_bound(size_t n, int kind, int num_terms, const double* delta_theta,
-                              const double* coeffs, double* bound, void* stream);
+                              size_t delta_len, const double* coeffs, size_t coeffs_len,
+                              double* bound, void* stream);
 
 /* conversion.hpp:100-113 leg2cheb_apply (transpose = 0) and :121-135
  * leg2cheb_apply_transpose (transpose = 1) with the Lambda table of a
@@ -129,11 +132,13 @@ fl_status fl_idlt(const fl_plan* plan, const double* in, double* out, size_t bat
  *                         exactly the reference's algorithm (ndct.hpp:98-143);
  *   1 = FL_NDCT_FAST    : same nodes, evaluated internally about the cheb1
  *                         grid over power-of-two real DCTs (SURVEY.md 7 H2
- *                         option B): for N <= 8192 by the Chebyshev
- *                         (Jacobi-Anger) expansion of cos(n delta), sin(n delta)
- *                         in n/N -- 14 transforms at 2^-52, tail
- *                         2 sum_{m>=M} |J_m(0.83845)| <= tol -- above 8192 by
- *                         min_taylor_terms(cheb1, tol) Taylor terms.
+ *                         option B), by the Chebyshev (Jacobi-Anger)
+ *                         expansion of cos(n delta), sin(n delta) in n/N --
+ *                         14 transforms at 2^-52, tail
+ *                         2 sum_{m>=M} |J_m(0.83845)| <= tol -- at every
+ *                         power-of-two size (fused on chip for N <= 8192,
+ *                         one pack -> multi-pass FFT -> unpack per term
+ *                         above).
  * Both are within the reference's certified bound of each other
  * (test_ndct.cpp:173-183). Default FL_NDCT_FAST for dlt/idlt of power-of-two
  * sizes; the free-function fl_ndct always evaluates its plan literally. */
@@ -178,9 +183,9 @@ fl_status fl_plan_leg2cheb(const fl_plan* plan, int transpose, const double* in,
 /* The plan's NDCT step alone, as dlt/idlt run it (same FL_NDCT_* mode):
  * out = NDCT(in) (transpose = 0, transforms.hpp:48) or NDCT^T(in) (1, the
  * unweighted ndct_apply_transpose of transforms.hpp:60).
- * fl_plan_ndct_terms: transforms per column it evaluates (fast mode, N <=
- * 8192: the Chebyshev / Jacobi-Anger expansion about cheb1, 14 terms at
- * 2^-52; Taylor about cheb1 above 8192; the plan's own L when literal). */
+ * fl_plan_ndct_terms: transforms per column it evaluates (fast mode: the
+ * Chebyshev / Jacobi-Anger expansion about cheb1, 14 terms at 2^-52, at
+ * every power-of-two size; the plan's own L when literal). */
 fl_status fl_plan_ndct(const fl_plan* plan, int transpose, const double* in, double* out,
                        size_t batch, size_t ld, void* stream);
 int fl_plan_ndct_terms(const fl_plan* plan);
@@ -191,8 +196,10 @@ int fl_plan_ndct_terms(const fl_plan* plan);
  * (paper_1505_00354_b200/distributed.py):
  *   FL_STAGE_LEG2CHEB : chat = sum_{r in [lo,hi)} D(l_r) T D(l_r) c, the
  *                       Toeplitz-Hankel rank terms of M (idlt: M^T with (m+1/2));
- *   FL_STAGE_NDCT     : f = sum_{l in [lo,hi)} Taylor term l of the NDCT
- *                       (idlt: the transpose, with the quadrature weights).
+ *   FL_STAGE_NDCT     : f = sum_{m in [lo,hi)} term m of the fast-mode NDCT
+ *                       (the Chebyshev-expansion terms about cheb1, 14 at
+ *                       2^-52; idlt: the transpose, with the quadrature
+ *                       weights).
  * One column; needs the fast paths (n >= 2^15 and a power of two > 8192).
  * fl_plan_stage_terms gives the number of terms of a stage. */
 enum { FL_STAGE_LEG2CHEB = 0, FL_STAGE_NDCT = 1 };

@@ -83,7 +83,7 @@ def _load() -> C.CDLL:
         "fl_lambda_table": (i, [sz, dp, vp]),
         "fl_trig": (i, [i, i, sz, dp, dp, sz, sz, vp]),
         "fl_ndct": (i, [i, i, sz, i, dp, dp, dp, sz, sz, vp]),
-        "fl_ndct_error_bound": (i, [sz, i, i, dp, dp, C.POINTER(d), vp]),
+        "fl_ndct_error_bound": (i, [sz, i, i, dp, sz, dp, sz, C.POINTER(d), vp]),
         "fl_leg2cheb": (i, [i, sz, dp, sz, dp, dp, sz, sz, vp]),
         "fl_plan_create": (i, [sz, d, i, C.POINTER(vp)]),
         "fl_plan_create_from_grid": (i, [sz, d, i, dp, dp, dp, C.POINTER(vp)]),

@@ -128,6 +128,11 @@ class _Arr:
         return self.obj.ctypes.data
 
     @property
+    def n(self) -> int:
+        """Number of elements."""
+        return int(self.obj.numel()) if self.device else int(self.obj.size)
+
+    @property
     def stream(self):
         if self.device:
             import torch
@@ -272,7 +277,7 @@ def ndct_error_bound(plan: TaylorPlan, coeffs) -> float:  # ndct.hpp:147-155
     c = _Arr(coeffs)
     out = C.c_double(0.0)
     check(LIB.fl_ndct_error_bound(int(plan.size), int(plan.kind), int(plan.num_terms), _vp(d.ptr),
-                                  _vp(c.ptr), C.byref(out), c.stream or d.stream))
+                                  d.n, _vp(c.ptr), c.n, C.byref(out), c.stream or d.stream))
     return out.value
 
 

@@ -99,6 +99,19 @@ bool is_device_ptr(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
 }
 
+// page-locked (cudaHostAlloc / cudaHostRegister) host memory: the only host
+// memory an async copy can overlap with kernels
+bool is_pinned_host(const void* p) {
+  if (!p) return false;
+  cudaPointerAttributes a;
+  const cudaError_t e = cudaPointerGetAttributes(&a, p);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
 cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
 // A column block (n rows x batch columns, stride ld) as a device pointer.
@@ -216,14 +229,12 @@ __global__ void nonfinite_kernel(const double* __restrict__ v, size_t n, size_t 
 }
 
 // one CTA: r[0] = max_k |delta_k|, r[1] = sum_k |c_k| (fixed reduction order)
-__global__ void maxabs_l1_kernel(const double* __restrict__ d, const double* __restrict__ c,
-                                 size_t n, double* r) {
+__global__ void maxabs_l1_kernel(const double* __restrict__ d, size_t nd,
+                                 const double* __restrict__ c, size_t nc, double* r) {
   __shared__ double sm[2][1024];
   double m = 0.0, s = 0.0;
-  for (size_t i = threadIdx.x; i < n; i += blockDim.x) {
-    m = fmax(m, fabs(d[i]));
-    s += fabs(c[i]);
-  }
+  for (size_t i = threadIdx.x; i < nd; i += blockDim.x) m = fmax(m, fabs(d[i]));
+  for (size_t i = threadIdx.x; i < nc; i += blockDim.x) s += fabs(c[i]);
   sm[0][threadIdx.x] = m;
   sm[1][threadIdx.x] = s;
   __syncthreads();
@@ -240,8 +251,9 @@ __global__ void maxabs_l1_kernel(const double* __restrict__ d, const double* __r
   }
 }
 
-void reduce_maxabs_l1(const double* d, const double* c, size_t n, double* r, cudaStream_t s) {
-  maxabs_l1_kernel<<<1, 1024, 0, s>>>(d, c, n, r);
+void reduce_maxabs_l1(const double* d, size_t nd, const double* c, size_t nc, double* r,
+                      cudaStream_t s) {
+  maxabs_l1_kernel<<<1, 1024, 0, s>>>(d, nd, c, nc, r);
   note_launch("maxabs_l1_kernel");
 }
 
@@ -354,8 +366,11 @@ const PipeStreams& pipe_streams(int dev) {
 #endif
 constexpr size_t kPipeMinBytes = size_t(64) << 20;  // below this one copy each way is as fast
 
+// Only pinned host buffers: a D2H copy into pageable memory blocks the host
+// until the chunk's compute is done, which would serialise the pipeline
+// (pageable buffers take the one-copy-each-way path instead).
 bool pipeline_ok(const double* in, const double* out, size_t n, size_t batch) {
-  return out != nullptr && !is_device_ptr(in) && !is_device_ptr(out) && batch >= 8 &&
+  return is_pinned_host(in) && is_pinned_host(out) && batch >= 8 &&
          n * batch * sizeof(double) >= kPipeMinBytes;
 }
 
@@ -471,7 +486,14 @@ const L2COzaki* plan_ozaki(fl_plan* p, int transpose, size_t batch, cudaStream_t
       p->n > 16384)
     return nullptr;
   std::lock_guard<std::mutex> lock(p->mu);
-  if (!p->oz[transpose]) p->oz[transpose] = l2c_ozaki_create(p->n, p->s, transpose, transpose, s);
+  if (!p->oz[transpose]) {
+    // the A digits are written on `s`: publish the product only once they are
+    // complete, so a caller on another stream never reads them half-written
+    // (TransformConfig is shared across threads, transforms.hpp:15-18)
+    L2COzaki* oz = l2c_ozaki_create(p->n, p->s, transpose, transpose, s);
+    FLB_CUDA(cudaStreamSynchronize(s));
+    p->oz[transpose] = oz;
+  }
   return p->oz[transpose];
 }
 
@@ -605,17 +627,20 @@ fl_status fl_ndct(int transpose, int kind, size_t n, int num_terms, const double
 }
 
 fl_status fl_ndct_error_bound(size_t n, int kind, int num_terms, const double* delta_theta,
-                              const double* coeffs, double* bound, void* stream) {
+                              size_t delta_len, const double* coeffs, size_t coeffs_len,
+                              double* bound, void* stream) {
   return guarded([&] {
     check_kind(kind);
+    // each reduction over its own vector's length, as the reference loops
+    // (ndct.hpp:149, :154 norm_l1(coeffs)); q uses the plan size n
     double maxd = 0.0, l1 = 0.0;
-    if (n > 0) {
+    if (delta_len > 0 || coeffs_len > 0) {
       require_device();
       cudaStream_t s = as_stream(stream);
-      DevIn d(delta_theta, n, 1, n, s);
-      DevIn c(coeffs, n, 1, n, s);
+      DevIn d(delta_theta, delta_len, 1, delta_len, s);
+      DevIn c(coeffs, coeffs_len, 1, coeffs_len, s);
       DevScratch<double> r(2, s);
-      reduce_maxabs_l1(d.ptr, c.ptr, n, r.p, s);
+      reduce_maxabs_l1(d.ptr, delta_len, c.ptr, coeffs_len, r.p, s);
       double h[2];
       FLB_CUDA(cudaMemcpyAsync(h, r.p, sizeof h, cudaMemcpyDeviceToHost, s));
       sync(s);

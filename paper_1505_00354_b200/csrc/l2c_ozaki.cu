@@ -901,6 +901,27 @@ void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t co
                      cudaStream_t st) {
   if (cols == 0) return;
   const size_t n = p.n, r = p.r;
+  // the digit split reads the columns as double2: a column start that is only
+  // 8-byte aligned (odd stride, or a view at an odd element offset) goes
+  // through a packed, aligned copy instead of faulting
+  if ((reinterpret_cast<uintptr_t>(in) & 15) != 0 || (ld & 1) != 0) {
+    double* packed = nullptr;
+    FLB_CUDA(cudaMallocAsync(&packed, n * cols * sizeof(double), st));
+    FLB_CUDA(cudaMemcpy2DAsync(packed, n * 8, in, ld * 8, n * 8, cols, cudaMemcpyDeviceToDevice,
+                               st));
+    if (ld == n) {
+      l2c_ozaki_apply(p, packed, out, cols, n, st);
+    } else {  // one stride serves both sides: the product goes through a stride-n scratch
+      double* res = nullptr;
+      FLB_CUDA(cudaMallocAsync(&res, n * cols * sizeof(double), st));
+      l2c_ozaki_apply(p, packed, res, cols, n, st);
+      FLB_CUDA(cudaMemcpy2DAsync(out, ld * 8, res, n * 8, n * 8, cols, cudaMemcpyDeviceToDevice,
+                                 st));
+      cudaFreeAsync(res, st);
+    }
+    cudaFreeAsync(packed, st);
+    return;
+  }
   int8_t* b = nullptr;
   double* bcol = nullptr;
   FLB_CUDA(cudaMallocAsync(&b, (size_t)oz::S * 2 * cols * r, st));
@@ -914,24 +935,18 @@ void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t co
     oz_split_b_kernel<16><<<(unsigned)cols, (unsigned)(n / 16), 0, st>>>(in, n, ld, cols, b, bcol);
   note_launch("oz_split_b_kernel");
   const CUtensorMap tmap_b = make_map(b, r, cols, 2 * oz::S, oz::BN);
-  static bool attr = [] {
-    FLB_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  oz::SMEM));
-    return true;
-  }();
-  (void)attr;
+  // the attribute is per device context: set it on every call (the library
+  // serves several devices in one process)
+  FLB_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                oz::SMEM));
 #ifndef FLB_OZ_PAIR
 #define FLB_OZ_PAIR 1
 #endif
   if (FLB_OZ_PAIR && (r / oz::BM) % 2 == 0) {
     // SM pairs: tiles of 256 rows x 64 columns, B staged as two 32-column halves
     const CUtensorMap tmap_b2 = make_map(b, r, cols, 2 * oz::S, oz::BN / 2);
-    static bool attr2 = [] {
-      FLB_CUDA(cudaFuncSetAttribute(oz_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                    oz2::SMEM));
-      return true;
-    }();
-    (void)attr2;
+    FLB_CUDA(cudaFuncSetAttribute(oz_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  oz2::SMEM));
     const size_t tiles = 2 * (r / oz::BM / 2) * ((cols + oz::BN - 1) / oz::BN);
     const unsigned clusters = (unsigned)std::min<size_t>(tiles, (size_t)sm_count() / 2);
     oz_gemm2_kernel<<<2 * clusters, oz::THREADS, oz2::SMEM, st>>>(

@@ -4,7 +4,8 @@ Both stages of the transform are sums of independent terms
 (include/fastleg_b200.h, fl_dlt_stage):
 
   chat = M c       = sum_{r < K} D(l_r) T D(l_r) c     (Toeplitz-Hankel rank terms)
-  f    = NDCT(chat) = sum_{l < L} W_l C_l D^l chat       (Taylor terms)
+  f    = NDCT(chat) = sum_{m < M} W_m C_m T_m(n/N) chat  (Chebyshev-expansion terms
+                                                        about cheb1, M = 14)
 
 so each of P ranks (one process per GPU) evaluates a contiguous slice of the
 terms on its own GPU -- full-length FFTs, no distributed FFT -- and one NCCL
