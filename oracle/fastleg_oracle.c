@@ -399,6 +399,10 @@ int fo_leg2cheb_apply(size_t n, const double* table, size_t max_index, const dou
   double* s = (double*)malloc(sizeof(double) * (n + 1));
   int rc = scaled_lambda_table(table, max_index, n, s);
   if (rc == 0) {
+    /* rows are independent and each keeps the reference's summation order, so
+       the row-parallel loop is bit-identical to the serial one (OpenMP only
+       shortens the O(N^2) oracle at N >= 2^16) */
+#pragma omp parallel for schedule(dynamic, 64) if (n >= 4096)
     for (size_t k = 0; k < n; ++k) {
       double acc = 0.0;
       for (size_t j = 0; k + 2 * j < n; ++j) acc += s[j] * s[k + j] * c[k + 2 * j];
@@ -415,6 +419,7 @@ int fo_leg2cheb_apply_transpose(size_t n, const double* table, size_t max_index,
   double* s = (double*)malloc(sizeof(double) * (n + 1));
   int rc = scaled_lambda_table(table, max_index, n, s);
   if (rc == 0) {
+#pragma omp parallel for schedule(dynamic, 64) if (n >= 4096)
     for (size_t m = 0; m < n; ++m) {
       double acc = 0.0;
       for (size_t j = 0; 2 * j < m; ++j) acc += s[j] * s[m - j] * v[m - 2 * j];

@@ -121,3 +121,63 @@ def test_oracle_nodes_vs_truth(nodes_truth):
             t = float(r["theta"])
             assert abs(th[r["k"]] - t) <= 4 * EPS / math.sin(t) + 2 * EPS
             assert abs(w[r["k"]] - float(r["w"])) <= (8 / math.sin(t) ** 2 + int(n) / 64 + 16) * EPS * float(r["w"])
+
+
+@pytest.mark.skipif(REF is None, reason="oracle/_ref not built")
+@pytest.mark.parametrize("n", [1024, 4096, 16384])
+def test_restatement_matches_compiled_reference_transforms_large(n):
+    """The pins above stop at N = 256; the GPU parity sweep runs to 2^18. The
+    restatement's DLT / IDLT on an injected grid equal the compiled
+    reference's bit for bit at the sweep's sizes where the reference's O(N^2)
+    conversion still runs in well under a second (both kinds)."""
+    th, x, w = O.nodes_weights(n)
+    rng = np.random.default_rng(n + 7)
+    c = rng.standard_normal(n) / np.sqrt(np.arange(n) + 1.0)
+    for kind in (CHEB1, CHEBSTAR):
+        f = O.dlt_grid(c, kind, EPS, th, x, w)
+        assert np.array_equal(f, REF.dlt_grid(c, kind, EPS, th, x, w)), kind
+        assert np.array_equal(O.idlt_grid(f, kind, EPS, th, x, w), REF.idlt_grid(f, kind, EPS, th, x, w)), kind
+
+
+@pytest.mark.skipif(REF is None, reason="oracle/_ref not built")
+def test_restatement_matches_compiled_reference_ndct_65536():
+    """C2's size: the restatement's NDCT / NDCT^T equal the compiled
+    reference's bit for bit on a perturbed grid, both kinds."""
+    n = 65536
+    th = (np.arange(n) + 0.5) * np.pi / n + 0.3 / n * np.sin(np.arange(n))
+    c = np.random.default_rng(3).standard_normal(n)
+    for kind, L in ((CHEB1, 17), (CHEBSTAR, 9)):
+        d = O.reference_delta(n, kind, th)
+        assert np.array_equal(O.ndct(c, kind, L, d), REF.ndct(c, kind, L, d)), kind
+        assert np.array_equal(O.ndct(c, kind, L, d, True), REF.ndct(c, kind, L, d, True)), kind
+
+
+@pytest.mark.parametrize("n", [1, 2, 7, 1000, 4096, 65536])
+def test_numpy_restatement_matches_c_oracle(n):
+    """oracle/ndct_np.py (the large-N NDCT oracle: pocketfft at the FFT
+    boundary) against the C restatement: the r2r passes and the NDCT / NDCT^T
+    agree to FFT rounding (<= 1e-15 ||c||_1), both kinds."""
+    from oracle import ndct_np as NP
+    rng = np.random.default_rng(n)
+    c = rng.standard_normal(n)
+    th = (np.arange(n) + 0.5) * np.pi / n + 0.3 / n * np.sin(np.arange(n) + 1.0)
+    s = np.abs(c).sum()
+    fns = (NP.dct_iii, NP.dst_iii, NP.dct_iii_transpose, NP.dst_iii_transpose)
+    for kind, L in ((CHEB1, 17), (CHEBSTAR, 9)):
+        for op in range(4):
+            assert np.max(np.abs(O.trig(op, c, kind) - fns[op](c, kind))) <= 1e-15 * s, (kind, op)
+        d = O.reference_delta(n, kind, th)
+        assert np.max(np.abs(O.ndct(c, kind, L, d) - NP.ndct_apply(c, kind, L, d))) <= 1e-15 * s
+        assert np.max(np.abs(O.ndct(c, kind, L, d, True) - NP.ndct_apply_transpose(c, kind, L, d))) <= 1e-15 * s
+
+
+def test_numpy_leg2cheb_rows_match_c_oracle():
+    n = 3001
+    c = np.random.default_rng(5).standard_normal(n)
+    lam = O.lambda_table(n - 1)
+    s = lam / lam[0]
+    from oracle import ndct_np as NP
+    rows = [0, 1, 2, 3, 100, 1500, n - 2, n - 1]
+    full, full_t = O.leg2cheb(c), O.leg2cheb(c, True)
+    assert np.max(np.abs(NP.leg2cheb_rows(c, s, rows) - full[rows])) <= 1e-15 * np.abs(c).sum()
+    assert np.max(np.abs(NP.leg2cheb_transpose_rows(c, s, rows) - full_t[rows])) <= 1e-15 * np.abs(c).sum()
