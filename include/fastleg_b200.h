@@ -141,10 +141,26 @@ fl_status fl_idlt(const fl_plan* plan, const double* in, double* out, size_t bat
  *                         above).
  * Both are within the reference's certified bound of each other
  * (test_ndct.cpp:173-183). Default FL_NDCT_FAST for dlt/idlt of power-of-two
- * sizes; the free-function fl_ndct always evaluates its plan literally. */
+ * sizes. */
 enum { FL_NDCT_LITERAL = 0, FL_NDCT_FAST = 1 };
 fl_status fl_plan_set_ndct_mode(fl_plan* plan, int mode);
 int fl_plan_ndct_mode(const fl_plan* plan);
+
+/* Process-wide mode of the free functions fl_ndct (ndct.hpp:98-143) and
+ * fl_trig (trig.hpp:55-136) at power-of-two N >= 512 (default FL_NDCT_FAST):
+ *   FL_NDCT_FAST    : fl_ndct evaluates the same nodes about the cheb1 grid by
+ *                     the Chebyshev expansion (either kind; the node offsets
+ *                     are re-based exactly, delta' = delta + theta*_kind -
+ *                     theta0) whenever the literal L-term evaluation is exact
+ *                     to fp64 rounding (its bound min((N max|delta|)^L/L!,
+ *                     C(L)) <= 2^-52) and delta is not identically zero; the
+ *                     chebstar dct_iii / dst_iii / transposes likewise (zero
+ *                     offsets, the sine flavour for the DSTs);
+ *   FL_NDCT_LITERAL : the plan's own L Taylor terms on its own grid (chirp-z
+ *                     length-(2N+1) transforms for chebstar) -- the ablation.
+ * The cheb1 DCT/DST passes and every other size are unaffected. */
+fl_status fl_set_free_ndct_mode(int mode);
+int fl_free_ndct_mode(void);
 
 /* Legendre -> Chebyshev conversion inside dlt/idlt of plans with n >= 2^15
  * and at most 16 columns:

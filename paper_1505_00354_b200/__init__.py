@@ -9,8 +9,8 @@ reference's header API; ``include/fastleg/*.hpp`` is the C++ one.
 """
 from ._lib import (  # noqa: F401
     DomainError, FastlegCudaError, FastlegError, InvalidArgument, OverflowErrorFL,
-    RuntimeErrorFL, device_available, launch_count, NDCT_FAST, NDCT_LITERAL, LEG2CHEB_DIRECT,
-    LEG2CHEB_FAST, GEMM_FP64, GEMM_INT8_SPLIT,
+    RuntimeErrorFL, device_available, launch_count, set_free_ndct_mode, free_ndct_mode, NDCT_FAST,
+    NDCT_LITERAL, LEG2CHEB_DIRECT, LEG2CHEB_FAST, GEMM_FP64, GEMM_INT8_SPLIT,
 )
 from .api import *  # noqa: F401,F403
 from .api import (  # noqa: F401

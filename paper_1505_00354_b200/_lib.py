@@ -64,7 +64,8 @@ EXPORTS = [
     "fl_eval_legendre_direct", "fl_eval_chebyshev_direct", "fl_idlt_direct",
     "fl_cheb_coeffs_of_legendre", "fl_plan_set_leg2cheb_mode", "fl_plan_leg2cheb_rank",
     "fl_plan_stage_terms", "fl_dlt_stage", "fl_plan_set_gemm_mode", "fl_plan_gemm_mode",
-    "fl_plan_leg2cheb", "fl_plan_ndct", "fl_plan_ndct_terms",
+    "fl_plan_leg2cheb", "fl_plan_ndct", "fl_plan_ndct_terms", "fl_set_free_ndct_mode",
+    "fl_free_ndct_mode",
 ]
 
 
@@ -115,6 +116,8 @@ def _load() -> C.CDLL:
         "fl_plan_leg2cheb": (i, [vp, i, dp, dp, sz, sz, vp]),
         "fl_plan_ndct": (i, [vp, i, dp, dp, sz, sz, vp]),
         "fl_plan_ndct_terms": (i, [vp]),
+        "fl_set_free_ndct_mode": (i, [i]),
+        "fl_free_ndct_mode": (i, []),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)
@@ -134,6 +137,17 @@ def check(status: int) -> None:
 
 def device_available() -> bool:
     return bool(LIB.fl_device_available())
+
+
+def set_free_ndct_mode(mode: int) -> None:
+    """NDCT_FAST (default) or NDCT_LITERAL for the free functions ndct_apply /
+    ndct_apply_transpose and the chebstar dct_iii / dst_iii / transposes
+    (include/fastleg_b200.h, fl_set_free_ndct_mode)."""
+    check(LIB.fl_set_free_ndct_mode(int(mode)))
+
+
+def free_ndct_mode() -> int:
+    return int(LIB.fl_free_ndct_mode())
 
 
 def launch_count() -> int:

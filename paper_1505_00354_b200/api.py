@@ -447,6 +447,27 @@ class TransformConfig:  # transforms.hpp:19-38
             self._lambda = LambdaCache(max(self.size() - 1, 0))
         return self._lambda
 
+    def _stage(self, fn, x, transpose: int):
+        a = _Arr(x)
+        batch, n = _ncols_n(a.obj)
+        if n != self.size():
+            raise _lib.InvalidArgument("fastleg: input size does not match config")
+        out = _Arr(None, out_like=a, shape=a.obj.shape)
+        check(fn(self._h, int(transpose), _vp(a.ptr), _vp(out.ptr), batch, n, a.stream))
+        return out.obj
+
+    def convert(self, x, transpose: bool = False):
+        """The plan's conversion step exactly as dlt / idlt run it
+        (fl_plan_leg2cheb): M x (transforms.hpp:47), or (m + 1/2) M^T x
+        (the last step of transforms.hpp:62) with transpose=True."""
+        return self._stage(LIB.fl_plan_leg2cheb, x, int(transpose))
+
+    def ndct(self, x, transpose: bool = False):
+        """The plan's NDCT step exactly as dlt / idlt run it (fl_plan_ndct,
+        same fast / literal mode): NDCT(x) (transforms.hpp:48), or the
+        unweighted NDCT^T(x) of transforms.hpp:60 with transpose=True."""
+        return self._stage(LIB.fl_plan_ndct, x, int(transpose))
+
 
 def dlt(c: CoefficientVector | Any, config: TransformConfig):  # transforms.hpp:42-49
     if isinstance(c, CoefficientVector):

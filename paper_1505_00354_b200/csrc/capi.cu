@@ -26,6 +26,7 @@ namespace flb {
 
 namespace {
 thread_local std::string g_last_error;
+std::atomic<int> g_free_mode{FL_NDCT_FAST};  // fl_set_free_ndct_mode
 std::atomic<unsigned long long> g_launches{0};
 }  // namespace
 
@@ -475,7 +476,7 @@ void plan_finish(fl_plan* p) {
   launch_reference_grid(n, p->kind, p->theta, p->tstar, p->delta, 0);
   launch_lambda(n - 1, p->lambda, 0);
   scaled_lambda(p->lambda, p->s, n, 0);
-  p->fast = fast_ndct_create(n, p->tolerance, p->kind, p->theta);
+  p->fast = fast_ndct_create(n, p->tolerance, p->kind, p->delta);
   if (n >= kL2CFastMin) p->l2c = l2c_fast_create(n, p->s, 0);
   FLB_CUDA(cudaDeviceSynchronize());
 }
@@ -531,6 +532,16 @@ int fl_device_available(void) {
 }
 
 uint64_t fl_kernel_launch_count(void) { return g_launches.load(); }
+
+fl_status fl_set_free_ndct_mode(int mode) {
+  return guarded([&] {
+    if (mode != FL_NDCT_LITERAL && mode != FL_NDCT_FAST)
+      fail(FL_INVALID_ARGUMENT, "fastleg: unknown ndct mode");
+    g_free_mode = mode;
+  });
+}
+
+int fl_free_ndct_mode(void) { return g_free_mode.load(); }
 
 fl_status fl_nodes_weights(size_t n, double* theta, double* x, double* weights, void* stream) {
   return guarded([&] {
@@ -589,6 +600,8 @@ fl_status fl_trig(int op, int kind, size_t n, const double* in, double* out, siz
     if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
     if (fast_trig_ok(n, kind))
       fast_trig(op, n, i.ptr, o.ptr, batch, o.ld, s);
+    else if (g_free_mode == FL_NDCT_FAST && fast_trig_bessel_ok(n, kind))
+      fast_trig_bessel(op, n, i.ptr, o.ptr, batch, o.ld, s);
     else
       czt_trig(op, kind, n, i.ptr, o.ptr, batch, o.ld, s);
     o.finish();
@@ -615,10 +628,13 @@ fl_status fl_ndct(int transpose, int kind, size_t n, int num_terms, const double
     if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
     const FastNdct* fast = nullptr;
     FastNdctHolder holder;
-    if (num_terms > 0 && fast_ndct_literal_ok(n, kind)) {
+    // fast mode: the Chebyshev expansion about cheb1 (either kind, power of
+    // two) when the literal evaluation is exact to rounding; else literal
+    if (num_terms > 0 && g_free_mode == FL_NDCT_FAST && !overflow_guard(n, num_terms))
+      holder.p = fast_ndct_create_bessel(n, kind, d.ptr, num_terms, 0, s);
+    if (!holder.p && num_terms > 0 && fast_ndct_literal_ok(n, kind))
       holder.p = fast_ndct_create_literal(n, kind, num_terms, d.ptr, s);
-      fast = holder.p;
-    }
+    fast = holder.p;
     run_ndct(where, transpose, kind, n, num_terms, d.ptr, i.ptr, i.ld, o.ptr, o.ld, batch,
              nullptr, fast, s);
     o.finish();

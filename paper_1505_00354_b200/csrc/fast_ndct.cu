@@ -36,6 +36,8 @@
 // dct_iii / dst_iii / *_transpose of trig.hpp (so ndct with zero
 // perturbation stays bit-identical to dct_iii, test_ndct.cpp:112-125).
 #include <algorithm>
+#include <cmath>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <tuple>
@@ -60,6 +62,12 @@ struct FastNdct {
   // num_terms terms; weight / row tables [m][N] for the fused kernels
   // (N <= 8192), computed on the fly by the multi-pass kernels
   int bes_terms = 0;
+  // swap: the sine flavour sum_n c_n sin(n theta_k) (dst_iii and its
+  // transpose on a non-cheb1 grid): DCT and DST trade places per term and the
+  // odd terms change sign (sin(a + b) = sin a cos b + cos a sin b)
+  int swap = 0;
+  cudaStream_t alloc_stream = nullptr;  // per-call objects: stream-ordered buffers
+  bool async_alloc = false;
   double* bes_wf = nullptr;  // forward weights, owned-row order
   double* bes_wt = nullptr;  // transpose weights, tr_slot order
   double* bes_tt = nullptr;  // transpose row factors T_m(n/N), tr_row order
@@ -525,7 +533,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
                          size_t ld_out, size_t batch, const double* __restrict__ delta,
                          int num_terms, int plain_op, const double2* __restrict__ tw4n,
                          const double2* __restrict__ fftw_g, const double* __restrict__ wtab,
-                         int* nonfinite) {
+                         int* nonfinite, int swap) {
   using C = Cfg<LOG2N>;
   using FC = FwdCfg<LOG2N, BES>;
   constexpr int N = C::N, T = C::T, OWN = C::OWN;
@@ -610,9 +618,11 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
     for (int m = 0; m < num_terms; ++m) {
       const double* wr = wtab + (size_t)m * N + t;
       double2* fin;
-      if (m == 0)
+      if (m == 0 && swap)
+        fin = tm_fwd_term<LOG2N, true, true>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF, tW);
+      else if (m == 0)
         fin = tm_fwd_term<LOG2N, false, true>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF, tW);
-      else if (m & 1)
+      else if ((m & 1) ^ swap)
         fin = tm_fwd_term<LOG2N, true, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF, tW);
       else
         fin = tm_fwd_term<LOG2N, false, false>(stage, zx, zy, t, ta_t, r4_t, fftw, wr, f, tA, tB, tF, tW);
@@ -639,9 +649,18 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
     // weights read where they are applied (PST = T), pack in two halves
     for (int m = 0; m < num_terms; ++m) {
       const double* wr = wtab + (size_t)m * N + t;
-      if (m == 0)
+      if (m == 0 && swap)
+        fwd_term<LOG2N, true, 1, false, T, true>(stage, stage_odd, zx, zx, t, bar, ta_t, r4_t,
+                                                 fftw, wr, f, 1.0);
+      else if (m == 0)
         fwd_term<LOG2N, false, 1, false, T, true>(stage, stage_odd, zx, zx, t, bar, ta_t, r4_t,
                                                   fftw, wr, f, 1.0);
+      else if (swap && (m & 1))  // sine flavour: a DCT of the odd-m stage
+        fwd_term<LOG2N, false, 2, false, T, true>(stage_odd, stage, zx, zx, t, bar, ta_t, r4_t,
+                                                  fftw, wr, f, 1.0);
+      else if (swap)  // m even, sine flavour: a DST of the even-m stage
+        fwd_term<LOG2N, true, 2, false, T, true>(stage, stage_odd, zx, zx, t, bar, ta_t, r4_t,
+                                                 fftw, wr, f, 1.0);
       else if (m & 1)
         fwd_term<LOG2N, true, 2, false, T, true>(stage_odd, stage, zx, zx, t, bar, ta_t, r4_t,
                                                  fftw, wr, f, 1.0);
@@ -654,9 +673,18 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, FwdCfg<LOG2N, BES>::MINB)
 #pragma unroll
       for (int i = 0; i < OWN; ++i) p[i] = __ldg(wtab + (size_t)m * N + i * T + t);
       double2* fin;
-      if (m == 0)
+      if (m == 0 && swap)
+        fin = fwd_term<LOG2N, true, 1, FC::PP>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+                                       p, f, 1.0);
+      else if (m == 0)
         fin = fwd_term<LOG2N, false, 1, FC::PP>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                                         p, f, 1.0);
+      else if (swap && (m & 1))  // sine flavour: a DCT of the odd-m stage
+        fin = fwd_term<LOG2N, false, 2, FC::PP>(stage_odd, stage, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+                                        p, f, 1.0);
+      else if (swap)
+        fin = fwd_term<LOG2N, true, 2, FC::PP>(stage, stage_odd, zx, other(zx), t, bar, ta_t, r4_t, fftw,
+                                       p, f, 1.0);
       else if (m & 1)
         fin = fwd_term<LOG2N, true, 2, FC::PP>(stage_odd, stage, zx, other(zx), t, bar, ta_t, r4_t, fftw,
                                        p, f, 1.0);
@@ -862,7 +890,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
                         int num_terms, int plain_op, const double* __restrict__ mult,
                         const double2* __restrict__ tw4n, const double2* __restrict__ fftw_g,
                         const double* __restrict__ wtab, const double* __restrict__ ttab,
-                        int* nonfinite) {
+                        int* nonfinite, int swap) {
   using C = Cfg<LOG2N>;
   using TC = TrCfg<LOG2N, BES>;
   constexpr int N = C::N, T = C::T, OWN = C::OWN;
@@ -966,7 +994,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
       const double* tr = ttab + (size_t)m * N + t;
       const double* wrow = wtab + (size_t)m * N;
       double2* fin;
-      if (m & 1)
+      if ((m & 1) ^ swap)
         fin = tr_term<LOG2N, true, 2, true, T, true, TC::T3>(hs, nullptr, nd, delta, 0.0, wrow, zx,
                                                              other(zx), t, bar, ta_t, r4_t, fftw, tr,
                                                              o, 1.0, tO, tH);
@@ -996,7 +1024,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
       const double* tr = ttab + (size_t)m * N + t;
       const double* wrow = wtab + (size_t)m * N;
       double2* fin;
-      if (m & 1)
+      if ((m & 1) ^ swap)
         fin = tr_term<LOG2N, true, 2, TC::ONE_STAGE, T>(hs, nullptr, nd, delta, 0.0, wrow, zx,
                                                        other(zx), t, bar, ta_t, r4_t, fftw, tr, o, 1.0);
       else
@@ -1010,7 +1038,7 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, TrCfg<LOG2N, BES>::MINB)
       for (int i = 0; i < OWN; ++i) rp[i] = __ldg(ttab + (size_t)m * N + i * T + t);
       const double* wrow = wtab + (size_t)m * N;
       double2* fin;
-      if (m & 1)
+      if ((m & 1) ^ swap)
         fin = tr_term<LOG2N, true, 2, TC::PP>(hs, nullptr, nd, delta, 0.0, wrow, zx, other(zx), t, bar,
                                       ta_t, r4_t, fftw, rp, o, 1.0);
       else
@@ -1386,7 +1414,8 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
       kern<<<grid, C::THREADS, smem, s>>>(
           in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta,
           use_bes ? bes->bes_terms : num_terms, plain_op, mult, tw, fftw,
-          use_bes ? bes->bes_wt : nullptr, use_bes ? bes->bes_tt : nullptr, nonfinite);
+          use_bes ? bes->bes_wt : nullptr, use_bes ? bes->bes_tt : nullptr, nonfinite,
+          use_bes ? bes->swap : 0);
       note_launch(use_bes ? "fast_ndct_tr_kernel<bessel>" : "fast_ndct_tr_kernel");
     } else {
       auto kern = use_bes ? fast_ndct_fwd_kernel<LOG2N, true> : fast_ndct_fwd_kernel<LOG2N, false>;
@@ -1395,7 +1424,7 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
       kern<<<grid, C::THREADS, smem, s>>>(
           in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out, nc, delta,
           use_bes ? bes->bes_terms : num_terms, plain_op, tw, fftw,
-          use_bes ? bes->bes_wf : nullptr, nonfinite);
+          use_bes ? bes->bes_wf : nullptr, nonfinite, use_bes ? bes->swap : 0);
       note_launch(use_bes ? "fast_ndct_fwd_kernel<bessel>" : "fast_ndct_fwd_kernel");
     }
   }
@@ -1427,7 +1456,7 @@ __host__ __device__ inline double bessel_weight(int m, double y) {
 template <int LOG2N>
 __global__ void bessel_tables_kernel(const double* __restrict__ delta, int terms,
                                      double* __restrict__ wf, double* __restrict__ wt,
-                                     double* __restrict__ tt) {
+                                     double* __restrict__ tt, int swap) {
   using C = Cfg<LOG2N>;
   constexpr int N = C::N, T = C::T;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1437,8 +1466,9 @@ __global__ void bessel_tables_kernel(const double* __restrict__ delta, int terms
   const double x = (double)tr_row<N>(j % T, j / T) / (double)N;
   double tm1 = 1.0, tm = x;  // T_{m-1}, T_m
   for (int m = 0; m < terms; ++m) {
-    wf[(size_t)m * N + j] = bessel_weight(m, yf);
-    wt[(size_t)m * N + j] = bessel_weight(m, yt);
+    const double sg = (swap && (m & 1)) ? -1.0 : 1.0;  // sine flavour: odd terms change sign
+    wf[(size_t)m * N + j] = sg * bessel_weight(m, yf);
+    wt[(size_t)m * N + j] = sg * bessel_weight(m, yt);
     const double tv = m == 0 ? 1.0 : m == 1 ? x : tm;
     tt[(size_t)m * N + j] = tv;
     if (m >= 1) {  // advance to T_{m+1}
@@ -1597,7 +1627,8 @@ __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, in
 
 void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double* out,
                 size_t ld_out, size_t batch, const double* delta, int l_lo, int l_hi,
-                int plain_op, const double* mult, int* nonfinite, cudaStream_t s, int cheb) {
+                int plain_op, const double* mult, int* nonfinite, cudaStream_t s, int cheb,
+                int swap) {
   const size_t n = size_t(1) << log2n, P = n / 2;
   if (ld_in != ld_out) fail(FL_RUNTIME_ERROR, "fast ndct: mismatched strides");
   const size_t chunk_cap = std::max<size_t>(1, (size_t(1) << 30) / (2 * P * sizeof(double2)));
@@ -1616,9 +1647,11 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
     dim3 grid(gx, (unsigned)nc);
     for (int l = l_lo; l < l_hi; ++l) {
       const int first = l == l_lo;
-      const int odd = plain ? plain_op : (l & 1);
+      const int odd = plain ? plain_op : ((l & 1) ^ swap);
       const int ch = plain ? 0 : cheb;
-      const double sign = (plain || ch) ? 1.0 : (((l + 1) / 2) % 2 == 0 ? 1.0 : -1.0);
+      const double sign = plain ? 1.0
+                          : ch ? ((swap && (l & 1)) ? -1.0 : 1.0)
+                               : (((l + 1) / 2) % 2 == 0 ? 1.0 : -1.0);
       if (!transpose) {
         big_fwd_pack_kernel<<<grid, 256, 0, s>>>(in + c0 * ld_in, ld_in, n, plain ? 0 : l, odd, ch,
                                                  Z, l == 0 ? nonfinite : nullptr);
@@ -1651,7 +1684,7 @@ void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* 
   if (l_hi < 0) l_hi = num_terms;
   if (log2n > 13) {
     launch_big(log2n, transpose, in, ld_in, out, ld_out, batch, delta, l_lo, l_hi, plain_op, mult,
-               nonfinite, s, cheb ? 1 : 0);
+               nonfinite, s, cheb ? 1 : 0, cheb ? bes->swap : 0);
     return;
   }
   if (plain_op < 0 && (l_lo != 0 || l_hi != num_terms))
@@ -1677,15 +1710,17 @@ int log2_exact(size_t n) {
 // bound as cheb1_terms (|N delta| <= 0.83845): smallest M with
 // 2 sum_{m >= M} |J_m(0.83845)| <= tol (|T_m| <= 1 on [0, 1]); 14 at 2^-52
 // against Taylor's 17.
-int bessel_terms(double tol) {
-  if (!(tol > 0.0 && tol < 1.0)) return -1;
+int bessel_terms_at(double y, double tol) {
+  if (!(tol > 0.0 && tol < 1.0) || !(y >= 0.0 && y <= 2.0)) return -1;
   for (int M = 1; M <= 30; ++M) {
     double tail = 0.0;
-    for (int m = M; m < M + 12; ++m) tail += 2.0 * fabs(bessel_j(m, 0.83845));
+    for (int m = M; m < M + 12; ++m) tail += 2.0 * fabs(bessel_j(m, y));
     if (tail <= tol) return M;
   }
   return -1;
 }
+
+int bessel_terms(double tol) { return bessel_terms_at(0.83845, tol); }
 
 int cheb1_terms(double tol) {  // ndct.hpp:49-59 for cheb1; -1 if unattainable
   if (!(tol > 0.0 && tol < 1.0)) return -1;
@@ -1713,6 +1748,26 @@ void fast_trig(int op, size_t n, const double* in, double* out, size_t batch, si
 
 bool fast_ndct_literal_ok(size_t n, int kind) { return fast_trig_ok(n, kind); }
 
+bool fast_trig_bessel_ok(size_t n, int kind) {
+  const int lg = log2_exact(n);
+  return kind == FL_CHEBSTAR && lg >= kFastMinLog2 && lg <= kFastMaxLog2;
+}
+
+// dct_iii / dst_iii / *_transpose on the chebstar grid (trig.hpp:55-136) at
+// power-of-two N: the chebstar angles are cheb1 angles plus an exact offset
+// (|N offset| < pi/4), so the length-(2N+1) transform becomes the fused
+// Chebyshev-expansion NDCT about cheb1 with zero node offsets (the sine
+// flavour for the DSTs).
+void fast_trig_bessel(int op, size_t n, const double* in, double* out, size_t batch, size_t ld,
+                      cudaStream_t s) {
+  const int transpose = op == FL_DCT_III_T || op == FL_DST_III_T;
+  const int swap = (op == FL_DST_III || op == FL_DST_III_T) ? 1 : 0;
+  FastNdctHolder h;
+  h.p = fast_ndct_create_bessel(n, FL_CHEBSTAR, nullptr, 1, swap, s);
+  if (!h.p) fail(FL_RUNTIME_ERROR, "fast trig: chebstar expansion unavailable");
+  fast_ndct_run(*h.p, transpose, in, ld, out, ld, batch, nullptr, nullptr, s);
+}
+
 FastNdct* fast_ndct_create_literal(size_t n, int kind, int num_terms, const double* delta,
                                    cudaStream_t) {
   if (!fast_ndct_literal_ok(n, kind)) return nullptr;
@@ -1724,44 +1779,137 @@ FastNdct* fast_ndct_create_literal(size_t n, int kind, int num_terms, const doub
   return p;
 }
 
-FastNdct* fast_ndct_create(size_t n, double tol, int kind, const double* theta) {
+// delta'_k = delta_k + (theta*_kind(k) - theta0_k): the angle the reference
+// evaluates for kind (its exact grid angle plus the fp64 offset delta_k,
+// ndct.hpp:98-117) re-expressed about the cheb1 angle theta0_k = (k + 1/2) pi / N.
+// The grid offset is exact up to one rounding: (k + 3/4) pi / (N + 1/2) -
+// (k + 1/2) pi / N = (N - 2k - 1) pi / (2N (2N + 1)). (Subtracting the two
+// rounded angles instead would move the evaluation point by their rounding
+// errors, ~1e-16 rad, i.e. ~N 1e-16 relative at degree N.) delta may be null
+// (zero offsets: the plain chebstar DCT). amax[0] = max |delta|, amax[1] =
+// max |delta'| (bit patterns of non-negative doubles order as integers).
+__global__ void fast_delta_kernel(size_t n, int kind, const double* __restrict__ delta,
+                                  double* __restrict__ out, unsigned long long* amax) {
+  const size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double d = delta ? delta[k] : 0.0;
+  double off = 0.0;
+  if (kind == FL_CHEBSTAR) {
+    const double nd = (double)n;
+    off = (double)((long long)n - 2 * (long long)k - 1) * (kPi / (2.0 * nd * (2.0 * nd + 1.0)));
+  }
+  const double dp = d + off;
+  out[k] = dp;
+  if (amax) {
+    atomicMax(&amax[0], (unsigned long long)__double_as_longlong(fabs(d)));
+    atomicMax(&amax[1], (unsigned long long)__double_as_longlong(fabs(dp)));
+  }
+}
+
+void build_bessel_tables(FastNdct* p, int M, cudaStream_t s) {
+  const size_t n = p->n;
+  for (double** t : {&p->bes_wf, &p->bes_wt, &p->bes_tt}) {
+    if (p->async_alloc)
+      FLB_CUDA(cudaMallocAsync(t, (size_t)M * n * sizeof(double), s));
+    else
+      FLB_CUDA(cudaMalloc(t, (size_t)M * n * sizeof(double)));
+  }
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  switch (p->log2n) {
+#define FLB_BES(LG)                                                                        \
+  case LG:                                                                                 \
+    bessel_tables_kernel<LG><<<grid, 256, 0, s>>>(p->delta, M, p->bes_wf, p->bes_wt,       \
+                                                  p->bes_tt, p->swap);                     \
+    break;
+    FLB_BES(9) FLB_BES(10) FLB_BES(11) FLB_BES(12) FLB_BES(13)
+#undef FLB_BES
+  }
+  note_launch("bessel_tables_kernel");
+}
+
+FastNdct* fast_ndct_create(size_t n, double tol, int kind, const double* delta) {
   const int lg = log2_exact(n);
   if (lg < kFastMinLog2 || lg > kFastMaxLog2) return nullptr;
   const int L = cheb1_terms(tol);
   if (L < 0) return nullptr;
-  (void)kind;
   FastNdct* p = new FastNdct;
   p->n = n;
   p->log2n = lg;
   p->num_terms = L;
   FLB_CUDA(cudaMalloc(&p->owned_delta, n * sizeof(double)));
-  launch_reference_grid(n, FL_CHEB1, theta, nullptr, p->owned_delta, 0);
+  fast_delta_kernel<<<(unsigned)((n + 255) / 256), 256>>>(n, kind, delta, p->owned_delta, nullptr);
+  note_launch("fast_delta_kernel");
   p->delta = p->owned_delta;
 #ifndef FLB_NDCT_BESSEL
 #define FLB_NDCT_BESSEL 1
 #endif
+  // |N delta'| <= pi/4 + 1/(6 pi) = 0.83845 for Legendre nodes on either grid
+  // (the cheb1 bound of ndct.hpp:38-44): the term count of that bound
   const int M = bessel_terms(tol);
   if (FLB_NDCT_BESSEL && M > 0 && M < L) p->bes_terms = M;  // multi-pass: weights on the fly
-  if (FLB_NDCT_BESSEL && lg <= 13 && M > 0 && M < L) {
-    for (double** t : {&p->bes_wf, &p->bes_wt, &p->bes_tt})
-      FLB_CUDA(cudaMalloc(t, (size_t)M * n * sizeof(double)));
-    const unsigned grid = (unsigned)((n + 255) / 256);
-    switch (lg) {
-#define FLB_BES(LG) \
-  case LG: bessel_tables_kernel<LG><<<grid, 256>>>(p->delta, M, p->bes_wf, p->bes_wt, p->bes_tt); break;
-      FLB_BES(9) FLB_BES(10) FLB_BES(11) FLB_BES(12) FLB_BES(13)
-#undef FLB_BES
-    }
-    note_launch("bessel_tables_kernel");
+  if (FLB_NDCT_BESSEL && lg <= 13 && M > 0 && M < L) build_bessel_tables(p, M, 0);
+  return p;
+}
+
+FastNdct* fast_ndct_create_bessel(size_t n, int kind, const double* delta, int num_terms,
+                                  int swap, cudaStream_t s) {
+  const int lg = log2_exact(n);
+  if (lg < kFastMinLog2 || lg > kFastMaxLog2 || num_terms <= 0) return nullptr;
+  FastNdct* p = new FastNdct;
+  p->n = n;
+  p->log2n = lg;
+  p->swap = swap;
+  p->alloc_stream = s;
+  p->async_alloc = true;
+  unsigned long long* amax = nullptr;
+  FLB_CUDA(cudaMallocAsync(&p->owned_delta, n * sizeof(double), s));
+  FLB_CUDA(cudaMallocAsync(&amax, 2 * sizeof(unsigned long long), s));
+  FLB_CUDA(cudaMemsetAsync(amax, 0, 2 * sizeof(unsigned long long), s));
+  fast_delta_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, kind, delta, p->owned_delta,
+                                                                amax);
+  note_launch("fast_delta_kernel");
+  p->delta = p->owned_delta;
+  unsigned long long h[2];
+  FLB_CUDA(cudaMemcpyAsync(h, amax, sizeof h, cudaMemcpyDeviceToHost, s));
+  FLB_CUDA(cudaStreamSynchronize(s));
+  cudaFreeAsync(amax, s);
+  double dmax, ymax;
+  memcpy(&dmax, &h[0], 8);
+  memcpy(&ymax, &h[1], 8);
+  // eligible when the literal evaluation is exact to fp64 rounding: its
+  // truncation bound min((N max|delta|)^L / L!, C(L)) (ndct.hpp:147-155) at
+  // or below 2^-52, and delta not identically zero (delta = 0 keeps the
+  // literal path, bit-identical to dct_iii, test_ndct.cpp:112-125)
+  const double nd = (double)n, q = nd * dmax;
+  double node_bound = 1.0, grid_bound = 1.0;
+  const double qq = kind == FL_CHEB1 ? 0.83845 : 1.0 / (6.0 * kPi);
+  for (int l = 1; l <= num_terms; ++l) {
+    node_bound *= q / (double)l;
+    grid_bound *= qq / (double)l;
   }
+  const double eps52 = 2.220446049250313e-16;
+  const int M = bessel_terms_at(nd * ymax, eps52);
+  const bool literal_exact = std::min(node_bound, grid_bound) <= eps52;
+  const bool zero = delta != nullptr && dmax == 0.0;
+  if (!(literal_exact && !zero && M > 0 && std::isfinite(ymax))) {
+    fast_ndct_destroy(p);
+    return nullptr;
+  }
+  p->num_terms = M;
+  p->bes_terms = M;
+  if (lg <= 13) build_bessel_tables(p, M, s);
   return p;
 }
 
 void fast_ndct_destroy(FastNdct* p) {
   if (!p) return;
-  if (p->owned_delta) cudaFree(p->owned_delta);
-  for (double* t : {p->bes_wf, p->bes_wt, p->bes_tt})
-    if (t) cudaFree(t);
+  for (double* t : {p->owned_delta, p->bes_wf, p->bes_wt, p->bes_tt}) {
+    if (!t) continue;
+    if (p->async_alloc)
+      cudaFreeAsync(t, p->alloc_stream);
+    else
+      cudaFree(t);
+  }
   delete p;
 }
 
