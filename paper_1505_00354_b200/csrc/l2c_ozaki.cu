@@ -672,6 +672,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
     kb_lo = transpose ? 0 : (int)(rp * 2 * (BM / BK));
     const int kb_hi = transpose ? (int)((rp + 1) * 2 * (BM / BK)) : (int)(r / BK);
     nk = kb_hi - kb_lo;
+#ifdef FLB_OZ_DENSE_PROBE
+    kb_lo = 0;  // timing probe only: every K block (a dense product's work)
+    nk = (int)(r / BK);
+#endif
   };
 
   if (threadIdx.x == 0) {

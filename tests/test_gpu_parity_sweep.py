@@ -141,10 +141,13 @@ def test_c5_2_26_stages():
     The conversion (Toeplitz-Hankel) at >= 90 sampled rows of the reference
     loop (conversion.hpp:106-111 / :126-133) incl. k = 0..3 and N-4..N-1; the
     NDCT / NDCT^T of the transform's own stage inputs against the full-length
-    O(N log N) oracle (ndct.hpp:98-143 on the injected grid's cheb1 offsets:
-    the same nodes, the cheb1 Taylor terms -- both sides evaluate
-    sum_n c_n cos(n theta_k) to 2^-52 ||c||_1; a length-(2N+1) chebstar
-    oracle does not fit the test's time)."""
+    O(N log N) oracle (ndct.hpp:98-143). The reference's chebstar NDCT
+    evaluates at theta*_k + delta_k (its exact grid angle plus the fp64
+    offset); the oracle evaluates the same angles as cheb1 Taylor terms about
+    theta0_k with the offsets re-based exactly, delta_k + (N - 2k - 1) pi /
+    (2N(2N+1)) (|N delta'| <= 0.83845, the cheb1 bound, so L = 17 terms
+    reach 2^-52): power-of-two transforms instead of length-(2N+1) ones,
+    which do not fit the test's time at 2^26."""
     n = 1 << 26
     cfg = fl.TransformConfig(n)
     g = cfg.grid()
@@ -159,13 +162,16 @@ def test_c5_2_26_stages():
     rows_pool = ThreadPoolExecutor(4)  # 2^25-element temporaries per row
     ref = list(rows_pool.map(lambda k: NP.leg2cheb_rows(c, s, [k])[0], rows))
     assert np.max(np.abs(chat[rows] - ref)) <= t * sc
-    plan1 = fl.plan_ndct(g, fl.GridKind.cheb1, TOL)
-    d1 = np.asarray(plan1.reference.delta_theta)
+    plan = cfg.plan()
+    k = np.arange(n, dtype=np.float64)
+    d1 = np.asarray(plan.reference.delta_theta) + (n - 2.0 * k - 1.0) * (math.pi / (2.0 * n * (2.0 * n + 1.0)))
+    L1 = O.min_taylor_terms(CHEB1, TOL)
+    assert np.max(np.abs(d1)) * n <= 0.83845
     f = cfg.ndct(chat)
-    assert rel(f, NP.ndct_apply(chat, CHEB1, plan1.num_terms, d1), np.abs(chat).sum()) <= t
+    assert rel(f, NP.ndct_apply(chat, CHEB1, L1, d1), np.abs(chat).sum()) <= t
     wf = g.weights * f
     vt = cfg.ndct(wf, transpose=True)
-    assert rel(vt, NP.ndct_apply_transpose(wf, CHEB1, plan1.num_terms, d1), np.abs(wf).sum()) <= t
+    assert rel(vt, NP.ndct_apply_transpose(wf, CHEB1, L1, d1), np.abs(wf).sum()) <= t
     back = cfg.convert(vt, transpose=True)
     ref_t = list(rows_pool.map(lambda k: (k + 0.5) * NP.leg2cheb_transpose_rows(vt, s, [k])[0], rows))
     assert np.max(np.abs(back[rows] - ref_t)) <= t * np.abs(vt).sum()

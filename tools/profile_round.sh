@@ -18,15 +18,15 @@ ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline \
     > gpurun_out/ncu_launches.log 2>&1
 echo "launch list rc=$?"
-python tools/dbg_oz2.py 4096 8192 > gpurun_out/kern_small.log 2>&1 &&
+python tools/kernel_probe.py dlt 4096 8192 3 > gpurun_out/kern_small.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:"fast_ndct_fwd|oz_gemm2|oz_split_b" -s 3 -c 3 \
-    -o gpurun_out/hot_full python tools/dbg_oz2.py 4096 8192 > gpurun_out/ncu_full.log 2>&1
+    -o gpurun_out/hot_full python tools/kernel_probe.py dlt 4096 8192 3 > gpurun_out/ncu_full.log 2>&1
 echo "ncu full rc=$?"
 python tools/dct_probe.py > gpurun_out/dct_probe.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:fast_dct_stream -s 2 -c 1 \
     -o gpurun_out/dct_full python tools/dct_probe.py > gpurun_out/dct_ncu.log 2>&1
 echo "ncu dct rc=$?"
-python tools/idlt_probe.py 16384 > gpurun_out/idlt_probe.log 2>&1 &&
+python tools/kernel_probe.py ndct_t 4096 16384 2 > gpurun_out/idlt_probe.log 2>&1 &&
 ncu --set full --clock-control none --import-source on -k regex:fast_ndct_tr -s 1 -c 1 \
-    -o gpurun_out/tr_full python tools/idlt_probe.py 16384 > gpurun_out/tr_ncu.log 2>&1
+    -o gpurun_out/tr_full python tools/kernel_probe.py ndct_t 4096 16384 2 > gpurun_out/tr_ncu.log 2>&1
 echo "ncu tr rc=$?"
