@@ -189,6 +189,29 @@ enum { FL_GEMM_FP64 = 0, FL_GEMM_INT8_SPLIT = 1 };
 fl_status fl_plan_set_gemm_mode(fl_plan* plan, int mode);
 int fl_plan_gemm_mode(const fl_plan* plan);
 
+/* How dlt / idlt evaluate (transforms.hpp:42-64):
+ *   0 = FL_DLT_FACTORED : the reference's factorisation, f = NDCT(M c) and
+ *                         c = D_s M^T NDCT^T(D_w f) (conversion + NDCT);
+ *   1 = FL_DLT_DIRECT   : the same transform as one dense product per parity,
+ *       f = P c and c = D_s P^T D_w f with P_kn = P_n(cos theta_k) evaluated
+ *       (double-double, once per plan) at the reference's angles
+ *       theta*_kind(k) + delta_k, on the int8 tcgen05 tensor cores with the
+ *       split arithmetic of FL_GEMM_INT8_SPLIT (exact digit products, fp64
+ *       recombination). The parity split (P_n(-x) = (-1)^n P_n(x)) halves
+ *       it: 2 (N/2)^2 MACs per column, N^2/2 -- against the factored path's
+ *       N^2/4 conversion plus the ~14-term NDCT, which it beats for
+ *       N <= 8192 on B200 (the paper's own direct/fast crossover is
+ *       N ~ 5000).
+ * FL_DLT_DIRECT (default) applies to n a multiple of 256 in [512, 8192],
+ * more than 16 columns and FL_GEMM_INT8_SPLIT; everything else is factored.
+ * A non-finite input column raises invalid_argument with the factored
+ * path's message (ndct_apply[_transpose]: non-finite input).
+ * fl_plan_uses_direct tells which one a call with `batch` columns takes. */
+enum { FL_DLT_FACTORED = 0, FL_DLT_DIRECT = 1 };
+fl_status fl_plan_set_dlt_method(fl_plan* plan, int method);
+int fl_plan_dlt_method(const fl_plan* plan);
+int fl_plan_uses_direct(const fl_plan* plan, size_t batch);
+
 /* The plan's conversion step alone, exactly as dlt/idlt run it (same
  * leg2cheb / gemm mode selection): out = M in (transpose = 0, the first step
  * of transforms.hpp:47) or (m + 1/2) M^T in (transpose = 1, the last step of

@@ -19,6 +19,7 @@ DCT_III, DST_III, DCT_III_T, DST_III_T = range(4)
 NDCT_LITERAL, NDCT_FAST = 0, 1
 LEG2CHEB_DIRECT, LEG2CHEB_FAST = 0, 1
 GEMM_FP64, GEMM_INT8_SPLIT = 0, 1
+DLT_FACTORED, DLT_DIRECT = 0, 1
 
 
 class FastlegError(Exception):
@@ -65,7 +66,7 @@ EXPORTS = [
     "fl_cheb_coeffs_of_legendre", "fl_plan_set_leg2cheb_mode", "fl_plan_leg2cheb_rank",
     "fl_plan_stage_terms", "fl_dlt_stage", "fl_plan_set_gemm_mode", "fl_plan_gemm_mode",
     "fl_plan_leg2cheb", "fl_plan_ndct", "fl_plan_ndct_terms", "fl_set_free_ndct_mode",
-    "fl_free_ndct_mode",
+    "fl_free_ndct_mode", "fl_plan_set_dlt_method", "fl_plan_dlt_method", "fl_plan_uses_direct",
 ]
 
 
@@ -118,6 +119,9 @@ def _load() -> C.CDLL:
         "fl_plan_ndct_terms": (i, [vp]),
         "fl_set_free_ndct_mode": (i, [i]),
         "fl_free_ndct_mode": (i, []),
+        "fl_plan_set_dlt_method": (i, [vp, i]),
+        "fl_plan_dlt_method": (i, [vp]),
+        "fl_plan_uses_direct": (i, [vp, sz]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

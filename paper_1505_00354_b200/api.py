@@ -425,6 +425,18 @@ class TransformConfig:  # transforms.hpp:19-38
     def gemm_mode(self) -> int:
         return int(LIB.fl_plan_gemm_mode(self._h))
 
+    def set_dlt_method(self, method: int) -> None:
+        """DLT_DIRECT (default: one dense split-int8 product per parity,
+        f = P c, for n % 256 == 0, 512 <= n <= 8192, > 16 columns) or
+        DLT_FACTORED (the reference's conversion + NDCT)."""
+        check(LIB.fl_plan_set_dlt_method(self._h, int(method)))
+
+    def dlt_method(self) -> int:
+        return int(LIB.fl_plan_dlt_method(self._h))
+
+    def uses_direct(self, batch: int) -> bool:
+        return bool(LIB.fl_plan_uses_direct(self._h, int(batch)))
+
     def grid(self) -> LegendreGrid:
         if self._grid is None:
             n = self.size()

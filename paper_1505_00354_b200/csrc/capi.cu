@@ -453,6 +453,8 @@ struct fl_plan {
   int l2c_mode = 1;          // 1: fast conversion for few columns when available; 0: direct
   int gemm_mode = FL_GEMM_INT8_SPLIT;  // arithmetic of the direct conversion product
   L2COzaki* oz[2] = {nullptr, nullptr};  // split-int8 slices of M, (m + 1/2) M^T (lazy)
+  int dlt_method = FL_DLT_DIRECT;        // dlt/idlt: dense product where supported
+  L2COzaki* dense[2] = {nullptr, nullptr};  // split-int8 slices of P, (m + 1/2) P^T (lazy)
   std::mutex mu;
 };
 
@@ -464,6 +466,7 @@ void plan_free(fl_plan* p) {
   if (p->fast) fast_ndct_destroy(p->fast);
   if (p->l2c) l2c_fast_destroy(p->l2c);
   for (L2COzaki* o : p->oz) l2c_ozaki_destroy(o);
+  for (L2COzaki* o : p->dense) l2c_ozaki_destroy(o);
   delete p;
 }
 
@@ -496,6 +499,23 @@ const L2COzaki* plan_ozaki(fl_plan* p, int transpose, size_t batch, cudaStream_t
     p->oz[transpose] = oz;
   }
   return p->oz[transpose];
+}
+
+// The direct product for this call (fl_dlt: P, fl_idlt: (m + 1/2) P^T), or
+// null (factored path): > 16 columns, the int8-split arithmetic, n a
+// multiple of 256 in [512, 8192]. Built once per plan and direction, on
+// first use, published after its digits are complete (as plan_ozaki).
+const L2COzaki* plan_dense(fl_plan* p, int idlt, size_t batch, cudaStream_t s) {
+  if (p->dlt_method != FL_DLT_DIRECT || p->gemm_mode != FL_GEMM_INT8_SPLIT || batch <= 16 ||
+      !l2c_dense_supported(p->n))
+    return nullptr;
+  std::lock_guard<std::mutex> lock(p->mu);
+  if (!p->dense[idlt]) {
+    L2COzaki* d = l2c_dense_create(p->n, p->kind, p->delta, idlt, s);
+    FLB_CUDA(cudaStreamSynchronize(s));
+    p->dense[idlt] = d;
+  }
+  return p->dense[idlt];
 }
 
 // The plan's conversion product (transforms.hpp:47 / :62): chat = M in, or
@@ -929,6 +949,24 @@ fl_status fl_plan_set_gemm_mode(fl_plan* p, int mode) {
 
 int fl_plan_gemm_mode(const fl_plan* p) { return p ? p->gemm_mode : -1; }
 
+fl_status fl_plan_set_dlt_method(fl_plan* p, int method) {
+  return guarded([&] {
+    if (!p) fail(FL_INVALID_ARGUMENT, "plan: null");
+    if (method != FL_DLT_FACTORED && method != FL_DLT_DIRECT)
+      fail(FL_INVALID_ARGUMENT, "plan: unknown dlt method");
+    p->dlt_method = method;
+  });
+}
+
+int fl_plan_dlt_method(const fl_plan* p) { return p ? p->dlt_method : -1; }
+
+int fl_plan_uses_direct(const fl_plan* p, size_t batch) {
+  return p && p->dlt_method == FL_DLT_DIRECT && p->gemm_mode == FL_GEMM_INT8_SPLIT && batch > 16 &&
+                 l2c_dense_supported(p->n)
+             ? 1
+             : 0;
+}
+
 int fl_plan_leg2cheb_rank(const fl_plan* p, int parity) {
   if (!p || !p->l2c || parity < 0 || parity > 1) return 0;
   return l2c_fast_rank(*p->l2c, parity);
@@ -945,6 +983,28 @@ fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, 
     cudaStream_t s = as_stream(stream);
     const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
     fl_plan* mp = const_cast<fl_plan*>(p);
+    // the direct product (P c on the int8 tensor cores) where it applies
+    if (const L2COzaki* dense = plan_dense(mp, 0, batch, s)) {
+      if (pipeline_ok(in, out, n, batch)) {
+        run_pipelined(p->device, n, in, out, batch, ld, s, "ndct_apply",
+                      [&](const double* di, double* dq, size_t cols, int* flag, cudaStream_t cs) {
+                        l2c_dense_apply(*dense, di, n, nullptr, dq, n, cols, flag, cs);
+                      });
+        return;
+      }
+      DevIn i(in, n, batch, ld, s);
+      DevOut o(out, n, batch, ld, s);
+      DevScratch<int> flag(1, s);
+      FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+      l2c_dense_apply(*dense, i.ptr, i.ld, nullptr, o.ptr, o.ld, batch, flag.p, s);
+      o.finish();
+      int h = 0;
+      FLB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      sync(s);
+      // the reference raises on the non-finite conversion output (ndct.hpp:79-91)
+      if (h) fail(FL_INVALID_ARGUMENT, "ndct_apply: non-finite input");
+      return;
+    }
     if (pipeline_ok(in, out, n, batch) && !overflow_guard(n, p->num_terms)) {
       run_pipelined(p->device, n, in, out, batch, ld, s, "ndct_apply",
                     [&](const double* di, double* dq, size_t cols, int* flag, cudaStream_t cs) {
@@ -995,6 +1055,26 @@ fl_status fl_idlt(const fl_plan* p, const double* in, double* out, size_t batch,
     cudaStream_t s = as_stream(stream);
     const FastNdct* fast = (p->mode == FL_NDCT_FAST) ? p->fast : nullptr;
     fl_plan* mp = const_cast<fl_plan*>(p);
+    if (const L2COzaki* dense = plan_dense(mp, 1, batch, s)) {
+      if (pipeline_ok(in, out, n, batch)) {
+        run_pipelined(p->device, n, in, out, batch, ld, s, "ndct_apply_transpose",
+                      [&](const double* di, double* dq, size_t cols, int* flag, cudaStream_t cs) {
+                        l2c_dense_apply(*dense, di, n, p->w, dq, n, cols, flag, cs);
+                      });
+        return;
+      }
+      DevIn i(in, n, batch, ld, s);
+      DevOut o(out, n, batch, ld, s);
+      DevScratch<int> flag(1, s);
+      FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+      l2c_dense_apply(*dense, i.ptr, i.ld, p->w, o.ptr, o.ld, batch, flag.p, s);
+      o.finish();
+      int h = 0;
+      FLB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      sync(s);
+      if (h) fail(FL_INVALID_ARGUMENT, "ndct_apply_transpose: non-finite input");
+      return;
+    }
     if (pipeline_ok(in, out, n, batch) && !overflow_guard(n, p->num_terms)) {
       run_pipelined(p->device, n, in, out, batch, ld, s, "ndct_apply_transpose",
                     [&](const double* di, double* dq, size_t cols, int* flag, cudaStream_t cs) {

@@ -87,7 +87,7 @@ constexpr uint32_t IDESC = (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(BN >
 
 struct L2COzaki {
   size_t n = 0, r = 0;       // r = n / 2 rows (and K) per parity
-  int transpose = 0;
+  int mode = 0;              // kMode* (the product the A digits hold)
   int8_t* a = nullptr;       // [S][2][r][r] digits, K-major rows
   double* arow = nullptr;    // [2][r] row scales 2^ea
   CUtensorMap tmap_a;
@@ -294,7 +294,8 @@ template <int EPT>
 __global__ void __launch_bounds__(1024) oz_split_b_kernel(const double* __restrict__ in, size_t n,
                                                           size_t ld, size_t cols,
                                                           int8_t* __restrict__ b,
-                                                          double* __restrict__ bcol) {
+                                                          double* __restrict__ bcol,
+                                                          int* nonfinite) {
   using W = typename std::conditional<EPT == 16, uint64_t, uint32_t>::type;  // EPT/2 digits
   constexpr int H = EPT / 2;
   const size_t col = blockIdx.x;
@@ -333,6 +334,7 @@ __global__ void __launch_bounds__(1024) oz_split_b_kernel(const double* __restri
     e_sh[threadIdx.x] = split_exp(m);
     bcol[threadIdx.x * cols + col] = bad_sh ? __longlong_as_double(0x7ff8000000000000ll)
                                             : ldexp(1.0, e_sh[threadIdx.x]);
+    if (bad_sh && nonfinite && threadIdx.x == 0) atomicOr(nonfinite, 1);
   }
   __syncthreads();
   const int e0 = e_sh[0], e1 = e_sh[1];
@@ -357,7 +359,248 @@ __global__ void __launch_bounds__(1024) oz_split_b_kernel(const double* __restri
   }
 }
 
+// ---- the direct (dense) Legendre product ----------------------------------
+// Plan-time table P_n(x_k), k < N/2, n < N, at the angles the reference
+// evaluates: theta_k = theta*_kind(k) + delta_k (its exact grid angle plus the
+// fp64 node offset, ndct.hpp:98-117 / quadrature.hpp:147-158), in
+// double-double: the angle, cos by Taylor series at theta/64 and six double
+// angle steps, and the three-term recurrence (oracle.hpp:19-48's order
+// restated in dd), each entry rounded once to fp64. Layout [n][k] (the
+// threads of a warp are consecutive nodes).
+struct dd {
+  double hi, lo;
+};
+__device__ __forceinline__ dd dd_two_sum(double a, double b) {
+  const double s = a + b, bb = s - a;
+  return {s, (a - (s - bb)) + (b - bb)};
+}
+__device__ __forceinline__ dd dd_fast(double a, double b) {
+  const double s = a + b;
+  return {s, b - (s - a)};
+}
+__device__ __forceinline__ dd dd_add(dd a, dd b) {
+  dd s = dd_two_sum(a.hi, b.hi);
+  const dd t = dd_two_sum(a.lo, b.lo);
+  s.lo += t.hi;
+  s = dd_fast(s.hi, s.lo);
+  s.lo += t.lo;
+  return dd_fast(s.hi, s.lo);
+}
+__device__ __forceinline__ dd dd_mul(dd a, dd b) {
+  const double p = a.hi * b.hi;
+  double e = fma(a.hi, b.hi, -p);
+  e += a.hi * b.lo + a.lo * b.hi;
+  return dd_fast(p, e);
+}
+__device__ __forceinline__ dd dd_mul_d(dd a, double b) {
+  const double p = a.hi * b;
+  double e = fma(a.hi, b, -p);
+  e += a.lo * b;
+  return dd_fast(p, e);
+}
+__device__ __forceinline__ dd dd_div_d(dd a, double b) {
+  const double q1 = a.hi / b;
+  const double p = q1 * b, pe = fma(q1, b, -p);
+  double r = (a.hi - p) - pe + a.lo;
+  return dd_fast(q1, r / b);
+}
+
+__global__ void legendre_table_kernel(size_t n, int kind, const double* __restrict__ delta,
+                                      double* __restrict__ table) {
+  const size_t r = n / 2;
+  const size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (k >= r) return;
+  const dd pi = {kPiHi, kPiLo};
+  // theta*_k: (4k + 3) pi / (4N + 2) (chebstar) or (2k + 1) pi / (2N) (cheb1)
+  dd th = kind == FL_CHEBSTAR ? dd_div_d(dd_mul_d(pi, 4.0 * (double)k + 3.0), 4.0 * (double)n + 2.0)
+                              : dd_div_d(dd_mul_d(pi, 2.0 * (double)k + 1.0), 2.0 * (double)n);
+  th = dd_add(th, dd{delta[k], 0.0});
+  // cos / sin of theta / 64 by their Taylor series (|t| < 0.025: 10 terms
+  // reach 1e-40), then six double-angle steps
+  const dd t = {ldexp(th.hi, -6), ldexp(th.lo, -6)};
+  const dd t2 = dd_mul(t, t);
+  dd c = {1.0, 0.0}, sn = t, tc = {1.0, 0.0}, ts = t;
+  for (int i = 1; i <= 10; ++i) {
+    tc = dd_div_d(dd_mul(tc, t2), -(double)((2 * i - 1) * (2 * i)));
+    ts = dd_div_d(dd_mul(ts, t2), -(double)((2 * i) * (2 * i + 1)));
+    c = dd_add(c, tc);
+    sn = dd_add(sn, ts);
+  }
+  for (int i = 0; i < 6; ++i) {
+    const dd c2 = dd_add(dd_mul(c, c), dd_mul(dd{-sn.hi, -sn.lo}, sn));
+    sn = dd_mul_d(dd_mul(sn, c), 2.0);
+    c = c2;
+  }
+  const dd x = c;
+  // P_0 = 1, P_1 = x, (m + 1) P_{m+1} = (2m + 1) x P_m - m P_{m-1}
+  dd pm1 = {1.0, 0.0}, pm = x;
+  table[k] = 1.0;
+  if (n > 1) table[r + k] = x.hi;
+  for (size_t m = 1; m + 1 < n; ++m) {
+    const dd a = dd_mul_d(dd_mul(x, pm), 2.0 * (double)m + 1.0);
+    const dd b = dd_mul_d(pm1, -(double)m);
+    const dd nx = dd_div_d(dd_add(a, b), (double)(m + 1));
+    pm1 = pm;
+    pm = nx;
+    table[(m + 1) * r + k] = pm.hi;
+  }
+}
+
+// Entry of the dense parity-p block (table[n][k] = P_n(x_k)).
+__device__ __forceinline__ double dense_entry(const double* __restrict__ table, size_t r, int idlt,
+                                              int p, size_t row, size_t col) {
+  if (!idlt) return table[(2 * col + p) * r + row];  // P_{2b+p}(x_a)
+  const size_t deg = 2 * row + p;
+  return ((double)deg + 0.5) * table[deg * r + col];  // (n + 1/2) P_n(x_b)
+}
+
+// One CTA per (parity, row): row scale and the S digit rows of the dense A.
+__global__ void __launch_bounds__(256) oz_split_a_dense_kernel(const double* __restrict__ table,
+                                                               size_t r, int idlt,
+                                                               int8_t* __restrict__ a,
+                                                               double* __restrict__ arow) {
+  const int p = blockIdx.y;
+  const size_t row = blockIdx.x;
+  __shared__ double red[8];
+  __shared__ int e_sh;
+  double mx = 0.0;
+  for (size_t c = threadIdx.x; c < r; c += blockDim.x)
+    mx = fmax(mx, fabs(dense_entry(table, r, idlt, p, row, c)));
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = mx;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double m = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, red[w]);
+    e_sh = split_exp(m);
+    arow[p * r + row] = ldexp(1.0, e_sh);
+  }
+  __syncthreads();
+  const int e = e_sh;
+  for (size_t c = threadIdx.x; c < r; c += blockDim.x) {
+    int8_t d[oz::S];
+    split_digits(dense_entry(table, r, idlt, p, row, c), e, d);
+#pragma unroll
+    for (int j = 0; j < oz::S; ++j) a[((size_t)(j * 2 + p) * r + row) * r + c] = d[j];
+  }
+}
+
+// The direct IDLT's B operand, one CTA of r / H threads per column: entries
+// b = t + i T (i < H) of u_p[b] = w_b (f_b + (-1)^p f_{N-1-b}), per-parity
+// scales and the S digit slices ([S][2][cols][r], as oz_split_b_kernel).
+template <int H>
+__global__ void __launch_bounds__(1024) oz_split_b_sym_kernel(const double* __restrict__ in,
+                                                              size_t n, size_t ld, size_t cols,
+                                                              const double* __restrict__ w,
+                                                              int8_t* __restrict__ b,
+                                                              double* __restrict__ bcol,
+                                                              int* nonfinite) {
+  const size_t col = blockIdx.x;
+  const size_t r = n / 2;
+  const size_t T = blockDim.x;
+  const size_t t = threadIdx.x;
+  __shared__ double red[2][32];
+  __shared__ int e_sh[2];
+  __shared__ int bad_sh;
+  if (threadIdx.x == 0) bad_sh = 0;
+  const double* f = in + col * ld;
+  double u0[H], u1[H];
+  double mx0 = 0.0, mx1 = 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const size_t bi = t + i * T;
+    const double wv = w[bi];
+    const double fa = __ldcs(f + bi), fb = __ldcs(f + (n - 1 - bi));
+    const double ga = wv * fa, gb = wv * fb;  // the weighted values (transforms.hpp:59)
+    bad |= !isfinite(ga) || !isfinite(gb);
+    u0[i] = ga + gb;
+    u1[i] = ga - gb;
+    mx0 = fmax(mx0, fabs(u0[i]));
+    mx1 = fmax(mx1, fabs(u1[i]));
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx0 = fmax(mx0, __shfl_xor_sync(0xffffffffu, mx0, o));
+    mx1 = fmax(mx1, __shfl_xor_sync(0xffffffffu, mx1, o));
+  }
+  __syncthreads();
+  if (bad) atomicOr(&bad_sh, 1);
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = mx0;
+    red[1][threadIdx.x >> 5] = mx1;
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    double m = 0.0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) m = fmax(m, red[threadIdx.x][q]);
+    e_sh[threadIdx.x] = split_exp(m);
+    bcol[threadIdx.x * cols + col] = bad_sh ? __longlong_as_double(0x7ff8000000000000ll)
+                                            : ldexp(1.0, e_sh[threadIdx.x]);
+    if (bad_sh && nonfinite && threadIdx.x == 0) atomicOr(nonfinite, 1);
+  }
+  __syncthreads();
+  const int e0 = e_sh[0], e1 = e_sh[1];
+#pragma unroll
+  for (int i = 0; i < H; ++i) {
+    const size_t bi = t + i * T;
+    int8_t d0[oz::S], d1[oz::S];
+    split_digits(isfinite(u0[i]) ? u0[i] : 0.0, e0, d0);
+    split_digits(isfinite(u1[i]) ? u1[i] : 0.0, e1, d1);
+#pragma unroll
+    for (int j = 0; j < oz::S; ++j) {
+      b[((size_t)(j * 2 + 0) * cols + col) * r + bi] = d0[j];
+      b[((size_t)(j * 2 + 1) * cols + col) * r + bi] = d1[j];
+    }
+  }
+}
+
 // ---- the split GEMM ------------------------------------------------------
+// Products the GEMM kernels compute (per parity p, rows a < r = N/2, K = r):
+//   kModeTri / kModeTriT : the conversion M (upper-triangular parity blocks)
+//                          or (m + 1/2) M^T (lower); output row 2a + p
+//   kModeDenseDlt        : the direct DLT, A_p[a][b] = P_{2b+p}(x_a) (node a,
+//                          degree 2b + p): E = A_0 c_even, O = A_1 c_odd, and
+//                          f_a = E_a + O_a, f_{N-1-a} = E_a - O_a
+//                          (P_n(-x) = (-1)^n P_n(x), x_{N-1-a} = -x_a)
+//   kModeDenseIdlt       : the direct IDLT, A_p[a][b] = (n + 1/2) P_n(x_b),
+//                          n = 2a + p, against u_p[b] = w_b (f_b + (-1)^p
+//                          f_{N-1-b}); output row 2a + p
+enum { kModeTri = 0, kModeTriT = 1, kModeDenseDlt = 2, kModeDenseIdlt = 3 };
+
+// Epilogue store of one output row (a = tile row) over the tile's BN columns.
+// Dense DLT: the parity-0 tile stores E_a at row a; the parity-1 tile of the
+// same unit runs next on the same thread, reads E_a back (its own store, L2)
+// and writes f_a = E_a + O_a and f_{N-1-a} = E_a - O_a.
+__device__ __forceinline__ void store_tile(double* __restrict__ out, const double* acc,
+                                           double ascale, const double* __restrict__ bcol,
+                                           int mode, int p, size_t a, size_t cb, size_t r,
+                                           size_t cols, size_t ld) {
+  using namespace oz;
+  if (mode == kModeDenseDlt) {
+#pragma unroll
+    for (int c = 0; c < BN; ++c) {
+      const size_t col = cb * BN + c;
+      if (col >= cols) continue;
+      const double v = (acc[c] * ascale) * bcol[(size_t)p * cols + col];
+      double* o = out + col * ld;
+      if (p == 0) {
+        o[a] = v;
+      } else {
+        const double e = o[a];
+        o[a] = e + v;
+        o[2 * r - 1 - a] = e - v;
+      }
+    }
+    return;
+  }
+  const size_t k = 2 * a + p;  // output row (interleaved parities)
+#pragma unroll
+  for (int c = 0; c < BN; ++c) {
+    const size_t col = cb * BN + c;
+    if (col < cols) out[col * ld + k] = (acc[c] * ascale) * bcol[(size_t)p * cols + col];
+  }
+}
+
 // Persistent: CTA b takes tiles b, b + grid, ... (consecutive CTAs share a
 // column block, so the B digits are reused from L2). The smem ring and its
 // phases run continuously across tiles; the epilogue drains the 8 TMEM
@@ -367,7 +610,7 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
     oz_gemm_kernel(const __grid_constant__ CUtensorMap tmap_a,
                    const __grid_constant__ CUtensorMap tmap_b, const double* __restrict__ arow,
                    const double* __restrict__ bcol, double* __restrict__ out, size_t r,
-                   size_t cols, size_t ld, int transpose, size_t ntiles) {
+                   size_t cols, size_t ld, int mode, size_t ntiles) {
   using namespace oz;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
@@ -382,15 +625,26 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t rb_count = r / BM;
+  const int transpose = mode == kModeTriT;
   auto tile_coords = [&](size_t tile, size_t& cb, int& p, size_t& rb, int& kb_lo, int& nk) {
     cb = tile / (2 * rb_count);
     p = (int)(tile % 2);
     rb = (tile / 2) % rb_count;
     // K blocks (of BK) with nonzero entries: on/above (forward) or on/below
-    // (transpose) the diagonal block
-    kb_lo = transpose ? 0 : (int)(rb * (BM / BK));
-    const int kb_hi = transpose ? (int)((rb + 1) * (BM / BK)) : (int)(r / BK);
+    // (transpose) the diagonal block; all of them for the dense products
+    kb_lo = (transpose || mode >= kModeDenseDlt) ? 0 : (int)(rb * (BM / BK));
+    const int kb_hi = mode >= kModeDenseDlt ? (int)(r / BK)
+                      : transpose         ? (int)((rb + 1) * (BM / BK))
+                                          : (int)(r / BK);
     nk = kb_hi - kb_lo;
+  };
+  // units of (column block, row block), both parities back to back on the
+  // same CTA (the dense DLT's epilogue combines them)
+  const size_t units = ntiles / 2;
+  auto tile_of = [&](size_t i, size_t& tile) -> bool {
+    const size_t u = blockIdx.x + (i >> 1) * gridDim.x;
+    tile = 2 * u + (i & 1);
+    return u < units;
   };
 
   if (threadIdx.x == 0) {
@@ -412,7 +666,8 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
       uint32_t it = 0;
-      for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      size_t tile;
+      for (size_t ti = 0; tile_of(ti, tile); ++ti) {
         size_t cb, rb;
         int p, kb_lo, nk;
         tile_coords(tile, cb, p, rb, kb_lo, nk);
@@ -435,7 +690,8 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
     {  // MMA issuer: the whole warp, one elected lane issues
       uint32_t it = 0, t = 0, aslot = 0;
       (void)aslot;
-      for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+      size_t tile;
+      for (size_t ti = 0; tile_of(ti, tile); ++ti, ++t) {
         size_t cb, rb;
         int p, kb_lo, nk;
         tile_coords(tile, cb, p, rb, kb_lo, nk);
@@ -495,7 +751,8 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     uint32_t t = 0;
-    for (size_t tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++t) {
+    size_t tile;
+    for (size_t ti = 0; tile_of(ti, tile); ++ti, ++t) {
       size_t cb, rb;
       int p, kb_lo, nk;
       tile_coords(tile, cb, p, rb, kb_lo, nk);
@@ -527,12 +784,7 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
       tc_fence_before();
       mbar_arrive(smem_u32(tempty_b));  // TMEM free for the next tile
       const double ascale = arow[(size_t)p * r + rb * BM + row];
-      const size_t k = 2 * (rb * BM + row) + p;  // output row (interleaved parities)
-#pragma unroll
-      for (int c = 0; c < BN; ++c) {
-        const size_t col = cb * BN + c;
-        if (col < cols) out[col * ld + k] = (acc[c] * ascale) * bcol[(size_t)p * cols + col];
-      }
+      store_tile(out, acc, ascale, bcol, mode, p, rb * BM + row, cb, r, cols, ld);
     }
   }
   __syncthreads();
@@ -643,7 +895,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
     oz_gemm2_kernel(const __grid_constant__ CUtensorMap tmap_a,
                     const __grid_constant__ CUtensorMap tmap_b, const double* __restrict__ arow,
                     const double* __restrict__ bcol, double* __restrict__ out, size_t r,
-                    size_t cols, size_t ld, int transpose, size_t ntiles) {
+                    size_t cols, size_t ld, int mode, size_t ntiles) {
   using namespace oz;
   using oz2::A_TILE;
   using oz2::B_TILE;
@@ -664,18 +916,24 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
   const bool leader = rank == 0;
   const size_t pairs = (r / BM) / 2;  // 256-row blocks
   const size_t cluster_id = blockIdx.x / 2, nclusters = gridDim.x / 2;
+  const int transpose = mode == kModeTriT;
   auto tile_coords = [&](size_t tile, size_t& cb, int& p, size_t& rp, int& kb_lo, int& nk) {
     cb = tile / (2 * pairs);
     p = (int)(tile % 2);
     rp = (tile / 2) % pairs;
-    // K blocks with nonzero entries for either 128-row block of the pair
-    kb_lo = transpose ? 0 : (int)(rp * 2 * (BM / BK));
-    const int kb_hi = transpose ? (int)((rp + 1) * 2 * (BM / BK)) : (int)(r / BK);
+    // K blocks with nonzero entries for either 128-row block of the pair (all
+    // of them for the dense products)
+    kb_lo = (transpose || mode >= kModeDenseDlt) ? 0 : (int)(rp * 2 * (BM / BK));
+    const int kb_hi = mode >= kModeDenseDlt ? (int)(r / BK)
+                      : transpose         ? (int)((rp + 1) * 2 * (BM / BK))
+                                          : (int)(r / BK);
     nk = kb_hi - kb_lo;
-#ifdef FLB_OZ_DENSE_PROBE
-    kb_lo = 0;  // timing probe only: every K block (a dense product's work)
-    nk = (int)(r / BK);
-#endif
+  };
+  const size_t units = ntiles / 2;  // both parities of a unit back to back (see oz_gemm_kernel)
+  auto tile_of = [&](size_t i, size_t& tile) -> bool {
+    const size_t u = cluster_id + (i >> 1) * nclusters;
+    tile = 2 * u + (i & 1);
+    return u < units;
   };
 
   if (threadIdx.x == 0) {
@@ -701,7 +959,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
   if (warp == 0) {
     if (lane == 0) {  // TMA producer (both CTAs)
       uint32_t it = 0;
-      for (size_t tile = cluster_id; tile < ntiles; tile += nclusters) {
+      size_t tile;
+      for (size_t ti = 0; tile_of(ti, tile); ++ti) {
         size_t cb, rp;
         int p, kb_lo, nk;
         tile_coords(tile, cb, p, rp, kb_lo, nk);
@@ -729,7 +988,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
     if (leader) {  // MMA issuer: the leader's whole warp, one elected lane issues
       uint32_t it = 0, t = 0, aslot = 0;
       (void)aslot;
-      for (size_t tile = cluster_id; tile < ntiles; tile += nclusters, ++t) {
+      size_t tile;
+      for (size_t ti = 0; tile_of(ti, tile); ++ti, ++t) {
         size_t cb, rp;
         int p, kb_lo, nk;
         tile_coords(tile, cb, p, rp, kb_lo, nk);
@@ -797,7 +1057,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
     const int row = q * 32 + lane;
     const uint32_t tempty_leader = map_to_rank(smem_u32(tempty_b), 0);
     uint32_t t = 0;
-    for (size_t tile = cluster_id; tile < ntiles; tile += nclusters, ++t) {
+    size_t tile;
+    for (size_t ti = 0; tile_of(ti, tile); ++ti, ++t) {
       size_t cb, rp;
       int p, kb_lo, nk;
       tile_coords(tile, cb, p, rp, kb_lo, nk);
@@ -829,12 +1090,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
       tc_fence_before();
       mbar_arrive_remote(tempty_leader);  // TMEM free for the pair's next tile
       const double ascale = arow[(size_t)p * r + rb * BM + row];
-      const size_t k = 2 * (rb * BM + row) + p;
-#pragma unroll
-      for (int c = 0; c < BN; ++c) {
-        const size_t col = cb * BN + c;
-        if (col < cols) out[col * ld + k] = (acc[c] * ascale) * bcol[(size_t)p * cols + col];
-      }
+      store_tile(out, acc, ascale, bcol, mode, p, rb * BM + row, cb, r, cols, ld);
     }
   }
   tc_fence_before();
@@ -883,7 +1139,7 @@ L2COzaki* l2c_ozaki_create(size_t n, const double* s, int transpose, int scale_h
   auto* p = new L2COzaki;
   p->n = n;
   p->r = n / 2;
-  p->transpose = transpose;
+  p->mode = transpose;  // kModeTri / kModeTriT
   const size_t r = p->r;
   FLB_CUDA(cudaMalloc(&p->a, (size_t)oz::S * 2 * r * r));
   FLB_CUDA(cudaMalloc(&p->arow, 2 * r * sizeof(double)));
@@ -900,6 +1156,41 @@ void l2c_ozaki_destroy(L2COzaki* p) {
   cudaFree(p->arow);
   delete p;
 }
+
+namespace {
+
+// The split GEMM over prepared B digits ([S][2][cols][r]) and column scales.
+void launch_gemm(const L2COzaki& p, const int8_t* b, const double* bcol, double* out, size_t cols,
+                 size_t ld, cudaStream_t st) {
+  const size_t r = p.r;
+  const CUtensorMap tmap_b = make_map(b, r, cols, 2 * oz::S, oz::BN);
+  // the attribute is per device context: set it on every call (the library
+  // serves several devices in one process)
+  FLB_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                oz::SMEM));
+#ifndef FLB_OZ_PAIR
+#define FLB_OZ_PAIR 1
+#endif
+  if (FLB_OZ_PAIR && (r / oz::BM) % 2 == 0) {
+    // SM pairs: tiles of 256 rows x 64 columns, B staged as two 32-column halves
+    const CUtensorMap tmap_b2 = make_map(b, r, cols, 2 * oz::S, oz::BN / 2);
+    FLB_CUDA(cudaFuncSetAttribute(oz_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  oz2::SMEM));
+    const size_t tiles = 2 * (r / oz::BM / 2) * ((cols + oz::BN - 1) / oz::BN);
+    const unsigned clusters = (unsigned)std::min<size_t>(tiles / 2, (size_t)sm_count() / 2);
+    oz_gemm2_kernel<<<2 * clusters, oz::THREADS, oz2::SMEM, st>>>(
+        p.tmap_a, tmap_b2, p.arow, bcol, out, r, cols, ld, p.mode, tiles);
+    note_launch("oz_gemm2_kernel");
+  } else {
+    const size_t tiles = 2 * (r / oz::BM) * ((cols + oz::BN - 1) / oz::BN);
+    const unsigned grid = (unsigned)std::min<size_t>(tiles / 2, (size_t)sm_count());
+    oz_gemm_kernel<<<grid, oz::THREADS, oz::SMEM, st>>>(p.tmap_a, tmap_b, p.arow, bcol, out, r,
+                                                         cols, ld, p.mode, tiles);
+    note_launch("oz_gemm_kernel");
+  }
+}
+
+}  // namespace
 
 void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t cols, size_t ld,
                      cudaStream_t st) {
@@ -934,35 +1225,69 @@ void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t co
 #define FLB_OZ_SPLIT8_MAX 8192  // largest N split with 8 entries per thread
 #endif
   if (n <= FLB_OZ_SPLIT8_MAX)
-    oz_split_b_kernel<8><<<(unsigned)cols, (unsigned)(n / 8), 0, st>>>(in, n, ld, cols, b, bcol);
+    oz_split_b_kernel<8><<<(unsigned)cols, (unsigned)(n / 8), 0, st>>>(in, n, ld, cols, b, bcol,
+                                                                      nullptr);
   else
-    oz_split_b_kernel<16><<<(unsigned)cols, (unsigned)(n / 16), 0, st>>>(in, n, ld, cols, b, bcol);
+    oz_split_b_kernel<16><<<(unsigned)cols, (unsigned)(n / 16), 0, st>>>(in, n, ld, cols, b, bcol,
+                                                                        nullptr);
   note_launch("oz_split_b_kernel");
-  const CUtensorMap tmap_b = make_map(b, r, cols, 2 * oz::S, oz::BN);
-  // the attribute is per device context: set it on every call (the library
-  // serves several devices in one process)
-  FLB_CUDA(cudaFuncSetAttribute(oz_gemm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                oz::SMEM));
-#ifndef FLB_OZ_PAIR
-#define FLB_OZ_PAIR 1
-#endif
-  if (FLB_OZ_PAIR && (r / oz::BM) % 2 == 0) {
-    // SM pairs: tiles of 256 rows x 64 columns, B staged as two 32-column halves
-    const CUtensorMap tmap_b2 = make_map(b, r, cols, 2 * oz::S, oz::BN / 2);
-    FLB_CUDA(cudaFuncSetAttribute(oz_gemm2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  oz2::SMEM));
-    const size_t tiles = 2 * (r / oz::BM / 2) * ((cols + oz::BN - 1) / oz::BN);
-    const unsigned clusters = (unsigned)std::min<size_t>(tiles, (size_t)sm_count() / 2);
-    oz_gemm2_kernel<<<2 * clusters, oz::THREADS, oz2::SMEM, st>>>(
-        p.tmap_a, tmap_b2, p.arow, bcol, out, r, cols, ld, p.transpose, tiles);
-    note_launch("oz_gemm2_kernel");
-  } else {
-    const size_t tiles = 2 * (r / oz::BM) * ((cols + oz::BN - 1) / oz::BN);
-    const unsigned grid = (unsigned)std::min<size_t>(tiles, (size_t)sm_count());
-    oz_gemm_kernel<<<grid, oz::THREADS, oz::SMEM, st>>>(p.tmap_a, tmap_b, p.arow, bcol, out, r,
-                                                         cols, ld, p.transpose, tiles);
-    note_launch("oz_gemm_kernel");
+  launch_gemm(p, b, bcol, out, cols, ld, st);
+  cudaFreeAsync(b, st);
+  cudaFreeAsync(bcol, st);
+}
+
+
+L2COzaki* l2c_dense_create(size_t n, int kind, const double* delta, int idlt, cudaStream_t st) {
+  if (!l2c_dense_supported(n)) fail(FL_INVALID_ARGUMENT, "l2c_dense: unsupported size");
+  auto* p = new L2COzaki;
+  p->n = n;
+  p->r = n / 2;
+  p->mode = idlt ? kModeDenseIdlt : kModeDenseDlt;
+  const size_t r = p->r;
+  double* table = nullptr;
+  FLB_CUDA(cudaMallocAsync(&table, n * r * sizeof(double), st));
+  legendre_table_kernel<<<(unsigned)((r + 127) / 128), 128, 0, st>>>(n, kind, delta, table);
+  note_launch("legendre_table_kernel");
+  FLB_CUDA(cudaMalloc(&p->a, (size_t)oz::S * 2 * r * r));
+  FLB_CUDA(cudaMalloc(&p->arow, 2 * r * sizeof(double)));
+  oz_split_a_dense_kernel<<<dim3((unsigned)r, 2), 256, 0, st>>>(table, r, idlt, p->a, p->arow);
+  note_launch("oz_split_a_dense_kernel");
+  cudaFreeAsync(table, st);
+  p->tmap_a = make_map(p->a, r, r, 2 * oz::S, oz::BM);
+  return p;
+}
+
+bool l2c_dense_supported(size_t n) { return l2c_ozaki_supported(n) && n <= kDenseMaxN; }
+
+void l2c_dense_apply(const L2COzaki& p, const double* in, size_t ld_in, const double* w,
+                     double* out, size_t ld_out, size_t cols, int* nonfinite, cudaStream_t st) {
+  if (cols == 0) return;
+  const size_t n = p.n, r = p.r;
+  const bool idlt = p.mode == kModeDenseIdlt;
+  if (!idlt && ((reinterpret_cast<uintptr_t>(in) & 15) != 0 || (ld_in & 1) != 0)) {
+    // the DLT's digit split reads double2: pack a misaligned block first
+    double* packed = nullptr;
+    FLB_CUDA(cudaMallocAsync(&packed, n * cols * sizeof(double), st));
+    FLB_CUDA(cudaMemcpy2DAsync(packed, n * 8, in, ld_in * 8, n * 8, cols,
+                               cudaMemcpyDeviceToDevice, st));
+    l2c_dense_apply(p, packed, n, w, out, ld_out, cols, nonfinite, st);
+    cudaFreeAsync(packed, st);
+    return;
   }
+  int8_t* b = nullptr;
+  double* bcol = nullptr;
+  FLB_CUDA(cudaMallocAsync(&b, (size_t)oz::S * 2 * cols * r, st));
+  FLB_CUDA(cudaMallocAsync(&bcol, 2 * cols * sizeof(double), st));
+  if (idlt) {
+    oz_split_b_sym_kernel<4><<<(unsigned)cols, (unsigned)(r / 4), 0, st>>>(in, n, ld_in, cols, w, b,
+                                                                          bcol, nonfinite);
+    note_launch("oz_split_b_sym_kernel");
+  } else {
+    oz_split_b_kernel<8><<<(unsigned)cols, (unsigned)(n / 8), 0, st>>>(in, n, ld_in, cols, b, bcol,
+                                                                      nonfinite);
+    note_launch("oz_split_b_kernel");
+  }
+  launch_gemm(p, b, bcol, out, cols, ld_out, st);
   cudaFreeAsync(b, st);
   cudaFreeAsync(bcol, st);
 }

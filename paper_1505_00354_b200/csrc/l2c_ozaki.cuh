@@ -21,4 +21,19 @@ void l2c_ozaki_destroy(L2COzaki* p);
 void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t cols, size_t ld,
                      cudaStream_t st);
 
+// The direct DLT / IDLT as one dense split GEMM per parity (transforms.hpp
+// :42-64 evaluated as f = P c and c = D_s P^T D_w f, P_kn = P_n(x_k)): for
+// n a multiple of 256 in [512, kDenseMaxN]. The A digits are built from a
+// double-double table of P_n(cos theta_k) at the reference's evaluation
+// angles theta*_kind(k) + delta_k (delta: the plan's own offsets, device).
+constexpr size_t kDenseMaxN = 8192;
+bool l2c_dense_supported(size_t n);
+L2COzaki* l2c_dense_create(size_t n, int kind, const double* delta, int idlt, cudaStream_t st);
+// DLT: out = P in; IDLT: out = (m + 1/2) P^T (w . in) (w: the quadrature
+// weights, device). Input / output columns of strides ld_in / ld_out.
+// nonfinite (device int, may be null): set when an input column (times w)
+// is not finite; that column comes out NaN.
+void l2c_dense_apply(const L2COzaki& p, const double* in, size_t ld_in, const double* w,
+                     double* out, size_t ld_out, size_t cols, int* nonfinite, cudaStream_t st);
+
 }  // namespace flb

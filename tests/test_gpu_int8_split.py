@@ -29,7 +29,9 @@ def rel(a, b, scale):
 
 
 def both(cfg, c):
-    """dlt and idlt of the (batch, n) block c with the split and the fp64 product."""
+    """dlt and idlt of the (batch, n) block c with the split and the fp64
+    conversion product (the factored path: conversion + NDCT)."""
+    cfg.set_dlt_method(fl.DLT_FACTORED)
     out = {}
     for mode in (fl.GEMM_INT8_SPLIT, fl.GEMM_FP64):
         cfg.set_gemm_mode(mode)
