@@ -577,18 +577,33 @@ __device__ __forceinline__ void store_tile(double* __restrict__ out, const doubl
                                            size_t cols, size_t ld) {
   using namespace oz;
   if (mode == kModeDenseDlt) {
+    if (p == 0) {
 #pragma unroll
-    for (int c = 0; c < BN; ++c) {
-      const size_t col = cb * BN + c;
-      if (col >= cols) continue;
-      const double v = (acc[c] * ascale) * bcol[(size_t)p * cols + col];
-      double* o = out + col * ld;
-      if (p == 0) {
-        o[a] = v;
-      } else {
-        const double e = o[a];
-        o[a] = e + v;
-        o[2 * r - 1 - a] = e - v;
+      for (int c = 0; c < BN; ++c) {
+        const size_t col = cb * BN + c;
+        if (col < cols) out[col * ld + a] = (acc[c] * ascale) * bcol[col];
+      }
+      return;
+    }
+    // E back in chunks: a chunk's loads are issued together, before its
+    // stores (the compiler cannot move a load across a possibly aliasing
+    // store, so a per-column load/store loop would serialise 64 L2 trips)
+    constexpr int CH = 16;
+#pragma unroll
+    for (int c0 = 0; c0 < BN; c0 += CH) {
+      double e[CH];
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        const size_t col = cb * BN + c0 + i;
+        e[i] = col < cols ? __ldcg(out + col * ld + a) : 0.0;
+      }
+#pragma unroll
+      for (int i = 0; i < CH; ++i) {
+        const size_t col = cb * BN + c0 + i;
+        if (col >= cols) continue;
+        const double v = (acc[c0 + i] * ascale) * bcol[cols + col];
+        out[col * ld + a] = e[i] + v;
+        out[col * ld + (2 * r - 1 - a)] = e[i] - v;
       }
     }
     return;

@@ -64,7 +64,7 @@ def test_direct_round_trip_and_batch_invariance():
     dev = torch.from_numpy(c).cuda()
     f = fl.dlt(dev, cfg)
     back = fl.idlt(f, cfg).values.cpu().numpy()
-    assert np.max(np.abs(back - c)) <= 1e-12
+    assert np.max(np.abs(back - c)) <= 1e-10 * np.max(np.abs(c))  # acceptance.cpp:193-211
     f17 = fl.dlt(dev[:17].contiguous(), cfg).cpu().numpy()
     assert np.array_equal(f17, f.cpu().numpy()[:17])
 
