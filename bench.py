@@ -625,6 +625,14 @@ def run_batched(args, rank: int, world: int, local: int) -> None:
                                                                   vp(y.data_ptr()), cols, n, sp)))
     ms_idlt = timed(lambda: _lib.check(_lib.LIB.fl_idlt(cfg.handle, vp(x.data_ptr()), vp(y.data_ptr()),
                                                         cols, n, sp)))
+    # the factored path (the reference's conversion + NDCT) on the same shard, as the ablation
+    direct = cfg.uses_direct(cols)
+    cfg.set_dlt_method(fl.DLT_FACTORED)
+    ms_dlt_f = timed(lambda: _lib.check(_lib.LIB.fl_dlt(cfg.handle, vp(x.data_ptr()), vp(y.data_ptr()),
+                                                        cols, n, sp)))
+    ms_idlt_f = timed(lambda: _lib.check(_lib.LIB.fl_idlt(cfg.handle, vp(x.data_ptr()), vp(y.data_ptr()),
+                                                          cols, n, sp)))
+    cfg.set_dlt_method(fl.DLT_DIRECT)
     coef = n * cols
     l2c_flops = coef * (n / 2.0)                   # N^2/4 MACs per column = N/2 flop per coefficient
     ndct_flops = coef * ndct_flops_per_coef(n, L1)
@@ -634,13 +642,15 @@ def run_batched(args, rank: int, world: int, local: int) -> None:
     rbs = r_rows // 128
     tri_macs = sum((r_rows - 128 * rb) * 128 for rb in range(rbs)) * 2 * cols
     i8_ops = 28 * 2 * tri_macs
+    # the direct product: 28 digit pairs x 2 parities x (N/2)^2 MACs per column, 2 ops per MAC
+    dense_ops = 28 * 2 * 2 * (n // 2) ** 2 * cols
+    dense_tops = dense_ops / (ms / 1e3) / 1e12
     gemm_mode = cfg.gemm_mode()
-    dom = "fast_ndct_fwd_kernel" if ms_ndct >= ms_l2c else "oz_gemm2_kernel"
     achieved = ndct_flops / (ms_ndct / 1e3) / 1e12
     peak = hbm_peak()
     # DRAM traffic of the NDCT kernel per launch, from the committed ncu
     # --set full capture (profiles/ncu_traffic.json: bytes per coefficient)
-    traffic = dct_traffic = None
+    traffic = dct_traffic = dense_traffic = None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tfile):
         tj = json.load(open(tfile))
@@ -651,6 +661,11 @@ def run_batched(args, rank: int, world: int, local: int) -> None:
                            "bytes_per_coef": rec["dram_bytes_per_coef"],
                            "algorithmic_bytes_per_coef": 16.0, "source": rec["capture"]}
                 break
+        rec = tj.get(f"oz_gemm2_kernel(dense, N={n})")
+        if rec:
+            dense_traffic = {"bytes_per_launch": rec["dram_bytes_per_coef"] * coef,
+                             "bytes_per_coef": rec["dram_bytes_per_coef"],
+                             "algorithmic_bytes_per_coef": 16.0, "source": rec["capture"]}
         rec = tj.get(f"fast_dct_stream_fwd_kernel<{lg}>")
         if rec:
             dct_traffic = {"bytes_per_coef": rec["dram_bytes_per_coef"], "algorithmic_bytes_per_coef": 16.0,
@@ -696,17 +711,35 @@ def run_batched(args, rank: int, world: int, local: int) -> None:
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": config_dict(args.config, world, total),
-            "method": {"ndct": f"fast mode: the chebstar nodes evaluated about cheb1 by the {L1}-term "
-                               "Chebyshev (Jacobi-Anger) expansion, fused on chip",
-                       "conversion": "exact int8 digit-split GEMM on the tcgen05 tensor cores (7 8-bit "
-                                     "digits/operand, int32 accumulation, fp64 recombination)"
-                                     if gemm_mode == fl.GEMM_INT8_SPLIT else "fp64 DMMA"},
-            "roofline": {"bound": "fp64", "kernel": "fast_ndct_fwd_kernel", "dominant": dom,
+            "method": {"dlt": ("direct: f = P c, one dense parity-split product per parity on the int8 "
+                               "tcgen05 tensor cores (P_n(cos theta_k) in double-double at the reference's "
+                               "angles; 7 8-bit digits/operand, exact int32 digit products, fp64 "
+                               "recombination); idlt: c = D_s P^T D_w f likewise")
+                       if direct else "factored: conversion + NDCT",
+                       "factored_ablation": {"ndct": f"the chebstar nodes evaluated about cheb1 by the {L1}-term "
+                                                     "Chebyshev (Jacobi-Anger) expansion, fused on chip",
+                                             "conversion": "exact int8 digit-split triangular GEMM (tcgen05)"
+                                             if gemm_mode == fl.GEMM_INT8_SPLIT else "fp64 DMMA"}},
+            "roofline": {"bound": "tensor", "kernel": "oz_split_b_kernel + oz_gemm2_kernel (direct product)",
+                         "achieved": dense_tops, "peak": INT8_PEAK_TOPS, "unit": "TOP/s int8",
+                         "frac": dense_tops / INT8_PEAK_TOPS, "traffic": dense_traffic,
+                         "timed": "the whole DLT step (digit split + GEMM) with CUDA events; "
+                                  "the GEMM alone is the ncu share in profiles/",
+                         "peak_source": "dense int8 tcgen05 peak measured by tools/tc_i8_peak.cu "
+                                        "(profiles/r01_tc_i8_peak.log); MEASURED_PEAKS.json has no int8 entry",
+                         "algorithmic": "28 digit pairs x 2 parities x (N/2)^2 MACs per column, 2 ops/MAC "
+                                        f"(fp64-equivalent N flop/coef = {n * n * cols / (ms / 1e3) / 1e12:.1f} TFLOP/s)"}
+            if direct else
+                        {"bound": "fp64", "kernel": "fast_ndct_fwd_kernel",
                          "achieved": achieved, "peak": DFMA_PEAK_TFLOPS,
                          "unit": "TFLOP/s", "frac": achieved / DFMA_PEAK_TFLOPS, "traffic": traffic,
                          "peak_source": "measured DFMA (fp64 CUDA-core) peak, tools/fp64_peak.cu (profiles/r01_fp64_peak.log)",
                          "algorithmic": f"NDCT L(2.5 log2N + 3) flop/coef, L = {L1} transforms "
                                         "(Chebyshev expansion about cheb1, 2^-52)"},
+            "roofline_fp64_factored_ndct": {"bound": "fp64", "kernel": "fast_ndct_fwd_kernel", "achieved": achieved,
+                                            "peak": DFMA_PEAK_TFLOPS, "unit": "TFLOP/s",
+                                            "frac": achieved / DFMA_PEAK_TFLOPS, "traffic": traffic,
+                                            "algorithmic": f"NDCT L(2.5 log2N + 3) flop/coef, L = {L1}"},
             "roofline_tensor": {"bound": "tensor", "kernel": "oz_split_b_kernel + oz_gemm2_kernel",
                                 "gemm_mode": "int8_split" if gemm_mode == fl.GEMM_INT8_SPLIT else "fp64",
                                 "achieved": i8_ops / (ms_l2c / 1e3) / 1e12, "peak": INT8_PEAK_TOPS,
@@ -722,8 +755,10 @@ def run_batched(args, rank: int, world: int, local: int) -> None:
                              "dct_pass_kernel": "fast_dct_stream_fwd_kernel (fl_trig DCT-III, same shard)",
                              "dct_pass_traffic": dct_traffic,
                              "dct_t_pass_gbs": dct_t_gbs, "dct_t_pass_frac": dct_t_gbs / peak},
-            "kernels_ms": {"leg2cheb_split_int8": ms_l2c, "ndct": ms_ndct, "dct_iii_pass": ms_dct,
-                           "dct_iii_t_pass": ms_dct_t, "dlt_step": ms, "idlt_step": ms_idlt,
+            "kernels_ms": {"dlt_step": ms, "idlt_step": ms_idlt,
+                           "factored_dlt_step": ms_dlt_f, "factored_idlt_step": ms_idlt_f,
+                           "leg2cheb_split_int8": ms_l2c, "ndct": ms_ndct, "dct_iii_pass": ms_dct,
+                           "dct_iii_t_pass": ms_dct_t,
                            "ndct_transpose": ms_ndct_t, "leg2cheb_transpose_split_int8": ms_l2c_t},
             "idlt": {"value": n * cols / (ms_idlt / 1e3) * world, "unit": "coeffs/s"},
             "e2e": {"value": n * total / (e2e_ms / 1e3), "unit": "coeffs/s",
