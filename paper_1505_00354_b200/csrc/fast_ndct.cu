@@ -1515,19 +1515,59 @@ __device__ __forceinline__ double cheb_t(int m, double x) {
   return b;
 }
 
-// cheb: term l of the Chebyshev expansion (stage T_l(n/N) c_n, weight
-// bessel_weight(l, N delta_k) with its sign), else the Taylor term.
-__global__ void big_fwd_pack_kernel(const double* __restrict__ in, size_t ld, size_t n, int l,
-                                    int odd, int cheb, double2* __restrict__ Z, int* nonfinite) {
+// Terms of one multi-pass NDCT call: plain (one DCT-III / DST-III pass,
+// odd = plain_op), the Chebyshev expansion (cheb, with the sine flavour swap)
+// or Taylor terms.
+struct BigTerms {
+  int plain, plain_op, cheb, swap;
+};
+__device__ __forceinline__ int big_odd(const BigTerms& bt, int l) {
+  return bt.plain ? bt.plain_op : ((l & 1) ^ bt.swap);
+}
+// weight of output row k in term l, its sign folded in (bessel_weight /
+// taylor_sign (N delta)^l / l!)
+__device__ __forceinline__ double big_weight(const BigTerms& bt, int l, double y0) {
+  if (bt.plain) return 1.0;
+  if (bt.cheb) return ((bt.swap && (l & 1)) ? -1.0 : 1.0) * bessel_weight(l, y0);
+  return (((l + 1) / 2) % 2 == 0 ? 1.0 : -1.0) * taylor_weight(y0, l);
+}
+// stage factor of entry j in term l: T_l(j/N) (Chebyshev) or (j/N)^l
+__device__ __forceinline__ double big_row(const BigTerms& bt, int l, double x) {
+  if (bt.plain) return 1.0;
+  return bt.cheb ? cheb_t(l, x) : ipow(x, l);
+}
+
+// Per-call tables for terms [l0, l0 + nt): wt[t][k] = big_weight(l0 + t,
+// N delta_k), rt[t][j] = big_row(l0 + t, j/N) (shared by all columns).
+__global__ void big_tables_kernel(size_t n, int l0, int nt, BigTerms bt,
+                                  const double* __restrict__ delta, double* __restrict__ wt,
+                                  double* __restrict__ rt) {
+  const size_t j = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const double y0 = bt.plain ? 0.0 : (double)n * delta[j];
+  const double x = (double)j / (double)n;
+  for (int t = 0; t < nt; ++t) {
+    wt[(size_t)t * n + j] = big_weight(bt, l0 + t, y0);
+    rt[(size_t)t * n + j] = big_row(bt, l0 + t, x);
+  }
+}
+
+// Forward pack of term l0 + blockIdx.z: Z[(z nc + col) P + m] from the stage
+// rt[z][j] c_j (the real-DCT packing of the file header).
+__global__ void big_fwd_pack_kernel(const double* __restrict__ in, size_t ld, size_t n, size_t nc,
+                                    int l0, BigTerms bt, const double* __restrict__ rt,
+                                    double2* __restrict__ Z, int* nonfinite) {
   const size_t P = n / 2;
   const size_t col = blockIdx.y;
+  const int tz = blockIdx.z, l = l0 + tz;
+  const int odd = big_odd(bt, l);
   const double* c = in + col * ld;
+  const double* rw = rt + (size_t)tz * n;
+  double2* Zc = Z + ((size_t)tz * nc + col) * P;
   const double nd = (double)n;
   for (size_t m = blockIdx.x * (size_t)blockDim.x + threadIdx.x; m < P;
        m += (size_t)gridDim.x * blockDim.x) {
-    auto st = [&](size_t j) -> double {
-      return c[j] * (cheb ? cheb_t(l, (double)j / nd) : ipow((double)j / nd, l));
-    };
+    auto st = [&](size_t j) -> double { return c[j] * rw[j]; };
     auto X = [&](size_t j) -> double {
       if (j == 0) return odd ? 0.0 : st(0);
       if (j >= n) return 0.0;
@@ -1546,41 +1586,48 @@ __global__ void big_fwd_pack_kernel(const double* __restrict__ in, size_t ld, si
     const double2 sm = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
     const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
     const double2 dr = make_double2(d.x * c4 - d.y * s4, d.x * s4 + d.y * c4);
-    Z[col * P + m] = make_double2(sm.x - dr.y, sm.y + dr.x);
+    Zc[m] = make_double2(sm.x - dr.y, sm.y + dr.x);
   }
 }
 
-__global__ void big_fwd_unpack_kernel(const double2* __restrict__ Z, size_t n, int l, int odd,
-                                      int cheb, double sign, const double* __restrict__ delta,
-                                      int plain, double* __restrict__ out, size_t ld, int first) {
+// Forward unpack of all nt terms: f_k (+)= sum_t wt[t][k] y_t(k), one store.
+__global__ void big_fwd_unpack_kernel(const double2* __restrict__ Z, size_t n, size_t nc, int l0,
+                                      int nt, BigTerms bt, const double* __restrict__ wt,
+                                      double* __restrict__ out, size_t ld, int first) {
   const size_t P = n / 2;
   const size_t col = blockIdx.y;
   for (size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x; k < n;
        k += (size_t)gridDim.x * blockDim.x) {
     const size_t q = (k & 1) ? (n - 1 - (k >> 1)) : (k >> 1);
-    const double2 z = Z[col * P + (q >> 1)];
-    double y = (q & 1) ? z.y : z.x;
-    if (odd && (k & 1)) y = -y;
-    const double y0 = (double)n * delta[k];
-    const double p = plain ? 1.0 : cheb ? bessel_weight(l, y0) : taylor_weight(y0, l);
+    double acc = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      const double2 z = Z[((size_t)t * nc + col) * P + (q >> 1)];
+      double y = (q & 1) ? z.y : z.x;
+      if (big_odd(bt, l0 + t) && (k & 1)) y = -y;
+      acc += wt[(size_t)t * n + k] * y;
+    }
     double* o = out + col * ld + k;
-    *o = (first ? 0.0 : *o) + sign * p * y;
+    *o = first ? acc : *o + acc;
   }
 }
 
-__global__ void big_tr_pack_kernel(const double* __restrict__ in, size_t ld, size_t n, int l,
-                                   int odd, int cheb, const double* __restrict__ delta, int plain,
+// Transposed pack of term l0 + blockIdx.z: the weighted input h_k = wt[z][k]
+// (mult_k) g_k (DST^T: odd entries negated), packed into Z.
+__global__ void big_tr_pack_kernel(const double* __restrict__ in, size_t ld, size_t n, size_t nc,
+                                   int l0, BigTerms bt, const double* __restrict__ wt,
                                    const double* __restrict__ mult, double2* __restrict__ Z,
                                    int* nonfinite) {
   const size_t P = n / 2;
   const size_t col = blockIdx.y;
+  const int tz = blockIdx.z, l = l0 + tz;
+  const int odd = big_odd(bt, l);
   const double* g = in + col * ld;
+  const double* ww = wt + (size_t)tz * n;
+  double2* Zc = Z + ((size_t)tz * nc + col) * P;
   auto h = [&](size_t k) -> double {
     double v = g[k];
     if (mult) v = mult[k] * v;
-    const double y0 = (double)n * delta[k];
-    const double p = plain ? 1.0 : cheb ? bessel_weight(l, y0) : taylor_weight(y0, l);
-    v = p * v;
+    v = ww[k] * v;
     return (odd && (k & 1)) ? -v : v;
   };
   auto V = [&](size_t q) -> double { return q < P ? h(2 * q) : h(2 * (n - 1 - q) + 1); };
@@ -1594,85 +1641,102 @@ __global__ void big_tr_pack_kernel(const double* __restrict__ in, size_t ld, siz
       }
       if (!isfinite(a) || !isfinite(b)) atomicOr(nonfinite, 1);
     }
-    Z[col * P + m] = make_double2(V(2 * m), V(2 * m + 1));
+    Zc[m] = make_double2(V(2 * m), V(2 * m + 1));
   }
 }
 
-__global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, int l, int odd,
-                                     int cheb, double sign, int plain, double* __restrict__ out,
-                                     size_t ld, int first) {
+// Transposed unpack of all nt terms: out_r (+)= sum_t rt[t][r] X_t(r).
+__global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, size_t nc, int l0,
+                                     int nt, BigTerms bt, const double* __restrict__ rt,
+                                     double* __restrict__ out, size_t ld, int first) {
   const size_t P = n / 2;
   const size_t col = blockIdx.y;
   const double nd = (double)n;
   for (size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x; r < n;
        r += (size_t)gridDim.x * blockDim.x) {
-    double X = 0.0;
-    const size_t kk = odd ? (n - r) : r;
-    if (!(odd && r == 0)) {
+    double acc = 0.0;
+    for (int t = 0; t < nt; ++t) {
+      const int odd = big_odd(bt, l0 + t);
+      if (odd && r == 0) continue;
+      const size_t kk = odd ? (n - r) : r;
       const size_t a = kk & (P - 1), b = (P - kk) & (P - 1);
-      const double2 za = Z[col * P + a], zc = Z[col * P + b];
+      const double2* Zc = Z + ((size_t)t * nc + col) * P;
+      const double2 za = Zc[a], zc = Zc[b];
       const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
       const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));
       double s2, c2, sh, ch;
       sincospi(-2.0 * (double)kk / nd, &s2, &c2);  // e^{-2 pi i kk/N}
       sincospi((double)kk / (2.0 * nd), &sh, &ch);  // e^{i pi kk/(2N)}
       const double2 Vv = make_double2(ev.x + od.x * c2 - od.y * s2, ev.y + od.x * s2 + od.y * c2);
-      X = ch * Vv.x + sh * Vv.y;
+      acc += rt[(size_t)t * n + r] * (ch * Vv.x + sh * Vv.y);
     }
-    const double rp = plain ? 1.0 : cheb ? cheb_t(l, (double)r / nd) : ipow((double)r / nd, l);
     double* o = out + col * ld + r;
-    *o = (first ? 0.0 : *o) + sign * rp * X;
+    *o = first ? acc : *o + acc;
   }
 }
 
+// N > 8192: every term's packed transform in one batched multi-pass FFT
+// (terms x columns), the per-term weights / stage factors from per-call
+// tables, and the unpack accumulating all terms in registers (one store per
+// output): 3 launches + the FFT's passes per batch of terms instead of 4 per
+// term. Terms are batched within a 2 GiB scratch budget (C2, 65536 x 64: all
+// 14 terms at once; C5, one 2^26 column: two at a time).
 void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double* out,
                 size_t ld_out, size_t batch, const double* delta, int l_lo, int l_hi,
                 int plain_op, const double* mult, int* nonfinite, cudaStream_t s, int cheb,
                 int swap) {
   const size_t n = size_t(1) << log2n, P = n / 2;
   if (ld_in != ld_out) fail(FL_RUNTIME_ERROR, "fast ndct: mismatched strides");
-  const size_t chunk_cap = std::max<size_t>(1, (size_t(1) << 30) / (2 * P * sizeof(double2)));
-  const size_t chunk = batch < chunk_cap ? batch : chunk_cap;
-  double2 *Z = nullptr, *S = nullptr;
-  FLB_CUDA(cudaMallocAsync(&Z, chunk * P * sizeof(double2), s));
-  FLB_CUDA(cudaMallocAsync(&S, chunk * P * sizeof(double2), s));
   const int plain = plain_op >= 0;
   if (plain) {
     l_lo = 0;
     l_hi = 1;
   }
+  const BigTerms bt{plain, plain_op, cheb, swap};
+  const int terms = l_hi - l_lo;
+  if (terms <= 0) return;
+  constexpr size_t kBudget = size_t(2) << 30;  // Z + S bytes
+  const size_t per_term_col = 2 * P * sizeof(double2);
+  const size_t chunk = std::max<size_t>(1, std::min<size_t>(batch, kBudget / per_term_col));
+  const int tb = (int)std::max<size_t>(1, std::min<size_t>(terms, kBudget / (per_term_col * chunk)));
+  double2 *Z = nullptr, *S = nullptr;
+  double *wt = nullptr, *rt = nullptr;
+  FLB_CUDA(cudaMallocAsync(&Z, (size_t)tb * chunk * P * sizeof(double2), s));
+  FLB_CUDA(cudaMallocAsync(&S, (size_t)tb * chunk * P * sizeof(double2), s));
+  FLB_CUDA(cudaMallocAsync(&wt, (size_t)tb * n * sizeof(double), s));
+  FLB_CUDA(cudaMallocAsync(&rt, (size_t)tb * n * sizeof(double), s));
   const unsigned gx = (unsigned)std::min<size_t>((P + 255) / 256, 2048);
-  for (size_t c0 = 0; c0 < batch; c0 += chunk) {
-    const size_t nc = batch - c0 < chunk ? batch - c0 : chunk;
-    dim3 grid(gx, (unsigned)nc);
-    for (int l = l_lo; l < l_hi; ++l) {
-      const int first = l == l_lo;
-      const int odd = plain ? plain_op : ((l & 1) ^ swap);
-      const int ch = plain ? 0 : cheb;
-      const double sign = plain ? 1.0
-                          : ch ? ((swap && (l & 1)) ? -1.0 : 1.0)
-                               : (((l + 1) / 2) % 2 == 0 ? 1.0 : -1.0);
+  const unsigned gxn = (unsigned)std::min<size_t>((n + 255) / 256, 4096);
+  for (int l0 = l_lo; l0 < l_hi; l0 += tb) {
+    const int nt = std::min(tb, l_hi - l0);
+    big_tables_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, l0, nt, bt, delta, wt, rt);
+    note_launch("big_tables_kernel");
+    for (size_t c0 = 0; c0 < batch; c0 += chunk) {
+      const size_t nc = batch - c0 < chunk ? batch - c0 : chunk;
+      const int first = l0 == l_lo;
       if (!transpose) {
-        big_fwd_pack_kernel<<<grid, 256, 0, s>>>(in + c0 * ld_in, ld_in, n, plain ? 0 : l, odd, ch,
-                                                 Z, l == 0 ? nonfinite : nullptr);
+        big_fwd_pack_kernel<<<dim3(gx, (unsigned)nc, (unsigned)nt), 256, 0, s>>>(
+            in + c0 * ld_in, ld_in, n, nc, l0, bt, rt, Z, nonfinite);
         note_launch("big_fwd_pack_kernel");
-        fft_pow2(Z, S, log2n - 1, nc, true, s);
-        big_fwd_unpack_kernel<<<grid, 256, 0, s>>>(Z, n, plain ? 0 : l, odd, ch, sign, delta,
-                                                   plain, out + c0 * ld_out, ld_out, first);
+        fft_pow2(Z, S, log2n - 1, nc * nt, true, s);
+        big_fwd_unpack_kernel<<<dim3(gxn, (unsigned)nc), 256, 0, s>>>(
+            Z, n, nc, l0, nt, bt, wt, out + c0 * ld_out, ld_out, first);
         note_launch("big_fwd_unpack_kernel");
       } else {
-        big_tr_pack_kernel<<<grid, 256, 0, s>>>(in + c0 * ld_in, ld_in, n, plain ? 0 : l, odd, ch,
-                                                delta, plain, mult, Z, l == 0 ? nonfinite : nullptr);
+        big_tr_pack_kernel<<<dim3(gx, (unsigned)nc, (unsigned)nt), 256, 0, s>>>(
+            in + c0 * ld_in, ld_in, n, nc, l0, bt, wt, mult, Z, nonfinite);
         note_launch("big_tr_pack_kernel");
-        fft_pow2(Z, S, log2n - 1, nc, false, s);
-        big_tr_unpack_kernel<<<grid, 256, 0, s>>>(Z, n, plain ? 0 : l, odd, ch, sign, plain,
-                                                  out + c0 * ld_out, ld_out, first);
+        fft_pow2(Z, S, log2n - 1, nc * nt, false, s);
+        big_tr_unpack_kernel<<<dim3(gxn, (unsigned)nc), 256, 0, s>>>(
+            Z, n, nc, l0, nt, bt, rt, out + c0 * ld_out, ld_out, first);
         note_launch("big_tr_unpack_kernel");
       }
     }
   }
   cudaFreeAsync(Z, s);
   cudaFreeAsync(S, s);
+  cudaFreeAsync(wt, s);
+  cudaFreeAsync(rt, s);
 }
 
 void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* out,
