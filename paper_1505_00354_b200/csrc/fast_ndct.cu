@@ -1300,6 +1300,117 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, StreamCfg<LOG2N>::MINB)
   if (bad && nonfinite) atomicOr(nonfinite, 1);
 }
 
+// Persistent, prefetching transposed pass (dct_iii_transpose /
+// dst_iii_transpose, the DCT-II type) for one column per CTA (N >= 4096):
+// the next column arrives by one contiguous bulk copy (cp.async.bulk,
+// mbarrier completion) into the stage buffer as soon as every thread has
+// packed the current one (after the first pass's barrier), so it overlaps
+// the remaining passes. The pack reads its even/odd entry pairs straight
+// from the natural-order column (no de-interleave copy, no element-strided
+// global access), which leaves room for two FFT rows used alternately per
+// pass and per column (ping-pong: one barrier per pass, none between
+// columns) at two CTAs per SM.
+template <int LOG2N>
+__global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, LOG2N <= 12 ? 2 : 1)
+    fast_dct_stream_tr_kernel(const double* __restrict__ in, size_t ld_in,
+                              double* __restrict__ out, size_t ld_out, size_t batch, int odd,
+                              const double2* __restrict__ tw4n, const double2* __restrict__ fftw,
+                              int* nonfinite) {
+  using C = Cfg<LOG2N>;
+  static_assert(C::COLS == 1, "one column per CTA");
+  constexpr int N = C::N, P = C::P, T = C::T, E = C::E, OWN = C::OWN;
+  extern __shared__ double smem[];
+  __shared__ uint64_t mbar;
+  double* raw = smem;  // the bulk-copied column, natural order
+  double2* zbA = reinterpret_cast<double2*>(smem + N);
+  double2* zbB = zbA + C::ZB / sizeof(double2);
+  const int t = threadIdx.x;
+  const uint32_t bar = static_cast<uint32_t>(__cvta_generic_to_shared(&mbar));
+  const uint32_t raw_s = static_cast<uint32_t>(__cvta_generic_to_shared(raw));
+  if (t == 0) {
+    mbar_init1(bar);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  size_t col = blockIdx.x;
+  if (t == 0 && col < batch) {
+    mbar_expect(bar, N * 8);
+    bulk_load(raw_s, in + col * ld_in, N * 8, bar);
+  }
+  const double2 ta_t = __ldg(&tw4n[t]);
+  const double2 r4_t = __ldg(&tw4n[4 * t]);
+  bool bad = false;
+  double2* zx = zbA;
+  constexpr double h = 0.70710678118654752440;
+  for (uint32_t it = 0; col < batch; col += gridDim.x, ++it) {
+    mbar_wait_parity(bar, it & 1u);
+    // pack (tr_term): v_r = (h_{4m}, h_{4m+2}) for r < 4, the swapped odd
+    // pair (h_{2N-3-4m}, h_{2N-1-4m}) for r >= 4 (m = t + r T); odd terms
+    // (DST^T) negate the odd-index entries
+    double2 v[E];
+#pragma unroll
+    for (int r = 0; r < E; ++r) {
+      const int m = t + r * T;
+      const int k0 = r < 4 ? 4 * m : 2 * N - 3 - 4 * m;
+      const double2 w = make_double2(raw[k0], raw[k0 + 2]);
+      bad |= !isfinite(w.x) || !isfinite(w.y);
+      v[r] = r < 4 ? w : (odd ? make_double2(-w.y, -w.x) : make_double2(w.y, w.x));
+    }
+    pass_compute<P, E, 8, 1, false>(v, t, fftw);
+    pass_store<P, E, 8, 1>(v, zx, t);
+    __syncthreads();  // every thread has packed: the stage buffer takes the next column
+    const size_t nxt = col + gridDim.x;
+    if (t == 0 && nxt < batch) {
+      mbar_expect(bar, N * 8);
+      bulk_load(raw_s, in + nxt * ld_in, N * 8, bar);
+    }
+    double2* zb = mid_passes_pp<P, E, 8, P, false, 0>(zx, zx == zbA ? zbB : zbA, t, fftw, 0);
+    // unpack (tr_term): rows {a, P - a, P + a, N - a} of each group g
+    double* dst = out + col * ld_out;
+#pragma unroll
+    for (int g = 0; g < OWN / 4; ++g) {
+      const int a = t + g * T;
+      const double2 A = make_double2(ta_t.x * kC32[g][0] - ta_t.y * kC32[g][1],
+                                     ta_t.x * kC32[g][1] + ta_t.y * kC32[g][0]);
+      const double2 R = make_double2(r4_t.x * kC8[g][0] - r4_t.y * kC8[g][1],
+                                     r4_t.x * kC8[g][1] + r4_t.y * kC8[g][0]);
+      const double2 zA = zb[smem_pad(a)], zB = zb[smem_pad((P - a) & (P - 1))];
+      double2 A1 = A, R1 = R, zA1 = zA, zB1 = zB;
+      if (a == 0) {
+        A1 = make_double2(kC32[4][0], kC32[4][1]);
+        R1 = make_double2(0.0, 1.0);
+        zA1 = zB1 = zb[smem_pad(P / 2)];
+      }
+      const double2 t0 = A, r0 = R;
+      const double2 t1 = make_double2(h * (A1.x + A1.y), h * (A1.x - A1.y));
+      const double2 r1 = make_double2(-R1.x, R1.y);
+      const double2 t2 = make_double2(h * (A.x - A.y), h * (A.x + A.y));
+      const double2 r2 = make_double2(-R.x, -R.y);
+      const double2 t3 = make_double2(A1.y, A1.x);
+      const double2 r3 = make_double2(R1.x, -R1.y);
+      double x0, x1, x2, x3;
+      if (odd) {
+        x0 = a == 0 ? 0.0 : tr_unpack<true>(zB, zA, t0, r0);
+        x1 = tr_unpack<true>(zA1, zB1, t1, r1);
+        x2 = tr_unpack<true>(zB, zA, t2, r2);
+        x3 = tr_unpack<true>(zA1, zB1, t3, r3);
+      } else {
+        x0 = tr_unpack<false>(zA, zB, t0, r0);
+        x1 = tr_unpack<false>(zB1, zA1, t1, r1);
+        x2 = tr_unpack<false>(zA, zB, t2, r2);
+        x3 = tr_unpack<false>(zB1, zA1, t3, r3);
+      }
+      const int a1 = a ? a : P / 2;
+      __stcs(dst + a, 0.5 * x0);
+      __stcs(dst + (P - a1), 0.5 * x1);
+      __stcs(dst + (P + a), 0.5 * x2);
+      __stcs(dst + (N - a1), 0.5 * x3);
+    }
+    zx = zb == zbA ? zbB : zbA;  // the next column's first pass: the row this unpack did not read
+  }
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
+}
+
 template <int LOG2N>
 __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, 2)
     fast_dct_plain_tr_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
@@ -1378,6 +1489,21 @@ void launch_fast(int transpose, const double* in, size_t ld_in, double* out, siz
   const bool use_bes = bes && bes->bes_terms > 0 && plain_op < 0;
   const size_t max_cols = (size_t)0x7fffffff * C::COLS;
   if constexpr (C::COLS == 1) {
+#ifndef FLB_STREAM_TR
+#define FLB_STREAM_TR 1
+#endif
+    if (FLB_STREAM_TR && plain_op >= 0 && !mult && transpose && ld_in == ld_out &&
+        (ld_in % 2) == 0 && (reinterpret_cast<uintptr_t>(in) & 15) == 0) {
+      const size_t smem = C::N * sizeof(double) + 2 * C::ZB;
+      FLB_CUDA(cudaFuncSetAttribute(fast_dct_stream_tr_kernel<LOG2N>,
+                                    cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const unsigned grid =
+          (unsigned)std::min<size_t>(batch, (size_t)sm_count() * (LOG2N <= 12 ? 2 : 1));
+      fast_dct_stream_tr_kernel<LOG2N><<<grid, C::THREADS, smem, s>>>(
+          in, ld_in, out, ld_out, batch, plain_op, tw, fftw, nonfinite);
+      note_launch("fast_dct_stream_tr_kernel");
+      return;
+    }
     if (plain_op >= 0 && !mult && !transpose && ld_in == ld_out && (ld_in % 2) == 0 &&
         (reinterpret_cast<uintptr_t>(in) & 15) == 0 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
       const size_t smem = StreamCfg<LOG2N>::SMEM;

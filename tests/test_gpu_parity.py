@@ -197,12 +197,14 @@ def test_trig_batched_large(n):
                 assert rel_err(got[j], ref, np.abs(c[j]).sum()) <= tol_n(n), (kind, op, j)
 
 
-@pytest.mark.parametrize("op", [0, 1])
+@pytest.mark.parametrize("op", [0, 1, 2, 3])
 def test_trig_streaming_pass_device(op):
-    """The persistent streaming DCT-III / DST-III pass (device columns, even
-    stride, 16-byte aligned; N = 4096: outputs stored straight from the
-    mirrored last-pass butterflies) against the oracle on sampled columns and
-    against the per-column kernel (odd stride) on all of them."""
+    """The persistent streaming passes (device columns, even stride, 16-byte
+    aligned): DCT-III / DST-III (N = 4096: outputs stored straight from the
+    mirrored last-pass butterflies) and their transposes (the next column
+    bulk-copied while the current one is transformed, de-interleaved in
+    shared memory) against the oracle on sampled columns and against the
+    per-column kernel (odd stride) on all of them."""
     import ctypes as C
     import torch
     from paper_1505_00354_b200 import _lib
