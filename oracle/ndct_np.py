@@ -99,7 +99,8 @@ def taylor_sign(l: int) -> float:  # ndct.hpp:77
     return 1.0 if ((l + 1) // 2) % 2 == 0 else -1.0
 
 
-def ndct_apply(c, kind: int, num_terms: int, delta) -> np.ndarray:  # ndct.hpp:98-117
+def ndct_apply(c, kind: int, num_terms: int, delta, lo: int = 0) -> np.ndarray:  # ndct.hpp:98-117
+    """Taylor terms l in [lo, num_terms) (lo = 0: the whole ndct_apply)."""
     c = np.asarray(c, dtype=np.float64)
     delta = np.asarray(delta, dtype=np.float64)
     n = len(c)
@@ -111,12 +112,15 @@ def ndct_apply(c, kind: int, num_terms: int, delta) -> np.ndarray:  # ndct.hpp:9
         if l > 0:
             stage *= j
             perturb *= delta / float(l)
+        if l < lo:
+            continue
         t = dct_iii(stage, kind) if l % 2 == 0 else dst_iii(stage, kind)
         f += taylor_sign(l) * perturb * t
     return f
 
 
-def ndct_apply_transpose(v, kind: int, num_terms: int, delta) -> np.ndarray:  # ndct.hpp:121-143
+def ndct_apply_transpose(v, kind: int, num_terms: int, delta, lo: int = 0) -> np.ndarray:  # ndct.hpp:121-143
+    """Taylor terms l in [lo, num_terms) of ndct_apply_transpose."""
     v = np.asarray(v, dtype=np.float64)
     delta = np.asarray(delta, dtype=np.float64)
     n = len(v)
@@ -128,6 +132,8 @@ def ndct_apply_transpose(v, kind: int, num_terms: int, delta) -> np.ndarray:  # 
         if l > 0:
             degree *= j
             perturb *= delta / float(l)
+        if l < lo:
+            continue
         h = perturb * v
         t = dct_iii_transpose(h, kind) if l % 2 == 0 else dst_iii_transpose(h, kind)
         out += taylor_sign(l) * degree * t

@@ -112,3 +112,124 @@ def test_term_parallel_transform_two_ranks():
     assert np.allclose(full, B @ (A @ x), rtol=1e-12, atol=1e-12)
     assert np.allclose(scattered, full, rtol=1e-12, atol=1e-12)
     assert np.allclose(inv, A.T @ (B.T @ x), rtol=1e-12, atol=1e-12)
+
+
+def test_term_slice_balanced():
+    from paper_1505_00354_b200.distributed import term_slice
+    for count in (0, 1, 5, 14, 74, 145):
+        for world in (1, 2, 3, 4, 8):
+            sl = [term_slice(count, world, r) for r in range(world)]
+            assert sl[0][0] == 0 and sl[-1][1] == count
+            assert all(sl[r][1] == sl[r + 1][0] for r in range(world - 1))
+            sizes = [hi - lo for lo, hi in sl]
+            assert max(sizes) - min(sizes) <= 1 and max(sizes) == -(-count // world)
+
+
+def _c4_worker(rank, world, port, out):
+    """BASELINE C4's sharded data path (bench.py run_batched): contiguous
+    column shards, inputs seeded per global column, one independent batched
+    DLT per rank (no data collective), barrier + max over ranks. The device
+    transform is stood in for by the CPU oracle's DLT on the same grid."""
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import ORACLE as O, uniform_pm1
+    n, total = 64, 11
+    th, x, w = O.nodes_weights(n)
+    first, cnt = column_shard(total, world, rank)
+    cols = np.stack([uniform_pm1(n, 4000 + first + j) for j in range(cnt)]) if cnt else np.zeros((0, n))
+    f = np.stack([O.dlt_grid(c, 1, 2.0 ** -52, th, x, w) for c in cols]) if cnt else np.zeros((0, n))
+    dist.barrier()
+    t = max_over_ranks(0.5 + rank, dist)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, (first, f))
+    if rank == 0:
+        out.put((gathered, t))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_c4_sharded_data_path_two_ranks():
+    from oracle import ORACLE as O, uniform_pm1
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c4_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    gathered, tmax = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert tmax == 1.5
+    n, total = 64, 11
+    th, x, w = O.nodes_weights(n)
+    full = np.stack([O.dlt_grid(uniform_pm1(n, 4000 + j), 1, 2.0 ** -52, th, x, w) for j in range(total)])
+    got = np.concatenate([f for _, f in sorted(gathered, key=lambda g: g[0])])
+    assert np.array_equal(got, full)
+
+
+def _c5_worker(rank, world, port, out):
+    """BASELINE C5's term-parallel DLT / IDLT (distributed.transform, the
+    bench's C5 call sequence) over gloo, with CPU stand-ins that compute the
+    real stage arithmetic as sums of independent terms: the conversion as
+    the direct product split by column blocks of M (transforms.hpp:47,
+    conversion.hpp:100-140), the NDCT as its Taylor terms (ndct.hpp:98-143,
+    oracle/ndct_np.py); the inverse with (m + 1/2) M^T and the weighted
+    NDCT^T (transforms.hpp:58-62)."""
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import ORACLE as O, ndct_np as NP
+    from paper_1505_00354_b200 import distributed as D
+    n, kind, blocks = 96, 1, 7
+    th, x, w = O.nodes_weights(n)
+    L = O.min_taylor_terms(kind, 2.0 ** -52)
+    delta = O.reference_delta(n, kind, th)
+    M = np.stack([O.leg2cheb(np.eye(n)[j]) for j in range(n)], axis=1)  # column j = M e_j
+    edges = np.linspace(0, n, blocks + 1).astype(int)
+    half = np.arange(n) + 0.5
+
+    def stage_fn(inverse, stage, lo, hi, xin, y):
+        v = xin.numpy()
+        if stage == D.STAGE_LEG2CHEB:
+            acc = np.zeros(n)
+            for b in range(lo, hi):
+                sl = slice(edges[b], edges[b + 1])
+                acc += (half[:, None] * M.T[:, sl]) @ v[sl] if inverse else M[:, sl] @ v[sl]
+        else:
+            acc = (NP.ndct_apply_transpose(w * v, kind, hi, delta, lo) if inverse
+                   else NP.ndct_apply(v, kind, hi, delta, lo)) if hi > lo else np.zeros(n)
+        y.copy_(torch.from_numpy(acc))
+
+    c = torch.from_numpy(O.random_decaying(n, 0.5, 7))
+    counts = (blocks, L)
+    f = D.transform(c, False, dist, counts=counts, stage_fn=stage_fn)
+    f_part = D.transform(c, False, dist, counts=counts, stage_fn=stage_fn, scatter=True)
+    back = D.transform(f, True, dist, counts=counts, stage_fn=stage_fn)
+    gathered = [None] * world
+    dist.all_gather_object(gathered, f_part.numpy())
+    if rank == 0:
+        out.put((c.numpy(), f.numpy(), np.concatenate(gathered), back.numpy(), th, x, w))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_c5_term_parallel_stages_two_ranks():
+    from oracle import ORACLE as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_c5_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    c, f, f_sc, back, th, x, w = q.get(timeout=180)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = len(c)
+    tol = 1e-13 * np.log2(n)
+    ref_f = O.dlt_grid(c, 1, 2.0 ** -52, th, x, w)
+    assert np.max(np.abs(f - ref_f)) <= tol * np.abs(c).sum()
+    assert np.array_equal(f_sc, f)
+    ref_b = O.idlt_grid(f, 1, 2.0 ** -52, th, x, w)
+    assert np.max(np.abs(back - ref_b)) <= tol * np.abs(f).sum()
