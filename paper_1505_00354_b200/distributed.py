@@ -47,17 +47,19 @@ def gpu_stage(cfg, inverse: int, stage: int, lo: int, hi: int, x, y) -> None:
                                      C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), s))
 
 
-def term_slice(count: int, world: int, rank: int) -> tuple[int, int]:
+def term_slice(count: int, world: int, rank: int, unit: int = 1) -> tuple[int, int]:
     """[lo, hi) of a stage's `count` equal-cost terms for `rank`: the first
     count % world ranks take one term more (a stage's time is its largest
     slice, ceil(count / world) terms; e.g. 14 NDCT terms over 8 ranks: 6 x 2 +
     2 x 1, bound 14 / 16 = 87.5 % of ideal; 74 rank terms: 2 x 10 + 6 x 9,
     92.5 %)."""
-    if world <= 0 or not 0 <= rank < world:
-        raise ValueError("term_slice: bad world/rank")
-    base, extra = divmod(count, world)
+    if world <= 0 or not 0 <= rank < world or unit < 1:
+        raise ValueError("term_slice: bad world/rank/unit")
+    units = -(-count // unit)  # slices in whole units (the conversion's terms come in FFT pairs)
+    base, extra = divmod(units, world)
     lo = rank * base + min(rank, extra)
-    return lo, lo + base + (1 if rank < extra else 0)
+    hi = lo + base + (1 if rank < extra else 0)
+    return min(lo * unit, count), min(hi * unit, count)
 
 
 def transform(x, inverse: bool, dist=None, *, counts: tuple[int, int],
@@ -71,7 +73,8 @@ def transform(x, inverse: bool, dist=None, *, counts: tuple[int, int],
     order = (STAGE_NDCT, STAGE_LEG2CHEB) if inverse else (STAGE_LEG2CHEB, STAGE_NDCT)
     cur = x
     for step, stage in enumerate(order):
-        lo, hi = term_slice(counts[stage], world, rank)
+        # the conversion's rank terms share complex FFTs two at a time
+        lo, hi = term_slice(counts[stage], world, rank, 2 if stage == STAGE_LEG2CHEB else 1)
         part = torch.empty_like(cur)
         stage_fn(int(inverse), stage, lo, hi, cur, part)
         last = step == len(order) - 1

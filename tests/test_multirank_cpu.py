@@ -123,6 +123,10 @@ def test_term_slice_balanced():
             assert all(sl[r][1] == sl[r + 1][0] for r in range(world - 1))
             sizes = [hi - lo for lo, hi in sl]
             assert max(sizes) - min(sizes) <= 1 and max(sizes) == -(-count // world)
+            sl2 = [term_slice(count, world, r, 2) for r in range(world)]
+            assert sl2[0][0] == 0 and sl2[-1][1] == count
+            assert all(sl2[r][1] == sl2[r + 1][0] for r in range(world - 1))
+            assert all(lo % 2 == 0 for lo, hi in sl2 if hi > lo)
 
 
 def _c4_worker(rank, world, port, out):
