@@ -112,7 +112,44 @@ __global__ void transpose_kernel(const double2* __restrict__ in, double2* __rest
 struct LineMap {
   unsigned long long M, Hin, Sin, Hout, Sout;   // addressing (M a power of two)
   unsigned long long Q, u, v, z;                // twiddle exponent (Q = 0: none; a power of two)
+  // two-level twiddle tables of w_Q (filled by launch_line when Q != 0):
+  // w_Q^m = twlo[m mod 2^twh] * twhi[m >> twh]
+  const double2* twlo = nullptr;
+  const double2* twhi = nullptr;
+  int twh = 0;
 };
+
+// w_Q^j = e^{-2 pi i j/Q} for j < 2^h (lo) and j = 2^h i, i < Q / 2^h (hi),
+// h = ceil(log2 Q / 2): one complex product per twiddle instead of an fp64
+// sincospi (the twiddled line passes were issue-bound on it: 1.6x the time
+// of the untwiddled pass at 2^26). Phases reduced exactly, long double.
+std::pair<const double2*, const double2*> twiddle_pair(int log2q) {
+  static std::mutex mu;
+  static std::map<std::pair<int, int>, std::pair<double2*, double2*>> tables;
+  int dev = 0;
+  FLB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto& slot = tables[{dev, log2q}];
+  if (!slot.first) {
+    const int h = (log2q + 1) / 2;
+    const long long q = 1ll << log2q, nlo = 1ll << h, nhi = q >> h;
+    const long double pi_l = 3.14159265358979323846264338327950288L;
+    std::vector<double2> lo(nlo), hi(nhi);
+    for (long long j = 0; j < nlo; ++j) {
+      const long double a = 2.0L * pi_l * (long double)j / (long double)q;
+      lo[j] = make_double2((double)cosl(a), (double)-sinl(a));
+    }
+    for (long long i = 0; i < nhi; ++i) {
+      const long double a = 2.0L * pi_l * (long double)(i * nlo) / (long double)q;
+      hi[i] = make_double2((double)cosl(a), (double)-sinl(a));
+    }
+    FLB_CUDA(cudaMalloc(&slot.first, nlo * sizeof(double2)));
+    FLB_CUDA(cudaMalloc(&slot.second, nhi * sizeof(double2)));
+    FLB_CUDA(cudaMemcpy(slot.first, lo.data(), nlo * sizeof(double2), cudaMemcpyHostToDevice));
+    FLB_CUDA(cudaMemcpy(slot.second, hi.data(), nhi * sizeof(double2), cudaMemcpyHostToDevice));
+  }
+  return {slot.first, slot.second};
+}
 
 // lines per CTA of a pass over lines of 2^log2l
 constexpr int line_ctas_lines(int log2l) { return log2l >= 12 ? 2 : log2l >= 10 ? 4 : 8; }
@@ -253,9 +290,12 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
         const unsigned long long kk = (unsigned long long)k;
         // exponent mod Q by masks (wrap-around of the 64-bit products is harmless mod 2^k)
         const unsigned long long m = (lo * (hi * mp.u + kk * mp.v) + hi * kk * mp.z) & qmask;
-        double sn, cs;
-        sincospi(2.0 * (double)m / (double)mp.Q, &sn, &cs);
-        if (!TW_INV) sn = -sn;
+        const double2 a = __ldg(&mp.twlo[m & ((1ull << mp.twh) - 1)]);
+        const double2 b = __ldg(&mp.twhi[m >> mp.twh]);
+        // w = a b = e^{-2 pi i m/Q}; the inverse direction uses its conjugate
+        const double cs = a.x * b.x - a.y * b.y;
+        double sn = a.x * b.y + a.y * b.x;
+        if (TW_INV) sn = -sn;
         x = make_double2(x.x * cs - x.y * sn, x.x * sn + x.y * cs);
       }
       const unsigned long long g = lo + hi * mp.Hout + (unsigned long long)k * mp.Sout;
@@ -271,12 +311,20 @@ void launch_line(const LineIO& io, unsigned long long P, size_t items, const Lin
   static_assert(Q::LINES * Q::L == Q::THREADS * Q::E, "one element per thread per E");
   const double2* tw = pass_twiddles(LOG2L);
   const unsigned long long lines = P >> LOG2L;
+  LineMap m2 = mp;
+  if (m2.Q) {
+    const int lq = __builtin_ctzll(m2.Q);
+    const auto t2 = twiddle_pair(lq);
+    m2.twlo = t2.first;
+    m2.twhi = t2.second;
+    m2.twh = (lq + 1) / 2;
+  }
   auto kern = fft_line_kernel<LOG2L, INV, IN, MID>;
   // MID: + the symbol rows when they fit
   const size_t smem = MID && 2 * Q::SMEM <= 80 * 1024 ? 2 * Q::SMEM : Q::SMEM;
   FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   dim3 grid((unsigned)(lines / Q::LINES), (unsigned)items);
-  kern<<<grid, Q::THREADS, smem, s>>>(io, P, mp, tw);
+  kern<<<grid, Q::THREADS, smem, s>>>(io, P, m2, tw);
   note_launch("fft_line_kernel");
 }
 
