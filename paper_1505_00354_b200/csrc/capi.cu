@@ -711,7 +711,7 @@ fl_status fl_leg2cheb(int transpose, size_t n, const double* lambda_table, size_
     DevOut o(out, n, batch, ld, s);
     if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
     if (i.ptr == o.ptr) fail(FL_INVALID_ARGUMENT, "leg2cheb: input and output must not alias");
-    if (n >= 4 * kL2CFastMin && batch <= kL2CFastMaxCols) {
+    if (n >= (size_t(1) << 17) && batch <= kL2CFastMaxCols) {
       // large single vectors: build the low-rank factors for this table once
       L2CFast* f = l2c_fast_create(n, sc.p, s);
       try {

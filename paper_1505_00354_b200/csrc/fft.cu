@@ -205,9 +205,15 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
   // the store twiddle belongs to the direction of the last transform
   constexpr bool TW_INV = MID ? !INV : INV;
   extern __shared__ double2 sm[];
-  const unsigned long long l0 = (unsigned long long)blockIdx.x * LINES;
-  const unsigned long long mmask = mp.M - 1, qmask = mp.Q - 1;
+  // element indices within one item are < P <= 2^27: 32-bit arithmetic (the
+  // 64-bit index products were a large share of the pass's issue slots);
+  // twiddle exponents mod Q | 2^32 are exact in wrapping 32-bit products
+  const uint32_t l0 = blockIdx.x * (uint32_t)LINES;
+  const uint32_t mmask = (uint32_t)mp.M - 1u, qmask = (uint32_t)(mp.Q - 1);
   const int mshift = __ffsll((long long)mp.M) - 1;
+  const uint32_t Hin = (uint32_t)mp.Hin, Sin = (uint32_t)mp.Sin, Hout = (uint32_t)mp.Hout,
+                 Sout = (uint32_t)mp.Sout;
+  const uint32_t tu = (uint32_t)mp.u, tv = (uint32_t)mp.v, tz = (uint32_t)mp.z;
   const bool rows_in = mp.Sin == 1;   // contiguous lines: element index fastest
   const bool rows_out = mp.Sout == 1;
   const int line = threadIdx.x / Q::TL, tid = threadIdx.x % Q::TL;
@@ -217,6 +223,8 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
   double2* sym_s = sm + LINES * Q::LS;
   {
     const size_t item = blockIdx.y;
+    const double2* src_item = IN == IO_PACK ? nullptr : io.src + item * P;
+    double2* dst_item = io.dst + item * P;
     // all PER loads of a thread are issued before the first smem store
     if constexpr (line_unroll(LOG2L)) {
       double2 v[PER];
@@ -224,12 +232,12 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
       for (int r = 0; r < PER; ++r) {
         const int i = threadIdx.x + r * Q::THREADS;
         const int j = rows_in ? i / L : i % LINES, e = rows_in ? i % L : i / LINES;
-        const unsigned long long l = l0 + j, lo = l & mmask, hi = l >> mshift;
-        const unsigned long long g = lo + hi * mp.Hin + (unsigned long long)e * mp.Sin;
+        const uint32_t l = l0 + j, lo = l & mmask, hi = l >> mshift;
+        const uint32_t g = lo + hi * Hin + (uint32_t)e * Sin;
         if constexpr (IN == IO_PACK)
           v[r] = th_pack_value(io.th, item, g);
         else
-          v[r] = io.src[item * P + g];
+          v[r] = src_item[g];
       }
 #pragma unroll
       for (int r = 0; r < PER; ++r) {
@@ -240,13 +248,13 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
     } else {
       for (int i = threadIdx.x; i < LINES * L; i += blockDim.x) {
         const int j = rows_in ? i / L : i % LINES, e = rows_in ? i % L : i / LINES;
-        const unsigned long long l = l0 + j, lo = l & mmask, hi = l >> mshift;
-        const unsigned long long g = lo + hi * mp.Hin + (unsigned long long)e * mp.Sin;
+        const uint32_t l = l0 + j, lo = l & mmask, hi = l >> mshift;
+        const uint32_t g = lo + hi * Hin + (uint32_t)e * Sin;
         double2 v;
         if constexpr (IN == IO_PACK)
           v = th_pack_value(io.th, item, g);
         else
-          v = io.src[item * P + g];
+          v = src_item[g];
         sm[j * Q::LS + smem_pad(e)] = v;
       }
     }
@@ -284,13 +292,13 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
     for (int r = 0; r < PER; ++r) {
       const int i = threadIdx.x + r * Q::THREADS;
       const int j = rows_out ? i / L : i % LINES, k = rows_out ? i % L : i / LINES;
-      const unsigned long long l = l0 + j, lo = l & mmask, hi = l >> mshift;
+      const uint32_t l = l0 + j, lo = l & mmask, hi = l >> mshift;
       double2 x = sm[j * Q::LS + smem_pad(k)];
       if (mp.Q) {
-        const unsigned long long kk = (unsigned long long)k;
-        // exponent mod Q by masks (wrap-around of the 64-bit products is harmless mod 2^k)
-        const unsigned long long m = (lo * (hi * mp.u + kk * mp.v) + hi * kk * mp.z) & qmask;
-        const double2 a = __ldg(&mp.twlo[m & ((1ull << mp.twh) - 1)]);
+        const uint32_t kk = (uint32_t)k;
+        // exponent mod Q by masks (wrap-around of the 32-bit products is harmless mod 2^k)
+        const uint32_t m = (lo * (hi * tu + kk * tv) + hi * kk * tz) & qmask;
+        const double2 a = __ldg(&mp.twlo[m & ((1u << mp.twh) - 1u)]);
         const double2 b = __ldg(&mp.twhi[m >> mp.twh]);
         // w = a b = e^{-2 pi i m/Q}; the inverse direction uses its conjugate
         const double cs = a.x * b.x - a.y * b.y;
@@ -298,8 +306,8 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
         if (TW_INV) sn = -sn;
         x = make_double2(x.x * cs - x.y * sn, x.x * sn + x.y * cs);
       }
-      const unsigned long long g = lo + hi * mp.Hout + (unsigned long long)k * mp.Sout;
-      io.dst[item * P + g] = x;
+      const uint32_t g = lo + hi * Hout + (uint32_t)k * Sout;
+      dst_item[g] = x;
     }
   }
 }
