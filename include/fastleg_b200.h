@@ -269,6 +269,21 @@ void fl_random_decaying(size_t n, double decay, uint64_t seed, double* out, size
                         int threads);
 void fl_random_uniform_pm1(size_t n, uint64_t seed, double* out, size_t batch, int threads);
 
+/* vector_io.hpp:22-102: the on-disk vector formats
+ * either side of the transforms, staged straight to / from device memory.
+ * format 0 = csv (one value per line), 1 = raw_binary ("FLEGVEC1", uint64 LE
+ * count, binary64 LE values). `out` / `in` may be device or host pointers.
+ *   fl_load_vector: the binary payload is read in chunks into two pinned
+ *     buffers whose async H2D copies overlap the next chunk's read; csv is
+ *     parsed into a pinned buffer and copied once. *count = the vector's
+ *     length; capacity < count -> FL_INVALID_ARGUMENT (nothing copied).
+ *   fl_save_vector: D2H in chunks into pinned buffers, written as they land.
+ * Errors: FL_RUNTIME_ERROR with the reference's IoError messages (cannot
+ * open, bad magic, truncated header / payload, not a number). */
+fl_status fl_load_vector(const char* path, int format, double* out, size_t capacity,
+                         size_t* count, void* stream);
+fl_status fl_save_vector(const char* path, int format, const double* in, size_t n, void* stream);
+
 /* Number of kernels this library has launched since load (telemetry for the
  * bench's gpu_launches field). */
 uint64_t fl_kernel_launch_count(void);

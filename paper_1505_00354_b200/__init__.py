@@ -21,4 +21,5 @@ from .api import (  # noqa: F401
     min_taylor_terms, ndct_apply, ndct_apply_transpose, ndct_error_bound, plan_ndct,
     random_decaying, random_uniform_pm1, reference_angle, reference_grid, taylor_term_bound,
     eval_legendre_direct, eval_chebyshev_direct, idlt_direct, cheb_coeffs_of_legendre,
+    load_vector, save_vector, VECTOR_CSV, VECTOR_RAW_BINARY,
 )

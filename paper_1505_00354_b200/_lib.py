@@ -67,6 +67,7 @@ EXPORTS = [
     "fl_plan_stage_terms", "fl_dlt_stage", "fl_plan_set_gemm_mode", "fl_plan_gemm_mode",
     "fl_plan_leg2cheb", "fl_plan_ndct", "fl_plan_ndct_terms", "fl_set_free_ndct_mode",
     "fl_free_ndct_mode", "fl_plan_set_dlt_method", "fl_plan_dlt_method", "fl_plan_uses_direct",
+    "fl_load_vector", "fl_save_vector",
 ]
 
 
@@ -122,6 +123,8 @@ def _load() -> C.CDLL:
         "fl_plan_set_dlt_method": (i, [vp, i]),
         "fl_plan_dlt_method": (i, [vp]),
         "fl_plan_uses_direct": (i, [vp, sz]),
+        "fl_load_vector": (i, [C.c_char_p, i, dp, sz, C.POINTER(sz), vp]),
+        "fl_save_vector": (i, [C.c_char_p, i, dp, sz, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

@@ -562,3 +562,35 @@ def random_uniform_pm1(n: int, seed: int, batch: int = 1, threads: int = 0) -> n
     out = np.empty((batch, n)) if batch > 1 else np.empty(n)
     LIB.fl_random_uniform_pm1(n, seed, _vp(out.ctypes.data), batch, threads)
     return out
+
+
+# ---------------------------------------------------------------------------
+# vector_io.hpp, staged through pinned buffers
+# ---------------------------------------------------------------------------
+
+VECTOR_CSV, VECTOR_RAW_BINARY = 0, 1
+
+
+def load_vector(path: str, fmt: int = VECTOR_RAW_BINARY, device=None):  # vector_io.hpp:66-102
+    """Read a csv / FLEGVEC1 vector; ``device`` (a torch device) -> the values
+    land in device memory through overlapped pinned chunks, else NumPy."""
+    cnt = C.c_size_t(0)
+    # first pass learns the length (capacity 0 raises invalid_argument for n > 0)
+    rc = LIB.fl_load_vector(str(path).encode(), int(fmt), None, 0, C.byref(cnt), None)
+    if rc not in (_lib.FL_OK, _lib.FL_INVALID_ARGUMENT):
+        check(rc)
+    n = cnt.value
+    if device is not None:
+        import torch
+        out = torch.empty(max(n, 1), dtype=torch.float64, device=device)
+        check(LIB.fl_load_vector(str(path).encode(), int(fmt), _vp(out.data_ptr()), n, C.byref(cnt),
+                                 _vp(torch.cuda.current_stream(out.device).cuda_stream)))
+        return out[:n]
+    out = np.empty(max(n, 1))
+    check(LIB.fl_load_vector(str(path).encode(), int(fmt), _vp(out.ctypes.data), n, C.byref(cnt), None))
+    return out[:n]
+
+
+def save_vector(path: str, values, fmt: int = VECTOR_RAW_BINARY) -> None:  # vector_io.hpp:49-64
+    a = _Arr(values)
+    check(LIB.fl_save_vector(str(path).encode(), int(fmt), _vp(a.ptr), a.n, a.stream))

@@ -2,6 +2,8 @@
 // order with its messages, host/device staging, per-call stream-ordered
 // scratch, and the TransformConfig-equivalent device plan.
 #include <algorithm>
+#include <charconv>
+#include <cstdio>
 #include <atomic>
 #include <cmath>
 #include <cstring>
@@ -1209,6 +1211,165 @@ static void decaying_column(size_t n, uint64_t seed, double* out, double decay) 
 static void uniform_column(size_t n, uint64_t seed, double* out, double) {
   std::mt19937_64 rng(seed);
   for (size_t i = 0; i < n; ++i) out[i] = 2.0 * (static_cast<double>(rng() >> 11) * 0x1.0p-53) - 1.0;
+}
+
+// ---- vector_io.hpp with pinned staging --------------------------------------
+namespace {
+constexpr size_t kIoChunk = size_t(1) << 20;  // doubles per staged chunk (8 MiB)
+
+struct Pinned {
+  double* p = nullptr;
+  explicit Pinned(size_t n) { FLB_CUDA(cudaMallocHost(&p, (n ? n : 1) * sizeof(double))); }
+  Pinned(const Pinned&) = delete;
+  Pinned& operator=(const Pinned&) = delete;
+  ~Pinned() {
+    if (p) cudaFreeHost(p);
+  }
+};
+
+uint64_t le64(const unsigned char* b) {
+  uint64_t v = 0;
+  for (int i = 7; i >= 0; --i) v = (v << 8) | b[i];
+  return v;
+}
+}  // namespace
+
+fl_status fl_load_vector(const char* path, int format, double* out, size_t capacity,
+                         size_t* count, void* stream) {
+  return guarded([&] {
+    if (format != 0 && format != 1) fail(FL_INVALID_ARGUMENT, "vector_io: unknown format");
+    FILE* f = std::fopen(path, "rb");
+    if (!f) fail(FL_RUNTIME_ERROR, std::string("cannot open for reading: ") + path);
+    struct Closer {
+      FILE* f;
+      ~Closer() { std::fclose(f); }
+    } closer{f};
+    const bool dev = is_device_ptr(out);
+    cudaStream_t s = as_stream(stream);
+    if (format == 0) {  // csv: parse on the host (vector_io.hpp:66-80), one staged copy
+      std::vector<double> vals;
+      char line[512];
+      for (size_t lineno = 1; std::fgets(line, sizeof line, f); ++lineno) {
+        char* b = line;
+        while (*b == ' ' || *b == '\t' || *b == '\r') ++b;
+        char* e = b + std::strlen(b);
+        while (e > b && (e[-1] == ' ' || e[-1] == '\t' || e[-1] == '\r' || e[-1] == '\n')) --e;
+        if (e == b) continue;
+        *e = '\0';
+        char* end = nullptr;
+        const double v = std::strtod(b, &end);
+        if (end != e)
+          fail(FL_RUNTIME_ERROR, std::string(path) + ":" + std::to_string(lineno) +
+                                     ": not a number: '" + b + "'");
+        vals.push_back(v);
+      }
+      *count = vals.size();
+      if (vals.size() > capacity) fail(FL_INVALID_ARGUMENT, "vector_io: output too small");
+      if (vals.empty()) return;
+      if (!dev) {
+        std::memcpy(out, vals.data(), vals.size() * 8);
+        return;
+      }
+      Pinned st(vals.size());
+      std::memcpy(st.p, vals.data(), vals.size() * 8);
+      FLB_CUDA(cudaMemcpyAsync(out, st.p, vals.size() * 8, cudaMemcpyHostToDevice, s));
+      sync(s);
+      return;
+    }
+    unsigned char head[16];
+    if (std::fread(head, 1, 8, f) != 8 || std::memcmp(head, "FLEGVEC1", 8) != 0)
+      fail(FL_RUNTIME_ERROR, std::string(path) + ": bad magic, not a vector file");
+    if (std::fread(head + 8, 1, 8, f) != 8)
+      fail(FL_RUNTIME_ERROR, std::string(path) + ": truncated header");
+    const uint64_t n = le64(head + 8);
+    *count = (size_t)n;
+    if (n > capacity) fail(FL_INVALID_ARGUMENT, "vector_io: output too small");
+    // two pinned chunks: the H2D copy of one overlaps the read of the next
+    // (binary64 LE is the device's layout on x86 hosts: no per-element work)
+    const size_t chunk = std::min<size_t>(kIoChunk, n ? n : 1);
+    Pinned buf[2] = {Pinned(chunk), Pinned(chunk)};
+    cudaEvent_t done[2];
+    for (cudaEvent_t& e : done) FLB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    bool used[2] = {false, false};
+    size_t i0 = 0;
+    int b = 0;
+    bool ok = true;
+    while (i0 < n) {
+      const size_t m = std::min<size_t>(chunk, n - i0);
+      if (used[b]) FLB_CUDA(cudaEventSynchronize(done[b]));
+      if (std::fread(buf[b].p, 8, m, f) != m) {
+        ok = false;
+        break;
+      }
+      if (dev) {
+        FLB_CUDA(cudaMemcpyAsync(out + i0, buf[b].p, m * 8, cudaMemcpyHostToDevice, s));
+        FLB_CUDA(cudaEventRecord(done[b], s));
+        used[b] = true;
+      } else {
+        std::memcpy(out + i0, buf[b].p, m * 8);
+      }
+      i0 += m;
+      b ^= 1;
+    }
+    FLB_CUDA(cudaStreamSynchronize(s));
+    for (cudaEvent_t e : done) cudaEventDestroy(e);
+    if (!ok) fail(FL_RUNTIME_ERROR, std::string(path) + ": truncated payload");
+  });
+}
+
+fl_status fl_save_vector(const char* path, int format, const double* in, size_t n, void* stream) {
+  return guarded([&] {
+    if (format != 0 && format != 1) fail(FL_INVALID_ARGUMENT, "vector_io: unknown format");
+    FILE* f = std::fopen(path, "wb");
+    if (!f) fail(FL_RUNTIME_ERROR, std::string("cannot open for writing: ") + path);
+    struct Closer {
+      FILE* f;
+      ~Closer() { std::fclose(f); }
+    } closer{f};
+    const bool dev = is_device_ptr(in);
+    cudaStream_t s = as_stream(stream);
+    if (format == 1) {
+      unsigned char head[16];
+      std::memcpy(head, "FLEGVEC1", 8);
+      for (int i = 0; i < 8; ++i) head[8 + i] = (unsigned char)((uint64_t)n >> (8 * i));
+      if (std::fwrite(head, 1, 16, f) != 16) fail(FL_RUNTIME_ERROR, std::string("write failed: ") + path);
+    }
+    const size_t chunk = std::min<size_t>(kIoChunk, n ? n : 1);
+    Pinned buf[2] = {Pinned(chunk), Pinned(chunk)};
+    cudaEvent_t done[2];
+    for (cudaEvent_t& e : done) FLB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    // D2H of chunk i + 1 runs while chunk i is written
+    auto issue = [&](size_t i0, int b) {
+      const size_t m = std::min<size_t>(chunk, n - i0);
+      if (dev) {
+        FLB_CUDA(cudaMemcpyAsync(buf[b].p, in + i0, m * 8, cudaMemcpyDeviceToHost, s));
+        FLB_CUDA(cudaEventRecord(done[b], s));
+      } else {
+        std::memcpy(buf[b].p, in + i0, m * 8);
+      }
+    };
+    bool ok = true;
+    if (n) issue(0, 0);
+    int b = 0;
+    char txt[32];
+    for (size_t i0 = 0; i0 < n; i0 += chunk, b ^= 1) {
+      const size_t m = std::min<size_t>(chunk, n - i0);
+      if (dev) FLB_CUDA(cudaEventSynchronize(done[b]));
+      if (i0 + chunk < n) issue(i0 + chunk, b ^ 1);
+      if (format == 1) {
+        ok = ok && std::fwrite(buf[b].p, 8, m, f) == m;
+      } else {
+        for (size_t i = 0; i < m; ++i) {  // shortest round-trip decimal (vector_io.hpp:56-60)
+          const auto r = std::to_chars(txt, txt + sizeof txt, buf[b].p[i]);
+          *r.ptr = '\n';
+          ok = ok && std::fwrite(txt, 1, (size_t)(r.ptr + 1 - txt), f) == (size_t)(r.ptr + 1 - txt);
+        }
+      }
+    }
+    FLB_CUDA(cudaStreamSynchronize(s));
+    for (cudaEvent_t e : done) cudaEventDestroy(e);
+    if (!ok || std::fflush(f) != 0) fail(FL_RUNTIME_ERROR, std::string("write failed: ") + path);
+  });
 }
 
 void fl_random_decaying(size_t n, double decay, uint64_t seed, double* out, size_t batch,

@@ -262,3 +262,32 @@ def test_free_ndct_literal_when_truncation_is_visible():
     plan = fl.plan_ndct(n, fl.GridKind.cheb1, TOL)
     plan.reference.delta_theta = np.zeros(n)
     assert np.array_equal(fl.ndct_apply(plan, c), fl.dct_iii(c, fl.GridKind.cheb1))
+
+
+@pytest.mark.parametrize("n", [1024, 4096, 65536])
+def test_reduced_tolerance_dlt_idlt(n):
+    """SURVEY.md 8f row f4, tolerance 2^-23 (L = 5 chebstar / 10 cheb1 Taylor
+    terms in the reference). The literal factored path (FL_NDCT_LITERAL)
+    reproduces the reference's truncated evaluation to 1e-13 log2 N; the
+    defaults (the direct product for batches, the Chebyshev expansion to
+    2^-23 otherwise) stay within the reference's certified bound of it
+    (test_ndct.cpp:173-183): |f - f_ref| <= (2 bound + 1e-13 log2 N) ||.||_1."""
+    tol = 2.0 ** -23
+    for kind in (CHEB1, CHEBSTAR):
+        cfg = fl.TransformConfig(n, tol, K[kind])
+        g = cfg.grid()
+        c = fl.random_decaying(n, 0.5, 300 + n, batch=20)
+        refs = [O.dlt_grid(c[j], kind, tol, g.theta, g.x, g.weights) for j in (0, 19)]
+        bound = O.taylor_term_bound(kind, O.min_taylor_terms(kind, tol))
+        f_def = fl.dlt(c, cfg)
+        lit = fl.TransformConfig(n, tol, K[kind], grid=g, ndct_mode=fl.NDCT_LITERAL)
+        lit.set_dlt_method(fl.DLT_FACTORED)
+        f_lit = fl.dlt(c, lit)
+        for j, ref in zip((0, 19), refs):
+            chat = O.leg2cheb(c[j])
+            assert rel(f_lit[j], ref, np.abs(c[j]).sum()) <= tol_n(n), (kind, "literal", j)
+            lim = 2 * bound * np.abs(chat).sum() + tol_n(n) * np.abs(c[j]).sum()
+            assert np.max(np.abs(f_def[j] - ref)) <= lim, (kind, "default", j)
+        b_lit = fl.idlt(f_lit, lit).values
+        refb = O.idlt_grid(f_lit[0], kind, tol, g.theta, g.x, g.weights)
+        assert rel(b_lit[0], refb, np.abs(f_lit[0]).sum()) <= tol_n(n), (kind, "literal idlt")
