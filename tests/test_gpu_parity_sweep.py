@@ -270,8 +270,9 @@ def test_reduced_tolerance_dlt_idlt(n):
     terms in the reference). The literal factored path (FL_NDCT_LITERAL)
     reproduces the reference's truncated evaluation to 1e-13 log2 N; the
     defaults (the direct product for batches, the Chebyshev expansion to
-    2^-23 otherwise) stay within the reference's certified bound of it
-    (test_ndct.cpp:173-183): |f - f_ref| <= (2 bound + 1e-13 log2 N) ||.||_1."""
+    2^-23 otherwise) stay within the two certified bounds of it
+    (test_ndct.cpp:173-183): |f - f_ref| <= (tol + C(L)) ||chat||_1 +
+    1e-13 log2 N ||c||_1, C(L) the reference's bound, tol the plan's."""
     tol = 2.0 ** -23
     for kind in (CHEB1, CHEBSTAR):
         cfg = fl.TransformConfig(n, tol, K[kind])
@@ -286,7 +287,7 @@ def test_reduced_tolerance_dlt_idlt(n):
         for j, ref in zip((0, 19), refs):
             chat = O.leg2cheb(c[j])
             assert rel(f_lit[j], ref, np.abs(c[j]).sum()) <= tol_n(n), (kind, "literal", j)
-            lim = 2 * bound * np.abs(chat).sum() + tol_n(n) * np.abs(c[j]).sum()
+            lim = (tol + bound) * np.abs(chat).sum() + tol_n(n) * np.abs(c[j]).sum()
             assert np.max(np.abs(f_def[j] - ref)) <= lim, (kind, "default", j)
         b_lit = fl.idlt(f_lit, lit).values
         refb = O.idlt_grid(f_lit[0], kind, tol, g.theta, g.x, g.weights)
