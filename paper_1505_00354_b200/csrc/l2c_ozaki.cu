@@ -823,6 +823,17 @@ __global__ void __launch_bounds__(oz::THREADS, 1)
 #endif
 namespace oz2 {
 constexpr bool TS = FLB_OZ_TS && oz::S * oz::BN + 64 <= 512;
+// 0 (default): the next tile's MMAs wait until the whole TMEM is drained;
+// 1: the first K step is issued by accumulator in the drain order (all A
+// digits copied first); 2: the epilogue drains the most significant
+// accumulator first and the first K step's MMAs, in their usual order, wait
+// for their own accumulator only. Both overlaps measured slower (C4 DLT 12.9
+// and 13.2 vs 12.6 ms on one box): seven mbarrier waits in the single MMA
+// issuing thread cost more than the drain they hide.
+#ifndef FLB_OZ_ACC_OVERLAP
+#define FLB_OZ_ACC_OVERLAP 0
+#endif
+constexpr int ACC_OVERLAP = TS ? FLB_OZ_ACC_OVERLAP : 0;
 constexpr int A_TILE = oz::BM * oz::BK;            // 128 rows
 constexpr int B_TILE = (oz::BN / 2) * oz::BK;      // 32 columns: this CTA's half
 constexpr int STAGE_BYTES = oz::S * (A_TILE + B_TILE);
@@ -950,7 +961,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
   uint64_t* empty_b = bars + STAGES;       // each CTA's own (multicast commit)
   uint64_t* tfull_b = bars + 2 * STAGES;   // each CTA's own (multicast commit)
   uint64_t* tempty_b = bars + 2 * STAGES + 1;  // leader's (both epilogues arrive)
-  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2);
+  // FLB_OZ_ACC_OVERLAP: one "drained" barrier per accumulator (leader's; one
+  // arrival per epilogue warp of both CTAs), so the next tile's first MMAs
+  // into accumulator d start as soon as d has been read out
+  uint64_t* acc_b = bars + 2 * STAGES + 2;
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(bars + 2 * STAGES + 2 + S);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t rank = cluster_rank();
@@ -984,6 +999,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
     }
     mbar_init(smem_u32(tfull_b), 1);
     mbar_init(smem_u32(tempty_b), 2 * EPI_THREADS);
+    for (int d = 0; d < S; ++d) mbar_init(smem_u32(&acc_b[d]), 2 * (EPI_THREADS / 32));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -1037,8 +1053,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
         size_t cb, rp;
         int p, kb_lo, nk;
         tile_coords(tile, cb, p, rp, kb_lo, nk);
-        mbar_wait(smem_u32(tempty_b), (t & 1u) ^ 1u);  // both epilogues drained TMEM
-        tc_fence_after();
+        if constexpr (!oz2::ACC_OVERLAP) {
+          mbar_wait(smem_u32(tempty_b), (t & 1u) ^ 1u);  // both epilogues drained TMEM
+          tc_fence_after();
+        }
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const uint32_t st = it % STAGES, ph = (it / STAGES) & 1u;
           mbar_wait(smem_u32(&full_b[st]), ph);
@@ -1046,7 +1064,83 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
           const uint32_t sa = smem_u32(smem + st * STAGE_BYTES);
           const uint64_t ad0 = smem_desc(sa), bd0 = smem_desc(sa + S * A_TILE);
           const uint32_t first = kb == 0 ? 0u : 1u;
-          if constexpr (oz2::TS) {
+          if (oz2::ACC_OVERLAP == 1 && kb == 0) {
+            // the tile's first K step, by accumulator in the epilogue's drain
+            // order (least significant first): all S A-digit tiles into S
+            // slots, then for d = S-1 .. 0 wait until both epilogues have read
+            // accumulator d of the previous tile and issue the pairs
+            // (i, d - i), the first one (i = 0) overwriting it
+#pragma unroll
+            for (int i = 0; i < S; ++i)
+              tc2_cp_128x256(tmem + (uint32_t)(S * BN + ((aslot + i) & 7u) * 8u),
+                             ad0 + (uint64_t)((i * A_TILE) >> 4));
+#pragma unroll
+            for (int d = S - 1; d >= 0; --d) {
+              mbar_wait(smem_u32(&acc_b[d]), (t & 1u) ^ 1u);
+              tc_fence_after();
+#pragma unroll
+              for (int i = 0; i <= d; ++i) {
+                const uint64_t bd = bd0 + (uint64_t)(((d - i) * B_TILE) >> 4);
+                tc2_mma_i8_ts(tmem + (uint32_t)(d * BN), tmem + (uint32_t)(S * BN + ((aslot + i) & 7u) * 8u),
+                              bd, oz2::IDESC, i > 0 ? 1u : 0u);
+              }
+            }
+            aslot += S;
+            // the remaining K steps of this block in the usual order
+            if constexpr (BK / 32 > 1) {
+              tc2_cp_128x256(tmem + (uint32_t)(S * BN + (aslot & 7u) * 8u),
+                             ad0 + (uint64_t)(32 >> 4));
+#pragma unroll
+              for (int ks = 1; ks < BK / 32; ++ks) {
+#pragma unroll
+                for (int i = 0; i < S; ++i, ++aslot) {
+                  const uint32_t ta = tmem + (uint32_t)(S * BN + (aslot & 7u) * 8u);
+                  if (i + 1 < S || ks + 1 < BK / 32) {
+                    const int ni = i + 1 < S ? i + 1 : 0, nks = i + 1 < S ? ks : ks + 1;
+                    tc2_cp_128x256(tmem + (uint32_t)(S * BN + ((aslot + 1) & 7u) * 8u),
+                                   ad0 + (uint64_t)((ni * A_TILE + nks * 32) >> 4));
+                  }
+#pragma unroll
+                  for (int j = 0; i + j < S; ++j) {
+                    const uint64_t bd = bd0 + (uint64_t)((j * B_TILE + ks * 32) >> 4);
+                    tc2_mma_i8_ts(tmem + (uint32_t)((i + j) * BN), ta, bd, oz2::IDESC, 1u);
+                  }
+                }
+              }
+            }
+          } else if constexpr (oz2::TS) {
+          if (oz2::ACC_OVERLAP == 2 && kb == 0) {
+            // the tile's first K step: the (0, j) MMA overwrites accumulator j
+            // once both epilogues have read it (drained 0 .. S-1, in this order)
+            tc2_cp_128x256(tmem + (uint32_t)(S * BN + (aslot & 7u) * 8u), ad0);
+            tc2_cp_128x256(tmem + (uint32_t)(S * BN + ((aslot + 1) & 7u) * 8u),
+                           ad0 + (uint64_t)((A_TILE) >> 4));
+#pragma unroll
+            for (int j = 0; j < S; ++j) {
+              mbar_wait(smem_u32(&acc_b[j]), (t & 1u) ^ 1u);
+              tc_fence_after();
+              tc2_mma_i8_ts(tmem + (uint32_t)(j * BN), tmem + (uint32_t)(S * BN + (aslot & 7u) * 8u),
+                            bd0 + (uint64_t)((j * B_TILE) >> 4), oz2::IDESC, 0u);
+            }
+            ++aslot;
+#pragma unroll
+            for (int ks = 0; ks < BK / 32; ++ks) {
+#pragma unroll
+              for (int i = ks == 0 ? 1 : 0; i < S; ++i, ++aslot) {
+                const uint32_t ta = tmem + (uint32_t)(S * BN + (aslot & 7u) * 8u);
+                if ((i + 1 < S || ks + 1 < BK / 32) && !(ks == 0 && i == 0)) {
+                  const int ni = i + 1 < S ? i + 1 : 0, nks = i + 1 < S ? ks : ks + 1;
+                  tc2_cp_128x256(tmem + (uint32_t)(S * BN + ((aslot + 1) & 7u) * 8u),
+                                 ad0 + (uint64_t)((ni * A_TILE + nks * 32) >> 4));
+                }
+#pragma unroll
+                for (int j = 0; i + j < S; ++j) {
+                  const uint64_t bd = bd0 + (uint64_t)((j * B_TILE + ks * 32) >> 4);
+                  tc2_mma_i8_ts(tmem + (uint32_t)((i + j) * BN), ta, bd, oz2::IDESC, 1u);
+                }
+              }
+            }
+          } else {
           // A digit tiles through TMEM: each (K-step, digit) tile is copied
           // once into one of 8 rotating 8-column slots after the S x 64
           // accumulator columns and read there by its S - i MMAs (the copy
@@ -1075,6 +1169,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
               }
             }
           }
+          }
           } else {
 #pragma unroll
           for (int i = 0; i < S; ++i) {
@@ -1100,6 +1195,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
     const int q = warp & 3;
     const int row = q * 32 + lane;
     const uint32_t tempty_leader = map_to_rank(smem_u32(tempty_b), 0);
+    const uint32_t acc_leader = map_to_rank(smem_u32(acc_b), 0);
     uint32_t t = 0;
     size_t tile;
     for (size_t ti = 0; tile_of(ti, tile); ++ti, ++t) {
@@ -1113,7 +1209,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
 #pragma unroll
       for (int c = 0; c < BN; ++c) acc[c] = 0.0;
 #pragma unroll 1
-      for (int d = S - 1; d >= 0; --d) {
+      for (int dd = S - 1; dd >= 0; --dd) {
+        // (overlap 2: the most significant accumulator first, so the next
+        // tile's first MMAs -- into accumulator 0 first -- can start)
+        const int d = oz2::ACC_OVERLAP == 2 ? S - 1 - dd : dd;
         // exact S_d 2^{-DB(d+2)} without the int->fp64 conversion unit: the
         // biased integer becomes the low mantissa bits of a double whose ulp
         // is 2^{-DB(d+2)}; subtracting the bias constant is exact
@@ -1125,6 +1224,11 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
         for (int h = 0; h < BN / 32; ++h)
           tmem_ld32_nowait(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(d * BN + h * 32), v[h]);
         tmem_wait_ld();
+        if constexpr (oz2::ACC_OVERLAP) {  // accumulator d read out: the next tile may overwrite it
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive_remote(acc_leader + 8u * (uint32_t)d);
+        }
 #pragma unroll
         for (int h = 0; h < BN / 32; ++h)
 #pragma unroll
@@ -1132,7 +1236,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(oz::THREADS, 1)
             acc[h * 32 + c] += __hiloint2double(hi_word, (int)(v[h][c] ^ 0x80000000u)) - bias;
       }
       tc_fence_before();
-      mbar_arrive_remote(tempty_leader);  // TMEM free for the pair's next tile
+      if constexpr (!oz2::ACC_OVERLAP) mbar_arrive_remote(tempty_leader);  // TMEM free for the pair's next tile
       const double ascale = arow[(size_t)p * r + rb * BM + row];
       store_tile(out, acc, ascale, bcol, mode, p, rb * BM + row, cb, r, cols, ld);
     }
