@@ -42,6 +42,8 @@
 #include <mutex>
 #include <tuple>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "fast_ndct.cuh"
 #include "fft.cuh"
@@ -71,6 +73,7 @@ struct FastNdct {
   double* bes_wf = nullptr;  // forward weights, owned-row order
   double* bes_wt = nullptr;  // transpose weights, tr_slot order
   double* bes_tt = nullptr;  // transpose row factors T_m(n/N), tr_row order
+  double* cl_wf = nullptr;   // forward weights in the cluster kernel's thread order (2^14..2^16)
 };
 
 namespace {
@@ -229,6 +232,32 @@ __constant__ double kC8[16][2] = {
     {-0.3826834323650898, -0.9238795325112867}, {0.0, -1.0}, {0.3826834323650898, -0.9238795325112867},
     {0.7071067811865476, -0.7071067811865476}, {0.9238795325112867, -0.3826834323650898}};
 
+// The pack arithmetic from the four stage values (stage[m], stage[m + P],
+// stage[N - m], stage[P - m]); m0: m == 0.
+template <bool ODD, int R, bool HALF = false>
+__device__ __forceinline__ double2 fwd_pack_vals(double s_m, double s_mp, double s_nm, double s_pm,
+                                                 bool m0, double2 ta_t, double2 r4_t) {
+  constexpr double h = 0.70710678118654752440;
+  // X_j = a_j / 2 (X_0 = a_0, X_N = 0); a = stage (DCT) or the reversed stage (DST)
+  constexpr double hf = HALF ? 1.0 : 0.5;  // (multiplications by 1.0 fold away)
+  const double xa = ODD ? (m0 ? 0.0 : hf * s_nm) : (m0 ? (HALF ? 2.0 * s_m : s_m) : hf * s_m);
+  const double xan = m0 ? 0.0 : hf * (ODD ? s_m : s_nm);
+  const double xb = hf * (ODD ? s_pm : s_mp);
+  const double xbn = hf * (ODD ? s_mp : s_pm);
+  constexpr double a32x = PackConst::c32[R][0], a32y = PackConst::c32[R][1];
+  constexpr double a8x = PackConst::c8[R][0], a8y = PackConst::c8[R][1];
+  // e^{i pi m/(2N)}, e^{i pi (m+P)/(2N)} = e^{i pi/4} e^{i pi m/(2N)}, e^{2 pi i m/N}
+  const double2 ta = make_double2(ta_t.x * a32x - ta_t.y * a32y, ta_t.x * a32y + ta_t.y * a32x);
+  const double2 tb = make_double2(h * (ta.x - ta.y), h * (ta.x + ta.y));
+  const double2 r4 = make_double2(r4_t.x * a8x - r4_t.y * a8y, r4_t.x * a8y + r4_t.y * a8x);
+  const double2 Wa = make_double2(ta.x * xa + ta.y * xan, ta.y * xa - ta.x * xan);
+  const double2 Wb = make_double2(tb.x * xb + tb.y * xbn, tb.y * xb - tb.x * xbn);
+  const double2 s = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
+  const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
+  const double2 dr = make_double2(d.x * r4.x - d.y * r4.y, d.x * r4.y + d.y * r4.x);
+  return make_double2(s.x - dr.y, s.y + dr.x);  // s + i dr
+}
+
 // Packed Z_m of the forward transform for term parity ODD, m = t + r T.
 // ta_t = e^{i pi t/(2N)}, r4_t = e^{2 pi i t/N} (per-thread bases).
 // The pack of Z_m reads stage entries {m, m + P, N - m, P - m} (both term
@@ -247,7 +276,6 @@ __device__ __forceinline__ double2 fwd_pack(const double* stage, double* next, i
                                             double2 r4_t, bool* bad = nullptr,
                                             double2* own = nullptr) {
   constexpr int P = N / 2;
-  constexpr double h = 0.70710678118654752440;
   const double s_m = stage[m], s_mp = stage[m + P];
   if (own) *own = make_double2(s_m, s_mp);
   if (bad) *bad |= !isfinite(s_m) || !isfinite(s_mp);
@@ -259,25 +287,7 @@ __device__ __forceinline__ double2 fwd_pack(const double* stage, double* next, i
     next[m] = fma(2.0 * ((double)m / (double)N), s_m, -next[m]);
     next[m + P] = fma(2.0 * ((double)(m + P) / (double)N), s_mp, -next[m + P]);
   }
-  // X_j = a_j / 2 (X_0 = a_0, X_N = 0); a = stage (DCT) or the reversed stage (DST)
-  const bool m0 = m == 0;
-  constexpr double hf = HALF ? 1.0 : 0.5;  // (multiplications by 1.0 fold away)
-  const double xa = ODD ? (m0 ? 0.0 : hf * s_nm) : (m0 ? (HALF ? 2.0 * s_m : s_m) : hf * s_m);
-  const double xan = m0 ? 0.0 : hf * (ODD ? s_m : s_nm);
-  const double xb = hf * (ODD ? s_pm : s_mp);
-  const double xbn = hf * (ODD ? s_mp : s_pm);
-  constexpr double a32x = PackConst::c32[R][0], a32y = PackConst::c32[R][1];
-  constexpr double a8x = PackConst::c8[R][0], a8y = PackConst::c8[R][1];
-  // e^{i pi m/(2N)}, e^{i pi (m+P)/(2N)} = e^{i pi/4} e^{i pi m/(2N)}, e^{2 pi i m/N}
-  const double2 ta = make_double2(ta_t.x * a32x - ta_t.y * a32y, ta_t.x * a32y + ta_t.y * a32x);
-  const double2 tb = make_double2(h * (ta.x - ta.y), h * (ta.x + ta.y));
-  const double2 r4 = make_double2(r4_t.x * a8x - r4_t.y * a8y, r4_t.x * a8y + r4_t.y * a8x);
-  const double2 Wa = make_double2(ta.x * xa + ta.y * xan, ta.y * xa - ta.x * xan);
-  const double2 Wb = make_double2(tb.x * xb + tb.y * xbn, tb.y * xb - tb.x * xbn);
-  const double2 s = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
-  const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
-  const double2 dr = make_double2(d.x * r4.x - d.y * r4.y, d.x * r4.y + d.y * r4.x);
-  return make_double2(s.x - dr.y, s.y + dr.x);  // s + i dr
+  return fwd_pack_vals<ODD, R, HALF>(s_m, s_mp, s_nm, s_pm, m == 0, ta_t, r4_t);
 }
 
 // The rows thread t of the forward kernel accumulates: the outputs of its
@@ -1579,6 +1589,234 @@ __host__ __device__ inline double bessel_weight(int m, double y) {
   return -2.0 * ((((m - 1) >> 1) & 1) ? -j : j);
 }
 
+// ---------------------------------------------------------------------------
+// 8192 < N <= 2^16: the forward Chebyshev-expansion NDCT of one column fused
+// on a thread-block CLUSTER, all terms on chip. The N/2-point
+// complex FFT of each term is a four-step over CS = N/8192 CTAs:
+//   P = CS Q (Q = 4096), m = CS m2 + m1 (CTA m1 packs Z at its m2 = t + T r),
+//   Y_{m1}[k1] = sum_{m2} Z_{CS m2 + m1} w_Q^{m2 k1}      (local smem FFT)
+//   z_{k1 + Q k2} = sum_{m1} (w_P^{m1 k1} Y_{m1}[k1]) w_CS^{m1 k2}
+//                                     (CTA s: k1 in [s Q/CS, (s+1) Q/CS), the
+//                                      Y rows of all CTAs read through DSMEM)
+// (inverse transforms, w = e^{+2 pi i/.}). The stage T_m(n/N) c lives in the
+// CTAs' shared memory (entry n = CS a + m1 at st[a]); the pack's mirror
+// entries N - m, P - m sit in CTA (CS - m1) mod CS and are read through DSMEM;
+// the previous stage stays in registers; the 16 outputs a thread's z values
+// map to accumulate in registers over all terms with weights from a table in
+// thread order (signs folded in). Two cluster barriers per term: Y rows
+// complete (and every pack done, so the stage may be updated), and every
+// Y read / stage write done before the next term. c is read once, f written
+// once; the Z / Y traffic stays in shared memory (~94 % of it local).
+template <int LOG2N>
+struct ClCfg {
+  static constexpr int N = 1 << LOG2N, P = N / 2;
+  static constexpr int Q = 4096;          // local FFT points per CTA
+  static constexpr int CS = P / Q;        // CTAs per column
+  static constexpr int T = 512, E = 8;    // threads, local points per thread
+  static constexpr int KQ = Q / CS;       // step-C k1 per CTA
+  static constexpr int D = KQ / T;        // k1 per thread
+  static constexpr int OUTS = 2 * D * CS;  // outputs per thread (16)
+  // the stage, the previous stage (own entries only), the FFT row
+  static constexpr size_t SMEM = (size_t)4 * Q * sizeof(double) + (size_t)smem_row(Q) * sizeof(double2);
+  static_assert(CS >= 2 && CS <= 8 && KQ % T == 0 && OUTS == 16, "2^14 <= N <= 2^16");
+};
+
+// Output row of slot i (= 2 (d CS + k2) + part) of thread t in CTA s.
+template <int LOG2N>
+__host__ __device__ __forceinline__ int cl_out_row(int s, int t, int i) {
+  using C = ClCfg<LOG2N>;
+  const int part = i & 1, zi = i >> 1, d = zi / C::CS, k2 = zi % C::CS;
+  const int k = s * C::KQ + t + d * C::T + C::Q * k2;  // z index
+  const int q = 2 * k + part;
+  return q < C::N / 2 ? 2 * q : 2 * (C::N - 1 - q) + 1;
+}
+
+template <int LOG2N>
+__global__ void __launch_bounds__(512, 1)
+    cluster_ndct_fwd_kernel(const double* __restrict__ in, size_t ld_in, double* __restrict__ out,
+                            size_t ld_out, int terms, int swap, const double* __restrict__ wt,
+                            const double2* __restrict__ tw4n, const double2* __restrict__ fftw,
+                            int* nonfinite) {
+  namespace cg = cooperative_groups;
+  using C = ClCfg<LOG2N>;
+  constexpr int N = C::N, Q = C::Q, CS = C::CS, T = C::T, E = C::E, KQ = C::KQ, D = C::D;
+  extern __shared__ double smem[];
+  double* st = smem;                                        // 2Q stage entries
+  double* pv = smem + 2 * Q;                                // T_{m-1} c at the same entries
+  double2* Y = reinterpret_cast<double2*>(smem + 4 * Q);   // the local FFT row
+  cg::cluster_group cl = cg::this_cluster();
+  const int m1 = (int)cl.block_rank();
+  const size_t col = blockIdx.x / CS;
+  const int t = threadIdx.x;
+  const double* rst = cl.map_shared_rank(st, (CS - m1) % CS);  // the mirror CTA's stage
+  const double* src = in + col * ld_in;
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < E; ++i)
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      const int a = h * Q + t + T * i;
+      const double v = src[(size_t)CS * a + m1];
+      bad |= !isfinite(v);
+      st[a] = v;
+    }
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
+  // step-C twiddle e^{+2 pi i r k1 / P} = e^{2 pi i (8 r k1) / (4N)}: tw4n holds
+  // the first half circle, the second is its negation
+  auto step_tw = [&](int r, int k1) -> double2 {
+    const int q = (8 * r * k1) & (4 * N - 1);
+    const double2 w = __ldg(&tw4n[q & (2 * N - 1)]);
+    return q >= 2 * N ? make_double2(-w.x, -w.y) : w;
+  };
+  // the 16 output accumulators live in the thread's TMEM lane (32 columns;
+  // 16 warps = 4 per lane quarter): no register spills around the FFT
+  __shared__ uint32_t tmem_base;
+  const int warp = t >> 5;
+  if (warp == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 128;" ::"r"(
+                     static_cast<uint32_t>(__cvta_generic_to_shared(&tmem_base)))
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tF = tmem_base + ((uint32_t)(32 * (warp & 3)) << 16) + 32u * (uint32_t)(warp >> 2);
+  {
+    uint32_t z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) tm_st8(tF + 8 * q, z);
+    tm_wait_st();
+  }
+  const int tp = CS * t + m1;  // Z index m = tp + (N/16) r: the pack's twiddle bases
+  const double2 ta_t = __ldg(&tw4n[tp]);
+  const double2 r4_t = __ldg(&tw4n[4 * tp]);
+  cl.sync();  // every CTA's stage loaded (the first pack reads the mirror's)
+  for (int m = 0; m < terms; ++m) {
+    const bool odd = ((m & 1) ^ swap) != 0;
+    double2 v[E];
+#define FLB_CL_PACK(R)                                                                     \
+  {                                                                                        \
+    const int m2 = t + T * (R);                                                            \
+    const int a_nm = m1 ? 2 * Q - 1 - m2 : (2 * Q - m2) & (2 * Q - 1);                     \
+    const int a_pm = m1 ? Q - 1 - m2 : Q - m2;                                             \
+    const double s_m = st[m2], s_mp = st[Q + m2], s_nm = rst[a_nm], s_pm = rst[a_pm];      \
+    const bool m0 = m1 == 0 && m2 == 0;                                                    \
+    v[R] = odd ? fwd_pack_vals<true, R>(s_m, s_mp, s_nm, s_pm, m0, ta_t, r4_t)             \
+               : fwd_pack_vals<false, R>(s_m, s_mp, s_nm, s_pm, m0, ta_t, r4_t);           \
+  }
+    FLB_CL_PACK(0) FLB_CL_PACK(1) FLB_CL_PACK(2) FLB_CL_PACK(3)
+    FLB_CL_PACK(4) FLB_CL_PACK(5) FLB_CL_PACK(6) FLB_CL_PACK(7)
+#undef FLB_CL_PACK
+    pass_compute<Q, E, 8, 1, true>(v, t, fftw);
+    pass_store<Q, E, 8, 1>(v, Y, t);
+    __syncthreads();
+    mid_passes<Q, E, 8, Q, true, 0>(Y, t, fftw, 0);
+    cl.sync();  // (1) every Y row final, every pack of this term done
+    // the next stage T_{m+1}(x) c at the own entries (x = n/N)
+#pragma unroll
+    for (int i = 0; i < E; ++i)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int a = h * Q + t + T * i;
+        const double x = (double)(CS * a + m1) / (double)N;
+        const double cur = st[a];
+        st[a] = m == 0 ? x * cur : fma(2.0 * x, cur, -pv[a]);
+        pv[a] = cur;
+      }
+    // step C: the CS-point inverse DFTs across the cluster, then the unpack
+    const double* w = wt + ((size_t)m * CS + m1) * 16 * T + t;
+#pragma unroll
+    for (int d = 0; d < D; ++d) {
+      const int k1 = m1 * KQ + t + d * T;
+      double2 y[CS];
+#pragma unroll
+      for (int r = 0; r < CS; ++r) {
+        const double2 a = cl.map_shared_rank(Y, r)[smem_pad(k1)];
+        y[r] = r ? cmul(a, step_tw(r, k1)) : a;
+      }
+      dft_r<CS, true>(y);
+      // this d's 2 CS outputs: slots 2 CS d .. (8 per TMEM x8 access of 4 doubles)
+#pragma unroll
+      for (int g = 0; g < CS / 2; ++g) {
+        uint32_t fw[8];
+        const uint32_t addr = tF + (uint32_t)(2 * (2 * CS * d + 4 * g));
+        tm_ld8(addr, fw);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int i = 2 * CS * d + 4 * g + u, k2 = (4 * g + u) >> 1;
+          const double val = (u & 1) ? y[k2].y : y[k2].x;
+          split2(join2(&fw[2 * u]) + __ldg(w + (size_t)i * T) * val, &fw[2 * u]);
+        }
+        tm_st8(addr, fw);
+      }
+    }
+    tm_wait_st();
+    cl.sync();  // (2) every Y read and stage write done before the next term
+  }
+  double* dst = out + col * ld_out;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t fw[8];
+    tm_ld8(tF + 8 * q, fw);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) dst[cl_out_row<LOG2N>(m1, t, 4 * q + u)] = join2(&fw[2 * u]);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 128;" ::"r"(tmem_base) : "memory");
+}
+
+// The cluster kernel's weights: wt[((m CS + s) 16 + i) T + t] = the term-m
+// weight of output row cl_out_row(s, t, i), with the sine flavour's sign and
+// the DST's (-1)^k output sign folded in.
+template <int LOG2N>
+__global__ void cluster_weight_table_kernel(const double* __restrict__ delta, int terms, int swap,
+                                            double* __restrict__ wt) {
+  using C = ClCfg<LOG2N>;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;  // (s 16 + i) T + t
+  if (j >= C::N) return;
+  const int t = j % C::T, si = j / C::T, i = si % 16, sct = si / 16;
+  const int k = cl_out_row<LOG2N>(sct, t, i);
+  const double y = (double)C::N * delta[k];
+  for (int m = 0; m < terms; ++m) {
+    const bool odd = ((m & 1) ^ swap) != 0;
+    double w = ((swap && (m & 1)) ? -1.0 : 1.0) * bessel_weight(m, y);
+    if (odd && (k & 1)) w = -w;
+    wt[(size_t)m * C::N + j] = w;
+  }
+}
+
+template <int LOG2N>
+void launch_cluster_fwd(const double* in, size_t ld_in, double* out, size_t ld_out, size_t batch,
+                        const FastNdct& p, int* nonfinite, cudaStream_t s) {
+  using C = ClCfg<LOG2N>;
+  auto kern = cluster_ndct_fwd_kernel<LOG2N>;
+  FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)C::SMEM));
+  const double2* tw = tw4n_table(LOG2N);
+  const double2* fftw = pass_twiddles(12);
+  cudaLaunchConfig_t cfg = {};
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = C::CS;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.blockDim = dim3(C::T);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  constexpr size_t kMaxCols = 65535 / C::CS;
+  for (size_t c0 = 0; c0 < batch; c0 += kMaxCols) {
+    const size_t nc = std::min(kMaxCols, batch - c0);
+    cfg.gridDim = dim3((unsigned)(nc * C::CS));
+    FLB_CUDA(cudaLaunchKernelEx(&cfg, kern, in + c0 * ld_in, ld_in, out + c0 * ld_out, ld_out,
+                                p.bes_terms, p.swap, (const double*)p.cl_wf, tw, fftw, nonfinite));
+    note_launch("cluster_ndct_fwd_kernel");
+  }
+}
+
 template <int LOG2N>
 __global__ void bessel_tables_kernel(const double* __restrict__ delta, int terms,
                                      double* __restrict__ wf, double* __restrict__ wt,
@@ -1872,6 +2110,25 @@ void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* 
   const bool cheb = bes && bes->bes_terms > 0 && plain_op < 0;
   if (cheb) num_terms = bes->bes_terms;
   if (l_hi < 0) l_hi = num_terms;
+#ifndef FLB_NDCT_CLUSTER
+#define FLB_NDCT_CLUSTER 1
+#endif
+  // the cluster kernel wins once its CTAs fill the GPU at least twice (one
+  // column occupies N/8192 SMs for all its terms): 16384 x 256 0.74 vs 1.11 ms,
+  // 32768 x 128 0.92 vs 1.16 ms, 65536 x 512 7.7 vs 8.9 ms; at 65536 x 64
+  // (C2, 3.5 waves) it ties the multi-pass path (1.25 vs 1.21 ms), and a
+  // single column is latency-bound on N/8192 SMs (0.26 vs 0.16 ms at 16384)
+  const size_t cs = (size_t(1) << log2n) / 8192;
+  const bool cl_fill = batch * cs >= 2 * (size_t)sm_count() && (log2n < 16 || batch >= 128);
+  if (FLB_NDCT_CLUSTER && cheb && !transpose && bes->cl_wf && l_lo == 0 && l_hi == num_terms &&
+      log2n >= 14 && log2n <= 16 && cl_fill) {
+    switch (log2n) {
+      case 14: launch_cluster_fwd<14>(in, ld_in, out, ld_out, batch, *bes, nonfinite, s); break;
+      case 15: launch_cluster_fwd<15>(in, ld_in, out, ld_out, batch, *bes, nonfinite, s); break;
+      default: launch_cluster_fwd<16>(in, ld_in, out, ld_out, batch, *bes, nonfinite, s); break;
+    }
+    return;
+  }
   if (log2n > 13) {
     launch_big(log2n, transpose, in, ld_in, out, ld_out, batch, delta, l_lo, l_hi, plain_op, mult,
                nonfinite, s, cheb ? 1 : 0, cheb ? bes->swap : 0);
@@ -2017,6 +2274,23 @@ void build_bessel_tables(FastNdct* p, int M, cudaStream_t s) {
   note_launch("bessel_tables_kernel");
 }
 
+// The cluster kernel's weight table (2^14 <= N <= 2^16, forward).
+void build_cluster_table(FastNdct* p, int M, cudaStream_t s) {
+  if (p->log2n < 14 || p->log2n > 16) return;
+  const size_t n = p->n;
+  if (p->async_alloc)
+    FLB_CUDA(cudaMallocAsync(&p->cl_wf, (size_t)M * n * sizeof(double), s));
+  else
+    FLB_CUDA(cudaMalloc(&p->cl_wf, (size_t)M * n * sizeof(double)));
+  const unsigned grid = (unsigned)((n + 255) / 256);
+  switch (p->log2n) {
+    case 14: cluster_weight_table_kernel<14><<<grid, 256, 0, s>>>(p->delta, M, p->swap, p->cl_wf); break;
+    case 15: cluster_weight_table_kernel<15><<<grid, 256, 0, s>>>(p->delta, M, p->swap, p->cl_wf); break;
+    default: cluster_weight_table_kernel<16><<<grid, 256, 0, s>>>(p->delta, M, p->swap, p->cl_wf); break;
+  }
+  note_launch("cluster_weight_table_kernel");
+}
+
 FastNdct* fast_ndct_create(size_t n, double tol, int kind, const double* delta) {
   const int lg = log2_exact(n);
   if (lg < kFastMinLog2 || lg > kFastMaxLog2) return nullptr;
@@ -2038,6 +2312,7 @@ FastNdct* fast_ndct_create(size_t n, double tol, int kind, const double* delta) 
   const int M = bessel_terms(tol);
   if (FLB_NDCT_BESSEL && M > 0 && M < L) p->bes_terms = M;  // multi-pass: weights on the fly
   if (FLB_NDCT_BESSEL && lg <= 13 && M > 0 && M < L) build_bessel_tables(p, M, 0);
+  if (p->bes_terms > 0) build_cluster_table(p, M, 0);
   return p;
 }
 
@@ -2088,12 +2363,13 @@ FastNdct* fast_ndct_create_bessel(size_t n, int kind, const double* delta, int n
   p->num_terms = M;
   p->bes_terms = M;
   if (lg <= 13) build_bessel_tables(p, M, s);
+  build_cluster_table(p, M, s);
   return p;
 }
 
 void fast_ndct_destroy(FastNdct* p) {
   if (!p) return;
-  for (double* t : {p->owned_delta, p->bes_wf, p->bes_wt, p->bes_tt}) {
+  for (double* t : {p->owned_delta, p->bes_wf, p->bes_wt, p->bes_tt, p->cl_wf}) {
     if (!t) continue;
     if (p->async_alloc)
       cudaFreeAsync(t, p->alloc_stream);
