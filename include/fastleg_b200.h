@@ -162,17 +162,35 @@ int fl_plan_ndct_mode(const fl_plan* plan);
 fl_status fl_set_free_ndct_mode(int mode);
 int fl_free_ndct_mode(void);
 
-/* Legendre -> Chebyshev conversion inside dlt/idlt of plans with n >= 2^15
+/* Legendre -> Chebyshev conversion inside dlt/idlt of plans with n >= 2^14
  * and at most 16 columns:
  *   0 = FL_LEG2CHEB_DIRECT : the reference's O(N^2) triangular product;
- *   1 = FL_LEG2CHEB_FAST   : Toeplitz-Hankel factorisation, per parity
+ *   1 = FL_LEG2CHEB_FAST   : (default) the asymptotic expansion (mode 2) for
+ *       power-of-two n >= 2^20, Toeplitz-Hankel (mode 3) otherwise;
+ *   3 = FL_LEG2CHEB_TOEPLITZ : Toeplitz-Hankel factorisation, per parity
  *       A = T .* H with H ~ sum_r l_r l_r^T (pivoted Cholesky, residual
  *       <= 1e-17, so |error| <= 1e-17 ||c||_1), applied as K FFT-based
- *       Toeplitz products (default).
- * fl_plan_leg2cheb_rank returns K for a parity (0 when not built). */
-enum { FL_LEG2CHEB_DIRECT = 0, FL_LEG2CHEB_FAST = 1 };
+ *       Toeplitz products;
+ *   2 = FL_LEG2CHEB_ASYMPTOTIC : Hale-Townsend asymptotic expansion of
+ *       P_n(cos t) at the N cheb1 points (power-of-two N in [2^10, 2^26]):
+ *       per level 2M DCT-III/DST-III of diagonally scaled inputs with
+ *       diagonal output weights, the low degrees by a chunked three-term
+ *       recurrence, then one DCT-II (plans of other sizes keep mode 1).
+ *       Replaces conversion.hpp:100-140 like mode 1.
+ * fl_plan_leg2cheb_rank returns K for a parity (0 when not built);
+ * fl_plan_leg2cheb_asy_info the asymptotic method's expansion terms M, its
+ * levels, its length-N transforms per column and its recurrence steps / N
+ * (building the method's tables on first call). */
+enum {
+  FL_LEG2CHEB_DIRECT = 0,
+  FL_LEG2CHEB_FAST = 1,
+  FL_LEG2CHEB_ASYMPTOTIC = 2,
+  FL_LEG2CHEB_TOEPLITZ = 3
+};
 fl_status fl_plan_set_leg2cheb_mode(fl_plan* plan, int mode);
 int fl_plan_leg2cheb_rank(const fl_plan* plan, int parity);
+fl_status fl_plan_leg2cheb_asy_info(const fl_plan* plan, int* terms, int* levels,
+                                    int* transforms, double* recurrence_steps_per_n);
 
 /* Arithmetic of the direct (dense, triangular) conversion product inside
  * dlt/idlt of plans with more than 16 columns:

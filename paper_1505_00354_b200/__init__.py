@@ -10,7 +10,7 @@ reference's header API; ``include/fastleg/*.hpp`` is the C++ one.
 from ._lib import (  # noqa: F401
     DomainError, FastlegCudaError, FastlegError, InvalidArgument, OverflowErrorFL,
     RuntimeErrorFL, device_available, launch_count, set_free_ndct_mode, free_ndct_mode, NDCT_FAST,
-    NDCT_LITERAL, LEG2CHEB_DIRECT, LEG2CHEB_FAST, GEMM_FP64, GEMM_INT8_SPLIT, DLT_FACTORED, DLT_DIRECT,
+    NDCT_LITERAL, LEG2CHEB_DIRECT, LEG2CHEB_FAST, LEG2CHEB_ASYMPTOTIC, LEG2CHEB_TOEPLITZ, GEMM_FP64, GEMM_INT8_SPLIT, DLT_FACTORED, DLT_DIRECT,
 )
 from .api import *  # noqa: F401,F403
 from .api import (  # noqa: F401

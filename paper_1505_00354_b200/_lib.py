@@ -17,7 +17,7 @@ FL_OK, FL_INVALID_ARGUMENT, FL_DOMAIN_ERROR, FL_OVERFLOW_ERROR, FL_RUNTIME_ERROR
 CHEB1, CHEBSTAR = 0, 1
 DCT_III, DST_III, DCT_III_T, DST_III_T = range(4)
 NDCT_LITERAL, NDCT_FAST = 0, 1
-LEG2CHEB_DIRECT, LEG2CHEB_FAST = 0, 1
+LEG2CHEB_DIRECT, LEG2CHEB_FAST, LEG2CHEB_ASYMPTOTIC, LEG2CHEB_TOEPLITZ = 0, 1, 2, 3
 GEMM_FP64, GEMM_INT8_SPLIT = 0, 1
 DLT_FACTORED, DLT_DIRECT = 0, 1
 
@@ -67,7 +67,7 @@ EXPORTS = [
     "fl_plan_stage_terms", "fl_dlt_stage", "fl_plan_set_gemm_mode", "fl_plan_gemm_mode",
     "fl_plan_leg2cheb", "fl_plan_ndct", "fl_plan_ndct_terms", "fl_set_free_ndct_mode",
     "fl_free_ndct_mode", "fl_plan_set_dlt_method", "fl_plan_dlt_method", "fl_plan_uses_direct",
-    "fl_load_vector", "fl_save_vector",
+    "fl_load_vector", "fl_save_vector", "fl_plan_leg2cheb_asy_info",
 ]
 
 
@@ -125,6 +125,7 @@ def _load() -> C.CDLL:
         "fl_plan_uses_direct": (i, [vp, sz]),
         "fl_load_vector": (i, [C.c_char_p, i, dp, sz, C.POINTER(sz), vp]),
         "fl_save_vector": (i, [C.c_char_p, i, dp, sz, vp]),
+        "fl_plan_leg2cheb_asy_info": (i, [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(d)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

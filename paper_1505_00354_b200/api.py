@@ -409,12 +409,24 @@ class TransformConfig:  # transforms.hpp:19-38
         check(LIB.fl_plan_set_ndct_mode(self._h, int(mode)))
 
     def set_leg2cheb_mode(self, mode: int) -> None:
-        """LEG2CHEB_DIRECT (reference O(N^2) product) or LEG2CHEB_FAST
-        (Toeplitz-Hankel, plans with n >= 2^15, <= 16 columns)."""
+        """LEG2CHEB_DIRECT (reference O(N^2) product), LEG2CHEB_FAST (default:
+        the asymptotic expansion for power-of-two n >= 2^20, else
+        Toeplitz-Hankel), LEG2CHEB_TOEPLITZ (Toeplitz-Hankel, n >= 2^14) or
+        LEG2CHEB_ASYMPTOTIC (Hale-Townsend asymptotic expansion, power-of-two
+        n in [2^10, 2^26]); the fast modes apply to <= 16 columns."""
         check(LIB.fl_plan_set_leg2cheb_mode(self._h, int(mode)))
 
     def leg2cheb_rank(self, parity: int = 0) -> int:
         return int(LIB.fl_plan_leg2cheb_rank(self._h, int(parity)))
+
+    def leg2cheb_asy_info(self) -> dict:
+        """The asymptotic conversion's shape: expansion terms M, levels,
+        length-N transforms per column, recurrence (point, degree) steps / N."""
+        m, lv, tr = C.c_int(), C.c_int(), C.c_int()
+        st = C.c_double()
+        check(LIB.fl_plan_leg2cheb_asy_info(self._h, C.byref(m), C.byref(lv), C.byref(tr), C.byref(st)))
+        return {"terms": m.value, "levels": lv.value, "transforms": tr.value,
+                "recurrence_steps_per_n": st.value}
 
     def set_gemm_mode(self, mode: int) -> None:
         """GEMM_INT8_SPLIT (default: exact split-integer conversion product on

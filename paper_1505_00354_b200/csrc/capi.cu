@@ -20,6 +20,7 @@
 #include "direct.cuh"
 #include "fast_ndct.cuh"
 #include "launch.cuh"
+#include "l2c_asy.cuh"
 #include "l2c_fast.cuh"
 #include "l2c_ozaki.cuh"
 #include "leg2cheb.cuh"
@@ -452,7 +453,9 @@ struct fl_plan {
   double* s = nullptr;       // n  (scaled Lambda)
   FastNdct* fast = nullptr;  // cheb1-internal NDCT (power-of-two n), or null
   L2CFast* l2c = nullptr;    // Toeplitz-Hankel leg2cheb (n >= kL2CFastMin), or null
-  int l2c_mode = 1;          // 1: fast conversion for few columns when available; 0: direct
+  int l2c_mode = 1;          // 1: fast conversion for few columns when available; 0: direct;
+                             // 2: asymptotic expansion (power-of-two n), else as 1
+  L2CAsy* asy = nullptr;     // asymptotic-expansion leg2cheb (lazy, mode 2)
   int gemm_mode = FL_GEMM_INT8_SPLIT;  // arithmetic of the direct conversion product
   L2COzaki* oz[2] = {nullptr, nullptr};  // split-int8 slices of M, (m + 1/2) M^T (lazy)
   int dlt_method = FL_DLT_DIRECT;        // dlt/idlt: dense product where supported
@@ -467,6 +470,7 @@ void plan_free(fl_plan* p) {
     if (q) cudaFree(q);
   if (p->fast) fast_ndct_destroy(p->fast);
   if (p->l2c) l2c_fast_destroy(p->l2c);
+  if (p->asy) l2c_asy_destroy(p->asy);
   for (L2COzaki* o : p->oz) l2c_ozaki_destroy(o);
   for (L2COzaki* o : p->dense) l2c_ozaki_destroy(o);
   delete p;
@@ -520,6 +524,19 @@ const L2COzaki* plan_dense(fl_plan* p, int idlt, size_t batch, cudaStream_t s) {
   return p->dense[idlt];
 }
 
+// The asymptotic-expansion conversion of the plan (built on first use and
+// published once its tables are complete, as plan_ozaki).
+const L2CAsy* plan_asy(fl_plan* p, cudaStream_t s) {
+  if (!l2c_asy_supported(p->n)) return nullptr;
+  std::lock_guard<std::mutex> lock(p->mu);
+  if (!p->asy) {
+    L2CAsy* a = l2c_asy_create(p->n, p->s, s);
+    FLB_CUDA(cudaStreamSynchronize(s));
+    p->asy = a;
+  }
+  return p->asy;
+}
+
 // The plan's conversion product (transforms.hpp:47 / :62): chat = M in, or
 // (m + 1/2) M^T in for the inverse; device columns of stride n.
 // in: columns of stride n; out: stride ld_out. The conversion kernels take a
@@ -535,7 +552,14 @@ void plan_convert(fl_plan* p, int transpose, const double* in, double* out, size
                                cudaMemcpyDeviceToDevice, s));
     return;
   }
-  if (p->l2c && p->l2c_mode == 1 && batch <= kL2CFastMaxCols)
+  // FAST: the asymptotic expansion where it beats Toeplitz-Hankel (power-of-two
+  // n >= 2^20: 2.4 vs 2.9 ms at 2^20, 172 vs 288 ms at 2^26), else Toeplitz-Hankel
+  const bool want_asy = p->l2c_mode == FL_LEG2CHEB_ASYMPTOTIC ||
+                        (p->l2c_mode == FL_LEG2CHEB_FAST && p->n >= kL2CAsyMin);
+  const L2CAsy* asy = want_asy && batch <= kL2CFastMaxCols ? plan_asy(p, s) : nullptr;
+  if (asy)
+    l2c_asy_apply(*asy, transpose, in, out, batch, n, transpose, s);
+  else if (p->l2c && p->l2c_mode != FL_LEG2CHEB_DIRECT && batch <= kL2CFastMaxCols)
     l2c_fast_apply(*p->l2c, transpose, in, out, batch, n, transpose, s);
   else if (const L2COzaki* oz = plan_ozaki(p, transpose, batch, s))
     l2c_ozaki_apply(*oz, in, out, batch, n, s);
@@ -713,7 +737,19 @@ fl_status fl_leg2cheb(int transpose, size_t n, const double* lambda_table, size_
     DevOut o(out, n, batch, ld, s);
     if (i.ld != o.ld) fail(FL_RUNTIME_ERROR, "fastleg: host/device stride mix unsupported");
     if (i.ptr == o.ptr) fail(FL_INVALID_ARGUMENT, "leg2cheb: input and output must not alias");
-    if (n >= (size_t(1) << 17) && batch <= kL2CFastMaxCols) {
+    if (l2c_asy_supported(n) && n >= kL2CAsyMin && batch <= kL2CFastMaxCols) {
+      // large power-of-two vectors: the asymptotic expansion (tables from this Lambda table)
+      L2CAsy* f = l2c_asy_create(n, sc.p, s);
+      try {
+        l2c_asy_apply(*f, transpose, i.ptr, o.ptr, batch, o.ld, 0, s);
+      } catch (...) {
+        FLB_CUDA(cudaStreamSynchronize(s));
+        l2c_asy_destroy(f);
+        throw;
+      }
+      FLB_CUDA(cudaStreamSynchronize(s));
+      l2c_asy_destroy(f);
+    } else if (n >= (size_t(1) << 17) && batch <= kL2CFastMaxCols) {
       // large single vectors: build the low-rank factors for this table once
       L2CFast* f = l2c_fast_create(n, sc.p, s);
       try {
@@ -909,9 +945,25 @@ fl_status fl_dlt_stage(const fl_plan* p, int inverse, int stage, int lo, int hi,
 
 fl_status fl_plan_set_leg2cheb_mode(fl_plan* p, int mode) {
   return guarded([&] {
-    if (mode != FL_LEG2CHEB_DIRECT && mode != FL_LEG2CHEB_FAST)
+    if (mode != FL_LEG2CHEB_DIRECT && mode != FL_LEG2CHEB_FAST && mode != FL_LEG2CHEB_ASYMPTOTIC &&
+        mode != FL_LEG2CHEB_TOEPLITZ)
       fail(FL_INVALID_ARGUMENT, "plan: unknown leg2cheb mode");
     p->l2c_mode = mode;
+  });
+}
+
+fl_status fl_plan_leg2cheb_asy_info(const fl_plan* p, int* terms, int* levels, int* transforms,
+                                    double* steps) {
+  return guarded([&] {
+    if (!p) fail(FL_INVALID_ARGUMENT, "plan: null");
+    FLB_CUDA(cudaSetDevice(p->device));
+    const L2CAsy* a = plan_asy(const_cast<fl_plan*>(p), 0);
+    if (!a) fail(FL_INVALID_ARGUMENT, "leg2cheb: no asymptotic conversion for this size");
+    const L2CAsyInfo i = l2c_asy_info(*a);
+    if (terms) *terms = i.M;
+    if (levels) *levels = i.levels;
+    if (transforms) *transforms = i.transforms;
+    if (steps) *steps = i.rec_steps_per_n;
   });
 }
 

@@ -1,0 +1,47 @@
+// Asymptotic-expansion Legendre <-> Chebyshev conversion for large N
+// (Hale & Townsend 2014, the fast leg2cheb the paper cites; north-star
+// subsystem 2). Replaces the O(N^2) loops of conversion.hpp:100-140 for
+// single vectors / few columns at power-of-two N.
+//
+// chat = M c is computed as the Chebyshev coefficients of the Legendre
+// series sampled at the N cheb1 points t_k = (k + 1/2) pi / N:
+//   f_k = sum_n c_n P_n(cos t_k),   chat_j = (2 - delta_j0)/N sum_k f_k cos(j t_k).
+// P_n(cos t) = C_n sum_{m<M} h_{m,n} cos((n+m+1/2) t - (m+1/2) pi/2) / (2 sin t)^{m+1/2} + R_M
+// for the degrees n >= nu_l of the point's level l (|R_M| <= eps there), so each
+// of the M terms is a DCT-III and a DST-III of the diagonally scaled input
+// (c_n C_n h_{m,n}, n >= nu_l) with a diagonal output weight; the degrees below
+// a point's cutoff come from the three-term recurrence (a chunked, transfer-
+// matrix-parallel warp kernel). M^T is the exact transpose of the same steps.
+#pragma once
+#include <cuda_runtime.h>
+#include <stddef.h>
+
+namespace flb {
+
+struct L2CAsy;
+
+// n: a power of two in [2^10, 2^26]; s: the device scaled Lambda table
+// (s_j = Lambda(j)/Lambda(0), n entries). M (expansion terms), R (level
+// ratio), max_levels (-1: all levels the tolerance allows; fewer trade
+// length-N transforms for recurrence steps): 0 / -1 = defaults
+// (FLB_ASY_M / FLB_ASY_R / FLB_ASY_LEVELS override them).
+L2CAsy* l2c_asy_create(size_t n, const double* s, cudaStream_t st, int M = 0, int R = 0,
+                       int max_levels = -1);
+void l2c_asy_destroy(L2CAsy* f);
+bool l2c_asy_supported(size_t n);
+// Size from which the plan's FAST conversion mode uses the expansion instead of
+// Toeplitz-Hankel (single vectors / <= 16 columns).
+constexpr size_t kL2CAsyMin = size_t(1) << 20;
+
+// out = M in (transpose 0) or M^T in (1, optional (n + 1/2) output scaling);
+// columns of stride ld; in and out must not alias.
+void l2c_asy_apply(const L2CAsy& f, int transpose, const double* in, double* out, size_t cols,
+                   size_t ld, int scale_half, cudaStream_t st);
+
+struct L2CAsyInfo {
+  int M, levels, transforms;   // transforms: length-N real DCT/DST per column
+  double rec_steps_per_n;      // recurrence (point, degree) steps / N
+};
+L2CAsyInfo l2c_asy_info(const L2CAsy& f);
+
+}  // namespace flb
