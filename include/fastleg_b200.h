@@ -251,16 +251,25 @@ int fl_plan_ndct_terms(const fl_plan* plan);
  * vector, C5). Both stages of fl_dlt are sums of independent terms, so P
  * ranks each take a slice and one collective sums the partials
  * (paper_1505_00354_b200/distributed.py):
- *   FL_STAGE_LEG2CHEB : chat = sum_{r in [lo,hi)} D(l_r) T D(l_r) c, the
- *                       Toeplitz-Hankel rank terms of M (idlt: M^T with (m+1/2));
+ *   FL_STAGE_LEG2CHEB : the conversion the plan runs for one column, as a
+ *                       sum of terms: with the asymptotic expansion (power-of-
+ *                       two n >= 2^20, FL_LEG2CHEB_FAST) its (level, m)
+ *                       DCT/DST pairs, then its recurrence bands (each partial
+ *                       ends with the DCT-II, which is linear); with
+ *                       Toeplitz-Hankel chat = sum_{r in [lo,hi)} D(l_r) T
+ *                       D(l_r) c, its rank terms (idlt: M^T with (m+1/2));
  *   FL_STAGE_NDCT     : f = sum_{m in [lo,hi)} term m of the fast-mode NDCT
  *                       (the Chebyshev-expansion terms about cheb1, 14 at
  *                       2^-52; idlt: the transpose, with the quadrature
  *                       weights).
  * One column; needs the fast paths (n >= 2^15 and a power of two > 8192).
- * fl_plan_stage_terms gives the number of terms of a stage. */
+ * fl_plan_stage_terms gives the number of terms of a stage,
+ * fl_plan_stage_cost a term's relative cost (the asymptotic conversion's
+ * terms differ: a (level, m) pair is two length-n transforms, a recurrence
+ * band its pairs x degrees; all other terms 1) for a balanced split. */
 enum { FL_STAGE_LEG2CHEB = 0, FL_STAGE_NDCT = 1 };
 fl_status fl_plan_stage_terms(const fl_plan* plan, int stage, int* count);
+fl_status fl_plan_stage_cost(const fl_plan* plan, int stage, int term, double* cost);
 fl_status fl_dlt_stage(const fl_plan* plan, int inverse, int stage, int lo, int hi,
                        const double* in, double* out, void* stream);
 

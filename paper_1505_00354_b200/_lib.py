@@ -67,7 +67,7 @@ EXPORTS = [
     "fl_plan_stage_terms", "fl_dlt_stage", "fl_plan_set_gemm_mode", "fl_plan_gemm_mode",
     "fl_plan_leg2cheb", "fl_plan_ndct", "fl_plan_ndct_terms", "fl_set_free_ndct_mode",
     "fl_free_ndct_mode", "fl_plan_set_dlt_method", "fl_plan_dlt_method", "fl_plan_uses_direct",
-    "fl_load_vector", "fl_save_vector", "fl_plan_leg2cheb_asy_info",
+    "fl_load_vector", "fl_save_vector", "fl_plan_leg2cheb_asy_info", "fl_plan_stage_cost",
 ]
 
 
@@ -126,6 +126,7 @@ def _load() -> C.CDLL:
         "fl_load_vector": (i, [C.c_char_p, i, dp, sz, C.POINTER(sz), vp]),
         "fl_save_vector": (i, [C.c_char_p, i, dp, sz, vp]),
         "fl_plan_leg2cheb_asy_info": (i, [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(d)]),
+        "fl_plan_stage_cost": (i, [vp, i, i, C.POINTER(d)]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

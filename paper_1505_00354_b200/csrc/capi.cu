@@ -537,6 +537,13 @@ const L2CAsy* plan_asy(fl_plan* p, cudaStream_t s) {
   return p->asy;
 }
 
+// Whether the plan converts `batch` columns by the asymptotic expansion.
+bool plan_wants_asy(const fl_plan* p, size_t batch) {
+  return l2c_asy_supported(p->n) && batch <= kL2CFastMaxCols &&
+         (p->l2c_mode == FL_LEG2CHEB_ASYMPTOTIC ||
+          (p->l2c_mode == FL_LEG2CHEB_FAST && p->n >= kL2CAsyMin));
+}
+
 // The plan's conversion product (transforms.hpp:47 / :62): chat = M in, or
 // (m + 1/2) M^T in for the inverse; device columns of stride n.
 // in: columns of stride n; out: stride ld_out. The conversion kernels take a
@@ -554,9 +561,7 @@ void plan_convert(fl_plan* p, int transpose, const double* in, double* out, size
   }
   // FAST: the asymptotic expansion where it beats Toeplitz-Hankel (power-of-two
   // n >= 2^20: 2.4 vs 2.9 ms at 2^20, 172 vs 288 ms at 2^26), else Toeplitz-Hankel
-  const bool want_asy = p->l2c_mode == FL_LEG2CHEB_ASYMPTOTIC ||
-                        (p->l2c_mode == FL_LEG2CHEB_FAST && p->n >= kL2CAsyMin);
-  const L2CAsy* asy = want_asy && batch <= kL2CFastMaxCols ? plan_asy(p, s) : nullptr;
+  const L2CAsy* asy = plan_wants_asy(p, batch) ? plan_asy(p, s) : nullptr;
   if (asy)
     l2c_asy_apply(*asy, transpose, in, out, batch, n, transpose, s);
   else if (p->l2c && p->l2c_mode != FL_LEG2CHEB_DIRECT && batch <= kL2CFastMaxCols)
@@ -899,6 +904,11 @@ fl_status fl_plan_stage_terms(const fl_plan* p, int stage, int* count) {
   return guarded([&] {
     *count = 0;
     if (stage == FL_STAGE_LEG2CHEB) {
+      if (plan_wants_asy(p, 1)) {
+        FLB_CUDA(cudaSetDevice(p->device));
+        *count = l2c_asy_terms(*plan_asy(const_cast<fl_plan*>(p), 0));
+        return;
+      }
       if (!p->l2c) fail(FL_INVALID_ARGUMENT, "dlt_stage: no Toeplitz-Hankel conversion for this size");
       *count = std::max(l2c_fast_rank(*p->l2c, 0), l2c_fast_rank(*p->l2c, 1));
     } else if (stage == FL_STAGE_NDCT) {
@@ -908,6 +918,18 @@ fl_status fl_plan_stage_terms(const fl_plan* p, int stage, int* count) {
     } else {
       fail(FL_INVALID_ARGUMENT, "dlt_stage: unknown stage");
     }
+  });
+}
+
+fl_status fl_plan_stage_cost(const fl_plan* p, int stage, int term, double* cost) {
+  return guarded([&] {
+    int count = 0;
+    const fl_status st = fl_plan_stage_terms(p, stage, &count);
+    if (st != FL_OK) fail(st, fl_last_error());
+    if (term < 0 || term >= count) fail(FL_INVALID_ARGUMENT, "dlt_stage: term out of bounds");
+    *cost = stage == FL_STAGE_LEG2CHEB && plan_wants_asy(p, 1)
+                ? l2c_asy_term_cost(*plan_asy(const_cast<fl_plan*>(p), 0), term)
+                : 1.0;
   });
 }
 
@@ -926,7 +948,11 @@ fl_status fl_dlt_stage(const fl_plan* p, int inverse, int stage, int lo, int hi,
     if (lo == hi) {
       FLB_CUDA(cudaMemsetAsync(o.ptr, 0, n * sizeof(double), s));
     } else if (stage == FL_STAGE_LEG2CHEB) {
-      l2c_fast_apply(*p->l2c, inverse, i.ptr, o.ptr, 1, n, inverse, s, lo, hi);
+      if (plan_wants_asy(p, 1))
+        l2c_asy_apply(*plan_asy(const_cast<fl_plan*>(p), s), inverse, i.ptr, o.ptr, 1, n, inverse, s, lo,
+                      hi);
+      else
+        l2c_fast_apply(*p->l2c, inverse, i.ptr, o.ptr, 1, n, inverse, s, lo, hi);
     } else {
       DevScratch<int> flag(1, s);
       FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));

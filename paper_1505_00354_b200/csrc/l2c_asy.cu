@@ -321,15 +321,17 @@ __global__ void __launch_bounds__(kRecThreads) asy_rec_fwd_kernel(
 // f_k = E + O, f_{N-1-k} = E - O (written: the expansion levels add to it)
 __global__ void asy_rec_fwd_finish_kernel(const __grid_constant__ RecTab t, const double2* __restrict__ Ep,
                                           double* __restrict__ F, size_t ldF, long long n) {
-  const long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x;
-  if (p >= n / 2) return;
+  const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i >= t.ngslots) return;
   const size_t col = blockIdx.y;
   Ep += col * t.nslots;
   F += col * ldF;
   int b = 0;
-  while (b + 1 < t.nb && p >= t.b[b + 1].p0) ++b;
+  while (b + 1 < t.nb && i >= t.b[b + 1].gbase) ++b;
   const RecBand& B = t.b[b];
-  const long long loc = p - B.p0, g = loc / kPairsPerWarp, slot = loc % kPairsPerWarp;
+  const long long loc = i - B.gbase, g = loc / kPairsPerWarp, slot = loc % kPairsPerWarp;
+  const long long p = B.p0 + loc;
+  if (p >= B.p1) return;
   const long long base = B.ibase + g * (long long)B.Q * kPairsPerWarp + slot;
   double E = 0.0, O = 0.0;
   for (int q = 0; q < B.Q; ++q) {
@@ -486,7 +488,8 @@ __global__ void __launch_bounds__(256) asy_rec_tr_finish_kernel(const __grid_con
 
 // ---- expansion levels: forward pack (u_{m,n} of every level of the batch and
 // every term, DCT-III and DST-III packing into N/2-point complex rows) --------
-__global__ void __launch_bounds__(256) asy_fwd_pack_kernel(const __grid_constant__ LevTab lt, int l0, const double* __restrict__ c,
+__global__ void __launch_bounds__(256) asy_fwd_pack_kernel(const __grid_constant__ LevTab lt, int l0, int m0,
+                                                           int nm, const double* __restrict__ c,
                                                            size_t ld, const double* __restrict__ Cn,
                                                            long long n, size_t nc,
                                                            double2* __restrict__ Z) {
@@ -494,7 +497,6 @@ __global__ void __launch_bounds__(256) asy_fwd_pack_kernel(const __grid_constant
   const size_t col = blockIdx.y;
   const int lv = blockIdx.z;
   const long long nu = lt.nu[l0 + lv];
-  const int M = lt.M;
   const double* cc = c + col * ld;
   const double nd = (double)n;
   for (long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x; m < P;
@@ -519,16 +521,17 @@ __global__ void __launch_bounds__(256) asy_fwd_pack_kernel(const __grid_constant
       const double2 dr = make_double2(dd2.x * c4 - dd2.y * s4, dd2.x * s4 + dd2.y * c4);
       return make_double2(sm.x - dr.y, sm.y + dr.x);
     };
-    for (int tm = 0; tm < M; ++tm) {
+    for (int tm = 0; tm < m0 + nm; ++tm) {
       if (tm > 0) {
 #pragma unroll
         for (int r = 0; r < 4; ++r) h[r] = h[r] * lt.hk[tm] / ((double)js[r] + (double)tm + 0.5);
       }
+      if (tm < m0) continue;
       const double st0 = bs[0] * h[0], st1 = bs[1] * h[1], st2 = bs[2] * h[2], st3 = bs[3] * h[3];
       // DCT-III: X(0) = st(0), X(j) = st(j)/2; DST-III: X(0) = 0, X(j) = st(N - j)/2
       const double2 zc = emit(m == 0 ? st0 : 0.5 * st0, m == 0 ? 0.0 : 0.5 * st1, 0.5 * st2, 0.5 * st3);
       const double2 zs = emit(m == 0 ? 0.0 : 0.5 * st1, m == 0 ? 0.0 : 0.5 * st0, 0.5 * st3, 0.5 * st2);
-      const size_t tr = ((size_t)(lv * M + tm) * 2) * nc + col;
+      const size_t tr = ((size_t)(lv * nm + tm - m0) * 2) * nc + col;
       Z[tr * P + m] = zc;
       Z[(tr + nc) * P + m] = zs;
     }
@@ -551,13 +554,13 @@ __device__ __forceinline__ void asy_weights(long long k, long long pk, double nd
 
 // ---- expansion levels: forward unpack at the points of the batch's levels ---
 __global__ void __launch_bounds__(256) asy_fwd_unpack_kernel(const __grid_constant__ LevTab lt, int l0, int l1,
+                                                             int m0, int nm,
                                                              const double2* __restrict__ Z, long long n,
                                                              size_t nc, double* __restrict__ F,
                                                              size_t ldF) {
   const long long P = n / 2;
   const size_t col = blockIdx.y;
   const long long lo = lt.pb[l1], hi = lt.pb[l0], cnt = hi - lo;
-  const int M = lt.M;
   const double nd = (double)n;
   for (long long idx = blockIdx.x * (long long)blockDim.x + threadIdx.x; idx < 2 * cnt;
        idx += (long long)gridDim.x * blockDim.x) {
@@ -570,9 +573,10 @@ __global__ void __launch_bounds__(256) asy_fwd_unpack_kernel(const __grid_consta
     const double sgn = (k & 1) ? -1.0 : 1.0;
     double2 g, rho;
     asy_weights(k, pk, nd, g, rho);
+    for (int tm = 0; tm < m0; ++tm) g = cmul(g, rho);
     double acc = 0.0;
-    for (int tm = 0; tm < M; ++tm) {
-      const size_t tr = ((size_t)(lv * M + tm) * 2) * nc + col;
+    for (int tm = 0; tm < nm; ++tm) {
+      const size_t tr = ((size_t)(lv * nm + tm) * 2) * nc + col;
       const double2 zc = Z[tr * P + qi], zs = Z[(tr + nc) * P + qi];
       const double yc = comp ? zc.y : zc.x;
       const double ys = sgn * (comp ? zs.y : zs.x);
@@ -584,13 +588,13 @@ __global__ void __launch_bounds__(256) asy_fwd_unpack_kernel(const __grid_consta
 }
 
 // ---- expansion levels: transposed pack (weighted values of the level's points)
-__global__ void __launch_bounds__(256) asy_tr_pack_kernel(const __grid_constant__ LevTab lt, int l0, const double* __restrict__ F,
+__global__ void __launch_bounds__(256) asy_tr_pack_kernel(const __grid_constant__ LevTab lt, int l0, int m0,
+                                                          int nm, const double* __restrict__ F,
                                                           size_t ldF, long long n, size_t nc,
                                                           double2* __restrict__ Z) {
   const long long P = n / 2;
   const size_t col = blockIdx.y;
   const int lv = blockIdx.z, l = l0 + lv;
-  const int M = lt.M;
   const double nd = (double)n;
   const double* f = F + col * ldF;
   for (long long m = blockIdx.x * (long long)blockDim.x + threadIdx.x; m < P;
@@ -610,14 +614,15 @@ __global__ void __launch_bounds__(256) asy_tr_pack_kernel(const __grid_constant_
       any |= in;
       if (in) {
         asy_weights(k, pk, nd, g[e], rho[e]);
+        for (int tm = 0; tm < m0; ++tm) g[e] = cmul(g[e], rho[e]);
       } else {
         g[e] = make_double2(0.0, 0.0);
         rho[e] = make_double2(0.0, 0.0);
       }
     }
     const double s0 = (ks[0] & 1) ? -1.0 : 1.0, s1 = (ks[1] & 1) ? -1.0 : 1.0;
-    for (int tm = 0; tm < M; ++tm) {
-      const size_t tr = ((size_t)(lv * M + tm) * 2) * nc + col;
+    for (int tm = 0; tm < nm; ++tm) {
+      const size_t tr = ((size_t)(lv * nm + tm) * 2) * nc + col;
       double2 zc = make_double2(0.0, 0.0), zs = zc;
       if (any) {
         zc = make_double2(fv[0] * g[0].x, fv[1] * g[1].x);
@@ -645,13 +650,13 @@ __device__ __forceinline__ double tr_unpack_value(double2 za, double2 zb, double
 // The outputs r in {a, P - a, P + a, 2P - a} read the same two entries a, P - a
 // of every packed row: one thread per a in [0, P/2] computes all four.
 __global__ void __launch_bounds__(256) asy_tr_unpack_kernel(const __grid_constant__ LevTab lt, int l0,
-                                                            int l1, const double2* __restrict__ Z,
+                                                            int l1, int m0, int nm,
+                                                            const double2* __restrict__ Z,
                                                             long long n, size_t nc,
                                                             const double* __restrict__ Cn,
                                                             double* __restrict__ out, size_t ld) {
   const long long P = n / 2;
   const size_t col = blockIdx.y;
-  const int M = lt.M;
   const double nd = (double)n;
   for (long long a = blockIdx.x * (long long)blockDim.x + threadIdx.x; a <= P / 2;
        a += (long long)gridDim.x * blockDim.x) {
@@ -680,8 +685,14 @@ __global__ void __launch_bounds__(256) asy_tr_unpack_kernel(const __grid_constan
       const long long nu = lt.nu[l0 + lv];
 #pragma unroll
       for (int e = 0; e < 4; ++e) h[e] = 1.0;
-      for (int tm = 0; tm < M; ++tm) {
-        const size_t tr = ((size_t)(lv * M + tm) * 2) * nc + col;
+      for (int tm = 0; tm < m0 + nm; ++tm) {
+        if (tm < m0) {
+#pragma unroll
+          for (int e = 0; e < 4; ++e)
+            if (tm > 0) h[e] = h[e] * lt.hk[tm] / ((double)r[e] + (double)tm + 0.5);
+          continue;
+        }
+        const size_t tr = ((size_t)(lv * nm + tm - m0) * 2) * nc + col;
         const double2* Zc = Z + tr * P;
         const double2* Zs = Z + (tr + nc) * P;
         const double2 ca = Zc[a], cb = Zc[bq], sa = Zs[a], sb = Zs[bq];
@@ -727,6 +738,8 @@ struct L2CAsy {
   int M = 0;
   LevTab lt{};
   RecTab rt{};
+  int nbands = 0;
+  RecBand band_all[kMaxBands];  // the bands in term order (stage terms L M ...)
   double* Cn = nullptr;
   double2* ab = nullptr;
   long long rec_steps = 0;  // (point, degree) recurrence steps
@@ -851,6 +864,8 @@ L2CAsy* l2c_asy_create(size_t n, const double* s, cudaStream_t st, int M, int R,
   rt.nslots = ib;
   rt.ngslots = gb;
   rt.nrows = rb;
+  f->nbands = rt.nb;
+  for (int b = 0; b < rt.nb; ++b) f->band_all[b] = rt.b[b];
   FLB_CUDA(cudaMalloc(&f->Cn, n * sizeof(double)));
   FLB_CUDA(cudaMalloc(&f->ab, n * sizeof(double2)));
   asy_tables_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(N, s, f->Cn, f->ab);
@@ -915,9 +930,9 @@ int levels_per_batch(const L2CAsy& f, size_t nc) {
   return (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(f.lt.L, 1), budget / per_level));
 }
 
-void recurrence_forward(const L2CAsy& f, const double* c, size_t ld, double* F, size_t cols,
-                        cudaStream_t s) {
-  const RecTab& rt = f.rt;
+void recurrence_forward(const L2CAsy& f, const RecTab& rt, const double* c, size_t ld, double* F,
+                        size_t cols, cudaStream_t s) {
+  if (rt.nb == 0) return;
   const long long n = (long long)f.n;
   const double nd = (double)n;
   AsyncBuf<double4> T(rt.nslots, s);
@@ -930,27 +945,29 @@ void recurrence_forward(const L2CAsy& f, const double* c, size_t ld, double* F, 
   note_launch("asy_rec_prefix_kernel");
   asy_rec_fwd_kernel<<<dim3(wg, (unsigned)cols), kRecThreads, 0, s>>>(rt, f.ab, c, ld, St.p, Ep.p, nd);
   note_launch("asy_rec_fwd_kernel");
-  asy_rec_fwd_finish_kernel<<<dim3(grid_for(n / 2, 256, 1ll << 31), (unsigned)cols), 256, 0, s>>>(
+  asy_rec_fwd_finish_kernel<<<dim3(grid_for(rt.ngslots, 256, 1ll << 31), (unsigned)cols), 256, 0, s>>>(
       rt, Ep.p, F, ld, n);
   note_launch("asy_rec_fwd_finish_kernel");
 }
 
-void recurrence_transpose(const L2CAsy& f, const double* F, size_t ld, double* out, size_t cols,
-                          int scale_half, cudaStream_t s) {
-  const RecTab& rt = f.rt;
+void recurrence_transpose(const L2CAsy& f, const RecTab& rt, const double* F, size_t ld, double* out,
+                          size_t cols, int scale_half, cudaStream_t s) {
   const long long n = (long long)f.n;
   const double nd = (double)n;
   AsyncBuf<double4> T(rt.nslots, s);
   AsyncBuf<double2> St(rt.nslots, s);
   AsyncBuf<double> R(rt.nrows * cols, s);
-  asy_rec_transfer_kernel<<<grid_for(rt.nwarps * 32, kRecThreads, 1ll << 31), kRecThreads, 0, s>>>(
-      rt, f.ab, nd, T.p);
-  note_launch("asy_rec_transfer_kernel");
-  asy_rec_prefix_kernel<<<grid_for(rt.ngslots, 128, 1ll << 31), 128, 0, s>>>(rt, T.p, St.p, nd);
-  note_launch("asy_rec_prefix_kernel");
-  asy_rec_tr_kernel<<<dim3(grid_for(rt.nxwarps * 32, kRecThreads, 1ll << 31), (unsigned)cols),
+  if (rt.nb > 0) {
+    asy_rec_transfer_kernel<<<grid_for(rt.nwarps * 32, kRecThreads, 1ll << 31), kRecThreads, 0, s>>>(
+        rt, f.ab, nd, T.p);
+    note_launch("asy_rec_transfer_kernel");
+    asy_rec_prefix_kernel<<<grid_for(rt.ngslots, 128, 1ll << 31), 128, 0, s>>>(rt, T.p, St.p, nd);
+    note_launch("asy_rec_prefix_kernel");
+    asy_rec_tr_kernel<<<dim3(grid_for(rt.nxwarps * 32, kRecThreads, 1ll << 31), (unsigned)cols),
                       kRecThreads, 0, s>>>(rt, f.ab, F, ld, St.p, R.p, nd, n);
-  note_launch("asy_rec_tr_kernel");
+    note_launch("asy_rec_tr_kernel");
+  }
+  // (also without bands: the (n + 1/2) scaling of the whole output)
   asy_rec_tr_finish_kernel<<<dim3((unsigned)(n / 32), (unsigned)cols), 256, 0, s>>>(rt, R.p, out, ld, n,
                                                                                    scale_half);
   note_launch("asy_rec_tr_finish_kernel");
@@ -958,31 +975,88 @@ void recurrence_transpose(const L2CAsy& f, const double* F, size_t ld, double* o
 
 }  // namespace
 
+int l2c_asy_terms(const L2CAsy& f) { return f.lt.L * f.M + f.nbands; }
+
+double l2c_asy_term_cost(const L2CAsy& f, int term) {
+  // measured on one B200 at 2^26: a level term (two length-N transforms with
+  // their pack / unpack) ~27.7 ps per coefficient, a recurrence pair-step ~0.67 ps
+  if (term < f.lt.L * f.M) return 27.7 * (double)f.n;
+  const RecBand& B = f.band_all[term - f.lt.L * f.M];
+  return 0.67 * (double)(B.p1 - B.p0) * (double)B.nu;
+}
+
 void l2c_asy_apply(const L2CAsy& f, int transpose, const double* in, double* out, size_t cols,
-                   size_t ld, int scale_half, cudaStream_t s) {
+                   size_t ld, int scale_half, cudaStream_t s, int t_lo, int t_hi) {
   if (cols == 0) return;
   keep_scratch_pool();
   const long long n = (long long)f.n, P = n / 2;
   const int log2n = __builtin_ctzll((unsigned long long)n);
-  const int L = f.lt.L, M = f.M;
+  const int L = f.lt.L, M = f.M, LM = L * M;
+  if (t_hi < 0) t_hi = l2c_asy_terms(f);
+  const bool full = t_lo <= 0 && t_hi >= l2c_asy_terms(f);
+  // the level segments (level, first term, terms) of this call: whole levels
+  // batched when all terms run, else one level at a time
+  struct Seg {
+    int l0, l1, m0, nm;
+  };
+  std::vector<Seg> segs;
   const int lpb = levels_per_batch(f, cols);
-  const size_t per_level = (size_t)2 * M * cols * P;
-  AsyncBuf<double2> Z(L > 0 ? per_level * std::min(lpb, L) : 0, s);
-  AsyncBuf<double2> S(L > 0 ? per_level * std::min(lpb, L) : 0, s);
+  if (full) {
+    for (int l0 = 0; l0 < L; l0 += lpb) segs.push_back({l0, std::min(L, l0 + lpb), 0, M});
+  } else {
+    for (int l = 0; l < L; ++l) {
+      const int a = std::max(t_lo, l * M), b = std::min(t_hi, (l + 1) * M);
+      if (a < b) segs.push_back({l, l + 1, a - l * M, b - a});
+    }
+  }
+  // the recurrence bands of this call
+  RecTab rt{};
+  if (full) {
+    rt = f.rt;
+  } else {
+    long long wb = 0, xb = 0, ib = 0, gb = 0, rb = 0;
+    for (int bi = 0; bi < f.nbands; ++bi) {
+      const int term = LM + bi;
+      if (term < t_lo || term >= t_hi) continue;
+      RecBand B = f.band_all[bi];
+      B.wbase = wb;
+      B.xbase = xb;
+      B.ibase = ib;
+      B.gbase = gb;
+      B.rbase = rb;
+      wb += (long long)B.G * B.Q;
+      xb += (long long)B.Q * B.W;
+      ib += (long long)B.G * B.Q * kPairsPerWarp;
+      gb += (long long)B.G * kPairsPerWarp;
+      rb += (long long)B.Q * B.W * B.lc;
+      rt.b[rt.nb++] = B;
+    }
+    rt.nwarps = wb;
+    rt.nxwarps = xb;
+    rt.nslots = ib;
+    rt.ngslots = gb;
+    rt.nrows = rb;
+  }
+  size_t zlev = 0;
+  for (const Seg& g : segs) zlev = std::max(zlev, (size_t)(g.l1 - g.l0) * g.nm);
+  const size_t per_term = (size_t)2 * cols * P;
+  AsyncBuf<double2> Z(zlev * per_term, s);
+  AsyncBuf<double2> S(zlev * per_term, s);
   AsyncBuf<double> F(ld * cols, s);
   const unsigned gp = grid_for(P, 256, 4096);
   if (!transpose) {
-    // values at the cheb1 points: recurrence part (written), then the levels
-    recurrence_forward(f, in, ld, F.p, cols, s);
-    for (int l0 = 0; l0 < L; l0 += lpb) {
-      const int l1 = std::min(L, l0 + lpb);
-      asy_fwd_pack_kernel<<<dim3(gp, (unsigned)cols, (unsigned)(l1 - l0)), 256, 0, s>>>(
-          f.lt, l0, in, ld, f.Cn, n, cols, Z.p);
+    // values at the cheb1 points: recurrence part (written; zero first unless
+    // every band runs), then the levels
+    if (!full) FLB_CUDA(cudaMemset2DAsync(F.p, ld * sizeof(double), 0, n * sizeof(double), cols, s));
+    recurrence_forward(f, rt, in, ld, F.p, cols, s);
+    for (const Seg& g : segs) {
+      asy_fwd_pack_kernel<<<dim3(gp, (unsigned)cols, (unsigned)(g.l1 - g.l0)), 256, 0, s>>>(
+          f.lt, g.l0, g.m0, g.nm, in, ld, f.Cn, n, cols, Z.p);
       note_launch("asy_fwd_pack_kernel");
-      fft_pow2(Z.p, S.p, log2n - 1, (size_t)2 * M * cols * (l1 - l0), true, s);
-      const long long pts = 2 * (f.lt.pb[l0] - f.lt.pb[l1]);
+      fft_pow2(Z.p, S.p, log2n - 1, (size_t)2 * g.nm * cols * (g.l1 - g.l0), true, s);
+      const long long pts = 2 * (f.lt.pb[g.l0] - f.lt.pb[g.l1]);
       asy_fwd_unpack_kernel<<<dim3(grid_for(pts, 256, 8192), (unsigned)cols), 256, 0, s>>>(
-          f.lt, l0, l1, Z.p, n, cols, F.p, ld);
+          f.lt, g.l0, g.l1, g.m0, g.nm, Z.p, n, cols, F.p, ld);
       note_launch("asy_fwd_unpack_kernel");
     }
     // chat = (2 - delta_j0)/N sum_k f_k cos(j t_k): dct_iii_transpose + scaling
@@ -998,17 +1072,16 @@ void l2c_asy_apply(const L2CAsy& f, int transpose, const double* in, double* out
     note_launch("asy_cheb_scale_kernel");
     fast_trig(FL_DCT_III, f.n, G.p, F.p, cols, ld, s);
     FLB_CUDA(cudaMemset2DAsync(out, ld * sizeof(double), 0, n * sizeof(double), cols, s));
-    for (int l0 = 0; l0 < L; l0 += lpb) {
-      const int l1 = std::min(L, l0 + lpb);
-      asy_tr_pack_kernel<<<dim3(gp, (unsigned)cols, (unsigned)(l1 - l0)), 256, 0, s>>>(
-          f.lt, l0, F.p, ld, n, cols, Z.p);
+    for (const Seg& g : segs) {
+      asy_tr_pack_kernel<<<dim3(gp, (unsigned)cols, (unsigned)(g.l1 - g.l0)), 256, 0, s>>>(
+          f.lt, g.l0, g.m0, g.nm, F.p, ld, n, cols, Z.p);
       note_launch("asy_tr_pack_kernel");
-      fft_pow2(Z.p, S.p, log2n - 1, (size_t)2 * M * cols * (l1 - l0), false, s);
+      fft_pow2(Z.p, S.p, log2n - 1, (size_t)2 * g.nm * cols * (g.l1 - g.l0), false, s);
       asy_tr_unpack_kernel<<<dim3(grid_for(P / 2 + 1, 256, 8192), (unsigned)cols), 256, 0, s>>>(
-          f.lt, l0, l1, Z.p, n, cols, f.Cn, out, ld);
+          f.lt, g.l0, g.l1, g.m0, g.nm, Z.p, n, cols, f.Cn, out, ld);
       note_launch("asy_tr_unpack_kernel");
     }
-    recurrence_transpose(f, F.p, ld, out, cols, scale_half, s);
+    recurrence_transpose(f, rt, F.p, ld, out, cols, scale_half, s);
   }
 }
 

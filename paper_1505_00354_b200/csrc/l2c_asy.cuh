@@ -35,8 +35,14 @@ constexpr size_t kL2CAsyMin = size_t(1) << 20;
 
 // out = M in (transpose 0) or M^T in (1, optional (n + 1/2) output scaling);
 // columns of stride ld; in and out must not alias.
+// t_lo / t_hi: only the terms [t_lo, t_hi) (a partial sum; the term-parallel
+// multi-GPU DLT splits them over ranks): terms [0, L M) are the expansion's
+// (level l = t / M, m = t % M) DCT/DST pairs, the next ones the recurrence's
+// bands of points (l2c_asy_terms in all, l2c_asy_term_cost their relative cost).
 void l2c_asy_apply(const L2CAsy& f, int transpose, const double* in, double* out, size_t cols,
-                   size_t ld, int scale_half, cudaStream_t st);
+                   size_t ld, int scale_half, cudaStream_t st, int t_lo = 0, int t_hi = -1);
+int l2c_asy_terms(const L2CAsy& f);
+double l2c_asy_term_cost(const L2CAsy& f, int term);
 
 struct L2CAsyInfo {
   int M, levels, transforms;   // transforms: length-N real DCT/DST per column

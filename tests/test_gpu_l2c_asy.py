@@ -131,3 +131,32 @@ def test_asy_deterministic():
     b = [cfg.convert(c, transpose=True) for _ in range(3)]
     assert all(np.array_equal(a[0], x) for x in a[1:])
     assert all(np.array_equal(b[0], x) for x in b[1:])
+
+
+def test_asy_stage_slices_sum_to_full():
+    """The term-parallel C5 split (fl_dlt_stage, FL_STAGE_LEG2CHEB): partial
+    conversions over weighted slices of the (level, m) terms and recurrence
+    bands sum to the full conversion (forward and transposed)."""
+    import torch
+    from paper_1505_00354_b200 import distributed as D
+    n = 1 << 20
+    cfg = fl.TransformConfig(n)  # FAST mode: the expansion at 2^20
+    count = D.stage_terms(cfg, D.STAGE_LEG2CHEB)
+    info = cfg.leg2cheb_asy_info()
+    assert count > info["levels"] * info["terms"]
+    costs = D.stage_costs(cfg, D.STAGE_LEG2CHEB, count)
+    x = torch.from_numpy(fl.random_decaying(n, 1.0, 3)).cuda()
+    for inverse in (0, 1):
+        full = torch.empty_like(x)
+        D.gpu_stage(cfg, inverse, D.STAGE_LEG2CHEB, 0, count, x, full)
+        for world in (2, 3, 8):
+            acc = torch.zeros_like(x)
+            for r in range(world):
+                lo, hi = D.weighted_slice(costs, world, r)
+                part = torch.empty_like(x)
+                D.gpu_stage(cfg, inverse, D.STAGE_LEG2CHEB, lo, hi, x, part)
+                acc += part
+            s = float(x.abs().sum()) * (n if inverse else 1)
+            assert float((acc - full).abs().max()) / s <= 1e-15 * math.log2(n), (inverse, world)
+        ref = cfg.convert(x.cpu().numpy(), transpose=bool(inverse))
+        assert float(np.abs(full.cpu().numpy() - ref).max()) / s <= 1e-15 * math.log2(n)

@@ -129,6 +129,26 @@ def test_term_slice_balanced():
             assert all(lo % 2 == 0 for lo, hi in sl2 if hi > lo)
 
 
+def test_weighted_slice_contiguous_and_balanced():
+    """The asymptotic conversion's stage terms have unequal costs (60 (level,
+    m) pairs of ~2 transforms, then ~7 recurrence bands of ~3 pairs each at
+    2^26): contiguous slices covering all terms, each within one term's cost
+    of the ideal share."""
+    from paper_1505_00354_b200.distributed import weighted_slice
+    rng = np.random.default_rng(0)
+    cases = [[1.0] * 14, [1.86] * 60 + [5.7, 5.7, 5.8, 5.6, 5.7, 5.7, 3.8], list(rng.uniform(0.1, 3.0, 37)), [2.0]]
+    for costs in cases:
+        for world in (1, 2, 3, 4, 8):
+            sl = [weighted_slice(costs, world, r) for r in range(world)]
+            assert sl[0][0] == 0 and sl[-1][1] == len(costs)
+            assert all(sl[r][1] == sl[r + 1][0] for r in range(world - 1))
+            share = sum(costs) / world
+            for lo, hi in sl:
+                assert sum(costs[lo:hi]) <= share + max(costs) + 1e-9
+    with pytest.raises(ValueError):
+        weighted_slice([1.0], 2, 2)
+
+
 def _c4_worker(rank, world, port, out):
     """BASELINE C4's sharded data path (bench.py run_batched): contiguous
     column shards, inputs seeded per global column, one independent batched
