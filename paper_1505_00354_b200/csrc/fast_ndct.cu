@@ -1352,29 +1352,69 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, LOG2N <= 12 ? 2 : 1)
   bool bad = false;
   double2* zx = zbA;
   constexpr double h = 0.70710678118654752440;
+#ifndef FLB_STREAM_TR_DEINTERLEAVE
+#define FLB_STREAM_TR_DEINTERLEAVE 1
+#endif
   for (uint32_t it = 0; col < batch; col += gridDim.x, ++it) {
     mbar_wait_parity(bar, it & 1u);
-    // pack (tr_term): v_r = (h_{4m}, h_{4m+2}) for r < 4, the swapped odd
-    // pair (h_{2N-3-4m}, h_{2N-1-4m}) for r >= 4 (m = t + r T); odd terms
-    // (DST^T) negate the odd-index entries
+    double2* zy = zx == zbA ? zbB : zbA;
     double2 v[E];
+    if constexpr (FLB_STREAM_TR_DEINTERLEAVE) {
+      // de-interleave the column by parity into the free FFT row (even entries,
+      // then odd ones): the pack's stride-4 reads of the natural-order column
+      // were 4-way shared-memory bank conflicts (81.6 M per 65536 columns)
+      double* ev = reinterpret_cast<double*>(zx);
+      double* od = ev + N / 2;
 #pragma unroll
-    for (int r = 0; r < E; ++r) {
-      const int m = t + r * T;
-      const int k0 = r < 4 ? 4 * m : 2 * N - 3 - 4 * m;
-      const double2 w = make_double2(raw[k0], raw[k0 + 2]);
-      bad |= !isfinite(w.x) || !isfinite(w.y);
-      v[r] = r < 4 ? w : (odd ? make_double2(-w.y, -w.x) : make_double2(w.y, w.x));
+      for (int r = 0; r < N / 2 / T; ++r) {
+        const int i = t + r * T;
+        const double2 w = *reinterpret_cast<const double2*>(raw + 2 * i);
+        ev[i] = w.x;
+        od[i] = w.y;
+      }
+      __syncthreads();  // the column is copied (and the previous unpack is done)
+      const size_t nxt = col + gridDim.x;
+      if (t == 0 && nxt < batch) {
+        mbar_expect(bar, N * 8);
+        bulk_load(raw_s, in + nxt * ld_in, N * 8, bar);
+      }
+      // pack (tr_term): v_r = (h_{4m}, h_{4m+2}) = ev[2m], ev[2m+1] for r < 4, the
+      // swapped odd pair (h_{2N-3-4m}, h_{2N-1-4m}) = od[N-2-2m], od[N-1-2m]
+      // for r >= 4 (m = t + r T); odd terms (DST^T) negate the odd-index entries
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        const int m = t + r * T;
+        const double2 w = r < 4 ? *reinterpret_cast<const double2*>(ev + 2 * m)
+                                : *reinterpret_cast<const double2*>(od + (N - 2 - 2 * m));
+        bad |= !isfinite(w.x) || !isfinite(w.y);
+        v[r] = r < 4 ? w : (odd ? make_double2(-w.y, -w.x) : make_double2(w.y, w.x));
+      }
+      pass_compute<P, E, 8, 1, false>(v, t, fftw);
+      pass_store<P, E, 8, 1>(v, zy, t);  // the other row (free after the barrier)
+      __syncthreads();
+    } else {
+      // pack (tr_term) straight from the natural-order column
+#pragma unroll
+      for (int r = 0; r < E; ++r) {
+        const int m = t + r * T;
+        const int k0 = r < 4 ? 4 * m : 2 * N - 3 - 4 * m;
+        const double2 w = make_double2(raw[k0], raw[k0 + 2]);
+        bad |= !isfinite(w.x) || !isfinite(w.y);
+        v[r] = r < 4 ? w : (odd ? make_double2(-w.y, -w.x) : make_double2(w.y, w.x));
+      }
+      pass_compute<P, E, 8, 1, false>(v, t, fftw);
+      pass_store<P, E, 8, 1>(v, zx, t);
+      __syncthreads();  // every thread has packed: the stage buffer takes the next column
+      const size_t nxt = col + gridDim.x;
+      if (t == 0 && nxt < batch) {
+        mbar_expect(bar, N * 8);
+        bulk_load(raw_s, in + nxt * ld_in, N * 8, bar);
+      }
+      zy = zx;
+      zx = zx == zbA ? zbB : zbA;
     }
-    pass_compute<P, E, 8, 1, false>(v, t, fftw);
-    pass_store<P, E, 8, 1>(v, zx, t);
-    __syncthreads();  // every thread has packed: the stage buffer takes the next column
-    const size_t nxt = col + gridDim.x;
-    if (t == 0 && nxt < batch) {
-      mbar_expect(bar, N * 8);
-      bulk_load(raw_s, in + nxt * ld_in, N * 8, bar);
-    }
-    double2* zb = mid_passes_pp<P, E, 8, P, false, 0>(zx, zx == zbA ? zbB : zbA, t, fftw, 0);
+    // zy holds the first pass; zx is free
+    double2* zb = mid_passes_pp<P, E, 8, P, false, 0>(zy, zx, t, fftw, 0);
     // unpack (tr_term): rows {a, P - a, P + a, N - a} of each group g
     double* dst = out + col * ld_out;
 #pragma unroll
