@@ -524,7 +524,7 @@ __global__ void __launch_bounds__(256) asy_fwd_pack_kernel(const __grid_constant
     for (int tm = 0; tm < m0 + nm; ++tm) {
       if (tm > 0) {
 #pragma unroll
-        for (int r = 0; r < 4; ++r) h[r] = h[r] * lt.hk[tm] / ((double)js[r] + (double)tm + 0.5);
+        for (int r = 0; r < 4; ++r) h[r] = h[r] * lt.hk[tm] * __drcp_rn((double)js[r] + (double)tm + 0.5);
       }
       if (tm < m0) continue;
       const double st0 = bs[0] * h[0], st1 = bs[1] * h[1], st2 = bs[2] * h[2], st3 = bs[3] * h[3];
@@ -685,21 +685,29 @@ __global__ void __launch_bounds__(256) asy_tr_unpack_kernel(const __grid_constan
       const long long nu = lt.nu[l0 + lv];
 #pragma unroll
       for (int e = 0; e < 4; ++e) h[e] = 1.0;
-      for (int tm = 0; tm < m0 + nm; ++tm) {
-        if (tm < m0) {
+      for (int tm = 1; tm < m0; ++tm) {
 #pragma unroll
-          for (int e = 0; e < 4; ++e)
-            if (tm > 0) h[e] = h[e] * lt.hk[tm] / ((double)r[e] + (double)tm + 0.5);
-          continue;
-        }
-        const size_t tr = ((size_t)(lv * nm + tm - m0) * 2) * nc + col;
+        for (int e = 0; e < 4; ++e) h[e] = h[e] * lt.hk[tm] * __drcp_rn((double)r[e] + (double)tm + 0.5);
+      }
+      // the four packed entries of term m0 + i, prefetched one term ahead
+      auto zrow = [&](int i, double2& ca, double2& cb, double2& sa, double2& sb) {
+        const size_t tr = ((size_t)(lv * nm + i) * 2) * nc + col;
         const double2* Zc = Z + tr * P;
         const double2* Zs = Z + (tr + nc) * P;
-        const double2 ca = Zc[a], cb = Zc[bq], sa = Zs[a], sb = Zs[bq];
+        ca = __ldcs(Zc + a);
+        cb = __ldcs(Zc + bq);
+        sa = __ldcs(Zs + a);
+        sb = __ldcs(Zs + bq);
+      };
+      double2 nca, ncb, nsa, nsb;
+      zrow(0, nca, ncb, nsa, nsb);
+      for (int tm = m0; tm < m0 + nm; ++tm) {
+        const double2 ca = nca, cb = ncb, sa = nsa, sb = nsb;
+        if (tm + 1 < m0 + nm) zrow(tm + 1 - m0, nca, ncb, nsa, nsb);
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
           if (e >= nr) break;
-          if (tm > 0) h[e] = h[e] * lt.hk[tm] / ((double)r[e] + (double)tm + 0.5);
+          if (tm > 0) h[e] = h[e] * lt.hk[tm] * __drcp_rn((double)r[e] + (double)tm + 0.5);
           if (r[e] < nu) continue;
           const double xc = swp[e] ? tr_unpack_value(cb, ca, c2[e], s2[e], ch[e], sh[e])
                                    : tr_unpack_value(ca, cb, c2[e], s2[e], ch[e], sh[e]);
