@@ -361,13 +361,20 @@ void line_pass(int log2l, const double2* src, double2* dst, unsigned long long P
   line_pass<INV>(log2l, io, P, items, mp, s);
 }
 
-// The pass plan: 2 passes for P <= 2^24, else 3 (rows of 2^lr, columns of
-// 2^lc = 2^l1 * 2^l2).
+// The pass plan: 2 passes for P <= 2^FLB_FFT_2PASS_MAX, else 3 (rows of
+// 2^lr, columns of 2^lc = 2^l1 * 2^l2). Three passes of short lines (<= 2^8,
+// eight lines per CTA: 128-byte column segments, several CTAs per SM) beat
+// two of 2^11-2^12-point lines (one 1024-thread CTA per SM, 32-byte column
+// segments) from P = 2^21: asymptotic conversion at N = 2^24 47.2 -> 40.3 ms,
+// 2^22 10.6 -> 10.0 ms; equal at P = 2^19.
+#ifndef FLB_FFT_2PASS_MAX
+#define FLB_FFT_2PASS_MAX 20
+#endif
 struct PassPlan {
   int passes, lr, lc, l1, l2;
   unsigned long long R, C, C1, C2;
   explicit PassPlan(int log2p) {
-    passes = log2p <= 24 ? 2 : 3;
+    passes = (log2p <= FLB_FFT_2PASS_MAX || log2p < 15) ? 2 : 3;
     lr = passes == 2 ? log2p / 2 : log2p / 3;
     lc = log2p - lr;
     l1 = lc / 2;
