@@ -1956,41 +1956,44 @@ __global__ void big_tables_kernel(size_t n, int l0, int nt, BigTerms bt,
   }
 }
 
-// Forward pack of term l0 + blockIdx.z: Z[(z nc + col) P + m] from the stage
-// rt[z][j] c_j (the real-DCT packing of the file header).
+// Forward pack of all nt terms: Z[(t nc + col) P + m] from the stage
+// rt[t][j] c_j (the real-DCT packing of the file header). One thread per m for
+// every term: the four column entries and the three twiddles of m are read /
+// evaluated once (per term they were half the kernel's time at C2).
 __global__ void big_fwd_pack_kernel(const double* __restrict__ in, size_t ld, size_t n, size_t nc,
-                                    int l0, BigTerms bt, const double* __restrict__ rt,
+                                    int l0, int nt, BigTerms bt, const double* __restrict__ rt,
                                     double2* __restrict__ Z, int* nonfinite) {
   const size_t P = n / 2;
   const size_t col = blockIdx.y;
-  const int tz = blockIdx.z, l = l0 + tz;
-  const int odd = big_odd(bt, l);
   const double* c = in + col * ld;
-  const double* rw = rt + (size_t)tz * n;
-  double2* Zc = Z + ((size_t)tz * nc + col) * P;
   const double nd = (double)n;
   for (size_t m = blockIdx.x * (size_t)blockDim.x + threadIdx.x; m < P;
        m += (size_t)gridDim.x * blockDim.x) {
-    auto st = [&](size_t j) -> double { return c[j] * rw[j]; };
-    auto X = [&](size_t j) -> double {
-      if (j == 0) return odd ? 0.0 : st(0);
-      if (j >= n) return 0.0;
-      return 0.5 * (odd ? st(n - j) : st(j));
-    };
-    if (nonfinite && l == 0) {
-      if (!isfinite(c[m]) || !isfinite(c[m + P])) atomicOr(nonfinite, 1);
+    // stage indices: m, n - m (none for m = 0), m + P, P - m
+    const double c0 = c[m], c1 = m ? c[n - m] : 0.0, c2 = c[m + P], c3 = c[P - m];
+    if (nonfinite && l0 == 0) {
+      if (!isfinite(c0) || !isfinite(c2)) atomicOr(nonfinite, 1);
     }
     double sa, ca, sb, cb, s4, c4;
     sincospi((double)m / (2.0 * nd), &sa, &ca);        // e^{i pi m/(2N)}
     sincospi((double)(m + P) / (2.0 * nd), &sb, &cb);  // e^{i pi (m+P)/(2N)}
     sincospi(2.0 * (double)m / nd, &s4, &c4);          // e^{2 pi i m/N}
-    const double xa = X(m), xan = X(n - m), xb = X(m + P), xbn = X(P - m);
-    const double2 Wa = make_double2(ca * xa + sa * xan, sa * xa - ca * xan);
-    const double2 Wb = make_double2(cb * xb + sb * xbn, sb * xb - cb * xbn);
-    const double2 sm = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
-    const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
-    const double2 dr = make_double2(d.x * c4 - d.y * s4, d.x * s4 + d.y * c4);
-    Zc[m] = make_double2(sm.x - dr.y, sm.y + dr.x);
+    for (int tz = 0; tz < nt; ++tz) {
+      const int odd = big_odd(bt, l0 + tz);
+      const double* rw = rt + (size_t)tz * n;
+      const double st0 = c0 * rw[m], st1 = m ? c1 * rw[n - m] : 0.0, st2 = c2 * rw[m + P],
+                   st3 = c3 * rw[P - m];
+      // DCT-III: X(0) = st(0), X(j) = st(j)/2; DST-III: X(0) = 0, X(j) = st(N - j)/2
+      const double xa = odd ? (m ? 0.5 * st1 : 0.0) : (m ? 0.5 * st0 : st0);
+      const double xan = m ? 0.5 * (odd ? st0 : st1) : 0.0;
+      const double xb = 0.5 * (odd ? st3 : st2), xbn = 0.5 * (odd ? st2 : st3);
+      const double2 Wa = make_double2(ca * xa + sa * xan, sa * xa - ca * xan);
+      const double2 Wb = make_double2(cb * xb + sb * xbn, sb * xb - cb * xbn);
+      const double2 sm = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
+      const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
+      const double2 dr = make_double2(d.x * c4 - d.y * s4, d.x * s4 + d.y * c4);
+      Z[((size_t)tz * nc + col) * P + m] = make_double2(sm.x - dr.y, sm.y + dr.x);
+    }
   }
 }
 
@@ -2050,32 +2053,64 @@ __global__ void big_tr_pack_kernel(const double* __restrict__ in, size_t ld, siz
 }
 
 // Transposed unpack of all nt terms: out_r (+)= sum_t rt[t][r] X_t(r).
+// The outputs r in {a, P - a, P + a, N - a} read the same two packed entries
+// a, P - a of every term (DCT^T rows at kk = r, DST^T rows at kk = N - r): one
+// thread per a in [0, P/2] computes all four with its twiddles evaluated once
+// (per output and term they were half of the kernel's time at C2).
+__device__ __forceinline__ double big_tr_value(double2 za, double2 zc, double c2, double s2, double ch,
+                                               double sh) {
+  const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
+  const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));
+  const double2 Vv = make_double2(ev.x + od.x * c2 - od.y * s2, ev.y + od.x * s2 + od.y * c2);
+  return ch * Vv.x + sh * Vv.y;
+}
 __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, size_t nc, int l0,
                                      int nt, BigTerms bt, const double* __restrict__ rt,
                                      double* __restrict__ out, size_t ld, int first) {
   const size_t P = n / 2;
   const size_t col = blockIdx.y;
   const double nd = (double)n;
-  for (size_t r = blockIdx.x * (size_t)blockDim.x + threadIdx.x; r < n;
-       r += (size_t)gridDim.x * blockDim.x) {
-    double acc = 0.0;
+  for (size_t a = blockIdx.x * (size_t)blockDim.x + threadIdx.x; a <= P / 2;
+       a += (size_t)gridDim.x * blockDim.x) {
+    const size_t bq = (P - a) & (P - 1);
+    const int nr = (a != 0 && a != P / 2) ? 4 : 2;
+    const size_t r[4] = {a, P + a, P - a, 2 * P - a};
+    double c2[4], s2[4], ch[4], sh[4], acc[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      acc[e] = 0.0;
+      c2[e] = s2[e] = ch[e] = sh[e] = 0.0;
+      if (e < nr) {
+        sincospi(-2.0 * (double)r[e] / nd, &s2[e], &c2[e]);  // e^{-2 pi i r/N}
+        sincospi((double)r[e] / (2.0 * nd), &sh[e], &ch[e]);  // e^{i pi r/(2N)}
+      }
+    }
     for (int t = 0; t < nt; ++t) {
       const int odd = big_odd(bt, l0 + t);
-      if (odd && r == 0) continue;
-      const size_t kk = odd ? (n - r) : r;
-      const size_t a = kk & (P - 1), b = (P - kk) & (P - 1);
       const double2* Zc = Z + ((size_t)t * nc + col) * P;
-      const double2 za = Zc[a], zc = Zc[b];
-      const double2 ev = make_double2(0.5 * (za.x + zc.x), 0.5 * (za.y - zc.y));
-      const double2 od = make_double2(0.5 * (za.y + zc.y), -0.5 * (za.x - zc.x));
-      double s2, c2, sh, ch;
-      sincospi(-2.0 * (double)kk / nd, &s2, &c2);  // e^{-2 pi i kk/N}
-      sincospi((double)kk / (2.0 * nd), &sh, &ch);  // e^{i pi kk/(2N)}
-      const double2 Vv = make_double2(ev.x + od.x * c2 - od.y * s2, ev.y + od.x * s2 + od.y * c2);
-      acc += rt[(size_t)t * n + r] * (ch * Vv.x + sh * Vv.y);
+      const double2 za = Zc[a], zb = Zc[bq];
+      const double* rw = rt + (size_t)t * n;
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (e >= nr) break;
+        // rows e >= 2 read the pair swapped; the DST^T rows use kk = N - r:
+        // e^{-2 pi i kk/N} = conj, e^{i pi kk/(2N)} = i conj, and swap again
+        const bool swp = (e >= 2) != (odd != 0);
+        const double2 p0 = swp ? zb : za, p1 = swp ? za : zb;
+        double x;
+        if (!odd)
+          x = big_tr_value(p0, p1, c2[e], s2[e], ch[e], sh[e]);
+        else
+          x = r[e] == 0 ? 0.0 : big_tr_value(p0, p1, c2[e], -s2[e], sh[e], ch[e]);
+        acc[e] = __fma_rn(rw[r[e]], x, acc[e]);
+      }
     }
-    double* o = out + col * ld + r;
-    *o = first ? acc : *o + acc;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (e >= nr) break;
+      double* o = out + col * ld + r[e];
+      *o = first ? acc[e] : *o + acc[e];
+    }
   }
 }
 
@@ -2111,6 +2146,7 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
   FLB_CUDA(cudaMallocAsync(&rt, (size_t)tb * n * sizeof(double), s));
   const unsigned gx = (unsigned)std::min<size_t>((P + 255) / 256, 2048);
   const unsigned gxn = (unsigned)std::min<size_t>((n + 255) / 256, 4096);
+  const unsigned gxq = (unsigned)std::min<size_t>((P / 2 + 256) / 256, 4096);
   for (int l0 = l_lo; l0 < l_hi; l0 += tb) {
     const int nt = std::min(tb, l_hi - l0);
     big_tables_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, l0, nt, bt, delta, wt, rt);
@@ -2119,8 +2155,8 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
       const size_t nc = batch - c0 < chunk ? batch - c0 : chunk;
       const int first = l0 == l_lo;
       if (!transpose) {
-        big_fwd_pack_kernel<<<dim3(gx, (unsigned)nc, (unsigned)nt), 256, 0, s>>>(
-            in + c0 * ld_in, ld_in, n, nc, l0, bt, rt, Z, nonfinite);
+        big_fwd_pack_kernel<<<dim3(gx, (unsigned)nc), 256, 0, s>>>(
+            in + c0 * ld_in, ld_in, n, nc, l0, nt, bt, rt, Z, nonfinite);
         note_launch("big_fwd_pack_kernel");
         fft_pow2(Z, S, log2n - 1, nc * nt, true, s);
         big_fwd_unpack_kernel<<<dim3(gxn, (unsigned)nc), 256, 0, s>>>(
@@ -2131,7 +2167,7 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
             in + c0 * ld_in, ld_in, n, nc, l0, bt, wt, mult, Z, nonfinite);
         note_launch("big_tr_pack_kernel");
         fft_pow2(Z, S, log2n - 1, nc * nt, false, s);
-        big_tr_unpack_kernel<<<dim3(gxn, (unsigned)nc), 256, 0, s>>>(
+        big_tr_unpack_kernel<<<dim3(gxq, (unsigned)nc), 256, 0, s>>>(
             Z, n, nc, l0, nt, bt, rt, out + c0 * ld_out, ld_out, first);
         note_launch("big_tr_unpack_kernel");
       }
