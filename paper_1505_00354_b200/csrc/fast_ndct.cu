@@ -2189,15 +2189,17 @@ void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* 
 #ifndef FLB_NDCT_CLUSTER
 #define FLB_NDCT_CLUSTER 1
 #endif
-  // the cluster kernel wins once its CTAs fill the GPU at least twice (one
-  // column occupies N/8192 SMs for all its terms): 16384 x 256 0.74 vs 1.11 ms,
-  // 32768 x 128 0.92 vs 1.16 ms, 65536 x 512 7.7 vs 8.9 ms; at 65536 x 64
-  // (C2, 3.5 waves) it ties the multi-pass path (1.25 vs 1.21 ms), and a
-  // single column is latency-bound on N/8192 SMs (0.26 vs 0.16 ms at 16384)
+  // the cluster kernel wins where the multi-pass path has to cut the batch
+  // into several scratch-sized pieces (all terms x columns > 2 GiB of packed
+  // rows): 16384 x 4096 8.8 vs 14.5 ms; elsewhere the multi-pass path (all
+  // terms packed per thread, shared twiddles) ties or wins: 16384 x 256 0.66
+  // vs 0.65, 32768 x 128 0.82 vs 0.68, 65536 x 128 1.98 vs 1.28, 65536 x 512
+  // 7.6 vs 6.1 ms
   const size_t cs = (size_t(1) << log2n) / 8192;
-  const bool cl_fill = batch * cs >= 2 * (size_t)sm_count() && (log2n < 16 || batch >= 128);
+  const bool cl_fill = batch * cs >= 2 * (size_t)sm_count() &&
+                       (size_t)num_terms * batch * (size_t(16) << log2n) > (size_t(2) << 30);
   if (FLB_NDCT_CLUSTER && cheb && !transpose && bes->cl_wf && l_lo == 0 && l_hi == num_terms &&
-      log2n >= 14 && log2n <= 16 && cl_fill) {
+      log2n >= 14 && log2n <= 15 && cl_fill) {
     switch (log2n) {
       case 14: launch_cluster_fwd<14>(in, ld_in, out, ld_out, batch, *bes, nonfinite, s); break;
       case 15: launch_cluster_fwd<15>(in, ld_in, out, ld_out, batch, *bes, nonfinite, s); break;

@@ -1,9 +1,10 @@
-"""The cluster-fused forward NDCT (8192 < N <= 2^16, cluster_ndct_fwd_kernel:
+"""The cluster-fused forward NDCT (N = 2^14, 2^15, cluster_ndct_fwd_kernel:
 one column per thread-block cluster of N/8192 CTAs, the N/2-point FFT of each
 Chebyshev-expansion term as a four-step over the cluster with the exchange
-through distributed shared memory). It runs for batches that fill the GPU
-twice; checked against the oracle and against the multi-pass path (a few
-columns of the same block) at the north star's tolerance."""
+through distributed shared memory). It runs for batches whose packed rows
+(terms x columns) exceed the multi-pass path's 2 GiB scratch; checked against
+the oracle and against the multi-pass path (a few columns of the same block)
+at the north star's tolerance."""
 import math
 
 import numpy as np
@@ -15,7 +16,7 @@ import paper_1505_00354_b200 as fl
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,cols", [(16384, 300), (32768, 160), (65536, 160)])
+@pytest.mark.parametrize("n,cols", [(16384, 640), (32768, 320)])
 def test_cluster_ndct_vs_oracle_and_multipass(n, cols):
     import torch
     grid = fl.legendre_nodes_weights(n)
@@ -37,7 +38,7 @@ def test_cluster_ndct_vs_oracle_and_multipass(n, cols):
 
 
 def test_cluster_dlt_batched_65536():
-    """The factored DLT of a 2^16 batch large enough for the cluster NDCT."""
+    """The factored DLT of a 2^16 batch (multi-pass NDCT, direct conversion)."""
     n, cols = 65536, 128
     cfg = fl.TransformConfig(n)
     g = cfg.grid()
