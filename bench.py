@@ -403,8 +403,28 @@ def sub_configs(args, dist, rank: int, world: int, local: int) -> dict:
                      # +8 B (delta) for the DLT, +16 B (delta, w) for the IDLT
                      "dlt_hbm_frac": 24.0 * n / (dlt / 1e3) / 1e9 / peak,
                      "idlt_hbm_frac": 32.0 * n / (idlt / 1e3) / 1e9 / peak,
-                     "leg2cheb": "toeplitz-hankel" if cfg.leg2cheb_rank(0) else "direct",
+                     "leg2cheb": l2c_method(cfg, n),
                      "round_trip_rel": rt}
+
+    def l2c_method(cfg, n):
+        if n >= (1 << 20) and n & (n - 1) == 0:
+            return "asymptotic expansion " + json.dumps(cfg.leg2cheb_asy_info())
+        return "toeplitz-hankel" if cfg.leg2cheb_rank(0) else "direct"
+
+    def conversions(n, reps):
+        """The conversion alone, one vector: the asymptotic expansion against
+        Toeplitz-Hankel (both directions)."""
+        cfg = fl.TransformConfig(n)
+        x = torch.from_numpy(fl.random_decaying(n, 1.0, 3)).cuda()
+        y = torch.empty_like(x)
+        r = {}
+        for mode, name in ((fl.LEG2CHEB_TOEPLITZ, "toeplitz_hankel"), (fl.LEG2CHEB_ASYMPTOTIC, "asymptotic")):
+            cfg.set_leg2cheb_mode(mode)
+            for t in (0, 1):
+                r[f"{name}{'_T' if t else ''}_ms"] = timed(lambda: _lib.check(_lib.LIB.fl_plan_leg2cheb(
+                    cfg.handle, t, vp(x.data_ptr()), vp(y.data_ptr()), 1, n, sp)), reps)
+        r["asymptotic_shape"] = cfg.leg2cheb_asy_info()
+        return r
 
     if world == 1:
         # C1: one N = 1024 vector (latency-bound: one CTA runs all NDCT terms)
@@ -451,6 +471,8 @@ def sub_configs(args, dist, rank: int, world: int, local: int) -> dict:
             _, r = single(n, torch.from_numpy(c).cuda(), max(3, min(100, (1 << 22) // n)))
             sweep.append(r)
         out["c3"] = {"workload": CONFIGS["c3"][3] + ", sweep 2^10..2^20", "sweep": sweep}
+        # the two fast conversions timed against each other (north-star subsystem 2)
+        out["leg2cheb_methods"] = {"2^20": conversions(1 << 20, 5), "2^26": conversions(1 << 26, 2)}
 
     # C5: one 2^26 vector; term-parallel over the ranks (all ranks take part)
     n = CONFIGS["c5"][0]
@@ -481,14 +503,15 @@ def sub_configs(args, dist, rank: int, world: int, local: int) -> dict:
                  "dlt_ms": res["dlt"], "idlt_ms": res["idlt"],
                  "dlt_coeffs_per_s": n / res["dlt"] * 1e3, "idlt_coeffs_per_s": n / res["idlt"] * 1e3,
                  "dlt_hbm_frac_per_gpu": 24.0 * n / (res["dlt"] / 1e3) / 1e9 / peak / world,
-                 "leg2cheb_rank": [cfg.leg2cheb_rank(0), cfg.leg2cheb_rank(1)],
+                 "leg2cheb": l2c_method(cfg, n),
                  "stage_terms": [D.stage_terms(cfg, 0), D.stage_terms(cfg, 1)]}
     return out if rank == 0 else {}
 
 
 def run_c5(args, rank: int, world: int, local: int) -> None:
-    """--config c5: one 2^26 DLT, its conversion (Toeplitz-Hankel rank terms)
-    and NDCT (Chebyshev-expansion terms) split over the ranks, partials
+    """--config c5: one 2^26 DLT, its conversion (the asymptotic expansion's
+    (level, m) terms and recurrence bands, split by cost) and NDCT
+    (Chebyshev-expansion terms) split over the ranks, partials
     combined by NCCL all-reduce / reduce-scatter (distributed.py). Fixed N:
     strong scaling."""
     import torch
@@ -545,7 +568,7 @@ def run_c5(args, rank: int, world: int, local: int) -> None:
                          "traffic": None, "note": "24 B/coef (c, f, delta) over the job"},
             "e2e": {"value": n / (e2e_ms / 1e3), "unit": "coeffs/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": int(8 * back.numel())},
-            "leg2cheb_rank": [cfg.leg2cheb_rank(0), cfg.leg2cheb_rank(1)],
+            "leg2cheb": "asymptotic expansion " + json.dumps(cfg.leg2cheb_asy_info()),
             "gpu_launches": launches, "clocks": clk.summary()}))
     if dist is not None:
         dist.barrier()
