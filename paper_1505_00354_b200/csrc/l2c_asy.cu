@@ -30,8 +30,6 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
-#include <mutex>
-#include <set>
 #include <vector>
 
 #include "common.cuh"
@@ -908,34 +906,27 @@ struct AsyncBuf {
   AsyncBuf& operator=(const AsyncBuf&) = delete;
 };
 
-// The per-call scratch (Z / FFT buffers: up to ~20 GB at 2^26) is stream-ordered;
-// let the device's default pool keep up to 32 GB of it across calls instead
-// of unmapping it at every synchronisation.
-void keep_scratch_pool() {
-  static std::mutex mu;
-  static std::set<int> done;
-  int dev = 0;
-  if (cudaGetDevice(&dev) != cudaSuccess) return;
-  std::lock_guard<std::mutex> lock(mu);
-  if (!done.insert(dev).second) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-    uint64_t thr = uint64_t(32) << 30;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-}
-
 unsigned grid_for(long long work, int threads, long long cap = 1 << 20) {
   return (unsigned)std::max<long long>(1, std::min<long long>((work + threads - 1) / threads, cap));
 }
 
-// levels per batch of the expansion's transforms (Z + FFT scratch within the budget)
+// levels per batch of the expansion's transforms (Z + FFT scratch within a
+// fixed 12 GiB budget: the same batching, hence the same scratch sizes, on
+// every call)
 int levels_per_batch(const L2CAsy& f, size_t nc) {
   const size_t per_level = (size_t)2 * f.M * nc * (f.n / 2) * sizeof(double2) * 2;
-  size_t budget = size_t(12) << 30;
-  size_t fr = 0, tot = 0;
-  if (cudaMemGetInfo(&fr, &tot) == cudaSuccess) budget = std::min(budget, fr / 2);
+  const size_t budget = size_t(12) << 30;
   return (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(f.lt.L, 1), budget / per_level));
+}
+
+// Grow the stream-ordered pool to a call's whole scratch in one allocation
+// (freed at once, kept by the pool's release threshold): the call's buffers
+// are then carved from memory the pool already holds, instead of an
+// occasional mid-call pool growth (a ~9 ms outlier at 2^20).
+void reserve_scratch(size_t bytes, cudaStream_t s) {
+  void* p = nullptr;
+  if (bytes && cudaMallocAsync(&p, bytes, s) == cudaSuccess) cudaFreeAsync(p, s);
+  cudaGetLastError();
 }
 
 void recurrence_forward(const L2CAsy& f, const RecTab& rt, const double* c, size_t ld, double* F,
@@ -996,7 +987,6 @@ double l2c_asy_term_cost(const L2CAsy& f, int term) {
 void l2c_asy_apply(const L2CAsy& f, int transpose, const double* in, double* out, size_t cols,
                    size_t ld, int scale_half, cudaStream_t s, int t_lo, int t_hi) {
   if (cols == 0) return;
-  keep_scratch_pool();
   const long long n = (long long)f.n, P = n / 2;
   const int log2n = __builtin_ctzll((unsigned long long)n);
   const int L = f.lt.L, M = f.M, LM = L * M;
@@ -1048,6 +1038,10 @@ void l2c_asy_apply(const L2CAsy& f, int transpose, const double* in, double* out
   size_t zlev = 0;
   for (const Seg& g : segs) zlev = std::max(zlev, (size_t)(g.l1 - g.l0) * g.nm);
   const size_t per_term = (size_t)2 * cols * P;
+  reserve_scratch(2 * zlev * per_term * sizeof(double2) + 2 * ld * cols * sizeof(double) +
+                      (size_t)rt.nslots * (sizeof(double4) + sizeof(double2) * (1 + cols)) +
+                      (size_t)rt.nrows * cols * sizeof(double) + (size_t(64) << 20),
+                  s);
   AsyncBuf<double2> Z(zlev * per_term, s);
   AsyncBuf<double2> S(zlev * per_term, s);
   AsyncBuf<double> F(ld * cols, s);
