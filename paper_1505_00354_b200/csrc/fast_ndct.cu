@@ -2200,11 +2200,10 @@ void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* 
                        (size_t)num_terms * batch * (size_t(16) << log2n) > (size_t(2) << 30);
   if (FLB_NDCT_CLUSTER && cheb && !transpose && bes->cl_wf && l_lo == 0 && l_hi == num_terms &&
       log2n >= 14 && log2n <= 15 && cl_fill) {
-    switch (log2n) {
-      case 14: launch_cluster_fwd<14>(in, ld_in, out, ld_out, batch, *bes, nonfinite, s); break;
-      case 15: launch_cluster_fwd<15>(in, ld_in, out, ld_out, batch, *bes, nonfinite, s); break;
-      default: launch_cluster_fwd<16>(in, ld_in, out, ld_out, batch, *bes, nonfinite, s); break;
-    }
+    if (log2n == 14)
+      launch_cluster_fwd<14>(in, ld_in, out, ld_out, batch, *bes, nonfinite, s);
+    else
+      launch_cluster_fwd<15>(in, ld_in, out, ld_out, batch, *bes, nonfinite, s);
     return;
   }
   if (log2n > 13) {
@@ -2352,9 +2351,10 @@ void build_bessel_tables(FastNdct* p, int M, cudaStream_t s) {
   note_launch("bessel_tables_kernel");
 }
 
-// The cluster kernel's weight table (2^14 <= N <= 2^16, forward).
+// The cluster kernel's weight table (N = 2^14, 2^15, forward: the sizes the
+// dispatch may pick it for).
 void build_cluster_table(FastNdct* p, int M, cudaStream_t s) {
-  if (p->log2n < 14 || p->log2n > 16) return;
+  if (p->log2n < 14 || p->log2n > 15) return;
   const size_t n = p->n;
   if (p->async_alloc)
     FLB_CUDA(cudaMallocAsync(&p->cl_wf, (size_t)M * n * sizeof(double), s));
@@ -2363,8 +2363,7 @@ void build_cluster_table(FastNdct* p, int M, cudaStream_t s) {
   const unsigned grid = (unsigned)((n + 255) / 256);
   switch (p->log2n) {
     case 14: cluster_weight_table_kernel<14><<<grid, 256, 0, s>>>(p->delta, M, p->swap, p->cl_wf); break;
-    case 15: cluster_weight_table_kernel<15><<<grid, 256, 0, s>>>(p->delta, M, p->swap, p->cl_wf); break;
-    default: cluster_weight_table_kernel<16><<<grid, 256, 0, s>>>(p->delta, M, p->swap, p->cl_wf); break;
+    default: cluster_weight_table_kernel<15><<<grid, 256, 0, s>>>(p->delta, M, p->swap, p->cl_wf); break;
   }
   note_launch("cluster_weight_table_kernel");
 }
