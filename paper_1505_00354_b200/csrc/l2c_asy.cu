@@ -45,6 +45,13 @@ constexpr int kMaxM = 24;
 constexpr int kMaxBands = kMaxLev + 1;
 constexpr int kPairsPerWarp = 64;  // two pairs per lane: p = p0 + 64 g + 32 i + lane
 constexpr int kRecThreads = 128;
+// pairs per lane in the transposed recurrence (summed in the lane before the
+// cross-lane reduction): super-groups of 32 kTrPairs pairs
+#ifndef FLB_ASY_TR_PAIRS
+#define FLB_ASY_TR_PAIRS 4
+#endif
+constexpr int kTrPairs = FLB_ASY_TR_PAIRS;
+constexpr int kTrGroups = kTrPairs / 2;  // groups of 64 pairs per super-group
 
 // The expansion's levels, by pair index (kernel parameter).
 struct LevTab {
@@ -362,7 +369,6 @@ __device__ __forceinline__ double warp_transpose_sum(double (&v)[32], int lane) 
 // the lane before the cross-lane reduction) over chunk q; per 32-degree window
 // the lanes' values are summed across the warp and accumulated into the
 // worker's private row of R (the first super-group writes it).
-constexpr int kTrPairs = 4;
 __global__ void __launch_bounds__(kRecThreads) asy_rec_tr_kernel(
     const __grid_constant__ RecTab t, const double2* __restrict__ ab, const double* __restrict__ F,
     size_t ldF, const double2* __restrict__ St, double* __restrict__ R, double nd, long long n) {
@@ -381,13 +387,13 @@ __global__ void __launch_bounds__(kRecThreads) asy_rec_tr_kernel(
   const int q = (int)(loc / B.W), wk = (int)(loc % B.W);
   const long long start = (long long)q * B.lc;
   const long long end = min((long long)(q + 1) * B.lc, B.nu);
-  const long long G2 = (B.G + 1) / 2;
+  const long long G2 = (B.G + kTrGroups - 1) / kTrGroups;
   double* row = R + B.rbase + ((long long)q * B.W + wk) * B.lc;
   for (long long gg = wk; gg < G2; gg += B.W) {
     double y[kTrPairs], P[kTrPairs], d[kTrPairs], ue[kTrPairs], uo[kTrPairs];
 #pragma unroll
     for (int i = 0; i < kTrPairs; ++i) {
-      const long long g = 2 * gg + (i >> 1);
+      const long long g = kTrGroups * gg + (i >> 1);
       const long long p = B.p0 + g * kPairsPerWarp + 32 * (i & 1) + lane;
       const bool ok = p < B.p1;
       y[i] = ok ? pair_y(p, nd) : 0.0;
@@ -847,7 +853,7 @@ L2CAsy* l2c_asy_create(size_t n, const double* s, cudaStream_t st, int M, int R,
     B.Q = (int)((nu + lc - 1) / lc);
     B.G = (int)((p1 - p0 + kPairsPerWarp - 1) / kPairsPerWarp);
     // transposed workers per chunk: ~1024 warps per band, partial rows <= 2^25 entries
-    const long long g2 = (B.G + 1) / 2;
+    const long long g2 = (B.G + kTrGroups - 1) / kTrGroups;
     long long W = std::min<long long>(g2, std::max<long long>(1, (1024 + B.Q - 1) / B.Q));
     while (W > 1 && (long long)B.Q * W * lc > (1ll << 25)) W = (W + 1) / 2;
     B.W = (int)W;
