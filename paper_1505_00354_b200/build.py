@@ -10,7 +10,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 SOURCES = ["capi.cu", "nodes.cu", "fft.cu", "czt.cu", "leg2cheb.cu", "fast_ndct.cu", "direct.cu",
-           "l2c_fast.cu", "l2c_ozaki.cu", "l2c_asy.cu"]
+           "l2c_fast.cu", "l2c_ozaki.cu", "l2c_asy.cu", "dense_gemv.cu"]
 LIB = os.path.join(HERE, "libfastleg_b200.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = [

@@ -20,6 +20,7 @@
 #include "direct.cuh"
 #include "fast_ndct.cuh"
 #include "launch.cuh"
+#include "dense_gemv.cuh"
 #include "l2c_asy.cuh"
 #include "l2c_fast.cuh"
 #include "l2c_ozaki.cuh"
@@ -460,6 +461,7 @@ struct fl_plan {
   L2COzaki* oz[2] = {nullptr, nullptr};  // split-int8 slices of M, (m + 1/2) M^T (lazy)
   int dlt_method = FL_DLT_DIRECT;        // dlt/idlt: dense product where supported
   L2COzaki* dense[2] = {nullptr, nullptr};  // split-int8 slices of P, (m + 1/2) P^T (lazy)
+  DenseGemv* gemv = nullptr;                // fp64 table of P for <= 16 columns (lazy)
   std::mutex mu;
 };
 
@@ -473,6 +475,7 @@ void plan_free(fl_plan* p) {
   if (p->asy) l2c_asy_destroy(p->asy);
   for (L2COzaki* o : p->oz) l2c_ozaki_destroy(o);
   for (L2COzaki* o : p->dense) l2c_ozaki_destroy(o);
+  if (p->gemv) dense_gemv_destroy(p->gemv);
   delete p;
 }
 
@@ -522,6 +525,20 @@ const L2COzaki* plan_dense(fl_plan* p, int idlt, size_t batch, cudaStream_t s) {
     p->dense[idlt] = d;
   }
   return p->dense[idlt];
+}
+
+// The direct method for <= 16 columns (fl_dlt / fl_idlt): fp64 products over
+// the plan's table of P_n(x_k), N even in [256, 8192] (built on first use,
+// published once complete, as plan_dense).
+const DenseGemv* plan_gemv(fl_plan* p, size_t batch, cudaStream_t s) {
+  if (p->dlt_method != FL_DLT_DIRECT || batch > 16 || !dense_gemv_supported(p->n)) return nullptr;
+  std::lock_guard<std::mutex> lock(p->mu);
+  if (!p->gemv) {
+    DenseGemv* g = dense_gemv_create(p->n, p->kind, p->delta, s);
+    FLB_CUDA(cudaStreamSynchronize(s));
+    p->gemv = g;
+  }
+  return p->gemv;
 }
 
 // The asymptotic-expansion conversion of the plan (built on first use and
@@ -1085,6 +1102,19 @@ fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, 
       if (h) fail(FL_INVALID_ARGUMENT, "ndct_apply: non-finite input");
       return;
     }
+    if (const DenseGemv* g = plan_gemv(mp, batch, s)) {
+      DevIn i(in, n, batch, ld, s);
+      DevOut o(out, n, batch, ld, s);
+      DevScratch<int> flag(1, s);
+      FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+      dense_gemv_dlt(*g, i.ptr, i.ld, o.ptr, o.ld, batch, flag.p, s);
+      o.finish();
+      int h = 0;
+      FLB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      sync(s);
+      if (h) fail(FL_INVALID_ARGUMENT, "ndct_apply: non-finite input");
+      return;
+    }
     if (pipeline_ok(in, out, n, batch) && !overflow_guard(n, p->num_terms)) {
       run_pipelined(p->device, n, in, out, batch, ld, s, "ndct_apply",
                     [&](const double* di, double* dq, size_t cols, int* flag, cudaStream_t cs) {
@@ -1148,6 +1178,19 @@ fl_status fl_idlt(const fl_plan* p, const double* in, double* out, size_t batch,
       DevScratch<int> flag(1, s);
       FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
       l2c_dense_apply(*dense, i.ptr, i.ld, p->w, o.ptr, o.ld, batch, flag.p, s);
+      o.finish();
+      int h = 0;
+      FLB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+      sync(s);
+      if (h) fail(FL_INVALID_ARGUMENT, "ndct_apply_transpose: non-finite input");
+      return;
+    }
+    if (const DenseGemv* g = plan_gemv(mp, batch, s)) {
+      DevIn i(in, n, batch, ld, s);
+      DevOut o(out, n, batch, ld, s);
+      DevScratch<int> flag(1, s);
+      FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+      dense_gemv_idlt(*g, i.ptr, i.ld, p->w, o.ptr, o.ld, batch, flag.p, s);
       o.finish();
       int h = 0;
       FLB_CUDA(cudaMemcpyAsync(&h, flag.p, sizeof(int), cudaMemcpyDeviceToHost, s));

@@ -1279,6 +1279,12 @@ CUtensorMap make_map(const int8_t* base, size_t k, size_t rows, size_t z, int bo
 
 }  // namespace
 
+void launch_legendre_table(size_t n, int kind, const double* delta, double* table, cudaStream_t st) {
+  const size_t r = n / 2;
+  legendre_table_kernel<<<(unsigned)((r + 127) / 128), 128, 0, st>>>(n, kind, delta, table);
+  note_launch("legendre_table_kernel");
+}
+
 bool l2c_ozaki_supported(size_t n) { return n % 256 == 0 && n >= 512 && n <= 16384; }
 
 L2COzaki* l2c_ozaki_create(size_t n, const double* s, int transpose, int scale_half,

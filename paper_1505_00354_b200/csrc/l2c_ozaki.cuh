@@ -29,6 +29,9 @@ void l2c_ozaki_apply(const L2COzaki& p, const double* in, double* out, size_t co
 constexpr size_t kDenseMaxN = 8192;
 bool l2c_dense_supported(size_t n);
 L2COzaki* l2c_dense_create(size_t n, int kind, const double* delta, int idlt, cudaStream_t st);
+// The table itself: table[m (n/2) + k] = P_m(cos(theta*_kind(k) + delta_k)),
+// k < n/2 (double-double, rounded once), n even.
+void launch_legendre_table(size_t n, int kind, const double* delta, double* table, cudaStream_t st);
 // DLT: out = P in; IDLT: out = (m + 1/2) P^T (w . in) (w: the quadrature
 // weights, device). Input / output columns of strides ld_in / ld_out.
 // nonfinite (device int, may be null): set when an input column (times w)

@@ -118,3 +118,60 @@ def test_direct_zero_and_scaled_columns():
     f = fl.dlt(c, cfg)
     assert np.all(f[3] == 0.0)
     assert np.array_equal(f[4], f[6] * 2.0 ** -600) and np.array_equal(f[5], f[6] * 2.0 ** 600)
+
+
+@pytest.mark.parametrize("n", [256, 300, 512, 1000, 1024, 2048, 4096, 8192])
+@pytest.mark.parametrize("kind", [CHEB1, CHEBSTAR])
+def test_direct_few_columns_fp64_table(n, kind):
+    """<= 16 columns (C1 and the C3 sweep up to 8192): the direct method as
+    fp64 products over the plan's table of P_n(x_k) (dense_gemv.cu), against
+    the oracle and the factored GPU path; one column and 3 / 16 columns with a
+    stride (host and device buffers)."""
+    import torch
+    cfg = fl.TransformConfig(n, TOL, K[kind])
+    g = cfg.grid()
+    c = fl.random_decaying(n, 0.5, 80 + n, batch=16)
+    v = fl.random_decaying(n, 0.0, 90 + n, batch=16)
+    t = tol_n(n)
+    f1 = fl.dlt(c[0], cfg)
+    b1 = fl.idlt(v[0], cfg).values
+    assert rel(f1, O.dlt_grid(c[0], kind, TOL, g.theta, g.x, g.weights), np.abs(c[0]).sum()) <= t
+    assert rel(b1, O.idlt_grid(v[0], kind, TOL, g.theta, g.x, g.weights), np.abs(v[0]).sum()) <= t
+    f16 = fl.dlt(torch.from_numpy(c).cuda(), cfg).cpu().numpy()
+    b16 = fl.idlt(torch.from_numpy(v).cuda(), cfg).values.cpu().numpy()
+    f3 = fl.dlt(c[:3], cfg)
+    for j in (0, 5, 15):
+        assert rel(f16[j], O.dlt_grid(c[j], kind, TOL, g.theta, g.x, g.weights), np.abs(c[j]).sum()) <= t, j
+        assert rel(b16[j], O.idlt_grid(v[j], kind, TOL, g.theta, g.x, g.weights),
+                   np.abs(v[j]).sum()) <= t, j
+    assert np.array_equal(f16[0], f1) and np.array_equal(f3[2], f16[2])  # batch-invariant
+    cfg.set_dlt_method(fl.DLT_FACTORED)
+    f2 = fl.dlt(c[:3], cfg)
+    b2 = fl.idlt(v[:3], cfg).values
+    for j in range(3):
+        assert rel(f3[j], f2[j], np.abs(c[j]).sum()) <= t, j
+        assert rel(b16[j], b2[j], np.abs(v[j]).sum()) <= t, j
+
+
+def test_direct_few_columns_edge_cases():
+    """Strided device columns, non-finite inputs (the reference's
+    invalid_argument), bit-identical repetition."""
+    import torch
+    n = 1024
+    cfg = fl.TransformConfig(n)
+    c = fl.random_decaying(n, 0.5, 7, batch=5)
+    base = fl.dlt(c, cfg)
+    wide = torch.zeros(5, n + 37, dtype=torch.float64, device="cuda")
+    wide[:, :n] = torch.from_numpy(c).cuda()
+    out = torch.zeros(5, n + 37, dtype=torch.float64, device="cuda")  # one stride for both
+    _lib.check(_lib.LIB.fl_dlt(cfg.handle, C.c_void_p(wide.data_ptr()), C.c_void_p(out.data_ptr()), 5, n + 37,
+                               C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    assert np.array_equal(out[:, :n].cpu().numpy(), base)
+    assert all(np.array_equal(fl.dlt(c, cfg), base) for _ in range(3))
+    bad = c.copy()
+    bad[3, 17] = np.nan
+    with pytest.raises(fl.InvalidArgument, match="ndct_apply: non-finite input"):
+        fl.dlt(bad, cfg)
+    bad[3, 17] = np.inf
+    with pytest.raises(fl.InvalidArgument, match="ndct_apply_transpose: non-finite input"):
+        fl.idlt(bad, cfg)

@@ -53,15 +53,21 @@ COLS = (0, 17, 39)
 @pytest.mark.parametrize("n", SWEEP)
 @pytest.mark.parametrize("kind", [CHEB1, CHEBSTAR])
 def test_dlt_idlt_sweep(n, kind):
-    fast = fl.TransformConfig(n, TOL, K[kind], ndct_mode=fl.NDCT_FAST)
-    g = fast.grid()
+    # the default plan (for N <= 8192 the direct method: the int8 tensor-core
+    # product for 40 columns, the fp64 table product for one) and the
+    # factored path (conversion + NDCT) in both NDCT modes
+    dflt = fl.TransformConfig(n, TOL, K[kind])
+    g = dflt.grid()
+    fast = fl.TransformConfig(n, TOL, K[kind], grid=g, ndct_mode=fl.NDCT_FAST)
+    fast.set_dlt_method(fl.DLT_FACTORED)
     lit = fl.TransformConfig(n, TOL, K[kind], grid=g, ndct_mode=fl.NDCT_LITERAL)
+    lit.set_dlt_method(fl.DLT_FACTORED)
     c = fl.random_decaying(n, 0.5, 900 + n, batch=40)
     v = fl.random_decaying(n, 0.0, 5000 + n, batch=40)  # values at the nodes for the IDLT
     jobs_f = {j: POOL.submit(O.dlt_grid, c[j], kind, TOL, g.theta, g.x, g.weights) for j in COLS}
     jobs_b = {j: POOL.submit(O.idlt_grid, v[j], kind, TOL, g.theta, g.x, g.weights) for j in COLS}
     got = {}
-    for name, cfg in (("fast", fast), ("literal", lit)):
+    for name, cfg in (("default", dflt), ("factored fast", fast), ("factored literal", lit)):
         got[name] = (fl.dlt(c, cfg), fl.idlt(v, cfg).values, fl.dlt(c[0], cfg), fl.idlt(v[0], cfg).values)
     ref_f = {j: jobs_f[j].result() for j in COLS}
     ref_b = {j: jobs_b[j].result() for j in COLS}
