@@ -440,7 +440,7 @@ def sub_configs(args, dist, rank: int, world: int, local: int) -> dict:
         except RuntimeError:
             pass
         r["workload"] = CONFIGS["c1"][3]
-        r["bound"] = "latency (one column: 14 NDCT terms in one CTA + one conversion)"
+        r["bound"] = "latency (one column: the direct method as two fp64 table row products, 4 MiB table in L2)"
         out["c1"] = r
 
         # C2: NDCT only, N = 65536 x 64 columns, iid N(0,1), the node kernel's grid
