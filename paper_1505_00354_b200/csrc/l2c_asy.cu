@@ -30,6 +30,8 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -323,7 +325,7 @@ __global__ void __launch_bounds__(kRecThreads) asy_rec_fwd_kernel(
   }
 }
 
-// f_k = E + O, f_{N-1-k} = E - O (written: the expansion levels add to it)
+// f_k += E + O, f_{N-1-k} += E - O (F zeroed; the expansion levels add to it too)
 __global__ void asy_rec_fwd_finish_kernel(const __grid_constant__ RecTab t, const double2* __restrict__ Ep,
                                           double* __restrict__ F, size_t ldF, long long n) {
   const long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
@@ -344,8 +346,8 @@ __global__ void asy_rec_fwd_finish_kernel(const __grid_constant__ RecTab t, cons
     E += v.x;
     O += v.y;
   }
-  F[p] = E + O;
-  F[n - 1 - p] = E - O;
+  F[p] += E + O;
+  F[n - 1 - p] += E - O;
 }
 
 // lane i gets sum over the warp's lanes of v[i] (31 shuffles, recursive halving)
@@ -935,48 +937,92 @@ void reserve_scratch(size_t bytes, cudaStream_t s) {
   cudaGetLastError();
 }
 
-void recurrence_forward(const L2CAsy& f, const RecTab& rt, const double* c, size_t ld, double* F,
-                        size_t cols, cudaStream_t s) {
+// The recurrence's scratch (allocated on the caller's stream before the fork).
+struct RecBufs {
+  double4* T;   // chunk transfer matrices
+  double2* St;  // chunk start states
+  double2* Ep;  // forward: per (pair, chunk) even / odd partial sums
+  double* R;    // transposed: per-worker partial rows
+};
+
+// The recurrence runs on an auxiliary stream beside the expansion's level
+// transforms: it is FP64-issue-bound, they are HBM-bound.
+cudaStream_t aux_stream() {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> per_dev;
+  int dev = 0;
+  FLB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  auto it = per_dev.find(dev);
+  if (it == per_dev.end()) {
+    // the lowest priority: the levels' kernels (the caller's stream) take
+    // the SMs first, the recurrence's CTAs fill what they leave
+    int least = 0, greatest = 0;
+    FLB_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    cudaStream_t st;
+    FLB_CUDA(cudaStreamCreateWithPriority(&st, cudaStreamNonBlocking, least));
+    it = per_dev.emplace(dev, st).first;
+  }
+  return it->second;
+}
+
+void recurrence_chains(const L2CAsy& f, const RecTab& rt, int transpose, const double* x, size_t ld,
+                       size_t cols, const RecBufs& b, cudaStream_t s) {
   if (rt.nb == 0) return;
   const long long n = (long long)f.n;
   const double nd = (double)n;
-  AsyncBuf<double4> T(rt.nslots, s);
-  AsyncBuf<double2> St(rt.nslots, s);
-  AsyncBuf<double2> Ep(rt.nslots * cols, s);
-  const unsigned wg = grid_for(rt.nwarps * 32, kRecThreads, 1ll << 31);
-  asy_rec_transfer_kernel<<<wg, kRecThreads, 0, s>>>(rt, f.ab, nd, T.p);
+  asy_rec_transfer_kernel<<<grid_for(rt.nwarps * 32, kRecThreads, 1ll << 31), kRecThreads, 0, s>>>(
+      rt, f.ab, nd, b.T);
   note_launch("asy_rec_transfer_kernel");
-  asy_rec_prefix_kernel<<<grid_for(rt.ngslots, 128, 1ll << 31), 128, 0, s>>>(rt, T.p, St.p, nd);
+  asy_rec_prefix_kernel<<<grid_for(rt.ngslots, 128, 1ll << 31), 128, 0, s>>>(rt, b.T, b.St, nd);
   note_launch("asy_rec_prefix_kernel");
-  asy_rec_fwd_kernel<<<dim3(wg, (unsigned)cols), kRecThreads, 0, s>>>(rt, f.ab, c, ld, St.p, Ep.p, nd);
-  note_launch("asy_rec_fwd_kernel");
+  if (!transpose) {
+    asy_rec_fwd_kernel<<<dim3(grid_for(rt.nwarps * 32, kRecThreads, 1ll << 31), (unsigned)cols),
+                         kRecThreads, 0, s>>>(rt, f.ab, x, ld, b.St, b.Ep, nd);
+    note_launch("asy_rec_fwd_kernel");
+  } else {
+    asy_rec_tr_kernel<<<dim3(grid_for(rt.nxwarps * 32, kRecThreads, 1ll << 31), (unsigned)cols),
+                        kRecThreads, 0, s>>>(rt, f.ab, x, ld, b.St, b.R, nd, n);
+    note_launch("asy_rec_tr_kernel");
+  }
+}
+
+// forward: F (zeroed, the levels added) += the recurrence's sums
+void recurrence_forward_finish(const L2CAsy& f, const RecTab& rt, const RecBufs& b, double* F, size_t ld,
+                               size_t cols, cudaStream_t s) {
+  if (rt.nb == 0) return;
   asy_rec_fwd_finish_kernel<<<dim3(grid_for(rt.ngslots, 256, 1ll << 31), (unsigned)cols), 256, 0, s>>>(
-      rt, Ep.p, F, ld, n);
+      rt, b.Ep, F, ld, (long long)f.n);
   note_launch("asy_rec_fwd_finish_kernel");
 }
 
-void recurrence_transpose(const L2CAsy& f, const RecTab& rt, const double* F, size_t ld, double* out,
-                          size_t cols, int scale_half, cudaStream_t s) {
+// transposed: out (the levels added) += the recurrence's rows, then (n + 1/2)
+// (also without bands: the scaling of the whole output)
+void recurrence_transpose_finish(const L2CAsy& f, const RecTab& rt, const RecBufs& b, double* out,
+                                 size_t ld, size_t cols, int scale_half, cudaStream_t s) {
   const long long n = (long long)f.n;
-  const double nd = (double)n;
-  AsyncBuf<double4> T(rt.nslots, s);
-  AsyncBuf<double2> St(rt.nslots, s);
-  AsyncBuf<double> R(rt.nrows * cols, s);
-  if (rt.nb > 0) {
-    asy_rec_transfer_kernel<<<grid_for(rt.nwarps * 32, kRecThreads, 1ll << 31), kRecThreads, 0, s>>>(
-        rt, f.ab, nd, T.p);
-    note_launch("asy_rec_transfer_kernel");
-    asy_rec_prefix_kernel<<<grid_for(rt.ngslots, 128, 1ll << 31), 128, 0, s>>>(rt, T.p, St.p, nd);
-    note_launch("asy_rec_prefix_kernel");
-    asy_rec_tr_kernel<<<dim3(grid_for(rt.nxwarps * 32, kRecThreads, 1ll << 31), (unsigned)cols),
-                      kRecThreads, 0, s>>>(rt, f.ab, F, ld, St.p, R.p, nd, n);
-    note_launch("asy_rec_tr_kernel");
-  }
-  // (also without bands: the (n + 1/2) scaling of the whole output)
-  asy_rec_tr_finish_kernel<<<dim3((unsigned)(n / 32), (unsigned)cols), 256, 0, s>>>(rt, R.p, out, ld, n,
+  asy_rec_tr_finish_kernel<<<dim3((unsigned)(n / 32), (unsigned)cols), 256, 0, s>>>(rt, b.R, out, ld, n,
                                                                                    scale_half);
   note_launch("asy_rec_tr_finish_kernel");
 }
+
+// Event fork / join between the caller's stream and the recurrence stream.
+struct Fork {
+  cudaStream_t main, aux;
+  cudaEvent_t ev[2];
+  Fork(cudaStream_t s) : main(s), aux(aux_stream()) {
+    for (cudaEvent_t& e : ev) FLB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    FLB_CUDA(cudaEventRecord(ev[0], main));
+    FLB_CUDA(cudaStreamWaitEvent(aux, ev[0], 0));
+  }
+  void join() {
+    FLB_CUDA(cudaEventRecord(ev[1], aux));
+    FLB_CUDA(cudaStreamWaitEvent(main, ev[1], 0));
+  }
+  ~Fork() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+};
 
 }  // namespace
 
@@ -1051,12 +1097,19 @@ void l2c_asy_apply(const L2CAsy& f, int transpose, const double* in, double* out
   AsyncBuf<double2> Z(zlev * per_term, s);
   AsyncBuf<double2> S(zlev * per_term, s);
   AsyncBuf<double> F(ld * cols, s);
+  AsyncBuf<double4> T(rt.nslots, s);
+  AsyncBuf<double2> St(rt.nslots, s);
+  AsyncBuf<double2> Ep(transpose ? 0 : rt.nslots * cols, s);
+  AsyncBuf<double> R(transpose ? rt.nrows * cols : 0, s);
+  const RecBufs rb{T.p, St.p, Ep.p, R.p};
   const unsigned gp = grid_for(P, 256, 4096);
   if (!transpose) {
-    // values at the cheb1 points: recurrence part (written; zero first unless
-    // every band runs), then the levels
-    if (!full) FLB_CUDA(cudaMemset2DAsync(F.p, ld * sizeof(double), 0, n * sizeof(double), cols, s));
-    recurrence_forward(f, rt, in, ld, F.p, cols, s);
+    // values at the cheb1 points: the recurrence's sums, then the levels'
+    // (on one stream: beside the levels' transforms the forward chains ran
+    // slower -- 2^20 2.9 vs 2.2 ms, 2^22 11.9 vs 10.5 ms)
+    FLB_CUDA(cudaMemset2DAsync(F.p, ld * sizeof(double), 0, n * sizeof(double), cols, s));
+    recurrence_chains(f, rt, 0, in, ld, cols, rb, s);
+    recurrence_forward_finish(f, rt, rb, F.p, ld, cols, s);
     for (const Seg& g : segs) {
       asy_fwd_pack_kernel<<<dim3(gp, (unsigned)cols, (unsigned)(g.l1 - g.l0)), 256, 0, s>>>(
           f.lt, g.l0, g.m0, g.nm, in, ld, f.Cn, n, cols, Z.p);
@@ -1080,6 +1133,10 @@ void l2c_asy_apply(const L2CAsy& f, int transpose, const double* in, double* out
     note_launch("asy_cheb_scale_kernel");
     fast_trig(FL_DCT_III, f.n, G.p, F.p, cols, ld, s);
     FLB_CUDA(cudaMemset2DAsync(out, ld * sizeof(double), 0, n * sizeof(double), cols, s));
+    // the transposed recurrence on the auxiliary stream beside the levels
+    // (2^20 2.6 -> 2.2 ms, 2^22 11.5 -> 9.4, 2^24 52.9 -> 44.1; 2^26 unchanged)
+    Fork fk(s);
+    recurrence_chains(f, rt, 1, F.p, ld, cols, rb, fk.aux);
     for (const Seg& g : segs) {
       asy_tr_pack_kernel<<<dim3(gp, (unsigned)cols, (unsigned)(g.l1 - g.l0)), 256, 0, s>>>(
           f.lt, g.l0, g.m0, g.nm, F.p, ld, n, cols, Z.p);
@@ -1089,7 +1146,8 @@ void l2c_asy_apply(const L2CAsy& f, int transpose, const double* in, double* out
           f.lt, g.l0, g.l1, g.m0, g.nm, Z.p, n, cols, f.Cn, out, ld);
       note_launch("asy_tr_unpack_kernel");
     }
-    recurrence_transpose(f, rt, F.p, ld, out, cols, scale_half, s);
+    fk.join();
+    recurrence_transpose_finish(f, rt, rb, out, ld, cols, scale_half, s);
   }
 }
 
