@@ -2120,6 +2120,14 @@ __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, si
 // output): 3 launches + the FFT's passes per batch of terms instead of 4 per
 // term. Terms are batched within a 2 GiB scratch budget (C2, 65536 x 64: all
 // 14 terms at once; C5, one 2^26 column: two at a time).
+// Scratch of one batched multi-pass NDCT call (packed rows + FFT scratch):
+// 8 GiB (2^26: 2 batches of 7 terms: NDCT 35.9 -> 32.0 ms, NDCT^T 42.4 ->
+// 37.6 ms against 2 GiB; 16 GiB: 31.5 / 36.5 ms).
+#ifndef FLB_BIG_BUDGET_GIB
+#define FLB_BIG_BUDGET_GIB 8
+#endif
+constexpr size_t kBigBudget = size_t(FLB_BIG_BUDGET_GIB) << 30;
+
 void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double* out,
                 size_t ld_out, size_t batch, const double* delta, int l_lo, int l_hi,
                 int plain_op, const double* mult, int* nonfinite, cudaStream_t s, int cheb,
@@ -2134,7 +2142,7 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
   const BigTerms bt{plain, plain_op, cheb, swap};
   const int terms = l_hi - l_lo;
   if (terms <= 0) return;
-  constexpr size_t kBudget = size_t(2) << 30;  // Z + S bytes
+  constexpr size_t kBudget = kBigBudget;  // Z + S bytes
   const size_t per_term_col = 2 * P * sizeof(double2);
   const size_t chunk = std::max<size_t>(1, std::min<size_t>(batch, kBudget / per_term_col));
   const int tb = (int)std::max<size_t>(1, std::min<size_t>(terms, kBudget / (per_term_col * chunk)));
@@ -2190,14 +2198,14 @@ void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* 
 #define FLB_NDCT_CLUSTER 1
 #endif
   // the cluster kernel wins where the multi-pass path has to cut the batch
-  // into several scratch-sized pieces (all terms x columns > 2 GiB of packed
-  // rows): 16384 x 4096 8.8 vs 14.5 ms; elsewhere the multi-pass path (all
+  // into several scratch-sized pieces (all terms x columns beyond its
+  // scratch): 16384 x 4096 8.8 vs 14.5 ms; elsewhere the multi-pass path (all
   // terms packed per thread, shared twiddles) ties or wins: 16384 x 256 0.66
   // vs 0.65, 32768 x 128 0.82 vs 0.68, 65536 x 128 1.98 vs 1.28, 65536 x 512
   // 7.6 vs 6.1 ms
   const size_t cs = (size_t(1) << log2n) / 8192;
   const bool cl_fill = batch * cs >= 2 * (size_t)sm_count() &&
-                       (size_t)num_terms * batch * (size_t(16) << log2n) > (size_t(2) << 30);
+                       (size_t)num_terms * batch * (size_t(16) << log2n) > kBigBudget;
   if (FLB_NDCT_CLUSTER && cheb && !transpose && bes->cl_wf && l_lo == 0 && l_hi == num_terms &&
       log2n >= 14 && log2n <= 15 && cl_fill) {
     if (log2n == 14)

@@ -2,7 +2,7 @@
 one column per thread-block cluster of N/8192 CTAs, the N/2-point FFT of each
 Chebyshev-expansion term as a four-step over the cluster with the exchange
 through distributed shared memory). It runs for batches whose packed rows
-(terms x columns) exceed the multi-pass path's 2 GiB scratch; checked against
+(terms x columns) exceed the multi-pass path's 8 GiB scratch; checked against
 the oracle and against the multi-pass path (a few columns of the same block)
 at the north star's tolerance."""
 import math
@@ -16,7 +16,7 @@ import paper_1505_00354_b200 as fl
 pytestmark = pytest.mark.gpu
 
 
-@pytest.mark.parametrize("n,cols", [(16384, 640), (32768, 320)])
+@pytest.mark.parametrize("n,cols", [(16384, 2400), (32768, 1200)])
 def test_cluster_ndct_vs_oracle_and_multipass(n, cols):
     import torch
     grid = fl.legendre_nodes_weights(n)
