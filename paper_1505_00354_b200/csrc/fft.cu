@@ -312,6 +312,112 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
   }
 }
 
+// The plain line pass with its first and last Stockham passes fused into the
+// global load / store: a thread loads its first radix-8 butterfly's inputs
+// x[tid + r L/8] straight from global memory, and (when the input and output
+// layouts agree) stores its last pass's outputs straight to global memory --
+// two of the per-element shared-memory round trips of fft_line_kernel saved
+// (its passes were L1/shared-memory-bound: 87-96 % l1tex throughput).
+// Threads are laid out line-minor for column passes (consecutive threads:
+// consecutive lines, LINES x 16 B runs) and element-minor for row passes.
+template <int LOG2L, bool INV>
+__global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
+    fft_line_fused_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
+                          unsigned long long P, LineMap mp, const double2* __restrict__ tw) {
+  using Q = LinePass<LOG2L>;
+  constexpr int L = Q::L, LINES = Q::LINES, TL = Q::TL, E = Q::E;
+  constexpr int R0 = pass_radix(L, 1);
+  static_assert(R0 == E, "one first-pass butterfly per thread");
+  constexpr int NSL = last_pass_ns(L), RL = L / NSL;
+  extern __shared__ double2 sm[];
+  const uint32_t l0 = blockIdx.x * (uint32_t)LINES;
+  const uint32_t mmask = (uint32_t)mp.M - 1u, qmask = (uint32_t)(mp.Q - 1);
+  const int mshift = __ffsll((long long)mp.M) - 1;
+  const uint32_t Hin = (uint32_t)mp.Hin, Sin = (uint32_t)mp.Sin, Hout = (uint32_t)mp.Hout,
+                 Sout = (uint32_t)mp.Sout;
+  const uint32_t tu = (uint32_t)mp.u, tv = (uint32_t)mp.v, tz = (uint32_t)mp.z;
+  const bool rows_in = mp.Sin == 1, rows_out = mp.Sout == 1;
+  const int t = threadIdx.x;
+  const int line = rows_in ? t / TL : t % LINES;
+  const int tid = rows_in ? t % TL : t / LINES;
+  const size_t item = blockIdx.y;
+  const double2* src_item = src + item * P;
+  double2* dst_item = dst + item * P;
+  double2* row = sm + line * Q::LS;
+  const uint32_t lq = l0 + line, lo = lq & mmask, hi = lq >> mshift;
+  auto out_twiddle = [&](uint32_t l_lo, uint32_t l_hi, uint32_t k, double2 x) {
+    if (mp.Q) {
+      const uint32_t m = (l_lo * (l_hi * tu + k * tv) + l_hi * k * tz) & qmask;
+      const double2 a = __ldg(&mp.twlo[m & ((1u << mp.twh) - 1u)]);
+      const double2 b = __ldg(&mp.twhi[m >> mp.twh]);
+      const double cs = a.x * b.x - a.y * b.y;
+      double sn = a.x * b.y + a.y * b.x;
+      if (INV) sn = -sn;
+      x = make_double2(x.x * cs - x.y * sn, x.x * sn + x.y * cs);
+    }
+    return x;
+  };
+  // first pass (NS = 1, no twiddles) from global memory
+  double2 v[E];
+#pragma unroll
+  for (int r = 0; r < R0; ++r) v[r] = src_item[lo + hi * Hin + (uint32_t)(tid + r * (L / R0)) * Sin];
+  pass_compute<L, E, R0, 1, INV>(v, tid, tw);
+  pass_store<L, E, R0, 1>(v, row, tid);
+  __syncthreads();
+  // middle passes in shared memory
+  mid_passes<L, E, R0, NSL, INV, 0>(row, tid, tw, 0);
+  // last pass
+  pass_load<L, E, RL>(v, row, tid);
+  pass_compute<L, E, RL, NSL, INV>(v, tid, tw + pass_tw_offset(L, NSL));
+  if (rows_in == rows_out) {
+#pragma unroll
+    for (int q = 0; q < E / RL; ++q)
+#pragma unroll
+      for (int r = 0; r < RL; ++r) {
+        const uint32_t k = (uint32_t)pass_out_index<L, E, RL, NSL>(tid, q, r);
+        dst_item[lo + hi * Hout + k * Sout] = out_twiddle(lo, hi, k, v[q * RL + r]);
+      }
+  } else {
+    // a transposing pass: through shared memory for a coalesced store
+    __syncthreads();
+    pass_store<L, E, RL, NSL>(v, row, tid);
+    __syncthreads();
+    constexpr int PER = LINES * L / Q::THREADS;
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int i = t + r * Q::THREADS;
+      const int j = rows_out ? i / L : i % LINES, k = rows_out ? i % L : i / LINES;
+      const uint32_t l = l0 + j, llo = l & mmask, lhi = l >> mshift;
+      dst_item[llo + lhi * Hout + (uint32_t)k * Sout] =
+          out_twiddle(llo, lhi, (uint32_t)k, sm[j * Q::LS + smem_pad(k)]);
+    }
+  }
+}
+
+#ifndef FLB_FFT_FUSED
+#define FLB_FFT_FUSED 1
+#endif
+template <int LOG2L, bool INV>
+void launch_line_fused(const double2* src, double2* dst, unsigned long long P, size_t items,
+                       const LineMap& mp, cudaStream_t s) {
+  using Q = LinePass<LOG2L>;
+  const double2* tw = pass_twiddles(LOG2L);
+  const unsigned long long lines = P >> LOG2L;
+  LineMap m2 = mp;
+  if (m2.Q) {
+    const int lq = __builtin_ctzll(m2.Q);
+    const auto t2 = twiddle_pair(lq);
+    m2.twlo = t2.first;
+    m2.twhi = t2.second;
+    m2.twh = (lq + 1) / 2;
+  }
+  auto kern = fft_line_fused_kernel<LOG2L, INV>;
+  FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM));
+  dim3 grid((unsigned)(lines / Q::LINES), (unsigned)items);
+  kern<<<grid, Q::THREADS, Q::SMEM, s>>>(src, dst, P, m2, tw);
+  note_launch("fft_line_fused_kernel");
+}
+
 template <int LOG2L, bool INV, int IN, bool MID>
 void launch_line(const LineIO& io, unsigned long long P, size_t items, const LineMap& mp,
                  cudaStream_t s) {
@@ -355,6 +461,19 @@ void line_pass(int log2l, const LineIO& io, unsigned long long P, size_t items, 
 template <bool INV>
 void line_pass(int log2l, const double2* src, double2* dst, unsigned long long P, size_t items,
                const LineMap& mp, cudaStream_t s) {
+  if (FLB_FFT_FUSED) {
+    switch (log2l) {
+      case 5: launch_line_fused<5, INV>(src, dst, P, items, mp, s); return;
+      case 6: launch_line_fused<6, INV>(src, dst, P, items, mp, s); return;
+      case 7: launch_line_fused<7, INV>(src, dst, P, items, mp, s); return;
+      case 8: launch_line_fused<8, INV>(src, dst, P, items, mp, s); return;
+      case 9: launch_line_fused<9, INV>(src, dst, P, items, mp, s); return;
+      case 10: launch_line_fused<10, INV>(src, dst, P, items, mp, s); return;
+      case 11: launch_line_fused<11, INV>(src, dst, P, items, mp, s); return;
+      case 12: launch_line_fused<12, INV>(src, dst, P, items, mp, s); return;
+      default: fail(FL_RUNTIME_ERROR, "fft: unsupported line length");
+    }
+  }
   LineIO io{};
   io.src = src;
   io.dst = dst;
