@@ -460,7 +460,18 @@ def sub_configs(args, dist, rank: int, world: int, local: int) -> dict:
                                                           vp(y.data_ptr()), cols, n, sp)), 5)
             r[kind.name] = {"L": L, "ndct_ms": f, "ndct_T_ms": t, "ndct_coeffs_per_s": n * cols / f * 1e3,
                             "ndct_T_coeffs_per_s": n * cols / t * 1e3,
-                            "hbm_frac": 16.0 * n * cols / (f / 1e3) / 1e9 / peak}
+                            "hbm_frac": 16.0 * n * cols / (f / 1e3) / 1e9 / peak,
+                            "api": "free functions ndct_apply / _transpose (ndct.hpp:98-143): the "
+                                   "expansion's tables are planned on every call"}
+        # the same NDCT through a TransformConfig (planned once: the dlt's NDCT step)
+        cfg2 = fl.TransformConfig(n)
+        f = timed(lambda: _lib.check(_lib.LIB.fl_plan_ndct(cfg2.handle, 0, vp(x.data_ptr()), vp(y.data_ptr()),
+                                                            cols, n, sp)), 5)
+        t = timed(lambda: _lib.check(_lib.LIB.fl_plan_ndct(cfg2.handle, 1, vp(x.data_ptr()), vp(y.data_ptr()),
+                                                            cols, n, sp)), 5)
+        r["planned_chebstar"] = {"ndct_ms": f, "ndct_T_ms": t, "ndct_coeffs_per_s": n * cols / f * 1e3,
+                                 "ndct_T_coeffs_per_s": n * cols / t * 1e3,
+                                 "api": "fl_plan_ndct (TransformConfig planned once)"}
         out["c2"] = r
 
         # C3: the sweep N = 2^10 .. 2^20 (headline 2^20)
