@@ -489,7 +489,6 @@ void plan_finish(fl_plan* p) {
   launch_lambda(n - 1, p->lambda, 0);
   scaled_lambda(p->lambda, p->s, n, 0);
   p->fast = fast_ndct_create(n, p->tolerance, p->kind, p->delta);
-  if (n >= kL2CFastMin) p->l2c = l2c_fast_create(n, p->s, 0);
   FLB_CUDA(cudaDeviceSynchronize());
 }
 
@@ -525,6 +524,21 @@ const L2COzaki* plan_dense(fl_plan* p, int idlt, size_t batch, cudaStream_t s) {
     p->dense[idlt] = d;
   }
   return p->dense[idlt];
+}
+
+// The plan's Toeplitz-Hankel factors (n >= 2^14), built on first use: plans
+// whose conversion is the asymptotic expansion (power-of-two n >= 2^20) never
+// pay the pivoted Cholesky (0.24 s at 2^26).
+L2CFast* plan_th(const fl_plan* cp, cudaStream_t s) {
+  fl_plan* p = const_cast<fl_plan*>(cp);
+  if (p->n < kL2CFastMin) return nullptr;
+  std::lock_guard<std::mutex> lock(p->mu);
+  if (!p->l2c) {
+    L2CFast* f = l2c_fast_create(p->n, p->s, s);
+    FLB_CUDA(cudaStreamSynchronize(s));
+    p->l2c = f;
+  }
+  return p->l2c;
 }
 
 // The direct method for <= 16 columns (fl_dlt / fl_idlt): fp64 products over
@@ -581,8 +595,8 @@ void plan_convert(fl_plan* p, int transpose, const double* in, double* out, size
   const L2CAsy* asy = plan_wants_asy(p, batch) ? plan_asy(p, s) : nullptr;
   if (asy)
     l2c_asy_apply(*asy, transpose, in, out, batch, n, transpose, s);
-  else if (p->l2c && p->l2c_mode != FL_LEG2CHEB_DIRECT && batch <= kL2CFastMaxCols)
-    l2c_fast_apply(*p->l2c, transpose, in, out, batch, n, transpose, s);
+  else if (p->l2c_mode != FL_LEG2CHEB_DIRECT && batch <= kL2CFastMaxCols && plan_th(p, s))
+    l2c_fast_apply(*plan_th(p, s), transpose, in, out, batch, n, transpose, s);
   else if (const L2COzaki* oz = plan_ozaki(p, transpose, batch, s))
     l2c_ozaki_apply(*oz, in, out, batch, n, s);
   else
@@ -926,8 +940,10 @@ fl_status fl_plan_stage_terms(const fl_plan* p, int stage, int* count) {
         *count = l2c_asy_terms(*plan_asy(const_cast<fl_plan*>(p), 0));
         return;
       }
-      if (!p->l2c) fail(FL_INVALID_ARGUMENT, "dlt_stage: no Toeplitz-Hankel conversion for this size");
-      *count = std::max(l2c_fast_rank(*p->l2c, 0), l2c_fast_rank(*p->l2c, 1));
+      FLB_CUDA(cudaSetDevice(p->device));
+      const L2CFast* th = plan_th(p, 0);
+      if (!th) fail(FL_INVALID_ARGUMENT, "dlt_stage: no Toeplitz-Hankel conversion for this size");
+      *count = std::max(l2c_fast_rank(*th, 0), l2c_fast_rank(*th, 1));
     } else if (stage == FL_STAGE_NDCT) {
       if (!p->fast || p->n <= 8192)
         fail(FL_INVALID_ARGUMENT, "dlt_stage: term-parallel NDCT needs a power-of-two N > 8192");
@@ -969,7 +985,7 @@ fl_status fl_dlt_stage(const fl_plan* p, int inverse, int stage, int lo, int hi,
         l2c_asy_apply(*plan_asy(const_cast<fl_plan*>(p), s), inverse, i.ptr, o.ptr, 1, n, inverse, s, lo,
                       hi);
       else
-        l2c_fast_apply(*p->l2c, inverse, i.ptr, o.ptr, 1, n, inverse, s, lo, hi);
+        l2c_fast_apply(*plan_th(p, s), inverse, i.ptr, o.ptr, 1, n, inverse, s, lo, hi);
     } else {
       DevScratch<int> flag(1, s);
       FLB_CUDA(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
@@ -1065,8 +1081,15 @@ int fl_plan_uses_direct(const fl_plan* p, size_t batch) {
 }
 
 int fl_plan_leg2cheb_rank(const fl_plan* p, int parity) {
-  if (!p || !p->l2c || parity < 0 || parity > 1) return 0;
-  return l2c_fast_rank(*p->l2c, parity);
+  if (!p || parity < 0 || parity > 1) return 0;
+  // builds the factors on first query (0 below 2^14, or when they fail)
+  L2CFast* th = nullptr;
+  if (guarded([&] {
+        FLB_CUDA(cudaSetDevice(p->device));
+        th = plan_th(p, 0);
+      }) != FL_OK)
+    return 0;
+  return th ? l2c_fast_rank(*th, parity) : 0;
 }
 
 fl_status fl_dlt(const fl_plan* p, const double* in, double* out, size_t batch, size_t ld,

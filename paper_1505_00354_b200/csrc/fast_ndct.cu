@@ -1943,6 +1943,38 @@ __device__ __forceinline__ double big_row(const BigTerms& bt, int l, double x) {
 
 // Per-call tables for terms [l0, l0 + nt): wt[t][k] = big_weight(l0 + t,
 // N delta_k), rt[t][j] = big_row(l0 + t, j/N) (shared by all columns).
+// 1 / i, i < 128: the Bessel series' divisions as products in the per-call
+// tables (one series per term and entry: 2^26 entries x 7 terms took 4.8 ms
+// per table launch with divisions)
+__constant__ double kRecip[128];
+bool recip_ready[64] = {};
+void ensure_recip() {
+  static std::mutex mu;
+  int dev = 0;
+  FLB_CUDA(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 64 && recip_ready[dev]) return;
+  double h[128];
+  h[0] = 0.0;
+  for (int i = 1; i < 128; ++i) h[i] = 1.0 / (double)i;
+  FLB_CUDA(cudaMemcpyToSymbol(kRecip, h, sizeof h));
+  if (dev < 64) recip_ready[dev] = true;
+}
+
+// J_m(y) by its power series (|y| <= ~1 here), reciprocals from kRecip
+__device__ __forceinline__ double bessel_j_tab(int m, double y) {
+  const double h = 0.5 * y, h2 = h * h;
+  double t = 1.0;
+  for (int i = 1; i <= m; ++i) t *= h * kRecip[i];
+  double sum = t;
+  for (int k = 1; k < 40 && m + k < 128; ++k) {
+    t *= -h2 * (kRecip[k] * kRecip[m + k]);
+    sum += t;
+    if (fabs(t) <= 1e-18 * fabs(sum)) break;
+  }
+  return sum;
+}
+
 __global__ void big_tables_kernel(size_t n, int l0, int nt, BigTerms bt,
                                   const double* __restrict__ delta, double* __restrict__ wt,
                                   double* __restrict__ rt) {
@@ -1950,9 +1982,31 @@ __global__ void big_tables_kernel(size_t n, int l0, int nt, BigTerms bt,
   if (j >= n) return;
   const double y0 = bt.plain ? 0.0 : (double)n * delta[j];
   const double x = (double)j / (double)n;
+  // T_l(x) continued by its recurrence from l0 (the same operations as cheb_t)
+  double ta = bt.cheb ? cheb_t(l0, x) : 0.0, tb = bt.cheb ? cheb_t(l0 + 1, x) : 0.0;
   for (int t = 0; t < nt; ++t) {
-    wt[(size_t)t * n + j] = big_weight(bt, l0 + t, y0);
-    rt[(size_t)t * n + j] = big_row(bt, l0 + t, x);
+    const int l = l0 + t;
+    double w;
+    if (bt.plain) {
+      w = 1.0;
+    } else if (bt.cheb) {
+      // bessel_weight with the tabulated series
+      const double jv = bessel_j_tab(l, y0);
+      w = (l & 1) == 0 ? (l == 0 ? 1.0 : 2.0) * (((l >> 1) & 1) ? -jv : jv)
+                       : -2.0 * ((((l - 1) >> 1) & 1) ? -jv : jv);
+      if (bt.swap && (l & 1)) w = -w;
+    } else {
+      w = big_weight(bt, l, y0);
+    }
+    wt[(size_t)t * n + j] = w;
+    if (bt.cheb) {
+      rt[(size_t)t * n + j] = ta;
+      const double tc = 2.0 * x * tb - ta;
+      ta = tb;
+      tb = tc;
+    } else {
+      rt[(size_t)t * n + j] = big_row(bt, l, x);
+    }
   }
 }
 
@@ -2157,6 +2211,7 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
   const unsigned gxq = (unsigned)std::min<size_t>((P / 2 + 256) / 256, 4096);
   for (int l0 = l_lo; l0 < l_hi; l0 += tb) {
     const int nt = std::min(tb, l_hi - l0);
+    ensure_recip();
     big_tables_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, l0, nt, bt, delta, wt, rt);
     note_launch("big_tables_kernel");
     for (size_t c0 = 0; c0 < batch; c0 += chunk) {
