@@ -273,6 +273,45 @@ fl_status fl_plan_stage_cost(const fl_plan* plan, int stage, int term, double* c
 fl_status fl_dlt_stage(const fl_plan* plan, int inverse, int stage, int lo, int hi,
                        const double* in, double* out, void* stream);
 
+/* Distributed four-step NDCT of one vector over P ranks (C5 sharded, the
+ * multi-GPU form north_star names; paper_1505_00354_b200/distributed.py
+ * drives it with NCCL). Replaces, for a vector spread over P GPUs, the
+ * per-term FFTW calls of ndct_apply / ndct_apply_transpose (ndct.hpp:98-143,
+ * trig.hpp:66-73): every term's N/2-point FFT is L1 x L2 (L1 L2 = N/2), the
+ * L2-point FFTs on the rank owning a symmetric set of residues m1 (mod L1)
+ * of the packed input, the L1-point FFTs on the rank owning a block of k2;
+ * ONE all-to-all per group of terms between them (the caller's collective:
+ * per peer and term fl_fs_coef_count complex entries). The coefficient side
+ * lives in a residue layout (fl_fs_to_residue / fl_fs_from_residue map a
+ * natural full vector to the [rank][res_max][2 L2] slabs of a reduce-scatter /
+ * all-gather), the value side in natural blocks of N/P (fl_fs_values maps
+ * them to / from the uniform [peer][N/P^2] exchange layout of the final
+ * all-to-all). Needs a fast-mode plan (power-of-two N), P a power of two,
+ * 2P <= L1 and N <= 2^27. All pointers device; stream-ordered on `stream`.
+ *   fl_fs_info: n, L, L1, L2, KB = L2/P, B = N/P, residues of this rank,
+ *               max residues over ranks, world, rank (10 entries).
+ *   fl_fs_ndct_part(transpose, part, t0, t1, in, out, work, first):
+ *     forward part 1: in = residue-layout chat, out = coefficient exchange
+ *       (send); part 2: in = received exchange, out = value exchange layout
+ *       (accumulated over term groups unless first).
+ *     transpose part 1: in = value exchange layout (received), out = send;
+ *       part 2: in = received, out = residue layout (accumulated unless first).
+ *     work: fl_fs_work_elems complex entries for t1 - t0 terms.
+ *   fl_fs_check: synchronises `stream`; FL_INVALID_ARGUMENT with the
+ *     reference's message when a part-1 call saw a non-finite input. */
+typedef struct fl_fs fl_fs;
+fl_status fl_fs_create(const fl_plan* plan, int world, int rank, fl_fs** fs);
+fl_status fl_fs_destroy(fl_fs* fs);
+fl_status fl_fs_info(const fl_fs* fs, size_t* info);
+fl_status fl_fs_coef_count(const fl_fs* fs, int transpose, int peer, int send, size_t* count);
+size_t fl_fs_work_elems(const fl_fs* fs, int terms);
+fl_status fl_fs_to_residue(const fl_fs* fs, const double* full, double* slabs, void* stream);
+fl_status fl_fs_from_residue(const fl_fs* fs, const double* slabs, double* full, void* stream);
+fl_status fl_fs_values(const fl_fs* fs, int to_block, const double* in, double* out, void* stream);
+fl_status fl_fs_ndct_part(const fl_fs* fs, int transpose, int part, int t0, int t1, const void* in,
+                          void* out, void* work, int first, void* stream);
+fl_status fl_fs_check(const fl_fs* fs, int transpose, void* stream);
+
 /* oracle.hpp:19-153 direct O(N^2) evaluations, on the device (independent of
  * the fast path: plain three-term recurrences, no FFTs).
  *   eval_legendre_direct / eval_chebyshev_direct: out[j] = sum_n c_n P_n(xs[j])

@@ -68,6 +68,8 @@ EXPORTS = [
     "fl_plan_leg2cheb", "fl_plan_ndct", "fl_plan_ndct_terms", "fl_set_free_ndct_mode",
     "fl_free_ndct_mode", "fl_plan_set_dlt_method", "fl_plan_dlt_method", "fl_plan_uses_direct",
     "fl_load_vector", "fl_save_vector", "fl_plan_leg2cheb_asy_info", "fl_plan_stage_cost",
+    "fl_fs_create", "fl_fs_destroy", "fl_fs_info", "fl_fs_coef_count", "fl_fs_work_elems",
+    "fl_fs_to_residue", "fl_fs_from_residue", "fl_fs_values", "fl_fs_ndct_part", "fl_fs_check",
 ]
 
 
@@ -127,6 +129,16 @@ def _load() -> C.CDLL:
         "fl_save_vector": (i, [C.c_char_p, i, dp, sz, vp]),
         "fl_plan_leg2cheb_asy_info": (i, [vp, C.POINTER(i), C.POINTER(i), C.POINTER(i), C.POINTER(d)]),
         "fl_plan_stage_cost": (i, [vp, i, i, C.POINTER(d)]),
+        "fl_fs_create": (i, [vp, i, i, C.POINTER(vp)]),
+        "fl_fs_destroy": (i, [vp]),
+        "fl_fs_info": (i, [vp, C.POINTER(sz)]),
+        "fl_fs_coef_count": (i, [vp, i, i, i, C.POINTER(sz)]),
+        "fl_fs_work_elems": (sz, [vp, i]),
+        "fl_fs_to_residue": (i, [vp, dp, dp, vp]),
+        "fl_fs_from_residue": (i, [vp, dp, dp, vp]),
+        "fl_fs_values": (i, [vp, i, dp, dp, vp]),
+        "fl_fs_ndct_part": (i, [vp, i, i, i, i, vp, vp, vp, i, vp]),
+        "fl_fs_check": (i, [vp, i, vp]),
     }
     for name, (res, args) in sigs.items():
         fn = getattr(lib, name)

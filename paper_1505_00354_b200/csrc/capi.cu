@@ -21,6 +21,7 @@
 #include "fast_ndct.cuh"
 #include "launch.cuh"
 #include "dense_gemv.cuh"
+#include "dist_ndct.cuh"
 #include "l2c_asy.cuh"
 #include "l2c_fast.cuh"
 #include "l2c_ozaki.cuh"
@@ -999,6 +1000,136 @@ fl_status fl_dlt_stage(const fl_plan* p, int inverse, int stage, int lo, int hi,
     }
     o.finish();
     sync(s);
+  });
+}
+
+struct fl_fs {
+  const fl_plan* plan = nullptr;
+  FsLayout* lay = nullptr;
+  int* flag = nullptr;  // non-finite input seen by a part-1 call
+};
+
+fl_status fl_fs_create(const fl_plan* p, int world, int rank, fl_fs** out) {
+  return guarded([&] {
+    if (!p || !out) fail(FL_INVALID_ARGUMENT, "four-step: null argument");
+    *out = nullptr;
+    if (!p->fast || p->mode != FL_NDCT_FAST)
+      fail(FL_INVALID_ARGUMENT, "four-step: needs a fast-mode plan of power-of-two size");
+    FLB_CUDA(cudaSetDevice(p->device));
+    auto* f = new fl_fs;
+    f->plan = p;
+    try {
+      f->lay = fs_create(p->n, world, rank);
+      FLB_CUDA(cudaMalloc(&f->flag, sizeof(int)));
+      FLB_CUDA(cudaMemset(f->flag, 0, sizeof(int)));
+    } catch (...) {
+      if (f->lay) fs_destroy(f->lay);
+      if (f->flag) cudaFree(f->flag);
+      delete f;
+      throw;
+    }
+    *out = f;
+  });
+}
+
+fl_status fl_fs_destroy(fl_fs* f) {
+  return guarded([&] {
+    if (!f) return;
+    fs_destroy(f->lay);
+    if (f->flag) cudaFree(f->flag);
+    delete f;
+  });
+}
+
+fl_status fl_fs_info(const fl_fs* f, size_t* info) {
+  return guarded([&] {
+    if (!f || !info) fail(FL_INVALID_ARGUMENT, "four-step: null argument");
+    const FsInfo i = fs_info(*f->lay);
+    const size_t v[10] = {i.n, i.L, i.L1, i.L2, i.KB, i.B, i.nres, i.res_max, (size_t)i.world,
+                          (size_t)i.rank};
+    std::copy(v, v + 10, info);
+  });
+}
+
+fl_status fl_fs_coef_count(const fl_fs* f, int transpose, int peer, int send, size_t* count) {
+  return guarded([&] {
+    if (!f || !count) fail(FL_INVALID_ARGUMENT, "four-step: null argument");
+    *count = fs_coef_count(*f->lay, transpose, peer, send);
+  });
+}
+
+size_t fl_fs_work_elems(const fl_fs* f, int terms) {
+  if (!f || terms <= 0) return 0;
+  const FsInfo i = fs_info(*f->lay);
+  // rows of either FFT stage: terms x max(nres L2, KB L1)
+  return (size_t)terms * std::max(i.nres * i.L2, i.KB * i.L1);
+}
+
+fl_status fl_fs_to_residue(const fl_fs* f, const double* full, double* slabs, void* stream) {
+  return guarded([&] {
+    if (!f || !full || !slabs) fail(FL_INVALID_ARGUMENT, "four-step: null argument");
+    FLB_CUDA(cudaSetDevice(f->plan->device));
+    fs_to_residue(*f->lay, full, slabs, as_stream(stream));
+  });
+}
+
+fl_status fl_fs_from_residue(const fl_fs* f, const double* slabs, double* full, void* stream) {
+  return guarded([&] {
+    if (!f || !full || !slabs) fail(FL_INVALID_ARGUMENT, "four-step: null argument");
+    FLB_CUDA(cudaSetDevice(f->plan->device));
+    fs_from_residue(*f->lay, slabs, full, as_stream(stream));
+  });
+}
+
+fl_status fl_fs_values(const fl_fs* f, int to_block, const double* in, double* out, void* stream) {
+  return guarded([&] {
+    if (!f || !in || !out) fail(FL_INVALID_ARGUMENT, "four-step: null argument");
+    FLB_CUDA(cudaSetDevice(f->plan->device));
+    if (to_block)
+      fs_values_from_exchange(*f->lay, in, out, as_stream(stream));
+    else
+      fs_values_to_exchange(*f->lay, in, out, as_stream(stream));
+  });
+}
+
+fl_status fl_fs_ndct_part(const fl_fs* f, int transpose, int part, int t0, int t1, const void* in,
+                          void* out, void* work, int first, void* stream) {
+  return guarded([&] {
+    if (!f || !in || !out || !work) fail(FL_INVALID_ARGUMENT, "four-step: null argument");
+    const fl_plan* p = f->plan;
+    FLB_CUDA(cudaSetDevice(p->device));
+    cudaStream_t s = as_stream(stream);
+    auto* w = static_cast<double2*>(work);
+    if (part == 1 && !transpose)
+      fs_fwd1(*f->lay, *p->fast, t0, t1, static_cast<const double*>(in), static_cast<double2*>(out), w,
+              f->flag, s);
+    else if (part == 2 && !transpose)
+      fs_fwd2(*f->lay, *p->fast, t0, t1, static_cast<const double2*>(in), w, static_cast<double*>(out),
+              first, s);
+    else if (part == 1)
+      fs_tr1(*f->lay, *p->fast, p->w, t0, t1, static_cast<const double*>(in), static_cast<double2*>(out),
+             w, f->flag, s);
+    else if (part == 2)
+      fs_tr2(*f->lay, *p->fast, t0, t1, static_cast<const double2*>(in), w, static_cast<double*>(out),
+             first, s);
+    else
+      fail(FL_INVALID_ARGUMENT, "four-step: part must be 1 or 2");
+  });
+}
+
+fl_status fl_fs_check(const fl_fs* f, int transpose, void* stream) {
+  return guarded([&] {
+    if (!f) fail(FL_INVALID_ARGUMENT, "four-step: null argument");
+    FLB_CUDA(cudaSetDevice(f->plan->device));
+    cudaStream_t s = as_stream(stream);
+    int h = 0;
+    FLB_CUDA(cudaMemcpyAsync(&h, f->flag, sizeof(int), cudaMemcpyDeviceToHost, s));
+    sync(s);
+    if (h) {
+      FLB_CUDA(cudaMemset(f->flag, 0, sizeof(int)));
+      fail(FL_INVALID_ARGUMENT, transpose ? "ndct_apply_transpose: non-finite input"
+                                          : "ndct_apply: non-finite input");
+    }
   });
 }
 

@@ -41,6 +41,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <vector>
 
 #include <cooperative_groups.h>
 
@@ -2531,4 +2532,677 @@ void fast_ndct_run(const FastNdct& p, int transpose, const double* in, size_t ld
 namespace flb {
 int fast_ndct_terms(const FastNdct& p) { return p.bes_terms > 0 ? p.bes_terms : p.num_terms; }
 int fast_ndct_dlt_terms(const FastNdct& p) { return fast_ndct_terms(p); }
+}  // namespace flb
+
+// ===========================================================================
+// Distributed four-step NDCT (dist_ndct.cuh): the multi-pass path's pack /
+// unpack arithmetic (big_*_kernel) over the rank-local layouts of a four-step
+// N/2-point FFT whose two FFT stages are separated by one all-to-all.
+// ===========================================================================
+#include "dist_ndct.cuh"
+
+namespace flb {
+
+struct FsLayout {
+  size_t n = 0, L = 0, L1 = 0, L2 = 0, KB = 0, B = 0, U = 0;
+  int log2n = 0, log2L1 = 0, log2L2 = 0, log2KB = 0;
+  int world = 1, rank = 0, device = 0;
+  std::vector<int> nres, cum;  // residues per rank, prefix sums (world + 1)
+  size_t res_max = 0;
+  int* d_res_all = nullptr;  // [world][res_max], -1 padded
+  int* d_mirror = nullptr;   // [nres_me]: local index of (L1 - res) mod L1
+  int* d_owner = nullptr;    // [L1]: rank owning residue m1
+  int* d_lidx = nullptr;     // [L1]: its index in the owner's list
+  int* d_cum = nullptr;      // [world + 1]
+  int* d_nres = nullptr;     // [world]
+  const int* res_me() const { return d_res_all + (size_t)rank * res_max; }
+};
+
+namespace {
+
+constexpr int kFsTile = 32, kFsRows = 8;
+
+struct FsDev {  // by-value kernel view of a layout
+  unsigned long long n, L, L1, L2, KB, B, U;
+  int log2L1, log2L2, log2KB, world, rank, nres_me;
+  unsigned long long res_max;
+  const int *res_all, *mirror, *owner, *lidx, *cum, *nres;
+};
+FsDev fs_dev(const FsLayout& f) {
+  return FsDev{f.n, f.L, f.L1, f.L2, f.KB, f.B, f.U, f.log2L1, f.log2L2, f.log2KB, f.world, f.rank,
+               f.nres[f.rank], f.res_max, f.d_res_all, f.d_mirror, f.d_owner, f.d_lidx, f.d_cum,
+               f.d_nres};
+}
+
+// value side: output index k of packed slot q (the forward unpack's map)
+__device__ __forceinline__ unsigned long long fs_k_of_q(const FsDev& d, unsigned long long q) {
+  return q < d.L ? 2 * q : 2 * (d.n - 1 - q) + 1;
+}
+// first p (= k2 + L2 k1) of block `blk`'s even (g = 0) / odd (g = 1) range
+__device__ __forceinline__ unsigned long long fs_p0(const FsDev& d, unsigned long long blk, int g) {
+  return g ? d.L - (blk + 1) * (d.B / 4) : blk * (d.B / 4);
+}
+// position of slot pair (p, b = 0) in the value exchange layout of the pair
+// (block owner dst, k2-block owner src): [src or dst][g][u][k2l][b]
+__device__ __forceinline__ unsigned long long fs_xpos(const FsDev& d, unsigned long long peer,
+                                                      unsigned long long blk, int g,
+                                                      unsigned long long k1,
+                                                      unsigned long long k2l) {
+  const unsigned long long u = k1 - fs_p0(d, blk, g) / d.L2;
+  return peer * (d.B / d.world) + (((unsigned long long)g * d.U + u) * d.KB + k2l) * 2;
+}
+
+// the Chebyshev-expansion weight of term l at y0 = N delta_k (big_tables_kernel)
+__device__ __forceinline__ double fs_weight(int l, double y0, int swap) {
+  const double jv = bessel_j_tab(l, y0);
+  double w = (l & 1) == 0 ? (l == 0 ? 1.0 : 2.0) * (((l >> 1) & 1) ? -jv : jv)
+                          : -2.0 * ((((l - 1) >> 1) & 1) ? -jv : jv);
+  if (swap && (l & 1)) w = -w;
+  return w;
+}
+
+// natural full vector <-> [dest][res_max][2 L2] (tile transpose: residues x j)
+template <bool TO>
+__global__ void fs_residue_kernel(FsDev d, const double* __restrict__ src, double* __restrict__ dst) {
+  __shared__ double tile[kFsTile][kFsTile + 1];
+  const unsigned long long J = 2 * d.L2;
+  const int dest = blockIdx.z;
+  const unsigned long long i0 = (unsigned long long)blockIdx.y * kFsTile;
+  const unsigned long long j0 = (unsigned long long)blockIdx.x * kFsTile;
+  const int* res = d.res_all + (size_t)dest * d.res_max;
+  const unsigned long long base = (unsigned long long)dest * d.res_max * J;
+  if (TO) {
+    // read along residues (threads over i), write along j
+    for (int jj = threadIdx.y; jj < kFsTile; jj += kFsRows) {
+      const unsigned long long i = i0 + threadIdx.x, j = j0 + jj;
+      double v = 0.0;
+      if (i < d.res_max && j < J) {
+        const int r = res[i];
+        if (r >= 0) v = src[(unsigned long long)r + d.L1 * j];
+      }
+      tile[jj][threadIdx.x] = v;
+    }
+    __syncthreads();
+    for (int ii = threadIdx.y; ii < kFsTile; ii += kFsRows) {
+      const unsigned long long i = i0 + ii, j = j0 + threadIdx.x;
+      if (i < d.res_max && j < J) dst[base + i * J + j] = tile[threadIdx.x][ii];
+    }
+  } else {
+    for (int ii = threadIdx.y; ii < kFsTile; ii += kFsRows) {
+      const unsigned long long i = i0 + ii, j = j0 + threadIdx.x;
+      tile[ii][threadIdx.x] = (i < d.res_max && j < J) ? src[base + i * J + j] : 0.0;
+    }
+    __syncthreads();
+    for (int jj = threadIdx.y; jj < kFsTile; jj += kFsRows) {
+      const unsigned long long i = i0 + threadIdx.x, j = j0 + jj;
+      if (i < d.res_max && j < J) {
+        const int r = res[i];
+        if (r >= 0) dst[(unsigned long long)r + d.L1 * j] = tile[threadIdx.x][jj];
+      }
+    }
+  }
+}
+
+// forward pack of terms [t0, t0 + nt) for this rank's residues: Z[t][i][m2]
+// for m = res_i + L1 m2 (big_fwd_pack_kernel's arithmetic)
+__global__ void fs_fwd_pack_kernel(FsDev d, const double* __restrict__ chat, int t0, int nt,
+                                   BigTerms bt, double2* __restrict__ Z, int* nonfinite) {
+  const unsigned long long J = 2 * d.L2;
+  const unsigned long long total = (unsigned long long)d.nres_me * d.L2;
+  const int* res_me = d.res_all + (size_t)d.rank * d.res_max;
+  const double nd = (double)d.n;
+  for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
+       e += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long i = e >> d.log2L2, m2 = e & (d.L2 - 1);
+    const unsigned long long res = (unsigned long long)res_me[i];
+    const unsigned long long m = res + d.L1 * m2;
+    const double* ci = chat + i * J;
+    const double c0 = ci[m2], c2 = ci[m2 + d.L2];
+    double c1, c3;
+    if (res == 0) {
+      c1 = m2 ? ci[J - m2] : 0.0;
+      c3 = ci[d.L2 - m2];
+    } else {
+      const double* cm = chat + (unsigned long long)d.mirror[i] * J;
+      c1 = cm[J - 1 - m2];
+      c3 = cm[d.L2 - 1 - m2];
+    }
+    if (nonfinite && t0 == 0) {
+      if (!isfinite(c0) || !isfinite(c2)) atomicOr(nonfinite, 1);
+    }
+    const unsigned long long P = d.L;
+    double sa, ca, sb, cb, s4, c4;
+    sincospi((double)m / (2.0 * nd), &sa, &ca);
+    sincospi((double)(m + P) / (2.0 * nd), &sb, &cb);
+    sincospi(2.0 * (double)m / nd, &s4, &c4);
+    // T_l of the four stage indices by the recurrence (cheb_t's operations)
+    const double x0 = (double)m / nd, x1 = (double)(d.n - m) / nd, x2 = (double)(m + P) / nd,
+                 x3 = (double)(P - m) / nd;
+    double a0 = 1.0, a1 = 1.0, a2 = 1.0, a3 = 1.0;  // T_{l-1}
+    double b0 = x0, b1 = x1, b2 = x2, b3 = x3;      // T_l
+    double r0 = 1.0, r1 = 1.0, r2 = 1.0, r3 = 1.0;  // T at the current term
+    for (int l = 0; l < t0 + nt; ++l) {
+      if (bt.cheb) {
+        if (l == 0) {
+          r0 = r1 = r2 = r3 = 1.0;
+        } else if (l == 1) {
+          r0 = x0; r1 = x1; r2 = x2; r3 = x3;
+        } else {
+          const double n0 = 2.0 * x0 * b0 - a0, n1 = 2.0 * x1 * b1 - a1, n2 = 2.0 * x2 * b2 - a2,
+                       n3 = 2.0 * x3 * b3 - a3;
+          a0 = b0; a1 = b1; a2 = b2; a3 = b3;
+          b0 = n0; b1 = n1; b2 = n2; b3 = n3;
+          r0 = b0; r1 = b1; r2 = b2; r3 = b3;
+        }
+      } else {
+        r0 = big_row(bt, l, x0); r1 = big_row(bt, l, x1); r2 = big_row(bt, l, x2); r3 = big_row(bt, l, x3);
+      }
+      if (l < t0) continue;
+      const int tz = l - t0;
+      const int odd = big_odd(bt, l);
+      const double st0 = c0 * r0, st1 = m ? c1 * r1 : 0.0, st2 = c2 * r2, st3 = c3 * r3;
+      const double xa = odd ? (m ? 0.5 * st1 : 0.0) : (m ? 0.5 * st0 : st0);
+      const double xan = m ? 0.5 * (odd ? st0 : st1) : 0.0;
+      const double xb = 0.5 * (odd ? st3 : st2), xbn = 0.5 * (odd ? st2 : st3);
+      const double2 Wa = make_double2(ca * xa + sa * xan, sa * xa - ca * xan);
+      const double2 Wb = make_double2(cb * xb + sb * xbn, sb * xb - cb * xbn);
+      const double2 sm = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
+      const double2 df = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
+      const double2 dr = make_double2(df.x * c4 - df.y * s4, df.x * s4 + df.y * c4);
+      Z[((unsigned long long)tz * d.nres_me + i) * d.L2 + m2] = make_double2(sm.x - dr.y, sm.y + dr.x);
+    }
+  }
+}
+
+// rows [t][i][k2] (after the L2-point inverse FFTs) times e^{+2 pi i res_i k2/L},
+// into the exchange buffer [dest][t][i][k2l] (dest = k2 / KB)
+__global__ void fs_fwd_twiddle_kernel(FsDev d, const double2* __restrict__ Z, int nt,
+                                      double2* __restrict__ send) {
+  const unsigned long long total = (unsigned long long)nt * d.nres_me * d.L2;
+  const int* res_me = d.res_all + (size_t)d.rank * d.res_max;
+  const unsigned long long chunk = (unsigned long long)nt * d.nres_me * d.KB;
+  for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
+       e += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long row = e >> d.log2L2, k2 = e & (d.L2 - 1);
+    const unsigned long long i = row % (unsigned long long)d.nres_me;
+    const unsigned long long ph = (unsigned long long)res_me[i] * k2;  // < L
+    double s, c;
+    sincospi(2.0 * (double)ph / (double)d.L, &s, &c);
+    const double2 v = cmul(Z[e], make_double2(c, s));
+    send[(k2 >> d.log2KB) * chunk + row * d.KB + (k2 & (d.KB - 1))] = v;
+  }
+}
+
+// exchange buffer (from every source s: [t][i_s][k2l]) -> rows [t][k2l][m1]
+__global__ void fs_fwd_gather_kernel(FsDev d, const double2* __restrict__ recv, int nt,
+                                     double2* __restrict__ rows) {
+  __shared__ double2 tile[kFsTile][kFsTile + 1];
+  const int t = blockIdx.z;
+  const unsigned long long m10 = (unsigned long long)blockIdx.x * kFsTile;
+  const unsigned long long k0 = (unsigned long long)blockIdx.y * kFsTile;
+  for (int mm = threadIdx.y; mm < kFsTile; mm += kFsRows) {
+    const unsigned long long m1 = m10 + mm, k2l = k0 + threadIdx.x;
+    double2 v = make_double2(0.0, 0.0);
+    if (m1 < d.L1 && k2l < d.KB) {
+      const int s = d.owner[m1];
+      v = recv[(unsigned long long)d.cum[s] * d.KB * nt +
+               ((unsigned long long)t * d.nres[s] + d.lidx[m1]) * d.KB + k2l];
+    }
+    tile[mm][threadIdx.x] = v;
+  }
+  __syncthreads();
+  for (int kk = threadIdx.y; kk < kFsTile; kk += kFsRows) {
+    const unsigned long long m1 = m10 + threadIdx.x, k2l = k0 + kk;
+    if (m1 < d.L1 && k2l < d.KB)
+      rows[((unsigned long long)t * d.KB + k2l) * d.L1 + m1] = tile[threadIdx.x][kk];
+  }
+}
+
+// rows [t][k2l][k1] (after the L1-point inverse FFTs) -> the weighted sum over
+// the group's terms at the two outputs of each slot pair, into the value
+// exchange layout [dest block][g][u][k2l][b]
+__global__ void fs_fwd_unpack_kernel(FsDev d, const double2* __restrict__ rows, int t0, int nt,
+                                     BigTerms bt, const double* __restrict__ delta,
+                                     double* __restrict__ fx, int first) {
+  __shared__ double2 tile[kFsTile][kFsTile + 1];
+  constexpr int IT = kFsTile / kFsRows;
+  const unsigned long long k10 = (unsigned long long)blockIdx.x * kFsTile;
+  const unsigned long long k20 = (unsigned long long)blockIdx.y * kFsTile;
+  // this thread's items: k2l = k20 + threadIdx.x, k1 = k10 + threadIdx.y + 8 it
+  const unsigned long long k2l = k20 + threadIdx.x;
+  unsigned long long kk[IT][2];
+  double y0[IT][2], acc[IT][2];
+  bool ok[IT];
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const unsigned long long k1 = k10 + threadIdx.y + kFsRows * it;
+    ok[it] = k1 < d.L1 && k2l < d.KB;
+    const unsigned long long p = (unsigned long long)d.rank * d.KB + k2l + d.L2 * k1;
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      kk[it][b] = ok[it] ? fs_k_of_q(d, 2 * p + b) : 0;
+      y0[it][b] = (ok[it] && !bt.plain) ? (double)d.n * delta[kk[it][b]] : 0.0;
+      acc[it][b] = 0.0;
+    }
+  }
+  for (int t = 0; t < nt; ++t) {
+    __syncthreads();
+    for (int ii = threadIdx.y; ii < kFsTile; ii += kFsRows) {  // read along k1
+      const unsigned long long r = k20 + ii, k1 = k10 + threadIdx.x;
+      tile[ii][threadIdx.x] = (r < d.KB && k1 < d.L1)
+                                  ? rows[((unsigned long long)t * d.KB + r) * d.L1 + k1]
+                                  : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    const int l = t0 + t;
+    const int odd = big_odd(bt, l);
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      if (!ok[it]) continue;
+      const double2 z = tile[threadIdx.x][threadIdx.y + kFsRows * it];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        double y = b ? z.y : z.x;
+        if (odd && (kk[it][b] & 1)) y = -y;
+        const double w = bt.plain ? 1.0 : bt.cheb ? fs_weight(l, y0[it][b], bt.swap)
+                                                  : big_weight(bt, l, y0[it][b]);
+        acc[it][b] += w * y;
+      }
+    }
+  }
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    if (!ok[it]) continue;
+    const unsigned long long k1 = k10 + threadIdx.y + kFsRows * it;
+    const unsigned long long k = kk[it][0];
+    const unsigned long long blk = k / d.B;
+    const int g = (int)(k & 1);
+    double2* o = reinterpret_cast<double2*>(fx + fs_xpos(d, blk, blk, g, k1, k2l));
+    const double2 v = make_double2(acc[it][0], acc[it][1]);
+    if (first) {
+      *o = v;
+    } else {
+      const double2 old = *o;
+      *o = make_double2(old.x + v.x, old.y + v.y);
+    }
+  }
+}
+
+// value exchange layout <-> this rank's natural block (rank = the block owner;
+// chunk s holds the slots of source / destination s's k2 block)
+template <bool TO_BLOCK>
+__global__ void fs_values_kernel(FsDev d, const double* __restrict__ src, double* __restrict__ dst) {
+  const unsigned long long per = d.B / d.world;
+  for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < d.B;
+       e += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long s = e / per, rem = e - s * per;
+    const int b = (int)(rem & 1);
+    const unsigned long long r2 = rem >> 1;
+    const unsigned long long k2l = r2 & (d.KB - 1), r3 = r2 >> d.log2KB;
+    const unsigned long long u = r3 % d.U;
+    const int g = (int)(r3 / d.U);
+    const unsigned long long p = s * d.KB + k2l + d.L2 * (fs_p0(d, d.rank, g) / d.L2 + u);
+    const unsigned long long k = fs_k_of_q(d, 2 * p + b) - (unsigned long long)d.rank * d.B;
+    if (TO_BLOCK)
+      dst[k] = src[e];
+    else
+      dst[e] = src[k];
+  }
+}
+
+// transposed pack: h_t(k) = w_t(k) mult_k g_k (odd terms: odd k negated) at the
+// slot pairs of this rank's k2 block, rows [t][k2l][k1] (read along k2l from
+// the value exchange layout, written along k1)
+__global__ void fs_tr_pack_kernel(FsDev d, const double* __restrict__ gx, const double* __restrict__ mult,
+                                  int t0, int nt, BigTerms bt, const double* __restrict__ delta,
+                                  double2* __restrict__ rows, int* nonfinite) {
+  __shared__ double2 tile[kFsTile][kFsTile + 1];
+  constexpr int IT = kFsTile / kFsRows;
+  const unsigned long long k10 = (unsigned long long)blockIdx.x * kFsTile;
+  const unsigned long long k20 = (unsigned long long)blockIdx.y * kFsTile;
+  const unsigned long long k2l = k20 + threadIdx.x;
+  unsigned long long kk[IT][2];
+  double y0[IT][2], gv[IT][2];
+  bool ok[IT];
+#pragma unroll
+  for (int it = 0; it < IT; ++it) {
+    const unsigned long long k1 = k10 + threadIdx.y + kFsRows * it;
+    ok[it] = k1 < d.L1 && k2l < d.KB;
+    const unsigned long long p = (unsigned long long)d.rank * d.KB + k2l + d.L2 * k1;
+    kk[it][0] = ok[it] ? fs_k_of_q(d, 2 * p) : 0;
+    kk[it][1] = ok[it] ? fs_k_of_q(d, 2 * p + 1) : 0;
+    double2 pair = make_double2(0.0, 0.0);
+    if (ok[it]) {
+      const unsigned long long blk = kk[it][0] / d.B;
+      pair = *reinterpret_cast<const double2*>(gx + fs_xpos(d, blk, blk, (int)(kk[it][0] & 1), k1, k2l));
+    }
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      double v = b ? pair.y : pair.x;
+      if (ok[it] && mult) v *= mult[kk[it][b]];
+      gv[it][b] = v;
+      y0[it][b] = (ok[it] && !bt.plain) ? (double)d.n * delta[kk[it][b]] : 0.0;
+      if (nonfinite && t0 == 0 && ok[it] && !isfinite(v)) atomicOr(nonfinite, 1);
+    }
+  }
+  for (int t = 0; t < nt; ++t) {
+    const int l = t0 + t;
+    const int odd = big_odd(bt, l);
+#pragma unroll
+    for (int it = 0; it < IT; ++it) {
+      double h[2];
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const double w = bt.plain ? 1.0 : bt.cheb ? fs_weight(l, y0[it][b], bt.swap)
+                                                  : big_weight(bt, l, y0[it][b]);
+        double v = w * gv[it][b];
+        if (odd && (kk[it][b] & 1)) v = -v;
+        h[b] = v;
+      }
+      tile[threadIdx.x][threadIdx.y + kFsRows * it] = make_double2(h[0], h[1]);
+    }
+    __syncthreads();
+    for (int ii = threadIdx.y; ii < kFsTile; ii += kFsRows) {  // write along k1
+      const unsigned long long r = k20 + ii, k1 = k10 + threadIdx.x;
+      if (r < d.KB && k1 < d.L1) rows[((unsigned long long)t * d.KB + r) * d.L1 + k1] = tile[ii][threadIdx.x];
+    }
+    __syncthreads();
+  }
+}
+
+// rows [t][k2l][m1] (after the L1-point forward FFTs) times e^{-2 pi i m1 k2/L}
+// into the exchange buffer (to the owner dest of m1: [t][i_dest][k2l])
+__global__ void fs_tr_twiddle_kernel(FsDev d, const double2* __restrict__ rows, int nt,
+                                     double2* __restrict__ send) {
+  __shared__ double2 tile[kFsTile][kFsTile + 1];
+  const int t = blockIdx.z;
+  const unsigned long long m10 = (unsigned long long)blockIdx.x * kFsTile;
+  const unsigned long long k0 = (unsigned long long)blockIdx.y * kFsTile;
+  for (int kk = threadIdx.y; kk < kFsTile; kk += kFsRows) {  // read along m1
+    const unsigned long long m1 = m10 + threadIdx.x, k2l = k0 + kk;
+    double2 v = make_double2(0.0, 0.0);
+    if (m1 < d.L1 && k2l < d.KB) {
+      const unsigned long long k2 = (unsigned long long)d.rank * d.KB + k2l;
+      double s, c;
+      sincospi(-2.0 * (double)(m1 * k2) / (double)d.L, &s, &c);
+      v = cmul(rows[((unsigned long long)t * d.KB + k2l) * d.L1 + m1], make_double2(c, s));
+    }
+    tile[threadIdx.x][kk] = v;
+  }
+  __syncthreads();
+  for (int mm = threadIdx.y; mm < kFsTile; mm += kFsRows) {  // write along k2l
+    const unsigned long long m1 = m10 + mm, k2l = k0 + threadIdx.x;
+    if (m1 < d.L1 && k2l < d.KB) {
+      const int dst = d.owner[m1];
+      send[(unsigned long long)d.cum[dst] * d.KB * nt +
+           ((unsigned long long)t * d.nres[dst] + d.lidx[m1]) * d.KB + k2l] = tile[mm][threadIdx.x];
+    }
+  }
+}
+
+// transposed unpack (big_tr_unpack_kernel's rows e = 0, 1): outputs r = a and
+// r = L + a of a = res_i + L1 m2 from the packed entries a and L - a
+__global__ void fs_tr_unpack_kernel(FsDev d, const double2* __restrict__ Z, int t0, int nt,
+                                    BigTerms bt, double* __restrict__ chat, int first) {
+  const unsigned long long J = 2 * d.L2;
+  const unsigned long long total = (unsigned long long)d.nres_me * d.L2;
+  const int* res_me = d.res_all + (size_t)d.rank * d.res_max;
+  const double nd = (double)d.n;
+  for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
+       e += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long i = e >> d.log2L2, m2 = e & (d.L2 - 1);
+    const unsigned long long res = (unsigned long long)res_me[i];
+    const unsigned long long a = res + d.L1 * m2;
+    unsigned long long ib, mb;
+    if (res == 0) {
+      ib = i;
+      mb = (d.L2 - m2) & (d.L2 - 1);
+    } else {
+      ib = (unsigned long long)d.mirror[i];
+      mb = d.L2 - 1 - m2;
+    }
+    const unsigned long long r[2] = {a, d.L + a};
+    double c2[2], s2[2], ch[2], sh[2], acc[2] = {0.0, 0.0};
+    double xr[2], ta[2], tb[2], tv[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+      sincospi(-2.0 * (double)r[q] / nd, &s2[q], &c2[q]);
+      sincospi((double)r[q] / (2.0 * nd), &sh[q], &ch[q]);
+      xr[q] = (double)r[q] / nd;
+      ta[q] = 1.0;
+      tb[q] = xr[q];
+    }
+    for (int l = 0; l < t0 + nt; ++l) {
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        if (bt.cheb) {
+          if (l == 0) {
+            tv[q] = 1.0;
+          } else if (l == 1) {
+            tv[q] = xr[q];
+          } else {
+            const double nx = 2.0 * xr[q] * tb[q] - ta[q];
+            ta[q] = tb[q];
+            tb[q] = nx;
+            tv[q] = nx;
+          }
+        } else {
+          tv[q] = big_row(bt, l, xr[q]);
+        }
+      }
+      if (l < t0) continue;
+      const int tz = l - t0;
+      const int odd = big_odd(bt, l);
+      const double2 za = Z[((unsigned long long)tz * d.nres_me + i) * d.L2 + m2];
+      const double2 zb = Z[((unsigned long long)tz * d.nres_me + ib) * d.L2 + mb];
+      const double2 p0 = odd ? zb : za, p1 = odd ? za : zb;
+#pragma unroll
+      for (int q = 0; q < 2; ++q) {
+        double x;
+        if (!odd)
+          x = big_tr_value(p0, p1, c2[q], s2[q], ch[q], sh[q]);
+        else
+          x = r[q] == 0 ? 0.0 : big_tr_value(p0, p1, c2[q], -s2[q], sh[q], ch[q]);
+        acc[q] = __fma_rn(tv[q], x, acc[q]);
+      }
+    }
+    double* o0 = chat + i * J + m2;
+    double* o1 = chat + i * J + m2 + d.L2;
+    *o0 = first ? acc[0] : *o0 + acc[0];
+    *o1 = first ? acc[1] : *o1 + acc[1];
+  }
+}
+
+unsigned fs_grid(unsigned long long total) {
+  return (unsigned)std::min<unsigned long long>((total + 255) / 256, 8ull * sm_count() * 8);
+}
+
+BigTerms fs_terms(const FastNdct& p) {
+  const bool cheb = p.bes_terms > 0;
+  return BigTerms{0, 0, cheb ? 1 : 0, cheb ? p.swap : 0};
+}
+
+void fs_check_terms(const FastNdct& p, const FsLayout& f, int t0, int t1) {
+  if (p.n != f.n) fail(FL_INVALID_ARGUMENT, "four-step: layout and plan sizes differ");
+  const int m = fast_ndct_terms(p);
+  if (t0 < 0 || t1 > m || t0 >= t1) fail(FL_INVALID_ARGUMENT, "four-step: term range out of bounds");
+}
+
+}  // namespace
+
+FsLayout* fs_create(size_t n, int world, int rank) {
+  const int log2n = log2_exact(n);
+  if (log2n < 0 || world < 1 || rank < 0 || rank >= world || (world & (world - 1)))
+    fail(FL_INVALID_ARGUMENT, "four-step: N and the world size must be powers of two");
+  const int log2L = log2n - 1;
+  const int log2L1 = log2L / 2, log2L2 = log2L - log2L1;
+  if (log2L2 > kMaxSmemLog2) fail(FL_INVALID_ARGUMENT, "four-step: N above 2^27");
+  const size_t L1 = size_t(1) << log2L1, L2 = size_t(1) << log2L2;
+  if (L1 < 2 * (size_t)world || L2 < (size_t)world)
+    fail(FL_INVALID_ARGUMENT, "four-step: N too small for this world size (needs 2P <= L1)");
+  auto* f = new FsLayout;
+  f->n = n;
+  f->L = n / 2;
+  f->L1 = L1;
+  f->L2 = L2;
+  f->KB = L2 / world;
+  f->B = n / world;
+  f->U = L1 / (2 * world);
+  f->log2n = log2n;
+  f->log2L1 = log2L1;
+  f->log2L2 = log2L2;
+  f->log2KB = log2L2 - log2_exact((size_t)world);
+  f->world = world;
+  f->rank = rank;
+  FLB_CUDA(cudaGetDevice(&f->device));
+  // symmetric residue sets
+  const size_t h = L1 / (2 * world);
+  std::vector<std::vector<int>> res(world);
+  for (int r = 0; r < world; ++r) {
+    for (size_t j = r * h; j < (r + 1) * h; ++j) res[r].push_back((int)j);
+    for (size_t j = r * h; j < (r + 1) * h; ++j)
+      if (j != 0) res[r].push_back((int)(L1 - j));
+    if (r == world - 1) res[r].push_back((int)(L1 / 2));
+  }
+  f->nres.resize(world);
+  f->cum.assign(world + 1, 0);
+  std::vector<int> owner(L1, -1), lidx(L1, -1);
+  for (int r = 0; r < world; ++r) {
+    f->nres[r] = (int)res[r].size();
+    f->cum[r + 1] = f->cum[r] + f->nres[r];
+    f->res_max = std::max(f->res_max, res[r].size());
+    for (size_t i = 0; i < res[r].size(); ++i) {
+      owner[res[r][i]] = r;
+      lidx[res[r][i]] = (int)i;
+    }
+  }
+  std::vector<int> all((size_t)world * f->res_max, -1);
+  for (int r = 0; r < world; ++r)
+    std::copy(res[r].begin(), res[r].end(), all.begin() + (size_t)r * f->res_max);
+  std::vector<int> mirror(res[rank].size());
+  for (size_t i = 0; i < res[rank].size(); ++i) mirror[i] = lidx[(L1 - res[rank][i]) % L1];
+  auto up = [](const std::vector<int>& v, int** dst) {
+    FLB_CUDA(cudaMalloc(dst, std::max<size_t>(1, v.size()) * sizeof(int)));
+    FLB_CUDA(cudaMemcpy(*dst, v.data(), v.size() * sizeof(int), cudaMemcpyHostToDevice));
+  };
+  try {
+    up(all, &f->d_res_all);
+    up(mirror, &f->d_mirror);
+    up(owner, &f->d_owner);
+    up(lidx, &f->d_lidx);
+    up(f->cum, &f->d_cum);
+    up(f->nres, &f->d_nres);
+  } catch (...) {
+    fs_destroy(f);
+    throw;
+  }
+  return f;
+}
+
+void fs_destroy(FsLayout* f) {
+  if (!f) return;
+  for (int* q : {f->d_res_all, f->d_mirror, f->d_owner, f->d_lidx, f->d_cum, f->d_nres})
+    if (q) cudaFree(q);
+  delete f;
+}
+
+FsInfo fs_info(const FsLayout& f) {
+  return FsInfo{f.n, f.L, f.L1, f.L2, f.KB, f.B, (size_t)f.nres[f.rank], f.res_max, f.world, f.rank};
+}
+
+size_t fs_coef_count(const FsLayout& f, int transpose, int peer, int send) {
+  if (peer < 0 || peer >= f.world) fail(FL_INVALID_ARGUMENT, "four-step: peer out of range");
+  // forward: sender's residues; transpose: receiver's residues
+  const bool mine = transpose ? !send : send;
+  return (size_t)(mine ? f.nres[f.rank] : f.nres[peer]) * f.KB;
+}
+
+void fs_to_residue(const FsLayout& f, const double* full, double* send, cudaStream_t s) {
+  const FsDev d = fs_dev(f);
+  const dim3 grid((unsigned)((2 * f.L2 + kFsTile - 1) / kFsTile),
+                  (unsigned)((f.res_max + kFsTile - 1) / kFsTile), (unsigned)f.world);
+  fs_residue_kernel<true><<<grid, dim3(kFsTile, kFsRows), 0, s>>>(d, full, send);
+  note_launch("fs_residue_kernel");
+}
+
+void fs_from_residue(const FsLayout& f, const double* gathered, double* full, cudaStream_t s) {
+  const FsDev d = fs_dev(f);
+  const dim3 grid((unsigned)((2 * f.L2 + kFsTile - 1) / kFsTile),
+                  (unsigned)((f.res_max + kFsTile - 1) / kFsTile), (unsigned)f.world);
+  fs_residue_kernel<false><<<grid, dim3(kFsTile, kFsRows), 0, s>>>(d, gathered, full);
+  note_launch("fs_residue_kernel");
+}
+
+void fs_fwd1(const FsLayout& f, const FastNdct& p, int t0, int t1, const double* chat,
+             double2* send, double2* work, int* nonfinite, cudaStream_t s) {
+  fs_check_terms(p, f, t0, t1);
+  const FsDev d = fs_dev(f);
+  const int nt = t1 - t0;
+  ensure_recip();
+  const unsigned long long items = (unsigned long long)d.nres_me * f.L2;
+  fs_fwd_pack_kernel<<<fs_grid(items), 256, 0, s>>>(d, chat, t0, nt, fs_terms(p), work, nonfinite);
+  note_launch("fs_fwd_pack_kernel");
+  fft_pow2(work, nullptr, f.log2L2, (size_t)nt * d.nres_me, true, s);
+  fs_fwd_twiddle_kernel<<<fs_grid(items * nt), 256, 0, s>>>(d, work, nt, send);
+  note_launch("fs_fwd_twiddle_kernel");
+}
+
+void fs_fwd2(const FsLayout& f, const FastNdct& p, int t0, int t1, const double2* recv,
+             double2* work, double* fx, int first, cudaStream_t s) {
+  fs_check_terms(p, f, t0, t1);
+  const FsDev d = fs_dev(f);
+  const int nt = t1 - t0;
+  ensure_recip();
+  const dim3 tb(kFsTile, kFsRows);
+  const unsigned gx = (unsigned)((f.L1 + kFsTile - 1) / kFsTile), gy = (unsigned)((f.KB + kFsTile - 1) / kFsTile);
+  fs_fwd_gather_kernel<<<dim3(gx, gy, (unsigned)nt), tb, 0, s>>>(d, recv, nt, work);
+  note_launch("fs_fwd_gather_kernel");
+  fft_pow2(work, nullptr, f.log2L1, (size_t)nt * f.KB, true, s);
+  fs_fwd_unpack_kernel<<<dim3(gx, gy), tb, 0, s>>>(d, work, t0, nt, fs_terms(p), p.delta, fx, first);
+  note_launch("fs_fwd_unpack_kernel");
+}
+
+void fs_values_from_exchange(const FsLayout& f, const double* fx, double* block, cudaStream_t s) {
+  fs_values_kernel<true><<<fs_grid(f.B), 256, 0, s>>>(fs_dev(f), fx, block);
+  note_launch("fs_values_kernel");
+}
+
+void fs_values_to_exchange(const FsLayout& f, const double* block, double* fx, cudaStream_t s) {
+  fs_values_kernel<false><<<fs_grid(f.B), 256, 0, s>>>(fs_dev(f), block, fx);
+  note_launch("fs_values_kernel");
+}
+
+void fs_tr1(const FsLayout& f, const FastNdct& p, const double* mult, int t0, int t1,
+            const double* gx, double2* send, double2* work, int* nonfinite, cudaStream_t s) {
+  fs_check_terms(p, f, t0, t1);
+  const FsDev d = fs_dev(f);
+  const int nt = t1 - t0;
+  ensure_recip();
+  const dim3 tb(kFsTile, kFsRows);
+  const unsigned gx1 = (unsigned)((f.L1 + kFsTile - 1) / kFsTile), gy = (unsigned)((f.KB + kFsTile - 1) / kFsTile);
+  fs_tr_pack_kernel<<<dim3(gx1, gy), tb, 0, s>>>(d, gx, mult, t0, nt, fs_terms(p), p.delta, work,
+                                                 nonfinite);
+  note_launch("fs_tr_pack_kernel");
+  fft_pow2(work, nullptr, f.log2L1, (size_t)nt * f.KB, false, s);
+  fs_tr_twiddle_kernel<<<dim3(gx1, gy, (unsigned)nt), tb, 0, s>>>(d, work, nt, send);
+  note_launch("fs_tr_twiddle_kernel");
+}
+
+void fs_tr2(const FsLayout& f, const FastNdct& p, int t0, int t1, const double2* recv,
+            double2* work, double* chat, int first, cudaStream_t s) {
+  fs_check_terms(p, f, t0, t1);
+  const FsDev d = fs_dev(f);
+  const int nt = t1 - t0;
+  // [src][t][i][k2l] -> rows [t][i][k2 = src KB + k2l]
+  const size_t chunk = (size_t)nt * d.nres_me * f.KB;
+  for (int src = 0; src < f.world; ++src)
+    FLB_CUDA(cudaMemcpy2DAsync(work + (size_t)src * f.KB, f.L2 * sizeof(double2), recv + src * chunk,
+                               f.KB * sizeof(double2), f.KB * sizeof(double2), (size_t)nt * d.nres_me,
+                               cudaMemcpyDeviceToDevice, s));
+  fft_pow2(work, nullptr, f.log2L2, (size_t)nt * d.nres_me, false, s);
+  const unsigned long long items = (unsigned long long)d.nres_me * f.L2;
+  fs_tr_unpack_kernel<<<fs_grid(items), 256, 0, s>>>(d, work, t0, nt, fs_terms(p), chat, first);
+  note_launch("fs_tr_unpack_kernel");
+}
+
 }  // namespace flb

@@ -157,3 +157,233 @@ def idlt(cfg, f, dist=None, scatter: bool = False):
     counts, costs = _plan_split(cfg)
     return transform(f, True, dist, counts=counts, scatter=scatter, costs=costs,
                      stage_fn=lambda inv, st, lo, hi, a, b: gpu_stage(cfg, inv, st, lo, hi, a, b))
+
+
+# ---------------------------------------------------------------------------
+# Distributed four-step NDCT (the sharded form of C5 north_star names): the
+# input and output of the NDCT stage are spread over the ranks and each
+# term's N/2-point FFT is a four-step whose two FFT stages are separated by
+# ONE NCCL all-to-all per group of terms (include/fastleg_b200.h, fl_fs_*).
+# The conversion stays term-parallel (its partials are full-length), but its
+# all-reduce becomes a reduce-scatter straight into the four-step's residue
+# layout, and the result leaves through a uniform all-to-all into natural
+# blocks of N/P:
+#
+#   dlt :  c (block) -all_gather-> c -> partial M c (term slice) -reduce_scatter->
+#          chat (residue layout) -> [pack, L2-FFTs, twiddle] -all_to_all->
+#          [L1-FFTs, weighted unpack] -all_to_all-> f (block)
+#   idlt:  f (block) -all_to_all-> [weighted pack, L1-FFTs, twiddle] -all_to_all->
+#          [L2-FFTs, unpack] -> g (residue layout) -all_gather-> g -> partial
+#          M^T g (term slice) -reduce_scatter-> c (block)
+#
+# The all-to-all of term group j runs on NCCL's stream while part 1 of group
+# j + 1 runs on the compute stream.
+# ---------------------------------------------------------------------------
+class FourStep:
+    """Rank-local half of the distributed four-step NDCT (fl_fs_*)."""
+
+    def __init__(self, cfg, world: int, rank: int):
+        import torch
+        self.cfg = cfg
+        h = C.c_void_p()
+        _lib.check(_lib.LIB.fl_fs_create(cfg.handle, int(world), int(rank), C.byref(h)))
+        self.handle = h
+        info = (C.c_size_t * 10)()
+        _lib.check(_lib.LIB.fl_fs_info(h, info))
+        (self.n, self.L, self.L1, self.L2, self.KB, self.B, self.nres, self.res_max,
+         self.world, self.rank) = (int(v) for v in info)
+        self.slab = self.res_max * 2 * self.L2    # doubles per rank of the residue slabs
+        self.res_len = self.nres * 2 * self.L2    # valid doubles of this rank's slab
+        self.terms = stage_terms(cfg, STAGE_NDCT)
+        self._torch = torch
+
+    def __del__(self):
+        if getattr(self, "handle", None):
+            _lib.LIB.fl_fs_destroy(self.handle)
+            self.handle = None
+
+    def _s(self, dev):
+        return C.c_void_p(self._torch.cuda.current_stream(dev).cuda_stream)
+
+    def coef_counts(self, transpose: bool, send: bool) -> list[int]:
+        """Complex entries per term exchanged with each peer (part 1 -> part 2)."""
+        out = []
+        v = C.c_size_t(0)
+        for peer in range(self.world):
+            _lib.check(_lib.LIB.fl_fs_coef_count(self.handle, int(transpose), peer, int(send), C.byref(v)))
+            out.append(int(v.value))
+        return out
+
+    def work_elems(self, terms: int) -> int:
+        return int(_lib.LIB.fl_fs_work_elems(self.handle, int(terms)))
+
+    def groups(self, budget_bytes: int = 12 << 30, min_groups: int = 1) -> list[tuple[int, int]]:
+        """Term groups: work + two send + two receive buffers per group within
+        the budget (two groups in flight)."""
+        per_term = 16 * self.work_elems(1) * 5
+        g = max(min_groups, -(-self.terms * per_term // max(1, budget_bytes)))
+        g = min(g, self.terms)
+        size = -(-self.terms // g)
+        return [(t, min(t + size, self.terms)) for t in range(0, self.terms, size)]
+
+    def to_residue(self, full):
+        slabs = self._torch.empty(self.world * self.slab, dtype=full.dtype, device=full.device)
+        _lib.check(_lib.LIB.fl_fs_to_residue(self.handle, C.c_void_p(full.data_ptr()),
+                                             C.c_void_p(slabs.data_ptr()), self._s(full.device)))
+        return slabs
+
+    def from_residue(self, slabs):
+        full = self._torch.empty(self.n, dtype=slabs.dtype, device=slabs.device)
+        _lib.check(_lib.LIB.fl_fs_from_residue(self.handle, C.c_void_p(slabs.data_ptr()),
+                                               C.c_void_p(full.data_ptr()), self._s(slabs.device)))
+        return full
+
+    def values(self, to_block: bool, x):
+        out = self._torch.empty(self.B, dtype=x.dtype, device=x.device)
+        _lib.check(_lib.LIB.fl_fs_values(self.handle, int(to_block), C.c_void_p(x.data_ptr()),
+                                         C.c_void_p(out.data_ptr()), self._s(x.device)))
+        return out
+
+    def part(self, transpose: bool, part: int, t0: int, t1: int, inp, out, work, first: bool = True):
+        _lib.check(_lib.LIB.fl_fs_ndct_part(self.handle, int(transpose), int(part), int(t0), int(t1),
+                                            C.c_void_p(inp.data_ptr()), C.c_void_p(out.data_ptr()),
+                                            C.c_void_p(work.data_ptr()), int(first), self._s(inp.device)))
+
+    def check(self, transpose: bool, dev) -> None:
+        _lib.check(_lib.LIB.fl_fs_check(self.handle, int(transpose), self._s(dev)))
+
+
+class TorchComm:
+    """The collectives of the four-step path over a torch.distributed group
+    (NCCL on GPUs); world 1 without a group is the identity."""
+
+    def __init__(self, dist=None):
+        self.dist = dist if dist is not None and dist.is_initialized() else None
+        self.world = self.dist.get_world_size() if self.dist else 1
+        self.rank = self.dist.get_rank() if self.dist else 0
+
+    def all_gather(self, x):
+        if self.world == 1:
+            return x
+        import torch
+        out = torch.empty(x.numel() * self.world, dtype=x.dtype, device=x.device)
+        self.dist.all_gather_into_tensor(out, x)
+        return out
+
+    def reduce_scatter(self, x):
+        if self.world == 1:
+            return x
+        import torch
+        out = torch.empty(x.numel() // self.world, dtype=x.dtype, device=x.device)
+        self.dist.reduce_scatter_tensor(out, x, op=self.dist.ReduceOp.SUM)
+        return out
+
+    def all_to_all(self, out, x, out_splits=None, in_splits=None):
+        """Returns a handle with .wait() (async where the backend allows)."""
+        if self.world == 1:
+            if out.data_ptr() != x.data_ptr():
+                out.copy_(x)
+            return _Done()
+        return self.dist.all_to_all_single(out, x, out_splits, in_splits, async_op=True)
+
+
+class _Done:
+    def wait(self):
+        return None
+
+
+def _pipeline(fs: FourStep, comm, transpose: bool, groups, inp, out):
+    """Part 1 of every term group, its all-to-all, part 2: the all-to-all of
+    group j runs on NCCL's stream while part 1 of group j + 1 runs on the
+    compute stream (double-buffered); at world 1 the exchange is the
+    identity and part 2 follows part 1 in place."""
+    import torch
+    dev = inp.device
+    tmax = max(t1 - t0 for t0, t1 in groups)
+    work = torch.empty(2 * fs.work_elems(tmax), dtype=torch.float64, device=dev)
+    s_cnt, r_cnt = fs.coef_counts(transpose, True), fs.coef_counts(transpose, False)
+    multi = comm.world > 1
+    bufs = [(torch.empty(2 * tmax * sum(s_cnt), dtype=torch.float64, device=dev),
+             torch.empty(2 * tmax * sum(r_cnt) if multi else 0, dtype=torch.float64, device=dev))
+            for _ in range(2 if multi else 1)]
+    first = groups[0][0]
+    pending = None
+    for gi, (t0, t1) in enumerate(groups):
+        nt = t1 - t0
+        send, recv = bufs[gi % len(bufs)]
+        send = send[:2 * nt * sum(s_cnt)]
+        fs.part(transpose, 1, t0, t1, inp, send, work)
+        if not multi:
+            fs.part(transpose, 2, t0, t1, send, out, work, first=t0 == first)
+            continue
+        recv = recv[:2 * nt * sum(r_cnt)]
+        h = comm.all_to_all(recv, send, [2 * nt * c for c in r_cnt], [2 * nt * c for c in s_cnt])
+        if pending is not None:
+            ph, prec, p0, p1 = pending
+            ph.wait()
+            fs.part(transpose, 2, p0, p1, prec, out, work, first=p0 == first)
+        pending = (h, recv, t0, t1)
+    if pending is not None:
+        ph, prec, p0, p1 = pending
+        ph.wait()
+        fs.part(transpose, 2, p0, p1, prec, out, work, first=p0 == first)
+    fs.check(transpose, dev)
+
+
+def _ndct_four_step(fs: FourStep, comm, chat_res, groups):
+    """Forward NDCT: residue-layout chat -> this rank's natural block of f."""
+    import torch
+    fx = torch.empty(fs.B, dtype=torch.float64, device=chat_res.device)
+    _pipeline(fs, comm, False, groups, chat_res, fx)
+    frecv = torch.empty_like(fx) if comm.world > 1 else fx
+    comm.all_to_all(frecv, fx).wait()
+    return fs.values(True, frecv)
+
+
+def _ndct_t_four_step(fs: FourStep, comm, f_block, groups):
+    """Transposed NDCT (with the quadrature weights): this rank's natural
+    block of f -> residue-layout result."""
+    import torch
+    gx = fs.values(False, f_block)
+    grecv = torch.empty_like(gx) if comm.world > 1 else gx
+    comm.all_to_all(grecv, gx).wait()
+    out = torch.zeros(fs.slab, dtype=torch.float64, device=f_block.device)
+    _pipeline(fs, comm, True, groups, grecv, out)
+    return out
+
+
+def _conversion_slice(cfg, world: int, rank: int):
+    counts, costs = _plan_split(cfg)
+    if costs[STAGE_LEG2CHEB] is not None:
+        return weighted_slice(costs[STAGE_LEG2CHEB], world, rank)
+    return term_slice(counts[STAGE_LEG2CHEB], world, rank, 2)
+
+
+def dlt_four_step(cfg, c_block, dist=None, fs: FourStep | None = None, groups=None):
+    """DLT of one vector whose coefficients are spread over the ranks in
+    natural blocks of N/P (c_block: this rank's); returns this rank's block of
+    f. The NDCT is the distributed four-step; the conversion term-parallel."""
+    import torch
+    comm = TorchComm(dist)
+    fs = fs or FourStep(cfg, comm.world, comm.rank)
+    groups = groups or fs.groups(min_groups=2 if comm.world > 1 else 1)
+    c = comm.all_gather(c_block)
+    lo, hi = _conversion_slice(cfg, comm.world, comm.rank)
+    part = torch.empty_like(c)
+    gpu_stage(cfg, 0, STAGE_LEG2CHEB, lo, hi, c, part)
+    chat = comm.reduce_scatter(fs.to_residue(part))
+    return _ndct_four_step(fs, comm, chat, groups)
+
+
+def idlt_four_step(cfg, f_block, dist=None, fs: FourStep | None = None, groups=None):
+    """IDLT of one vector whose values are spread over the ranks in natural
+    blocks of N/P; returns this rank's block of the coefficients."""
+    import torch
+    comm = TorchComm(dist)
+    fs = fs or FourStep(cfg, comm.world, comm.rank)
+    groups = groups or fs.groups(min_groups=2 if comm.world > 1 else 1)
+    g = fs.from_residue(comm.all_gather(_ndct_t_four_step(fs, comm, f_block, groups)))
+    lo, hi = _conversion_slice(cfg, comm.world, comm.rank)
+    part = torch.empty_like(g)
+    gpu_stage(cfg, 1, STAGE_LEG2CHEB, lo, hi, g, part)
+    return comm.reduce_scatter(part)
