@@ -2555,6 +2555,12 @@ struct FsLayout {
   int* d_lidx = nullptr;     // [L1]: its index in the owner's list
   int* d_cum = nullptr;      // [world + 1]
   int* d_nres = nullptr;     // [world]
+  // per-rank weight table of the value side, wt[l][k1][k2l][b] = the
+  // Chebyshev-expansion weight of term l at output k(p, b) (built on first
+  // use for one FastNdct: terms x N/P doubles)
+  mutable double* wt = nullptr;
+  mutable const FastNdct* wt_for = nullptr;
+  mutable std::mutex wt_mu;
   const int* res_me() const { return d_res_all + (size_t)rank * res_max; }
 };
 
@@ -2762,7 +2768,7 @@ __global__ void fs_fwd_gather_kernel(FsDev d, const double2* __restrict__ recv, 
 // the group's terms at the two outputs of each slot pair, into the value
 // exchange layout [dest block][g][u][k2l][b]
 __global__ void fs_fwd_unpack_kernel(FsDev d, const double2* __restrict__ rows, int t0, int nt,
-                                     BigTerms bt, const double* __restrict__ delta,
+                                     BigTerms bt, const double2* __restrict__ wt,
                                      double* __restrict__ fx, int first) {
   __shared__ double2 tile[kFsTile][kFsTile + 1];
   constexpr int IT = kFsTile / kFsRows;
@@ -2770,20 +2776,16 @@ __global__ void fs_fwd_unpack_kernel(FsDev d, const double2* __restrict__ rows, 
   const unsigned long long k20 = (unsigned long long)blockIdx.y * kFsTile;
   // this thread's items: k2l = k20 + threadIdx.x, k1 = k10 + threadIdx.y + 8 it
   const unsigned long long k2l = k20 + threadIdx.x;
-  unsigned long long kk[IT][2];
-  double y0[IT][2], acc[IT][2];
+  unsigned long long k0[IT];
+  double acc[IT][2];
   bool ok[IT];
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
     const unsigned long long k1 = k10 + threadIdx.y + kFsRows * it;
     ok[it] = k1 < d.L1 && k2l < d.KB;
     const unsigned long long p = (unsigned long long)d.rank * d.KB + k2l + d.L2 * k1;
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      kk[it][b] = ok[it] ? fs_k_of_q(d, 2 * p + b) : 0;
-      y0[it][b] = (ok[it] && !bt.plain) ? (double)d.n * delta[kk[it][b]] : 0.0;
-      acc[it][b] = 0.0;
-    }
+    k0[it] = ok[it] ? fs_k_of_q(d, 2 * p) : 0;  // both outputs of the pair have k's parity
+    acc[it][0] = acc[it][1] = 0.0;
   }
   for (int t = 0; t < nt; ++t) {
     __syncthreads();
@@ -2799,22 +2801,19 @@ __global__ void fs_fwd_unpack_kernel(FsDev d, const double2* __restrict__ rows, 
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
       if (!ok[it]) continue;
+      const unsigned long long k1 = k10 + threadIdx.y + kFsRows * it;
       const double2 z = tile[threadIdx.x][threadIdx.y + kFsRows * it];
-#pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        double y = b ? z.y : z.x;
-        if (odd && (kk[it][b] & 1)) y = -y;
-        const double w = bt.plain ? 1.0 : bt.cheb ? fs_weight(l, y0[it][b], bt.swap)
-                                                  : big_weight(bt, l, y0[it][b]);
-        acc[it][b] += w * y;
-      }
+      const double2 w = wt[((unsigned long long)l * d.L1 + k1) * d.KB + k2l];
+      const double sg = (odd && (k0[it] & 1)) ? -1.0 : 1.0;
+      acc[it][0] += w.x * (sg * z.x);
+      acc[it][1] += w.y * (sg * z.y);
     }
   }
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
     if (!ok[it]) continue;
     const unsigned long long k1 = k10 + threadIdx.y + kFsRows * it;
-    const unsigned long long k = kk[it][0];
+    const unsigned long long k = k0[it];
     const unsigned long long blk = k / d.B;
     const int g = (int)(k & 1);
     double2* o = reinterpret_cast<double2*>(fx + fs_xpos(d, blk, blk, g, k1, k2l));
@@ -2824,6 +2823,25 @@ __global__ void fs_fwd_unpack_kernel(FsDev d, const double2* __restrict__ rows, 
     } else {
       const double2 old = *o;
       *o = make_double2(old.x + v.x, old.y + v.y);
+    }
+  }
+}
+
+// the value side's weight table (see FsLayout::wt): per slot pair all terms
+// (big_tables_kernel's series)
+__global__ void fs_weights_kernel(FsDev d, const double* __restrict__ delta, int terms, BigTerms bt,
+                                  double2* __restrict__ wt) {
+  const unsigned long long total = d.L1 * d.KB;
+  for (unsigned long long e = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x; e < total;
+       e += (unsigned long long)gridDim.x * blockDim.x) {
+    const unsigned long long k1 = e >> d.log2KB, k2l = e & (d.KB - 1);
+    const unsigned long long p = (unsigned long long)d.rank * d.KB + k2l + d.L2 * k1;
+    const double ya = (double)d.n * delta[fs_k_of_q(d, 2 * p)];
+    const double yb = (double)d.n * delta[fs_k_of_q(d, 2 * p + 1)];
+    for (int l = 0; l < terms; ++l) {
+      const double wa = bt.plain ? 1.0 : bt.cheb ? fs_weight(l, ya, bt.swap) : big_weight(bt, l, ya);
+      const double wb = bt.plain ? 1.0 : bt.cheb ? fs_weight(l, yb, bt.swap) : big_weight(bt, l, yb);
+      wt[(unsigned long long)l * total + e] = make_double2(wa, wb);
     }
   }
 }
@@ -2854,52 +2872,48 @@ __global__ void fs_values_kernel(FsDev d, const double* __restrict__ src, double
 // slot pairs of this rank's k2 block, rows [t][k2l][k1] (read along k2l from
 // the value exchange layout, written along k1)
 __global__ void fs_tr_pack_kernel(FsDev d, const double* __restrict__ gx, const double* __restrict__ mult,
-                                  int t0, int nt, BigTerms bt, const double* __restrict__ delta,
+                                  int t0, int nt, BigTerms bt, const double2* __restrict__ wt,
                                   double2* __restrict__ rows, int* nonfinite) {
   __shared__ double2 tile[kFsTile][kFsTile + 1];
   constexpr int IT = kFsTile / kFsRows;
   const unsigned long long k10 = (unsigned long long)blockIdx.x * kFsTile;
   const unsigned long long k20 = (unsigned long long)blockIdx.y * kFsTile;
   const unsigned long long k2l = k20 + threadIdx.x;
-  unsigned long long kk[IT][2];
-  double y0[IT][2], gv[IT][2];
+  unsigned long long k0[IT];
+  double gv[IT][2];
   bool ok[IT];
 #pragma unroll
   for (int it = 0; it < IT; ++it) {
     const unsigned long long k1 = k10 + threadIdx.y + kFsRows * it;
     ok[it] = k1 < d.L1 && k2l < d.KB;
     const unsigned long long p = (unsigned long long)d.rank * d.KB + k2l + d.L2 * k1;
-    kk[it][0] = ok[it] ? fs_k_of_q(d, 2 * p) : 0;
-    kk[it][1] = ok[it] ? fs_k_of_q(d, 2 * p + 1) : 0;
+    k0[it] = ok[it] ? fs_k_of_q(d, 2 * p) : 0;
     double2 pair = make_double2(0.0, 0.0);
     if (ok[it]) {
-      const unsigned long long blk = kk[it][0] / d.B;
-      pair = *reinterpret_cast<const double2*>(gx + fs_xpos(d, blk, blk, (int)(kk[it][0] & 1), k1, k2l));
+      const unsigned long long blk = k0[it] / d.B;
+      pair = *reinterpret_cast<const double2*>(gx + fs_xpos(d, blk, blk, (int)(k0[it] & 1), k1, k2l));
+      if (mult) {
+        pair.x *= mult[k0[it]];
+        pair.y *= mult[fs_k_of_q(d, 2 * p + 1)];
+      }
     }
-#pragma unroll
-    for (int b = 0; b < 2; ++b) {
-      double v = b ? pair.y : pair.x;
-      if (ok[it] && mult) v *= mult[kk[it][b]];
-      gv[it][b] = v;
-      y0[it][b] = (ok[it] && !bt.plain) ? (double)d.n * delta[kk[it][b]] : 0.0;
-      if (nonfinite && t0 == 0 && ok[it] && !isfinite(v)) atomicOr(nonfinite, 1);
-    }
+    gv[it][0] = pair.x;
+    gv[it][1] = pair.y;
+    if (nonfinite && t0 == 0 && ok[it] && (!isfinite(pair.x) || !isfinite(pair.y))) atomicOr(nonfinite, 1);
   }
   for (int t = 0; t < nt; ++t) {
     const int l = t0 + t;
     const int odd = big_odd(bt, l);
 #pragma unroll
     for (int it = 0; it < IT; ++it) {
-      double h[2];
-#pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        const double w = bt.plain ? 1.0 : bt.cheb ? fs_weight(l, y0[it][b], bt.swap)
-                                                  : big_weight(bt, l, y0[it][b]);
-        double v = w * gv[it][b];
-        if (odd && (kk[it][b] & 1)) v = -v;
-        h[b] = v;
+      const unsigned long long k1 = k10 + threadIdx.y + kFsRows * it;
+      double2 h = make_double2(0.0, 0.0);
+      if (ok[it]) {
+        const double2 w = wt[((unsigned long long)l * d.L1 + k1) * d.KB + k2l];
+        h = make_double2(w.x * gv[it][0], w.y * gv[it][1]);
+        if (odd && (k0[it] & 1)) h = make_double2(-h.x, -h.y);
       }
-      tile[threadIdx.x][threadIdx.y + kFsRows * it] = make_double2(h[0], h[1]);
+      tile[threadIdx.x][threadIdx.y + kFsRows * it] = h;
     }
     __syncthreads();
     for (int ii = threadIdx.y; ii < kFsTile; ii += kFsRows) {  // write along k1
@@ -3022,6 +3036,23 @@ BigTerms fs_terms(const FastNdct& p) {
   return BigTerms{0, 0, cheb ? 1 : 0, cheb ? p.swap : 0};
 }
 
+const double2* fs_weights(const FsLayout& f, const FastNdct& p, cudaStream_t s) {
+  std::lock_guard<std::mutex> lock(f.wt_mu);
+  if (f.wt && f.wt_for == &p) return reinterpret_cast<const double2*>(f.wt);
+  if (f.wt) {
+    FLB_CUDA(cudaFree(f.wt));
+    f.wt = nullptr;
+  }
+  const int terms = fast_ndct_terms(p);
+  FLB_CUDA(cudaMalloc(&f.wt, (size_t)terms * f.B * sizeof(double)));
+  ensure_recip();
+  fs_weights_kernel<<<fs_grid(f.L1 * f.KB), 256, 0, s>>>(fs_dev(f), p.delta, terms, fs_terms(p),
+                                                         reinterpret_cast<double2*>(f.wt));
+  note_launch("fs_weights_kernel");
+  f.wt_for = &p;
+  return reinterpret_cast<const double2*>(f.wt);
+}
+
 void fs_check_terms(const FastNdct& p, const FsLayout& f, int t0, int t1) {
   if (p.n != f.n) fail(FL_INVALID_ARGUMENT, "four-step: layout and plan sizes differ");
   const int m = fast_ndct_terms(p);
@@ -3103,6 +3134,7 @@ void fs_destroy(FsLayout* f) {
   if (!f) return;
   for (int* q : {f->d_res_all, f->d_mirror, f->d_owner, f->d_lidx, f->d_cum, f->d_nres})
     if (q) cudaFree(q);
+  if (f->wt) cudaFree(f->wt);
   delete f;
 }
 
@@ -3158,7 +3190,8 @@ void fs_fwd2(const FsLayout& f, const FastNdct& p, int t0, int t1, const double2
   fs_fwd_gather_kernel<<<dim3(gx, gy, (unsigned)nt), tb, 0, s>>>(d, recv, nt, work);
   note_launch("fs_fwd_gather_kernel");
   fft_pow2(work, nullptr, f.log2L1, (size_t)nt * f.KB, true, s);
-  fs_fwd_unpack_kernel<<<dim3(gx, gy), tb, 0, s>>>(d, work, t0, nt, fs_terms(p), p.delta, fx, first);
+  const double2* wt = fs_weights(f, p, s);
+  fs_fwd_unpack_kernel<<<dim3(gx, gy), tb, 0, s>>>(d, work, t0, nt, fs_terms(p), wt, fx, first);
   note_launch("fs_fwd_unpack_kernel");
 }
 
@@ -3180,8 +3213,8 @@ void fs_tr1(const FsLayout& f, const FastNdct& p, const double* mult, int t0, in
   ensure_recip();
   const dim3 tb(kFsTile, kFsRows);
   const unsigned gx1 = (unsigned)((f.L1 + kFsTile - 1) / kFsTile), gy = (unsigned)((f.KB + kFsTile - 1) / kFsTile);
-  fs_tr_pack_kernel<<<dim3(gx1, gy), tb, 0, s>>>(d, gx, mult, t0, nt, fs_terms(p), p.delta, work,
-                                                 nonfinite);
+  const double2* wt = fs_weights(f, p, s);
+  fs_tr_pack_kernel<<<dim3(gx1, gy), tb, 0, s>>>(d, gx, mult, t0, nt, fs_terms(p), wt, work, nonfinite);
   note_launch("fs_tr_pack_kernel");
   fft_pow2(work, nullptr, f.log2L1, (size_t)nt * f.KB, false, s);
   fs_tr_twiddle_kernel<<<dim3(gx1, gy, (unsigned)nt), tb, 0, s>>>(d, work, nt, send);
