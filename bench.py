@@ -93,6 +93,9 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=12.0, help="CPU baseline sample budget")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-configs", action="store_true", help="skip the C1/C2/C3/C5 sub-results")
+    ap.add_argument("--c5-mode", choices=["term", "four_step"], default="term",
+                    help="--config c5: term-parallel (full vector on every rank) or the sharded "
+                         "distributed four-step NDCT (N/P per rank in and out)")
     ap.add_argument("--dry-run", action="store_true",
                     help="launch + sharding + timing protocol over gloo on CPU (no GPU)")
     return ap.parse_args()
@@ -510,8 +513,29 @@ def sub_configs(args, dist, rank: int, world: int, local: int) -> dict:
         e1.record(stream)
         barrier()
         res[name] = max_over_ranks(e0.elapsed_time(e1) / 3, dist, f"cuda:{local}")
+    # the sharded form: coefficients / values in natural blocks of N/P per
+    # rank, the NDCT as the distributed four-step (one NCCL all-to-all per
+    # term group), the conversion term-parallel (distributed.dlt_four_step)
+    fs = D.FourStep(cfg, world, rank)
+    blk = x[rank * fs.B:(rank + 1) * fs.B].contiguous()
+    fs_res = {}
+    for name, fn in (("dlt", D.dlt_four_step), ("idlt", D.idlt_four_step)):
+        for _ in range(2):
+            fn(cfg, blk, dist, fs)
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for _ in range(3):
+            fn(cfg, blk, dist, fs)
+        e1.record(stream)
+        barrier()
+        fs_res[name] = max_over_ranks(e0.elapsed_time(e1) / 3, dist, f"cuda:{local}")
+    del fs
     out["c5"] = {"workload": CONFIGS["c5"][3], "N": n, "n_gpus": world, "plan_s": plan_s,
                  "dlt_ms": res["dlt"], "idlt_ms": res["idlt"],
+                 "four_step": {"dlt_ms": fs_res["dlt"], "idlt_ms": fs_res["idlt"],
+                               "note": "sharded in / out (N/P per rank); NDCT as the distributed "
+                                       "four-step with one all-to-all per term group"},
                  "dlt_coeffs_per_s": n / res["dlt"] * 1e3, "idlt_coeffs_per_s": n / res["idlt"] * 1e3,
                  "dlt_hbm_frac_per_gpu": 24.0 * n / (res["dlt"] / 1e3) / 1e9 / peak / world,
                  "leg2cheb": l2c_method(cfg, n),
@@ -544,8 +568,19 @@ def run_c5(args, rank: int, world: int, local: int) -> None:
             dist.barrier()
         torch.cuda.synchronize()
 
+    if args.c5_mode == "four_step":
+        fs = D.FourStep(cfg, world, rank)
+        sl = slice(rank * fs.B, (rank + 1) * fs.B)
+        xh = xh[sl].contiguous().pin_memory()
+        x = xh.cuda()
+
+        def step(v):
+            return D.dlt_four_step(cfg, v, dist, fs)
+    else:
+        def step(v):
+            return D.dlt(cfg, v, dist, scatter=True)
     for _ in range(max(args.warmup, 3)):
-        D.dlt(cfg, x, dist, scatter=True)
+        step(x)
     barrier()
     l0 = fl.launch_count()
     s = torch.cuda.current_stream()
@@ -554,7 +589,7 @@ def run_c5(args, rank: int, world: int, local: int) -> None:
         barrier()
         e0.record(s)
         for _ in range(args.steps):
-            D.dlt(cfg, x, dist, scatter=True)
+            step(x)
         e1.record(s)
         barrier()
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, dist, f"cuda:{local}")
@@ -563,7 +598,7 @@ def run_c5(args, rank: int, world: int, local: int) -> None:
     e0.record(s)
     for _ in range(2):
         xd = xh.cuda(non_blocking=True)
-        part = D.dlt(cfg, xd, dist, scatter=True)
+        part = step(xd)
         back = part.cpu()
     e1.record(s)
     barrier()
@@ -577,9 +612,10 @@ def run_c5(args, rank: int, world: int, local: int) -> None:
             "roofline": {"bound": "hbm", "achieved": 24.0 * n / (ms / 1e3) / 1e9, "peak": hbm_peak() * world,
                          "unit": "GB/s", "frac": 24.0 * n / (ms / 1e3) / 1e9 / (hbm_peak() * world),
                          "traffic": None, "note": "24 B/coef (c, f, delta) over the job"},
-            "e2e": {"value": n / (e2e_ms / 1e3), "unit": "coeffs/s", "h2d_bytes_per_step": 8 * n,
+            "e2e": {"value": n / (e2e_ms / 1e3), "unit": "coeffs/s", "h2d_bytes_per_step": int(8 * xh.numel()),
                     "d2h_bytes_per_step": int(8 * back.numel())},
             "leg2cheb": "asymptotic expansion " + json.dumps(cfg.leg2cheb_asy_info()),
+            "c5_mode": args.c5_mode,
             "gpu_launches": launches, "clocks": clk.summary()}))
     if dist is not None:
         dist.barrier()
