@@ -1415,7 +1415,10 @@ __global__ void __launch_bounds__(Cfg<LOG2N>::THREADS, LOG2N <= 12 ? 2 : 1)
       zx = zx == zbA ? zbB : zbA;
     }
     // zy holds the first pass; zx is free
-    double2* zb = mid_passes_pp<P, E, 8, P, false, 0>(zy, zx, t, fftw, 0);
+#ifndef FLB_STREAM_TR_TWP
+#define FLB_STREAM_TR_TWP 1  // 4096 x 65536: 1.108 -> 1.040 ms (59 -> 63 % of HBM)
+#endif
+    double2* zb = mid_passes_pp<P, E, 8, P, false, 0, FLB_STREAM_TR_TWP != 0>(zy, zx, t, fftw, 0);
     // unpack (tr_term): rows {a, P - a, P + a, N - a} of each group g
     double* dst = out + col * ld_out;
 #pragma unroll
