@@ -75,6 +75,14 @@ struct FastNdct {
   double* bes_wt = nullptr;  // transpose weights, tr_slot order
   double* bes_tt = nullptr;  // transpose row factors T_m(n/N), tr_row order
   double* cl_wf = nullptr;   // forward weights in the cluster kernel's thread order (2^14..2^16)
+  // multi-pass path (N > 8192) of a plan-owned object: the weight / stage
+  // tables [bes_terms][N] of all terms, kept after the first call (they
+  // depend on the plan's offsets only; per call they cost 0.12 of 0.44 ms at
+  // 2^20 and 14 of 25 ms at 2^26)
+  mutable std::mutex big_mu;
+  mutable double* big_wt = nullptr;
+  mutable double* big_rt = nullptr;
+  mutable bool big_tried = false;
 };
 
 namespace {
@@ -2185,11 +2193,16 @@ __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, si
 #define FLB_BIG_BUDGET_GIB 8
 #endif
 constexpr size_t kBigBudget = size_t(FLB_BIG_BUDGET_GIB) << 30;
+// largest pair of kept plan tables (2^26 x 14 terms: 15 GiB of the 180)
+#ifndef FLB_BIG_TABLE_CACHE_GIB
+#define FLB_BIG_TABLE_CACHE_GIB 16
+#endif
+constexpr size_t kBigTableCache = size_t(FLB_BIG_TABLE_CACHE_GIB) << 30;
 
 void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double* out,
                 size_t ld_out, size_t batch, const double* delta, int l_lo, int l_hi,
                 int plain_op, const double* mult, int* nonfinite, cudaStream_t s, int cheb,
-                int swap) {
+                int swap, const FastNdct* owner = nullptr) {
   const size_t n = size_t(1) << log2n, P = n / 2;
   if (ld_in != ld_out) fail(FL_RUNTIME_ERROR, "fast ndct: mismatched strides");
   const int plain = plain_op >= 0;
@@ -2208,16 +2221,51 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
   double *wt = nullptr, *rt = nullptr;
   FLB_CUDA(cudaMallocAsync(&Z, (size_t)tb * chunk * P * sizeof(double2), s));
   FLB_CUDA(cudaMallocAsync(&S, (size_t)tb * chunk * P * sizeof(double2), s));
-  FLB_CUDA(cudaMallocAsync(&wt, (size_t)tb * n * sizeof(double), s));
-  FLB_CUDA(cudaMallocAsync(&rt, (size_t)tb * n * sizeof(double), s));
+  // a plan's tables of all its terms: built on the first call, then kept
+  // (published after one synchronisation; other threads wait on the mutex)
+  const double *wt_all = nullptr, *rt_all = nullptr;
+  if (owner && cheb && !plain && !owner->async_alloc && delta == owner->delta &&
+      owner->bes_terms > 0 && l_hi <= owner->bes_terms) {
+    const size_t bytes = (size_t)owner->bes_terms * n * sizeof(double);
+    std::lock_guard<std::mutex> lock(owner->big_mu);
+    if (!owner->big_tried) {
+      owner->big_tried = true;
+      if (2 * bytes <= kBigTableCache) {
+        double *w = nullptr, *r = nullptr;
+        if (cudaMalloc(&w, bytes) == cudaSuccess && cudaMalloc(&r, bytes) == cudaSuccess) {
+          ensure_recip();
+          big_tables_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, 0, owner->bes_terms, bt,
+                                                                        delta, w, r);
+          note_launch("big_tables_kernel");
+          FLB_CUDA(cudaStreamSynchronize(s));
+          owner->big_wt = w;
+          owner->big_rt = r;
+        } else {
+          if (w) cudaFree(w);
+          cudaGetLastError();
+        }
+      }
+    }
+    wt_all = owner->big_wt;
+    rt_all = owner->big_rt;
+  }
+  if (!wt_all) {
+    FLB_CUDA(cudaMallocAsync(&wt, (size_t)tb * n * sizeof(double), s));
+    FLB_CUDA(cudaMallocAsync(&rt, (size_t)tb * n * sizeof(double), s));
+  }
   const unsigned gx = (unsigned)std::min<size_t>((P + 255) / 256, 2048);
   const unsigned gxn = (unsigned)std::min<size_t>((n + 255) / 256, 4096);
   const unsigned gxq = (unsigned)std::min<size_t>((P / 2 + 256) / 256, 4096);
   for (int l0 = l_lo; l0 < l_hi; l0 += tb) {
     const int nt = std::min(tb, l_hi - l0);
-    ensure_recip();
-    big_tables_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, l0, nt, bt, delta, wt, rt);
-    note_launch("big_tables_kernel");
+    if (wt_all) {
+      wt = const_cast<double*>(wt_all) + (size_t)l0 * n;
+      rt = const_cast<double*>(rt_all) + (size_t)l0 * n;
+    } else {
+      ensure_recip();
+      big_tables_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, l0, nt, bt, delta, wt, rt);
+      note_launch("big_tables_kernel");
+    }
     for (size_t c0 = 0; c0 < batch; c0 += chunk) {
       const size_t nc = batch - c0 < chunk ? batch - c0 : chunk;
       const int first = l0 == l_lo;
@@ -2242,8 +2290,10 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
   }
   cudaFreeAsync(Z, s);
   cudaFreeAsync(S, s);
-  cudaFreeAsync(wt, s);
-  cudaFreeAsync(rt, s);
+  if (!wt_all) {
+    cudaFreeAsync(wt, s);
+    cudaFreeAsync(rt, s);
+  }
 }
 
 void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* out,
@@ -2275,7 +2325,7 @@ void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* 
   }
   if (log2n > 13) {
     launch_big(log2n, transpose, in, ld_in, out, ld_out, batch, delta, l_lo, l_hi, plain_op, mult,
-               nonfinite, s, cheb ? 1 : 0, cheb ? bes->swap : 0);
+               nonfinite, s, cheb ? 1 : 0, cheb ? bes->swap : 0, bes);
     return;
   }
   if (plain_op < 0 && (l_lo != 0 || l_hi != num_terms))
@@ -2513,6 +2563,8 @@ FastNdct* fast_ndct_create_bessel(size_t n, int kind, const double* delta, int n
 
 void fast_ndct_destroy(FastNdct* p) {
   if (!p) return;
+  if (p->big_wt) cudaFree(p->big_wt);
+  if (p->big_rt) cudaFree(p->big_rt);
   for (double* t : {p->owned_delta, p->bes_wf, p->bes_wt, p->bes_tt, p->cl_wf}) {
     if (!t) continue;
     if (p->async_alloc)
