@@ -768,6 +768,7 @@ struct L2CAsy {
   };
   mutable std::mutex mu;
   mutable std::vector<Starts> starts;
+  bool keep_starts = true;
 };
 
 namespace {
@@ -904,6 +905,10 @@ void l2c_asy_destroy(L2CAsy* f) {
   if (f->ab) cudaFree(f->ab);
   for (const L2CAsy::Starts& c : f->starts) cudaFree(c.St);
   delete f;
+}
+
+void l2c_asy_one_shot(L2CAsy* f) {
+  if (f) f->keep_starts = false;
 }
 
 L2CAsyInfo l2c_asy_info(const L2CAsy& f) {
@@ -1122,7 +1127,7 @@ void l2c_asy_apply(const L2CAsy& f, int transpose, const double* in, double* out
   constexpr size_t kMaxStarts = 4;
   double2* st_cached = nullptr;
   bool st_keep = false;
-  if (rt.nslots > 0) {
+  if (rt.nslots > 0 && f.keep_starts) {
     const int k_lo = full ? 0 : t_lo, k_hi = full ? l2c_asy_terms(f) : t_hi;
     std::lock_guard<std::mutex> lock(f.mu);
     for (const L2CAsy::Starts& c : f.starts)
