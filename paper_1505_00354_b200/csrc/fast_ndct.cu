@@ -82,7 +82,8 @@ struct FastNdct {
   mutable std::mutex big_mu;
   mutable double* big_wt = nullptr;
   mutable double* big_rt = nullptr;
-  mutable bool big_tried = false;
+  mutable double2* big_wp = nullptr;  // forward weights in packed-entry order (big_wp_kernel)
+  mutable bool big_tried = false, big_wp_tried = false;
 };
 
 namespace {
@@ -2022,6 +2023,23 @@ __global__ void big_tables_kernel(size_t n, int l0, int nt, BigTerms bt,
   }
 }
 
+// The forward weights in the order of the packed transforms' entries, for the
+// unpack fused into the last FFT pass (fft.cuh: NdctUnpack): entry m of term
+// t holds outputs kx (real part) and ky (imaginary part), wp[t][m] =
+// (+-wt[t][kx], +-wt[t][ky]) with big_fwd_unpack_kernel's signs (odd terms
+// negate the odd outputs).
+__global__ void big_wp_kernel(size_t n, int l0, int nt, BigTerms bt, const double* __restrict__ wt,
+                              double2* __restrict__ wp) {
+  const size_t P = n / 2;
+  const size_t m = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (m >= P) return;
+  const size_t kx = m < P / 2 ? 4 * m : 2 * n - 4 * m - 1, ky = m < P / 2 ? 4 * m + 2 : 2 * n - 4 * m - 3;
+  for (int t = 0; t < nt; ++t) {
+    const double sg = (big_odd(bt, l0 + t) && (kx & 1)) ? -1.0 : 1.0;  // kx, ky share their parity
+    wp[(size_t)t * P + m] = make_double2(sg * wt[(size_t)t * n + kx], sg * wt[(size_t)t * n + ky]);
+  }
+}
+
 // Forward pack of all nt terms: Z[(t nc + col) P + m] from the stage
 // rt[t][j] c_j (the real-DCT packing of the file header). One thread per m for
 // every term: the four column entries and the three twiddles of m are read /
@@ -2198,6 +2216,9 @@ constexpr size_t kBigBudget = size_t(FLB_BIG_BUDGET_GIB) << 30;
 #define FLB_BIG_TABLE_CACHE_GIB 16
 #endif
 constexpr size_t kBigTableCache = size_t(FLB_BIG_TABLE_CACHE_GIB) << 30;
+#ifndef FLB_BIG_FUSED_UNPACK
+#define FLB_BIG_FUSED_UNPACK 1
+#endif
 
 void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double* out,
                 size_t ld_out, size_t batch, const double* delta, int l_lo, int l_hi,
@@ -2253,6 +2274,27 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
     FLB_CUDA(cudaMallocAsync(&wt, (size_t)tb * n * sizeof(double), s));
     FLB_CUDA(cudaMallocAsync(&rt, (size_t)tb * n * sizeof(double), s));
   }
+  // forward: the unpack fused into the last FFT pass (packed-order weights)
+  const bool fused_unpack = FLB_BIG_FUSED_UNPACK && !transpose && fft_pow2_ndct_unpack_ok(log2n - 1);
+  const double2* wp_all = nullptr;
+  double2* wp = nullptr;
+  if (fused_unpack && wt_all) {
+    std::lock_guard<std::mutex> lock(owner->big_mu);
+    if (!owner->big_wp_tried) {
+      owner->big_wp_tried = true;
+      double2* w = nullptr;
+      if (cudaMalloc(&w, (size_t)owner->bes_terms * P * sizeof(double2)) == cudaSuccess) {
+        big_wp_kernel<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(n, 0, owner->bes_terms, bt, wt_all, w);
+        note_launch("big_wp_kernel");
+        FLB_CUDA(cudaStreamSynchronize(s));
+        owner->big_wp = w;
+      } else {
+        cudaGetLastError();
+      }
+    }
+    wp_all = owner->big_wp;
+  }
+  if (fused_unpack && !wp_all) FLB_CUDA(cudaMallocAsync(&wp, (size_t)tb * P * sizeof(double2), s));
   const unsigned gx = (unsigned)std::min<size_t>((P + 255) / 256, 2048);
   const unsigned gxn = (unsigned)std::min<size_t>((n + 255) / 256, 4096);
   const unsigned gxq = (unsigned)std::min<size_t>((P / 2 + 256) / 256, 4096);
@@ -2261,10 +2303,15 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
     if (wt_all) {
       wt = const_cast<double*>(wt_all) + (size_t)l0 * n;
       rt = const_cast<double*>(rt_all) + (size_t)l0 * n;
+      if (wp_all) wp = const_cast<double2*>(wp_all) + (size_t)l0 * P;
     } else {
       ensure_recip();
       big_tables_kernel<<<(unsigned)((n + 255) / 256), 256, 0, s>>>(n, l0, nt, bt, delta, wt, rt);
       note_launch("big_tables_kernel");
+    }
+    if (fused_unpack && !wp_all) {
+      big_wp_kernel<<<(unsigned)((P + 255) / 256), 256, 0, s>>>(n, l0, nt, bt, wt, wp);
+      note_launch("big_wp_kernel");
     }
     for (size_t c0 = 0; c0 < batch; c0 += chunk) {
       const size_t nc = batch - c0 < chunk ? batch - c0 : chunk;
@@ -2273,10 +2320,15 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
         big_fwd_pack_kernel<<<dim3(gx, (unsigned)nc), 256, 0, s>>>(
             in + c0 * ld_in, ld_in, n, nc, l0, nt, bt, rt, Z, nonfinite);
         note_launch("big_fwd_pack_kernel");
-        fft_pow2(Z, S, log2n - 1, nc * nt, true, s);
-        big_fwd_unpack_kernel<<<dim3(gxn, (unsigned)nc), 256, 0, s>>>(
-            Z, n, nc, l0, nt, bt, wt, out + c0 * ld_out, ld_out, first);
-        note_launch("big_fwd_unpack_kernel");
+        if (fused_unpack) {
+          fft_pow2_ndct_unpack(Z, S, log2n - 1, true,
+                               NdctUnpack{wp, out + c0 * ld_out, ld_out, nc, nt, first}, s);
+        } else {
+          fft_pow2(Z, S, log2n - 1, nc * nt, true, s);
+          big_fwd_unpack_kernel<<<dim3(gxn, (unsigned)nc), 256, 0, s>>>(
+              Z, n, nc, l0, nt, bt, wt, out + c0 * ld_out, ld_out, first);
+          note_launch("big_fwd_unpack_kernel");
+        }
       } else {
         big_tr_pack_kernel<<<dim3(gx, (unsigned)nc, (unsigned)nt), 256, 0, s>>>(
             in + c0 * ld_in, ld_in, n, nc, l0, bt, wt, mult, Z, nonfinite);
@@ -2294,6 +2346,7 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
     cudaFreeAsync(wt, s);
     cudaFreeAsync(rt, s);
   }
+  if (fused_unpack && !wp_all) cudaFreeAsync(wp, s);
 }
 
 void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* out,
@@ -2565,6 +2618,7 @@ void fast_ndct_destroy(FastNdct* p) {
   if (!p) return;
   if (p->big_wt) cudaFree(p->big_wt);
   if (p->big_rt) cudaFree(p->big_rt);
+  if (p->big_wp) cudaFree(p->big_wp);
   for (double* t : {p->owned_delta, p->bes_wf, p->bes_wt, p->bes_tt, p->cl_wf}) {
     if (!t) continue;
     if (p->async_alloc)

@@ -527,6 +527,115 @@ void fft_multipass(double2* d, double2* t, int log2p, size_t items, cudaStream_t
   line_pass<INV>(pp.lr, t, d, P, items, LineMap{1, pp.R, 1, 1, pp.C, 0, 0, 0, 0}, s);
 }
 
+// The last (row) pass of fft_multipass for the multi-pass NDCT, all terms of
+// one column in one CTA with the unpack's weighted sum in registers
+// (fft.cuh: NdctUnpack). Lines l = b2 (LINES adjacent ones per CTA) of the
+// contiguous rows src[b2 R + a1]; output index m = b2 + C b1.
+template <int LOG2L, bool INV>
+__global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
+    fft_row_unpack_kernel(const double2* __restrict__ src, unsigned long long P,
+                          unsigned long long C, NdctUnpack a, const double2* __restrict__ tw) {
+  using Q = LinePass<LOG2L>;
+  constexpr int L = Q::L, LINES = Q::LINES, TL = Q::TL, E = Q::E;
+  constexpr int R0 = pass_radix(L, 1);
+  static_assert(R0 == E, "one first-pass butterfly per thread");
+  constexpr int NSL = last_pass_ns(L), RL = L / NSL;
+  constexpr int PER = LINES * L / Q::THREADS;
+  extern __shared__ double2 sm[];
+  const uint32_t l0 = blockIdx.x * (uint32_t)LINES;
+  const int t = threadIdx.x;
+  const int line = t / TL, tid = t % TL;
+  const size_t col = blockIdx.y;
+  double2* row = sm + line * Q::LS;
+  double2 acc[PER];
+#pragma unroll
+  for (int r = 0; r < PER; ++r) acc[r] = make_double2(0.0, 0.0);
+  const double2* src_line = src + col * P + (size_t)(l0 + line) * L + tid;
+  const size_t term_stride = a.nc * P;
+#pragma unroll 1
+  for (int tz = 0; tz < a.nt; ++tz) {
+    // the twiddle loads stay inside the loop (hoisted out of it they cost
+    // ~150 registers: one CTA per SM)
+    const double2* twi = tw;
+    asm volatile("" : "+l"(twi));
+    double2 v[E];
+#pragma unroll
+    for (int r = 0; r < R0; ++r) v[r] = src_line[(size_t)tz * term_stride + r * (L / R0)];
+    pass_compute<L, E, R0, 1, INV>(v, tid, twi);
+    pass_store<L, E, R0, 1>(v, row, tid);
+    __syncthreads();
+    mid_passes<L, E, R0, NSL, INV, 0>(row, tid, twi, 0);
+    pass_load<L, E, RL>(v, row, tid);
+    pass_compute<L, E, RL, NSL, INV>(v, tid, twi + pass_tw_offset(L, NSL));
+    __syncthreads();
+    pass_store<L, E, RL, NSL>(v, row, tid);
+    __syncthreads();
+    const double2* wp = a.wp + (size_t)tz * P;
+#pragma unroll
+    for (int r = 0; r < PER; ++r) {
+      const int i = t + r * Q::THREADS;
+      const int j = i % LINES, k = i / LINES;
+      const double2 x = sm[j * Q::LS + smem_pad(k)];
+      const double2 w = __ldg(&wp[(size_t)(l0 + j) + C * (size_t)k]);
+      acc[r].x = __fma_rn(w.x, x.x, acc[r].x);
+      acc[r].y = __fma_rn(w.y, x.y, acc[r].y);
+    }
+    __syncthreads();
+  }
+  double* o = a.out + col * a.ld;
+  const size_t n2 = 4 * (size_t)P;  // 2N
+#pragma unroll
+  for (int r = 0; r < PER; ++r) {
+    const int i = t + r * Q::THREADS;
+    const int j = i % LINES, k = i / LINES;
+    const size_t m = (size_t)(l0 + j) + C * (size_t)k;
+    const size_t kx = m < P / 2 ? 4 * m : n2 - 4 * m - 1, ky = m < P / 2 ? 4 * m + 2 : n2 - 4 * m - 3;
+    if (a.first) {
+      o[kx] = acc[r].x;
+      o[ky] = acc[r].y;
+    } else {
+      o[kx] += acc[r].x;
+      o[ky] += acc[r].y;
+    }
+  }
+}
+
+template <int LOG2L, bool INV>
+void launch_row_unpack(const double2* src, unsigned long long P, const NdctUnpack& a,
+                       cudaStream_t s) {
+  using Q = LinePass<LOG2L>;
+  const double2* tw = pass_twiddles(LOG2L);
+  const unsigned long long lines = P >> LOG2L;
+  auto kern = fft_row_unpack_kernel<LOG2L, INV>;
+  FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM));
+  dim3 grid((unsigned)(lines / Q::LINES), (unsigned)a.nc);
+  kern<<<grid, Q::THREADS, Q::SMEM, s>>>(src, P, lines, a, tw);
+  note_launch("fft_row_unpack_kernel");
+}
+
+template <bool INV>
+void ndct_unpack_multipass(double2* d, double2* t, int log2p, const NdctUnpack& a, cudaStream_t s) {
+  const unsigned long long P = 1ull << log2p;
+  const PassPlan pp(log2p);
+  const size_t items = (size_t)a.nt * a.nc;
+  for (size_t b0 = 0; b0 < items; b0 += 65535) {
+    const size_t nb = items - b0 < 65535 ? items - b0 : 65535;
+    if (pp.passes == 2) {
+      line_pass<INV>(pp.lc, d + b0 * P, t + b0 * P, P, nb, pp.col(), s);
+    } else {
+      line_pass<INV>(pp.l2, d + b0 * P, d + b0 * P, P, nb, pp.col1(), s);
+      line_pass<INV>(pp.l1, d + b0 * P, t + b0 * P, P, nb, pp.col2(), s);
+    }
+  }
+  switch (pp.lr) {
+    case 7: launch_row_unpack<7, INV>(t, P, a, s); break;
+    case 8: launch_row_unpack<8, INV>(t, P, a, s); break;
+    case 9: launch_row_unpack<9, INV>(t, P, a, s); break;
+    case 10: launch_row_unpack<10, INV>(t, P, a, s); break;
+    default: fail(FL_RUNTIME_ERROR, "fft: unsupported row length for the fused unpack");
+  }
+}
+
 template <int LOG2P, bool INV>
 void launch_smem(double2* data, size_t rows, const double2* tw, cudaStream_t s) {
   constexpr int P = 1 << LOG2P;
@@ -655,6 +764,23 @@ void fft_pow2(double2* data, double2* scratch, int log2p, size_t batch, bool inv
     else
       fft_multipass<false>(data + b0 * P, scratch + b0 * P, log2p, nb, s);
   }
+}
+
+bool fft_pow2_ndct_unpack_ok(int log2p) {
+  if (log2p <= kMaxSmemLog2 || log2p > kMaxLog2) return false;
+  const int lr = PassPlan(log2p).lr;
+  return lr >= 7 && lr <= 10;
+}
+
+void fft_pow2_ndct_unpack(double2* data, double2* scratch, int log2p, bool inverse,
+                          const NdctUnpack& a, cudaStream_t s) {
+  if (!fft_pow2_ndct_unpack_ok(log2p)) fail(FL_RUNTIME_ERROR, "fft: fused unpack: length");
+  if (a.nc == 0 || a.nt == 0) return;
+  if (a.nc > 65535) fail(FL_RUNTIME_ERROR, "fft: fused unpack: too many columns");
+  if (inverse)
+    ndct_unpack_multipass<true>(data, scratch, log2p, a, s);
+  else
+    ndct_unpack_multipass<false>(data, scratch, log2p, a, s);
 }
 
 void th_symbol_layout(double2* sym, double2* scratch, int log2p, cudaStream_t s) {

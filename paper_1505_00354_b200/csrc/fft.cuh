@@ -22,6 +22,25 @@ void fft_pow2(double2* data, double2* scratch, int log2p, size_t batch, bool inv
 constexpr int kMaxSmemLog2 = 13;  // 8192 points = 128 KiB of double2 per CTA
 constexpr int kMaxLog2 = 26;
 
+// The multi-pass NDCT's forward transforms with the unpack fused into the last
+// (row) pass (fast_ndct.cu, N > 16384): `data` holds nt * nc packed rows of
+// 2^log2p points (row tz * nc + col); all passes but the last run as in
+// fft_pow2, then one CTA per group of adjacent lines and column runs the row
+// pass of every term in turn and accumulates
+//   out[col][kx(m)] (+)= sum_tz wp[tz][m].x Re X_tz[m],  out[col][ky(m)] likewise with Im,
+// kx, ky = 4m, 4m + 2 (m < P/2) or 2N - 4m - 1, 2N - 4m - 3 (the real-DCT
+// packing's output order, N = 2P), in registers: the transformed rows are
+// never written (one write and one read of all terms x columns less).
+struct NdctUnpack {
+  const double2* wp;  // [nt][P] output weights (signs folded in)
+  double* out;        // columns of stride ld
+  size_t ld, nc;
+  int nt, first;      // first: store, else add to out
+};
+bool fft_pow2_ndct_unpack_ok(int log2p);
+void fft_pow2_ndct_unpack(double2* data, double2* scratch, int log2p, bool inverse,
+                          const NdctUnpack& a, cudaStream_t s);
+
 // ---- fused Toeplitz-Hankel sweep (l2c_fast.cu) for 2^log2p > 8192 -------------
 // One batched sweep over rank pairs q < pairs computes, per pair,
 //   W_q = IFFT(FFT(V_q) . S~),  V_q[b] = (l_{ra}(b) u_b, l_{ra+1}(b) u_b) (b < np, else 0),
