@@ -2136,6 +2136,28 @@ __global__ void big_tr_pack_kernel(const double* __restrict__ in, size_t ld, siz
   }
 }
 
+// The transposed pack fused into the first FFT pass (fft.cuh: NdctTrPack): the
+// column's input (times mult) once in packed-entry order, G[col][m] =
+// (v(kx), v(ky)); the per-term weights and signs are wp's (big_wp_kernel).
+__global__ void big_tr_g_kernel(const double* __restrict__ in, size_t ld, size_t n,
+                                const double* __restrict__ mult, double2* __restrict__ G,
+                                int* nonfinite) {
+  const size_t P = n / 2;
+  const size_t col = blockIdx.y;
+  const double* g = in + col * ld;
+  for (size_t m = blockIdx.x * (size_t)blockDim.x + threadIdx.x; m < P;
+       m += (size_t)gridDim.x * blockDim.x) {
+    const size_t kx = m < P / 2 ? 4 * m : 2 * n - 4 * m - 1, ky = m < P / 2 ? 4 * m + 2 : 2 * n - 4 * m - 3;
+    double a = g[kx], b = g[ky];
+    if (mult) {
+      a *= mult[kx];
+      b *= mult[ky];
+    }
+    if (nonfinite && (!isfinite(a) || !isfinite(b))) atomicOr(nonfinite, 1);
+    G[col * P + m] = make_double2(a, b);
+  }
+}
+
 // Transposed unpack of all nt terms: out_r (+)= sum_t rt[t][r] X_t(r).
 // The outputs r in {a, P - a, P + a, N - a} read the same two packed entries
 // a, P - a of every term (DCT^T rows at kk = r, DST^T rows at kk = N - r): one
@@ -2275,7 +2297,8 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
     FLB_CUDA(cudaMallocAsync(&rt, (size_t)tb * n * sizeof(double), s));
   }
   // forward: the unpack fused into the last FFT pass (packed-order weights)
-  const bool fused_unpack = FLB_BIG_FUSED_UNPACK && !transpose && fft_pow2_ndct_unpack_ok(log2n - 1);
+  const bool fused_unpack = FLB_BIG_FUSED_UNPACK && fft_pow2_ndct_unpack_ok(log2n - 1) &&
+                            (!transpose || (size_t)tb * chunk <= 65535);
   const double2* wp_all = nullptr;
   double2* wp = nullptr;
   if (fused_unpack && wt_all) {
@@ -2295,6 +2318,8 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
     wp_all = owner->big_wp;
   }
   if (fused_unpack && !wp_all) FLB_CUDA(cudaMallocAsync(&wp, (size_t)tb * P * sizeof(double2), s));
+  double2* G = nullptr;  // transposed: the weighted input in packed order
+  if (fused_unpack && transpose) FLB_CUDA(cudaMallocAsync(&G, chunk * P * sizeof(double2), s));
   const unsigned gx = (unsigned)std::min<size_t>((P + 255) / 256, 2048);
   const unsigned gxn = (unsigned)std::min<size_t>((n + 255) / 256, 4096);
   const unsigned gxq = (unsigned)std::min<size_t>((P / 2 + 256) / 256, 4096);
@@ -2330,10 +2355,18 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
           note_launch("big_fwd_unpack_kernel");
         }
       } else {
-        big_tr_pack_kernel<<<dim3(gx, (unsigned)nc, (unsigned)nt), 256, 0, s>>>(
-            in + c0 * ld_in, ld_in, n, nc, l0, bt, wt, mult, Z, nonfinite);
-        note_launch("big_tr_pack_kernel");
-        fft_pow2(Z, S, log2n - 1, nc * nt, false, s);
+        if (fused_unpack) {
+          // the pack fused into the first FFT pass's loads
+          big_tr_g_kernel<<<dim3(gx, (unsigned)nc), 256, 0, s>>>(in + c0 * ld_in, ld_in, n, mult, G,
+                                                                 l0 == l_lo ? nonfinite : nullptr);
+          note_launch("big_tr_g_kernel");
+          fft_pow2_ndct_tr_pack(Z, S, log2n - 1, false, NdctTrPack{wp, G, nc, nt}, s);
+        } else {
+          big_tr_pack_kernel<<<dim3(gx, (unsigned)nc, (unsigned)nt), 256, 0, s>>>(
+              in + c0 * ld_in, ld_in, n, nc, l0, bt, wt, mult, Z, nonfinite);
+          note_launch("big_tr_pack_kernel");
+          fft_pow2(Z, S, log2n - 1, nc * nt, false, s);
+        }
         big_tr_unpack_kernel<<<dim3(gxq, (unsigned)nc), 256, 0, s>>>(
             Z, n, nc, l0, nt, bt, rt, out + c0 * ld_out, ld_out, first);
         note_launch("big_tr_unpack_kernel");
@@ -2347,6 +2380,7 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
     cudaFreeAsync(rt, s);
   }
   if (fused_unpack && !wp_all) cudaFreeAsync(wp, s);
+  if (G) cudaFreeAsync(G, s);
 }
 
 void dispatch(int log2n, int transpose, const double* in, size_t ld_in, double* out,

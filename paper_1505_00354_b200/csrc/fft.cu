@@ -320,10 +320,11 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
 // (its passes were L1/shared-memory-bound: 87-96 % l1tex throughput).
 // Threads are laid out line-minor for column passes (consecutive threads:
 // consecutive lines, LINES x 16 B runs) and element-minor for row passes.
-template <int LOG2L, bool INV>
+template <int LOG2L, bool INV, bool PK = false>
 __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
     fft_line_fused_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
-                          unsigned long long P, LineMap mp, const double2* __restrict__ tw) {
+                          unsigned long long P, LineMap mp, const double2* __restrict__ tw,
+                          NdctTrPack pk = NdctTrPack{}) {
   using Q = LinePass<LOG2L>;
   constexpr int L = Q::L, LINES = Q::LINES, TL = Q::TL, E = Q::E;
   constexpr int R0 = pass_radix(L, 1);
@@ -359,8 +360,21 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
   };
   // first pass (NS = 1, no twiddles) from global memory
   double2 v[E];
+  if constexpr (PK) {
+    // the NDCT^T pack: entry m of row (tz, col) = wp[tz][m] (.) G[col][m]
+    const size_t col = item % pk.nc, tz = item / pk.nc;
+    const double2* G = pk.G + col * P;
+    const double2* W = pk.wp + tz * P;
 #pragma unroll
-  for (int r = 0; r < R0; ++r) v[r] = src_item[lo + hi * Hin + (uint32_t)(tid + r * (L / R0)) * Sin];
+    for (int r = 0; r < R0; ++r) {
+      const uint32_t g = lo + hi * Hin + (uint32_t)(tid + r * (L / R0)) * Sin;
+      const double2 a = __ldg(&G[g]), w = __ldg(&W[g]);
+      v[r] = make_double2(w.x * a.x, w.y * a.y);
+    }
+  } else {
+#pragma unroll
+    for (int r = 0; r < R0; ++r) v[r] = src_item[lo + hi * Hin + (uint32_t)(tid + r * (L / R0)) * Sin];
+  }
   pass_compute<L, E, R0, 1, INV>(v, tid, tw);
   pass_store<L, E, R0, 1>(v, row, tid);
   __syncthreads();
@@ -399,7 +413,7 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
 #endif
 template <int LOG2L, bool INV>
 void launch_line_fused(const double2* src, double2* dst, unsigned long long P, size_t items,
-                       const LineMap& mp, cudaStream_t s) {
+                       const LineMap& mp, cudaStream_t s, const NdctTrPack* pk = nullptr) {
   using Q = LinePass<LOG2L>;
   const double2* tw = pass_twiddles(LOG2L);
   const unsigned long long lines = P >> LOG2L;
@@ -411,10 +425,16 @@ void launch_line_fused(const double2* src, double2* dst, unsigned long long P, s
     m2.twhi = t2.second;
     m2.twh = (lq + 1) / 2;
   }
-  auto kern = fft_line_fused_kernel<LOG2L, INV>;
-  FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM));
   dim3 grid((unsigned)(lines / Q::LINES), (unsigned)items);
-  kern<<<grid, Q::THREADS, Q::SMEM, s>>>(src, dst, P, m2, tw);
+  if (pk) {
+    auto kern = fft_line_fused_kernel<LOG2L, INV, true>;
+    FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM));
+    kern<<<grid, Q::THREADS, Q::SMEM, s>>>(src, dst, P, m2, tw, *pk);
+  } else {
+    auto kern = fft_line_fused_kernel<LOG2L, INV>;
+    FLB_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Q::SMEM));
+    kern<<<grid, Q::THREADS, Q::SMEM, s>>>(src, dst, P, m2, tw, NdctTrPack{});
+  }
   note_launch("fft_line_fused_kernel");
 }
 
@@ -460,17 +480,17 @@ void line_pass(int log2l, const LineIO& io, unsigned long long P, size_t items, 
 
 template <bool INV>
 void line_pass(int log2l, const double2* src, double2* dst, unsigned long long P, size_t items,
-               const LineMap& mp, cudaStream_t s) {
-  if (FLB_FFT_FUSED) {
+               const LineMap& mp, cudaStream_t s, const NdctTrPack* pk = nullptr) {
+  if (FLB_FFT_FUSED || pk) {
     switch (log2l) {
-      case 5: launch_line_fused<5, INV>(src, dst, P, items, mp, s); return;
-      case 6: launch_line_fused<6, INV>(src, dst, P, items, mp, s); return;
-      case 7: launch_line_fused<7, INV>(src, dst, P, items, mp, s); return;
-      case 8: launch_line_fused<8, INV>(src, dst, P, items, mp, s); return;
-      case 9: launch_line_fused<9, INV>(src, dst, P, items, mp, s); return;
-      case 10: launch_line_fused<10, INV>(src, dst, P, items, mp, s); return;
-      case 11: launch_line_fused<11, INV>(src, dst, P, items, mp, s); return;
-      case 12: launch_line_fused<12, INV>(src, dst, P, items, mp, s); return;
+      case 5: launch_line_fused<5, INV>(src, dst, P, items, mp, s, pk); return;
+      case 6: launch_line_fused<6, INV>(src, dst, P, items, mp, s, pk); return;
+      case 7: launch_line_fused<7, INV>(src, dst, P, items, mp, s, pk); return;
+      case 8: launch_line_fused<8, INV>(src, dst, P, items, mp, s, pk); return;
+      case 9: launch_line_fused<9, INV>(src, dst, P, items, mp, s, pk); return;
+      case 10: launch_line_fused<10, INV>(src, dst, P, items, mp, s, pk); return;
+      case 11: launch_line_fused<11, INV>(src, dst, P, items, mp, s, pk); return;
+      case 12: launch_line_fused<12, INV>(src, dst, P, items, mp, s, pk); return;
       default: fail(FL_RUNTIME_ERROR, "fft: unsupported line length");
     }
   }
@@ -764,6 +784,31 @@ void fft_pow2(double2* data, double2* scratch, int log2p, size_t batch, bool inv
     else
       fft_multipass<false>(data + b0 * P, scratch + b0 * P, log2p, nb, s);
   }
+}
+
+template <bool INV>
+void ndct_tr_pack_multipass(double2* d, double2* t, int log2p, const NdctTrPack& a, cudaStream_t s) {
+  const unsigned long long P = 1ull << log2p;
+  const PassPlan pp(log2p);
+  const size_t items = (size_t)a.nt * a.nc;
+  if (items > 65535) fail(FL_RUNTIME_ERROR, "fft: fused pack: too many rows");
+  if (pp.passes == 2) {
+    line_pass<INV>(pp.lc, d, t, P, items, pp.col(), s, &a);
+  } else {
+    line_pass<INV>(pp.l2, d, d, P, items, pp.col1(), s, &a);
+    line_pass<INV>(pp.l1, d, t, P, items, pp.col2(), s);
+  }
+  line_pass<INV>(pp.lr, t, d, P, items, LineMap{1, pp.R, 1, 1, pp.C, 0, 0, 0, 0}, s);
+}
+
+void fft_pow2_ndct_tr_pack(double2* data, double2* scratch, int log2p, bool inverse,
+                           const NdctTrPack& a, cudaStream_t s) {
+  if (log2p <= kMaxSmemLog2 || log2p > kMaxLog2) fail(FL_RUNTIME_ERROR, "fft: fused pack: length");
+  if (a.nc == 0 || a.nt == 0) return;
+  if (inverse)
+    ndct_tr_pack_multipass<true>(data, scratch, log2p, a, s);
+  else
+    ndct_tr_pack_multipass<false>(data, scratch, log2p, a, s);
 }
 
 bool fft_pow2_ndct_unpack_ok(int log2p) {

@@ -37,6 +37,18 @@ struct NdctUnpack {
   size_t ld, nc;
   int nt, first;      // first: store, else add to out
 };
+// The transposed direction's counterpart: the pack fused into the first pass's
+// loads. Row tz * nc + col of the transform is wp[tz][m] (.) G[col][m]
+// (componentwise: real part with real part), G the column's weighted input in
+// packed-entry order; the packed rows are never written or read.
+struct NdctTrPack {
+  const double2* wp;  // [nt][P]
+  const double2* G;   // [nc][P]
+  size_t nc;
+  int nt;
+};
+void fft_pow2_ndct_tr_pack(double2* data, double2* scratch, int log2p, bool inverse,
+                           const NdctTrPack& a, cudaStream_t s);
 bool fft_pow2_ndct_unpack_ok(int log2p);
 void fft_pow2_ndct_unpack(double2* data, double2* scratch, int log2p, bool inverse,
                           const NdctUnpack& a, cudaStream_t s);
