@@ -486,7 +486,8 @@ def sub_configs(args, dist, rank: int, world: int, local: int) -> dict:
             sweep.append(r)
         out["c3"] = {"workload": CONFIGS["c3"][3] + ", sweep 2^10..2^20", "sweep": sweep}
         # the two fast conversions timed against each other (north-star subsystem 2)
-        out["leg2cheb_methods"] = {"2^20": conversions(1 << 20, 5), "2^26": conversions(1 << 26, 2)}
+        out["leg2cheb_methods"] = {"2^17": conversions(1 << 17, 20), "2^20": conversions(1 << 20, 5),
+                                   "2^26": conversions(1 << 26, 2)}
 
     # C5: one 2^26 vector; term-parallel over the ranks (all ranks take part)
     n = CONFIGS["c5"][0]
