@@ -320,8 +320,12 @@ __global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
 // (its passes were L1/shared-memory-bound: 87-96 % l1tex throughput).
 // Threads are laid out line-minor for column passes (consecutive threads:
 // consecutive lines, LINES x 16 B runs) and element-minor for row passes.
+#ifndef FLB_LINE_MIN_CTAS_512
+#define FLB_LINE_MIN_CTAS_512 2
+#endif
 template <int LOG2L, bool INV, bool PK = false>
-__global__ void __launch_bounds__(LinePass<LOG2L>::THREADS)
+__global__ void __launch_bounds__(LinePass<LOG2L>::THREADS,
+                                  LinePass<LOG2L>::THREADS == 512 ? FLB_LINE_MIN_CTAS_512 : 0)
     fft_line_fused_kernel(const double2* __restrict__ src, double2* __restrict__ dst,
                           unsigned long long P, LineMap mp, const double2* __restrict__ tw,
                           NdctTrPack pk = NdctTrPack{}) {
