@@ -848,11 +848,16 @@ L2CAsy* l2c_asy_create(size_t n, const double* s, cudaStream_t st, int M, int R,
   // recurrence bands: [0, pb[L]) to N, then level L-1 ... 0
   RecTab& rt = f->rt;
   rt.nb = 0;
-  // chains of up to chain_cap steps run whole: long enough that few bands
-  // need the transfer-matrix pass, short enough for enough warps per SM
-  // sub-partition (a 65536-step chain alone runs ~40 cycles per step)
-  long long chain_cap = 4096;
-  while (chain_cap < 65536 && chain_cap * 64 < N) chain_cap *= 2;
+  // chains of up to chain_cap steps run whole, longer ones in chunks of it.
+  // A chain is sequential (~36 cycles per step: one 16384-step chain alone is
+  // 0.3 ms), and the chunks' start states are kept by the plan, so chunking
+  // costs nothing per call: short chunks up to 2^22 (N / 256 in [1024, 8192]:
+  // 2^17 0.273 -> 0.251 ms, 2^20 1.62 -> 1.50, 2^22 6.98 -> 6.35 forward),
+  // 65536 above (2^24, 2^26: no difference between 8192 and 65536; fewer
+  // start-state slots). FLB_ASY_CHAIN overrides.
+  long long chain_cap = N < (1ll << 23) ? std::min<long long>(8192, std::max<long long>(1024, N / 256))
+                                        : 65536;
+  if (env_int("FLB_ASY_CHAIN", 0) > 0) chain_cap = (env_int("FLB_ASY_CHAIN", 0) + 31) / 32 * 32;
   long long wb = 0, xb = 0, ib = 0, gb = 0, rb = 0;
   auto add_band = [&](long long p0, long long p1, long long nu) {
     if (p1 <= p0) return;
