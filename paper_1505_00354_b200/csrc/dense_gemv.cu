@@ -97,36 +97,28 @@ __global__ void gemv_transpose_kernel(const double* __restrict__ table, size_t n
   }
 }
 
-// u_par[k] = w_k (f_k +- f_{N-1-k}) (k < N/2), per column: [col][2][r]
-__global__ void gemv_idlt_prep_kernel(const double* __restrict__ in, size_t ld_in,
-                                      const double* __restrict__ wq, size_t n, size_t cols,
-                                      double* __restrict__ u, int* nonfinite) {
-  const size_t r = n / 2;
-  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (i >= r * cols) return;
-  const size_t col = i / r, k = i - col * r;
-  const double* f = in + col * ld_in;
-  const double a = f[k], b = f[n - 1 - k], wk = wq[k], wb = wq[n - 1 - k];
-  if (nonfinite && (!isfinite(a * wk) || !isfinite(b * wb))) atomicOr(nonfinite, 1);
-  // w is symmetric (w_{N-1-k} = w_k), so w_k (f_k +- f_{N-1-k}) is the
-  // reference's (w f)_k +- (w f)_{N-1-k}
-  u[(col * 2 + 0) * r + k] = wk * a + wb * b;
-  u[(col * 2 + 1) * r + k] = wk * a - wb * b;
-}
-
 // Transposed: one warp per degree m; lanes stride the nodes k (row m of the
-// table is contiguous), a shuffle reduction, c_m = (m + 1/2) sum.
+// table is contiguous), a shuffle reduction, c_m = (m + 1/2) sum. The input
+// u_par[k] = w_k f_k +- w_{N-1-k} f_{N-1-k} (the reference's (w f)_k +-
+// (w f)_{N-1-k}) is formed from the column as it is read (the values are
+// L1 / L2 hits beside the table stream; a separate pass cost an allocation
+// and a launch per call). The warp of m = 0 checks every input entry.
 __global__ void __launch_bounds__(32 * kRows) gemv_idlt_kernel(const double* __restrict__ table, size_t n,
-                                                               const double* __restrict__ u, double* __restrict__ out,
-                                                               size_t ld_out, size_t cols) {
+                                                               const double* __restrict__ in, size_t ld_in,
+                                                               const double* __restrict__ wq,
+                                                               double* __restrict__ out, size_t ld_out,
+                                                               size_t cols, int* nonfinite) {
   const size_t r = n / 2;
   const int lane = threadIdx.x & 31;
   const size_t m = blockIdx.x * (size_t)kRows + (threadIdx.x >> 5);
   if (m >= n) return;
   const size_t c0 = blockIdx.y * (size_t)kCB;
   const int nc = (int)std::min<size_t>(kCB, cols - c0);
-  const int par = (int)(m & 1);
+  const bool odd = (m & 1) != 0;
+  const bool check = m == 0;
+  bool bad = false;
   const double* row = table + m * r;
+  const double* fin = in + c0 * ld_in;
   double acc[kCB];
 #pragma unroll
   for (int j = 0; j < kCB; ++j) acc[j] = 0.0;
@@ -142,13 +134,20 @@ __global__ void __launch_bounds__(32 * kRows) gemv_idlt_kernel(const double* __r
     for (int q = 0; q < kU; ++q) {
       const size_t k = k0 + 32 * q;
       if (k >= r) break;
+      const double wk = __ldg(wq + k), wb = __ldg(wq + (n - 1 - k));
 #pragma unroll
       for (int j = 0; j < kCB; ++j) {
         if (j >= nc) break;
-        acc[j] = __fma_rn(p[q], __ldg(u + ((c0 + j) * 2 + par) * r + k), acc[j]);
+        const double a = __ldg(fin + j * ld_in + k), b = __ldg(fin + j * ld_in + (n - 1 - k));
+        // rounded products, then the sum (as the reference forms (w f)_k first)
+        const double wa = __dmul_rn(wk, a), wbb = __dmul_rn(wb, b);
+        if (check) bad |= !isfinite(wa) || !isfinite(wbb);
+        const double u = odd ? __dsub_rn(wa, wbb) : __dadd_rn(wa, wbb);
+        acc[j] = __fma_rn(p[q], u, acc[j]);
       }
     }
   }
+  if (bad && nonfinite) atomicOr(nonfinite, 1);
 #pragma unroll
   for (int j = 0; j < kCB; ++j) {
     double v = acc[j];
@@ -199,16 +198,10 @@ void dense_gemv_dlt(const DenseGemv& g, const double* in, size_t ld_in, double* 
 void dense_gemv_idlt(const DenseGemv& g, const double* in, size_t ld_in, const double* w, double* out,
                      size_t ld_out, size_t cols, int* nonfinite, cudaStream_t st) {
   if (cols == 0) return;
-  const size_t n = g.n, r = n / 2;
-  double* u = nullptr;
-  FLB_CUDA(cudaMallocAsync(&u, 2 * r * cols * sizeof(double), st));
-  gemv_idlt_prep_kernel<<<(unsigned)((r * cols + 255) / 256), 256, 0, st>>>(in, ld_in, w, n, cols, u,
-                                                                             nonfinite);
-  note_launch("gemv_idlt_prep_kernel");
+  const size_t n = g.n;
   const dim3 grid((unsigned)((n + kRows - 1) / kRows), (unsigned)((cols + kCB - 1) / kCB));
-  gemv_idlt_kernel<<<grid, 32 * kRows, 0, st>>>(g.table, n, u, out, ld_out, cols);
+  gemv_idlt_kernel<<<grid, 32 * kRows, 0, st>>>(g.table, n, in, ld_in, w, out, ld_out, cols, nonfinite);
   note_launch("gemv_idlt_kernel");
-  cudaFreeAsync(u, st);
 }
 
 }  // namespace flb

@@ -79,8 +79,10 @@ def run(name, reps):
     rt = float((z - x).abs().max() / x.abs().max())
     return {"config": desc, "plan_s": t_plan, "dlt_ms": dlt, "idlt_ms": idlt,
             "dlt_coeffs_per_s": n / dlt * 1e3, "idlt_coeffs_per_s": n / idlt * 1e3,
-            "leg2cheb": "toeplitz-hankel" if cfg.leg2cheb_rank(0) else "direct",
-            "leg2cheb_rank": [cfg.leg2cheb_rank(0), cfg.leg2cheb_rank(1)], "round_trip_rel": rt}
+            "leg2cheb": ("asymptotic expansion " + json.dumps(cfg.leg2cheb_asy_info())
+                         if n >= (1 << 17) and n & (n - 1) == 0
+                         else "toeplitz-hankel" if cfg.leg2cheb_rank(0) else "direct"),
+            "round_trip_rel": rt}
 
 
 def main():
