@@ -26,9 +26,12 @@ constexpr int kCB = 4;      // columns per pass (each table entry read once per 
 constexpr int kRows = 8;    // table rows (one per warp) per CTA
 
 // Forward: one warp per node k over the transposed table (row k = P_m(x_k),
-// m < N, contiguous): lanes stride the degrees, so even lanes sum the even
-// degrees (E) and odd lanes the odd ones (O); parity-preserving shuffles
-// combine them (fixed order: bit-reproducible).
+// m < N, contiguous, 16-byte aligned as N is even): a lane reads the entries
+// of two consecutive degrees at once (128-bit loads, 8 entries in flight per
+// lane: the 8-byte version reached 2.1 TB/s on the 256 MiB table of N = 8192),
+// sums the even degrees (E) and the odd ones (O) separately, and two shuffle
+// reductions combine the lanes (fixed order: bit-reproducible). The column
+// entries are read by 8-byte loads (any alignment of the caller's pointer).
 __global__ void __launch_bounds__(32 * kRows) gemv_dlt_kernel(const double* __restrict__ table_t, size_t n,
                                                               const double* __restrict__ in, size_t ld_in,
                                                               double* __restrict__ out, size_t ld_out,
@@ -39,44 +42,47 @@ __global__ void __launch_bounds__(32 * kRows) gemv_dlt_kernel(const double* __re
   if (k >= r) return;
   const size_t c0 = blockIdx.y * (size_t)kCB;
   const int nc = (int)std::min<size_t>(kCB, cols - c0);
-  const double* row = table_t + k * n;
+  const double2* row = reinterpret_cast<const double2*>(table_t + k * n);
   const double* cin = in + c0 * ld_in;
-  double acc[kCB];
+  double ev[kCB], od[kCB];
 #pragma unroll
-  for (int j = 0; j < kCB; ++j) acc[j] = 0.0;
+  for (int j = 0; j < kCB; ++j) ev[j] = od[j] = 0.0;
   bool bad = false;
   const bool check = k == 0;  // one warp checks every input entry
-  constexpr int kU = 8;       // table entries in flight per lane
-  for (size_t m0 = lane; m0 < n; m0 += 32 * kU) {
-    double p[kU];
+  constexpr int kU = 4;       // 128-bit table loads in flight per lane
+  for (size_t h0 = lane; h0 < r; h0 += 32 * kU) {  // h: degree pair (2h, 2h + 1)
+    double2 p[kU];
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      const size_t m = m0 + 32 * q;
-      p[q] = m < n ? __ldg(row + m) : 0.0;
+      const size_t h = h0 + 32 * q;
+      p[q] = h < r ? __ldg(row + h) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int q = 0; q < kU; ++q) {
-      const size_t m = m0 + 32 * q;
-      if (m >= n) break;
+      const size_t h = h0 + 32 * q;
+      if (h >= r) break;
 #pragma unroll
       for (int j = 0; j < kCB; ++j) {
         if (j >= nc) break;
-        const double cm = __ldg(cin + j * ld_in + m);
-        if (check) bad |= !isfinite(cm);
-        acc[j] = __fma_rn(p[q], cm, acc[j]);
+        const double ce = __ldg(cin + j * ld_in + 2 * h), co = __ldg(cin + j * ld_in + 2 * h + 1);
+        if (check) bad |= !isfinite(ce) || !isfinite(co);
+        ev[j] = __fma_rn(p[q].x, ce, ev[j]);
+        od[j] = __fma_rn(p[q].y, co, od[j]);
       }
     }
   }
   if (bad && nonfinite) atomicOr(nonfinite, 1);
 #pragma unroll
   for (int j = 0; j < kCB; ++j) {
-    double v = acc[j];
-    for (int o = 16; o >= 2; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);  // lane parity kept
-    const double odd = __shfl_sync(0xffffffffu, v, 1);
+    double e = ev[j], o = od[j];
+    for (int sh = 16; sh > 0; sh >>= 1) {
+      e += __shfl_xor_sync(0xffffffffu, e, sh);
+      o += __shfl_xor_sync(0xffffffffu, o, sh);
+    }
     if (lane == 0 && j < nc) {
       double* f = out + (c0 + j) * ld_out;
-      f[k] = v + odd;
-      f[n - 1 - k] = v - odd;
+      f[k] = e + o;
+      f[n - 1 - k] = e - o;
     }
   }
 }
@@ -97,15 +103,35 @@ __global__ void gemv_transpose_kernel(const double* __restrict__ table, size_t n
   }
 }
 
+// u_par[k] = w_k f_k +- w_{N-1-k} f_{N-1-k} (k < N/2), per column: [col][2][r]
+// (rounded products, then the sum: the reference's (w f)_k +- (w f)_{N-1-k})
+__global__ void gemv_idlt_prep_kernel(const double* __restrict__ in, size_t ld_in,
+                                      const double* __restrict__ wq, size_t n, size_t cols,
+                                      double* __restrict__ u, int* nonfinite) {
+  const size_t r = n / 2;
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= r * cols) return;
+  const size_t col = i / r, k = i - col * r;
+  const double* f = in + col * ld_in;
+  const double wa = __dmul_rn(wq[k], f[k]), wbb = __dmul_rn(wq[n - 1 - k], f[n - 1 - k]);
+  if (nonfinite && (!isfinite(wa) || !isfinite(wbb))) atomicOr(nonfinite, 1);
+  u[(col * 2 + 0) * r + k] = __dadd_rn(wa, wbb);
+  u[(col * 2 + 1) * r + k] = __dsub_rn(wa, wbb);
+}
+
 // Transposed: one warp per degree m; lanes stride the nodes k (row m of the
-// table is contiguous), a shuffle reduction, c_m = (m + 1/2) sum. The input
-// u_par[k] = w_k f_k +- w_{N-1-k} f_{N-1-k} (the reference's (w f)_k +-
-// (w f)_{N-1-k}) is formed from the column as it is read (the values are
-// L1 / L2 hits beside the table stream; a separate pass cost an allocation
-// and a launch per call). The warp of m = 0 checks every input entry.
+// table is contiguous), a shuffle reduction, c_m = (m + 1/2) sum.
+// INLINE (short single columns, C1): u is formed from the column as it is
+// read, which saves the prep launch and its scratch allocation (N = 1024:
+// 31 -> 18 us per call) but repeats the products in every warp (N = 8192:
+// 88 -> 120 us, so larger sizes keep the prep pass). The warp of m = 0 then
+// checks every input entry.
+// VEC: N/2 even, rows 16-byte aligned: 128-bit table loads (two nodes per lane).
+template <bool VEC, bool INLINE>
 __global__ void __launch_bounds__(32 * kRows) gemv_idlt_kernel(const double* __restrict__ table, size_t n,
                                                                const double* __restrict__ in, size_t ld_in,
                                                                const double* __restrict__ wq,
+                                                               const double* __restrict__ uu,
                                                                double* __restrict__ out, size_t ld_out,
                                                                size_t cols, int* nonfinite) {
   const size_t r = n / 2;
@@ -115,35 +141,71 @@ __global__ void __launch_bounds__(32 * kRows) gemv_idlt_kernel(const double* __r
   const size_t c0 = blockIdx.y * (size_t)kCB;
   const int nc = (int)std::min<size_t>(kCB, cols - c0);
   const bool odd = (m & 1) != 0;
-  const bool check = m == 0;
+  const bool check = INLINE && m == 0;
   bool bad = false;
   const double* row = table + m * r;
-  const double* fin = in + c0 * ld_in;
+  const double* fin = INLINE ? in + c0 * ld_in : nullptr;
+  const double* up = INLINE ? nullptr : uu + (c0 * 2 + (odd ? 1 : 0)) * r;  // column j: + 2 j r
   double acc[kCB];
 #pragma unroll
   for (int j = 0; j < kCB; ++j) acc[j] = 0.0;
-  constexpr int kU = 8;
-  for (size_t k0 = lane; k0 < r; k0 += 32 * kU) {
-    double p[kU];
+  // u_k of column j: rounded products, then the sum (as the reference forms (w f)_k first)
+  auto u_of = [&](int j, size_t k, double wk, double wb) {
+    if constexpr (!INLINE) return __ldg(up + 2 * (size_t)j * r + k);
+    const double a = __ldg(fin + j * ld_in + k), b = __ldg(fin + j * ld_in + (n - 1 - k));
+    const double wa = __dmul_rn(wk, a), wbb = __dmul_rn(wb, b);
+    if (check) bad |= !isfinite(wa) || !isfinite(wbb);
+    return odd ? __dsub_rn(wa, wbb) : __dadd_rn(wa, wbb);
+  };
+  if constexpr (VEC) {
+    constexpr int kU = 4;
+    const double2* row2 = reinterpret_cast<const double2*>(row);
+    double acc2[kCB];
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const size_t k = k0 + 32 * q;
-      p[q] = k < r ? __ldg(row + k) : 0.0;
+    for (int j = 0; j < kCB; ++j) acc2[j] = 0.0;
+    for (size_t h0 = lane; h0 < r / 2; h0 += 32 * kU) {  // h: node pair (2h, 2h + 1)
+      double2 p[kU];
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        const size_t h = h0 + 32 * q;
+        p[q] = h < r / 2 ? __ldg(row2 + h) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        const size_t h = h0 + 32 * q;
+        if (h >= r / 2) break;
+        const size_t k = 2 * h;
+        const double wk0 = INLINE ? __ldg(wq + k) : 0.0, wb0 = INLINE ? __ldg(wq + (n - 1 - k)) : 0.0;
+        const double wk1 = INLINE ? __ldg(wq + k + 1) : 0.0, wb1 = INLINE ? __ldg(wq + (n - 2 - k)) : 0.0;
+#pragma unroll
+        for (int j = 0; j < kCB; ++j) {
+          if (j >= nc) break;
+          acc[j] = __fma_rn(p[q].x, u_of(j, k, wk0, wb0), acc[j]);
+          acc2[j] = __fma_rn(p[q].y, u_of(j, k + 1, wk1, wb1), acc2[j]);
+        }
+      }
     }
 #pragma unroll
-    for (int q = 0; q < kU; ++q) {
-      const size_t k = k0 + 32 * q;
-      if (k >= r) break;
-      const double wk = __ldg(wq + k), wb = __ldg(wq + (n - 1 - k));
+    for (int j = 0; j < kCB; ++j) acc[j] += acc2[j];
+  } else {
+    constexpr int kU = 8;
+    for (size_t k0 = lane; k0 < r; k0 += 32 * kU) {
+      double p[kU];
 #pragma unroll
-      for (int j = 0; j < kCB; ++j) {
-        if (j >= nc) break;
-        const double a = __ldg(fin + j * ld_in + k), b = __ldg(fin + j * ld_in + (n - 1 - k));
-        // rounded products, then the sum (as the reference forms (w f)_k first)
-        const double wa = __dmul_rn(wk, a), wbb = __dmul_rn(wb, b);
-        if (check) bad |= !isfinite(wa) || !isfinite(wbb);
-        const double u = odd ? __dsub_rn(wa, wbb) : __dadd_rn(wa, wbb);
-        acc[j] = __fma_rn(p[q], u, acc[j]);
+      for (int q = 0; q < kU; ++q) {
+        const size_t k = k0 + 32 * q;
+        p[q] = k < r ? __ldg(row + k) : 0.0;
+      }
+#pragma unroll
+      for (int q = 0; q < kU; ++q) {
+        const size_t k = k0 + 32 * q;
+        if (k >= r) break;
+        const double wk = INLINE ? __ldg(wq + k) : 0.0, wb = INLINE ? __ldg(wq + (n - 1 - k)) : 0.0;
+#pragma unroll
+        for (int j = 0; j < kCB; ++j) {
+          if (j >= nc) break;
+          acc[j] = __fma_rn(p[q], u_of(j, k, wk, wb), acc[j]);
+        }
       }
     }
   }
@@ -198,10 +260,24 @@ void dense_gemv_dlt(const DenseGemv& g, const double* in, size_t ld_in, double* 
 void dense_gemv_idlt(const DenseGemv& g, const double* in, size_t ld_in, const double* w, double* out,
                      size_t ld_out, size_t cols, int* nonfinite, cudaStream_t st) {
   if (cols == 0) return;
-  const size_t n = g.n;
+  const size_t n = g.n, r = n / 2;
   const dim3 grid((unsigned)((n + kRows - 1) / kRows), (unsigned)((cols + kCB - 1) / kCB));
-  gemv_idlt_kernel<<<grid, 32 * kRows, 0, st>>>(g.table, n, in, ld_in, w, out, ld_out, cols, nonfinite);
+  const bool vec = r % 2 == 0;
+  if (n <= 2048 && cols <= (size_t)kCB) {  // short single columns: no prep pass
+    auto kern = vec ? gemv_idlt_kernel<true, true> : gemv_idlt_kernel<false, true>;
+    kern<<<grid, 32 * kRows, 0, st>>>(g.table, n, in, ld_in, w, nullptr, out, ld_out, cols, nonfinite);
+    note_launch("gemv_idlt_kernel");
+    return;
+  }
+  double* u = nullptr;
+  FLB_CUDA(cudaMallocAsync(&u, 2 * r * cols * sizeof(double), st));
+  gemv_idlt_prep_kernel<<<(unsigned)((r * cols + 255) / 256), 256, 0, st>>>(in, ld_in, w, n, cols, u,
+                                                                             nonfinite);
+  note_launch("gemv_idlt_prep_kernel");
+  auto kern = vec ? gemv_idlt_kernel<true, false> : gemv_idlt_kernel<false, false>;
+  kern<<<grid, 32 * kRows, 0, st>>>(g.table, n, nullptr, 0, nullptr, u, out, ld_out, cols, nonfinite);
   note_launch("gemv_idlt_kernel");
+  cudaFreeAsync(u, st);
 }
 
 }  // namespace flb

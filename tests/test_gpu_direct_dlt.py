@@ -120,7 +120,7 @@ def test_direct_zero_and_scaled_columns():
     assert np.array_equal(f[4], f[6] * 2.0 ** -600) and np.array_equal(f[5], f[6] * 2.0 ** 600)
 
 
-@pytest.mark.parametrize("n", [256, 300, 512, 1000, 1024, 2048, 4096, 8192])
+@pytest.mark.parametrize("n", [256, 258, 300, 512, 1000, 1002, 1024, 2048, 4096, 8192])
 @pytest.mark.parametrize("kind", [CHEB1, CHEBSTAR])
 def test_direct_few_columns_fp64_table(n, kind):
     """<= 16 columns (C1 and the C3 sweep up to 8192): the direct method as
