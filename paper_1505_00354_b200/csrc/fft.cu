@@ -513,12 +513,19 @@ void line_pass(int log2l, const double2* src, double2* dst, unsigned long long P
 #ifndef FLB_FFT_2PASS_MAX
 #define FLB_FFT_2PASS_MAX 20
 #endif
+#ifndef FLB_FFT_ROW_CEIL
+#define FLB_FFT_ROW_CEIL 0  // 1: every odd log2p gives the longer line to the row pass
+#endif
+// (by default only 2^19: 512-point column lines, eight per CTA = 128-byte
+// runs, and 1024-point contiguous rows instead of 1024-point columns in
+// 64-byte runs: N = 2^20 DLT 1.74 -> 1.58 ms; at 2^15 and 2^17 the shorter
+// row line wins: C2 0.495 vs 0.507 ms, 2^18 DLT 0.465 vs 0.484 ms)
 struct PassPlan {
   int passes, lr, lc, l1, l2;
   unsigned long long R, C, C1, C2;
   explicit PassPlan(int log2p) {
     passes = (log2p <= FLB_FFT_2PASS_MAX || log2p < 15) ? 2 : 3;
-    lr = passes == 2 ? log2p / 2 : log2p / 3;
+    lr = passes == 2 ? (log2p + (FLB_FFT_ROW_CEIL || log2p == 19)) / 2 : log2p / 3;
     lc = log2p - lr;
     l1 = lc / 2;
     l2 = lc - l1;
