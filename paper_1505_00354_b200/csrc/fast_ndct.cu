@@ -2519,18 +2519,32 @@ FastNdct* fast_ndct_create_literal(size_t n, int kind, int num_terms, const doub
 __global__ void fast_delta_kernel(size_t n, int kind, const double* __restrict__ delta,
                                   double* __restrict__ out, unsigned long long* amax) {
   const size_t k = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
-  if (k >= n) return;
-  const double d = delta ? delta[k] : 0.0;
-  double off = 0.0;
-  if (kind == FL_CHEBSTAR) {
-    const double nd = (double)n;
-    off = (double)((long long)n - 2 * (long long)k - 1) * (kPi / (2.0 * nd * (2.0 * nd + 1.0)));
+  double d = 0.0, dp = 0.0;
+  if (k < n) {
+    d = delta ? delta[k] : 0.0;
+    double off = 0.0;
+    if (kind == FL_CHEBSTAR) {
+      const double nd = (double)n;
+      off = (double)((long long)n - 2 * (long long)k - 1) * (kPi / (2.0 * nd * (2.0 * nd + 1.0)));
+    }
+    dp = d + off;
+    out[k] = dp;
   }
-  const double dp = d + off;
-  out[k] = dp;
   if (amax) {
-    atomicMax(&amax[0], (unsigned long long)__double_as_longlong(fabs(d)));
-    atomicMax(&amax[1], (unsigned long long)__double_as_longlong(fabs(dp)));
+    // one atomic pair per warp (one per thread serialised on the two
+    // addresses: 91 us at N = 65536); a NaN offset has the largest bit pattern
+    unsigned long long a = (unsigned long long)__double_as_longlong(fabs(d));
+    unsigned long long b = (unsigned long long)__double_as_longlong(fabs(dp));
+    for (int o = 16; o > 0; o >>= 1) {
+      const unsigned long long a2 = __shfl_xor_sync(0xffffffffu, a, o);
+      const unsigned long long b2 = __shfl_xor_sync(0xffffffffu, b, o);
+      a = a2 > a ? a2 : a;
+      b = b2 > b ? b2 : b;
+    }
+    if ((threadIdx.x & 31) == 0) {
+      atomicMax(&amax[0], a);
+      atomicMax(&amax[1], b);
+    }
   }
 }
 
