@@ -35,11 +35,14 @@ def _repeat(fn, out, reps=12):
     return first
 
 
-@pytest.mark.parametrize("n", [1024, 4096, 8192, 65536])
+@pytest.mark.parametrize("n", [1024, 4096, 8192, 65536, 1 << 18, 1 << 20])
 def test_hot_kernels_bit_reproducible(n):
+    # 65536 / 2^18 / 2^20: the multi-pass NDCT with its fused row-pass unpack
+    # (row lines of 2^7 / 2^8 / 2^10 points) and fused first-pass pack, the
+    # asymptotic conversion from 2^18
     import torch
     cfg = fl.TransformConfig(n)
-    cols = {1024: 300, 4096: 300, 8192: 64, 65536: 8}[n]
+    cols = {1024: 300, 4096: 300, 8192: 64, 65536: 8, 1 << 18: 3, 1 << 20: 2}[n]
     x = torch.from_numpy(fl.random_uniform_pm1(n, 77, batch=cols)).cuda()
     y = torch.empty_like(x)
     noise = torch.empty_like(x)
@@ -60,3 +63,17 @@ def test_hot_kernels_bit_reproducible(n):
         _repeat(run(lambda: _lib.LIB.fl_trig(op, 0, n, vp(x.data_ptr()), vp(y.data_ptr()), cols, n, s)), y)
     _repeat(run(lambda: _lib.LIB.fl_dlt(cfg.handle, vp(x.data_ptr()), vp(y.data_ptr()), cols, n, s)), y)
     _repeat(run(lambda: _lib.LIB.fl_idlt(cfg.handle, vp(x.data_ptr()), vp(y.data_ptr()), cols, n, s)), y)
+
+
+@pytest.mark.parametrize("n", [1024, 2048, 8192])
+@pytest.mark.parametrize("cols", [1, 3])
+def test_few_column_direct_bit_reproducible(n, cols):
+    """The single-column direct DLT / IDLT (dense_gemv.cu: 128-bit table loads,
+    the IDLT's input formed in the kernel for N <= 2048)."""
+    import torch
+    cfg = fl.TransformConfig(n)
+    x = torch.from_numpy(fl.random_uniform_pm1(n, 78, batch=cols)).cuda()
+    y = torch.empty_like(x)
+    s = vp(torch.cuda.current_stream().cuda_stream)
+    _repeat(lambda: _lib.check(_lib.LIB.fl_dlt(cfg.handle, vp(x.data_ptr()), vp(y.data_ptr()), cols, n, s)), y)
+    _repeat(lambda: _lib.check(_lib.LIB.fl_idlt(cfg.handle, vp(x.data_ptr()), vp(y.data_ptr()), cols, n, s)), y)
