@@ -2170,21 +2170,25 @@ __device__ __forceinline__ double big_tr_value(double2 za, double2 zc, double c2
   const double2 Vv = make_double2(ev.x + od.x * c2 - od.y * s2, ev.y + od.x * s2 + od.y * c2);
   return ch * Vv.x + sh * Vv.y;
 }
+// NC columns per thread (the twiddles and the row factors rt[t][r] are shared
+// by all columns: per column they were as much L2 traffic as the packed rows).
+template <int NC>
 __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, size_t nc, int l0,
                                      int nt, BigTerms bt, const double* __restrict__ rt,
                                      double* __restrict__ out, size_t ld, int first) {
   const size_t P = n / 2;
-  const size_t col = blockIdx.y;
+  const size_t col = blockIdx.y * (size_t)NC;
   const double nd = (double)n;
   for (size_t a = blockIdx.x * (size_t)blockDim.x + threadIdx.x; a <= P / 2;
        a += (size_t)gridDim.x * blockDim.x) {
     const size_t bq = (P - a) & (P - 1);
     const int nr = (a != 0 && a != P / 2) ? 4 : 2;
     const size_t r[4] = {a, P + a, P - a, 2 * P - a};
-    double c2[4], s2[4], ch[4], sh[4], acc[4];
+    double c2[4], s2[4], ch[4], sh[4], acc[NC][4];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      acc[e] = 0.0;
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) acc[cc][e] = 0.0;
       c2[e] = s2[e] = ch[e] = sh[e] = 0.0;
       if (e < nr) {
         sincospi(-2.0 * (double)r[e] / nd, &s2[e], &c2[e]);  // e^{-2 pi i r/N}
@@ -2194,7 +2198,12 @@ __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, si
     for (int t = 0; t < nt; ++t) {
       const int odd = big_odd(bt, l0 + t);
       const double2* Zc = Z + ((size_t)t * nc + col) * P;
-      const double2 za = Zc[a], zb = Zc[bq];
+      double2 za[NC], zb[NC];
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        za[cc] = Zc[(size_t)cc * P + a];
+        zb[cc] = Zc[(size_t)cc * P + bq];
+      }
       const double* rw = rt + (size_t)t * n;
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
@@ -2202,21 +2211,27 @@ __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, si
         // rows e >= 2 read the pair swapped; the DST^T rows use kk = N - r:
         // e^{-2 pi i kk/N} = conj, e^{i pi kk/(2N)} = i conj, and swap again
         const bool swp = (e >= 2) != (odd != 0);
-        const double2 p0 = swp ? zb : za, p1 = swp ? za : zb;
-        double x;
-        if (!odd)
-          x = big_tr_value(p0, p1, c2[e], s2[e], ch[e], sh[e]);
-        else
-          x = r[e] == 0 ? 0.0 : big_tr_value(p0, p1, c2[e], -s2[e], sh[e], ch[e]);
-        acc[e] = __fma_rn(rw[r[e]], x, acc[e]);
+        const double w = rw[r[e]];
+#pragma unroll
+        for (int cc = 0; cc < NC; ++cc) {
+          const double2 p0 = swp ? zb[cc] : za[cc], p1 = swp ? za[cc] : zb[cc];
+          double x;
+          if (!odd)
+            x = big_tr_value(p0, p1, c2[e], s2[e], ch[e], sh[e]);
+          else
+            x = r[e] == 0 ? 0.0 : big_tr_value(p0, p1, c2[e], -s2[e], sh[e], ch[e]);
+          acc[cc][e] = __fma_rn(w, x, acc[cc][e]);
+        }
       }
     }
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      if (e >= nr) break;
-      double* o = out + col * ld + r[e];
-      *o = first ? acc[e] : *o + acc[e];
-    }
+    for (int cc = 0; cc < NC; ++cc)
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (e >= nr) break;
+        double* o = out + (col + cc) * ld + r[e];
+        *o = first ? acc[cc][e] : *o + acc[cc][e];
+      }
   }
 }
 
@@ -2238,6 +2253,9 @@ constexpr size_t kBigBudget = size_t(FLB_BIG_BUDGET_GIB) << 30;
 #define FLB_BIG_TABLE_CACHE_GIB 16
 #endif
 constexpr size_t kBigTableCache = size_t(FLB_BIG_TABLE_CACHE_GIB) << 30;
+#ifndef FLB_BIG_TR_COLS
+#define FLB_BIG_TR_COLS 2  // columns per thread of the transposed unpack
+#endif
 #ifndef FLB_BIG_FUSED_UNPACK
 #define FLB_BIG_FUSED_UNPACK 1
 #endif
@@ -2367,8 +2385,12 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
           note_launch("big_tr_pack_kernel");
           fft_pow2(Z, S, log2n - 1, nc * nt, false, s);
         }
-        big_tr_unpack_kernel<<<dim3(gxq, (unsigned)nc), 256, 0, s>>>(
-            Z, n, nc, l0, nt, bt, rt, out + c0 * ld_out, ld_out, first);
+        if (nc % FLB_BIG_TR_COLS == 0 && FLB_BIG_TR_COLS > 1)
+          big_tr_unpack_kernel<FLB_BIG_TR_COLS><<<dim3(gxq, (unsigned)(nc / FLB_BIG_TR_COLS)), 256, 0, s>>>(
+              Z, n, nc, l0, nt, bt, rt, out + c0 * ld_out, ld_out, first);
+        else
+          big_tr_unpack_kernel<1><<<dim3(gxq, (unsigned)nc), 256, 0, s>>>(
+              Z, n, nc, l0, nt, bt, rt, out + c0 * ld_out, ld_out, first);
         note_launch("big_tr_unpack_kernel");
       }
     }
