@@ -2044,19 +2044,30 @@ __global__ void big_wp_kernel(size_t n, int l0, int nt, BigTerms bt, const doubl
 // rt[t][j] c_j (the real-DCT packing of the file header). One thread per m for
 // every term: the four column entries and the three twiddles of m are read /
 // evaluated once (per term they were half the kernel's time at C2).
+// NC columns per thread: the twiddles and the stage factors rt[t][.] of m are
+// shared by all columns.
+template <int NC>
 __global__ void big_fwd_pack_kernel(const double* __restrict__ in, size_t ld, size_t n, size_t nc,
                                     int l0, int nt, BigTerms bt, const double* __restrict__ rt,
                                     double2* __restrict__ Z, int* nonfinite) {
   const size_t P = n / 2;
-  const size_t col = blockIdx.y;
+  const size_t col = blockIdx.y * (size_t)NC;
   const double* c = in + col * ld;
   const double nd = (double)n;
   for (size_t m = blockIdx.x * (size_t)blockDim.x + threadIdx.x; m < P;
        m += (size_t)gridDim.x * blockDim.x) {
     // stage indices: m, n - m (none for m = 0), m + P, P - m
-    const double c0 = c[m], c1 = m ? c[n - m] : 0.0, c2 = c[m + P], c3 = c[P - m];
-    if (nonfinite && l0 == 0) {
-      if (!isfinite(c0) || !isfinite(c2)) atomicOr(nonfinite, 1);
+    double c0[NC], c1[NC], c2[NC], c3[NC];
+#pragma unroll
+    for (int cc = 0; cc < NC; ++cc) {
+      const double* cq = c + (size_t)cc * ld;
+      c0[cc] = cq[m];
+      c1[cc] = m ? cq[n - m] : 0.0;
+      c2[cc] = cq[m + P];
+      c3[cc] = cq[P - m];
+      if (nonfinite && l0 == 0) {
+        if (!isfinite(c0[cc]) || !isfinite(c2[cc])) atomicOr(nonfinite, 1);
+      }
     }
     double sa, ca, sb, cb, s4, c4;
     sincospi((double)m / (2.0 * nd), &sa, &ca);        // e^{i pi m/(2N)}
@@ -2065,18 +2076,22 @@ __global__ void big_fwd_pack_kernel(const double* __restrict__ in, size_t ld, si
     for (int tz = 0; tz < nt; ++tz) {
       const int odd = big_odd(bt, l0 + tz);
       const double* rw = rt + (size_t)tz * n;
-      const double st0 = c0 * rw[m], st1 = m ? c1 * rw[n - m] : 0.0, st2 = c2 * rw[m + P],
-                   st3 = c3 * rw[P - m];
-      // DCT-III: X(0) = st(0), X(j) = st(j)/2; DST-III: X(0) = 0, X(j) = st(N - j)/2
-      const double xa = odd ? (m ? 0.5 * st1 : 0.0) : (m ? 0.5 * st0 : st0);
-      const double xan = m ? 0.5 * (odd ? st0 : st1) : 0.0;
-      const double xb = 0.5 * (odd ? st3 : st2), xbn = 0.5 * (odd ? st2 : st3);
-      const double2 Wa = make_double2(ca * xa + sa * xan, sa * xa - ca * xan);
-      const double2 Wb = make_double2(cb * xb + sb * xbn, sb * xb - cb * xbn);
-      const double2 sm = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
-      const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
-      const double2 dr = make_double2(d.x * c4 - d.y * s4, d.x * s4 + d.y * c4);
-      Z[((size_t)tz * nc + col) * P + m] = make_double2(sm.x - dr.y, sm.y + dr.x);
+      const double r0 = rw[m], r1 = m ? rw[n - m] : 0.0, r2 = rw[m + P], r3 = rw[P - m];
+#pragma unroll
+      for (int cc = 0; cc < NC; ++cc) {
+        const double st0 = c0[cc] * r0, st1 = m ? c1[cc] * r1 : 0.0, st2 = c2[cc] * r2,
+                     st3 = c3[cc] * r3;
+        // DCT-III: X(0) = st(0), X(j) = st(j)/2; DST-III: X(0) = 0, X(j) = st(N - j)/2
+        const double xa = odd ? (m ? 0.5 * st1 : 0.0) : (m ? 0.5 * st0 : st0);
+        const double xan = m ? 0.5 * (odd ? st0 : st1) : 0.0;
+        const double xb = 0.5 * (odd ? st3 : st2), xbn = 0.5 * (odd ? st2 : st3);
+        const double2 Wa = make_double2(ca * xa + sa * xan, sa * xa - ca * xan);
+        const double2 Wb = make_double2(cb * xb + sb * xbn, sb * xb - cb * xbn);
+        const double2 sm = make_double2(Wa.x + Wb.x, Wa.y + Wb.y);
+        const double2 d = make_double2(Wa.x - Wb.x, Wa.y - Wb.y);
+        const double2 dr = make_double2(d.x * c4 - d.y * s4, d.x * s4 + d.y * c4);
+        Z[((size_t)tz * nc + col + cc) * P + m] = make_double2(sm.x - dr.y, sm.y + dr.x);
+      }
     }
   }
 }
@@ -2253,6 +2268,9 @@ constexpr size_t kBigBudget = size_t(FLB_BIG_BUDGET_GIB) << 30;
 #define FLB_BIG_TABLE_CACHE_GIB 16
 #endif
 constexpr size_t kBigTableCache = size_t(FLB_BIG_TABLE_CACHE_GIB) << 30;
+#ifndef FLB_BIG_PACK_COLS
+#define FLB_BIG_PACK_COLS 2  // columns per thread of the forward pack (C2 0.501 -> 0.478 ms; 4: 0.483)
+#endif
 #ifndef FLB_BIG_TR_COLS
 #define FLB_BIG_TR_COLS 2  // columns per thread of the transposed unpack
 #endif
@@ -2360,8 +2378,12 @@ void launch_big(int log2n, int transpose, const double* in, size_t ld_in, double
       const size_t nc = batch - c0 < chunk ? batch - c0 : chunk;
       const int first = l0 == l_lo;
       if (!transpose) {
-        big_fwd_pack_kernel<<<dim3(gx, (unsigned)nc), 256, 0, s>>>(
-            in + c0 * ld_in, ld_in, n, nc, l0, nt, bt, rt, Z, nonfinite);
+        if (nc % FLB_BIG_PACK_COLS == 0 && FLB_BIG_PACK_COLS > 1)
+          big_fwd_pack_kernel<FLB_BIG_PACK_COLS><<<dim3(gx, (unsigned)(nc / FLB_BIG_PACK_COLS)), 256, 0, s>>>(
+              in + c0 * ld_in, ld_in, n, nc, l0, nt, bt, rt, Z, nonfinite);
+        else
+          big_fwd_pack_kernel<1><<<dim3(gx, (unsigned)nc), 256, 0, s>>>(
+              in + c0 * ld_in, ld_in, n, nc, l0, nt, bt, rt, Z, nonfinite);
         note_launch("big_fwd_pack_kernel");
         if (fused_unpack) {
           fft_pow2_ndct_unpack(Z, S, log2n - 1, true,
