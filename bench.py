@@ -410,7 +410,7 @@ def sub_configs(args, dist, rank: int, world: int, local: int) -> dict:
                      "round_trip_rel": rt}
 
     def l2c_method(cfg, n):
-        if n >= (1 << 17) and n & (n - 1) == 0:
+        if n >= (1 << 16) and n & (n - 1) == 0:
             return "asymptotic expansion " + json.dumps(cfg.leg2cheb_asy_info())
         return "toeplitz-hankel" if cfg.leg2cheb_rank(0) else "direct"
 

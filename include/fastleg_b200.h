@@ -166,7 +166,7 @@ int fl_free_ndct_mode(void);
  * and at most 16 columns:
  *   0 = FL_LEG2CHEB_DIRECT : the reference's O(N^2) triangular product;
  *   1 = FL_LEG2CHEB_FAST   : (default) the asymptotic expansion (mode 2) for
- *       power-of-two n >= 2^17, Toeplitz-Hankel (mode 3) otherwise;
+ *       power-of-two n >= 2^16, Toeplitz-Hankel (mode 3) otherwise;
  *   3 = FL_LEG2CHEB_TOEPLITZ : Toeplitz-Hankel factorisation, per parity
  *       A = T .* H with H ~ sum_r l_r l_r^T (pivoted Cholesky, residual
  *       <= 1e-17, so |error| <= 1e-17 ||c||_1), applied as K FFT-based
@@ -253,7 +253,7 @@ int fl_plan_ndct_terms(const fl_plan* plan);
  * (paper_1505_00354_b200/distributed.py):
  *   FL_STAGE_LEG2CHEB : the conversion the plan runs for one column, as a
  *                       sum of terms: with the asymptotic expansion (power-of-
- *                       two n >= 2^17, FL_LEG2CHEB_FAST) its (level, m)
+ *                       two n >= 2^16, FL_LEG2CHEB_FAST) its (level, m)
  *                       DCT/DST pairs, then its recurrence bands (each partial
  *                       ends with the DCT-II, which is linear); with
  *                       Toeplitz-Hankel chat = sum_{r in [lo,hi)} D(l_r) T

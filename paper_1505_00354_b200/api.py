@@ -410,7 +410,7 @@ class TransformConfig:  # transforms.hpp:19-38
 
     def set_leg2cheb_mode(self, mode: int) -> None:
         """LEG2CHEB_DIRECT (reference O(N^2) product), LEG2CHEB_FAST (default:
-        the asymptotic expansion for power-of-two n >= 2^17, else
+        the asymptotic expansion for power-of-two n >= 2^16, else
         Toeplitz-Hankel), LEG2CHEB_TOEPLITZ (Toeplitz-Hankel, n >= 2^14) or
         LEG2CHEB_ASYMPTOTIC (Hale-Townsend asymptotic expansion, power-of-two
         n in [2^10, 2^26]); the fast modes apply to <= 16 columns."""

@@ -629,7 +629,7 @@ void plan_convert(fl_plan* p, int transpose, const double* in, double* out, size
     return;
   }
   // FAST: the asymptotic expansion where it beats Toeplitz-Hankel (power-of-two
-  // n >= 2^17: 0.26 vs 0.32 ms there, 1.75 vs 2.86 ms at 2^20, 142 vs 288 ms
+  // n >= 2^16: 0.15 vs 0.19 ms there, 1.75 vs 2.86 ms at 2^20, 142 vs 288 ms
   // at 2^26), else Toeplitz-Hankel
   const L2CAsy* asy = plan_wants_asy(p, batch) ? plan_asy(p, s) : nullptr;
   if (asy)

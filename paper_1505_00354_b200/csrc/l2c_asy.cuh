@@ -31,10 +31,11 @@ void l2c_asy_destroy(L2CAsy* f);
 bool l2c_asy_supported(size_t n);
 // Size from which the plan's FAST conversion mode uses the expansion instead of
 // Toeplitz-Hankel (single vectors / <= 16 columns): with the chunk start
-// states kept by the plan it wins from 2^17 (0.26 vs 0.32 ms; 2^19 0.83 vs
-// 1.27; 2^16 ties at 0.19, below Toeplitz-Hankel wins). The free function
+// states kept by the plan (and its recurrence in short chunks) it wins from
+// 2^16 (0.148 vs 0.189 ms; 2^17 0.25 vs 0.32; 2^19 0.68 vs 1.30; 2^15 ties
+// at 0.12, 2^14 Toeplitz-Hankel wins 0.097 vs 0.115). The free function
 // (a new table per call, nothing kept) switches at kL2CAsyMinFree.
-constexpr size_t kL2CAsyMin = size_t(1) << 17;
+constexpr size_t kL2CAsyMin = size_t(1) << 16;
 constexpr size_t kL2CAsyMinFree = size_t(1) << 20;
 // A per-call object (fl_leg2cheb): do not keep the start states.
 void l2c_asy_one_shot(L2CAsy* f);

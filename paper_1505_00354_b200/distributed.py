@@ -4,7 +4,7 @@ Both stages of the transform are sums of independent terms
 (include/fastleg_b200.h, fl_dlt_stage):
 
   chat = M c       = DCT-II( sum_{l,m} level l's term m + sum_b recurrence band b )
-                     (the asymptotic expansion, power-of-two N >= 2^17; the
+                     (the asymptotic expansion, power-of-two N >= 2^16; the
                       DCT-II is linear, so every partial ends with it), or
                    = sum_{r < K} D(l_r) T D(l_r) c     (Toeplitz-Hankel rank terms)
   f    = NDCT(chat) = sum_{m < M} W_m C_m T_m(n/N) chat  (Chebyshev-expansion terms

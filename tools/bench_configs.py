@@ -80,7 +80,7 @@ def run(name, reps):
     return {"config": desc, "plan_s": t_plan, "dlt_ms": dlt, "idlt_ms": idlt,
             "dlt_coeffs_per_s": n / dlt * 1e3, "idlt_coeffs_per_s": n / idlt * 1e3,
             "leg2cheb": ("asymptotic expansion " + json.dumps(cfg.leg2cheb_asy_info())
-                         if n >= (1 << 17) and n & (n - 1) == 0
+                         if n >= (1 << 16) and n & (n - 1) == 0
                          else "toeplitz-hankel" if cfg.leg2cheb_rank(0) else "direct"),
             "round_trip_rel": rt}
 
