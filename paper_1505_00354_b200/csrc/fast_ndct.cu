@@ -2251,11 +2251,15 @@ __global__ void big_tr_unpack_kernel(const double2* __restrict__ Z, size_t n, si
 }
 
 // N > 8192: every term's packed transform in one batched multi-pass FFT
-// (terms x columns), the per-term weights / stage factors from per-call
-// tables, and the unpack accumulating all terms in registers (one store per
-// output): 3 launches + the FFT's passes per batch of terms instead of 4 per
-// term. Terms are batched within a 2 GiB scratch budget (C2, 65536 x 64: all
-// 14 terms at once; C5, one 2^26 column: two at a time).
+// (terms x columns). The per-term weights / stage factors come from tables
+// [terms][N] that a plan builds on its first call and keeps (per-call tables
+// for the free functions). From N = 2^15: forward, the unpack runs inside the
+// FFT's row pass (fft_pow2_ndct_unpack: all terms of a column per CTA, the
+// weighted sum in registers, the transformed rows never written); transposed,
+// the pack runs inside the first pass's loads (fft_pow2_ndct_tr_pack: the
+// column's weighted input once in packed order times the packed-order
+// weights). At N = 2^14 (one shared-memory FFT per row) the separate unpack /
+// pack kernels run.
 // Scratch of one batched multi-pass NDCT call (packed rows + FFT scratch):
 // 8 GiB (2^26: 2 batches of 7 terms: NDCT 35.9 -> 32.0 ms, NDCT^T 42.4 ->
 // 37.6 ms against 2 GiB; 16 GiB: 31.5 / 36.5 ms).
